@@ -1,0 +1,198 @@
+/*
+ * scout_b200.h — C ABI of the B200-native ScoutAttention decode hot path.
+ *
+ * Drop-in boundary for the reference's hot-path functions
+ * (/root/reference/proj/include/scout/{digest,attention,kv_store}.hpp).  Every entry point here replaces
+ * one reference function, batched over "units" = (request, KV head) pairs of
+ * one layer; the header-only C++ wrapper include/scout_b200.hpp restates the
+ * reference signatures on top of these calls.
+ *
+ * Conventions:
+ *   - every call returns an int status (SCOUT_OK == 0); the message of the
+ *     last failure on the calling thread is scout_last_error();
+ *   - all buffers are caller-owned device pointers unless a parameter says
+ *     "host" (pinned, device-mapped host memory for K4);
+ *   - each launching call takes a cudaStream_t (as void*; NULL = legacy default
+ *     stream) and neither allocates nor synchronises the host;
+ *   - argument errors -> SCOUT_ERR_INVALID_ARGUMENT (the reference throws
+ *     std::invalid_argument), sequencing errors -> SCOUT_ERR_LOGIC
+ *     (std::logic_error), launch failures -> SCOUT_ERR_CUDA.
+ *
+ * Fixed geometry (the reference's configs): head_dim d = 128,
+ * block size B = 64 tokens, GQA group G = Hq/Hkv in {1,2,4,8}.
+ *
+ * Data layouts in HBM:
+ *   KV pool    : slot-major array of blocks. Slot s holds K then V of one block
+ *                (64 tokens x 128 channels). bf16 slots are 32 KiB, stored in the
+ *                "half/slab/row" 128B-swizzled order (scout_kv_write_tokens
+ *                writes it); f32 slots are 64 KiB, plain row-major.
+ *   digests    : per unit [2][128][nb_stride] (lo then hi, channel-major, block
+ *                id fastest) in the KV dtype for minmax; [128][nb_stride] f64
+ *                for the mean method.
+ *   queries    : [req][Hq][128] f32 (f64 for the generic f64 scoring path).
+ *   partials   : o [req][Hq][128] f32 (normalised) + ml [req][Hq][2] f32
+ *                = (max logit, denominator); empty partial = (0, -inf, 0).
+ */
+#ifndef SCOUT_B200_H
+#define SCOUT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCOUT_HEAD_DIM 128
+#define SCOUT_BLOCK_SIZE 64
+#define SCOUT_MAX_BLOCKS 4096 /* per unit (256K tokens) */
+#define SCOUT_MAX_K 512
+
+enum scout_status {
+    SCOUT_OK = 0,
+    SCOUT_ERR_INVALID_ARGUMENT = 1, /* reference: std::invalid_argument */
+    SCOUT_ERR_LOGIC = 2,            /* reference: std::logic_error */
+    SCOUT_ERR_CUDA = 3,
+    SCOUT_ERR_UNSUPPORTED = 4
+};
+
+enum scout_dtype { SCOUT_F32 = 0, SCOUT_BF16 = 1, SCOUT_F64 = 2 };
+
+/* DigestMethod, digest.hpp:23 */
+enum scout_digest_method { SCOUT_DIGEST_MINMAX = 0, SCOUT_DIGEST_MEAN = 1 };
+
+/* Message of the last failed call on this thread ("" if none). */
+const char* scout_last_error(void);
+int scout_version(void);
+/* Bytes of one KV slot (K + V) for a dtype (SCOUT_F32 / SCOUT_BF16); 0 if unsupported. */
+size_t scout_slot_bytes(int kv_dtype);
+
+/* ------------------------------------------------------------------ K0 --
+ * Write token rows into KV slots (kv_store.hpp:90-117 append_token's data
+ * movement). Row i of k_rows/v_rows (f32, [n][128]) goes to slot slots[i],
+ * row rows[i] (0..63), converted to kv_dtype.                              */
+int scout_kv_write_tokens(void* kv_pool, int kv_dtype, const int32_t* slots, const int32_t* rows,
+                          const float* k_rows, const float* v_rows, int n, void* stream);
+/* Inverse of the above (tests / host tier spill): rows back to f32. */
+int scout_kv_read_tokens(const void* kv_pool, int kv_dtype, const int32_t* slots,
+                         const int32_t* rows, float* k_rows, float* v_rows, int n, void* stream);
+
+/* Digest build for n blocks (build_digest, digest.hpp:34-60; the open-block
+ * refresh of kv_store.hpp:108). Block i = slot slots[i] with block_rows[i]
+ * valid rows (>= 1) is summarised into unit units[i], column block_ids[i] of
+ * the digest array. minmax: digests in kv_dtype, exact. mean: f64 digests,
+ * sequential double sum / rows (bit-exact with the reference).             */
+int scout_digest_build(const void* kv_pool, int kv_dtype, int method, int n, const int32_t* slots,
+                       const int32_t* block_rows, const int32_t* units, const int32_t* block_ids,
+                       void* digests, int nb_stride, void* stream);
+
+/* ------------------------------------------------------------------ K1 --
+ * Score + top-k + resident/CPU split for n_units units of one layer
+ * (digest_score digest.hpp:62-72, select_topk :101-118, set_intersection /
+ * set_difference :77-87 as called at engine.hpp:238-242).
+ *
+ * q: [n_units/Hkv... ] laid out as [unit][G][128] — i.e. [req][Hq][128] with
+ *    unit = req*Hkv + kvh and head = kvh*G + g. f32 for bf16/f32 digests,
+ *    f64 for f64 digests.
+ * Score of block b = sum over c (outer) and g (inner) of
+ *    max(q_g[c]*lo[c], q_g[c]*hi[c])   (minmax)   or   q_g[c]*mean[c]   (mean),
+ *    accumulated sequentially in double from +0.0: the reference's
+ *    digest_score on the stacked G*128-vector q_s[c*G+g].
+ * n_tokens[u]: tokens cached for unit u; blocks = ceil(n_tokens/64); the last
+ *    block is the open block with n_tokens - 64*(blocks-1) rows.
+ * Selection: the min(k, blocks) best scores, ties to the lower block id; ids
+ *    written ascending to sel_ids[u*k_stride ...], count to n_sel[u].
+ * block_table (optional, [unit][nb_stride] int32): slot of a block that is
+ *    (or will be, for planned recalls) GPU-resident, -1 otherwise. If given,
+ *    res_slots/res_ids/n_res receive the resident share (ascending ids) and
+ *    cpu_ids/n_cpu the rest; res_tokens/cpu_tokens (optional) the row counts.
+ * last_selected (optional, [unit][nb_stride] int32): set to `step` for every
+ *    selected block (mark_selected, kv_store.hpp:222-228).
+ * scores_out (optional, [unit][nb_stride] f64): the raw scores.
+ * k == 0 -> SCOUT_ERR_INVALID_ARGUMENT (digest.hpp:103).                    */
+typedef struct scout_topk_args {
+    int n_units;
+    int group;      /* G */
+    int digest_dtype;
+    int method;
+    int k;
+    int k_stride;   /* row stride of the id/slot outputs (>= k) */
+    int nb_stride;  /* digest / table row stride in blocks (multiple of 8) */
+    int step;
+    const void* q;
+    const void* digests;
+    const int32_t* n_tokens;
+    const int32_t* block_table;
+    int32_t* sel_ids;
+    int32_t* n_sel;
+    int32_t* res_slots;
+    int32_t* res_ids;
+    int32_t* n_res;
+    int32_t* cpu_ids;
+    int32_t* n_cpu;
+    int32_t* res_tokens;
+    int32_t* cpu_tokens;
+    int32_t* last_selected;
+    double* scores_out;
+} scout_topk_args;
+
+int scout_score_topk_split(const scout_topk_args* args, void* stream);
+
+/* ------------------------------------------------------------------ K2 --
+ * Block-sparse flash-decode over the GPU-resident selected blocks of every
+ * unit (partial_attention attention.hpp:73-95 with accumulate_token :38-50,
+ * GPU side of engine.hpp:257-258), optionally LSE-merged with a CPU partial
+ * (merge :100-114, finalize :117-122, empty -> zeros engine.hpp:273).
+ *
+ * q [req][Hq][128] f32 (the true query), res_slots/res_ids/n_res as written
+ * by K1 (row stride k_stride), n_tokens per unit (for the open block's rows).
+ * Outputs o [req][Hq][128] f32 normalised and ml [req][Hq][2] = (m, l) with m
+ * the max scaled logit and l the softmax denominator relative to m.
+ * cpu_o / cpu_ml (optional, same layout): the co-attention partial to merge.
+ * workspace: scout_sparse_decode_workspace_bytes(); zero it ONCE after
+ * allocation (the kernel leaves its counters zeroed).                      */
+typedef struct scout_decode_args {
+    int n_units;
+    int group;
+    int kv_dtype;
+    int k_stride;
+    float scale;
+    const float* q;
+    const void* kv_pool;
+    const int32_t* res_slots;
+    const int32_t* res_ids;
+    const int32_t* n_res;
+    const int32_t* n_tokens;
+    const float* cpu_o;
+    const float* cpu_ml;
+    float* o;
+    float* ml;
+    void* workspace;
+    size_t workspace_bytes;
+    int max_ctas; /* 0 = one persistent CTA per SM */
+} scout_decode_args;
+
+size_t scout_sparse_decode_workspace_bytes(int n_units, int group, int max_ctas);
+int scout_sparse_decode(const scout_decode_args* args, void* stream);
+
+/* ------------------------------------------------------------------ K3 --
+ * Standalone LSE merge of two partial sets (merge attention.hpp:100-114):
+ * out = merge(a, b) row-wise over n_rows heads. Empty operands are exact
+ * identities; both empty -> o = 0, ml = (-inf, 0).  out may alias a.       */
+int scout_merge_partials(const float* a_o, const float* a_ml, const float* b_o, const float* b_ml,
+                         float* out_o, float* out_ml, int n_rows, void* stream);
+
+/* ------------------------------------------------------------------ K4 --
+ * Periodic-recall gather (the slow->fast move that kv_store.hpp:201-218
+ * applies as a tier flip): copy n whole block images from device-mapped
+ * pinned host memory (host_blocks + src_index[i]*slot_bytes) into pool slots
+ * dst_slots[i]. Launch it on a side stream and gate the consumer with an
+ * event; the kernel streams over PCIe / C2C with 16-byte loads.            */
+int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host_blocks,
+                        const int64_t* src_index, const int32_t* dst_slots, int n, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SCOUT_B200_H */

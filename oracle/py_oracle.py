@@ -1,0 +1,205 @@
+"""numpy wrappers over the CPU checkers (TEST / BASELINE INFRASTRUCTURE ONLY).
+
+  oracle()  -> oracle/_build/liboracle.so   C restatement (scout_oracle.c)
+  ref()     -> oracle/_ref/libscout_ref.so   the unmodified reference headers
+               behind ref_shim.cpp (None when not built / not shipped)
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs import
+this module; the product package never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import subprocess
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ORACLE_SO = HERE / "_build" / "liboracle.so"
+REF_SO = HERE / "_ref" / "libscout_ref.so"
+D = 128
+B = 64
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_lp = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_c = {}
+
+
+def _build():
+    subprocess.run(["make", "-s", "-C", str(HERE)], check=True, stdout=subprocess.DEVNULL)
+
+
+def oracle() -> C.CDLL:
+    if "o" not in _c:
+        if not ORACLE_SO.exists():
+            _build()
+        L = C.CDLL(str(ORACLE_SO))
+        dbl = C.c_double
+        L.oracle_build_digest_minmax.argtypes = [_dp, C.c_int, C.c_int, _dp, _dp]
+        L.oracle_build_digest_mean.argtypes = [_dp, C.c_int, C.c_int, _dp]
+        L.oracle_digest_score_minmax.argtypes = [_dp, _dp, _dp, C.c_int]
+        L.oracle_digest_score_minmax.restype = dbl
+        L.oracle_digest_score_mean.argtypes = [_dp, _dp, C.c_int]
+        L.oracle_digest_score_mean.restype = dbl
+        L.oracle_select_topk.argtypes = [_dp, C.c_void_p, C.c_int, C.c_int, _lp]
+        L.oracle_score_topk_split.argtypes = [C.c_int] * 6 + [_dp, _dp, _ip, C.c_void_p] + [_ip] * 7 + [C.c_void_p]
+        L.oracle_partial_attention.argtypes = [_dp, C.c_int, _dp, _dp, C.c_int, dbl, _dp, C.POINTER(dbl),
+                                               C.POINTER(dbl), C.POINTER(C.c_int64)]
+        L.oracle_merge.argtypes = [C.c_int, _dp, dbl, dbl, C.c_int64, _dp, dbl, dbl, C.c_int64, _dp,
+                                   C.POINTER(dbl), C.POINTER(dbl), C.POINTER(C.c_int64)]
+        L.oracle_finalize.argtypes = [C.c_int, _dp, dbl, C.c_int64, _dp]
+        _c["o"] = L
+    return _c["o"]
+
+
+def ref():
+    if "r" not in _c:
+        L = None
+        if not REF_SO.exists() and Path("/root/reference/proj/include/scout").exists():
+            _build()
+        if REF_SO.exists():
+            L = C.CDLL(str(REF_SO))
+            dbl = C.c_double
+            L.ref_build_digest.argtypes = [_dp, C.c_int, C.c_int, C.c_int, _dp, _dp]
+            L.ref_digest_score.argtypes = [_dp, _dp, _dp, C.c_int, C.c_int]
+            L.ref_digest_score.restype = dbl
+            L.ref_unit_topk.argtypes = [_dp, C.c_int, C.c_int, _dp, C.c_int, C.c_int, C.c_int, C.c_int, _ip,
+                                        C.c_void_p]
+            L.ref_select_topk.argtypes = [_dp, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_int, _ip]
+            L.ref_partial_attention.argtypes = [_dp, C.c_int, _dp, _dp, _ip, C.c_int, dbl, _dp, C.POINTER(dbl),
+                                                C.POINTER(dbl), C.POINTER(C.c_int64)]
+            L.ref_merge.argtypes = [C.c_int, _dp, dbl, dbl, C.c_int64, _dp, dbl, dbl, C.c_int64, _dp,
+                                    C.POINTER(dbl), C.POINTER(dbl), C.POINTER(C.c_int64)]
+            L.ref_finalize.argtypes = [C.c_int, _dp, dbl, C.c_int64, _dp]
+            L.ref_cpu_baseline.argtypes = [C.c_int] * 6 + [_dp, _dp, _ip, _dp, _ip, C.c_int, C.c_int, C.c_int,
+                                                           C.POINTER(dbl)]
+            L.ref_cpu_baseline.restype = dbl
+        _c["r"] = L
+    return _c["r"]
+
+
+def f64(x) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(x, dtype=np.float64))
+
+
+# ------------------------------------------------------------------ oracle --
+class Partial:
+    """PartialAttention (attention.hpp:22-35)."""
+
+    def __init__(self, o_acc, max_logit, denom, count):
+        self.o_acc, self.max_logit, self.denom, self.count = o_acc, max_logit, denom, count
+
+    @staticmethod
+    def empty(d=D):
+        return Partial(np.zeros(d), -np.inf, 0.0, 0)
+
+    def finalize(self, lib=None):
+        return finalize(self, lib)
+
+
+def build_digest(keys, method=0, lib=None):
+    keys = f64(keys)
+    rows, d = keys.shape
+    if lib is not None and lib is ref():
+        lo, hi = np.zeros(d), np.zeros(d)
+        if lib.ref_build_digest(keys, rows, d, method, lo, hi) != 0:
+            raise ValueError("build_digest: empty block")
+        return (lo, hi) if method == 0 else lo
+    L = oracle()
+    if rows == 0:
+        raise ValueError("build_digest: empty block")
+    if method == 0:
+        lo, hi = np.zeros(d), np.zeros(d)
+        L.oracle_build_digest_minmax(keys, rows, d, lo, hi)
+        return lo, hi
+    mean = np.zeros(d)
+    L.oracle_build_digest_mean(keys, rows, d, mean)
+    return mean
+
+
+def select_topk_scores(scores, k):
+    """select_topk given the scores (ids = positions)."""
+    scores = f64(scores)
+    out = np.zeros(max(k, 1), dtype=np.int64)
+    m = oracle().oracle_select_topk(scores, None, len(scores), int(k), out)
+    if m < 0:
+        raise ValueError("select_topk: k must be >= 1")
+    return out[:m].astype(np.int32)
+
+
+def unit_topk(q, dig, nb, k, method=0, lib=None):
+    """Stacked-GQA select_topk of one unit: q [G][d], dig [2|1][d][nb_stride]. Returns (ids, scores)."""
+    q = f64(q)
+    G = q.shape[0]
+    dig = f64(dig)
+    nbs = dig.shape[-1]
+    if lib is not None and lib is ref():
+        out = np.zeros(max(k, 1), dtype=np.int32)
+        sc = np.zeros(max(nb, 1))
+        m = lib.ref_unit_topk(q, G, D, dig.reshape(-1), nbs, nb, int(k), method, out,
+                              sc.ctypes.data_as(C.c_void_p))
+        if m < 0:
+            raise ValueError("select_topk: k must be >= 1")
+        return out[:m], sc[:nb]
+    r = score_topk_split(q, dig[None], np.array([nb * B], dtype=np.int32), k, G, method=method)
+    return r["sel_ids"][0, :r["n_sel"][0]], r["scores"][0, :nb]
+
+
+def score_topk_split(q, digests, n_tokens, k, G, table=None, method=0, k_stride=None):
+    """Batched K1 statement. q [U*G][d]; digests [U][2|1][d][nbs]; table [U][nbs] or None."""
+    q = f64(q)
+    digests = f64(digests)
+    n_tokens = np.ascontiguousarray(n_tokens, dtype=np.int32)
+    U = len(n_tokens)
+    nbs = digests.shape[-1]
+    ks = k_stride or max(k, 1)
+    z = lambda *s: np.full(s, -7, dtype=np.int32)  # noqa: E731
+    sel, nsel, rid, rsl, nres, cid, ncpu = z(U, ks), z(U), z(U, ks), z(U, ks), z(U), z(U, ks), z(U)
+    scores = np.zeros((U, nbs))
+    tb = None if table is None else np.ascontiguousarray(table, dtype=np.int32)
+    rc = oracle().oracle_score_topk_split(U, G, method, int(k), ks, nbs, q.reshape(-1), digests.reshape(-1),
+                                          n_tokens, None if tb is None else tb.ctypes.data_as(C.c_void_p),
+                                          sel, nsel, rid, rsl, nres, cid, ncpu,
+                                          scores.ctypes.data_as(C.c_void_p))
+    if rc < 0:
+        raise ValueError("select_topk: k must be >= 1")
+    return dict(sel_ids=sel, n_sel=nsel, res_ids=rid, res_slots=rsl, n_res=nres, cpu_ids=cid, n_cpu=ncpu,
+                scores=scores)
+
+
+def partial_attention(q, keys, values, scale, lib=None, rows=None):
+    """partial_attention over rows (blocks concatenated in visiting order)."""
+    q, keys, values = f64(q), f64(keys).reshape(-1, len(q)), f64(values).reshape(-1, len(q))
+    d = len(q)
+    if not (scale > 0):
+        raise ValueError("partial_attention: scale must be > 0")
+    o = np.zeros(d)
+    m, l, n = C.c_double(), C.c_double(), C.c_int64()
+    if lib is not None and lib is ref():
+        r = np.ascontiguousarray(rows if rows is not None else [keys.shape[0]], dtype=np.int32)
+        lib.ref_partial_attention(q, d, keys, values, r, len(r), float(scale), o, C.byref(m), C.byref(l), C.byref(n))
+    else:
+        oracle().oracle_partial_attention(q, d, keys, values, keys.shape[0], float(scale), o, C.byref(m), C.byref(l),
+                                          C.byref(n))
+    return Partial(o, m.value, l.value, n.value)
+
+
+def merge(a: Partial, b: Partial, lib=None) -> Partial:
+    d = len(a.o_acc)
+    o = np.zeros(d)
+    m, l, n = C.c_double(), C.c_double(), C.c_int64()
+    fn = lib.ref_merge if (lib is not None and lib is ref()) else oracle().oracle_merge
+    fn(d, f64(a.o_acc), a.max_logit, a.denom, a.count, f64(b.o_acc), b.max_logit, b.denom, b.count, o, C.byref(m),
+       C.byref(l), C.byref(n))
+    return Partial(o, m.value, l.value, n.value)
+
+
+def finalize(p: Partial, lib=None):
+    d = len(p.o_acc)
+    out = np.zeros(d)
+    fn = lib.ref_finalize if (lib is not None and lib is ref()) else oracle().oracle_finalize
+    if fn(d, f64(p.o_acc), p.denom, p.count, out) != 0:
+        raise ValueError("finalize: empty partial")
+    return out

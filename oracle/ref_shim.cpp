@@ -1,0 +1,295 @@
+// ref_shim.cpp — C entry points over the UNMODIFIED reference headers.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY. Built by oracle/Makefile with
+// -I /root/reference/proj/include into oracle/_ref/libscout_ref.so (git-ignored,
+// travels to the GPU box). It is (1) the generator of the golden vectors under
+// tests/golden/ (script tests/golden/make_golden.py), (2) a second oracle for
+// the restatement oracle/scout_oracle.c, and (3) the CPU baseline that
+// bench.py times ("kind": "reference"): the reference's own select_topk /
+// partial_attention / merge / finalize on the same workload shape.
+#include <atomic>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <span>
+#include <stdexcept>
+#include <thread>
+#include <vector>
+
+#include "scout/attention.hpp"
+#include "scout/digest.hpp"
+#include "scout/kv_store.hpp"
+
+using scout::BlockDigest;
+using scout::BlockIdSet;
+using scout::KvBlock;
+using scout::Mat;
+using scout::PartialAttention;
+using scout::Vec;
+
+namespace {
+
+Mat mat_from(const double* p, int rows, int cols) {
+    Mat m(rows, cols);
+    std::memcpy(m.data.data(), p, sizeof(double) * static_cast<size_t>(rows) * cols);
+    return m;
+}
+
+// Stacked GQA digest for block b of one unit: q_s[c*G+g], lo/hi tiled G times.
+BlockDigest stacked_digest(const double* dig, int G, int d, int nb_stride, int b, int method) {
+    BlockDigest bd;
+    bd.block_id = static_cast<size_t>(b);
+    if (method == 0) {
+        bd.method = scout::DigestMethod::minmax;
+        bd.lo.resize(static_cast<size_t>(G) * d);
+        bd.hi.resize(static_cast<size_t>(G) * d);
+        for (int c = 0; c < d; ++c)
+            for (int g = 0; g < G; ++g) {
+                bd.lo[c * G + g] = dig[static_cast<size_t>(c) * nb_stride + b];
+                bd.hi[c * G + g] = dig[static_cast<size_t>(d + c) * nb_stride + b];
+            }
+    } else {
+        bd.method = scout::DigestMethod::mean;
+        bd.mean.resize(static_cast<size_t>(G) * d);
+        for (int c = 0; c < d; ++c)
+            for (int g = 0; g < G; ++g) bd.mean[c * G + g] = dig[static_cast<size_t>(c) * nb_stride + b];
+    }
+    return bd;
+}
+
+Vec stacked_query(const double* q, int G, int d) {
+    Vec qs(static_cast<size_t>(G) * d);
+    for (int c = 0; c < d; ++c)
+        for (int g = 0; g < G; ++g) qs[c * G + g] = q[static_cast<size_t>(g) * d + c];
+    return qs;
+}
+
+}  // namespace
+
+extern "C" {
+
+// build_digest (digest.hpp:34) — method 0 minmax (lo, hi), 1 mean (lo = mean).
+int ref_build_digest(const double* keys, int rows, int d, int method, double* lo, double* hi) {
+    try {
+        const BlockDigest bd = scout::build_digest(mat_from(keys, rows, d),
+                                                   method == 0 ? scout::DigestMethod::minmax : scout::DigestMethod::mean);
+        if (method == 0) {
+            std::memcpy(lo, bd.lo.data(), sizeof(double) * d);
+            std::memcpy(hi, bd.hi.data(), sizeof(double) * d);
+        } else {
+            std::memcpy(lo, bd.mean.data(), sizeof(double) * d);
+        }
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// digest_score (digest.hpp:62) on an n-vector.
+double ref_digest_score(const double* q, const double* lo, const double* hi, int n, int method) {
+    BlockDigest bd;
+    if (method == 0) {
+        bd.method = scout::DigestMethod::minmax;
+        bd.lo.assign(lo, lo + n);
+        bd.hi.assign(hi, hi + n);
+    } else {
+        bd.method = scout::DigestMethod::mean;
+        bd.mean.assign(lo, lo + n);
+    }
+    return scout::digest_score(Vec(q, q + n), bd);
+}
+
+// select_topk (digest.hpp:101) for one unit under the stacked-GQA rule.
+// digests: [2][d][nb_stride] (minmax) or [d][nb_stride] (mean). Returns the
+// number of ids written ascending to out, -1 on std::invalid_argument.
+int ref_unit_topk(const double* q, int G, int d, const double* dig, int nb_stride, int nb, int k, int method,
+                  int32_t* out, double* scores) {
+    std::vector<BlockDigest> ds;
+    ds.reserve(static_cast<size_t>(nb));
+    for (int b = 0; b < nb; ++b) ds.push_back(stacked_digest(dig, G, d, nb_stride, b, method));
+    const Vec qs = stacked_query(q, G, d);
+    try {
+        if (scores)
+            for (int b = 0; b < nb; ++b) scores[b] = scout::digest_score(qs, ds[b]);
+        const BlockIdSet ids = scout::select_topk(qs, ds, static_cast<size_t>(k));
+        for (size_t i = 0; i < ids.size(); ++i) out[i] = static_cast<int32_t>(ids[i]);
+        return static_cast<int>(ids.size());
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// Generic select_topk over single-head digests given as [n][dim] arrays.
+int ref_select_topk(const double* q, int dim, const double* lo, const double* hi, int n, int k, int method,
+                    int32_t* out) {
+    std::vector<BlockDigest> ds(static_cast<size_t>(n));
+    for (int i = 0; i < n; ++i) {
+        ds[i].block_id = static_cast<size_t>(i);
+        if (method == 0) {
+            ds[i].method = scout::DigestMethod::minmax;
+            ds[i].lo.assign(lo + static_cast<size_t>(i) * dim, lo + static_cast<size_t>(i + 1) * dim);
+            ds[i].hi.assign(hi + static_cast<size_t>(i) * dim, hi + static_cast<size_t>(i + 1) * dim);
+        } else {
+            ds[i].method = scout::DigestMethod::mean;
+            ds[i].mean.assign(lo + static_cast<size_t>(i) * dim, lo + static_cast<size_t>(i + 1) * dim);
+        }
+    }
+    try {
+        const BlockIdSet ids = scout::select_topk(Vec(q, q + dim), ds, static_cast<size_t>(k));
+        for (size_t i = 0; i < ids.size(); ++i) out[i] = static_cast<int32_t>(ids[i]);
+        return static_cast<int>(ids.size());
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// partial_attention (attention.hpp:73) over nblk blocks; block i has rows[i]
+// rows starting at row offset sum(rows[:i]) of keys/values [total][d].
+int ref_partial_attention(const double* q, int d, const double* keys, const double* values, const int32_t* rows,
+                          int nblk, double scale, double* o_acc, double* max_logit, double* denom, int64_t* count) {
+    std::vector<KvBlock> blocks(static_cast<size_t>(nblk));
+    size_t off = 0;
+    for (int i = 0; i < nblk; ++i) {
+        blocks[i].block_id = static_cast<size_t>(i);
+        blocks[i].keys = mat_from(keys + off * d, rows[i], d);
+        blocks[i].values = mat_from(values + off * d, rows[i], d);
+        blocks[i].sealed = true;
+        off += static_cast<size_t>(rows[i]);
+    }
+    std::vector<const KvBlock*> ptrs;
+    for (const KvBlock& b : blocks) ptrs.push_back(&b);
+    try {
+        const PartialAttention p = scout::partial_attention(Vec(q, q + d), ptrs, scale);
+        std::memcpy(o_acc, p.o_acc.data(), sizeof(double) * d);
+        *max_logit = p.max_logit;
+        *denom = p.denom;
+        *count = static_cast<int64_t>(p.token_count);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// merge (attention.hpp:100) of two partials.
+int ref_merge(int d, const double* oa, double ma, double la, int64_t na, const double* ob, double mb, double lb,
+              int64_t nb, double* o, double* m, double* l, int64_t* n) {
+    PartialAttention a, b;
+    a.o_acc.assign(oa, oa + d); a.max_logit = ma; a.denom = la; a.token_count = static_cast<size_t>(na);
+    b.o_acc.assign(ob, ob + d); b.max_logit = mb; b.denom = lb; b.token_count = static_cast<size_t>(nb);
+    try {
+        const PartialAttention r = scout::merge(a, b);
+        std::memcpy(o, r.o_acc.data(), sizeof(double) * d);
+        *m = r.max_logit; *l = r.denom; *n = static_cast<int64_t>(r.token_count);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// finalize (attention.hpp:117); -1 for an empty partial.
+int ref_finalize(int d, const double* o_acc, double denom, int64_t count, double* out) {
+    PartialAttention p;
+    p.o_acc.assign(o_acc, o_acc + d); p.denom = denom; p.token_count = static_cast<size_t>(count);
+    try {
+        const Vec v = scout::finalize(p);
+        std::memcpy(out, v.data(), sizeof(double) * d);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+
+// ------------------------------------------------------------------ baseline
+// The reference's per-(request, layer) decode work, as the GPU arm does it:
+// for each of hkv units: select_topk (stacked) over nb digests, split against
+// the resident set (set_intersection, engine.hpp:240), partial_attention per
+// query head over the resident blocks, merge with a pre-staged CPU partial,
+// finalize. `samples` distinct (request, layer) inputs are cycled through
+// `units_total` times by `threads` std::threads. Returns seconds.
+struct RefSample {
+    std::vector<std::vector<BlockDigest>> digests;  // [hkv][nb]
+    std::vector<BlockIdSet> residency;              // [hkv]
+    std::vector<std::vector<KvBlock>> blocks;       // [hkv][nb] (only resident ones filled)
+    std::vector<Vec> q;                             // [hq] (true query, widened f32)
+    std::vector<Vec> qs;                            // [hkv] stacked predicted query
+    std::vector<PartialAttention> cpu;              // [hq]
+};
+
+double ref_cpu_baseline(int samples, int hq, int hkv, int d, int nb, int k, const double* q /*[s][hq][d]*/,
+                        const double* digests /*[s][hkv][2][d][nb]*/, const int32_t* resident /*[s][hkv][nb] 0/1*/,
+                        const double* kv /*[s][hkv][nb_res_max][2][64][d]*/, const int32_t* res_index /*[s][hkv][nb]*/,
+                        int nb_res_max, int units_total, int threads, double* checksum) {
+    const int G = hq / hkv;
+    const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+    std::vector<RefSample> S(static_cast<size_t>(samples));
+    for (int s = 0; s < samples; ++s) {
+        RefSample& rs = S[s];
+        rs.digests.resize(hkv);
+        rs.residency.resize(hkv);
+        rs.blocks.resize(hkv);
+        rs.qs.resize(hkv);
+        for (int h = 0; h < hq; ++h) {
+            const double* qp = q + (static_cast<size_t>(s) * hq + h) * d;
+            rs.q.emplace_back(qp, qp + d);
+            PartialAttention cp = PartialAttention::empty(static_cast<size_t>(d));
+            for (int c = 0; c < d; ++c) cp.o_acc[c] = qp[c] * 0.01;  // synthetic pre-staged CPU partial
+            cp.max_logit = 0.5; cp.denom = 3.0; cp.token_count = 64;
+            rs.cpu.push_back(cp);
+        }
+        for (int u = 0; u < hkv; ++u) {
+            const double* dig = digests + (static_cast<size_t>(s) * hkv + u) * 2 * d * nb;
+            for (int b = 0; b < nb; ++b) rs.digests[u].push_back(stacked_digest(dig, G, d, nb, b, 0));
+            rs.qs[u] = stacked_query(q + (static_cast<size_t>(s) * hq + u * G) * d, G, d);
+            rs.blocks[u].resize(static_cast<size_t>(nb));
+            for (int b = 0; b < nb; ++b) {
+                if (!resident[(static_cast<size_t>(s) * hkv + u) * nb + b]) continue;
+                rs.residency[u].push_back(static_cast<size_t>(b));
+                const int ri = res_index[(static_cast<size_t>(s) * hkv + u) * nb + b];
+                const double* kb = kv + ((static_cast<size_t>(s) * hkv + u) * nb_res_max + ri) * 2 * 64 * d;
+                KvBlock& blk = rs.blocks[u][b];
+                blk.block_id = static_cast<size_t>(b);
+                blk.keys = mat_from(kb, 64, d);
+                blk.values = mat_from(kb + 64 * d, 64, d);
+                blk.sealed = true;
+            }
+        }
+    }
+    std::atomic<int> next{0};
+    std::vector<double> sums(static_cast<size_t>(threads), 0.0);
+    auto worker = [&](int tix) {
+        double acc = 0.0;
+        for (;;) {
+            const int i = next.fetch_add(1);
+            if (i >= units_total) break;
+            const RefSample& rs = S[i % samples];
+            for (int u = 0; u < hkv; ++u) {
+                const BlockIdSet pred = scout::select_topk(rs.qs[u], rs.digests[u], static_cast<size_t>(k));
+                const BlockIdSet res = scout::set_intersection(pred, rs.residency[u]);
+                std::vector<const KvBlock*> ptrs;
+                ptrs.reserve(res.size());
+                for (size_t id : res) ptrs.push_back(&rs.blocks[u][id]);
+                for (int g = 0; g < G; ++g) {
+                    const int h = u * G + g;
+                    const PartialAttention gp = scout::partial_attention(rs.q[h], ptrs, scale);
+                    const PartialAttention m = scout::merge(gp, rs.cpu[h]);
+                    const Vec o = m.is_empty() ? Vec(static_cast<size_t>(d), 0.0) : scout::finalize(m);
+                    acc += o[0];
+                }
+            }
+        }
+        sums[tix] = acc;
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t) pool.emplace_back(worker, t);
+    for (auto& th : pool) th.join();
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (checksum) {
+        double s = 0.0;
+        for (double v : sums) s += v;
+        *checksum = s;
+    }
+    return secs;
+}
+
+}  // extern "C"

@@ -1,0 +1,96 @@
+"""ctypes binding of the C ABI declared in include/scout_b200.h.
+
+This is exactly the binding a maintainer of a Python caller would add (see
+INTEGRATION.md); the product path loads libscout_b200.so and fails loudly if
+it is missing — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libscout_b200.so"
+
+SCOUT_OK = 0
+SCOUT_ERR_INVALID_ARGUMENT = 1
+SCOUT_ERR_LOGIC = 2
+SCOUT_ERR_CUDA = 3
+SCOUT_ERR_UNSUPPORTED = 4
+
+SCOUT_F32, SCOUT_BF16, SCOUT_F64 = 0, 1, 2
+SCOUT_DIGEST_MINMAX, SCOUT_DIGEST_MEAN = 0, 1
+HEAD_DIM = 128
+BLOCK_SIZE = 64
+
+# every extern "C" symbol of include/scout_b200.h
+EXPORTED = (
+    "scout_last_error", "scout_version", "scout_slot_bytes",
+    "scout_kv_write_tokens", "scout_kv_read_tokens", "scout_digest_build",
+    "scout_score_topk_split", "scout_sparse_decode_workspace_bytes",
+    "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather",
+)
+
+_vp = C.c_void_p
+_i32p = C.c_void_p  # device pointers travel as void*
+
+
+class TopkArgs(C.Structure):
+    _fields_ = [
+        ("n_units", C.c_int), ("group", C.c_int), ("digest_dtype", C.c_int), ("method", C.c_int),
+        ("k", C.c_int), ("k_stride", C.c_int), ("nb_stride", C.c_int), ("step", C.c_int),
+        ("q", _vp), ("digests", _vp), ("n_tokens", _vp), ("block_table", _vp),
+        ("sel_ids", _vp), ("n_sel", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
+        ("cpu_ids", _vp), ("n_cpu", _vp), ("res_tokens", _vp), ("cpu_tokens", _vp),
+        ("last_selected", _vp), ("scores_out", _vp),
+    ]
+
+
+class DecodeArgs(C.Structure):
+    _fields_ = [
+        ("n_units", C.c_int), ("group", C.c_int), ("kv_dtype", C.c_int), ("k_stride", C.c_int),
+        ("scale", C.c_float),
+        ("q", _vp), ("kv_pool", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
+        ("n_tokens", _vp), ("cpu_o", _vp), ("cpu_ml", _vp), ("o", _vp), ("ml", _vp),
+        ("workspace", _vp), ("workspace_bytes", C.c_size_t), ("max_ctas", C.c_int),
+    ]
+
+
+class ScoutError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[scout status {code}] {msg}")
+        self.code = code
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libscout_b200.so (raises if it was not built — no fallback)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(str(LIB_PATH))
+        L.scout_last_error.restype = C.c_char_p
+        L.scout_version.restype = C.c_int
+        L.scout_slot_bytes.restype = C.c_size_t
+        L.scout_slot_bytes.argtypes = [C.c_int]
+        L.scout_kv_write_tokens.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]
+        L.scout_kv_read_tokens.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]
+        L.scout_digest_build.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]
+        L.scout_score_topk_split.argtypes = [C.POINTER(TopkArgs), _vp]
+        L.scout_sparse_decode_workspace_bytes.restype = C.c_size_t
+        L.scout_sparse_decode_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.scout_sparse_decode.argtypes = [C.POINTER(DecodeArgs), _vp]
+        L.scout_merge_partials.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]
+        L.scout_recall_gather.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]
+        _lib = L
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != SCOUT_OK:
+        msg = lib().scout_last_error().decode()
+        if rc == SCOUT_ERR_INVALID_ARGUMENT:
+            raise ValueError(msg)  # std::invalid_argument in the reference
+        raise ScoutError(rc, msg)

@@ -1,0 +1,648 @@
+// K2 (+K3 fused) — paged block-sparse flash-decode over GPU-resident blocks.
+//
+// Replaces the GPU side of one decode layer in the reference:
+//   partial_attention  proj/include/scout/attention.hpp:73-95
+//   accumulate_token   attention.hpp:38-50 (online softmax, unnormalised)
+//   merge / finalize   attention.hpp:100-122, engine.hpp:271-273
+// batched over every (request, KV head) unit of a layer, GQA-grouped: the G
+// query heads of a KV head share one pass over its selected K/V blocks (the
+// reference, single-head, re-reads K/V per head).
+//
+// bf16 path (the hot one), per persistent CTA (one per SM):
+//   * work balance ("stream-K"): the concatenation of every unit's resident
+//     block list is cut into gridDim.x equal ranges; a range covers pieces
+//     ("segments") of one or more units. Segment (cta c, unit u) owns partial
+//     slot c+u; the last CTA to finish a unit (atomic counter) LSE-merges the
+//     unit's segment partials and the CPU co-attention partial.
+//   * one producer warp streams 32-token half blocks (8 KiB K + 8 KiB V) with
+//     1-D bulk async copies (TMA engine) into a 12-stage mbarrier ring;
+//   * NC consumer warps take half blocks round robin and run both GEMMs on the
+//     tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate) in a transposed
+//     form that wastes no rows at G=8:
+//        S^T[32 tok x 8 heads] = K[32 x 128] . Q^T      (q split hi+lo bf16)
+//        O^T[128 x 8 heads]   += V^T[128 x 32] . P^T    (P^T via movmatrix)
+//     with the online-softmax state per head in registers (log2 domain).
+// f32 path (config 1, CUDA cores): split-K over blocks, 4 warps per CTA, then
+// a small combine kernel (same merge rule).
+#include "scout_common.cuh"
+
+#include <math_constants.h>
+
+using namespace scout_dev;
+
+namespace {
+
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr float LN2 = 0.6931471805599453f;
+
+// ------------------------------------------------------------ workspace --
+constexpr int PART_STRIDE = 8 * (D + 2);  // floats per partial slot: [8 heads][o(128), m, l]
+constexpr int SIMPLE_SPLIT = 8;
+constexpr int GRID_CAP = 1024;
+
+__host__ __device__ inline size_t ctr_bytes(int n_units) { return ((static_cast<size_t>(n_units) * 4 + 255) / 256) * 256; }
+
+// =========================================================== bf16 kernel ==
+namespace tc {
+constexpr int NC = 4;                       // consumer warps
+constexpr int NTHREADS = (NC + 1) * 32;     // + 1 producer warp
+constexpr int NST = 12;                     // ring stages (one half block each)
+constexpr int STAGE_BYTES = 16384;          // 8 KiB K half + 8 KiB V half
+constexpr int MAXSEG = 256;
+constexpr int CB_ROW = D + 4;               // combine-buffer row stride (bank-conflict pad)
+constexpr int CB_WARP = 8 * CB_ROW + 16;    // floats per warp: O[8][CB_ROW], m[8], l[8]
+constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES + static_cast<size_t>(NC) * CB_WARP * 4;
+
+struct Seg {
+    int unit, j0, j1, nseg, cfirst;
+};
+
+struct Smem {
+    uint64_t full[NST];
+    uint64_t empty[NST];
+    Seg segs[MAXSEG];
+    int nsegs;
+    int scan_tot[8];
+    int last_flag;
+    long long run_total;
+};
+
+__device__ __forceinline__ int unit_nb(const scout_decode_args& a, int u, int* tail) {
+    const int nt = a.n_tokens[u];
+    const int nb = (nt + BS - 1) / BS;
+    *tail = nt - (nb - 1) * BS;
+    return nb;
+}
+
+// merge n partial slots (+ optional cpu partial) of unit u into the outputs.
+// Executed by the NC*32 consumer threads; thread i -> head i/16, 8 channels.
+template <int G>
+__device__ void finalize_unit(const scout_decode_args& a, int u, const float* parts, int first_slot, int nslots,
+                              int ctid) {
+    const int h = ctid >> 4;
+    const int d0 = (ctid & 15) * 8;
+    if (h >= G) return;
+    const size_t head = static_cast<size_t>(u) * G + h;
+    float M = -CUDART_INF_F;
+    for (int i = 0; i < nslots; ++i) {
+        const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * (D + 2);
+        M = fmaxf(M, __ldcg(p + D));
+    }
+    float cm = -CUDART_INF_F, cl = 0.f;
+    if (a.cpu_ml) {
+        cm = a.cpu_ml[head * 2] * LOG2E;
+        cl = a.cpu_ml[head * 2 + 1];
+        if (cl > 0.f) M = fmaxf(M, cm);
+    }
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float L = 0.f;
+    if (M != -CUDART_INF_F) {
+        for (int i = 0; i < nslots; ++i) {
+            const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * (D + 2);
+            const float l = __ldcg(p + D + 1);
+            if (!(l > 0.f)) continue;
+            const float w = l * exp2f(__ldcg(p + D) - M);
+            L += w;
+            const float4 x0 = __ldcg(reinterpret_cast<const float4*>(p + d0));
+            const float4 x1 = __ldcg(reinterpret_cast<const float4*>(p + d0 + 4));
+            acc[0] += w * x0.x; acc[1] += w * x0.y; acc[2] += w * x0.z; acc[3] += w * x0.w;
+            acc[4] += w * x1.x; acc[5] += w * x1.y; acc[6] += w * x1.z; acc[7] += w * x1.w;
+        }
+        if (cl > 0.f) {
+            const float w = cl * exp2f(cm - M);
+            L += w;
+            const float* co = a.cpu_o + head * D + d0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += w * co[e];
+        }
+    }
+    float* o = a.o + head * D + d0;
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    *reinterpret_cast<float4*>(o) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+    if ((ctid & 15) == 0) {
+        a.ml[head * 2] = L > 0.f ? M * LN2 : -CUDART_INF_F;
+        a.ml[head * 2 + 1] = L;
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const scout_decode_args a) {
+    extern __shared__ __align__(1024) uint8_t dsmem[];
+    __shared__ Smem sm;
+    uint8_t* stages = dsmem;
+    float* cbuf = reinterpret_cast<float*>(dsmem + static_cast<size_t>(NST) * STAGE_BYTES);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nunits = a.n_units;
+    const int ks = a.k_stride;
+    int* ctr = reinterpret_cast<int*>(a.workspace);
+    float* parts = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + ctr_bytes(nunits));
+
+    if (tid == 0) {
+        for (int i = 0; i < NST; ++i) {
+            mbar_init(&sm.full[i], 1);
+            mbar_init(&sm.empty[i], 1);
+        }
+        fence_mbar_init();
+        sm.nsegs = 0;
+        sm.run_total = 0;
+    }
+    __syncthreads();
+
+    // ---- pass 1: total resident blocks T
+    long long T = 0;
+    {
+        int loc = 0;
+        for (int u = tid; u < nunits; u += NTHREADS) loc += a.n_res[u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+        if (lane == 0) sm.scan_tot[warp] = loc;
+        __syncthreads();
+        for (int w = 0; w < NTHREADS / 32; ++w) T += sm.scan_tot[w];
+        __syncthreads();
+    }
+    const long long grid = gridDim.x, c = blockIdx.x;
+    const long long lo = T * c / grid, hi = T * (c + 1) / grid;
+
+    // ---- pass 2: exclusive prefix over units -> this CTA's segments
+    for (int base = 0; base < nunits; base += NTHREADS) {
+        const int u = base + tid;
+        const int n = u < nunits ? a.n_res[u] : 0;
+        int x = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) sm.scan_tot[warp] = x;
+        __syncthreads();
+        long long pre = sm.run_total;
+        for (int w = 0; w < warp; ++w) pre += sm.scan_tot[w];
+        pre += x - n;  // exclusive prefix of unit u
+        if (n > 0) {
+            const long long s0 = max(pre, lo), s1 = min(pre + n, hi);
+            if (s0 < s1) {
+                // CTA holding position p: floor(((p+1)*grid - 1)/T)
+                const long long cf = ((pre + 1) * grid - 1) / T;
+                const long long cl = ((pre + n) * grid - 1) / T;
+                const int idx = atomicAdd(&sm.nsegs, 1);
+                if (idx < MAXSEG)
+                    sm.segs[idx] = Seg{u, static_cast<int>(s0 - pre), static_cast<int>(s1 - pre),
+                                       static_cast<int>(cl - cf + 1), static_cast<int>(cf)};
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {
+            long long t = 0;
+            for (int w = 0; w < NTHREADS / 32; ++w) t += sm.scan_tot[w];
+            sm.run_total += t;
+        }
+        __syncthreads();
+    }
+    // segments were appended in arbitrary order within a chunk; sort by unit
+    // (a CTA range is contiguous, so unit order == stream order).
+    const int nsegs = min(sm.nsegs, MAXSEG);
+    if (tid == 0) {
+        for (int i = 1; i < nsegs; ++i) {
+            Seg s = sm.segs[i];
+            int j = i - 1;
+            while (j >= 0 && sm.segs[j].unit > s.unit) { sm.segs[j + 1] = sm.segs[j]; --j; }
+            sm.segs[j + 1] = s;
+        }
+    }
+    __syncthreads();
+
+    if (warp == NC) {
+        // ================================================== producer warp
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
+            int q = 0;
+            for (int si = 0; si < nsegs; ++si) {
+                const Seg sg = sm.segs[si];
+                int tail;
+                const int nb = unit_nb(a, sg.unit, &tail);
+                for (int j = sg.j0; j < sg.j1; ++j) {
+                    const size_t slot = static_cast<size_t>(a.res_slots[static_cast<size_t>(sg.unit) * ks + j]);
+                    const int id = a.res_ids[static_cast<size_t>(sg.unit) * ks + j];
+                    const int rows = (id == nb - 1) ? tail : BS;
+                    const uint8_t* kb = pool + slot * BF16_SLOT_BYTES;
+                    for (int h = 0; h * HALF_ROWS < rows; ++h) {
+                        const int s = q % NST;
+                        if (q >= NST) mbar_wait(&sm.empty[s], ((q / NST) - 1) & 1);
+                        mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
+                        bulk_g2s_evict_first(stages + s * STAGE_BYTES, kb + h * HALF_BYTES_BF16, HALF_BYTES_BF16,
+                                             &sm.full[s], pol);
+                        bulk_g2s_evict_first(stages + s * STAGE_BYTES + HALF_BYTES_BF16,
+                                             kb + BF16_TILE_BYTES + h * HALF_BYTES_BF16, HALF_BYTES_BF16, &sm.full[s],
+                                             pol);
+                        ++q;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ====================================================== consumer warps
+    const int g = lane >> 2, t = lane & 3;
+    const float sl2 = a.scale * LOG2E;
+    const int ctid = tid;  // 0 .. NC*32-1
+    float* mycb = cbuf + warp * CB_WARP;
+    int q = 0;
+    for (int si = 0; si < nsegs; ++si) {
+        const Seg sg = sm.segs[si];
+        const int u = sg.unit;
+        int tail;
+        const int nb = unit_nb(a, u, &tail);
+        // Q^T fragments (hi/lo split), heads >= G are zero
+        uint32_t bh[8][2], bl[8][2];
+        {
+            const bool live = g < G;
+            const float* qh = a.q + (static_cast<size_t>(u) * G + (live ? g : 0)) * D;
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    float2 v = live ? *reinterpret_cast<const float2*>(qh + 16 * kk + 8 * half + 2 * t)
+                                    : make_float2(0.f, 0.f);
+                    const __nv_bfloat162 hv = __floats2bfloat162_rn(v.x, v.y);
+                    const float2 hf = __bfloat1622float2(hv);
+                    bh[kk][half] = *reinterpret_cast<const uint32_t*>(&hv);
+                    bl[kk][half] = pack_bf16(v.x - hf.x, v.y - hf.y);
+                }
+            }
+        }
+        float m2[2] = {-CUDART_INF_F, -CUDART_INF_F};
+        float lp[2] = {0.f, 0.f};
+        float oacc[8][4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+
+        for (int j = sg.j0; j < sg.j1; ++j) {
+            const int id = a.res_ids[static_cast<size_t>(u) * ks + j];
+            const int rows = (id == nb - 1) ? tail : BS;
+            for (int h = 0; h * HALF_ROWS < rows; ++h, ++q) {
+                if ((q % NC) != warp) continue;
+                const int s = q % NST;
+                const int valid = min(HALF_ROWS, rows - h * HALF_ROWS);
+                mbar_wait(&sm.full[s], (q / NST) & 1);
+                const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES);
+                const uint32_t vbase = kbase + HALF_BYTES_BF16;
+                // ---- S^T = K . Q^T
+                float sh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, slo[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int slab = kk >> 2, cb = (kk & 3) * 2;
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt) {
+                        const int row = 16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8;
+                        const int chunk = cb + (lane >> 4);
+                        const uint32_t addr = kbase + slab * 4096 + row * 128 + ((chunk ^ (row & 7)) << 4);
+                        uint32_t a0, a1, a2, a3;
+                        ldsm_x4(addr, a0, a1, a2, a3);
+                        mma_bf16(sh[mt], a0, a1, a2, a3, bh[kk][0], bh[kk][1]);
+                        mma_bf16(slo[mt], a0, a1, a2, a3, bl[kk][0], bl[kk][1]);
+                    }
+                }
+                // ---- online softmax (columns = heads 2t, 2t+1; rows = tokens)
+                float sv[2][4];
+                float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int r0 = 16 * mt + g, r1 = r0 + 8;
+                    sv[mt][0] = r0 < valid ? (sh[mt][0] + slo[mt][0]) * sl2 : -CUDART_INF_F;
+                    sv[mt][1] = r0 < valid ? (sh[mt][1] + slo[mt][1]) * sl2 : -CUDART_INF_F;
+                    sv[mt][2] = r1 < valid ? (sh[mt][2] + slo[mt][2]) * sl2 : -CUDART_INF_F;
+                    sv[mt][3] = r1 < valid ? (sh[mt][3] + slo[mt][3]) * sl2 : -CUDART_INF_F;
+                    mx0 = fmaxf(mx0, fmaxf(sv[mt][0], sv[mt][2]));
+                    mx1 = fmaxf(mx1, fmaxf(sv[mt][1], sv[mt][3]));
+                }
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) {
+                    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+                    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+                }
+                const float mn0 = fmaxf(m2[0], mx0), mn1 = fmaxf(m2[1], mx1);
+                const float al0 = fast_exp2(m2[0] - mn0), al1 = fast_exp2(m2[1] - mn1);
+                m2[0] = mn0;
+                m2[1] = mn1;
+                float ps0 = 0.f, ps1 = 0.f;
+                uint32_t pb[2][2];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const float p0 = fast_exp2(sv[mt][0] - mn0), p1 = fast_exp2(sv[mt][1] - mn1);
+                    const float p2 = fast_exp2(sv[mt][2] - mn0), p3 = fast_exp2(sv[mt][3] - mn1);
+                    ps0 += p0 + p2;
+                    ps1 += p1 + p3;
+                    pb[mt][0] = movmatrix_t(pack_bf16(p0, p1));
+                    pb[mt][1] = movmatrix_t(pack_bf16(p2, p3));
+                }
+                lp[0] = lp[0] * al0 + ps0;
+                lp[1] = lp[1] * al1 + ps1;
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+                    oacc[md][0] *= al0; oacc[md][1] *= al1; oacc[md][2] *= al0; oacc[md][3] *= al1;
+                }
+                // ---- O^T += V^T . P^T
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const int row = 16 * kk + (lane & 7) + ((lane >> 4) & 1) * 8;
+                        const int cg = 2 * md + ((lane >> 3) & 1);
+                        const uint32_t addr = vbase + (cg >> 3) * 4096 + row * 128 + (((cg & 7) ^ (row & 7)) << 4);
+                        uint32_t a0, a1, a2, a3;
+                        ldsm_x4_t(addr, a0, a1, a2, a3);
+                        mma_bf16(oacc[md], a0, a1, a2, a3, pb[kk][0], pb[kk][1]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[s]);
+            }
+        }
+        // ---- per-warp state -> combine buffer
+#pragma unroll
+        for (int o = 4; o < 32; o <<= 1) {
+            lp[0] += __shfl_xor_sync(0xffffffffu, lp[0], o);
+            lp[1] += __shfl_xor_sync(0xffffffffu, lp[1], o);
+        }
+#pragma unroll
+        for (int md = 0; md < 8; ++md) {
+            mycb[(2 * t) * CB_ROW + 16 * md + g] = oacc[md][0];
+            mycb[(2 * t + 1) * CB_ROW + 16 * md + g] = oacc[md][1];
+            mycb[(2 * t) * CB_ROW + 16 * md + g + 8] = oacc[md][2];
+            mycb[(2 * t + 1) * CB_ROW + 16 * md + g + 8] = oacc[md][3];
+        }
+        if (g == 0) {
+            mycb[8 * CB_ROW + 2 * t] = m2[0];
+            mycb[8 * CB_ROW + 2 * t + 1] = m2[1];
+            mycb[8 * CB_ROW + 8 + 2 * t] = lp[0];
+            mycb[8 * CB_ROW + 8 + 2 * t + 1] = lp[1];
+        }
+        named_bar_sync(1, NC * 32);
+        // ---- merge the NC warp states: thread -> head ctid/16, 8 channels
+        const int hh = ctid >> 4, d0 = (ctid & 15) * 8;
+        float M = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < NC; ++w) M = fmaxf(M, cbuf[w * CB_WARP + 8 * CB_ROW + hh]);
+        float L = 0.f, acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int w = 0; w < NC; ++w) {
+            const float* wb = cbuf + w * CB_WARP;
+            const float l = wb[8 * CB_ROW + 8 + hh];
+            if (!(l > 0.f)) continue;
+            const float f = exp2f(wb[8 * CB_ROW + hh] - M);
+            L += l * f;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += f * wb[hh * CB_ROW + d0 + e];
+        }
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        if (sg.nseg == 1) {
+            // the whole unit is here: merge with the CPU partial and write out
+            if (hh < G) {
+                const size_t head = static_cast<size_t>(u) * G + hh;
+                float cm = -CUDART_INF_F, cl = 0.f;
+                if (a.cpu_ml) { cm = a.cpu_ml[head * 2] * LOG2E; cl = a.cpu_ml[head * 2 + 1]; }
+                float Mt = M, wa = 1.f, wb = 0.f, Lt = L;
+                if (cl > 0.f) {
+                    Mt = fmaxf(M, cm);
+                    wa = L > 0.f ? exp2f(M - Mt) : 0.f;
+                    wb = cl * exp2f(cm - Mt);
+                    Lt = L * wa + wb;
+                }
+                const float invt = Lt > 0.f ? 1.f / Lt : 0.f;
+                float* o = a.o + head * D + d0;
+                float r[8];
+                if (cl > 0.f) {
+                    const float* co = a.cpu_o + head * D + d0;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) r[e] = (acc[e] * wa + wb * co[e]) * invt;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) r[e] = acc[e] * inv;
+                }
+                *reinterpret_cast<float4*>(o) = make_float4(r[0], r[1], r[2], r[3]);
+                *reinterpret_cast<float4*>(o + 4) = make_float4(r[4], r[5], r[6], r[7]);
+                if ((ctid & 15) == 0) {
+                    a.ml[head * 2] = Lt > 0.f ? Mt * LN2 : -CUDART_INF_F;
+                    a.ml[head * 2 + 1] = Lt;
+                }
+            }
+            named_bar_sync(1, NC * 32);  // combine buffer reuse
+        } else {
+            // write this segment's partial (o normalised, m2, l) to slot c+u
+            float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * (D + 2);
+            *reinterpret_cast<float4*>(p + d0) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+            *reinterpret_cast<float4*>(p + d0 + 4) =
+                make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+            if ((ctid & 15) == 0) { p[D] = M; p[D + 1] = L; }
+            __threadfence();
+            named_bar_sync(1, NC * 32);
+            if (ctid == 0) {
+                const int old = atomicAdd(&ctr[u], 1);
+                sm.last_flag = (old == sg.nseg - 1);
+            }
+            named_bar_sync(1, NC * 32);
+            if (sm.last_flag) {
+                // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
+                __threadfence();
+                finalize_unit<G>(a, u, parts, sg.cfirst + u, sg.nseg, ctid);
+                if (ctid == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
+            }
+        }
+    }
+    // ---- units with no resident block: output = CPU partial (or empty)
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        if (a.n_res[u] != 0) continue;
+        finalize_unit<G>(a, u, parts, 0, 0, ctid);
+    }
+}
+
+}  // namespace tc
+
+// ========================================================= f32 kernel ====
+// CUDA-core split-K path (f32 KV, config 1). CTA (unit, split) handles blocks
+// j = split, split+SIMPLE_SPLIT, ...; warp w handles tokens r = w, w+4, ...;
+// lane owns channels 4*lane .. 4*lane+3.
+namespace simple {
+constexpr int NW = 4;
+
+template <int G>
+__global__ void __launch_bounds__(NW * 32) decode_f32_kernel(const scout_decode_args a) {
+    __shared__ float sm_o[NW][G][D];
+    __shared__ float sm_ml[NW][G][2];
+    const int u = blockIdx.x, split = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ks = a.k_stride;
+    const int nres = a.n_res[u];
+    const int nt = a.n_tokens[u];
+    const int nb = (nt + BS - 1) / BS, tail = nt - (nb - 1) * BS;
+    const float sl2 = a.scale * LOG2E;
+    float qv[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const float4 x = *reinterpret_cast<const float4*>(a.q + (static_cast<size_t>(u) * G + g) * D + 4 * lane);
+        qv[g][0] = x.x; qv[g][1] = x.y; qv[g][2] = x.z; qv[g][3] = x.w;
+    }
+    float m2[G], l[G], o[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        m2[g] = -CUDART_INF_F; l[g] = 0.f;
+        o[g][0] = o[g][1] = o[g][2] = o[g][3] = 0.f;
+    }
+    const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
+    for (int j = split; j < nres; j += SIMPLE_SPLIT) {
+        const size_t slot = static_cast<size_t>(a.res_slots[static_cast<size_t>(u) * ks + j]);
+        const int id = a.res_ids[static_cast<size_t>(u) * ks + j];
+        const int rows = (id == nb - 1) ? tail : BS;
+        const float* kt = reinterpret_cast<const float*>(pool + slot * F32_SLOT_BYTES);
+        const float* vt = kt + BS * D;
+        for (int r = warp; r < rows; r += NW) {
+            const float4 k4 = *reinterpret_cast<const float4*>(kt + r * D + 4 * lane);
+            const float4 v4 = *reinterpret_cast<const float4*>(vt + r * D + 4 * lane);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float s = qv[g][0] * k4.x + qv[g][1] * k4.y + qv[g][2] * k4.z + qv[g][3] * k4.w;
+#pragma unroll
+                for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                s *= sl2;
+                const float mn = fmaxf(m2[g], s);
+                const float al = exp2f(m2[g] - mn), p = exp2f(s - mn);
+                m2[g] = mn;
+                l[g] = l[g] * al + p;
+                o[g][0] = o[g][0] * al + p * v4.x;
+                o[g][1] = o[g][1] * al + p * v4.y;
+                o[g][2] = o[g][2] * al + p * v4.z;
+                o[g][3] = o[g][3] * al + p * v4.w;
+            }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        *reinterpret_cast<float4*>(&sm_o[warp][g][4 * lane]) = make_float4(o[g][0], o[g][1], o[g][2], o[g][3]);
+        if (lane == 0) { sm_ml[warp][g][0] = m2[g]; sm_ml[warp][g][1] = l[g]; }
+    }
+    __syncthreads();
+    // combine the NW warps -> partial (o normalised, m2, l) for (unit, split)
+    float* parts = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + ctr_bytes(a.n_units));
+    float* p = parts + (static_cast<size_t>(u) * SIMPLE_SPLIT + split) * PART_STRIDE;
+    for (int i = threadIdx.x; i < G * D; i += NW * 32) {
+        const int g = i / D, d = i % D;
+        float M = -CUDART_INF_F;
+        for (int w = 0; w < NW; ++w) M = fmaxf(M, sm_ml[w][g][0]);
+        float L = 0.f, acc = 0.f;
+        for (int w = 0; w < NW; ++w) {
+            if (!(sm_ml[w][g][1] > 0.f)) continue;
+            const float f = exp2f(sm_ml[w][g][0] - M);
+            L += sm_ml[w][g][1] * f;
+            acc += sm_o[w][g][d] * f;
+        }
+        p[g * (D + 2) + d] = L > 0.f ? acc / L : 0.f;
+        if (d == 0) { p[g * (D + 2) + D] = M; p[g * (D + 2) + D + 1] = L; }
+    }
+}
+
+template <int G>
+__global__ void combine_kernel(const scout_decode_args a) {
+    const int u = blockIdx.x;
+    const float* parts = reinterpret_cast<const float*>(static_cast<const uint8_t*>(a.workspace) + ctr_bytes(a.n_units));
+    tc::finalize_unit<G>(a, u, parts, u * SIMPLE_SPLIT, SIMPLE_SPLIT, threadIdx.x);
+}
+}  // namespace simple
+
+int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+int tc_grid(int max_ctas) {
+    int g = max_ctas > 0 ? max_ctas : num_sms();
+    return g > GRID_CAP ? GRID_CAP : g;
+}
+
+}  // namespace
+
+extern "C" size_t scout_sparse_decode_workspace_bytes(int n_units, int group, int max_ctas) {
+    (void)group;
+    if (n_units < 0) return 0;
+    const size_t g = static_cast<size_t>(max_ctas > 0 ? (max_ctas > GRID_CAP ? GRID_CAP : max_ctas) : GRID_CAP);
+    const size_t slots_tc = g + static_cast<size_t>(n_units);
+    const size_t slots_simple = static_cast<size_t>(n_units) * SIMPLE_SPLIT;
+    const size_t slots = slots_tc > slots_simple ? slots_tc : slots_simple;
+    return ctr_bytes(n_units) + slots * PART_STRIDE * sizeof(float);
+}
+
+extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) {
+    using namespace scout_host;
+    if (!args) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_sparse_decode: null args");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    const scout_decode_args& a = *args;
+    if (a.n_units < 0 || a.k_stride <= 0) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_sparse_decode: bad n_units %d / k_stride %d", a.n_units,
+                  a.k_stride);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (!(a.scale > 0.f)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "partial_attention: scale must be > 0");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (a.group != 1 && a.group != 2 && a.group != 4 && a.group != 8) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_sparse_decode: group %d not in {1,2,4,8}", a.group);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (a.n_units == 0) return SCOUT_OK;
+    if (!a.q || !a.kv_pool || !a.res_slots || !a.res_ids || !a.n_res || !a.n_tokens || !a.o || !a.ml ||
+        !a.workspace || ((a.cpu_o == nullptr) != (a.cpu_ml == nullptr))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_sparse_decode: null buffer");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (a.workspace_bytes < scout_sparse_decode_workspace_bytes(a.n_units, a.group, a.max_ctas)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_sparse_decode: workspace too small (%zu < %zu)",
+                  a.workspace_bytes, scout_sparse_decode_workspace_bytes(a.n_units, a.group, a.max_ctas));
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    if (a.kv_dtype == SCOUT_BF16) {
+        // a CTA range must not touch more than MAXSEG units
+        const int min_grid = (a.n_units + tc::MAXSEG - 3) / (tc::MAXSEG - 2);
+        int grid = tc_grid(a.max_ctas);
+        if (grid < min_grid) grid = min_grid;
+        if (grid > GRID_CAP) grid = GRID_CAP;
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tc::SMEM_BYTES));
+            kern<<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(a);
+        };
+        switch (a.group) {
+            case 1: go(tc::sparse_decode_tc_kernel<1>); break;
+            case 2: go(tc::sparse_decode_tc_kernel<2>); break;
+            case 4: go(tc::sparse_decode_tc_kernel<4>); break;
+            default: go(tc::sparse_decode_tc_kernel<8>); break;
+        }
+    } else if (a.kv_dtype == SCOUT_F32) {
+        const dim3 grid(a.n_units, SIMPLE_SPLIT);
+        switch (a.group) {
+            case 1: simple::decode_f32_kernel<1><<<grid, simple::NW * 32, 0, st>>>(a);
+                    simple::combine_kernel<1><<<a.n_units, 128, 0, st>>>(a); break;
+            case 2: simple::decode_f32_kernel<2><<<grid, simple::NW * 32, 0, st>>>(a);
+                    simple::combine_kernel<2><<<a.n_units, 128, 0, st>>>(a); break;
+            case 4: simple::decode_f32_kernel<4><<<grid, simple::NW * 32, 0, st>>>(a);
+                    simple::combine_kernel<4><<<a.n_units, 128, 0, st>>>(a); break;
+            default: simple::decode_f32_kernel<8><<<grid, simple::NW * 32, 0, st>>>(a);
+                     simple::combine_kernel<8><<<a.n_units, 128, 0, st>>>(a); break;
+        }
+    } else {
+        set_error(SCOUT_ERR_UNSUPPORTED, "scout_sparse_decode: kv dtype %d unsupported", a.kv_dtype);
+        return SCOUT_ERR_UNSUPPORTED;
+    }
+    return check_launch("scout_sparse_decode");
+}

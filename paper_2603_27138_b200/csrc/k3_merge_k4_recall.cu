@@ -1,0 +1,106 @@
+// K3 — standalone LSE merge of partial sets; K4 — periodic-recall gather.
+//
+// K3 replaces merge (reference proj/include/scout/attention.hpp:100-114) for
+// callers that keep GPU and CPU partials apart (the fused path lives in K2).
+// Partials are (o normalised, m, l): the reference's (o_acc, max_logit, denom)
+// with o = o_acc / denom. Empty operands are exact identities (:101-102); both
+// empty give o = 0 (engine.hpp:273) and ml = (-inf, 0).
+//
+// K4 moves the bytes that TieredKvCache::begin_layer (kv_store.hpp:201-218)
+// only flags: whole block images from device-mapped pinned host memory into
+// freed pool slots, on a side stream, 16-byte loads over PCIe / C2C.
+#include "scout_common.cuh"
+
+#include <math_constants.h>
+
+using namespace scout_dev;
+
+namespace {
+
+__global__ void merge_kernel(const float* __restrict__ a_o, const float* __restrict__ a_ml,
+                             const float* __restrict__ b_o, const float* __restrict__ b_ml, float* out_o,
+                             float* out_ml, int n_rows) {
+    const int row = blockIdx.x;
+    if (row >= n_rows) return;
+    const int d = threadIdx.x;  // 0..127
+    const float ma = a_ml[2 * row], la = a_ml[2 * row + 1];
+    const float mb = b_ml[2 * row], lb = b_ml[2 * row + 1];
+    const float oa = a_o[static_cast<size_t>(row) * D + d], ob = b_o[static_cast<size_t>(row) * D + d];
+    float o, m, l;
+    if (!(la > 0.f) && !(lb > 0.f)) {
+        o = 0.f; m = -CUDART_INF_F; l = 0.f;
+    } else if (!(la > 0.f)) {
+        o = ob; m = mb; l = lb;
+    } else if (!(lb > 0.f)) {
+        o = oa; m = ma; l = la;
+    } else {
+        m = fmaxf(ma, mb);
+        const float wa = la * expf(ma - m), wb = lb * expf(mb - m);
+        l = wa + wb;
+        o = (wa * oa + wb * ob) / l;
+    }
+    __syncthreads();  // out may alias a
+    out_o[static_cast<size_t>(row) * D + d] = o;
+    if (d == 0) { out_ml[2 * row] = m; out_ml[2 * row + 1] = l; }
+}
+
+// One CTA per recalled block; each thread keeps 4 x 16 B loads in flight.
+__global__ void __launch_bounds__(256) recall_gather_kernel(uint8_t* pool, const uint8_t* host, const int64_t* src,
+                                                            const int32_t* dst, int n, size_t slot_bytes) {
+    const int i = blockIdx.x;
+    if (i >= n) return;
+    const int4* s = reinterpret_cast<const int4*>(host + static_cast<size_t>(src[i]) * slot_bytes);
+    int4* d = reinterpret_cast<int4*>(pool + static_cast<size_t>(dst[i]) * slot_bytes);
+    const int nvec = static_cast<int>(slot_bytes / 16);
+    for (int base = threadIdx.x; base < nvec; base += 4 * blockDim.x) {
+        int4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int idx = base + k * blockDim.x;
+            if (idx < nvec) v[k] = __ldcv(s + idx);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int idx = base + k * blockDim.x;
+            if (idx < nvec) d[idx] = v[k];
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" int scout_merge_partials(const float* a_o, const float* a_ml, const float* b_o, const float* b_ml,
+                                    float* out_o, float* out_ml, int n_rows, void* stream) {
+    using namespace scout_host;
+    if (n_rows < 0 || (n_rows > 0 && (!a_o || !a_ml || !b_o || !b_ml || !out_o || !out_ml))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_merge_partials: bad arguments");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (n_rows == 0) return SCOUT_OK;
+    merge_kernel<<<n_rows, D, 0, static_cast<cudaStream_t>(stream)>>>(a_o, a_ml, b_o, b_ml, out_o, out_ml, n_rows);
+    return check_launch("scout_merge_partials");
+}
+
+extern "C" int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host_blocks, const int64_t* src_index,
+                                   const int32_t* dst_slots, int n, void* stream) {
+    using namespace scout_host;
+    if (kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32) {
+        set_error(SCOUT_ERR_UNSUPPORTED, "scout_recall_gather: kv dtype %d unsupported", kv_dtype);
+        return SCOUT_ERR_UNSUPPORTED;
+    }
+    if (n < 0 || (n > 0 && (!kv_pool || !host_blocks || !src_index || !dst_slots))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_recall_gather: bad arguments");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (n == 0) return SCOUT_OK;
+    // pinned host memory is mapped under UVA; translate in case the mapping differs
+    void* dev_view = nullptr;
+    if (cudaHostGetDevicePointer(&dev_view, const_cast<void*>(host_blocks), 0) == cudaSuccess && dev_view)
+        host_blocks = dev_view;
+    else
+        cudaGetLastError();  // not a registered host pointer: use as given (e.g. device memory)
+    recall_gather_kernel<<<n, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<uint8_t*>(kv_pool), static_cast<const uint8_t*>(host_blocks), src_index, dst_slots, n,
+        slot_bytes(kv_dtype));
+    return check_launch("scout_recall_gather");
+}

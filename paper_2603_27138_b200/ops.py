@@ -1,0 +1,163 @@
+"""Torch-tensor entry points over the C ABI (device memory / streams only).
+
+Each function launches on torch's current CUDA stream and returns device
+tensors; torch is plumbing here, every computation is one of the sm_100a
+kernels in csrc/. Layouts are those of include/scout_b200.h.
+"""
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _capi as A
+
+_DTYPE_CODE = {torch.float32: A.SCOUT_F32, torch.bfloat16: A.SCOUT_BF16, torch.float64: A.SCOUT_F64}
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    return _DTYPE_CODE[dt]
+
+
+def slot_bytes(kv_dtype: torch.dtype) -> int:
+    return int(A.lib().scout_slot_bytes(dtype_code(kv_dtype)))
+
+
+def alloc_pool(n_slots: int, kv_dtype: torch.dtype, device="cuda") -> torch.Tensor:
+    """KV pool: n_slots blocks of (K, V) 64 x 128 in the kernel layout (raw bytes)."""
+    return torch.empty(n_slots * slot_bytes(kv_dtype), dtype=torch.uint8, device=device)
+
+
+def _i32(x, device):
+    return torch.as_tensor(x, dtype=torch.int32, device=device).contiguous()
+
+
+def kv_write_tokens(pool, kv_dtype, slots, rows, k_rows, v_rows):
+    dev = pool.device
+    slots, rows = _i32(slots, dev), _i32(rows, dev)
+    k_rows = k_rows.to(device=dev, dtype=torch.float32).contiguous()
+    v_rows = v_rows.to(device=dev, dtype=torch.float32).contiguous()
+    A.check(A.lib().scout_kv_write_tokens(_p(pool), dtype_code(kv_dtype), _p(slots), _p(rows), _p(k_rows),
+                                          _p(v_rows), int(slots.numel()), _stream()))
+
+
+def kv_read_tokens(pool, kv_dtype, slots, rows):
+    dev = pool.device
+    slots, rows = _i32(slots, dev), _i32(rows, dev)
+    n = int(slots.numel())
+    k = torch.empty(n, A.HEAD_DIM, dtype=torch.float32, device=dev)
+    v = torch.empty_like(k)
+    A.check(A.lib().scout_kv_read_tokens(_p(pool), dtype_code(kv_dtype), _p(slots), _p(rows), _p(k), _p(v), n,
+                                         _stream()))
+    return k, v
+
+
+def write_blocks(pool, kv_dtype, slots, keys, values):
+    """Write whole blocks: keys/values [n][rows<=64][128] -> slots[n] (rows 0..)."""
+    n, rows = keys.shape[0], keys.shape[1]
+    dev = pool.device
+    sl = _i32(slots, dev).repeat_interleave(rows)
+    rr = torch.arange(rows, device=dev, dtype=torch.int32).repeat(n)
+    kv_write_tokens(pool, kv_dtype, sl, rr, keys.reshape(-1, A.HEAD_DIM), values.reshape(-1, A.HEAD_DIM))
+
+
+def digest_build(pool, kv_dtype, method, slots, block_rows, units, block_ids, digests, nb_stride):
+    dev = pool.device
+    slots, block_rows, units, block_ids = (_i32(x, dev) for x in (slots, block_rows, units, block_ids))
+    A.check(A.lib().scout_digest_build(_p(pool), dtype_code(kv_dtype), int(method), int(slots.numel()), _p(slots),
+                                       _p(block_rows), _p(units), _p(block_ids), _p(digests), int(nb_stride),
+                                       _stream()))
+
+
+def score_topk_split(q, digests, n_tokens, k, group, *, method=A.SCOUT_DIGEST_MINMAX, block_table=None, step=0,
+                     k_stride=None, want_scores=False, last_selected=None, out=None):
+    """K1. q [units*G][128] (f32, or f64 for f64 digests); digests [units][2|1][128][nb_stride].
+
+    Returns a dict of device tensors: sel_ids/n_sel, and when block_table is given
+    res_slots/res_ids/n_res, cpu_ids/n_cpu, res_tokens/cpu_tokens (+ scores)."""
+    dev = digests.device
+    n_units = int(n_tokens.numel())
+    nb_stride = int(digests.shape[-1])
+    ks = int(k_stride or max(int(k), 1))
+    o = out if out is not None else {}
+
+    def buf(name, shape, dt=torch.int32):
+        if name not in o:
+            o[name] = torch.empty(shape, dtype=dt, device=dev)
+        return o[name]
+
+    args = A.TopkArgs()
+    args.n_units, args.group, args.digest_dtype, args.method = n_units, int(group), dtype_code(digests.dtype), int(method)
+    args.k, args.k_stride, args.nb_stride, args.step = int(k), ks, nb_stride, int(step)
+    args.q, args.digests, args.n_tokens = _p(q), _p(digests), _p(n_tokens)
+    args.sel_ids, args.n_sel = _p(buf("sel_ids", (n_units, ks))), _p(buf("n_sel", (n_units,)))
+    if block_table is not None:
+        args.block_table = _p(block_table)
+        args.res_slots, args.res_ids = _p(buf("res_slots", (n_units, ks))), _p(buf("res_ids", (n_units, ks)))
+        args.n_res, args.cpu_ids = _p(buf("n_res", (n_units,))), _p(buf("cpu_ids", (n_units, ks)))
+        args.n_cpu = _p(buf("n_cpu", (n_units,)))
+        args.res_tokens, args.cpu_tokens = _p(buf("res_tokens", (n_units,))), _p(buf("cpu_tokens", (n_units,)))
+    if last_selected is not None:
+        args.last_selected = _p(last_selected)
+    if want_scores:
+        args.scores_out = _p(buf("scores", (n_units, nb_stride), torch.float64))
+    A.check(A.lib().scout_score_topk_split(args, _stream()))
+    return o
+
+
+class DecodeWorkspace:
+    """Caller-owned K2 workspace (zeroed once; kernels leave counters zeroed)."""
+
+    def __init__(self, n_units: int, group: int, device="cuda", max_ctas: int = 0):
+        nbytes = int(A.lib().scout_sparse_decode_workspace_bytes(n_units, group, max_ctas))
+        self.buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+        self.n_units, self.max_ctas = n_units, max_ctas
+
+
+def sparse_decode(q, pool, kv_dtype, res_slots, res_ids, n_res, n_tokens, group, scale=None, *, cpu_o=None,
+                  cpu_ml=None, o=None, ml=None, workspace=None, max_ctas=0):
+    """K2 (+K3 fused). Returns (o [units*G][128] f32, ml [units*G][2] f32)."""
+    dev = q.device
+    n_units = int(n_tokens.numel())
+    if scale is None:
+        scale = 1.0 / math.sqrt(A.HEAD_DIM)
+    if o is None:
+        o = torch.empty(n_units * group, A.HEAD_DIM, dtype=torch.float32, device=dev)
+    if ml is None:
+        ml = torch.empty(n_units * group, 2, dtype=torch.float32, device=dev)
+    if workspace is None or workspace.n_units < n_units or workspace.max_ctas != max_ctas:
+        workspace = DecodeWorkspace(n_units, group, dev, max_ctas)
+    args = A.DecodeArgs()
+    args.n_units, args.group, args.kv_dtype, args.k_stride = n_units, int(group), dtype_code(kv_dtype), int(res_slots.shape[-1])
+    args.scale = float(scale)
+    args.q, args.kv_pool, args.res_slots, args.res_ids = _p(q), _p(pool), _p(res_slots), _p(res_ids)
+    args.n_res, args.n_tokens, args.cpu_o, args.cpu_ml = _p(n_res), _p(n_tokens), _p(cpu_o), _p(cpu_ml)
+    args.o, args.ml = _p(o), _p(ml)
+    args.workspace, args.workspace_bytes, args.max_ctas = _p(workspace.buf), workspace.buf.numel(), int(max_ctas)
+    A.check(A.lib().scout_sparse_decode(args, _stream()))
+    return o, ml
+
+
+def merge_partials(a_o, a_ml, b_o, b_ml, out_o=None, out_ml=None):
+    n = int(a_o.shape[0])
+    out_o = torch.empty_like(a_o) if out_o is None else out_o
+    out_ml = torch.empty_like(a_ml) if out_ml is None else out_ml
+    A.check(A.lib().scout_merge_partials(_p(a_o), _p(a_ml), _p(b_o), _p(b_ml), _p(out_o), _p(out_ml), n, _stream()))
+    return out_o, out_ml
+
+
+def recall_gather(pool, kv_dtype, host_blocks, src_index, dst_slots):
+    """K4. host_blocks: pinned CPU uint8 tensor of block images (slot layout)."""
+    dev = pool.device
+    src = torch.as_tensor(src_index, dtype=torch.int64, device=dev).contiguous()
+    dst = _i32(dst_slots, dev)
+    A.check(A.lib().scout_recall_gather(_p(pool), dtype_code(kv_dtype), _p(host_blocks), _p(src), _p(dst),
+                                        int(dst.numel()), _stream()))

@@ -1,0 +1,49 @@
+"""Shared test helpers: golden fixtures, bf16 round trips, synthetic unit builders."""
+from __future__ import annotations
+
+from pathlib import Path
+
+import numpy as np
+import torch
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+D, B = 128, 64
+
+
+def load_golden(name: str) -> dict[str, dict[str, np.ndarray]]:
+    z = np.load(GOLDEN / f"golden_{name}.npz")
+    out: dict[str, dict[str, np.ndarray]] = {}
+    for key in z.files:
+        case, field = key.split("__", 1)
+        out.setdefault(case, {})[field] = z[key]
+    return out
+
+
+def from_bf16(bits: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).view(torch.bfloat16).float().numpy()
+
+
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def nbs_for(nb: int) -> int:
+    return max(8, ((nb + 7) // 8) * 8)
+
+
+def make_digests(rng, U, nbs, kind="iid", dtype=np.float32):
+    """lo/hi [U][2][D][nbs] (bf16-exact values as f32)."""
+    if kind == "tie":
+        a = rng.integers(-2, 3, size=(U, D, nbs)).astype(np.float32)
+        b = rng.integers(-2, 3, size=(U, D, nbs)).astype(np.float32)
+    else:
+        a = rng.standard_normal((U, D, nbs)).astype(np.float32)
+        b = rng.standard_normal((U, D, nbs)).astype(np.float32)
+    lo, hi = np.minimum(a, b), np.maximum(a, b)
+    return bf16_round(np.stack([lo, hi], axis=1))
+
+
+def make_queries(rng, U, G, kind="iid"):
+    if kind == "tie":
+        return rng.integers(-1, 2, size=(U * G, D)).astype(np.float32)
+    return rng.standard_normal((U * G, D)).astype(np.float32)

@@ -1,0 +1,114 @@
+"""K1 parity on the GPU: selected block sets bit-exact against the reference
+(golden vectors) and the oracle (seeded iid / clustered / tie-prone inputs,
+ragged open blocks, k >= blocks, one block), plus the resident/CPU split."""
+import numpy as np
+import pytest
+import torch
+
+import py_oracle as P
+from helpers import D, from_bf16, load_golden, make_digests, make_queries, nbs_for
+from paper_2603_27138_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu_topk(q, dig, n_tokens, k, G, dtype=torch.bfloat16, table=None, want_scores=True, method=0, step=0,
+              last_sel=None):
+    dev = torch.device("cuda")
+    qd = torch.as_tensor(q, device=dev)
+    qd = qd.double() if dtype == torch.float64 else qd.float()
+    dd = torch.as_tensor(dig, device=dev).to(dtype).contiguous()
+    nt = torch.as_tensor(n_tokens, dtype=torch.int32, device=dev)
+    tb = None if table is None else torch.as_tensor(table, dtype=torch.int32, device=dev)
+    r = ops.score_topk_split(qd, dd, nt, k, G, block_table=tb, want_scores=want_scores, method=method, step=step,
+                             last_selected=last_sel)
+    torch.cuda.synchronize()
+    return {k_: v.cpu().numpy() for k_, v in r.items()}
+
+
+@pytest.mark.parametrize("case", sorted(load_golden("topk")))
+def test_topk_bit_exact_vs_reference_golden(cuda, case):
+    c = load_golden("topk")[case]
+    G, nt, k = int(c["G"]), int(c["n_tokens"]), int(c["k"])
+    nb = (nt + 63) // 64
+    dig = np.stack([from_bf16(c["lo"]), from_bf16(c["hi"])])[None]  # [1][2][D][nbs]
+    r = _gpu_topk(c["q"], dig, [nt], k, G)
+    assert r["n_sel"][0] == len(c["ids"])
+    assert np.array_equal(r["sel_ids"][0, : r["n_sel"][0]], c["ids"])
+    assert np.array_equal(r["scores"][0, :nb].view(np.uint64), c["scores"].view(np.uint64))
+
+
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
+@pytest.mark.parametrize("kind", ["iid", "tie"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_topk_split_vs_oracle(cuda, G, kind, dtype):
+    rng = np.random.default_rng(hash((G, kind, str(dtype))) % 2**32)
+    U = 24
+    n_tokens = rng.integers(1, 64 * 300, size=U).astype(np.int32)
+    n_tokens[0], n_tokens[1], n_tokens[2] = 64, 1, 64 * 300
+    nbs = nbs_for(300)
+    dig = make_digests(rng, U, nbs, kind)
+    q = make_queries(rng, U, G, kind)
+    table = np.where(rng.random((U, nbs)) < 0.8, rng.integers(0, 10**6, size=(U, nbs)), -1).astype(np.int32)
+    for k in (1, 7, 64, 300, 400):
+        want = P.score_topk_split(q, dig, n_tokens, k, G, table=table, k_stride=k)
+        got = _gpu_topk(q, dig, n_tokens, k, G, dtype=dtype, table=table)
+        for u in range(U):
+            ns = want["n_sel"][u]
+            assert got["n_sel"][u] == ns
+            assert np.array_equal(got["sel_ids"][u, :ns], want["sel_ids"][u, :ns]), (u, k)
+            nr, nc = want["n_res"][u], want["n_cpu"][u]
+            assert got["n_res"][u] == nr and got["n_cpu"][u] == nc
+            assert np.array_equal(got["res_ids"][u, :nr], want["res_ids"][u, :nr])
+            assert np.array_equal(got["res_slots"][u, :nr], want["res_slots"][u, :nr])
+            assert np.array_equal(got["cpu_ids"][u, :nc], want["cpu_ids"][u, :nc])
+            nb = (n_tokens[u] + 63) // 64
+            tail = n_tokens[u] - 64 * (nb - 1)
+            rows = lambda ids: sum(tail if i == nb - 1 else 64 for i in ids)  # noqa: E731
+            assert got["res_tokens"][u] == rows(want["res_ids"][u, :nr])
+            assert got["cpu_tokens"][u] == rows(want["cpu_ids"][u, :nc])
+            assert np.array_equal(got["scores"][u, :nb].view(np.uint64), want["scores"][u, :nb].view(np.uint64))
+
+
+def test_topk_generic_f64_paths(cuda):
+    """Arbitrary doubles (the drop-in wrapper's path): minmax and mean, no fma."""
+    rng = np.random.default_rng(7)
+    U, G, nbs = 6, 2, 64
+    n_tokens = np.full(U, 64 * 50, np.int32)
+    q = rng.standard_normal((U * G, D)) * np.pi
+    a, b = rng.standard_normal((U, D, nbs)) / 3, rng.standard_normal((U, D, nbs)) / 3
+    dig = np.stack([np.minimum(a, b), np.maximum(a, b)], axis=1)
+    for method, dg in ((0, dig), (1, dig[:, :1])):
+        want = P.score_topk_split(q, dg, n_tokens, 9, G, method=method)
+        got = _gpu_topk(q, dg, n_tokens, 9, G, dtype=torch.float64, method=method)
+        assert np.array_equal(got["sel_ids"][:, :9], want["sel_ids"][:, :9])
+        assert np.array_equal(got["scores"][:, :50], want["scores"][:, :50])
+
+
+def test_topk_kat_embedded(cuda):
+    """test_digest.cpp:46-55 KAT embedded in d=128 (zero padding adds +0.0)."""
+    dig = np.zeros((1, 2, D, 8), np.float32)
+    dig[0, 0, :2, 0], dig[0, 1, :2, 0] = [0.0, -2.0], [3.0, 1.0]
+    q = np.zeros((1, D), np.float32)
+    q[0, :2] = [1.0, -1.0]
+    r = _gpu_topk(q, dig, [64], 1, 1)
+    assert r["scores"][0, 0] == 5.0
+
+
+def test_topk_k_zero_rejected_and_mark_selected(cuda):
+    rng = np.random.default_rng(3)
+    dig = make_digests(rng, 2, 16)
+    q = make_queries(rng, 2, 1)
+    with pytest.raises(ValueError, match="k must be >= 1"):
+        _gpu_topk(q, dig, [640, 640], 0, 1)
+    last = torch.full((2, 16), -1, dtype=torch.int32, device="cuda")
+    r = _gpu_topk(q, dig, [640, 640], 4, 1, step=11, last_sel=last)
+    last = last.cpu().numpy()
+    for u in range(2):
+        assert set(np.nonzero(last[u] == 11)[0]) == set(r["sel_ids"][u, :4])
+
+
+def test_topk_empty_unit(cuda):
+    rng = np.random.default_rng(5)
+    r = _gpu_topk(make_queries(rng, 2, 1), make_digests(rng, 2, 8), [0, 128], 3, 1)
+    assert r["n_sel"][0] == 0 and r["n_sel"][1] == 2
