@@ -36,7 +36,8 @@ constexpr float LOG2E = 1.4426950408889634f;
 constexpr float LN2 = 0.6931471805599453f;
 
 // ------------------------------------------------------------ workspace --
-constexpr int PART_STRIDE = 8 * (D + 2);  // floats per partial slot: [8 heads][o(128), m, l]
+constexpr int HEAD_STRIDE = D + 4;         // per head in a partial slot: o(128), m, l, pad (16B-aligned)
+constexpr int PART_STRIDE = 8 * HEAD_STRIDE;  // floats per partial slot: [8 heads]
 constexpr int SIMPLE_SPLIT = 8;
 constexpr int GRID_CAP = 1024;
 
@@ -85,7 +86,7 @@ __device__ void finalize_unit(const scout_decode_args& a, int u, const float* pa
     const size_t head = static_cast<size_t>(u) * G + h;
     float M = -CUDART_INF_F;
     for (int i = 0; i < nslots; ++i) {
-        const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * (D + 2);
+        const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * HEAD_STRIDE;
         M = fmaxf(M, __ldcg(p + D));
     }
     float cm = -CUDART_INF_F, cl = 0.f;
@@ -98,7 +99,7 @@ __device__ void finalize_unit(const scout_decode_args& a, int u, const float* pa
     float L = 0.f;
     if (M != -CUDART_INF_F) {
         for (int i = 0; i < nslots; ++i) {
-            const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * (D + 2);
+            const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * HEAD_STRIDE;
             const float l = __ldcg(p + D + 1);
             if (!(l > 0.f)) continue;
             const float w = l * exp2f(__ldcg(p + D) - M);
@@ -162,8 +163,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
         for (int w = 0; w < NTHREADS / 32; ++w) T += sm.scan_tot[w];
         __syncthreads();
     }
-    const long long grid = gridDim.x, c = blockIdx.x;
-    const long long lo = T * c / grid, hi = T * (c + 1) / grid;
+    // Ranges are cut over geff = min(grid, T) CTAs so that every range is
+    // non-empty: a unit's segment count is then the number of CTAs between
+    // the ones holding its first and last block. CTAs >= geff only do the
+    // zero-length-unit duty at the end.
+    const long long grid = T < static_cast<long long>(gridDim.x) ? (T > 0 ? T : 1) : gridDim.x;
+    const long long c = blockIdx.x;
+    const long long lo = c < grid ? T * c / grid : T, hi = c < grid ? T * (c + 1) / grid : T;
 
     // ---- pass 2: exclusive prefix over units -> this CTA's segments
     for (int base = 0; base < nunits; base += NTHREADS) {
@@ -290,6 +296,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
                 mbar_wait(&sm.full[s], (q / NST) & 1);
                 const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES);
                 const uint32_t vbase = kbase + HALF_BYTES_BF16;
+                if (valid < HALF_ROWS) {
+                    // rows past the open block's fill hold stale bytes: P is 0
+                    // there, but 0 * NaN would poison O, so zero those V rows.
+                    for (int i = lane; i < (HALF_ROWS - valid) * 16; i += 32) {
+                        const int row = valid + (i >> 4), chunk = i & 15;
+                        const uint32_t addr = vbase + (chunk >> 3) * 4096 + row * 128 + ((chunk & 7) << 4);
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0) : "memory");
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                }
                 // ---- S^T = K . Q^T
                 float sh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, slo[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
@@ -433,7 +450,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
             named_bar_sync(1, NC * 32);  // combine buffer reuse
         } else {
             // write this segment's partial (o normalised, m2, l) to slot c+u
-            float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * (D + 2);
+            float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
             *reinterpret_cast<float4*>(p + d0) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
             *reinterpret_cast<float4*>(p + d0 + 4) =
                 make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
@@ -539,8 +556,8 @@ __global__ void __launch_bounds__(NW * 32) decode_f32_kernel(const scout_decode_
             L += sm_ml[w][g][1] * f;
             acc += sm_o[w][g][d] * f;
         }
-        p[g * (D + 2) + d] = L > 0.f ? acc / L : 0.f;
-        if (d == 0) { p[g * (D + 2) + D] = M; p[g * (D + 2) + D + 1] = L; }
+        p[g * HEAD_STRIDE + d] = L > 0.f ? acc / L : 0.f;
+        if (d == 0) { p[g * HEAD_STRIDE + D] = M; p[g * HEAD_STRIDE + D + 1] = L; }
     }
 }
 
