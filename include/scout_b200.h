@@ -191,6 +191,65 @@ int scout_merge_partials(const float* a_o, const float* a_ml, const float* b_o, 
 int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host_blocks,
                         const int64_t* src_index, const int32_t* dst_slots, int n, void* stream);
 
+/* ------------------------------------------------------------- engine --
+ * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,
+ * engine.hpp:205-314, GPU side): per layer i, K1 for layer i+1 with the
+ * predicted query (layer 0: K1 with the true query, pinned resident,
+ * engine.hpp:227-233), K2+K3 for layer i with the true query over the
+ * resident share chosen during layer i-1, merged with layer i's CPU partial;
+ * then, every recall_interval steps (staggered: layer i recalls when
+ * (step + i) % interval == 0), K4 moves that layer's recall plan host->device
+ * on a side stream; layer i's next attention waits for it (issue (m, i) ->
+ * visible (m+1, i), kv_store.hpp:175-218). The tier policy (which blocks go
+ * where) stays with the caller: it owns the tables and recall plans.       */
+typedef struct scout_layer_desc {
+    const void* digests;         /* [U][2][128][nb_stride] in kv dtype */
+    const int32_t* block_table;  /* [U][nb_stride] slot or -1 (planning view) */
+    const int64_t* recall_src;   /* optional recall plan: host block indices */
+    const int32_t* recall_dst;   /* ... and destination pool slots */
+    int recall_n;
+} scout_layer_desc;
+
+typedef struct scout_engine_config {
+    int layers, batch, hq, hkv, k, nb_stride, kv_dtype;
+    float scale;
+    int recall_interval;       /* 0 disables K4 */
+    void* kv_pool;
+    const int32_t* n_tokens;   /* [U] device */
+    const void* host_tier;     /* pinned host block images (K4 source) */
+    int max_ctas;              /* K2 grid (0 = one CTA per SM) */
+    int host_staging;          /* 1: allocate device staging for decode_step_host */
+    int chunk_layers;          /* layers per H2D/D2H chunk of the host path (0 = 8) */
+} scout_engine_config;
+
+typedef struct scout_engine scout_engine;
+
+int scout_engine_create(const scout_engine_config* cfg, const scout_layer_desc* layers, scout_engine** out);
+int scout_engine_destroy(scout_engine* eng);
+/* One decode step, device-resident inputs: q_true / q_pred / cpu_o [L][U*G][128],
+ * cpu_ml [L][U*G][2] f32; outputs out_o [L][U*G][128], out_ml [L][U*G][2]. */
+int scout_engine_decode_step(scout_engine* eng, int step, const float* q_true, const float* q_pred,
+                             const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml, void* stream);
+/* Same step from pinned HOST buffers (same layouts): H2D of the inputs and
+ * D2H of the outputs plus each layer's CPU-side block ids (h_cpu_ids
+ * [L][U][k], h_n_cpu [L][U], the host co-attention worker's input) are
+ * pipelined by layer chunks on copy streams. Completion is ordered on
+ * `stream`: synchronise it before reading the host outputs. */
+int scout_engine_decode_step_host(scout_engine* eng, int step, const float* h_q_true, const float* h_q_pred,
+                                  const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o, float* h_out_ml,
+                                  int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream);
+/* Order all outstanding side-stream work (recalls) before `stream`. */
+int scout_engine_sync(scout_engine* eng, void* stream);
+/* Instrumentation: when enabled, CUDA events bracket every K2 launch (on the
+ * launching stream). scout_engine_stats synchronises, reports the summed K2
+ * event time, K2 count and the number of kernels launched since the last
+ * call, then resets. */
+int scout_engine_set_timing(scout_engine* eng, int enable);
+int scout_engine_stats(scout_engine* eng, double* k2_ms_total, int* k2_count, long long* launches);
+/* Device views of the engine's per-layer K1 outputs ([L][U][k] / [L][U]). */
+int scout_engine_k1_outputs(scout_engine* eng, int32_t** res_slots, int32_t** res_ids, int32_t** n_res,
+                            int32_t** cpu_ids, int32_t** n_cpu, int32_t** res_tokens, int32_t** cpu_tokens);
+
 #ifdef __cplusplus
 }
 #endif

@@ -17,6 +17,8 @@ OBJ = PKG / "_obj"
 LIB = PKG / "libscout_b200.so"
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+CXX = os.environ.get("CXX", "g++")
+CUDA_INC = "/usr/local/cuda/include"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
            "-diag-suppress", "177", f"-I{ROOT / 'include'}"]
@@ -43,8 +45,9 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         objs.append(obj)
         if force or _stale(obj, [src] + hdrs):
             cmd = [NVCC, *ARCH, *NVFLAGS, "-c", str(src), "-o", str(obj)]
-            if src.suffix == ".cpp":
-                cmd = [NVCC, *NVFLAGS, "-x", "c++", "-c", str(src), "-o", str(obj)]
+            if src.suffix == ".cpp":  # host-only C++: the system compiler
+                cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{CUDA_INC}", f"-I{ROOT / 'include'}",
+                       "-c", str(src), "-o", str(obj)]
             if verbose:
                 print(" ".join(cmd))
             subprocess.run(cmd, check=True)

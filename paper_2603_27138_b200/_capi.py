@@ -28,6 +28,8 @@ EXPORTED = (
     "scout_kv_write_tokens", "scout_kv_read_tokens", "scout_digest_build",
     "scout_score_topk_split", "scout_sparse_decode_workspace_bytes",
     "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather",
+    "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
+    "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k1_outputs",
 )
 
 _vp = C.c_void_p
@@ -52,6 +54,20 @@ class DecodeArgs(C.Structure):
         ("q", _vp), ("kv_pool", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
         ("n_tokens", _vp), ("cpu_o", _vp), ("cpu_ml", _vp), ("o", _vp), ("ml", _vp),
         ("workspace", _vp), ("workspace_bytes", C.c_size_t), ("max_ctas", C.c_int),
+    ]
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [("digests", _vp), ("block_table", _vp), ("recall_src", _vp), ("recall_dst", _vp),
+                ("recall_n", C.c_int)]
+
+
+class EngineConfig(C.Structure):
+    _fields_ = [
+        ("layers", C.c_int), ("batch", C.c_int), ("hq", C.c_int), ("hkv", C.c_int), ("k", C.c_int),
+        ("nb_stride", C.c_int), ("kv_dtype", C.c_int), ("scale", C.c_float), ("recall_interval", C.c_int),
+        ("kv_pool", _vp), ("n_tokens", _vp), ("host_tier", _vp), ("max_ctas", C.c_int),
+        ("host_staging", C.c_int), ("chunk_layers", C.c_int),
     ]
 
 
@@ -84,6 +100,14 @@ def lib() -> C.CDLL:
         L.scout_sparse_decode.argtypes = [C.POINTER(DecodeArgs), _vp]
         L.scout_merge_partials.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_recall_gather.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]
+        L.scout_engine_create.argtypes = [C.POINTER(EngineConfig), C.POINTER(LayerDesc), C.POINTER(_vp)]
+        L.scout_engine_destroy.argtypes = [_vp]
+        L.scout_engine_decode_step.argtypes = [_vp, C.c_int] + [_vp] * 6 + [_vp]
+        L.scout_engine_decode_step_host.argtypes = [_vp, C.c_int] + [_vp] * 8 + [_vp]
+        L.scout_engine_sync.argtypes = [_vp, _vp]
+        L.scout_engine_set_timing.argtypes = [_vp, C.c_int]
+        L.scout_engine_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]
+        L.scout_engine_k1_outputs.argtypes = [_vp] + [C.POINTER(_vp)] * 7
         _lib = L
     return _lib
 

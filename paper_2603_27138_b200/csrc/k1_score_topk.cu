@@ -316,7 +316,11 @@ template <typename DigT, int MODE>
 int launch_g(const scout_topk_args& a, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(D) * a.group * 8 + static_cast<size_t>(a.nb_stride) * 8;
     auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        static size_t configured = 0;  // per instantiation; the attribute call is not free
+        if (smem > 48 * 1024 && smem > configured) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            configured = smem;
+        }
         kern<<<a.n_units, K1_THREADS, smem, st>>>(a);
     };
     switch (a.group) {

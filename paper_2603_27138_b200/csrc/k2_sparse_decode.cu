@@ -636,7 +636,12 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
         if (grid < min_grid) grid = min_grid;
         if (grid > GRID_CAP) grid = GRID_CAP;
         auto go = [&](auto kern) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(tc::SMEM_BYTES));
+            static bool configured = false;  // per instantiation
+            if (!configured) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tc::SMEM_BYTES));
+                configured = true;
+            }
             kern<<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(a);
         };
         switch (a.group) {

@@ -1,0 +1,110 @@
+"""Python handle on the C++ decode-step engine (csrc/engine.cpp, C ABI
+scout_engine_*): the GPU side of ScoutEngine::decode_step
+(reference proj/include/scout/engine.hpp:205-314).
+
+The engine is C++; this class only passes device / pinned-host pointers and
+the current torch stream. Tier policy (tables, recall plans) is owned by the
+caller, as in the reference where it lives in TieredKvCache / recall.hpp.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _capi as A
+from . import ops
+
+
+@dataclass
+class LayerState:
+    digests: torch.Tensor                     # [U][2][128][nbs] kv dtype
+    table: torch.Tensor                       # [U][nbs] int32 slot or -1 (planning view)
+    recall_src: torch.Tensor | None = None    # [n] int64 host block index
+    recall_dst: torch.Tensor | None = None    # [n] int32 pool slot
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+class DecodeEngine:
+    def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
+                 recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8):
+        self.L, self.batch, self.hq, self.hkv, self.G, self.k = layers, batch, hq, hkv, hq // hkv, k
+        self.U = batch * hkv
+        self.layer_states = layer_states  # keep tensors alive
+        self.n_tokens = n_tokens
+        self.pool, self.host_tier = pool, host_tier
+        cfg = A.EngineConfig()
+        cfg.layers, cfg.batch, cfg.hq, cfg.hkv, cfg.k = layers, batch, hq, hkv, k
+        cfg.nb_stride = int(layer_states[0].digests.shape[-1])
+        cfg.kv_dtype = ops.dtype_code(kv_dtype)
+        cfg.scale = float(scale)
+        cfg.recall_interval = int(recall_interval)
+        cfg.kv_pool, cfg.n_tokens, cfg.host_tier = _p(pool), _p(n_tokens), _p(host_tier)
+        cfg.max_ctas, cfg.host_staging, cfg.chunk_layers = int(max_ctas), int(host_staging), int(chunk_layers)
+        descs = (A.LayerDesc * layers)()
+        for i, st in enumerate(layer_states):
+            descs[i].digests, descs[i].block_table = _p(st.digests), _p(st.table)
+            if st.recall_src is not None:
+                descs[i].recall_src, descs[i].recall_dst = _p(st.recall_src), _p(st.recall_dst)
+                descs[i].recall_n = int(st.recall_dst.numel())
+        h = C.c_void_p()
+        A.check(A.lib().scout_engine_create(C.byref(cfg), descs, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            A.lib().scout_engine_destroy(h)
+            self._h = None
+
+    @staticmethod
+    def _stream():
+        return torch.cuda.current_stream().cuda_stream
+
+    def decode_step(self, step, q_true, q_pred, cpu_o, cpu_ml, out_o, out_ml):
+        """Device tensors: q_true/q_pred/cpu_o/out_o [L][U*G][128] f32, cpu_ml/out_ml [L][U*G][2]."""
+        A.check(A.lib().scout_engine_decode_step(self._h, int(step), _p(q_true), _p(q_pred), _p(cpu_o), _p(cpu_ml),
+                                                 _p(out_o), _p(out_ml), self._stream()))
+
+    def decode_step_host(self, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, h_out_o, h_out_ml, h_cpu_ids=None,
+                         h_n_cpu=None):
+        """Pinned host tensors, same layouts; h_cpu_ids [L][U][k], h_n_cpu [L][U] int32."""
+        A.check(A.lib().scout_engine_decode_step_host(self._h, int(step), _p(h_q_true), _p(h_q_pred), _p(h_cpu_o),
+                                                      _p(h_cpu_ml), _p(h_out_o), _p(h_out_ml), _p(h_cpu_ids),
+                                                      _p(h_n_cpu), self._stream()))
+
+    def sync(self):
+        A.check(A.lib().scout_engine_sync(self._h, self._stream()))
+
+    def set_timing(self, on: bool):
+        A.check(A.lib().scout_engine_set_timing(self._h, int(on)))
+
+    def stats(self):
+        ms, n, launches = C.c_double(), C.c_int(), C.c_longlong()
+        A.check(A.lib().scout_engine_stats(self._h, C.byref(ms), C.byref(n), C.byref(launches)))
+        return ms.value, n.value, launches.value
+
+    def k1_outputs(self):
+        """Zero-copy torch views of the engine's per-layer K1 outputs (device)."""
+        ptrs = [C.c_void_p() for _ in range(7)]
+        A.check(A.lib().scout_engine_k1_outputs(self._h, *[C.byref(p) for p in ptrs]))
+        L, U, k = self.L, self.U, self.k
+        names = ["res_slots", "res_ids", "n_res", "cpu_ids", "n_cpu", "res_tokens", "cpu_tokens"]
+        shapes = [(L, U, k), (L, U, k), (L, U), (L, U, k), (L, U), (L, U), (L, U)]
+        return {n: torch.as_tensor(_DeviceArray(p.value, sh), device=self.pool.device)
+                for n, p, sh in zip(names, ptrs, shapes)}
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ over engine-owned int32 device memory."""
+
+    def __init__(self, ptr, shape):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i4", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+__all__ = ["DecodeEngine", "LayerState"]
