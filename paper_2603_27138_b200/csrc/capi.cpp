@@ -2,6 +2,8 @@
 // slot geometry. (Status convention: include/scout_b200.h.)
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 
 #include <cuda_runtime.h>
 
@@ -27,6 +29,16 @@ int check_launch(const char* what) {
         return SCOUT_ERR_CUDA;
     }
     return SCOUT_OK;
+}
+void ensure_smem(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[kernel];
+    if (bytes > have) {
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+        have = bytes;
+    }
 }
 }  // namespace scout_host
 

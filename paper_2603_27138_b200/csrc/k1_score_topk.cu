@@ -24,7 +24,7 @@ using namespace scout_dev;
 
 namespace {
 
-constexpr int K1_THREADS = 256;
+constexpr int K1_THREADS = 512;
 constexpr int K1_WARPS = K1_THREADS / 32;
 
 __device__ __forceinline__ uint64_t score_key(double s) {
@@ -74,87 +74,166 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
     return before;
 }
 
-// Scores for one unit. MODE 0: exact minmax (f32 q x f32/bf16 digests, fma),
-// MODE 1: generic f64 minmax, MODE 2: generic f64 mean.
-template <typename DigT, int G, int MODE>
-__device__ __forceinline__ void score_unit(const scout_topk_args& a, int u, int nb, const double* qs,
-                                           uint64_t* keys) {
-    const size_t ns = static_cast<size_t>(a.nb_stride);
-    if constexpr (MODE == 0) {
-        const DigT* lo = static_cast<const DigT*>(a.digests) + static_cast<size_t>(u) * 2 * D * ns;
-        const DigT* hi = lo + D * ns;
-        const int npairs = (nb + 1) >> 1;
-        for (int p = threadIdx.x; p < npairs; p += K1_THREADS) {
-            const int b0 = 2 * p;
-            double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll 4
-            for (int c = 0; c < D; ++c) {
-                double l0, l1, h0, h1;
-                if constexpr (sizeof(DigT) == 2) {
-                    const __nv_bfloat162 lv = *reinterpret_cast<const __nv_bfloat162*>(lo + c * ns + b0);
-                    const __nv_bfloat162 hv = *reinterpret_cast<const __nv_bfloat162*>(hi + c * ns + b0);
-                    l0 = widen(lv.x); l1 = widen(lv.y); h0 = widen(hv.x); h1 = widen(hv.y);
-                } else {
-                    const float2 lv = *reinterpret_cast<const float2*>(lo + c * ns + b0);
-                    const float2 hv = *reinterpret_cast<const float2*>(hi + c * ns + b0);
-                    l0 = lv.x; l1 = lv.y; h0 = hv.x; h1 = hv.y;
-                }
+// ------------------------------------------------------------- scoring --
+// Exact reference-order score of one block (MODE 0): fma chain over the
+// stacked vector, channel-major (digest.hpp:62-72 on q_s[c*G+g]).
+template <typename DigT, int G>
+__device__ __forceinline__ double exact_score_minmax(const DigT* lo, const DigT* hi, size_t ns, int b,
+                                                     const double* qs) {
+    double acc = 0.0;
+    for (int c = 0; c < D; ++c) {
+        const double l = widen(lo[c * ns + b]), h = widen(hi[c * ns + b]);
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const double qv = qs[c * G + g];
-                    const bool pos = qv >= 0.0;
-                    acc0 = fma(qv, pos ? h0 : l0, acc0);
-                    acc1 = fma(qv, pos ? h1 : l1, acc1);
-                }
-            }
-            keys[b0] = score_key(acc0);
-            if (a.scores_out) a.scores_out[u * ns + b0] = acc0;
-            if (b0 + 1 < nb) {
-                keys[b0 + 1] = score_key(acc1);
-                if (a.scores_out) a.scores_out[u * ns + b0 + 1] = acc1;
-            }
-        }
-    } else if constexpr (MODE == 1) {
-        const double* lo = static_cast<const double*>(a.digests) + static_cast<size_t>(u) * 2 * D * ns;
-        const double* hi = lo + D * ns;
-        for (int b = threadIdx.x; b < nb; b += K1_THREADS) {
-            double acc = 0.0;
-            for (int c = 0; c < D; ++c) {
-                const double l = lo[c * ns + b], h = hi[c * ns + b];
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const double qv = qs[c * G + g];
-                    acc = __dadd_rn(acc, ref_max(__dmul_rn(qv, l), __dmul_rn(qv, h)));
-                }
-            }
-            keys[b] = score_key(acc);
-            if (a.scores_out) a.scores_out[u * ns + b] = acc;
-        }
-    } else {
-        const double* mean = static_cast<const double*>(a.digests) + static_cast<size_t>(u) * D * ns;
-        for (int b = threadIdx.x; b < nb; b += K1_THREADS) {
-            double acc = 0.0;
-            for (int c = 0; c < D; ++c) {
-                const double m = mean[c * ns + b];
-#pragma unroll
-                for (int g = 0; g < G; ++g) acc = __dadd_rn(acc, __dmul_rn(qs[c * G + g], m));
-            }
-            keys[b] = score_key(acc);
-            if (a.scores_out) a.scores_out[u * ns + b] = acc;
+        for (int g = 0; g < G; ++g) {
+            const double qv = qs[c * G + g];
+            acc = fma(qv, qv >= 0.0 ? h : l, acc);
         }
     }
+    return acc;
 }
 
+// Generic f64 paths (the drop-in wrapper): exact, no contraction.
+template <int G, int MODE>
+__device__ __forceinline__ double exact_score_f64(const double* dig, size_t ns, int b, const double* qs) {
+    double acc = 0.0;
+    if constexpr (MODE == 1) {
+        const double* lo = dig;
+        const double* hi = dig + D * ns;
+        for (int c = 0; c < D; ++c) {
+            const double l = lo[c * ns + b], h = hi[c * ns + b];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double qv = qs[c * G + g];
+                acc = __dadd_rn(acc, ref_max(__dmul_rn(qv, l), __dmul_rn(qv, h)));
+            }
+        }
+    } else {
+        for (int c = 0; c < D; ++c) {
+            const double m = dig[c * ns + b];
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc = __dadd_rn(acc, __dmul_rn(qs[c * G + g], m));
+        }
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double key_to_double(uint64_t k) {
+    const uint64_t u = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+    return __longlong_as_double(static_cast<long long>(u));
+}
+
+struct SelScratch {
+    uint32_t hist[256];
+    uint64_t cand[32];
+    uint64_t prefix;
+    int krem;
+    int count;
+    int n;
+};
+
+// k-th largest key among the candidates (radix select, 8-bit digits, MSB
+// first; once <= 32 candidates share the prefix one warp finishes by rank).
+// Returns thr and need_eq = how many candidates equal to thr belong to the
+// top k (the lowest ids among them, digest.hpp:108-111). k <= #candidates.
+template <class KeyF, class CandF>
+__device__ void radix_kth(int nb, int k, KeyF keyf, CandF candf, SelScratch& S, uint64_t& thr, int& need_eq) {
+    const int tid = threadIdx.x;
+    uint64_t prefix = 0, mask = 0;
+    int krem = k;
+    for (int pass = 0; pass < 8; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (int i = tid; i < 256; i += K1_THREADS) S.hist[i] = 0;
+        __syncthreads();
+        for (int b = tid; b < nb; b += K1_THREADS) {
+            if (!candf(b)) continue;
+            const uint64_t key = keyf(b);
+            if ((key & mask) == prefix) atomicAdd(&S.hist[(key >> shift) & 255u], 1u);
+        }
+        __syncthreads();
+        if (tid < 32) {
+            uint32_t cnt[8];
+            uint32_t local = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                cnt[i] = S.hist[255 - 8 * tid - i];  // lane l: bins 255-8l .. 248-8l
+                local += cnt[i];
+            }
+            uint32_t incl = local;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            const uint32_t excl = incl - local;
+            if (excl < static_cast<uint32_t>(krem) && incl >= static_cast<uint32_t>(krem)) {
+                uint32_t cum = excl;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (cum + cnt[i] >= static_cast<uint32_t>(krem)) {
+                        S.prefix = prefix | (static_cast<uint64_t>(255 - 8 * tid - i) << shift);
+                        S.krem = krem - static_cast<int>(cum);
+                        S.count = static_cast<int>(cnt[i]);
+                        break;
+                    }
+                    cum += cnt[i];
+                }
+            }
+        }
+        __syncthreads();
+        prefix = S.prefix;
+        krem = S.krem;
+        mask |= 0xFFull << shift;
+        if (pass < 7 && S.count <= 32) {
+            // few candidates left: gather them and rank inside one warp
+            if (tid == 0) S.n = 0;
+            __syncthreads();
+            for (int b = tid; b < nb; b += K1_THREADS) {
+                if (!candf(b)) continue;
+                const uint64_t key = keyf(b);
+                if ((key & mask) == prefix) S.cand[atomicAdd(&S.n, 1)] = key;
+            }
+            __syncthreads();
+            if (tid < 32) {
+                const int n = S.n;
+                const uint64_t mine = tid < n ? S.cand[tid] : 0;
+                int gt = 0, eq = 0;
+                for (int j = 0; j < n; ++j) {
+                    const uint64_t o = S.cand[j];
+                    gt += o > mine;
+                    eq += o == mine;
+                }
+                __syncwarp();
+                if (tid < n && gt < krem && krem <= gt + eq) {
+                    S.prefix = mine;
+                    S.krem = krem - gt;
+                }
+            }
+            __syncthreads();
+            thr = S.prefix;
+            need_eq = S.krem;
+            __syncthreads();
+            return;
+        }
+    }
+    thr = prefix;
+    need_eq = krem;
+}
+
+enum : uint8_t { CLS_OUT = 0, CLS_IN = 1, CLS_Z = 2 };
+
 template <typename DigT, int G, int MODE>
-__global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk_args a) {
+__global__ void __launch_bounds__(K1_THREADS, 2) score_topk_kernel(const scout_topk_args a) {
     extern __shared__ __align__(16) uint8_t k1_smem[];
-    double* qs = reinterpret_cast<double*>(k1_smem);              // [D][G] stacked order
-    uint64_t* keys = reinterpret_cast<uint64_t*>(qs + D * G);     // [nb_stride]
-    __shared__ uint32_t hist[256];
+    double* qs = reinterpret_cast<double*>(k1_smem);            // [D][G] stacked order
+    double2* pn = reinterpret_cast<double2*>(qs + D * G);       // [D] (sum q>=0, sum q<0)
+    float2* pna = reinterpret_cast<float2*>(pn + D);            // [D] abs sums, rounded up
+    uint64_t* keys = reinterpret_cast<uint64_t*>(pna + D);      // [nb_stride]
+    uint8_t* cls = reinterpret_cast<uint8_t*>(keys + a.nb_stride);  // [nb_stride]
+    __shared__ SelScratch S;
     __shared__ int warp_tot[K1_WARPS];
-    __shared__ uint64_t s_prefix;
-    __shared__ int s_krem;
     __shared__ int s_tok[2];
+    __shared__ int s_cnt[2];
+    __shared__ float s_amax;
 
     const int u = blockIdx.x;
     const int tid = threadIdx.x;
@@ -162,8 +241,8 @@ __global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk
     ntok = max(0, min(ntok, a.nb_stride * BS));
     const int nb = (ntok + BS - 1) / BS;
     const int tail = ntok - (nb - 1) * BS;
+    const size_t ns = static_cast<size_t>(a.nb_stride);
 
-    // stage the G queries in stacked channel-major order q_s[c*G+g] (double)
     for (int i = tid; i < D * G; i += K1_THREADS) {
         const int g = i / D, c = i % D;
         double v;
@@ -171,99 +250,192 @@ __global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk
         else v = static_cast<const double*>(a.q)[(static_cast<size_t>(u) * G + g) * D + c];
         qs[c * G + g] = v;
     }
-    if (tid < 2) s_tok[tid] = 0;
-    __syncthreads();
-
-    score_unit<DigT, G, MODE>(a, u, nb, qs, keys);
+    if (tid < 2) { s_tok[tid] = 0; s_cnt[tid] = 0; }
+    if (tid == 0) s_amax = 0.f;
     __syncthreads();
 
     const int k = a.k;
-    // ---- radix select of the k-th largest key (skipped when everything is selected)
-    uint64_t thr = 0;
-    int need_eq = 0;  // how many key == thr blocks (lowest ids) to take
     const bool take_all = nb <= k;
-    if (!take_all) {
-        uint64_t prefix = 0, mask = 0;
-        int krem = k;
-        for (int pass = 0; pass < 8; ++pass) {
-            const int shift = 56 - 8 * pass;
-            hist[tid] = 0;  // K1_THREADS == 256 bins
-            __syncthreads();
-            for (int b = tid; b < nb; b += K1_THREADS) {
-                const uint64_t key = keys[b];
-                if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    const DigT* lo = static_cast<const DigT*>(a.digests) + static_cast<size_t>(u) * 2 * D * ns;
+    const DigT* hi = lo + D * ns;
+
+    if constexpr (MODE == 0) {
+        // ---- fast score: s~_b = sum_c hi_c * P_c + lo_c * N_c  (P_c / N_c = sums of
+        // the non-negative / negative q_g[c]); |s~ - s_ref| <= ~1300 u A_b with
+        // A_b = sum |terms|; eps_b = A_b * 2^-40 covers it with a 6x margin.
+        if (tid < D) {
+            double P = 0.0, N = 0.0;
+            float Pa = 0.f, Na = 0.f;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double qv = qs[tid * G + g];
+                if (qv >= 0.0) { P += qv; Pa += static_cast<float>(qv); }
+                else { N += qv; Na -= static_cast<float>(qv); }
             }
-            __syncthreads();
-            if (tid < 32) {
-                // lane l owns bins 255-8l ... 248-8l (descending)
-                uint32_t cnt[8];
-                uint32_t local = 0;
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    cnt[i] = hist[255 - 8 * tid - i];
-                    local += cnt[i];
-                }
-                uint32_t incl = local;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (tid >= o) incl += y;
-                }
-                const uint32_t excl = incl - local;
-                const bool hit = excl < static_cast<uint32_t>(krem) && incl >= static_cast<uint32_t>(krem);
-                if (hit) {
-                    uint32_t cum = excl;
-                    int digit = 0;
-                    uint32_t above = 0;
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        if (cum + cnt[i] >= static_cast<uint32_t>(krem)) {
-                            digit = 255 - 8 * tid - i;
-                            above = cum;
-                            break;
-                        }
-                        cum += cnt[i];
-                    }
-                    s_prefix = prefix | (static_cast<uint64_t>(digit) << shift);
-                    s_krem = krem - static_cast<int>(above);
-                }
-            }
-            __syncthreads();
-            prefix = s_prefix;
-            krem = s_krem;
-            mask |= 0xFFull << shift;
+            pn[tid] = make_double2(P, N);
+            pna[tid] = make_float2(Pa * 1.0001f, Na * 1.0001f);
         }
-        thr = prefix;
-        need_eq = krem;
+        __syncthreads();
+        if (!take_all || a.scores_out) {
+            // thread -> (block quad j, channel part p): P parts of 128/P channels so
+            // every thread streams digests (memory-level parallelism); the parts
+            // are summed in a fixed order afterwards (order is free: approximate).
+            const int nq = (nb + 3) >> 2;
+            int P = 1;
+            while (P < 4 && nq * P * 2 <= K1_THREADS) P *= 2;
+            const int cper = D / P;
+            // [P][nb] partials overlay keys/cls (P*nq <= K1_THREADS, so P*nb <= max(4*K1_THREADS+12,
+            // nb_stride): sized at launch)
+            double* part_s = reinterpret_cast<double*>(keys);
+            float* part_a = reinterpret_cast<float*>(part_s + P * nb);
+            for (int t = tid; t < nq * P; t += K1_THREADS) {
+                const int j = t % nq, p = t / nq;
+                const int b0 = 4 * j;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+                const int c0 = p * cper;
+#pragma unroll 8
+                for (int c = c0; c < c0 + cper; ++c) {
+                    float l[4], h[4];
+                    if constexpr (sizeof(DigT) == 2) {
+                        const uint2 lv = __ldg(reinterpret_cast<const uint2*>(lo + c * ns + b0));
+                        const uint2 hv = __ldg(reinterpret_cast<const uint2*>(hi + c * ns + b0));
+                        l[0] = __uint_as_float(lv.x << 16); l[1] = __uint_as_float(lv.x & 0xFFFF0000u);
+                        l[2] = __uint_as_float(lv.y << 16); l[3] = __uint_as_float(lv.y & 0xFFFF0000u);
+                        h[0] = __uint_as_float(hv.x << 16); h[1] = __uint_as_float(hv.x & 0xFFFF0000u);
+                        h[2] = __uint_as_float(hv.y << 16); h[3] = __uint_as_float(hv.y & 0xFFFF0000u);
+                    } else {
+                        const float4 lv = __ldg(reinterpret_cast<const float4*>(lo + c * ns + b0));
+                        const float4 hv = __ldg(reinterpret_cast<const float4*>(hi + c * ns + b0));
+                        l[0] = lv.x; l[1] = lv.y; l[2] = lv.z; l[3] = lv.w;
+                        h[0] = hv.x; h[1] = hv.y; h[2] = hv.z; h[3] = hv.w;
+                    }
+                    const double2 pv = pn[c];
+                    const float2 pa = pna[c];
+                    s0 = fma(static_cast<double>(h[0]), pv.x, s0); s0 = fma(static_cast<double>(l[0]), pv.y, s0);
+                    s1 = fma(static_cast<double>(h[1]), pv.x, s1); s1 = fma(static_cast<double>(l[1]), pv.y, s1);
+                    s2 = fma(static_cast<double>(h[2]), pv.x, s2); s2 = fma(static_cast<double>(l[2]), pv.y, s2);
+                    s3 = fma(static_cast<double>(h[3]), pv.x, s3); s3 = fma(static_cast<double>(l[3]), pv.y, s3);
+                    a0 = fmaf(fabsf(h[0]), pa.x, fmaf(fabsf(l[0]), pa.y, a0));
+                    a1 = fmaf(fabsf(h[1]), pa.x, fmaf(fabsf(l[1]), pa.y, a1));
+                    a2 = fmaf(fabsf(h[2]), pa.x, fmaf(fabsf(l[2]), pa.y, a2));
+                    a3 = fmaf(fabsf(h[3]), pa.x, fmaf(fabsf(l[3]), pa.y, a3));
+                }
+                const double sv[4] = {s0, s1, s2, s3};
+                const float av[4] = {a0, a1, a2, a3};
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    if (b0 + i < nb) {
+                        part_s[p * nb + b0 + i] = sv[i];
+                        part_a[p * nb + b0 + i] = av[i];
+                    }
+            }
+            __syncthreads();
+            // fold the parts (fixed order) -> approximate keys; keys overlay part 0
+            float amax = 0.f;
+            double sfold[8];
+            int nmine = 0;
+            for (int b = tid; b < nb; b += K1_THREADS) {
+                double sv = part_s[b];
+                float av = part_a[b];
+                for (int p = 1; p < P; ++p) { sv += part_s[p * nb + b]; av += part_a[p * nb + b]; }
+                if (nmine < 8) sfold[nmine] = sv;
+                ++nmine;
+                amax = fmaxf(amax, av * 1.0001f);
+            }
+            __syncthreads();  // all parts read before keys overwrite them
+            {
+                int i = 0;
+                for (int b = tid; b < nb; b += K1_THREADS, ++i) keys[b] = score_key(sfold[i]);
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+            if ((tid & 31) == 0) atomicMax(reinterpret_cast<int*>(&s_amax), __float_as_int(amax));
+        }
+        if (a.scores_out)  // exact reference-order scores (tests / diagnostics only)
+            for (int b = tid; b < nb; b += K1_THREADS)
+                a.scores_out[u * ns + b] = exact_score_minmax<DigT, G>(lo, hi, ns, b, qs);
+    } else {
+        for (int b = tid; b < nb; b += K1_THREADS) {
+            const double sc = exact_score_f64<G, MODE>(static_cast<const double*>(a.digests) +
+                                                            static_cast<size_t>(u) * (MODE == 1 ? 2 : 1) * D * ns,
+                                                        ns, b, qs);
+            keys[b] = score_key(sc);
+            if (a.scores_out) a.scores_out[u * ns + b] = sc;
+        }
     }
+    __syncthreads();
+
+    // ---- classify every block: IN (certainly top-k), OUT, or Z (decide exactly)
+    uint64_t thr = 0;
+    int need_eq = 0;
+    bool z_exact = false;  // Z members carry exact keys and a radix select among them
+    if (take_all) {
+        for (int b = tid; b < nb; b += K1_THREADS) cls[b] = CLS_IN;
+    } else if constexpr (MODE != 0) {
+        // keys are exact already: plain top-k
+        radix_kth(nb, k, [&](int b) { return keys[b]; }, [](int) { return true; }, S, thr, need_eq);
+        for (int b = tid; b < nb; b += K1_THREADS) cls[b] = CLS_Z;
+        z_exact = true;
+    } else {
+        uint64_t tkey;
+        int dummy;
+        radix_kth(nb, k, [&](int b) { return keys[b]; }, [](int) { return true; }, S, tkey, dummy);
+        const double T = key_to_double(tkey);
+        const double band = 2.0 * static_cast<double>(s_amax) * 0x1p-40;
+        int nin = 0, nz = 0;
+        for (int b = tid; b < nb; b += K1_THREADS) {
+            const double v = key_to_double(keys[b]);
+            const uint8_t c = v > T + band ? CLS_IN : (v < T - band ? CLS_OUT : CLS_Z);
+            cls[b] = c;
+            nin += c == CLS_IN;
+            nz += c == CLS_Z;
+        }
+        if (nin) atomicAdd(&s_cnt[0], nin);
+        if (nz) atomicAdd(&s_cnt[1], nz);
+        __syncthreads();
+        const int need = k - s_cnt[0];
+        if (s_cnt[1] > need) {
+            // genuinely ambiguous boundary: exact reference-order scores for Z
+            for (int b = tid; b < nb; b += K1_THREADS)
+                if (cls[b] == CLS_Z) keys[b] = score_key(exact_score_minmax<DigT, G>(lo, hi, ns, b, qs));
+            __syncthreads();
+            radix_kth(nb, need, [&](int b) { return keys[b]; }, [&](int b) { return cls[b] == CLS_Z; }, S, thr,
+                      need_eq);
+            z_exact = true;
+        }
+    }
+    __syncthreads();
 
     // ---- selection flags in id order: contiguous chunks per thread
     const int chunk = (nb + K1_THREADS - 1) / K1_THREADS;
     const int b_begin = min(nb, tid * chunk), b_end = min(nb, b_begin + chunk);
     int total;
     int eq_rank = 0;
-    if (!take_all) {
+    if (z_exact) {
         int eq_local = 0;
-        for (int b = b_begin; b < b_end; ++b) eq_local += keys[b] == thr;
+        for (int b = b_begin; b < b_end; ++b) eq_local += (cls[b] == CLS_Z && keys[b] == thr);
         eq_rank = block_exclusive_scan(eq_local, warp_tot, &total);
     }
-    // selected count and resident count per chunk
+    auto selected = [&](int b, int& er) {
+        const uint8_t c = cls[b];
+        if (c == CLS_IN) return true;
+        if (c != CLS_Z) return false;
+        if (!z_exact) return true;
+        const uint64_t key = keys[b];
+        if (key > thr) return true;
+        if (key == thr) return er++ < need_eq;
+        return false;
+    };
     const int32_t* table = a.block_table ? a.block_table + static_cast<size_t>(u) * a.nb_stride : nullptr;
     int sel_local = 0, res_local = 0;
     {
         int er = eq_rank;
-        for (int b = b_begin; b < b_end; ++b) {
-            bool sel = take_all;
-            if (!take_all) {
-                const uint64_t key = keys[b];
-                if (key > thr) sel = true;
-                else if (key == thr) { sel = er < need_eq; ++er; }
-            }
-            if (sel) {
+        for (int b = b_begin; b < b_end; ++b)
+            if (selected(b, er)) {
                 ++sel_local;
                 if (table && table[b] >= 0) ++res_local;
             }
-        }
     }
     const int packed = block_exclusive_scan(sel_local | (res_local << 16), warp_tot, &total);
     int sel_pos = packed & 0xFFFF, res_pos = packed >> 16;
@@ -272,13 +444,7 @@ __global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk
         int er = eq_rank;
         const size_t row = static_cast<size_t>(u) * a.k_stride;
         for (int b = b_begin; b < b_end; ++b) {
-            bool sel = take_all;
-            if (!take_all) {
-                const uint64_t key = keys[b];
-                if (key > thr) sel = true;
-                else if (key == thr) { sel = er < need_eq; ++er; }
-            }
-            if (!sel) continue;
+            if (!selected(b, er)) continue;
             const int rows = (b == nb - 1) ? tail : BS;
             if (a.sel_ids) a.sel_ids[row + sel_pos] = b;
             if (a.last_selected) a.last_selected[static_cast<size_t>(u) * a.nb_stride + b] = a.step;
@@ -314,13 +480,14 @@ __global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk
 
 template <typename DigT, int MODE>
 int launch_g(const scout_topk_args& a, cudaStream_t st) {
-    const size_t smem = static_cast<size_t>(D) * a.group * 8 + static_cast<size_t>(a.nb_stride) * 8;
+    // qs | pn | pna | max(keys + cls, part_s[P][nb] + part_a[P][nb]) with P*nb <= max(4*K1_THREADS+12, nbs)
+    const size_t nbs = static_cast<size_t>(a.nb_stride);
+    const size_t pmax = 4 * K1_THREADS + 12;
+    const size_t pnb = nbs > pmax ? nbs : pmax;
+    const size_t tail = nbs * 9 > pnb * 12 ? nbs * 9 : pnb * 12;
+    const size_t smem = static_cast<size_t>(D) * a.group * 8 + static_cast<size_t>(D) * 24 + tail;
     auto go = [&](auto kern) {
-        static size_t configured = 0;  // per instantiation; the attribute call is not free
-        if (smem > 48 * 1024 && smem > configured) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            configured = smem;
-        }
+        if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
         kern<<<a.n_units, K1_THREADS, smem, st>>>(a);
     };
     switch (a.group) {

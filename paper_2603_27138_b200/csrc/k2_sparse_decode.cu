@@ -636,12 +636,7 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
         if (grid < min_grid) grid = min_grid;
         if (grid > GRID_CAP) grid = GRID_CAP;
         auto go = [&](auto kern) {
-            static bool configured = false;  // per instantiation
-            if (!configured) {
-                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(tc::SMEM_BYTES));
-                configured = true;
-            }
+            scout_host::ensure_smem(reinterpret_cast<const void*>(kern), tc::SMEM_BYTES);
             kern<<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(a);
         };
         switch (a.group) {

@@ -126,4 +126,7 @@ __device__ __forceinline__ float fast_exp2(float x) {
 namespace scout_host {
 void set_error(int code, const char* fmt, ...);
 int check_launch(const char* what);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel (keyed by
+// the kernel's address; the call is not free on the launch path).
+void ensure_smem(const void* kernel, size_t bytes);
 }  // namespace scout_host

@@ -41,6 +41,7 @@ def topk_cases(ref):
         (1, 64 * 20, 5, "iid"), (4, 64 * 64, 32, "iid"), (8, 64 * 100 + 17, 64, "iid"),
         (8, 64 * 130, 64, "clustered"), (4, 64 * 40, 8, "tie"), (8, 64 * 33 + 1, 16, "tie"),
         (2, 64 * 7, 64, "iid"), (8, 64 * 1, 3, "iid"), (1, 64 * 24, 7, "tie"), (8, 64 * 520, 128, "iid"),
+        (8, 64 * 96, 20, "perm"), (4, 64 * 64 + 9, 32, "perm"),
     ]
     cases = {}
     for i, (G, nt, k, kind) in enumerate(specs):
@@ -51,6 +52,16 @@ def topk_cases(ref):
             a = rng.integers(-2, 3, size=(D, nbs)).astype(np.float32)
             b = rng.integers(-2, 3, size=(D, nbs)).astype(np.float32)
             lo, hi = np.minimum(a, b), np.maximum(a, b)
+        elif kind == "perm":  # channel permutations of 3 bases, q constant per head: ulp-level near-ties
+            q = np.repeat(rng.standard_normal((G, 1)), D, axis=1).astype(np.float32)
+            base = (rng.standard_normal((3, 2, D)) * 2.0 ** rng.integers(-20, 21, size=(3, 2, D))).astype(np.float32)
+            lo = np.empty((D, nbs), np.float32)
+            hi = np.empty((D, nbs), np.float32)
+            for j in range(nbs):
+                p_ = rng.permutation(D)
+                w = rng.integers(0, 3)
+                a_, b_ = base[w, 0, p_], base[w, 1, p_]
+                lo[:, j], hi[:, j] = np.minimum(a_, b_), np.maximum(a_, b_)
         elif kind == "clustered":
             q = rng.standard_normal((G, D)).astype(np.float32)
             mu = rng.standard_normal((D, nbs)).astype(np.float32) * 0.7

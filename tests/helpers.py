@@ -36,6 +36,19 @@ def make_digests(rng, U, nbs, kind="iid", dtype=np.float32):
     if kind == "tie":
         a = rng.integers(-2, 3, size=(U, D, nbs)).astype(np.float32)
         b = rng.integers(-2, 3, size=(U, D, nbs)).astype(np.float32)
+    elif kind == "perm":
+        # near-ties at the ulp level: every block is a channel permutation of
+        # one of 3 base digests (values spread over 2^+-20), so with q constant
+        # over channels the real sums are equal and only the reference's
+        # sequential rounding orders them
+        base = (rng.standard_normal((U, 3, 2, D)) * 2.0 ** rng.integers(-20, 21, size=(U, 3, 2, D))).astype(np.float32)
+        a = np.empty((U, D, nbs), np.float32)
+        b = np.empty((U, D, nbs), np.float32)
+        for u in range(U):
+            for j in range(nbs):
+                perm = rng.permutation(D)
+                w = rng.integers(0, 3)
+                a[u, :, j], b[u, :, j] = base[u, w, 0, perm], base[u, w, 1, perm]
     else:
         a = rng.standard_normal((U, D, nbs)).astype(np.float32)
         b = rng.standard_normal((U, D, nbs)).astype(np.float32)
@@ -46,4 +59,6 @@ def make_digests(rng, U, nbs, kind="iid", dtype=np.float32):
 def make_queries(rng, U, G, kind="iid"):
     if kind == "tie":
         return rng.integers(-1, 2, size=(U * G, D)).astype(np.float32)
+    if kind == "perm":  # constant over channels (per head) so channel permutations keep the term multiset
+        return np.repeat(rng.standard_normal((U * G, 1)), D, axis=1).astype(np.float32)
     return rng.standard_normal((U * G, D)).astype(np.float32)

@@ -39,7 +39,7 @@ def test_topk_bit_exact_vs_reference_golden(cuda, case):
 
 
 @pytest.mark.parametrize("G", [1, 2, 4, 8])
-@pytest.mark.parametrize("kind", ["iid", "tie"])
+@pytest.mark.parametrize("kind", ["iid", "tie", "perm"])
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 def test_topk_split_vs_oracle(cuda, G, kind, dtype):
     rng = np.random.default_rng(hash((G, kind, str(dtype))) % 2**32)
