@@ -171,8 +171,8 @@ class Workload:
             dst = base + torch.arange(U, device=dev)[:, None] * (cap + head) + cap + torch.arange(
                 cpu_per_unit, device=dev)[None]
             src = (cpu_ids * 2654435761 + li * 97 + torch.arange(U, device=dev)[:, None] * 31) % host_blocks
-            layers.append(LayerState(dig, table, src.reshape(-1).to(torch.int64).contiguous(),
-                                     dst.reshape(-1).to(torch.int32).contiguous()))
+            layers.append(LayerState(dig, table, src.reshape(-1).to(torch.int64).cpu().contiguous(),
+                                     dst.reshape(-1).to(torch.int32).cpu().contiguous()))
         self.layer_states = layers
         self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=pool,
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),

@@ -190,6 +190,11 @@ int scout_merge_partials(const float* a_o, const float* a_ml, const float* b_o, 
  * event; the kernel streams over PCIe / C2C with 16-byte loads.            */
 int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host_blocks,
                         const int64_t* src_index, const int32_t* dst_slots, int n, void* stream);
+/* Same move on the copy engines (one cudaMemcpyBatchAsync, no SM time):
+ * src_index / dst_slots are HOST arrays here. Preferred next to a persistent
+ * K2 that needs every SM; `stream` must not be the legacy default stream. */
+int scout_recall_copy(void* kv_pool, int kv_dtype, const void* host_blocks, const int64_t* src_index,
+                      const int32_t* dst_slots, int n, void* stream);
 
 /* ------------------------------------------------------------- engine --
  * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,
@@ -205,7 +210,8 @@ int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host_blocks,
 typedef struct scout_layer_desc {
     const void* digests;         /* [U][2][128][nb_stride] in kv dtype */
     const int32_t* block_table;  /* [U][nb_stride] slot or -1 (planning view) */
-    const int64_t* recall_src;   /* optional recall plan: host block indices */
+    const int64_t* recall_src;   /* optional recall plan (HOST arrays, copied at create):
+                                    host block indices ... */
     const int32_t* recall_dst;   /* ... and destination pool slots */
     int recall_n;
 } scout_layer_desc;
@@ -220,6 +226,7 @@ typedef struct scout_engine_config {
     int max_ctas;              /* K2 grid (0 = one CTA per SM) */
     int host_staging;          /* 1: allocate device staging for decode_step_host */
     int chunk_layers;          /* layers per H2D/D2H chunk of the host path (0 = 8) */
+    int recall_mode;           /* 0: copy engines (scout_recall_copy), 1: SM gather kernel (K4) */
 } scout_engine_config;
 
 typedef struct scout_engine scout_engine;

@@ -27,7 +27,7 @@ EXPORTED = (
     "scout_last_error", "scout_version", "scout_slot_bytes",
     "scout_kv_write_tokens", "scout_kv_read_tokens", "scout_digest_build",
     "scout_score_topk_split", "scout_sparse_decode_workspace_bytes",
-    "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather",
+    "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather", "scout_recall_copy",
     "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
     "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k1_outputs",
 )
@@ -67,7 +67,7 @@ class EngineConfig(C.Structure):
         ("layers", C.c_int), ("batch", C.c_int), ("hq", C.c_int), ("hkv", C.c_int), ("k", C.c_int),
         ("nb_stride", C.c_int), ("kv_dtype", C.c_int), ("scale", C.c_float), ("recall_interval", C.c_int),
         ("kv_pool", _vp), ("n_tokens", _vp), ("host_tier", _vp), ("max_ctas", C.c_int),
-        ("host_staging", C.c_int), ("chunk_layers", C.c_int),
+        ("host_staging", C.c_int), ("chunk_layers", C.c_int), ("recall_mode", C.c_int),
     ]
 
 
@@ -100,6 +100,7 @@ def lib() -> C.CDLL:
         L.scout_sparse_decode.argtypes = [C.POINTER(DecodeArgs), _vp]
         L.scout_merge_partials.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_recall_gather.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]
+        L.scout_recall_copy.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_engine_create.argtypes = [C.POINTER(EngineConfig), C.POINTER(LayerDesc), C.POINTER(_vp)]
         L.scout_engine_destroy.argtypes = [_vp]
         L.scout_engine_decode_step.argtypes = [_vp, C.c_int] + [_vp] * 6 + [_vp]

@@ -51,7 +51,11 @@ struct scout_engine {
     Buf sel_ids, n_sel, res_slots, res_ids, n_res, cpu_ids, n_cpu, res_tok, cpu_tok;
     Buf ws;
     size_t ws_bytes = 0;
-    // recall plumbing
+    // recall plumbing (plans copied at create: host arrays for the copy
+    // engines, device arrays for the SM gather kernel)
+    std::vector<std::vector<int64_t>> rc_src;
+    std::vector<std::vector<int32_t>> rc_dst;
+    std::vector<Buf> rc_dev;
     cudaStream_t side = nullptr;
     std::vector<cudaEvent_t> recall_ev;
     std::vector<char> recall_pending;
@@ -165,9 +169,16 @@ struct scout_engine {
         if ((step + layer) % cfg.recall_interval != 0) return SCOUT_OK;
         CU(cudaEventRecord(ev_main, st));  // issued after the layer's attention
         CU(cudaStreamWaitEvent(side, ev_main, 0));
-        ++launches;
-        const int rc = scout_recall_gather(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, L.recall_src, L.recall_dst,
-                                           L.recall_n, side);
+        int rc;
+        if (cfg.recall_mode == 1) {
+            ++launches;
+            const int64_t* src = static_cast<const int64_t*>(rc_dev[layer].p);
+            const int32_t* dst = reinterpret_cast<const int32_t*>(src + L.recall_n);
+            rc = scout_recall_gather(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, src, dst, L.recall_n, side);
+        } else {
+            rc = scout_recall_copy(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, rc_src[layer].data(),
+                                   rc_dst[layer].data(), L.recall_n, side);
+        }
         if (rc != SCOUT_OK) return rc;
         CU(cudaEventRecord(recall_ev[layer], side));
         recall_pending[layer] = 1;
@@ -238,6 +249,26 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     e->recall_ev.resize(c.layers);
     for (auto& ev : e->recall_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     e->recall_pending.assign(c.layers, 0);
+    e->rc_src.resize(c.layers);
+    e->rc_dst.resize(c.layers);
+    e->rc_dev = std::vector<Buf>(c.layers);
+    for (int l = 0; l < c.layers; ++l) {
+        const scout_layer_desc& d = layers[l];
+        if (d.recall_n <= 0 || !d.recall_src || !d.recall_dst) continue;
+        e->rc_src[l].assign(d.recall_src, d.recall_src + d.recall_n);
+        e->rc_dst[l].assign(d.recall_dst, d.recall_dst + d.recall_n);
+        if (c.recall_mode == 1) {
+            const size_t bytes = static_cast<size_t>(d.recall_n) * (8 + 4);
+            if (e->rc_dev[l].alloc(bytes) != 0 ||
+                cudaMemcpy(e->rc_dev[l].p, d.recall_src, d.recall_n * 8, cudaMemcpyHostToDevice) != cudaSuccess ||
+                cudaMemcpy(static_cast<int64_t*>(e->rc_dev[l].p) + d.recall_n, d.recall_dst, d.recall_n * 4,
+                           cudaMemcpyHostToDevice) != cudaSuccess) {
+                delete e;
+                set_error(SCOUT_ERR_CUDA, "scout_engine_create: recall plan upload failed");
+                return SCOUT_ERR_CUDA;
+            }
+        }
+    }
     const int nch = (c.layers + e->cfg.chunk_layers - 1) / e->cfg.chunk_layers;
     e->chunk_ev.resize(nch);
     e->done_ev.resize(nch);

@@ -13,6 +13,8 @@
 
 #include <math_constants.h>
 
+#include <vector>
+
 using namespace scout_dev;
 
 namespace {
@@ -103,4 +105,43 @@ extern "C" int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host
         static_cast<uint8_t*>(kv_pool), static_cast<const uint8_t*>(host_blocks), src_index, dst_slots, n,
         slot_bytes(kv_dtype));
     return check_launch("scout_recall_gather");
+}
+
+extern "C" int scout_recall_copy(void* kv_pool, int kv_dtype, const void* host_blocks, const int64_t* src_index,
+                                 const int32_t* dst_slots, int n, void* stream) {
+    using namespace scout_host;
+    if (kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32) {
+        set_error(SCOUT_ERR_UNSUPPORTED, "scout_recall_copy: kv dtype %d unsupported", kv_dtype);
+        return SCOUT_ERR_UNSUPPORTED;
+    }
+    if (n < 0 || (n > 0 && (!kv_pool || !host_blocks || !src_index || !dst_slots)) || stream == nullptr) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_recall_copy: bad arguments (a non-default stream is required)");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (n == 0) return SCOUT_OK;
+    const size_t sb = slot_bytes(kv_dtype);
+    thread_local std::vector<void*> dsts, srcs;
+    thread_local std::vector<size_t> sizes;
+    dsts.resize(n);
+    srcs.resize(n);
+    sizes.assign(n, sb);
+    for (int i = 0; i < n; ++i) {
+        dsts[i] = static_cast<uint8_t*>(kv_pool) + static_cast<size_t>(dst_slots[i]) * sb;
+        srcs[i] = const_cast<uint8_t*>(static_cast<const uint8_t*>(host_blocks)) + static_cast<size_t>(src_index[i]) * sb;
+    }
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail = 0;
+    const cudaError_t e = cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), static_cast<size_t>(n), &attr,
+                                               &attr_idx, 1, &fail, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        for (int i = 0; i < n; ++i)  // driver without batch support: per-block copies
+            if (cudaMemcpyAsync(dsts[i], srcs[i], sb, cudaMemcpyHostToDevice, static_cast<cudaStream_t>(stream)) !=
+                cudaSuccess) {
+                set_error(SCOUT_ERR_CUDA, "scout_recall_copy: %s", cudaGetErrorString(cudaGetLastError()));
+                return SCOUT_ERR_CUDA;
+            }
+    }
+    return SCOUT_OK;
 }

@@ -21,8 +21,8 @@ from . import ops
 class LayerState:
     digests: torch.Tensor                     # [U][2][128][nbs] kv dtype
     table: torch.Tensor                       # [U][nbs] int32 slot or -1 (planning view)
-    recall_src: torch.Tensor | None = None    # [n] int64 host block index
-    recall_dst: torch.Tensor | None = None    # [n] int32 pool slot
+    recall_src: torch.Tensor | None = None    # [n] int64 host block index (CPU tensor)
+    recall_dst: torch.Tensor | None = None    # [n] int32 pool slot (CPU tensor)
 
 
 def _p(t):
@@ -31,7 +31,8 @@ def _p(t):
 
 class DecodeEngine:
     def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
-                 recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8):
+                 recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
+                 recall_mode=0):
         self.L, self.batch, self.hq, self.hkv, self.G, self.k = layers, batch, hq, hkv, hq // hkv, k
         self.U = batch * hkv
         self.layer_states = layer_states  # keep tensors alive
@@ -45,10 +46,12 @@ class DecodeEngine:
         cfg.recall_interval = int(recall_interval)
         cfg.kv_pool, cfg.n_tokens, cfg.host_tier = _p(pool), _p(n_tokens), _p(host_tier)
         cfg.max_ctas, cfg.host_staging, cfg.chunk_layers = int(max_ctas), int(host_staging), int(chunk_layers)
+        cfg.recall_mode = int(recall_mode)
         descs = (A.LayerDesc * layers)()
         for i, st in enumerate(layer_states):
             descs[i].digests, descs[i].block_table = _p(st.digests), _p(st.table)
             if st.recall_src is not None:
+                assert st.recall_src.device.type == "cpu" and st.recall_dst.device.type == "cpu"
                 descs[i].recall_src, descs[i].recall_dst = _p(st.recall_src), _p(st.recall_dst)
                 descs[i].recall_n = int(st.recall_dst.numel())
         h = C.c_void_p()

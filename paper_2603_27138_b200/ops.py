@@ -161,3 +161,11 @@ def recall_gather(pool, kv_dtype, host_blocks, src_index, dst_slots):
     dst = _i32(dst_slots, dev)
     A.check(A.lib().scout_recall_gather(_p(pool), dtype_code(kv_dtype), _p(host_blocks), _p(src), _p(dst),
                                         int(dst.numel()), _stream()))
+
+
+def recall_copy(pool, kv_dtype, host_blocks, src_index, dst_slots):
+    """K4 on the copy engines. src_index / dst_slots: host (CPU) arrays."""
+    src = torch.as_tensor(src_index, dtype=torch.int64).contiguous()
+    dst = torch.as_tensor(dst_slots, dtype=torch.int32).contiguous()
+    A.check(A.lib().scout_recall_copy(_p(pool), dtype_code(kv_dtype), _p(host_blocks), _p(src), _p(dst),
+                                      int(dst.numel()), _stream()))

@@ -82,3 +82,18 @@ def test_recall_gather_copies_block_images(cuda, dtype):
     for s, d in ((8, 5), (0, 1), (3, 2)):
         assert torch.equal(p[d * sb:(d + 1) * sb], host[s * sb:(s + 1) * sb])
     assert torch.count_nonzero(p[:sb]) == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_recall_copy_engine_path(cuda, dtype):
+    sb = ops.slot_bytes(dtype)
+    host = torch.randint(0, 256, (9 * sb,), dtype=torch.uint8).pin_memory()
+    pool = torch.zeros(6 * sb, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ops.recall_copy(pool, dtype, host, [8, 0, 3], [5, 1, 2])
+    s.synchronize()
+    p = pool.cpu()
+    for src, d in ((8, 5), (0, 1), (3, 2)):
+        assert torch.equal(p[d * sb:(d + 1) * sb], host[src * sb:(src + 1) * sb])
+    assert torch.count_nonzero(p[:sb]) == 0
