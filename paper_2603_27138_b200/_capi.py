@@ -7,9 +7,10 @@ it is missing — there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libscout_b200.so"
+LIB_PATH = Path(os.environ.get("SCOUT_B200_LIB", Path(__file__).resolve().parent / "libscout_b200.so"))
 
 SCOUT_OK = 0
 SCOUT_ERR_INVALID_ARGUMENT = 1

@@ -45,25 +45,45 @@ __host__ __device__ inline size_t ctr_bytes(int n_units) { return ((static_cast<
 
 // =========================================================== bf16 kernel ==
 namespace tc {
-constexpr int NC = 4;                       // consumer warps
-constexpr int NTHREADS = (NC + 1) * 32;     // + 1 producer warp
-constexpr int NST = 12;                     // ring stages (one half block each)
+#ifndef SCOUT_K2_NC
+#define SCOUT_K2_NC 8
+#endif
+#ifndef SCOUT_K2_NST
+#define SCOUT_K2_NST 13
+#endif
+constexpr int NC = SCOUT_K2_NC;             // consumer warps (2 per scheduler)
+constexpr int NCT = NC * 32;                // consumer threads
+constexpr int NTHREADS = NCT + 32;          // + 1 producer warp
+constexpr int NST = SCOUT_K2_NST;           // ring stages (one 32-token half block each)
 constexpr int STAGE_BYTES = 16384;          // 8 KiB K half + 8 KiB V half
-constexpr int MAXSEG = 256;
-constexpr int CB_ROW = D + 4;               // combine-buffer row stride (bank-conflict pad)
-constexpr int CB_WARP = 8 * CB_ROW + 16;    // floats per warp: O[8][CB_ROW], m[8], l[8]
-constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES + static_cast<size_t>(NC) * CB_WARP * 4;
+constexpr int MAXSEG = 128;
+constexpr int MAXB = 512;                   // blocks per CTA range (staged in smem)
+constexpr int CB_ROW = D + 4;               // combine rows (bank-conflict pad)
+#ifndef SCOUT_K2_SEPCB
+#define SCOUT_K2_SEPCB 0
+#endif
+constexpr int CBW = 8 * CB_ROW + 16;        // floats of one warp's combine area
+constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES + (SCOUT_K2_SEPCB ? NC * CBW * 4 : 0);
+static_assert(8 * CB_ROW * 4 + 64 <= STAGE_BYTES, "combine area must fit in a stage");
+static_assert(NST > NC, "a warp's held stage must never be needed inside its segment");
+static_assert(NCT == 256, "combine mapping: 8 heads x 32 threads x 4 channels");
 
 struct Seg {
-    int unit, j0, j1, nseg, cfirst;
+    int unit, j0, j1, nseg, cfirst, f0, q0, q1;  // f0: first block in the CTA list; [q0,q1): halves
 };
 
 struct Smem {
     uint64_t full[NST];
     uint64_t empty[NST];
     Seg segs[MAXSEG];
+    int blk_slot[MAXB];        // the CTA's resident blocks in stream order: pool slot
+    int16_t blk_rows[MAXB];    // valid rows (64, or the open block's fill)
+    int16_t blk_h0[MAXB];      // first half index of the block (CTA-local)
+    int16_t half_blk[2 * MAXB];  // half -> block
+    int warp_stage[NC];        // stage holding a warp's combine area, -1: warp had no half
     int nsegs;
-    int scan_tot[8];
+    int nhalf;
+    int scan_tot[NTHREADS / 32];
     int last_flag;
     long long run_total;
 };
@@ -75,13 +95,15 @@ __device__ __forceinline__ int unit_nb(const scout_decode_args& a, int u, int* t
     return nb;
 }
 
-// merge n partial slots (+ optional cpu partial) of unit u into the outputs.
-// Executed by the NC*32 consumer threads; thread i -> head i/16, 8 channels.
-template <int G>
+// Merge n partial slots (+ the optional CPU partial) of unit u into the
+// outputs (merge / finalize, attention.hpp:100-122; both empty -> zeros,
+// engine.hpp:273). NT threads: thread i -> head i/(NT/8), 1024/NT channels.
+template <int G, int NT>
 __device__ void finalize_unit(const scout_decode_args& a, int u, const float* parts, int first_slot, int nslots,
                               int ctid) {
-    const int h = ctid >> 4;
-    const int d0 = (ctid & 15) * 8;
+    constexpr int TPH = NT / 8, CPT = D / TPH;  // threads per head, channels per thread
+    const int h = ctid / TPH;
+    const int d0 = (ctid % TPH) * CPT;
     if (h >= G) return;
     const size_t head = static_cast<size_t>(u) * G + h;
     float M = -CUDART_INF_F;
@@ -95,7 +117,9 @@ __device__ void finalize_unit(const scout_decode_args& a, int u, const float* pa
         cl = a.cpu_ml[head * 2 + 1];
         if (cl > 0.f) M = fmaxf(M, cm);
     }
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    float acc[CPT];
+#pragma unroll
+    for (int e = 0; e < CPT; ++e) acc[e] = 0.f;
     float L = 0.f;
     if (M != -CUDART_INF_F) {
         for (int i = 0; i < nslots; ++i) {
@@ -104,24 +128,26 @@ __device__ void finalize_unit(const scout_decode_args& a, int u, const float* pa
             if (!(l > 0.f)) continue;
             const float w = l * exp2f(__ldcg(p + D) - M);
             L += w;
-            const float4 x0 = __ldcg(reinterpret_cast<const float4*>(p + d0));
-            const float4 x1 = __ldcg(reinterpret_cast<const float4*>(p + d0 + 4));
-            acc[0] += w * x0.x; acc[1] += w * x0.y; acc[2] += w * x0.z; acc[3] += w * x0.w;
-            acc[4] += w * x1.x; acc[5] += w * x1.y; acc[6] += w * x1.z; acc[7] += w * x1.w;
+#pragma unroll
+            for (int e = 0; e < CPT; e += 4) {
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(p + d0 + e));
+                acc[e] += w * x.x; acc[e + 1] += w * x.y; acc[e + 2] += w * x.z; acc[e + 3] += w * x.w;
+            }
         }
         if (cl > 0.f) {
             const float w = cl * exp2f(cm - M);
             L += w;
             const float* co = a.cpu_o + head * D + d0;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] += w * co[e];
+            for (int e = 0; e < CPT; ++e) acc[e] += w * co[e];
         }
     }
     float* o = a.o + head * D + d0;
     const float inv = L > 0.f ? 1.f / L : 0.f;
-    *reinterpret_cast<float4*>(o) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    *reinterpret_cast<float4*>(o + 4) = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
-    if ((ctid & 15) == 0) {
+#pragma unroll
+    for (int e = 0; e < CPT; e += 4)
+        *reinterpret_cast<float4*>(o + e) = make_float4(acc[e] * inv, acc[e + 1] * inv, acc[e + 2] * inv, acc[e + 3] * inv);
+    if ((ctid % TPH) == 0) {
         a.ml[head * 2] = L > 0.f ? M * LN2 : -CUDART_INF_F;
         a.ml[head * 2 + 1] = L;
     }
@@ -132,7 +158,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
     extern __shared__ __align__(1024) uint8_t dsmem[];
     __shared__ Smem sm;
     uint8_t* stages = dsmem;
-    float* cbuf = reinterpret_cast<float*>(dsmem + static_cast<size_t>(NST) * STAGE_BYTES);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nunits = a.n_units;
@@ -195,7 +220,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
                 const int idx = atomicAdd(&sm.nsegs, 1);
                 if (idx < MAXSEG)
                     sm.segs[idx] = Seg{u, static_cast<int>(s0 - pre), static_cast<int>(s1 - pre),
-                                       static_cast<int>(cl - cf + 1), static_cast<int>(cf)};
+                                       static_cast<int>(cl - cf + 1), static_cast<int>(cf), 0, 0, 0};
             }
         }
         __syncthreads();
@@ -206,8 +231,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
         }
         __syncthreads();
     }
-    // segments were appended in arbitrary order within a chunk; sort by unit
-    // (a CTA range is contiguous, so unit order == stream order).
+    // sort segments by unit (a CTA range is contiguous: unit order == stream order)
     const int nsegs = min(sm.nsegs, MAXSEG);
     if (tid == 0) {
         for (int i = 1; i < nsegs; ++i) {
@@ -216,36 +240,79 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
             while (j >= 0 && sm.segs[j].unit > s.unit) { sm.segs[j + 1] = sm.segs[j]; --j; }
             sm.segs[j + 1] = s;
         }
+        int f = 0;
+        for (int i = 0; i < nsegs; ++i) { sm.segs[i].f0 = f; f += sm.segs[i].j1 - sm.segs[i].j0; }
     }
     __syncthreads();
+    // stage the block list (slot, rows); producer and consumers walk it from smem
+    const int nblk = min(static_cast<int>(hi - lo), MAXB);
+    for (int f = tid; f < nblk; f += NTHREADS) {
+        int si = 0;
+        while (si + 1 < nsegs && sm.segs[si + 1].f0 <= f) ++si;
+        const Seg sg = sm.segs[si];
+        const size_t idx = static_cast<size_t>(sg.unit) * ks + sg.j0 + (f - sg.f0);
+        int tail;
+        const int nb = unit_nb(a, sg.unit, &tail);
+        sm.blk_slot[f] = a.res_slots[idx];
+        sm.blk_rows[f] = static_cast<int16_t>((a.res_ids[idx] == nb - 1) ? tail : BS);
+    }
+    __syncthreads();
+    // half-block table: prefix of halves per block (warp 0), then half -> block
+    if (warp == 0) {
+        constexpr int PER = MAXB / 32;
+        int cnt[PER];
+        int loc = 0;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int f = lane * PER + i;
+            cnt[i] = f < nblk ? (sm.blk_rows[f] > HALF_ROWS ? 2 : 1) : 0;
+            loc += cnt[i];
+        }
+        int x = loc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        int pre = x - loc;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) {
+            const int f = lane * PER + i;
+            if (f < nblk) {
+                sm.blk_h0[f] = static_cast<int16_t>(pre);
+                sm.half_blk[pre] = static_cast<int16_t>(f);
+                if (cnt[i] == 2) sm.half_blk[pre + 1] = static_cast<int16_t>(f);
+            }
+            pre += cnt[i];
+        }
+        if (lane == 31) sm.nhalf = x;
+    }
+    __syncthreads();
+    if (tid < nsegs) {
+        Seg& sg = sm.segs[tid];
+        const int fe = sg.f0 + (sg.j1 - sg.j0);
+        sg.q0 = sm.blk_h0[sg.f0];
+        sg.q1 = fe < nblk ? sm.blk_h0[fe] : sm.nhalf;
+    }
+    __syncthreads();
+    const int nhalf = sm.nhalf;
 
     if (warp == NC) {
         // ================================================== producer warp
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
-            int q = 0;
-            for (int si = 0; si < nsegs; ++si) {
-                const Seg sg = sm.segs[si];
-                int tail;
-                const int nb = unit_nb(a, sg.unit, &tail);
-                for (int j = sg.j0; j < sg.j1; ++j) {
-                    const size_t slot = static_cast<size_t>(a.res_slots[static_cast<size_t>(sg.unit) * ks + j]);
-                    const int id = a.res_ids[static_cast<size_t>(sg.unit) * ks + j];
-                    const int rows = (id == nb - 1) ? tail : BS;
-                    const uint8_t* kb = pool + slot * BF16_SLOT_BYTES;
-                    for (int h = 0; h * HALF_ROWS < rows; ++h) {
-                        const int s = q % NST;
-                        if (q >= NST) mbar_wait(&sm.empty[s], ((q / NST) - 1) & 1);
-                        mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
-                        bulk_g2s_evict_first(stages + s * STAGE_BYTES, kb + h * HALF_BYTES_BF16, HALF_BYTES_BF16,
-                                             &sm.full[s], pol);
-                        bulk_g2s_evict_first(stages + s * STAGE_BYTES + HALF_BYTES_BF16,
-                                             kb + BF16_TILE_BYTES + h * HALF_BYTES_BF16, HALF_BYTES_BF16, &sm.full[s],
-                                             pol);
-                        ++q;
-                    }
-                }
+            for (int q = 0; q < nhalf; ++q) {
+                const int f = sm.half_blk[q];
+                const int h = q - sm.blk_h0[f];
+                const uint8_t* kb = pool + static_cast<size_t>(sm.blk_slot[f]) * BF16_SLOT_BYTES;
+                const int s = q % NST;
+                if (q >= NST) mbar_wait(&sm.empty[s], ((q / NST) - 1) & 1);
+                mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
+                bulk_g2s_evict_first(stages + s * STAGE_BYTES, kb + h * HALF_BYTES_BF16, HALF_BYTES_BF16,
+                                     &sm.full[s], pol);
+                bulk_g2s_evict_first(stages + s * STAGE_BYTES + HALF_BYTES_BF16,
+                                     kb + BF16_TILE_BYTES + h * HALF_BYTES_BF16, HALF_BYTES_BF16, &sm.full[s], pol);
             }
         }
         return;
@@ -254,14 +321,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
     // ====================================================== consumer warps
     const int g = lane >> 2, t = lane & 3;
     const float sl2 = a.scale * LOG2E;
-    const int ctid = tid;  // 0 .. NC*32-1
-    float* mycb = cbuf + warp * CB_WARP;
-    int q = 0;
+    const int ctid = tid;  // 0 .. NCT-1
     for (int si = 0; si < nsegs; ++si) {
         const Seg sg = sm.segs[si];
         const int u = sg.unit;
-        int tail;
-        const int nb = unit_nb(a, u, &tail);
         // Q^T fragments (hi/lo split), heads >= G are zero
         uint32_t bh[8][2], bl[8][2];
         {
@@ -286,134 +349,164 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
 #pragma unroll
         for (int i = 0; i < 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
 
-        for (int j = sg.j0; j < sg.j1; ++j) {
-            const int id = a.res_ids[static_cast<size_t>(u) * ks + j];
-            const int rows = (id == nb - 1) ? tail : BS;
-            for (int h = 0; h * HALF_ROWS < rows; ++h, ++q) {
-                if ((q % NC) != warp) continue;
-                const int s = q % NST;
-                const int valid = min(HALF_ROWS, rows - h * HALF_ROWS);
-                mbar_wait(&sm.full[s], (q / NST) & 1);
-                const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES);
-                const uint32_t vbase = kbase + HALF_BYTES_BF16;
-                if (valid < HALF_ROWS) {
-                    // rows past the open block's fill hold stale bytes: P is 0
-                    // there, but 0 * NaN would poison O, so zero those V rows.
-                    for (int i = lane; i < (HALF_ROWS - valid) * 16; i += 32) {
-                        const int row = valid + (i >> 4), chunk = i & 15;
-                        const uint32_t addr = vbase + (chunk >> 3) * 4096 + row * 128 + ((chunk & 7) << 4);
-                        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0) : "memory");
-                    }
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    __syncwarp();
-                }
-                // ---- S^T = K . Q^T
-                float sh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, slo[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
-#pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
-                    const int slab = kk >> 2, cb = (kk & 3) * 2;
-#pragma unroll
-                    for (int mt = 0; mt < 2; ++mt) {
-                        const int row = 16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8;
-                        const int chunk = cb + (lane >> 4);
-                        const uint32_t addr = kbase + slab * 4096 + row * 128 + ((chunk ^ (row & 7)) << 4);
-                        uint32_t a0, a1, a2, a3;
-                        ldsm_x4(addr, a0, a1, a2, a3);
-                        mma_bf16(sh[mt], a0, a1, a2, a3, bh[kk][0], bh[kk][1]);
-                        mma_bf16(slo[mt], a0, a1, a2, a3, bl[kk][0], bl[kk][1]);
-                    }
-                }
-                // ---- online softmax (columns = heads 2t, 2t+1; rows = tokens)
-                float sv[2][4];
-                float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const int r0 = 16 * mt + g, r1 = r0 + 8;
-                    sv[mt][0] = r0 < valid ? (sh[mt][0] + slo[mt][0]) * sl2 : -CUDART_INF_F;
-                    sv[mt][1] = r0 < valid ? (sh[mt][1] + slo[mt][1]) * sl2 : -CUDART_INF_F;
-                    sv[mt][2] = r1 < valid ? (sh[mt][2] + slo[mt][2]) * sl2 : -CUDART_INF_F;
-                    sv[mt][3] = r1 < valid ? (sh[mt][3] + slo[mt][3]) * sl2 : -CUDART_INF_F;
-                    mx0 = fmaxf(mx0, fmaxf(sv[mt][0], sv[mt][2]));
-                    mx1 = fmaxf(mx1, fmaxf(sv[mt][1], sv[mt][3]));
-                }
-#pragma unroll
-                for (int o = 4; o < 32; o <<= 1) {
-                    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-                    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-                }
-                const float mn0 = fmaxf(m2[0], mx0), mn1 = fmaxf(m2[1], mx1);
-                const float al0 = fast_exp2(m2[0] - mn0), al1 = fast_exp2(m2[1] - mn1);
-                m2[0] = mn0;
-                m2[1] = mn1;
-                float ps0 = 0.f, ps1 = 0.f;
-                uint32_t pb[2][2];
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const float p0 = fast_exp2(sv[mt][0] - mn0), p1 = fast_exp2(sv[mt][1] - mn1);
-                    const float p2 = fast_exp2(sv[mt][2] - mn0), p3 = fast_exp2(sv[mt][3] - mn1);
-                    ps0 += p0 + p2;
-                    ps1 += p1 + p3;
-                    pb[mt][0] = movmatrix_t(pack_bf16(p0, p1));
-                    pb[mt][1] = movmatrix_t(pack_bf16(p2, p3));
-                }
-                lp[0] = lp[0] * al0 + ps0;
-                lp[1] = lp[1] * al1 + ps1;
-#pragma unroll
-                for (int md = 0; md < 8; ++md) {
-                    oacc[md][0] *= al0; oacc[md][1] *= al1; oacc[md][2] *= al0; oacc[md][3] *= al1;
-                }
-                // ---- O^T += V^T . P^T
-#pragma unroll
-                for (int md = 0; md < 8; ++md) {
-#pragma unroll
-                    for (int kk = 0; kk < 2; ++kk) {
-                        const int row = 16 * kk + (lane & 7) + ((lane >> 4) & 1) * 8;
-                        const int cg = 2 * md + ((lane >> 3) & 1);
-                        const uint32_t addr = vbase + (cg >> 3) * 4096 + row * 128 + (((cg & 7) ^ (row & 7)) << 4);
-                        uint32_t a0, a1, a2, a3;
-                        ldsm_x4_t(addr, a0, a1, a2, a3);
-                        mma_bf16(oacc[md], a0, a1, a2, a3, pb[kk][0], pb[kk][1]);
-                    }
+        int held = -1;  // stage kept as this warp's combine area
+        int q = sg.q0 + ((warp - sg.q0) % NC + NC) % NC;
+        for (; q < sg.q1; q += NC) {
+            if (held >= 0 && !SCOUT_K2_SEPCB) {  // previous half fully consumed: hand its stage back
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[held]);
+            }
+            const int f = sm.half_blk[q];
+            const int valid = min(HALF_ROWS, sm.blk_rows[f] - (q - sm.blk_h0[f]) * HALF_ROWS);
+            const int s = q % NST;
+            held = s;
+            // Successive fills of a stage go to different warps, so this warp may
+            // arrive here while fill f-1 of the stage is still in flight; the
+            // full-barrier parity would then alias (it only tells phase parity).
+            // Observing fill f-1's release on `empty` first makes it exact.
+            if (q >= NST) mbar_wait(&sm.empty[s], ((q / NST) - 1) & 1);
+            mbar_wait(&sm.full[s], (q / NST) & 1);
+            __syncwarp();  // lanes may leave the try_wait loop apart: reconverge before .aligned ops
+            const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES);
+            const uint32_t vbase = kbase + HALF_BYTES_BF16;
+            if (valid < HALF_ROWS) {
+                // rows past the open block's fill hold stale bytes: P is 0
+                // there, but 0 * NaN would poison O, so zero those V rows.
+                for (int i = lane; i < (HALF_ROWS - valid) * 16; i += 32) {
+                    const int row = valid + (i >> 4), chunk = i & 15;
+                    const uint32_t addr = vbase + (chunk >> 3) * 4096 + row * 128 + ((chunk & 7) << 4);
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0) : "memory");
                 }
                 __syncwarp();
+            }
+            // ---- S^T = K . Q^T (hi and lo halves of q accumulate separately)
+            float sh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, slo[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+            for (int kk = 0; kk < 8; ++kk) {
+                const int slab = kk >> 2, cb = (kk & 3) * 2;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int row = 16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8;
+                    const int chunk = cb + (lane >> 4);
+                    const uint32_t addr = kbase + slab * 4096 + row * 128 + ((chunk ^ (row & 7)) << 4);
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4(addr, a0, a1, a2, a3);
+                    mma_bf16(sh[mt], a0, a1, a2, a3, bh[kk][0], bh[kk][1]);
+                    mma_bf16(slo[mt], a0, a1, a2, a3, bl[kk][0], bl[kk][1]);
+                }
+            }
+            // ---- online softmax (columns = heads 2t, 2t+1; rows = tokens)
+            float sv[2][4];
+            float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int r0 = 16 * mt + g, r1 = r0 + 8;
+                sv[mt][0] = r0 < valid ? (sh[mt][0] + slo[mt][0]) * sl2 : -CUDART_INF_F;
+                sv[mt][1] = r0 < valid ? (sh[mt][1] + slo[mt][1]) * sl2 : -CUDART_INF_F;
+                sv[mt][2] = r1 < valid ? (sh[mt][2] + slo[mt][2]) * sl2 : -CUDART_INF_F;
+                sv[mt][3] = r1 < valid ? (sh[mt][3] + slo[mt][3]) * sl2 : -CUDART_INF_F;
+                mx0 = fmaxf(mx0, fmaxf(sv[mt][0], sv[mt][2]));
+                mx1 = fmaxf(mx1, fmaxf(sv[mt][1], sv[mt][3]));
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+            }
+            const float mn0 = fmaxf(m2[0], mx0), mn1 = fmaxf(m2[1], mx1);
+            const float al0 = fast_exp2(m2[0] - mn0), al1 = fast_exp2(m2[1] - mn1);
+            m2[0] = mn0;
+            m2[1] = mn1;
+            float ps0 = 0.f, ps1 = 0.f;
+            uint32_t pb[2][2];
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const float p0 = fast_exp2(sv[mt][0] - mn0), p1 = fast_exp2(sv[mt][1] - mn1);
+                const float p2 = fast_exp2(sv[mt][2] - mn0), p3 = fast_exp2(sv[mt][3] - mn1);
+                ps0 += p0 + p2;
+                ps1 += p1 + p3;
+                pb[mt][0] = movmatrix_t(pack_bf16(p0, p1));
+                pb[mt][1] = movmatrix_t(pack_bf16(p2, p3));
+            }
+            lp[0] = lp[0] * al0 + ps0;
+            lp[1] = lp[1] * al1 + ps1;
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+                oacc[md][0] *= al0; oacc[md][1] *= al1; oacc[md][2] *= al0; oacc[md][3] *= al1;
+            }
+            // ---- O^T += V^T . P^T
+#pragma unroll
+            for (int md = 0; md < 8; ++md) {
+#pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    const int row = 16 * kk + (lane & 7) + ((lane >> 4) & 1) * 8;
+                    const int cg = 2 * md + ((lane >> 3) & 1);
+                    const uint32_t addr = vbase + (cg >> 3) * 4096 + row * 128 + (((cg & 7) ^ (row & 7)) << 4);
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_t(addr, a0, a1, a2, a3);
+                    mma_bf16(oacc[md], a0, a1, a2, a3, pb[kk][0], pb[kk][1]);
+                }
+            }
+            if (SCOUT_K2_SEPCB) {
+                __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.empty[s]);
+                held = -2 - s;
             }
         }
-        // ---- per-warp state -> combine buffer
+        // ---- warp state -> its held stage (combine area); no half -> empty
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
             lp[0] += __shfl_xor_sync(0xffffffffu, lp[0], o);
             lp[1] += __shfl_xor_sync(0xffffffffu, lp[1], o);
         }
+        __syncwarp();
+        const bool had = held != -1;
+        if (had) {
+            float* cb = SCOUT_K2_SEPCB ? reinterpret_cast<float*>(stages + NST * STAGE_BYTES) + warp * CBW
+                                       : reinterpret_cast<float*>(stages + held * STAGE_BYTES);
 #pragma unroll
-        for (int md = 0; md < 8; ++md) {
-            mycb[(2 * t) * CB_ROW + 16 * md + g] = oacc[md][0];
-            mycb[(2 * t + 1) * CB_ROW + 16 * md + g] = oacc[md][1];
-            mycb[(2 * t) * CB_ROW + 16 * md + g + 8] = oacc[md][2];
-            mycb[(2 * t + 1) * CB_ROW + 16 * md + g + 8] = oacc[md][3];
+            for (int md = 0; md < 8; ++md) {
+                cb[(2 * t) * CB_ROW + 16 * md + g] = oacc[md][0];
+                cb[(2 * t + 1) * CB_ROW + 16 * md + g] = oacc[md][1];
+                cb[(2 * t) * CB_ROW + 16 * md + g + 8] = oacc[md][2];
+                cb[(2 * t + 1) * CB_ROW + 16 * md + g + 8] = oacc[md][3];
+            }
+            if (g == 0) {
+                cb[8 * CB_ROW + 2 * t] = m2[0];
+                cb[8 * CB_ROW + 2 * t + 1] = m2[1];
+                cb[8 * CB_ROW + 8 + 2 * t] = lp[0];
+                cb[8 * CB_ROW + 8 + 2 * t + 1] = lp[1];
+            }
         }
-        if (g == 0) {
-            mycb[8 * CB_ROW + 2 * t] = m2[0];
-            mycb[8 * CB_ROW + 2 * t + 1] = m2[1];
-            mycb[8 * CB_ROW + 8 + 2 * t] = lp[0];
-            mycb[8 * CB_ROW + 8 + 2 * t + 1] = lp[1];
-        }
-        named_bar_sync(1, NC * 32);
-        // ---- merge the NC warp states: thread -> head ctid/16, 8 channels
-        const int hh = ctid >> 4, d0 = (ctid & 15) * 8;
+        if (lane == 0) sm.warp_stage[warp] = had ? (SCOUT_K2_SEPCB ? warp : held) : -1;
+        named_bar_sync(1, NCT);
+        // ---- merge the NC warp states: thread -> head ctid/32, 4 channels
+        const int hh = ctid >> 5, d0 = (ctid & 31) * 4;
         float M = -CUDART_INF_F;
 #pragma unroll
-        for (int w = 0; w < NC; ++w) M = fmaxf(M, cbuf[w * CB_WARP + 8 * CB_ROW + hh]);
-        float L = 0.f, acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int w = 0; w < NC; ++w) {
+            const int st = sm.warp_stage[w];
+            if (st >= 0) M = fmaxf(M, (SCOUT_K2_SEPCB ? reinterpret_cast<const float*>(stages + NST * STAGE_BYTES) + st * CBW
+                                                      : reinterpret_cast<const float*>(stages + st * STAGE_BYTES))[8 * CB_ROW + hh]);
+        }
+        float L = 0.f, acc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int w = 0; w < NC; ++w) {
-            const float* wb = cbuf + w * CB_WARP;
+            const int st = sm.warp_stage[w];
+            if (st < 0) continue;
+            const float* wb = SCOUT_K2_SEPCB ? reinterpret_cast<const float*>(stages + NST * STAGE_BYTES) + st * CBW
+                                             : reinterpret_cast<const float*>(stages + st * STAGE_BYTES);
             const float l = wb[8 * CB_ROW + 8 + hh];
             if (!(l > 0.f)) continue;
-            const float f = exp2f(wb[8 * CB_ROW + hh] - M);
-            L += l * f;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] += f * wb[hh * CB_ROW + d0 + e];
+            const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
+            L += l * fct;
+            const float4 x = *reinterpret_cast<const float4*>(wb + hh * CB_ROW + d0);
+            acc[0] += fct * x.x; acc[1] += fct * x.y; acc[2] += fct * x.z; acc[3] += fct * x.w;
+        }
+        named_bar_sync(1, NCT);  // every combine area read: stages can go back
+        if (held >= 0 && !SCOUT_K2_SEPCB) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.empty[held]);
         }
         const float inv = L > 0.f ? 1.f / L : 0.f;
         if (sg.nseg == 1) {
@@ -430,42 +523,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
                     Lt = L * wa + wb;
                 }
                 const float invt = Lt > 0.f ? 1.f / Lt : 0.f;
-                float* o = a.o + head * D + d0;
-                float r[8];
+                float r[4];
                 if (cl > 0.f) {
-                    const float* co = a.cpu_o + head * D + d0;
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) r[e] = (acc[e] * wa + wb * co[e]) * invt;
+                    const float4 co = *reinterpret_cast<const float4*>(a.cpu_o + head * D + d0);
+                    r[0] = (acc[0] * wa + wb * co.x) * invt; r[1] = (acc[1] * wa + wb * co.y) * invt;
+                    r[2] = (acc[2] * wa + wb * co.z) * invt; r[3] = (acc[3] * wa + wb * co.w) * invt;
                 } else {
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) r[e] = acc[e] * inv;
+                    for (int e = 0; e < 4; ++e) r[e] = acc[e] * inv;
                 }
-                *reinterpret_cast<float4*>(o) = make_float4(r[0], r[1], r[2], r[3]);
-                *reinterpret_cast<float4*>(o + 4) = make_float4(r[4], r[5], r[6], r[7]);
-                if ((ctid & 15) == 0) {
+                *reinterpret_cast<float4*>(a.o + head * D + d0) = make_float4(r[0], r[1], r[2], r[3]);
+                if ((ctid & 31) == 0) {
                     a.ml[head * 2] = Lt > 0.f ? Mt * LN2 : -CUDART_INF_F;
                     a.ml[head * 2 + 1] = Lt;
                 }
             }
-            named_bar_sync(1, NC * 32);  // combine buffer reuse
         } else {
             // write this segment's partial (o normalised, m2, l) to slot c+u
             float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
             *reinterpret_cast<float4*>(p + d0) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-            *reinterpret_cast<float4*>(p + d0 + 4) =
-                make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
-            if ((ctid & 15) == 0) { p[D] = M; p[D + 1] = L; }
+            if ((ctid & 31) == 0) { p[D] = M; p[D + 1] = L; }
             __threadfence();
-            named_bar_sync(1, NC * 32);
+            named_bar_sync(1, NCT);
             if (ctid == 0) {
                 const int old = atomicAdd(&ctr[u], 1);
                 sm.last_flag = (old == sg.nseg - 1);
             }
-            named_bar_sync(1, NC * 32);
+            named_bar_sync(1, NCT);
             if (sm.last_flag) {
                 // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
                 __threadfence();
-                finalize_unit<G>(a, u, parts, sg.cfirst + u, sg.nseg, ctid);
+                finalize_unit<G, NCT>(a, u, parts, sg.cfirst + u, sg.nseg, ctid);
                 if (ctid == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
             }
         }
@@ -473,7 +561,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
     // ---- units with no resident block: output = CPU partial (or empty)
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         if (a.n_res[u] != 0) continue;
-        finalize_unit<G>(a, u, parts, 0, 0, ctid);
+        finalize_unit<G, NCT>(a, u, parts, 0, 0, ctid);
     }
 }
 
@@ -565,7 +653,7 @@ template <int G>
 __global__ void combine_kernel(const scout_decode_args a) {
     const int u = blockIdx.x;
     const float* parts = reinterpret_cast<const float*>(static_cast<const uint8_t*>(a.workspace) + ctr_bytes(a.n_units));
-    tc::finalize_unit<G>(a, u, parts, u * SIMPLE_SPLIT, SIMPLE_SPLIT, threadIdx.x);
+    tc::finalize_unit<G, 128>(a, u, parts, u * SIMPLE_SPLIT, SIMPLE_SPLIT, threadIdx.x);
 }
 }  // namespace simple
 
@@ -630,8 +718,12 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
     }
     auto st = static_cast<cudaStream_t>(stream);
     if (a.kv_dtype == SCOUT_BF16) {
-        // a CTA range must not touch more than MAXSEG units
-        const int min_grid = (a.n_units + tc::MAXSEG - 3) / (tc::MAXSEG - 2);
+        // a CTA range must not touch more than MAXSEG units nor hold more than
+        // MAXB blocks (T <= n_units * k_stride)
+        int min_grid = (a.n_units + tc::MAXSEG - 3) / (tc::MAXSEG - 2);
+        const long long tmax = static_cast<long long>(a.n_units) * a.k_stride;
+        const int min_grid_b = static_cast<int>((tmax + tc::MAXB - 2) / (tc::MAXB - 1));
+        if (min_grid < min_grid_b) min_grid = min_grid_b;
         int grid = tc_grid(a.max_ctas);
         if (grid < min_grid) grid = min_grid;
         if (grid > GRID_CAP) grid = GRID_CAP;
