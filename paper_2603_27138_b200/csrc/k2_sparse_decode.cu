@@ -44,32 +44,41 @@ constexpr int GRID_CAP = 1024;
 __host__ __device__ inline size_t ctr_bytes(int n_units) { return ((static_cast<size_t>(n_units) * 4 + 255) / 256) * 256; }
 
 // =========================================================== bf16 kernel ==
+#ifdef SCOUT_K2_TIMING
+__device__ unsigned long long g_k2_ts[1024][6];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define K2TS(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_k2_ts[blockIdx.x][i] = gtime(); } while (0)
+#define K2TS_T(i, tid_) do { if (threadIdx.x == (tid_) && blockIdx.x < 1024) g_k2_ts[blockIdx.x][i] = gtime(); } while (0)
+#else
+#define K2TS(i) do {} while (0)
+#define K2TS_T(i, tid_) do {} while (0)
+#endif
+
 namespace tc {
-#ifndef SCOUT_K2_NC
-#define SCOUT_K2_NC 8
-#endif
-#ifndef SCOUT_K2_NST
-#define SCOUT_K2_NST 13
-#endif
-constexpr int NC = SCOUT_K2_NC;             // consumer warps (2 per scheduler)
+// One stage = one whole 32 KiB block (K tile then V tile): a single bulk copy,
+// the transfer size at which random gathers get the most out of HBM3e
+// (tools/microbench/gather.cu: 2x8 KiB 5.1, 16 KiB 5.9, 32 KiB 6.7 TB/s).
+// Consumer warps work in pairs: warp 2p+h takes 32-token half h of every
+// block j with j % NPAIR == p; pair p double-buffers its own stages p and
+// p + NPAIR, so every stage is filled and drained in order by one pair.
+constexpr int NPAIR = 3;
+constexpr int NC = 2 * NPAIR;               // consumer warps
 constexpr int NCT = NC * 32;                // consumer threads
 constexpr int NTHREADS = NCT + 32;          // + 1 producer warp
-constexpr int NST = SCOUT_K2_NST;           // ring stages (one 32-token half block each)
-constexpr int STAGE_BYTES = 16384;          // 8 KiB K half + 8 KiB V half
+constexpr int NST = 2 * NPAIR;              // ring stages
+constexpr int STAGE_BYTES = 32768;          // one block: K tile (16 KiB) + V tile (16 KiB)
 constexpr int MAXSEG = 128;
 constexpr int MAXB = 512;                   // blocks per CTA range (staged in smem)
 constexpr int CB_ROW = D + 4;               // combine rows (bank-conflict pad)
-#ifndef SCOUT_K2_SEPCB
-#define SCOUT_K2_SEPCB 0
-#endif
-constexpr int CBW = 8 * CB_ROW + 16;        // floats of one warp's combine area
-constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES + (SCOUT_K2_SEPCB ? NC * CBW * 4 : 0);
-static_assert(8 * CB_ROW * 4 + 64 <= STAGE_BYTES, "combine area must fit in a stage");
-static_assert(NST > NC, "a warp's held stage must never be needed inside its segment");
-static_assert(NCT == 256, "combine mapping: 8 heads x 32 threads x 4 channels");
+constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES;
+static_assert(8 * CB_ROW * 4 + 64 <= HALF_BYTES_BF16, "a warp's combine area must fit in its K half");
 
 struct Seg {
-    int unit, j0, j1, nseg, cfirst, f0, q0, q1;  // f0: first block in the CTA list; [q0,q1): halves
+    int unit, j0, j1, nseg, cfirst, f0;  // f0: first block in the CTA list
 };
 
 struct Smem {
@@ -78,15 +87,14 @@ struct Smem {
     Seg segs[MAXSEG];
     int blk_slot[MAXB];        // the CTA's resident blocks in stream order: pool slot
     int16_t blk_rows[MAXB];    // valid rows (64, or the open block's fill)
-    int16_t blk_h0[MAXB];      // first half index of the block (CTA-local)
-    int16_t half_blk[2 * MAXB];  // half -> block
-    int warp_stage[NC];        // stage holding a warp's combine area, -1: warp had no half
+    int warp_area[NC];         // byte offset of a warp's combine area, -1: no state
     int nsegs;
-    int nhalf;
     int scan_tot[NTHREADS / 32];
     int last_flag;
     long long run_total;
 };
+
+__device__ __forceinline__ int stage_of(int j) { return (j % NPAIR) + NPAIR * ((j / NPAIR) & 1); }
 
 __device__ __forceinline__ int unit_nb(const scout_decode_args& a, int u, int* tail) {
     const int nt = a.n_tokens[u];
@@ -97,59 +105,51 @@ __device__ __forceinline__ int unit_nb(const scout_decode_args& a, int u, int* t
 
 // Merge n partial slots (+ the optional CPU partial) of unit u into the
 // outputs (merge / finalize, attention.hpp:100-122; both empty -> zeros,
-// engine.hpp:273). NT threads: thread i -> head i/(NT/8), 1024/NT channels.
+// engine.hpp:273). NT threads cover 8 heads x 32 lanes x 4 channels.
 template <int G, int NT>
 __device__ void finalize_unit(const scout_decode_args& a, int u, const float* parts, int first_slot, int nslots,
                               int ctid) {
-    constexpr int TPH = NT / 8, CPT = D / TPH;  // threads per head, channels per thread
-    const int h = ctid / TPH;
-    const int d0 = (ctid % TPH) * CPT;
-    if (h >= G) return;
-    const size_t head = static_cast<size_t>(u) * G + h;
-    float M = -CUDART_INF_F;
-    for (int i = 0; i < nslots; ++i) {
-        const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * HEAD_STRIDE;
-        M = fmaxf(M, __ldcg(p + D));
-    }
-    float cm = -CUDART_INF_F, cl = 0.f;
-    if (a.cpu_ml) {
-        cm = a.cpu_ml[head * 2] * LOG2E;
-        cl = a.cpu_ml[head * 2 + 1];
-        if (cl > 0.f) M = fmaxf(M, cm);
-    }
-    float acc[CPT];
-#pragma unroll
-    for (int e = 0; e < CPT; ++e) acc[e] = 0.f;
-    float L = 0.f;
-    if (M != -CUDART_INF_F) {
+    for (int idx = ctid; idx < 8 * 32; idx += NT) {
+        const int h = idx >> 5;
+        const int d0 = (idx & 31) * 4;
+        if (h >= G) continue;
+        const size_t head = static_cast<size_t>(u) * G + h;
+        float M = -CUDART_INF_F;
         for (int i = 0; i < nslots; ++i) {
             const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * HEAD_STRIDE;
-            const float l = __ldcg(p + D + 1);
-            if (!(l > 0.f)) continue;
-            const float w = l * exp2f(__ldcg(p + D) - M);
-            L += w;
-#pragma unroll
-            for (int e = 0; e < CPT; e += 4) {
-                const float4 x = __ldcg(reinterpret_cast<const float4*>(p + d0 + e));
-                acc[e] += w * x.x; acc[e + 1] += w * x.y; acc[e + 2] += w * x.z; acc[e + 3] += w * x.w;
+            M = fmaxf(M, __ldcg(p + D));
+        }
+        float cm = -CUDART_INF_F, cl = 0.f;
+        if (a.cpu_ml) {
+            cm = a.cpu_ml[head * 2] * LOG2E;
+            cl = a.cpu_ml[head * 2 + 1];
+            if (cl > 0.f) M = fmaxf(M, cm);
+        }
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float L = 0.f;
+        if (M != -CUDART_INF_F) {
+            for (int i = 0; i < nslots; ++i) {
+                const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE + h * HEAD_STRIDE;
+                const float l = __ldcg(p + D + 1);
+                if (!(l > 0.f)) continue;
+                const float w = l * exp2f(__ldcg(p + D) - M);
+                L += w;
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(p + d0));
+                acc.x += w * x.x; acc.y += w * x.y; acc.z += w * x.z; acc.w += w * x.w;
+            }
+            if (cl > 0.f) {
+                const float w = cl * exp2f(cm - M);
+                L += w;
+                const float4 co = *reinterpret_cast<const float4*>(a.cpu_o + head * D + d0);
+                acc.x += w * co.x; acc.y += w * co.y; acc.z += w * co.z; acc.w += w * co.w;
             }
         }
-        if (cl > 0.f) {
-            const float w = cl * exp2f(cm - M);
-            L += w;
-            const float* co = a.cpu_o + head * D + d0;
-#pragma unroll
-            for (int e = 0; e < CPT; ++e) acc[e] += w * co[e];
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        *reinterpret_cast<float4*>(a.o + head * D + d0) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        if ((idx & 31) == 0) {
+            a.ml[head * 2] = L > 0.f ? M * LN2 : -CUDART_INF_F;
+            a.ml[head * 2 + 1] = L;
         }
-    }
-    float* o = a.o + head * D + d0;
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-#pragma unroll
-    for (int e = 0; e < CPT; e += 4)
-        *reinterpret_cast<float4*>(o + e) = make_float4(acc[e] * inv, acc[e + 1] * inv, acc[e + 2] * inv, acc[e + 3] * inv);
-    if ((ctid % TPH) == 0) {
-        a.ml[head * 2] = L > 0.f ? M * LN2 : -CUDART_INF_F;
-        a.ml[head * 2 + 1] = L;
     }
 }
 
@@ -164,11 +164,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
     const int ks = a.k_stride;
     int* ctr = reinterpret_cast<int*>(a.workspace);
     float* parts = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + ctr_bytes(nunits));
+    K2TS(0);
 
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&sm.full[i], 1);
-            mbar_init(&sm.empty[i], 1);
+            mbar_init(&sm.empty[i], 2);  // both warps of the owning pair release
         }
         fence_mbar_init();
         sm.nsegs = 0;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
                 const int idx = atomicAdd(&sm.nsegs, 1);
                 if (idx < MAXSEG)
                     sm.segs[idx] = Seg{u, static_cast<int>(s0 - pre), static_cast<int>(s1 - pre),
-                                       static_cast<int>(cl - cf + 1), static_cast<int>(cf), 0, 0, 0};
+                                       static_cast<int>(cl - cf + 1), static_cast<int>(cf), 0};
             }
         }
         __syncthreads();
@@ -257,62 +258,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
         sm.blk_rows[f] = static_cast<int16_t>((a.res_ids[idx] == nb - 1) ? tail : BS);
     }
     __syncthreads();
-    // half-block table: prefix of halves per block (warp 0), then half -> block
-    if (warp == 0) {
-        constexpr int PER = MAXB / 32;
-        int cnt[PER];
-        int loc = 0;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int f = lane * PER + i;
-            cnt[i] = f < nblk ? (sm.blk_rows[f] > HALF_ROWS ? 2 : 1) : 0;
-            loc += cnt[i];
-        }
-        int x = loc;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        int pre = x - loc;
-#pragma unroll
-        for (int i = 0; i < PER; ++i) {
-            const int f = lane * PER + i;
-            if (f < nblk) {
-                sm.blk_h0[f] = static_cast<int16_t>(pre);
-                sm.half_blk[pre] = static_cast<int16_t>(f);
-                if (cnt[i] == 2) sm.half_blk[pre + 1] = static_cast<int16_t>(f);
-            }
-            pre += cnt[i];
-        }
-        if (lane == 31) sm.nhalf = x;
-    }
-    __syncthreads();
-    if (tid < nsegs) {
-        Seg& sg = sm.segs[tid];
-        const int fe = sg.f0 + (sg.j1 - sg.j0);
-        sg.q0 = sm.blk_h0[sg.f0];
-        sg.q1 = fe < nblk ? sm.blk_h0[fe] : sm.nhalf;
-    }
-    __syncthreads();
-    const int nhalf = sm.nhalf;
 
+    K2TS(1);
     if (warp == NC) {
         // ================================================== producer warp
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
-            for (int q = 0; q < nhalf; ++q) {
-                const int f = sm.half_blk[q];
-                const int h = q - sm.blk_h0[f];
-                const uint8_t* kb = pool + static_cast<size_t>(sm.blk_slot[f]) * BF16_SLOT_BYTES;
-                const int s = q % NST;
-                if (q >= NST) mbar_wait(&sm.empty[s], ((q / NST) - 1) & 1);
+            for (int j = 0; j < nblk; ++j) {
+                const int s = stage_of(j);
+                if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
                 mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
-                bulk_g2s_evict_first(stages + s * STAGE_BYTES, kb + h * HALF_BYTES_BF16, HALF_BYTES_BF16,
+                bulk_g2s_evict_first(stages + s * STAGE_BYTES,
+                                     pool + static_cast<size_t>(sm.blk_slot[j]) * BF16_SLOT_BYTES, STAGE_BYTES,
                                      &sm.full[s], pol);
-                bulk_g2s_evict_first(stages + s * STAGE_BYTES + HALF_BYTES_BF16,
-                                     kb + BF16_TILE_BYTES + h * HALF_BYTES_BF16, HALF_BYTES_BF16, &sm.full[s], pol);
             }
         }
         return;
@@ -320,6 +279,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
 
     // ====================================================== consumer warps
     const int g = lane >> 2, t = lane & 3;
+    const int pair = warp >> 1, hsel = warp & 1;
     const float sl2 = a.scale * LOG2E;
     const int ctid = tid;  // 0 .. NCT-1
     for (int si = 0; si < nsegs; ++si) {
@@ -349,26 +309,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
 #pragma unroll
         for (int i = 0; i < 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
 
-        int held = -1;  // stage kept as this warp's combine area
-        int q = sg.q0 + ((warp - sg.q0) % NC + NC) % NC;
-        for (; q < sg.q1; q += NC) {
-            if (held >= 0 && !SCOUT_K2_SEPCB) {  // previous half fully consumed: hand its stage back
+        int held = -1;  // stage of the pair's last block: hosts the combine areas
+        bool any = false;
+        const int f1 = sg.f0 + (sg.j1 - sg.j0);
+        for (int f = sg.f0 + ((pair - sg.f0) % NPAIR + NPAIR) % NPAIR; f < f1; f += NPAIR) {
+            if (held >= 0) {  // the pair's previous block is done: hand its stage back
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.empty[held]);
             }
-            const int f = sm.half_blk[q];
-            const int valid = min(HALF_ROWS, sm.blk_rows[f] - (q - sm.blk_h0[f]) * HALF_ROWS);
-            const int s = q % NST;
+            const int s = stage_of(f);
             held = s;
-            // Successive fills of a stage go to different warps, so this warp may
-            // arrive here while fill f-1 of the stage is still in flight; the
-            // full-barrier parity would then alias (it only tells phase parity).
-            // Observing fill f-1's release on `empty` first makes it exact.
-            if (q >= NST) mbar_wait(&sm.empty[s], ((q / NST) - 1) & 1);
-            mbar_wait(&sm.full[s], (q / NST) & 1);
+            const int valid = min(HALF_ROWS, static_cast<int>(sm.blk_rows[f]) - hsel * HALF_ROWS);
+            mbar_wait(&sm.full[s], (f / NST) & 1);
             __syncwarp();  // lanes may leave the try_wait loop apart: reconverge before .aligned ops
-            const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES);
-            const uint32_t vbase = kbase + HALF_BYTES_BF16;
+            if (f == 0) K2TS(2);
+            if (valid <= 0) continue;  // open block with one half: the other warp idles
+            any = true;
+            const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES) + hsel * HALF_BYTES_BF16;
+            const uint32_t vbase = kbase + BF16_TILE_BYTES;
             if (valid < HALF_ROWS) {
                 // rows past the open block's fill hold stale bytes: P is 0
                 // there, but 0 * NaN would poison O, so zero those V rows.
@@ -447,23 +405,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
                     mma_bf16(oacc[md], a0, a1, a2, a3, pb[kk][0], pb[kk][1]);
                 }
             }
-            if (SCOUT_K2_SEPCB) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[s]);
-                held = -2 - s;
-            }
         }
-        // ---- warp state -> its held stage (combine area); no half -> empty
+        // ---- warp state -> its combine area: the K half it read of the pair's
+        // last stage (the partner reads only the other half of that stage)
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
             lp[0] += __shfl_xor_sync(0xffffffffu, lp[0], o);
             lp[1] += __shfl_xor_sync(0xffffffffu, lp[1], o);
         }
         __syncwarp();
-        const bool had = held != -1;
-        if (had) {
-            float* cb = SCOUT_K2_SEPCB ? reinterpret_cast<float*>(stages + NST * STAGE_BYTES) + warp * CBW
-                                       : reinterpret_cast<float*>(stages + held * STAGE_BYTES);
+        const int area = (held >= 0 && any) ? held * STAGE_BYTES + hsel * HALF_BYTES_BF16 : -1;
+        if (area >= 0) {
+            float* cb = reinterpret_cast<float*>(stages + area);
 #pragma unroll
             for (int md = 0; md < 8; ++md) {
                 cb[(2 * t) * CB_ROW + 16 * md + g] = oacc[md][0];
@@ -478,40 +431,56 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
                 cb[8 * CB_ROW + 8 + 2 * t + 1] = lp[1];
             }
         }
-        if (lane == 0) sm.warp_stage[warp] = had ? (SCOUT_K2_SEPCB ? warp : held) : -1;
+        if (lane == 0) sm.warp_area[warp] = area;
+        if (si == nsegs - 1) K2TS(3);
         named_bar_sync(1, NCT);
-        // ---- merge the NC warp states: thread -> head ctid/32, 4 channels
-        const int hh = ctid >> 5, d0 = (ctid & 31) * 4;
-        float M = -CUDART_INF_F;
+        // ---- merge the NC warp states (8 heads x 32 lanes x 4 channels)
+        float Ms[2], Ls[2];
+        float4 accs[2];
 #pragma unroll
-        for (int w = 0; w < NC; ++w) {
-            const int st = sm.warp_stage[w];
-            if (st >= 0) M = fmaxf(M, (SCOUT_K2_SEPCB ? reinterpret_cast<const float*>(stages + NST * STAGE_BYTES) + st * CBW
-                                                      : reinterpret_cast<const float*>(stages + st * STAGE_BYTES))[8 * CB_ROW + hh]);
-        }
-        float L = 0.f, acc[4] = {0, 0, 0, 0};
+        for (int r = 0; r < 2; ++r) {
+            const int idx = ctid + r * NCT;
+            Ms[r] = -CUDART_INF_F; Ls[r] = 0.f; accs[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (idx >= 256) continue;
+            const int hh = idx >> 5, d0 = (idx & 31) * 4;
+            float M = -CUDART_INF_F;
 #pragma unroll
-        for (int w = 0; w < NC; ++w) {
-            const int st = sm.warp_stage[w];
-            if (st < 0) continue;
-            const float* wb = SCOUT_K2_SEPCB ? reinterpret_cast<const float*>(stages + NST * STAGE_BYTES) + st * CBW
-                                             : reinterpret_cast<const float*>(stages + st * STAGE_BYTES);
-            const float l = wb[8 * CB_ROW + 8 + hh];
-            if (!(l > 0.f)) continue;
-            const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
-            L += l * fct;
-            const float4 x = *reinterpret_cast<const float4*>(wb + hh * CB_ROW + d0);
-            acc[0] += fct * x.x; acc[1] += fct * x.y; acc[2] += fct * x.z; acc[3] += fct * x.w;
+            for (int w = 0; w < NC; ++w) {
+                const int ar = sm.warp_area[w];
+                if (ar >= 0) M = fmaxf(M, reinterpret_cast<const float*>(stages + ar)[8 * CB_ROW + hh]);
+            }
+            float L = 0.f;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int w = 0; w < NC; ++w) {
+                const int ar = sm.warp_area[w];
+                if (ar < 0) continue;
+                const float* wb = reinterpret_cast<const float*>(stages + ar);
+                const float l = wb[8 * CB_ROW + 8 + hh];
+                if (!(l > 0.f)) continue;
+                const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
+                L += l * fct;
+                const float4 x = *reinterpret_cast<const float4*>(wb + hh * CB_ROW + d0);
+                acc.x += fct * x.x; acc.y += fct * x.y; acc.z += fct * x.z; acc.w += fct * x.w;
+            }
+            Ms[r] = M; Ls[r] = L; accs[r] = acc;
         }
         named_bar_sync(1, NCT);  // every combine area read: stages can go back
-        if (held >= 0 && !SCOUT_K2_SEPCB) {
+        if (held >= 0) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.empty[held]);
         }
-        const float inv = L > 0.f ? 1.f / L : 0.f;
-        if (sg.nseg == 1) {
-            // the whole unit is here: merge with the CPU partial and write out
-            if (hh < G) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int idx = ctid + r * NCT;
+            if (idx >= 256) continue;
+            const int hh = idx >> 5, d0 = (idx & 31) * 4;
+            const float M = Ms[r], L = Ls[r];
+            const float4 acc = accs[r];
+            const float inv = L > 0.f ? 1.f / L : 0.f;
+            if (sg.nseg == 1) {
+                // the whole unit is here: merge with the CPU partial and write out
+                if (hh >= G) continue;
                 const size_t head = static_cast<size_t>(u) * G + hh;
                 float cm = -CUDART_INF_F, cl = 0.f;
                 if (a.cpu_ml) { cm = a.cpu_ml[head * 2] * LOG2E; cl = a.cpu_ml[head * 2 + 1]; }
@@ -523,26 +492,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
                     Lt = L * wa + wb;
                 }
                 const float invt = Lt > 0.f ? 1.f / Lt : 0.f;
-                float r[4];
+                float4 res;
                 if (cl > 0.f) {
                     const float4 co = *reinterpret_cast<const float4*>(a.cpu_o + head * D + d0);
-                    r[0] = (acc[0] * wa + wb * co.x) * invt; r[1] = (acc[1] * wa + wb * co.y) * invt;
-                    r[2] = (acc[2] * wa + wb * co.z) * invt; r[3] = (acc[3] * wa + wb * co.w) * invt;
+                    res = make_float4((acc.x * wa + wb * co.x) * invt, (acc.y * wa + wb * co.y) * invt,
+                                      (acc.z * wa + wb * co.z) * invt, (acc.w * wa + wb * co.w) * invt);
                 } else {
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) r[e] = acc[e] * inv;
+                    res = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
                 }
-                *reinterpret_cast<float4*>(a.o + head * D + d0) = make_float4(r[0], r[1], r[2], r[3]);
-                if ((ctid & 31) == 0) {
+                *reinterpret_cast<float4*>(a.o + head * D + d0) = res;
+                if ((idx & 31) == 0) {
                     a.ml[head * 2] = Lt > 0.f ? Mt * LN2 : -CUDART_INF_F;
                     a.ml[head * 2 + 1] = Lt;
                 }
+            } else {
+                // this segment's partial (o normalised, m2, l) -> slot c+u
+                float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
+                *reinterpret_cast<float4*>(p + d0) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                if ((idx & 31) == 0) { p[D] = M; p[D + 1] = L; }
             }
-        } else {
-            // write this segment's partial (o normalised, m2, l) to slot c+u
-            float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
-            *reinterpret_cast<float4*>(p + d0) = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-            if ((ctid & 31) == 0) { p[D] = M; p[D + 1] = L; }
+        }
+        if (sg.nseg != 1) {
             __threadfence();
             named_bar_sync(1, NCT);
             if (ctid == 0) {
@@ -558,11 +528,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
             }
         }
     }
+    K2TS(4);
     // ---- units with no resident block: output = CPU partial (or empty)
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         if (a.n_res[u] != 0) continue;
         finalize_unit<G, NCT>(a, u, parts, 0, 0, ctid);
     }
+    K2TS(5);
 }
 
 }  // namespace tc
@@ -755,3 +727,9 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
     }
     return check_launch("scout_sparse_decode");
 }
+
+#ifdef SCOUT_K2_TIMING
+extern "C" int scout_debug_k2_times(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, g_k2_ts, sizeof(g_k2_ts)) == cudaSuccess ? 0 : 3;
+}
+#endif
