@@ -58,6 +58,13 @@ enum scout_status {
 
 enum scout_dtype { SCOUT_F32 = 0, SCOUT_BF16 = 1, SCOUT_F64 = 2 };
 
+/* Launch flags. SCOUT_LAUNCH_PDL launches with programmatic stream
+ * serialization: K1 scores before waiting on the preceding kernel (it only
+ * waits to publish its lists), K2 waits before reading K1's lists, so
+ * consecutive K1/K2 launches overlap their prologues and tails. Every kernel
+ * still observes all prior stream work before it reads dependent data. */
+#define SCOUT_LAUNCH_PDL 1
+
 /* DigestMethod, digest.hpp:23 */
 enum scout_digest_method { SCOUT_DIGEST_MINMAX = 0, SCOUT_DIGEST_MEAN = 1 };
 
@@ -134,6 +141,7 @@ typedef struct scout_topk_args {
     int32_t* cpu_tokens;
     int32_t* last_selected;
     double* scores_out;
+    int flags;      /* SCOUT_LAUNCH_PDL: programmatic dependent launch */
 } scout_topk_args;
 
 int scout_score_topk_split(const scout_topk_args* args, void* stream);
@@ -170,6 +178,7 @@ typedef struct scout_decode_args {
     void* workspace;
     size_t workspace_bytes;
     int max_ctas; /* 0 = one persistent CTA per SM */
+    int flags;    /* SCOUT_LAUNCH_PDL: programmatic dependent launch */
 } scout_decode_args;
 
 size_t scout_sparse_decode_workspace_bytes(int n_units, int group, int max_ctas);

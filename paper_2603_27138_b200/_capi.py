@@ -44,7 +44,7 @@ class TopkArgs(C.Structure):
         ("q", _vp), ("digests", _vp), ("n_tokens", _vp), ("block_table", _vp),
         ("sel_ids", _vp), ("n_sel", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
         ("cpu_ids", _vp), ("n_cpu", _vp), ("res_tokens", _vp), ("cpu_tokens", _vp),
-        ("last_selected", _vp), ("scores_out", _vp),
+        ("last_selected", _vp), ("scores_out", _vp), ("flags", C.c_int),
     ]
 
 
@@ -54,7 +54,7 @@ class DecodeArgs(C.Structure):
         ("scale", C.c_float),
         ("q", _vp), ("kv_pool", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
         ("n_tokens", _vp), ("cpu_o", _vp), ("cpu_ml", _vp), ("o", _vp), ("ml", _vp),
-        ("workspace", _vp), ("workspace_bytes", C.c_size_t), ("max_ctas", C.c_int),
+        ("workspace", _vp), ("workspace_bytes", C.c_size_t), ("max_ctas", C.c_int), ("flags", C.c_int),
     ]
 
 

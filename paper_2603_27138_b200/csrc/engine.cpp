@@ -67,6 +67,14 @@ struct scout_engine {
     std::vector<cudaEvent_t> chunk_ev;   // h2d chunk ready
     std::vector<cudaEvent_t> done_ev;    // compute chunk done
     cudaEvent_t k1_ev = nullptr;
+    bool pdl = false;  // programmatic dependent launch (off: K1 runs on its own stream)
+    // K1 runs one layer ahead on its own stream, co-resident with the
+    // persistent K2 CTAs (K1 fits in the shared memory K2 leaves free)
+    cudaStream_t k1s = nullptr;
+    std::vector<cudaEvent_t> ev_k1;     // K1(i) done  -> K2(i) may read its lists
+    std::vector<cudaEvent_t> ev_k2;     // K2(i) done  -> next step's K1(i) may overwrite them
+    std::vector<char> k2_recorded;
+    cudaEvent_t ev_start = nullptr;
     // timing
     bool timing = false;
     std::vector<cudaEvent_t> tev;
@@ -78,6 +86,10 @@ struct scout_engine {
     int32_t* I(Buf& b) const { return static_cast<int32_t*>(b.p); }
 
     ~scout_engine() {
+        if (k1s) cudaStreamDestroy(k1s);
+        for (auto e : ev_k1) cudaEventDestroy(e);
+        for (auto e : ev_k2) cudaEventDestroy(e);
+        if (ev_start) cudaEventDestroy(ev_start);
         if (side) cudaStreamDestroy(side);
         if (h2d) cudaStreamDestroy(h2d);
         if (d2h) cudaStreamDestroy(d2h);
@@ -115,6 +127,7 @@ struct scout_engine {
         a.n_cpu = I(n_cpu) + lu(layer);
         a.res_tokens = I(res_tok) + lu(layer);
         a.cpu_tokens = I(cpu_tok) + lu(layer);
+        a.flags = pdl ? SCOUT_LAUNCH_PDL : 0;
         ++launches;
         return scout_score_topk_split(&a, st);
     }
@@ -155,6 +168,7 @@ struct scout_engine {
         a.workspace = ws.p;
         a.workspace_bytes = ws_bytes;
         a.max_ctas = cfg.max_ctas;
+        a.flags = pdl ? SCOUT_LAUNCH_PDL : 0;
         ++launches;
         const int rc = scout_sparse_decode(&a, st);
         if (rc != SCOUT_OK) return rc;
@@ -185,13 +199,34 @@ struct scout_engine {
         return SCOUT_OK;
     }
 
-    int layer_step(int i, int step, const float* qt, const float* qp_next, const float* co, const float* cml,
-                   float* o, float* ml, cudaStream_t st) {
-        int rc;
-        if (i == 0 && (rc = select(0, qt, step, st)) != SCOUT_OK) return rc;
-        if (i + 1 < cfg.layers && (rc = select(i + 1, qp_next, step, st)) != SCOUT_OK) return rc;
-        if ((rc = attend(i, qt, co, cml, o, ml, st)) != SCOUT_OK) return rc;
+    // K1(i) on the K1 stream (after the previous step's K2(i) released layer
+    // i's lists), K2(i) on the caller's stream after K1(i).
+    int k1_layer(int i, const float* q, int step) {
+        if (k2_recorded[i]) CU(cudaStreamWaitEvent(k1s, ev_k2[i], 0));
+        const int rc = select(i, q, step, k1s);
+        if (rc != SCOUT_OK) return rc;
+        CU(cudaEventRecord(ev_k1[i], k1s));
+        return SCOUT_OK;
+    }
+    int k2_layer(int i, int step, const float* qt, const float* co, const float* cml, float* o, float* ml,
+                 cudaStream_t st) {
+        CU(cudaStreamWaitEvent(st, ev_k1[i], 0));
+        int rc = attend(i, qt, co, cml, o, ml, st);
+        if (rc != SCOUT_OK) return rc;
+        CU(cudaEventRecord(ev_k2[i], st));
+        k2_recorded[i] = 1;
         return maybe_recall(i, step, st);
+    }
+    // inputs written to `st` before the step are visible to the K1 stream
+    int begin_step(cudaStream_t st) {
+        CU(cudaEventRecord(ev_start, st));
+        CU(cudaStreamWaitEvent(k1s, ev_start, 0));
+        return SCOUT_OK;
+    }
+    int end_step(cudaStream_t st) {
+        CU(cudaEventRecord(ev_start, k1s));
+        CU(cudaStreamWaitEvent(st, ev_start, 0));
+        return SCOUT_OK;
     }
 };
 
@@ -241,6 +276,13 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         return SCOUT_ERR_CUDA;
     }
     cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&e->k1s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&e->ev_start, cudaEventDisableTiming);
+    e->ev_k1.resize(c.layers);
+    e->ev_k2.resize(c.layers);
+    for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    for (auto& ev : e->ev_k2) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    e->k2_recorded.assign(c.layers, 0);
     cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&e->ev_main, cudaEventDisableTiming);
@@ -298,12 +340,16 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const float* 
     }
     auto st = static_cast<cudaStream_t>(stream);
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
-    for (int i = 0; i < e->cfg.layers; ++i) {
-        const int rc = e->layer_step(i, step, q_true + i * qd, q_pred + (i + 1) * qd, cpu_o ? cpu_o + i * qd : nullptr,
-                                     cpu_ml ? cpu_ml + i * md : nullptr, out_o + i * qd, out_ml + i * md, st);
-        if (rc != SCOUT_OK) return rc;
+    const int L = e->cfg.layers;
+    int rc = e->begin_step(st);
+    // K1 runs ahead: layer 0 with the true query, layer i+1 with the predicted one
+    for (int i = 0; i < L && rc == SCOUT_OK; ++i) {
+        rc = e->k1_layer(i, i == 0 ? q_true : q_pred + i * qd, step);
+        if (rc == SCOUT_OK) rc = e->k2_layer(i, step, q_true + i * qd, cpu_o ? cpu_o + i * qd : nullptr,
+                                             cpu_ml ? cpu_ml + i * md : nullptr, out_o + i * qd, out_ml + i * md, st);
     }
-    return SCOUT_OK;
+    if (rc != SCOUT_OK) return rc;
+    return e->end_step(st);
 }
 
 extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const float* h_q_true, const float* h_q_pred,
@@ -339,24 +385,28 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
     }
     float* d_o = d_cm + L * md;   // outputs: [L][UG][128] then [L][UG][2]
     float* d_oml = d_o + L * qd;
+    // K1 stream: waits for each input chunk, runs one layer ahead of K2
+    int rc = e->begin_step(st);
+    if (rc != SCOUT_OK) return rc;
     for (int i = 0; i < L; ++i) {
-        if (i % CH == 0) CU(cudaStreamWaitEvent(st, e->chunk_ev[i / CH], 0));
-        if (i + 1 < L && (i + 1) % CH == 0) CU(cudaStreamWaitEvent(st, e->chunk_ev[(i + 1) / CH], 0));
-        float* o = d_o + i * qd;
-        float* ml = d_oml + i * md;
-        int rc = e->layer_step(i, step, d_qt + i * qd, d_qp + (i + 1) * qd, h_cpu_o ? d_co + i * qd : nullptr,
-                               h_cpu_ml ? d_cm + i * md : nullptr, o, ml, st);
+        if (i % CH == 0) {
+            CU(cudaStreamWaitEvent(st, e->chunk_ev[i / CH], 0));
+            CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[i / CH], 0));
+        }
+        rc = e->k1_layer(i, i == 0 ? d_qt : d_qp + i * qd, step);
         if (rc != SCOUT_OK) return rc;
-        if (h_cpu_ids && i + 1 < L) {
-            // the host co-attention worker needs layer i+1's CPU-side ids now
-            CU(cudaEventRecord(e->k1_ev, st));
-            CU(cudaStreamWaitEvent(e->d2h, e->k1_ev, 0));
-            CU(cudaMemcpyAsync(h_cpu_ids + e->lk(i + 1), e->I(e->cpu_ids) + e->lk(i + 1),
+        if (h_cpu_ids && i > 0) {
+            // the host co-attention worker needs layer i's CPU-side ids as soon as K1(i) is done
+            CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[i], 0));
+            CU(cudaMemcpyAsync(h_cpu_ids + e->lk(i), e->I(e->cpu_ids) + e->lk(i),
                                static_cast<size_t>(e->U) * e->cfg.k * 4, cudaMemcpyDeviceToHost, e->d2h));
             if (h_n_cpu)
-                CU(cudaMemcpyAsync(h_n_cpu + e->lu(i + 1), e->I(e->n_cpu) + e->lu(i + 1), static_cast<size_t>(e->U) * 4,
+                CU(cudaMemcpyAsync(h_n_cpu + e->lu(i), e->I(e->n_cpu) + e->lu(i), static_cast<size_t>(e->U) * 4,
                                    cudaMemcpyDeviceToHost, e->d2h));
         }
+        rc = e->k2_layer(i, step, d_qt + i * qd, h_cpu_o ? d_co + i * qd : nullptr, h_cpu_ml ? d_cm + i * md : nullptr,
+                         d_o + i * qd, d_oml + i * md, st);
+        if (rc != SCOUT_OK) return rc;
         if (i % CH == CH - 1 || i == L - 1) {
             const int c = i / CH, lo = c * CH, n = i + 1 - lo;
             CU(cudaEventRecord(e->done_ev[c], st));
@@ -365,6 +415,7 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
             CU(cudaMemcpyAsync(h_out_ml + lo * md, d_oml + lo * md, n * md * 4, cudaMemcpyDeviceToHost, e->d2h));
         }
     }
+    if ((rc = e->end_step(st)) != SCOUT_OK) return rc;
     if (h_cpu_ids) {  // layer 0's ids (selected on the true query; layer 0 is pinned so none)
         CU(cudaMemcpyAsync(h_cpu_ids, e->I(e->cpu_ids), static_cast<size_t>(e->U) * e->cfg.k * 4,
                            cudaMemcpyDeviceToHost, e->d2h));

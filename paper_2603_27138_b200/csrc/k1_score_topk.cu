@@ -24,7 +24,7 @@ using namespace scout_dev;
 
 namespace {
 
-constexpr int K1_THREADS = 512;
+constexpr int K1_THREADS = 256;
 constexpr int K1_WARPS = K1_THREADS / 32;
 
 __device__ __forceinline__ uint64_t score_key(double s) {
@@ -222,7 +222,7 @@ __device__ void radix_kth(int nb, int k, KeyF keyf, CandF candf, SelScratch& S, 
 enum : uint8_t { CLS_OUT = 0, CLS_IN = 1, CLS_Z = 2 };
 
 template <typename DigT, int G, int MODE>
-__global__ void __launch_bounds__(K1_THREADS, 2) score_topk_kernel(const scout_topk_args a) {
+__global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk_args a) {
     extern __shared__ __align__(16) uint8_t k1_smem[];
     double* qs = reinterpret_cast<double*>(k1_smem);            // [D][G] stacked order
     double2* pn = reinterpret_cast<double2*>(qs + D * G);       // [D] (sum q>=0, sum q<0)
@@ -237,6 +237,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) score_topk_kernel(const scout_t
 
     const int u = blockIdx.x;
     const int tid = threadIdx.x;
+    // PDL: the next kernel may launch now; this one only reads inputs until it
+    // publishes its lists (griddep_wait below orders those writes).
+    griddep_launch_dependents();
+    if (a.scores_out) griddep_wait();
     int ntok = a.n_tokens[u];
     ntok = max(0, min(ntok, a.nb_stride * BS));
     const int nb = (ntok + BS - 1) / BS;
@@ -282,10 +286,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) score_topk_kernel(const scout_t
             // are summed in a fixed order afterwards (order is free: approximate).
             const int nq = (nb + 3) >> 2;
             int P = 1;
-            while (P < 4 && nq * P * 2 <= K1_THREADS) P *= 2;
+            while (P < 2 && nq * P * 2 <= K1_THREADS) P *= 2;
             const int cper = D / P;
             // [P][nb] partials overlay keys/cls (P*nq <= K1_THREADS, so P*nb <= max(4*K1_THREADS+12,
-            // nb_stride): sized at launch)
+            // nb_stride): sized at launch; small so K1 can co-reside with a K2 CTA)
             double* part_s = reinterpret_cast<double*>(keys);
             float* part_a = reinterpret_cast<float*>(part_s + P * nb);
             for (int t = tid; t < nq * P; t += K1_THREADS) {
@@ -333,13 +337,13 @@ __global__ void __launch_bounds__(K1_THREADS, 2) score_topk_kernel(const scout_t
             __syncthreads();
             // fold the parts (fixed order) -> approximate keys; keys overlay part 0
             float amax = 0.f;
-            double sfold[8];
+            double sfold[16];
             int nmine = 0;
             for (int b = tid; b < nb; b += K1_THREADS) {
                 double sv = part_s[b];
                 float av = part_a[b];
                 for (int p = 1; p < P; ++p) { sv += part_s[p * nb + b]; av += part_a[p * nb + b]; }
-                if (nmine < 8) sfold[nmine] = sv;
+                if (nmine < 16) sfold[nmine] = sv;
                 ++nmine;
                 amax = fmaxf(amax, av * 1.0001f);
             }
@@ -407,6 +411,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) score_topk_kernel(const scout_t
     }
     __syncthreads();
 
+    griddep_wait();  // everything before this launch is complete: safe to publish
     // ---- selection flags in id order: contiguous chunks per thread
     const int chunk = (nb + K1_THREADS - 1) / K1_THREADS;
     const int b_begin = min(nb, tid * chunk), b_end = min(nb, b_begin + chunk);
@@ -482,13 +487,13 @@ template <typename DigT, int MODE>
 int launch_g(const scout_topk_args& a, cudaStream_t st) {
     // qs | pn | pna | max(keys + cls, part_s[P][nb] + part_a[P][nb]) with P*nb <= max(4*K1_THREADS+12, nbs)
     const size_t nbs = static_cast<size_t>(a.nb_stride);
-    const size_t pmax = 4 * K1_THREADS + 12;
+    const size_t pmax = 4 * K1_THREADS + 12;  // P * nq <= K1_THREADS
     const size_t pnb = nbs > pmax ? nbs : pmax;
     const size_t tail = nbs * 9 > pnb * 12 ? nbs * 9 : pnb * 12;
     const size_t smem = static_cast<size_t>(D) * a.group * 8 + static_cast<size_t>(D) * 24 + tail;
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
-        kern<<<a.n_units, K1_THREADS, smem, st>>>(a);
+        scout_host::launch(kern, dim3(a.n_units), dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, a);
     };
     switch (a.group) {
         case 1: go(score_topk_kernel<DigT, 1, MODE>); break;

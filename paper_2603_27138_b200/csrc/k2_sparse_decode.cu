@@ -175,6 +175,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
         sm.nsegs = 0;
         sm.run_total = 0;
     }
+    // PDL: K1's lists (n_res, res_slots, res_ids) are complete past this point
+    griddep_wait();
+    griddep_launch_dependents();
     __syncthreads();
 
     // ---- pass 1: total resident blocks T
@@ -701,7 +704,8 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
         if (grid > GRID_CAP) grid = GRID_CAP;
         auto go = [&](auto kern) {
             scout_host::ensure_smem(reinterpret_cast<const void*>(kern), tc::SMEM_BYTES);
-            kern<<<grid, tc::NTHREADS, tc::SMEM_BYTES, st>>>(a);
+            scout_host::launch(kern, dim3(grid), dim3(tc::NTHREADS), tc::SMEM_BYTES, st, (a.flags & SCOUT_LAUNCH_PDL) != 0,
+                               a);
         };
         switch (a.group) {
             case 1: go(tc::sparse_decode_tc_kernel<1>); break;
