@@ -399,6 +399,11 @@ def main():
     except OSError:
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
+    traffic = None
+    try:  # dram read+write bytes per K2 launch from the committed ncu --set full capture
+        traffic = json.load(open(ROOT / "profiles" / "k2_traffic.json"))["bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        pass
     achieved = k2_bytes / (k2_avg / 1000.0) / 1e9
     step_bytes = sum(wl.k2_bytes(t) for t in res_tok_layers) + wl.L * wl.digest_bytes_layer
     step_gbs = step_bytes / (ms_step / 1000.0) / 1e9
@@ -431,7 +436,7 @@ def main():
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},
             "step_gbs": step_gbs,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "kernel": "sparse_decode_tc_kernel (K2+K3)",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "sparse_decode_tc_kernel (K2+K3)",
                          "bytes_per_launch": k2_bytes, "avg_launch_us": k2_avg * 1000.0,
                          "share_of_step": k2_share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"},
             "clocks": clk,
