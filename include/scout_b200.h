@@ -142,6 +142,12 @@ typedef struct scout_topk_args {
     int32_t* last_selected;
     double* scores_out;
     int flags;      /* SCOUT_LAUNCH_PDL: programmatic dependent launch */
+    /* optional completion flag: when every CTA has written its lists, the
+     * last one stores done_token to *done_flag (release, gpu scope);
+     * done_ctr is a zero-initialised counter it leaves zeroed */
+    unsigned* done_flag;
+    unsigned* done_ctr;
+    unsigned done_token;
 } scout_topk_args;
 
 int scout_score_topk_split(const scout_topk_args* args, void* stream);

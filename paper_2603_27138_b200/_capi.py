@@ -45,6 +45,7 @@ class TopkArgs(C.Structure):
         ("sel_ids", _vp), ("n_sel", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
         ("cpu_ids", _vp), ("n_cpu", _vp), ("res_tokens", _vp), ("cpu_tokens", _vp),
         ("last_selected", _vp), ("scores_out", _vp), ("flags", C.c_int),
+        ("done_flag", _vp), ("done_ctr", _vp), ("done_token", C.c_uint),
     ]
 
 

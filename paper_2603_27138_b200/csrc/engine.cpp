@@ -1,19 +1,32 @@
 // Host-side decode-step orchestration in C++ (the GPU side of
 // ScoutEngine::decode_step, reference proj/include/scout/engine.hpp:205-314).
 //
-// The engine owns only launch plumbing: per-layer K1 output buffers, the K2
-// workspace, a side stream + per-layer events for K4 recalls, copy streams and
-// double-buffered device staging for the host-buffer path, and an event pool
-// for K2 timing. Kernel launches go through the C ABI entry points; nothing
-// here allocates or synchronises inside a step.
+// One decode step = two concurrent streams plus two copy streams:
+//   K1 stream : K1(0) (true query; layer 0 is pinned resident, engine.hpp:227-233)
+//               then K1(i) for i >= 1 with the predicted query (engine.hpp:236-251),
+//               each publishing a device flag when its lists are written;
+//   caller's stream : ONE persistent K2 launch that walks all layers, polling
+//               the K1 flag of layer i before planning it (K1 CTAs co-reside
+//               with the K2 CTAs, so the two overlap on every SM);
+//   side stream : per-layer recall copies (copy engines) gated on the layer's
+//               K2 completion counter via cuStreamWaitValue32 (issued after the
+//               layer's attention, kv_store.hpp:175-197) and publishing a
+//               recall flag the next step's K2 waits on before it streams the
+//               layer (visible at (m+1, i), kv_store.hpp:201-218);
+//   h2d / d2h : the host-buffer path's pipelined input / output copies, also
+//               flag-gated per layer chunk.
+// K1 outputs are double-buffered by step parity; K2 workspaces are per layer.
+// Nothing here allocates or synchronises the host inside a step.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <cmath>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <vector>
 
 #include "../../include/scout_b200.h"
+#include "k2_step.h"
 
 namespace scout_host {
 void set_error(int code, const char* fmt, ...);
@@ -41,41 +54,70 @@ struct Buf {
         }                                                                                  \
     } while (0)
 
+// stream memory operations (driver API, resolved at run time)
+using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WaitValueFn g_wait = nullptr;
+WriteValueFn g_write = nullptr;
+
+bool load_stream_memops() {
+    if (g_wait && g_write) return true;
+    cudaDriverEntryPointQueryResult q1, q2;
+    void* f1 = nullptr;
+    void* f2 = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f1, cudaEnableDefault, &q1) != cudaSuccess ||
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &f2, cudaEnableDefault, &q2) != cudaSuccess || !f1 || !f2)
+        return false;
+    g_wait = reinterpret_cast<WaitValueFn>(f1);
+    g_write = reinterpret_cast<WriteValueFn>(f2);
+    return true;
+}
+
+int wait_value(cudaStream_t st, const unsigned* addr, unsigned v) {
+    if (g_wait(st, reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
+        scout_host::set_error(SCOUT_ERR_CUDA, "cuStreamWaitValue32 failed");
+        return SCOUT_ERR_CUDA;
+    }
+    return SCOUT_OK;
+}
+int write_value(cudaStream_t st, unsigned* addr, unsigned v) {
+    if (g_write(st, reinterpret_cast<CUdeviceptr>(addr), v, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+        scout_host::set_error(SCOUT_ERR_CUDA, "cuStreamWriteValue32 failed");
+        return SCOUT_ERR_CUDA;
+    }
+    return SCOUT_OK;
+}
+
 }  // namespace
 
 struct scout_engine {
     scout_engine_config cfg{};
     std::vector<scout_layer_desc> layers;
-    int U = 0, G = 0, UG = 0;
-    // per-layer K1 outputs
-    Buf sel_ids, n_sel, res_slots, res_ids, n_res, cpu_ids, n_cpu, res_tok, cpu_tok;
-    Buf ws;
-    size_t ws_bytes = 0;
-    // recall plumbing (plans copied at create: host arrays for the copy
-    // engines, device arrays for the SM gather kernel)
+    int U = 0, G = 0, UG = 0, grid = 0, nch = 0;
+    // per-layer K1 outputs, two sets (step parity)
+    Buf sel_ids[2], n_sel[2], res_slots[2], res_ids[2], n_res[2], cpu_ids[2], n_cpu[2], res_tok[2], cpu_tok[2];
+    Buf ws;  // per-layer K2 workspaces
+    size_t ws_layer = 0;
+    Buf flags;  // k1_flag[L] | k1_ctr[L] | recall_flag[L] | layer_done[L] | in_flag[nch]
+    unsigned *k1_flag = nullptr, *k1_ctr = nullptr, *recall_flag = nullptr, *layer_done = nullptr, *in_flag = nullptr;
+    unsigned token = 0;  // number of steps launched
+    std::vector<unsigned> rc_token;  // per layer: token of its last recall (0: none)
+    // recall plans (host arrays for the copy engines, device for the SM kernel)
     std::vector<std::vector<int64_t>> rc_src;
     std::vector<std::vector<int32_t>> rc_dst;
     std::vector<Buf> rc_dev;
-    cudaStream_t side = nullptr;
-    std::vector<cudaEvent_t> recall_ev;
-    std::vector<char> recall_pending;
-    cudaEvent_t ev_main = nullptr;
-    // host path
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    Buf stage[2];  // q_true | q_pred | cpu_o | cpu_ml | out_o | out_ml, per step parity
+    // streams / events
+    cudaStream_t k1s = nullptr, side = nullptr, h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_k1_end = nullptr, ev_tmp = nullptr;
+    cudaEvent_t ev_k2[2] = {nullptr, nullptr};
+    bool k2_recorded[2] = {false, false};
+    std::vector<cudaEvent_t> ev_k1;     // per layer: K1 done (host path: CPU-side id copies)
+    std::vector<cudaEvent_t> chunk_ev;  // host path: input chunk landed
+    // host path staging (per step parity): q_true | q_pred | cpu_o | cpu_ml | out_o | out_ml
+    Buf stage[2];
     cudaEvent_t stage_free[2] = {nullptr, nullptr};
-    std::vector<cudaEvent_t> chunk_ev;   // h2d chunk ready
-    std::vector<cudaEvent_t> done_ev;    // compute chunk done
-    cudaEvent_t k1_ev = nullptr;
-    bool pdl = false;  // programmatic dependent launch (off: K1 runs on its own stream)
-    // K1 runs one layer ahead on its own stream, co-resident with the
-    // persistent K2 CTAs (K1 fits in the shared memory K2 leaves free)
-    cudaStream_t k1s = nullptr;
-    std::vector<cudaEvent_t> ev_k1;     // K1(i) done  -> K2(i) may read its lists
-    std::vector<cudaEvent_t> ev_k2;     // K2(i) done  -> next step's K1(i) may overwrite them
-    std::vector<char> k2_recorded;
-    cudaEvent_t ev_start = nullptr;
-    // timing
+    bool stage_recorded[2] = {false, false};
+    // instrumentation
     bool timing = false;
     std::vector<cudaEvent_t> tev;
     size_t tev_used = 0;
@@ -83,28 +125,20 @@ struct scout_engine {
 
     size_t lk(int layer) const { return static_cast<size_t>(layer) * U * cfg.k; }
     size_t lu(int layer) const { return static_cast<size_t>(layer) * U; }
-    int32_t* I(Buf& b) const { return static_cast<int32_t*>(b.p); }
+    int32_t* I(const Buf& b) const { return static_cast<int32_t*>(b.p); }
 
     ~scout_engine() {
-        if (k1s) cudaStreamDestroy(k1s);
-        for (auto e : ev_k1) cudaEventDestroy(e);
-        for (auto e : ev_k2) cudaEventDestroy(e);
-        if (ev_start) cudaEventDestroy(ev_start);
-        if (side) cudaStreamDestroy(side);
-        if (h2d) cudaStreamDestroy(h2d);
-        if (d2h) cudaStreamDestroy(d2h);
-        for (auto e : recall_ev) cudaEventDestroy(e);
-        for (auto e : chunk_ev) cudaEventDestroy(e);
-        for (auto e : done_ev) cudaEventDestroy(e);
-        for (auto e : tev) cudaEventDestroy(e);
-        for (auto e : stage_free)
+        for (cudaStream_t s : {k1s, side, h2d, d2h})
+            if (s) cudaStreamDestroy(s);
+        for (cudaEvent_t e : {ev_start, ev_k1_end, ev_tmp, ev_k2[0], ev_k2[1], stage_free[0], stage_free[1]})
             if (e) cudaEventDestroy(e);
-        if (ev_main) cudaEventDestroy(ev_main);
-        if (k1_ev) cudaEventDestroy(k1_ev);
+        for (auto e : ev_k1) cudaEventDestroy(e);
+        for (auto e : chunk_ev) cudaEventDestroy(e);
+        for (auto e : tev) cudaEventDestroy(e);
     }
 
     // ---------------------------------------------------------------- K1
-    int select(int layer, const float* q, int step, cudaStream_t st) {
+    int select(int layer, const float* q, int step, int par, cudaStream_t st) {
         scout_topk_args a{};
         a.n_units = U;
         a.group = G;
@@ -118,26 +152,43 @@ struct scout_engine {
         a.digests = layers[layer].digests;
         a.n_tokens = cfg.n_tokens;
         a.block_table = layers[layer].block_table;
-        a.sel_ids = I(sel_ids) + lk(layer);
-        a.n_sel = I(n_sel) + lu(layer);
-        a.res_slots = I(res_slots) + lk(layer);
-        a.res_ids = I(res_ids) + lk(layer);
-        a.n_res = I(n_res) + lu(layer);
-        a.cpu_ids = I(cpu_ids) + lk(layer);
-        a.n_cpu = I(n_cpu) + lu(layer);
-        a.res_tokens = I(res_tok) + lu(layer);
-        a.cpu_tokens = I(cpu_tok) + lu(layer);
-        a.flags = pdl ? SCOUT_LAUNCH_PDL : 0;
+        a.sel_ids = I(sel_ids[par]) + lk(layer);
+        a.n_sel = I(n_sel[par]) + lu(layer);
+        a.res_slots = I(res_slots[par]) + lk(layer);
+        a.res_ids = I(res_ids[par]) + lk(layer);
+        a.n_res = I(n_res[par]) + lu(layer);
+        a.cpu_ids = I(cpu_ids[par]) + lk(layer);
+        a.n_cpu = I(n_cpu[par]) + lu(layer);
+        a.res_tokens = I(res_tok[par]) + lu(layer);
+        a.cpu_tokens = I(cpu_tok[par]) + lu(layer);
+        a.done_flag = k1_flag + layer;
+        a.done_ctr = k1_ctr + layer;
+        a.done_token = token;
         ++launches;
         return scout_score_topk_split(&a, st);
     }
 
-    // ------------------------------------------------------------- K2+K3
-    int attend(int layer, const float* q, const float* co, const float* cml, float* o, float* ml, cudaStream_t st) {
-        if (recall_pending[layer]) {
-            CU(cudaStreamWaitEvent(st, recall_ev[layer], 0));
-            recall_pending[layer] = 0;
-        }
+    // ---------------------------------------------------------------- K2
+    int launch_k2(int par, const float* const* q, const float* const* co, const float* const* cml, float* const* o,
+                  float* const* ml, const unsigned* const* inflag, cudaStream_t st) {
+        K2StepArgs a{};
+        a.n_units = U;
+        a.group = G;
+        a.k_stride = cfg.k;
+        a.n_layers = cfg.layers;
+        a.scale = cfg.scale;
+        a.kv_pool = cfg.kv_pool;
+        a.n_tokens = cfg.n_tokens;
+        a.workspace = ws.p;
+        a.ws_layer_bytes = ws_layer;
+        a.k1_flag = k1_flag;
+        a.recall_flag = recall_flag;
+        a.layer_done = layer_done;
+        a.token = token;
+        a.max_ctas = cfg.max_ctas;
+        for (int i = 0; i < cfg.layers; ++i)
+            a.layers[i] = K2Layer{q[i], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
+                                  co[i], cml[i], o[i], ml[i], inflag ? inflag[i] : nullptr, rc_token[i], 0u};
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timing) {
             while (tev.size() < tev_used + 2) {
@@ -149,83 +200,52 @@ struct scout_engine {
             e1 = tev[tev_used++];
             CU(cudaEventRecord(e0, st));
         }
-        scout_decode_args a{};
-        a.n_units = U;
-        a.group = G;
-        a.kv_dtype = cfg.kv_dtype;
-        a.k_stride = cfg.k;
-        a.scale = cfg.scale;
-        a.q = q;
-        a.kv_pool = cfg.kv_pool;
-        a.res_slots = I(res_slots) + lk(layer);
-        a.res_ids = I(res_ids) + lk(layer);
-        a.n_res = I(n_res) + lu(layer);
-        a.n_tokens = cfg.n_tokens;
-        a.cpu_o = co;
-        a.cpu_ml = cml;
-        a.o = o;
-        a.ml = ml;
-        a.workspace = ws.p;
-        a.workspace_bytes = ws_bytes;
-        a.max_ctas = cfg.max_ctas;
-        a.flags = pdl ? SCOUT_LAUNCH_PDL : 0;
         ++launches;
-        const int rc = scout_sparse_decode(&a, st);
+        const int rc = scout_k2_launch(a, st, false);
         if (rc != SCOUT_OK) return rc;
         if (timing) CU(cudaEventRecord(e1, st));
+        CU(cudaEventRecord(ev_k2[par], st));
+        k2_recorded[par] = true;
         return SCOUT_OK;
     }
 
     // ---------------------------------------------------------------- K4
-    int maybe_recall(int layer, int step, cudaStream_t st) {
-        const scout_layer_desc& L = layers[layer];
-        if (cfg.recall_interval <= 0 || L.recall_n <= 0 || !L.recall_src || !L.recall_dst) return SCOUT_OK;
-        if ((step + layer) % cfg.recall_interval != 0) return SCOUT_OK;
-        CU(cudaEventRecord(ev_main, st));  // issued after the layer's attention
-        CU(cudaStreamWaitEvent(side, ev_main, 0));
-        int rc;
-        if (cfg.recall_mode == 1) {
-            ++launches;
-            const int64_t* src = static_cast<const int64_t*>(rc_dev[layer].p);
-            const int32_t* dst = reinterpret_cast<const int32_t*>(src + L.recall_n);
-            rc = scout_recall_gather(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, src, dst, L.recall_n, side);
-        } else {
-            rc = scout_recall_copy(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, rc_src[layer].data(),
-                                   rc_dst[layer].data(), L.recall_n, side);
+    // recalls of this step: layer i recalls when (step + i) % interval == 0;
+    // the copy waits for every CTA to finish layer i of this launch
+    int issue_recalls(int step) {
+        if (cfg.recall_interval <= 0) return SCOUT_OK;
+        for (int i = 0; i < cfg.layers; ++i) {
+            const scout_layer_desc& L = layers[i];
+            if (L.recall_n <= 0 || rc_src[i].empty() || (step + i) % cfg.recall_interval != 0) continue;
+            int rc = wait_value(side, layer_done + i, token * static_cast<unsigned>(grid));
+            if (rc != SCOUT_OK) return rc;
+            if (cfg.recall_mode == 1) {
+                ++launches;
+                const int64_t* src = static_cast<const int64_t*>(rc_dev[i].p);
+                const int32_t* dst = reinterpret_cast<const int32_t*>(src + L.recall_n);
+                rc = scout_recall_gather(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, src, dst, L.recall_n, side);
+            } else {
+                rc = scout_recall_copy(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, rc_src[i].data(), rc_dst[i].data(),
+                                       L.recall_n, side);
+            }
+            if (rc != SCOUT_OK) return rc;
+            if ((rc = write_value(side, recall_flag + i, token)) != SCOUT_OK) return rc;
+            rc_token[i] = token;  // the next step's K2 waits for it before streaming layer i
         }
-        if (rc != SCOUT_OK) return rc;
-        CU(cudaEventRecord(recall_ev[layer], side));
-        recall_pending[layer] = 1;
         return SCOUT_OK;
     }
 
-    // K1(i) on the K1 stream (after the previous step's K2(i) released layer
-    // i's lists), K2(i) on the caller's stream after K1(i).
-    int k1_layer(int i, const float* q, int step) {
-        if (k2_recorded[i]) CU(cudaStreamWaitEvent(k1s, ev_k2[i], 0));
-        const int rc = select(i, q, step, k1s);
-        if (rc != SCOUT_OK) return rc;
-        CU(cudaEventRecord(ev_k1[i], k1s));
-        return SCOUT_OK;
-    }
-    int k2_layer(int i, int step, const float* qt, const float* co, const float* cml, float* o, float* ml,
-                 cudaStream_t st) {
-        CU(cudaStreamWaitEvent(st, ev_k1[i], 0));
-        int rc = attend(i, qt, co, cml, o, ml, st);
-        if (rc != SCOUT_OK) return rc;
-        CU(cudaEventRecord(ev_k2[i], st));
-        k2_recorded[i] = 1;
-        return maybe_recall(i, step, st);
-    }
-    // inputs written to `st` before the step are visible to the K1 stream
-    int begin_step(cudaStream_t st) {
+    // K1 lists of this parity were read by the K2 two steps back: wait for it;
+    // inputs recorded on `st` before the step are visible to the K1 stream
+    int begin_step(cudaStream_t st, int par) {
         CU(cudaEventRecord(ev_start, st));
         CU(cudaStreamWaitEvent(k1s, ev_start, 0));
+        if (k2_recorded[par]) CU(cudaStreamWaitEvent(k1s, ev_k2[par], 0));
         return SCOUT_OK;
     }
     int end_step(cudaStream_t st) {
-        CU(cudaEventRecord(ev_start, k1s));
-        CU(cudaStreamWaitEvent(st, ev_start, 0));
+        CU(cudaEventRecord(ev_k1_end, k1s));
+        CU(cudaStreamWaitEvent(st, ev_k1_end, 0));
         return SCOUT_OK;
     }
 };
@@ -238,14 +258,18 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     const scout_engine_config& c = *cfg;
-    if (c.layers <= 0 || c.batch <= 0 || c.hkv <= 0 || c.hq % c.hkv != 0 || c.k <= 0 || c.nb_stride <= 0 ||
-        !c.kv_pool || !c.n_tokens || !(c.scale > 0.f)) {
-        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config");
+    if (c.layers <= 0 || c.layers > K2_MAX_LAYERS || c.batch <= 0 || c.hkv <= 0 || c.hq % c.hkv != 0 || c.k <= 0 ||
+        c.nb_stride <= 0 || !c.kv_pool || !c.n_tokens || !(c.scale > 0.f) || c.kv_dtype != SCOUT_BF16) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 KV)", K2_MAX_LAYERS);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     if (c.recall_interval > 0 && !c.host_tier) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: recall needs a host tier");
         return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (!load_stream_memops()) {
+        set_error(SCOUT_ERR_UNSUPPORTED, "scout_engine_create: driver lacks stream memory operations");
+        return SCOUT_ERR_UNSUPPORTED;
     }
     auto* e = new (std::nothrow) scout_engine();
     if (!e) {
@@ -258,15 +282,22 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     e->U = c.batch * c.hkv;
     e->G = c.hq / c.hkv;
     e->UG = e->U * e->G;
+    e->grid = scout_k2_grid(e->U, c.k, c.max_ctas);
+    e->nch = (c.layers + e->cfg.chunk_layers - 1) / e->cfg.chunk_layers;
     const size_t lk = static_cast<size_t>(c.layers) * e->U * c.k * 4, lu = static_cast<size_t>(c.layers) * e->U * 4;
-    int bad = e->sel_ids.alloc(lk) | e->res_slots.alloc(lk) | e->res_ids.alloc(lk) | e->cpu_ids.alloc(lk) |
-              e->n_sel.alloc(lu) | e->n_res.alloc(lu) | e->n_cpu.alloc(lu) | e->res_tok.alloc(lu) |
-              e->cpu_tok.alloc(lu);
-    e->ws_bytes = scout_sparse_decode_workspace_bytes(e->U, e->G, c.max_ctas);
-    bad |= e->ws.alloc(e->ws_bytes);
-    if (!bad && cudaMemset(e->ws.p, 0, e->ws_bytes) != cudaSuccess) bad = 1;
+    int bad = 0;
+    for (int p = 0; p < 2; ++p)
+        bad |= e->sel_ids[p].alloc(lk) | e->res_slots[p].alloc(lk) | e->res_ids[p].alloc(lk) |
+               e->cpu_ids[p].alloc(lk) | e->n_sel[p].alloc(lu) | e->n_res[p].alloc(lu) | e->n_cpu[p].alloc(lu) |
+               e->res_tok[p].alloc(lu) | e->cpu_tok[p].alloc(lu);
+    e->ws_layer = scout_k2_ws_layer_bytes(e->U, e->grid);
+    bad |= e->ws.alloc(e->ws_layer * c.layers);
+    const size_t nflags = 4 * static_cast<size_t>(c.layers) + e->nch;
+    bad |= e->flags.alloc(nflags * 4);
+    if (!bad && (cudaMemset(e->ws.p, 0, e->ws_layer * c.layers) != cudaSuccess ||
+                 cudaMemset(e->flags.p, 0, nflags * 4) != cudaSuccess))
+        bad = 1;
     if (!bad && c.host_staging) {
-        // q_true | q_pred | cpu_o | cpu_ml | out_o | out_ml, per step parity
         const size_t per = static_cast<size_t>(c.layers) * e->UG * (4 * SCOUT_HEAD_DIM + 4) * 4;
         bad |= e->stage[0].alloc(per) | e->stage[1].alloc(per);
     }
@@ -275,22 +306,13 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         set_error(SCOUT_ERR_CUDA, "scout_engine_create: device allocation failed");
         return SCOUT_ERR_CUDA;
     }
-    cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&e->k1s, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&e->ev_start, cudaEventDisableTiming);
-    e->ev_k1.resize(c.layers);
-    e->ev_k2.resize(c.layers);
-    for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    for (auto& ev : e->ev_k2) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    e->k2_recorded.assign(c.layers, 0);
-    cudaStreamCreateWithFlags(&e->h2d, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&e->d2h, cudaStreamNonBlocking);
-    cudaEventCreateWithFlags(&e->ev_main, cudaEventDisableTiming);
-    cudaEventCreateWithFlags(&e->k1_ev, cudaEventDisableTiming);
-    for (int i = 0; i < 2; ++i) cudaEventCreateWithFlags(&e->stage_free[i], cudaEventDisableTiming);
-    e->recall_ev.resize(c.layers);
-    for (auto& ev : e->recall_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    e->recall_pending.assign(c.layers, 0);
+    auto* f = static_cast<unsigned*>(e->flags.p);
+    e->k1_flag = f;
+    e->k1_ctr = f + c.layers;
+    e->recall_flag = f + 2 * c.layers;
+    e->layer_done = f + 3 * c.layers;
+    e->in_flag = f + 4 * c.layers;
+    e->rc_token.assign(c.layers, 0u);
     e->rc_src.resize(c.layers);
     e->rc_dst.resize(c.layers);
     e->rc_dev = std::vector<Buf>(c.layers);
@@ -311,11 +333,14 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
             }
         }
     }
-    const int nch = (c.layers + e->cfg.chunk_layers - 1) / e->cfg.chunk_layers;
-    e->chunk_ev.resize(nch);
-    e->done_ev.resize(nch);
+    for (cudaStream_t* s : {&e->k1s, &e->side, &e->h2d, &e->d2h}) cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    for (cudaEvent_t* ev : {&e->ev_start, &e->ev_k1_end, &e->ev_tmp, &e->ev_k2[0], &e->ev_k2[1], &e->stage_free[0],
+                            &e->stage_free[1]})
+        cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    e->ev_k1.resize(c.layers);
+    for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    e->chunk_ev.resize(e->nch);
     for (auto& ev : e->chunk_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    for (auto& ev : e->done_ev) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) {
         delete e;
@@ -327,6 +352,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
 }
 
 extern "C" int scout_engine_destroy(scout_engine* eng) {
+    if (eng) cudaDeviceSynchronize();  // flags / copies still reference engine memory
     delete eng;
     return SCOUT_OK;
 }
@@ -341,14 +367,23 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const float* 
     auto st = static_cast<cudaStream_t>(stream);
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
     const int L = e->cfg.layers;
-    int rc = e->begin_step(st);
-    // K1 runs ahead: layer 0 with the true query, layer i+1 with the predicted one
-    for (int i = 0; i < L && rc == SCOUT_OK; ++i) {
-        rc = e->k1_layer(i, i == 0 ? q_true : q_pred + i * qd, step);
-        if (rc == SCOUT_OK) rc = e->k2_layer(i, step, q_true + i * qd, cpu_o ? cpu_o + i * qd : nullptr,
-                                             cpu_ml ? cpu_ml + i * md : nullptr, out_o + i * qd, out_ml + i * md, st);
-    }
+    const unsigned token = ++e->token;
+    const int par = token & 1;
+    int rc = e->begin_step(st, par);
+    for (int i = 0; i < L && rc == SCOUT_OK; ++i) rc = e->select(i, i == 0 ? q_true : q_pred + i * qd, step, par, e->k1s);
     if (rc != SCOUT_OK) return rc;
+    std::vector<const float*> q(L), co(L), cml(L);
+    std::vector<float*> o(L), ml(L);
+    for (int i = 0; i < L; ++i) {
+        q[i] = q_true + i * qd;
+        co[i] = cpu_o ? cpu_o + i * qd : nullptr;
+        cml[i] = cpu_ml ? cpu_ml + i * md : nullptr;
+        o[i] = out_o + i * qd;
+        ml[i] = out_ml + i * md;
+    }
+    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, st)) != SCOUT_OK)
+        return rc;
+    if ((rc = e->issue_recalls(step)) != SCOUT_OK) return rc;
     return e->end_step(st);
 }
 
@@ -362,17 +397,21 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     auto st = static_cast<cudaStream_t>(stream);
-    const int L = e->cfg.layers, CH = e->cfg.chunk_layers;
-    const int nch = (L + CH - 1) / CH;
+    const int L = e->cfg.layers, CH = e->cfg.chunk_layers, nch = e->nch;
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
-    const int par = step & 1;
-    float* base = static_cast<float*>(e->stage[par].p);
-    float* d_qt = base;
+    const unsigned token = ++e->token;
+    const int par = token & 1;
+    float* d_qt = static_cast<float*>(e->stage[par].p);
     float* d_qp = d_qt + L * qd;
     float* d_co = d_qp + L * qd;
     float* d_cm = d_co + L * qd;
-    // staging of this parity is free once the step two steps back finished
-    CU(cudaStreamWaitEvent(e->h2d, e->stage_free[par], 0));
+    float* d_o = d_cm + L * md;
+    float* d_oml = d_o + L * qd;
+    int rc = e->begin_step(st, par);
+    if (rc != SCOUT_OK) return rc;
+    // ---- inputs: chunked H2D; each chunk publishes a flag (K2) and an event (K1)
+    if (e->stage_recorded[par]) CU(cudaStreamWaitEvent(e->h2d, e->stage_free[par], 0));
+    CU(cudaStreamWaitEvent(e->h2d, e->ev_start, 0));
     for (int c = 0; c < nch; ++c) {
         const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
         CU(cudaMemcpyAsync(d_qt + lo * qd, h_q_true + lo * qd, n * qd * 4, cudaMemcpyHostToDevice, e->h2d));
@@ -382,58 +421,59 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
             CU(cudaMemcpyAsync(d_cm + lo * md, h_cpu_ml + lo * md, n * md * 4, cudaMemcpyHostToDevice, e->h2d));
         }
         CU(cudaEventRecord(e->chunk_ev[c], e->h2d));
+        if ((rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
     }
-    float* d_o = d_cm + L * md;   // outputs: [L][UG][128] then [L][UG][2]
-    float* d_oml = d_o + L * qd;
-    // K1 stream: waits for each input chunk, runs one layer ahead of K2
-    int rc = e->begin_step(st);
-    if (rc != SCOUT_OK) return rc;
+    // ---- K1 stream, layer by layer as the chunks land; CPU-side ids out right after
     for (int i = 0; i < L; ++i) {
-        if (i % CH == 0) {
-            CU(cudaStreamWaitEvent(st, e->chunk_ev[i / CH], 0));
-            CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[i / CH], 0));
-        }
-        rc = e->k1_layer(i, i == 0 ? d_qt : d_qp + i * qd, step);
-        if (rc != SCOUT_OK) return rc;
-        if (h_cpu_ids && i > 0) {
+        if (i % CH == 0) CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[i / CH], 0));
+        if ((rc = e->select(i, i == 0 ? d_qt : d_qp + i * qd, step, par, e->k1s)) != SCOUT_OK) return rc;
+        if (h_cpu_ids) {
             // the host co-attention worker needs layer i's CPU-side ids as soon as K1(i) is done
+            CU(cudaEventRecord(e->ev_k1[i], e->k1s));
             CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[i], 0));
-            CU(cudaMemcpyAsync(h_cpu_ids + e->lk(i), e->I(e->cpu_ids) + e->lk(i),
+            CU(cudaMemcpyAsync(h_cpu_ids + e->lk(i), e->I(e->cpu_ids[par]) + e->lk(i),
                                static_cast<size_t>(e->U) * e->cfg.k * 4, cudaMemcpyDeviceToHost, e->d2h));
             if (h_n_cpu)
-                CU(cudaMemcpyAsync(h_n_cpu + e->lu(i), e->I(e->n_cpu) + e->lu(i), static_cast<size_t>(e->U) * 4,
+                CU(cudaMemcpyAsync(h_n_cpu + e->lu(i), e->I(e->n_cpu[par]) + e->lu(i), static_cast<size_t>(e->U) * 4,
                                    cudaMemcpyDeviceToHost, e->d2h));
         }
-        rc = e->k2_layer(i, step, d_qt + i * qd, h_cpu_o ? d_co + i * qd : nullptr, h_cpu_ml ? d_cm + i * md : nullptr,
-                         d_o + i * qd, d_oml + i * md, st);
-        if (rc != SCOUT_OK) return rc;
-        if (i % CH == CH - 1 || i == L - 1) {
-            const int c = i / CH, lo = c * CH, n = i + 1 - lo;
-            CU(cudaEventRecord(e->done_ev[c], st));
-            CU(cudaStreamWaitEvent(e->d2h, e->done_ev[c], 0));
-            CU(cudaMemcpyAsync(h_out_o + lo * qd, d_o + lo * qd, n * qd * 4, cudaMemcpyDeviceToHost, e->d2h));
-            CU(cudaMemcpyAsync(h_out_ml + lo * md, d_oml + lo * md, n * md * 4, cudaMemcpyDeviceToHost, e->d2h));
-        }
     }
+    // ---- K2: one launch; layer i waits for its input chunk's flag on the device
+    std::vector<const float*> q(L), co(L), cml(L);
+    std::vector<float*> o(L), ml(L);
+    std::vector<const unsigned*> inflag(L);
+    for (int i = 0; i < L; ++i) {
+        q[i] = d_qt + i * qd;
+        co[i] = h_cpu_o ? d_co + i * qd : nullptr;
+        cml[i] = h_cpu_ml ? d_cm + i * md : nullptr;
+        o[i] = d_o + i * qd;
+        ml[i] = d_oml + i * md;
+        inflag[i] = e->in_flag + i / CH;
+    }
+    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), st)) != SCOUT_OK)
+        return rc;
+    if ((rc = e->issue_recalls(step)) != SCOUT_OK) return rc;
+    // ---- outputs: each chunk leaves once every CTA finished its last layer
+    for (int c = 0; c < nch; ++c) {
+        const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
+        if ((rc = wait_value(e->d2h, e->layer_done + lo + n - 1, token * static_cast<unsigned>(e->grid))) != SCOUT_OK)
+            return rc;
+        CU(cudaMemcpyAsync(h_out_o + lo * qd, d_o + lo * qd, n * qd * 4, cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaMemcpyAsync(h_out_ml + lo * md, d_oml + lo * md, n * md * 4, cudaMemcpyDeviceToHost, e->d2h));
+    }
+    CU(cudaEventRecord(e->ev_tmp, e->d2h));
+    CU(cudaStreamWaitEvent(st, e->ev_tmp, 0));
     if ((rc = e->end_step(st)) != SCOUT_OK) return rc;
-    if (h_cpu_ids) {  // layer 0's ids (selected on the true query; layer 0 is pinned so none)
-        CU(cudaMemcpyAsync(h_cpu_ids, e->I(e->cpu_ids), static_cast<size_t>(e->U) * e->cfg.k * 4,
-                           cudaMemcpyDeviceToHost, e->d2h));
-        if (h_n_cpu)
-            CU(cudaMemcpyAsync(h_n_cpu, e->I(e->n_cpu), static_cast<size_t>(e->U) * 4, cudaMemcpyDeviceToHost, e->d2h));
-    }
-    CU(cudaEventRecord(e->ev_main, e->d2h));
-    CU(cudaStreamWaitEvent(st, e->ev_main, 0));
     CU(cudaEventRecord(e->stage_free[par], st));
+    e->stage_recorded[par] = true;
     return SCOUT_OK;
 }
 
 extern "C" int scout_engine_sync(scout_engine* e, void* stream) {
     if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
-    CU(cudaEventRecord(e->ev_main, e->side));
-    CU(cudaStreamWaitEvent(st, e->ev_main, 0));
-    std::fill(e->recall_pending.begin(), e->recall_pending.end(), 0);
+    CU(cudaEventRecord(e->ev_tmp, e->side));
+    CU(cudaStreamWaitEvent(st, e->ev_tmp, 0));
     return SCOUT_OK;
 }
 
@@ -465,12 +505,13 @@ extern "C" int scout_engine_k1_outputs(scout_engine* e, int32_t** res_slots, int
                                        int32_t** cpu_ids, int32_t** n_cpu, int32_t** res_tokens,
                                        int32_t** cpu_tokens) {
     if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
-    if (res_slots) *res_slots = e->I(e->res_slots);
-    if (res_ids) *res_ids = e->I(e->res_ids);
-    if (n_res) *n_res = e->I(e->n_res);
-    if (cpu_ids) *cpu_ids = e->I(e->cpu_ids);
-    if (n_cpu) *n_cpu = e->I(e->n_cpu);
-    if (res_tokens) *res_tokens = e->I(e->res_tok);
-    if (cpu_tokens) *cpu_tokens = e->I(e->cpu_tok);
+    const int par = e->token & 1;  // the lists of the last step launched
+    if (res_slots) *res_slots = e->I(e->res_slots[par]);
+    if (res_ids) *res_ids = e->I(e->res_ids[par]);
+    if (n_res) *n_res = e->I(e->n_res[par]);
+    if (cpu_ids) *cpu_ids = e->I(e->cpu_ids[par]);
+    if (n_cpu) *n_cpu = e->I(e->n_cpu[par]);
+    if (res_tokens) *res_tokens = e->I(e->res_tok[par]);
+    if (cpu_tokens) *cpu_tokens = e->I(e->cpu_tok[par]);
     return SCOUT_OK;
 }

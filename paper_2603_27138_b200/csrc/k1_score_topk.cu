@@ -480,6 +480,17 @@ __global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk
             if (a.res_tokens) a.res_tokens[u] = s_tok[0];
             if (a.cpu_tokens) a.cpu_tokens[u] = s_tok[1];
         }
+        if (a.done_flag) {
+            // grid-wide completion: the last CTA publishes the flag a
+            // concurrently running K2 polls (ld.acquire) before reading the lists
+            __threadfence();
+            const unsigned old = atomicAdd(a.done_ctr, 1u);
+            if (old == gridDim.x - 1) {
+                *a.done_ctr = 0u;
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done_flag), "r"(a.done_token) : "memory");
+            }
+        }
     }
 }
 

@@ -8,17 +8,21 @@
 // query heads of a KV head share one pass over its selected K/V blocks (the
 // reference, single-head, re-reads K/V per head).
 //
-// bf16 path (the hot one), per persistent CTA (one per SM):
-//   * work balance ("stream-K"): the concatenation of every unit's resident
-//     block list is cut into gridDim.x equal ranges; a range covers pieces
+// bf16 path (the hot one): one persistent CTA per SM that walks a whole
+// decode step's layers (the engine's launch) or one layer (the C ABI):
+//   * per layer, work balance ("stream-K"): the concatenation of every unit's
+//     resident block list is cut into equal ranges; a range covers pieces
 //     ("segments") of one or more units. Segment (cta c, unit u) owns partial
 //     slot c+u; the last CTA to finish a unit (atomic counter) LSE-merges the
-//     unit's segment partials and the CPU co-attention partial.
-//   * one producer warp streams 32-token half blocks (8 KiB K + 8 KiB V) with
-//     1-D bulk async copies (TMA engine) into a 12-stage mbarrier ring;
-//   * NC consumer warps take half blocks round robin and run both GEMMs on the
-//     tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate) in a transposed
-//     form that wastes no rows at G=8:
+//     unit's segment partials and the CPU co-attention partial;
+//   * a planner/producer warp builds layer L+1's plan while layer L computes
+//     (double-buffered) and streams each 32 KiB block with one 1-D bulk copy
+//     (TMA engine) into an mbarrier ring that never drains between layers;
+//     it waits on device flags for K1's lists (K1 runs concurrently on
+//     another stream) and for recalls landed;
+//   * six consumer warps (three pairs, one 32-token half each) run both GEMMs
+//     on the tensor cores (mma.sync m16n8k16 bf16, fp32 accumulate) in a
+//     transposed form that wastes no rows at G=8:
 //        S^T[32 tok x 8 heads] = K[32 x 128] . Q^T      (q split hi+lo bf16)
 //        O^T[128 x 8 heads]   += V^T[128 x 32] . P^T    (P^T via movmatrix)
 //     with the online-softmax state per head in registers (log2 domain).
@@ -42,73 +46,86 @@ constexpr int SIMPLE_SPLIT = 8;
 constexpr int GRID_CAP = 1024;
 
 __host__ __device__ inline size_t ctr_bytes(int n_units) { return ((static_cast<size_t>(n_units) * 4 + 255) / 256) * 256; }
+}  // namespace
+
+#include "k2_step.h"
+
+namespace {
 
 // =========================================================== bf16 kernel ==
-#ifdef SCOUT_K2_TIMING
-__device__ unsigned long long g_k2_ts[1024][6];
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-#define K2TS(i) do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_k2_ts[blockIdx.x][i] = gtime(); } while (0)
-#define K2TS_T(i, tid_) do { if (threadIdx.x == (tid_) && blockIdx.x < 1024) g_k2_ts[blockIdx.x][i] = gtime(); } while (0)
-#else
-#define K2TS(i) do {} while (0)
-#define K2TS_T(i, tid_) do {} while (0)
-#endif
-
 namespace tc {
 // One stage = one whole 32 KiB block (K tile then V tile): a single bulk copy,
 // the transfer size at which random gathers get the most out of HBM3e
 // (tools/microbench/gather.cu: 2x8 KiB 5.1, 16 KiB 5.9, 32 KiB 6.7 TB/s).
 // Consumer warps work in pairs: warp 2p+h takes 32-token half h of every
-// block j with j % NPAIR == p; pair p double-buffers its own stages p and
-// p + NPAIR, so every stage is filled and drained in order by one pair.
+// block j (CTA-global stream index, continuing across layers) with
+// j % NPAIR == p; pair p double-buffers its own stages p and p + NPAIR, so
+// every stage is filled and drained in order by one pair.
 constexpr int NPAIR = 3;
 constexpr int NC = 2 * NPAIR;               // consumer warps
 constexpr int NCT = NC * 32;                // consumer threads
-constexpr int NTHREADS = NCT + 32;          // + 1 producer warp
+constexpr int NTHREADS = NCT + 32;          // + 1 producer / planner warp
 constexpr int NST = 2 * NPAIR;              // ring stages
 constexpr int STAGE_BYTES = 32768;          // one block: K tile (16 KiB) + V tile (16 KiB)
-constexpr int MAXSEG = 128;
-constexpr int MAXB = 512;                   // blocks per CTA range (staged in smem)
+constexpr int MAXSEG = 64;                  // units touched by one CTA range
+constexpr int MAXB = 384;                   // blocks per CTA range per layer
 constexpr int CB_ROW = D + 4;               // combine rows (bank-conflict pad)
 constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES;
 static_assert(8 * CB_ROW * 4 + 64 <= HALF_BYTES_BF16, "a warp's combine area must fit in its K half");
 
 struct Seg {
-    int unit, j0, j1, nseg, cfirst, f0;  // f0: first block in the CTA list
+    int unit, j0, j1, nseg, cfirst, f0;  // f0: first block of the segment in the layer's CTA list
+};
+
+// A layer's work list for this CTA, built by the planner warp one layer ahead
+// (double-buffered), consumed by the consumer warps.
+struct Plan {
+    Seg segs[MAXSEG];
+    int blk_slot[MAXB];      // resident blocks in stream order: pool slot
+    int16_t blk_rows[MAXB];  // valid rows (64, or the open block's fill)
+    int nsegs, nblk, jbase, pad;
 };
 
 struct Smem {
     uint64_t full[NST];
     uint64_t empty[NST];
-    Seg segs[MAXSEG];
-    int blk_slot[MAXB];        // the CTA's resident blocks in stream order: pool slot
-    int16_t blk_rows[MAXB];    // valid rows (64, or the open block's fill)
-    int warp_area[NC];         // byte offset of a warp's combine area, -1: no state
-    int nsegs;
-    int scan_tot[NTHREADS / 32];
+    uint64_t plan_full[2];
+    uint64_t plan_empty[2];
+    Plan plan[2];
+    int warp_area[NC];   // byte offset of a warp's combine area, -1: no state
     int last_flag;
-    long long run_total;
 };
 
 __device__ __forceinline__ int stage_of(int j) { return (j % NPAIR) + NPAIR * ((j / NPAIR) & 1); }
 
-__device__ __forceinline__ int unit_nb(const scout_decode_args& a, int u, int* tail) {
-    const int nt = a.n_tokens[u];
-    const int nb = (nt + BS - 1) / BS;
-    *tail = nt - (nb - 1) * BS;
-    return nb;
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Spin until *p >= token (wrap-safe). A flag that never arrives (a producer
+// that cannot be scheduled) traps after 10 s instead of hanging the device.
+__device__ __forceinline__ void wait_flag(const unsigned* p, unsigned token) {
+    if (p == nullptr) return;
+    if (static_cast<int>(ld_acquire(p) - token) >= 0) return;
+    const unsigned long long t0 = global_ns();
+    while (static_cast<int>(ld_acquire(p) - token) < 0) {
+        __nanosleep(256);
+        if (global_ns() - t0 > 10000000000ull) __trap();
+    }
 }
 
 // Merge n partial slots (+ the optional CPU partial) of unit u into the
 // outputs (merge / finalize, attention.hpp:100-122; both empty -> zeros,
 // engine.hpp:273). NT threads cover 8 heads x 32 lanes x 4 channels.
 template <int G, int NT>
-__device__ void finalize_unit(const scout_decode_args& a, int u, const float* parts, int first_slot, int nslots,
-                              int ctid) {
+__device__ void finalize_unit(const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml, int u,
+                              const float* parts, int first_slot, int nslots, int ctid) {
     for (int idx = ctid; idx < 8 * 32; idx += NT) {
         const int h = idx >> 5;
         const int d0 = (idx & 31) * 4;
@@ -120,9 +137,9 @@ __device__ void finalize_unit(const scout_decode_args& a, int u, const float* pa
             M = fmaxf(M, __ldcg(p + D));
         }
         float cm = -CUDART_INF_F, cl = 0.f;
-        if (a.cpu_ml) {
-            cm = a.cpu_ml[head * 2] * LOG2E;
-            cl = a.cpu_ml[head * 2 + 1];
+        if (cpu_ml) {
+            cm = cpu_ml[head * 2] * LOG2E;
+            cl = cpu_ml[head * 2 + 1];
             if (cl > 0.f) M = fmaxf(M, cm);
         }
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -140,142 +157,150 @@ __device__ void finalize_unit(const scout_decode_args& a, int u, const float* pa
             if (cl > 0.f) {
                 const float w = cl * exp2f(cm - M);
                 L += w;
-                const float4 co = *reinterpret_cast<const float4*>(a.cpu_o + head * D + d0);
+                const float4 co = *reinterpret_cast<const float4*>(cpu_o + head * D + d0);
                 acc.x += w * co.x; acc.y += w * co.y; acc.z += w * co.z; acc.w += w * co.w;
             }
         }
         const float inv = L > 0.f ? 1.f / L : 0.f;
-        *reinterpret_cast<float4*>(a.o + head * D + d0) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+        *reinterpret_cast<float4*>(out_o + head * D + d0) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
         if ((idx & 31) == 0) {
-            a.ml[head * 2] = L > 0.f ? M * LN2 : -CUDART_INF_F;
-            a.ml[head * 2 + 1] = L;
+            out_ml[head * 2] = L > 0.f ? M * LN2 : -CUDART_INF_F;
+            out_ml[head * 2 + 1] = L;
         }
     }
 }
 
+// Planner (one warp): this CTA's share of layer io's resident blocks.
+// Stream-K: the concatenation of every unit's resident block list is cut into
+// geff = min(grid, T) equal ranges (every range non-empty, so a unit's segment
+// count is the number of CTAs between the ones holding its first and last
+// block); segment (cta c, unit u) owns partial slot c+u.
+__device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int jbase, int lane) {
+    const int nunits = a.n_units;
+    long long T = 0;
+    {
+        int loc = 0;
+        for (int u = lane; u < nunits; u += 32) loc += io.n_res[u];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+        T = loc;
+    }
+    const long long grid = T < static_cast<long long>(gridDim.x) ? (T > 0 ? T : 1) : gridDim.x;
+    const long long c = blockIdx.x;
+    const long long lo = c < grid ? T * c / grid : T, hi = c < grid ? T * (c + 1) / grid : T;
+    long long run = 0;
+    int nseg = 0, frun = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    for (int base = 0; base < nunits; base += 32) {
+        const int u = base + lane;
+        const int n = u < nunits ? io.n_res[u] : 0;
+        int incl = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const long long pre = run + incl - n;
+        const long long s0 = max(pre, lo), s1 = min(pre + n, hi);
+        const bool has = n > 0 && s0 < s1;
+        const int len = has ? static_cast<int>(s1 - s0) : 0;
+        int lincl = len;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, lincl, o);
+            if (lane >= o) lincl += y;
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (has) {
+            const int pos = nseg + __popc(bal & lt);
+            const long long cf = ((pre + 1) * grid - 1) / T;  // CTA holding position p: floor(((p+1)*grid-1)/T)
+            const long long cl = ((pre + n) * grid - 1) / T;
+            if (pos < MAXSEG)
+                P.segs[pos] = Seg{u, static_cast<int>(s0 - pre), static_cast<int>(s1 - pre),
+                                  static_cast<int>(cl - cf + 1), static_cast<int>(cf), frun + lincl - len};
+        }
+        nseg += __popc(bal);
+        frun += __shfl_sync(0xffffffffu, lincl, 31);
+        run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    nseg = min(nseg, MAXSEG);
+    const int nblk = min(static_cast<int>(hi - lo), MAXB);
+    __syncwarp();
+    for (int f = lane; f < nblk; f += 32) {
+        int si = 0;
+        while (si + 1 < nseg && P.segs[si + 1].f0 <= f) ++si;
+        const Seg sg = P.segs[si];
+        const size_t idx = static_cast<size_t>(sg.unit) * a.k_stride + sg.j0 + (f - sg.f0);
+        const int nt = a.n_tokens[sg.unit];
+        const int nb = (nt + BS - 1) / BS;
+        P.blk_slot[f] = io.res_slots[idx];
+        P.blk_rows[f] = static_cast<int16_t>((io.res_ids[idx] == nb - 1) ? nt - (nb - 1) * BS : BS);
+    }
+    if (lane == 0) {
+        P.nsegs = nseg;
+        P.nblk = nblk;
+        P.jbase = jbase;
+    }
+    __syncwarp();
+}
+
 template <int G>
-__global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const scout_decode_args a) {
+__global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2StepArgs a) {
     extern __shared__ __align__(1024) uint8_t dsmem[];
     __shared__ Smem sm;
     uint8_t* stages = dsmem;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nunits = a.n_units;
-    const int ks = a.k_stride;
-    int* ctr = reinterpret_cast<int*>(a.workspace);
-    float* parts = reinterpret_cast<float*>(static_cast<uint8_t*>(a.workspace) + ctr_bytes(nunits));
-    K2TS(0);
 
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 2);  // both warps of the owning pair release
         }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sm.plan_full[i], 1);
+            mbar_init(&sm.plan_empty[i], 1);
+        }
         fence_mbar_init();
-        sm.nsegs = 0;
-        sm.run_total = 0;
     }
-    // PDL: K1's lists (n_res, res_slots, res_ids) are complete past this point
+    // PDL (single-layer launches): inputs from the preceding kernel are
+    // complete past this point
     griddep_wait();
     griddep_launch_dependents();
     __syncthreads();
 
-    // ---- pass 1: total resident blocks T
-    long long T = 0;
-    {
-        int loc = 0;
-        for (int u = tid; u < nunits; u += NTHREADS) loc += a.n_res[u];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
-        if (lane == 0) sm.scan_tot[warp] = loc;
-        __syncthreads();
-        for (int w = 0; w < NTHREADS / 32; ++w) T += sm.scan_tot[w];
-        __syncthreads();
-    }
-    // Ranges are cut over geff = min(grid, T) CTAs so that every range is
-    // non-empty: a unit's segment count is then the number of CTAs between
-    // the ones holding its first and last block. CTAs >= geff only do the
-    // zero-length-unit duty at the end.
-    const long long grid = T < static_cast<long long>(gridDim.x) ? (T > 0 ? T : 1) : gridDim.x;
-    const long long c = blockIdx.x;
-    const long long lo = c < grid ? T * c / grid : T, hi = c < grid ? T * (c + 1) / grid : T;
-
-    // ---- pass 2: exclusive prefix over units -> this CTA's segments
-    for (int base = 0; base < nunits; base += NTHREADS) {
-        const int u = base + tid;
-        const int n = u < nunits ? a.n_res[u] : 0;
-        int x = n;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) sm.scan_tot[warp] = x;
-        __syncthreads();
-        long long pre = sm.run_total;
-        for (int w = 0; w < warp; ++w) pre += sm.scan_tot[w];
-        pre += x - n;  // exclusive prefix of unit u
-        if (n > 0) {
-            const long long s0 = max(pre, lo), s1 = min(pre + n, hi);
-            if (s0 < s1) {
-                // CTA holding position p: floor(((p+1)*grid - 1)/T)
-                const long long cf = ((pre + 1) * grid - 1) / T;
-                const long long cl = ((pre + n) * grid - 1) / T;
-                const int idx = atomicAdd(&sm.nsegs, 1);
-                if (idx < MAXSEG)
-                    sm.segs[idx] = Seg{u, static_cast<int>(s0 - pre), static_cast<int>(s1 - pre),
-                                       static_cast<int>(cl - cf + 1), static_cast<int>(cf), 0};
-            }
-        }
-        __syncthreads();
-        if (tid == 0) {
-            long long t = 0;
-            for (int w = 0; w < NTHREADS / 32; ++w) t += sm.scan_tot[w];
-            sm.run_total += t;
-        }
-        __syncthreads();
-    }
-    // sort segments by unit (a CTA range is contiguous: unit order == stream order)
-    const int nsegs = min(sm.nsegs, MAXSEG);
-    if (tid == 0) {
-        for (int i = 1; i < nsegs; ++i) {
-            Seg s = sm.segs[i];
-            int j = i - 1;
-            while (j >= 0 && sm.segs[j].unit > s.unit) { sm.segs[j + 1] = sm.segs[j]; --j; }
-            sm.segs[j + 1] = s;
-        }
-        int f = 0;
-        for (int i = 0; i < nsegs; ++i) { sm.segs[i].f0 = f; f += sm.segs[i].j1 - sm.segs[i].j0; }
-    }
-    __syncthreads();
-    // stage the block list (slot, rows); producer and consumers walk it from smem
-    const int nblk = min(static_cast<int>(hi - lo), MAXB);
-    for (int f = tid; f < nblk; f += NTHREADS) {
-        int si = 0;
-        while (si + 1 < nsegs && sm.segs[si + 1].f0 <= f) ++si;
-        const Seg sg = sm.segs[si];
-        const size_t idx = static_cast<size_t>(sg.unit) * ks + sg.j0 + (f - sg.f0);
-        int tail;
-        const int nb = unit_nb(a, sg.unit, &tail);
-        sm.blk_slot[f] = a.res_slots[idx];
-        sm.blk_rows[f] = static_cast<int16_t>((a.res_ids[idx] == nb - 1) ? tail : BS);
-    }
-    __syncthreads();
-
-    K2TS(1);
     if (warp == NC) {
-        // ================================================== producer warp
-        if (lane == 0) {
-            const uint64_t pol = policy_evict_first();
-            const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
-            for (int j = 0; j < nblk; ++j) {
-                const int s = stage_of(j);
-                if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
-                mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
-                bulk_g2s_evict_first(stages + s * STAGE_BYTES,
-                                     pool + static_cast<size_t>(sm.blk_slot[j]) * BF16_SLOT_BYTES, STAGE_BYTES,
-                                     &sm.full[s], pol);
+        // ======================================== planner + producer warp
+        const uint64_t pol = policy_evict_first();
+        const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
+        int j = 0;  // CTA-global block stream index (continues across layers)
+        for (int L = 0; L < a.n_layers; ++L) {
+            const int b = L & 1;
+            const K2Layer& io = a.layers[L];
+            if (L >= 2) mbar_wait(&sm.plan_empty[b], ((L >> 1) - 1) & 1);
+            if (lane == 0) {
+                // K1 published layer L's lists / the layer's inputs landed
+                if (a.k1_flag) wait_flag(a.k1_flag + L, a.token);
+                if (io.in_flag) wait_flag(io.in_flag, a.token);
             }
+            __syncwarp();
+            make_plan(a, io, sm.plan[b], j, lane);
+            const int nblk = sm.plan[b].nblk;
+            if (lane == 0) {
+                mbar_arrive(&sm.plan_full[b]);
+                // blocks recalled for this layer one step ago must have landed
+                if (io.recall_token && a.recall_flag) wait_flag(a.recall_flag + L, io.recall_token);
+                for (int f = 0; f < nblk; ++f, ++j) {
+                    const int s = stage_of(j);
+                    if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
+                    mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
+                    bulk_g2s_evict_first(stages + s * STAGE_BYTES,
+                                         pool + static_cast<size_t>(sm.plan[b].blk_slot[f]) * BF16_SLOT_BYTES,
+                                         STAGE_BYTES, &sm.full[s], pol);
+                }
+            }
+            j = __shfl_sync(0xffffffffu, j, 0);
         }
         return;
     }
@@ -285,259 +310,273 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const sco
     const int pair = warp >> 1, hsel = warp & 1;
     const float sl2 = a.scale * LOG2E;
     const int ctid = tid;  // 0 .. NCT-1
-    for (int si = 0; si < nsegs; ++si) {
-        const Seg sg = sm.segs[si];
-        const int u = sg.unit;
-        // Q^T fragments (hi/lo split), heads >= G are zero
-        uint32_t bh[8][2], bl[8][2];
-        {
-            const bool live = g < G;
-            const float* qh = a.q + (static_cast<size_t>(u) * G + (live ? g : 0)) * D;
+    for (int L = 0; L < a.n_layers; ++L) {
+        const int b = L & 1;
+        const K2Layer& io = a.layers[L];
+        int* ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(a.workspace) + static_cast<size_t>(L) * a.ws_layer_bytes);
+        float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ctr) + ctr_bytes(nunits));
+        mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
+        const Plan& P = sm.plan[b];
+        const int nsegs = P.nsegs, jbase = P.jbase;
+        for (int si = 0; si < nsegs; ++si) {
+            const Seg sg = P.segs[si];
+            const int u = sg.unit;
+            // Q^T fragments (hi/lo split), heads >= G are zero
+            uint32_t bh[8][2], bl[8][2];
+            {
+                const bool live = g < G;
+                const float* qh = io.q + (static_cast<size_t>(u) * G + (live ? g : 0)) * D;
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
+                for (int kk = 0; kk < 8; ++kk) {
 #pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    float2 v = live ? *reinterpret_cast<const float2*>(qh + 16 * kk + 8 * half + 2 * t)
-                                    : make_float2(0.f, 0.f);
-                    const __nv_bfloat162 hv = __floats2bfloat162_rn(v.x, v.y);
-                    const float2 hf = __bfloat1622float2(hv);
-                    bh[kk][half] = *reinterpret_cast<const uint32_t*>(&hv);
-                    bl[kk][half] = pack_bf16(v.x - hf.x, v.y - hf.y);
+                    for (int half = 0; half < 2; ++half) {
+                        float2 v = live ? *reinterpret_cast<const float2*>(qh + 16 * kk + 8 * half + 2 * t)
+                                        : make_float2(0.f, 0.f);
+                        const __nv_bfloat162 hv = __floats2bfloat162_rn(v.x, v.y);
+                        const float2 hf = __bfloat1622float2(hv);
+                        bh[kk][half] = *reinterpret_cast<const uint32_t*>(&hv);
+                        bl[kk][half] = pack_bf16(v.x - hf.x, v.y - hf.y);
+                    }
                 }
             }
-        }
-        float m2[2] = {-CUDART_INF_F, -CUDART_INF_F};
-        float lp[2] = {0.f, 0.f};
-        float oacc[8][4];
+            float m2[2] = {-CUDART_INF_F, -CUDART_INF_F};
+            float lp[2] = {0.f, 0.f};
+            float oacc[8][4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+            for (int i = 0; i < 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
 
-        int held = -1;  // stage of the pair's last block: hosts the combine areas
-        bool any = false;
-        const int f1 = sg.f0 + (sg.j1 - sg.j0);
-        for (int f = sg.f0 + ((pair - sg.f0) % NPAIR + NPAIR) % NPAIR; f < f1; f += NPAIR) {
-            if (held >= 0) {  // the pair's previous block is done: hand its stage back
+            int held = -1;  // stage of the pair's last block: hosts the combine areas
+            bool any = false;
+            const int f1 = sg.f0 + (sg.j1 - sg.j0);
+            const int jf0 = jbase + sg.f0;
+            for (int f = sg.f0 + ((pair - jf0) % NPAIR + NPAIR) % NPAIR; f < f1; f += NPAIR) {
+                if (held >= 0) {  // the pair's previous block is done: hand its stage back
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&sm.empty[held]);
+                }
+                const int jj = jbase + f;
+                const int s = stage_of(jj);
+                held = s;
+                const int valid = min(HALF_ROWS, static_cast<int>(P.blk_rows[f]) - hsel * HALF_ROWS);
+                mbar_wait(&sm.full[s], (jj / NST) & 1);
+                __syncwarp();  // lanes may leave the try_wait loop apart: reconverge before .aligned ops
+                if (valid <= 0) continue;  // open block with one half: the other warp idles
+                any = true;
+                const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES) + hsel * HALF_BYTES_BF16;
+                const uint32_t vbase = kbase + BF16_TILE_BYTES;
+                if (valid < HALF_ROWS) {
+                    // rows past the open block's fill hold stale bytes: P is 0
+                    // there, but 0 * NaN would poison O, so zero those V rows.
+                    for (int i = lane; i < (HALF_ROWS - valid) * 16; i += 32) {
+                        const int row = valid + (i >> 4), chunk = i & 15;
+                        const uint32_t addr = vbase + (chunk >> 3) * 4096 + row * 128 + ((chunk & 7) << 4);
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0) : "memory");
+                    }
+                    __syncwarp();
+                }
+                // ---- S^T = K . Q^T (hi and lo halves of q accumulate separately)
+                float sh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, slo[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+#pragma unroll
+                for (int kk = 0; kk < 8; ++kk) {
+                    const int slab = kk >> 2, cb = (kk & 3) * 2;
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt) {
+                        const int row = 16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8;
+                        const int chunk = cb + (lane >> 4);
+                        const uint32_t addr = kbase + slab * 4096 + row * 128 + ((chunk ^ (row & 7)) << 4);
+                        uint32_t a0, a1, a2, a3;
+                        ldsm_x4(addr, a0, a1, a2, a3);
+                        mma_bf16(sh[mt], a0, a1, a2, a3, bh[kk][0], bh[kk][1]);
+                        mma_bf16(slo[mt], a0, a1, a2, a3, bl[kk][0], bl[kk][1]);
+                    }
+                }
+                // ---- online softmax (columns = heads 2t, 2t+1; rows = tokens)
+                float sv[2][4];
+                float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const int r0 = 16 * mt + g, r1 = r0 + 8;
+                    sv[mt][0] = r0 < valid ? (sh[mt][0] + slo[mt][0]) * sl2 : -CUDART_INF_F;
+                    sv[mt][1] = r0 < valid ? (sh[mt][1] + slo[mt][1]) * sl2 : -CUDART_INF_F;
+                    sv[mt][2] = r1 < valid ? (sh[mt][2] + slo[mt][2]) * sl2 : -CUDART_INF_F;
+                    sv[mt][3] = r1 < valid ? (sh[mt][3] + slo[mt][3]) * sl2 : -CUDART_INF_F;
+                    mx0 = fmaxf(mx0, fmaxf(sv[mt][0], sv[mt][2]));
+                    mx1 = fmaxf(mx1, fmaxf(sv[mt][1], sv[mt][3]));
+                }
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) {
+                    mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+                    mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+                }
+                const float mn0 = fmaxf(m2[0], mx0), mn1 = fmaxf(m2[1], mx1);
+                const float al0 = fast_exp2(m2[0] - mn0), al1 = fast_exp2(m2[1] - mn1);
+                m2[0] = mn0;
+                m2[1] = mn1;
+                float ps0 = 0.f, ps1 = 0.f;
+                uint32_t pb[2][2];
+#pragma unroll
+                for (int mt = 0; mt < 2; ++mt) {
+                    const float p0 = fast_exp2(sv[mt][0] - mn0), p1 = fast_exp2(sv[mt][1] - mn1);
+                    const float p2 = fast_exp2(sv[mt][2] - mn0), p3 = fast_exp2(sv[mt][3] - mn1);
+                    ps0 += p0 + p2;
+                    ps1 += p1 + p3;
+                    pb[mt][0] = movmatrix_t(pack_bf16(p0, p1));
+                    pb[mt][1] = movmatrix_t(pack_bf16(p2, p3));
+                }
+                lp[0] = lp[0] * al0 + ps0;
+                lp[1] = lp[1] * al1 + ps1;
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+                    oacc[md][0] *= al0; oacc[md][1] *= al1; oacc[md][2] *= al0; oacc[md][3] *= al1;
+                }
+                // ---- O^T += V^T . P^T
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk) {
+                        const int row = 16 * kk + (lane & 7) + ((lane >> 4) & 1) * 8;
+                        const int cg = 2 * md + ((lane >> 3) & 1);
+                        const uint32_t addr = vbase + (cg >> 3) * 4096 + row * 128 + (((cg & 7) ^ (row & 7)) << 4);
+                        uint32_t a0, a1, a2, a3;
+                        ldsm_x4_t(addr, a0, a1, a2, a3);
+                        mma_bf16(oacc[md], a0, a1, a2, a3, pb[kk][0], pb[kk][1]);
+                    }
+                }
+            }
+            // ---- warp state -> its combine area: the K half it read of the pair's
+            // last stage (the partner reads only the other half of that stage)
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+                lp[0] += __shfl_xor_sync(0xffffffffu, lp[0], o);
+                lp[1] += __shfl_xor_sync(0xffffffffu, lp[1], o);
+            }
+            __syncwarp();
+            const int area = (held >= 0 && any) ? held * STAGE_BYTES + hsel * HALF_BYTES_BF16 : -1;
+            if (area >= 0) {
+                float* cb = reinterpret_cast<float*>(stages + area);
+#pragma unroll
+                for (int md = 0; md < 8; ++md) {
+                    cb[(2 * t) * CB_ROW + 16 * md + g] = oacc[md][0];
+                    cb[(2 * t + 1) * CB_ROW + 16 * md + g] = oacc[md][1];
+                    cb[(2 * t) * CB_ROW + 16 * md + g + 8] = oacc[md][2];
+                    cb[(2 * t + 1) * CB_ROW + 16 * md + g + 8] = oacc[md][3];
+                }
+                if (g == 0) {
+                    cb[8 * CB_ROW + 2 * t] = m2[0];
+                    cb[8 * CB_ROW + 2 * t + 1] = m2[1];
+                    cb[8 * CB_ROW + 8 + 2 * t] = lp[0];
+                    cb[8 * CB_ROW + 8 + 2 * t + 1] = lp[1];
+                }
+            }
+            if (lane == 0) sm.warp_area[warp] = area;
+            named_bar_sync(1, NCT);
+            // ---- merge the NC warp states (8 heads x 32 lanes x 4 channels)
+            float Ms[2], Ls[2];
+            float4 accs[2];
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const int idx = ctid + r * NCT;
+                Ms[r] = -CUDART_INF_F; Ls[r] = 0.f; accs[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (idx >= 256) continue;
+                const int hh = idx >> 5, d0 = (idx & 31) * 4;
+                float M = -CUDART_INF_F;
+#pragma unroll
+                for (int w = 0; w < NC; ++w) {
+                    const int ar = sm.warp_area[w];
+                    if (ar >= 0) M = fmaxf(M, reinterpret_cast<const float*>(stages + ar)[8 * CB_ROW + hh]);
+                }
+                float Lsum = 0.f;
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int w = 0; w < NC; ++w) {
+                    const int ar = sm.warp_area[w];
+                    if (ar < 0) continue;
+                    const float* wb = reinterpret_cast<const float*>(stages + ar);
+                    const float l = wb[8 * CB_ROW + 8 + hh];
+                    if (!(l > 0.f)) continue;
+                    const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
+                    Lsum += l * fct;
+                    const float4 x = *reinterpret_cast<const float4*>(wb + hh * CB_ROW + d0);
+                    acc.x += fct * x.x; acc.y += fct * x.y; acc.z += fct * x.z; acc.w += fct * x.w;
+                }
+                Ms[r] = M; Ls[r] = Lsum; accs[r] = acc;
+            }
+            named_bar_sync(1, NCT);  // every combine area read: stages can go back
+            if (held >= 0) {
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&sm.empty[held]);
             }
-            const int s = stage_of(f);
-            held = s;
-            const int valid = min(HALF_ROWS, static_cast<int>(sm.blk_rows[f]) - hsel * HALF_ROWS);
-            mbar_wait(&sm.full[s], (f / NST) & 1);
-            __syncwarp();  // lanes may leave the try_wait loop apart: reconverge before .aligned ops
-            if (f == 0) K2TS(2);
-            if (valid <= 0) continue;  // open block with one half: the other warp idles
-            any = true;
-            const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES) + hsel * HALF_BYTES_BF16;
-            const uint32_t vbase = kbase + BF16_TILE_BYTES;
-            if (valid < HALF_ROWS) {
-                // rows past the open block's fill hold stale bytes: P is 0
-                // there, but 0 * NaN would poison O, so zero those V rows.
-                for (int i = lane; i < (HALF_ROWS - valid) * 16; i += 32) {
-                    const int row = valid + (i >> 4), chunk = i & 15;
-                    const uint32_t addr = vbase + (chunk >> 3) * 4096 + row * 128 + ((chunk & 7) << 4);
-                    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "r"(0) : "memory");
-                }
-                __syncwarp();
-            }
-            // ---- S^T = K . Q^T (hi and lo halves of q accumulate separately)
-            float sh[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}}, slo[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
 #pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
-                const int slab = kk >> 2, cb = (kk & 3) * 2;
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const int row = 16 * mt + (lane & 7) + ((lane >> 3) & 1) * 8;
-                    const int chunk = cb + (lane >> 4);
-                    const uint32_t addr = kbase + slab * 4096 + row * 128 + ((chunk ^ (row & 7)) << 4);
-                    uint32_t a0, a1, a2, a3;
-                    ldsm_x4(addr, a0, a1, a2, a3);
-                    mma_bf16(sh[mt], a0, a1, a2, a3, bh[kk][0], bh[kk][1]);
-                    mma_bf16(slo[mt], a0, a1, a2, a3, bl[kk][0], bl[kk][1]);
-                }
-            }
-            // ---- online softmax (columns = heads 2t, 2t+1; rows = tokens)
-            float sv[2][4];
-            float mx0 = -CUDART_INF_F, mx1 = -CUDART_INF_F;
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                const int r0 = 16 * mt + g, r1 = r0 + 8;
-                sv[mt][0] = r0 < valid ? (sh[mt][0] + slo[mt][0]) * sl2 : -CUDART_INF_F;
-                sv[mt][1] = r0 < valid ? (sh[mt][1] + slo[mt][1]) * sl2 : -CUDART_INF_F;
-                sv[mt][2] = r1 < valid ? (sh[mt][2] + slo[mt][2]) * sl2 : -CUDART_INF_F;
-                sv[mt][3] = r1 < valid ? (sh[mt][3] + slo[mt][3]) * sl2 : -CUDART_INF_F;
-                mx0 = fmaxf(mx0, fmaxf(sv[mt][0], sv[mt][2]));
-                mx1 = fmaxf(mx1, fmaxf(sv[mt][1], sv[mt][3]));
-            }
-#pragma unroll
-            for (int o = 4; o < 32; o <<= 1) {
-                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
-                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
-            }
-            const float mn0 = fmaxf(m2[0], mx0), mn1 = fmaxf(m2[1], mx1);
-            const float al0 = fast_exp2(m2[0] - mn0), al1 = fast_exp2(m2[1] - mn1);
-            m2[0] = mn0;
-            m2[1] = mn1;
-            float ps0 = 0.f, ps1 = 0.f;
-            uint32_t pb[2][2];
-#pragma unroll
-            for (int mt = 0; mt < 2; ++mt) {
-                const float p0 = fast_exp2(sv[mt][0] - mn0), p1 = fast_exp2(sv[mt][1] - mn1);
-                const float p2 = fast_exp2(sv[mt][2] - mn0), p3 = fast_exp2(sv[mt][3] - mn1);
-                ps0 += p0 + p2;
-                ps1 += p1 + p3;
-                pb[mt][0] = movmatrix_t(pack_bf16(p0, p1));
-                pb[mt][1] = movmatrix_t(pack_bf16(p2, p3));
-            }
-            lp[0] = lp[0] * al0 + ps0;
-            lp[1] = lp[1] * al1 + ps1;
-#pragma unroll
-            for (int md = 0; md < 8; ++md) {
-                oacc[md][0] *= al0; oacc[md][1] *= al1; oacc[md][2] *= al0; oacc[md][3] *= al1;
-            }
-            // ---- O^T += V^T . P^T
-#pragma unroll
-            for (int md = 0; md < 8; ++md) {
-#pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                    const int row = 16 * kk + (lane & 7) + ((lane >> 4) & 1) * 8;
-                    const int cg = 2 * md + ((lane >> 3) & 1);
-                    const uint32_t addr = vbase + (cg >> 3) * 4096 + row * 128 + (((cg & 7) ^ (row & 7)) << 4);
-                    uint32_t a0, a1, a2, a3;
-                    ldsm_x4_t(addr, a0, a1, a2, a3);
-                    mma_bf16(oacc[md], a0, a1, a2, a3, pb[kk][0], pb[kk][1]);
-                }
-            }
-        }
-        // ---- warp state -> its combine area: the K half it read of the pair's
-        // last stage (the partner reads only the other half of that stage)
-#pragma unroll
-        for (int o = 4; o < 32; o <<= 1) {
-            lp[0] += __shfl_xor_sync(0xffffffffu, lp[0], o);
-            lp[1] += __shfl_xor_sync(0xffffffffu, lp[1], o);
-        }
-        __syncwarp();
-        const int area = (held >= 0 && any) ? held * STAGE_BYTES + hsel * HALF_BYTES_BF16 : -1;
-        if (area >= 0) {
-            float* cb = reinterpret_cast<float*>(stages + area);
-#pragma unroll
-            for (int md = 0; md < 8; ++md) {
-                cb[(2 * t) * CB_ROW + 16 * md + g] = oacc[md][0];
-                cb[(2 * t + 1) * CB_ROW + 16 * md + g] = oacc[md][1];
-                cb[(2 * t) * CB_ROW + 16 * md + g + 8] = oacc[md][2];
-                cb[(2 * t + 1) * CB_ROW + 16 * md + g + 8] = oacc[md][3];
-            }
-            if (g == 0) {
-                cb[8 * CB_ROW + 2 * t] = m2[0];
-                cb[8 * CB_ROW + 2 * t + 1] = m2[1];
-                cb[8 * CB_ROW + 8 + 2 * t] = lp[0];
-                cb[8 * CB_ROW + 8 + 2 * t + 1] = lp[1];
-            }
-        }
-        if (lane == 0) sm.warp_area[warp] = area;
-        if (si == nsegs - 1) K2TS(3);
-        named_bar_sync(1, NCT);
-        // ---- merge the NC warp states (8 heads x 32 lanes x 4 channels)
-        float Ms[2], Ls[2];
-        float4 accs[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int idx = ctid + r * NCT;
-            Ms[r] = -CUDART_INF_F; Ls[r] = 0.f; accs[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (idx >= 256) continue;
-            const int hh = idx >> 5, d0 = (idx & 31) * 4;
-            float M = -CUDART_INF_F;
-#pragma unroll
-            for (int w = 0; w < NC; ++w) {
-                const int ar = sm.warp_area[w];
-                if (ar >= 0) M = fmaxf(M, reinterpret_cast<const float*>(stages + ar)[8 * CB_ROW + hh]);
-            }
-            float L = 0.f;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int w = 0; w < NC; ++w) {
-                const int ar = sm.warp_area[w];
-                if (ar < 0) continue;
-                const float* wb = reinterpret_cast<const float*>(stages + ar);
-                const float l = wb[8 * CB_ROW + 8 + hh];
-                if (!(l > 0.f)) continue;
-                const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
-                L += l * fct;
-                const float4 x = *reinterpret_cast<const float4*>(wb + hh * CB_ROW + d0);
-                acc.x += fct * x.x; acc.y += fct * x.y; acc.z += fct * x.z; acc.w += fct * x.w;
-            }
-            Ms[r] = M; Ls[r] = L; accs[r] = acc;
-        }
-        named_bar_sync(1, NCT);  // every combine area read: stages can go back
-        if (held >= 0) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.empty[held]);
-        }
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int idx = ctid + r * NCT;
-            if (idx >= 256) continue;
-            const int hh = idx >> 5, d0 = (idx & 31) * 4;
-            const float M = Ms[r], L = Ls[r];
-            const float4 acc = accs[r];
-            const float inv = L > 0.f ? 1.f / L : 0.f;
-            if (sg.nseg == 1) {
-                // the whole unit is here: merge with the CPU partial and write out
-                if (hh >= G) continue;
-                const size_t head = static_cast<size_t>(u) * G + hh;
-                float cm = -CUDART_INF_F, cl = 0.f;
-                if (a.cpu_ml) { cm = a.cpu_ml[head * 2] * LOG2E; cl = a.cpu_ml[head * 2 + 1]; }
-                float Mt = M, wa = 1.f, wb = 0.f, Lt = L;
-                if (cl > 0.f) {
-                    Mt = fmaxf(M, cm);
-                    wa = L > 0.f ? exp2f(M - Mt) : 0.f;
-                    wb = cl * exp2f(cm - Mt);
-                    Lt = L * wa + wb;
-                }
-                const float invt = Lt > 0.f ? 1.f / Lt : 0.f;
-                float4 res;
-                if (cl > 0.f) {
-                    const float4 co = *reinterpret_cast<const float4*>(a.cpu_o + head * D + d0);
-                    res = make_float4((acc.x * wa + wb * co.x) * invt, (acc.y * wa + wb * co.y) * invt,
-                                      (acc.z * wa + wb * co.z) * invt, (acc.w * wa + wb * co.w) * invt);
+            for (int r = 0; r < 2; ++r) {
+                const int idx = ctid + r * NCT;
+                if (idx >= 256) continue;
+                const int hh = idx >> 5, d0 = (idx & 31) * 4;
+                const float M = Ms[r], Lsum = Ls[r];
+                const float4 acc = accs[r];
+                const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+                if (sg.nseg == 1) {
+                    // the whole unit is here: merge with the CPU partial and write out
+                    if (hh >= G) continue;
+                    const size_t head = static_cast<size_t>(u) * G + hh;
+                    float cm = -CUDART_INF_F, cl = 0.f;
+                    if (io.cpu_ml) { cm = io.cpu_ml[head * 2] * LOG2E; cl = io.cpu_ml[head * 2 + 1]; }
+                    float Mt = M, wa = 1.f, wb = 0.f, Lt = Lsum;
+                    if (cl > 0.f) {
+                        Mt = fmaxf(M, cm);
+                        wa = Lsum > 0.f ? exp2f(M - Mt) : 0.f;
+                        wb = cl * exp2f(cm - Mt);
+                        Lt = Lsum * wa + wb;
+                    }
+                    const float invt = Lt > 0.f ? 1.f / Lt : 0.f;
+                    float4 res;
+                    if (cl > 0.f) {
+                        const float4 co = *reinterpret_cast<const float4*>(io.cpu_o + head * D + d0);
+                        res = make_float4((acc.x * wa + wb * co.x) * invt, (acc.y * wa + wb * co.y) * invt,
+                                          (acc.z * wa + wb * co.z) * invt, (acc.w * wa + wb * co.w) * invt);
+                    } else {
+                        res = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                    }
+                    *reinterpret_cast<float4*>(io.o + head * D + d0) = res;
+                    if ((idx & 31) == 0) {
+                        io.ml[head * 2] = Lt > 0.f ? Mt * LN2 : -CUDART_INF_F;
+                        io.ml[head * 2 + 1] = Lt;
+                    }
                 } else {
-                    res = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                    // this segment's partial (o normalised, m2, l) -> slot c+u
+                    float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
+                    *reinterpret_cast<float4*>(p + d0) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                    if ((idx & 31) == 0) { p[D] = M; p[D + 1] = Lsum; }
                 }
-                *reinterpret_cast<float4*>(a.o + head * D + d0) = res;
-                if ((idx & 31) == 0) {
-                    a.ml[head * 2] = Lt > 0.f ? Mt * LN2 : -CUDART_INF_F;
-                    a.ml[head * 2 + 1] = Lt;
-                }
-            } else {
-                // this segment's partial (o normalised, m2, l) -> slot c+u
-                float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
-                *reinterpret_cast<float4*>(p + d0) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-                if ((idx & 31) == 0) { p[D] = M; p[D + 1] = L; }
             }
-        }
-        if (sg.nseg != 1) {
-            __threadfence();
-            named_bar_sync(1, NCT);
-            if (ctid == 0) {
-                const int old = atomicAdd(&ctr[u], 1);
-                sm.last_flag = (old == sg.nseg - 1);
-            }
-            named_bar_sync(1, NCT);
-            if (sm.last_flag) {
-                // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
+            if (sg.nseg != 1) {
                 __threadfence();
-                finalize_unit<G, NCT>(a, u, parts, sg.cfirst + u, sg.nseg, ctid);
-                if (ctid == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
+                named_bar_sync(1, NCT);
+                if (ctid == 0) {
+                    const int old = atomicAdd(&ctr[u], 1);
+                    sm.last_flag = (old == sg.nseg - 1);
+                }
+                named_bar_sync(1, NCT);
+                if (sm.last_flag) {
+                    // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
+                    __threadfence();
+                    finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, sg.cfirst + u, sg.nseg, ctid);
+                    if (ctid == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
+                }
             }
         }
+        // ---- units with no resident block: output = CPU partial (or empty)
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            if (io.n_res[u] != 0) continue;
+            finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, ctid);
+        }
+        // layer done in this CTA: release the plan buffer, count the CTA in
+        __threadfence();
+        named_bar_sync(1, NCT);
+        if (ctid == 0) {
+            mbar_arrive(&sm.plan_empty[b]);
+            if (a.layer_done) atomicAdd(a.layer_done + L, 1u);
+        }
     }
-    K2TS(4);
-    // ---- units with no resident block: output = CPU partial (or empty)
-    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-        if (a.n_res[u] != 0) continue;
-        finalize_unit<G, NCT>(a, u, parts, 0, 0, ctid);
-    }
-    K2TS(5);
 }
 
 }  // namespace tc
@@ -628,7 +667,7 @@ template <int G>
 __global__ void combine_kernel(const scout_decode_args a) {
     const int u = blockIdx.x;
     const float* parts = reinterpret_cast<const float*>(static_cast<const uint8_t*>(a.workspace) + ctr_bytes(a.n_units));
-    tc::finalize_unit<G, 128>(a, u, parts, u * SIMPLE_SPLIT, SIMPLE_SPLIT, threadIdx.x);
+    tc::finalize_unit<G, 128>(a.cpu_o, a.cpu_ml, a.o, a.ml, u, parts, u * SIMPLE_SPLIT, SIMPLE_SPLIT, threadIdx.x);
 }
 }  // namespace simple
 
@@ -650,10 +689,48 @@ int tc_grid(int max_ctas) {
 
 }  // namespace
 
+int scout_k2_grid(int n_units, int k_stride, int max_ctas) {
+    // a CTA range must not touch more than MAXSEG units nor hold more than MAXB
+    // blocks of one layer (T <= n_units * k_stride)
+    int min_grid = (n_units + tc::MAXSEG - 3) / (tc::MAXSEG - 2);
+    const long long tmax = static_cast<long long>(n_units) * k_stride;
+    const int min_grid_b = static_cast<int>((tmax + tc::MAXB - 2) / (tc::MAXB - 1));
+    if (min_grid < min_grid_b) min_grid = min_grid_b;
+    int grid = tc_grid(max_ctas);
+    if (grid < min_grid) grid = min_grid;
+    return grid > GRID_CAP ? GRID_CAP : grid;
+}
+
+size_t scout_k2_ws_layer_bytes(int n_units, int grid) {
+    const size_t slots = static_cast<size_t>(grid) + static_cast<size_t>(n_units);
+    return ((ctr_bytes(n_units) + slots * PART_STRIDE * sizeof(float)) + 255) / 256 * 256;
+}
+
+int scout_k2_launch(const K2StepArgs& a, cudaStream_t st, bool pdl) {
+    using namespace scout_host;
+    if (a.n_layers < 1 || a.n_layers > K2_MAX_LAYERS) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "K2: n_layers %d out of range (max %d)", a.n_layers, K2_MAX_LAYERS);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    const int grid = scout_k2_grid(a.n_units, a.k_stride, a.max_ctas);
+    auto go = [&](auto kern) {
+        ensure_smem(reinterpret_cast<const void*>(kern), tc::SMEM_BYTES);
+        launch(kern, dim3(grid), dim3(tc::NTHREADS), tc::SMEM_BYTES, st, pdl, a);
+    };
+    switch (a.group) {
+        case 1: go(tc::sparse_decode_tc_kernel<1>); break;
+        case 2: go(tc::sparse_decode_tc_kernel<2>); break;
+        case 4: go(tc::sparse_decode_tc_kernel<4>); break;
+        default: go(tc::sparse_decode_tc_kernel<8>); break;
+    }
+    return check_launch("scout_sparse_decode");
+}
+
 extern "C" size_t scout_sparse_decode_workspace_bytes(int n_units, int group, int max_ctas) {
     (void)group;
+    (void)max_ctas;
     if (n_units < 0) return 0;
-    const size_t g = static_cast<size_t>(max_ctas > 0 ? (max_ctas > GRID_CAP ? GRID_CAP : max_ctas) : GRID_CAP);
+    const size_t g = GRID_CAP;  // covers any grid scout_k2_grid can pick
     const size_t slots_tc = g + static_cast<size_t>(n_units);
     const size_t slots_simple = static_cast<size_t>(n_units) * SIMPLE_SPLIT;
     const size_t slots = slots_tc > slots_simple ? slots_tc : slots_simple;
@@ -693,26 +770,19 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
     }
     auto st = static_cast<cudaStream_t>(stream);
     if (a.kv_dtype == SCOUT_BF16) {
-        // a CTA range must not touch more than MAXSEG units nor hold more than
-        // MAXB blocks (T <= n_units * k_stride)
-        int min_grid = (a.n_units + tc::MAXSEG - 3) / (tc::MAXSEG - 2);
-        const long long tmax = static_cast<long long>(a.n_units) * a.k_stride;
-        const int min_grid_b = static_cast<int>((tmax + tc::MAXB - 2) / (tc::MAXB - 1));
-        if (min_grid < min_grid_b) min_grid = min_grid_b;
-        int grid = tc_grid(a.max_ctas);
-        if (grid < min_grid) grid = min_grid;
-        if (grid > GRID_CAP) grid = GRID_CAP;
-        auto go = [&](auto kern) {
-            scout_host::ensure_smem(reinterpret_cast<const void*>(kern), tc::SMEM_BYTES);
-            scout_host::launch(kern, dim3(grid), dim3(tc::NTHREADS), tc::SMEM_BYTES, st, (a.flags & SCOUT_LAUNCH_PDL) != 0,
-                               a);
-        };
-        switch (a.group) {
-            case 1: go(tc::sparse_decode_tc_kernel<1>); break;
-            case 2: go(tc::sparse_decode_tc_kernel<2>); break;
-            case 4: go(tc::sparse_decode_tc_kernel<4>); break;
-            default: go(tc::sparse_decode_tc_kernel<8>); break;
-        }
+        K2StepArgs k{};
+        k.n_units = a.n_units;
+        k.group = a.group;
+        k.k_stride = a.k_stride;
+        k.n_layers = 1;
+        k.scale = a.scale;
+        k.kv_pool = a.kv_pool;
+        k.n_tokens = a.n_tokens;
+        k.workspace = a.workspace;
+        k.ws_layer_bytes = a.workspace_bytes;
+        k.max_ctas = a.max_ctas;
+        k.layers[0] = K2Layer{a.q, a.res_slots, a.res_ids, a.n_res, a.cpu_o, a.cpu_ml, a.o, a.ml, nullptr, 0u, 0u};
+        return scout_k2_launch(k, st, (a.flags & SCOUT_LAUNCH_PDL) != 0);
     } else if (a.kv_dtype == SCOUT_F32) {
         const dim3 grid(a.n_units, SIMPLE_SPLIT);
         switch (a.group) {
@@ -732,8 +802,3 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
     return check_launch("scout_sparse_decode");
 }
 
-#ifdef SCOUT_K2_TIMING
-extern "C" int scout_debug_k2_times(unsigned long long* out) {
-    return cudaMemcpyFromSymbol(out, g_k2_ts, sizeof(g_k2_ts)) == cudaSuccess ? 0 : 3;
-}
-#endif
