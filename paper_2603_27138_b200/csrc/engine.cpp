@@ -26,6 +26,7 @@
 #include <vector>
 
 #include "../../include/scout_b200.h"
+#include "k1_batch.h"
 #include "k2_step.h"
 
 namespace scout_host {
@@ -138,7 +139,7 @@ struct scout_engine {
     }
 
     // ---------------------------------------------------------------- K1
-    int select(int layer, const float* q, int step, int par, cudaStream_t st) {
+    scout_topk_args k1_args(int layer, const float* q, int step, int par) {
         scout_topk_args a{};
         a.n_units = U;
         a.group = G;
@@ -164,13 +165,24 @@ struct scout_engine {
         a.done_flag = k1_flag + layer;
         a.done_ctr = k1_ctr + layer;
         a.done_token = token;
+        return a;
+    }
+    // K1 over layers [l0, l0+n) in one launch (grid units x layers): layer 0
+    // selects with the true query, the others with the predicted one
+    int select_batch(int l0, int n, const float* q_true, const float* q_pred, int step, int par, cudaStream_t st) {
+        const size_t qd = static_cast<size_t>(UG) * SCOUT_HEAD_DIM;
+        std::vector<scout_topk_args> v(n);
+        for (int i = 0; i < n; ++i) {
+            const int l = l0 + i;
+            v[i] = k1_args(l, l == 0 ? q_true : q_pred + l * qd, step, par);
+        }
         ++launches;
-        return scout_score_topk_split(&a, st);
+        return scout_k1_launch_batch(v.data(), n, st);
     }
 
     // ---------------------------------------------------------------- K2
     int launch_k2(int par, const float* const* q, const float* const* co, const float* const* cml, float* const* o,
-                  float* const* ml, const unsigned* const* inflag, cudaStream_t st) {
+                  float* const* ml, const unsigned* const* inflag, bool poll_k1, cudaStream_t st) {
         K2StepArgs a{};
         a.n_units = U;
         a.group = G;
@@ -181,7 +193,7 @@ struct scout_engine {
         a.n_tokens = cfg.n_tokens;
         a.workspace = ws.p;
         a.ws_layer_bytes = ws_layer;
-        a.k1_flag = k1_flag;
+        a.k1_flag = poll_k1 ? k1_flag : nullptr;
         a.recall_flag = recall_flag;
         a.layer_done = layer_done;
         a.token = token;
@@ -369,8 +381,10 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const float* 
     const int L = e->cfg.layers;
     const unsigned token = ++e->token;
     const int par = token & 1;
-    int rc = e->begin_step(st, par);
-    for (int i = 0; i < L && rc == SCOUT_OK; ++i) rc = e->select(i, i == 0 ? q_true : q_pred + i * qd, step, par, e->k1s);
+    (void)token;
+    // K1 for every layer in one wide launch (bandwidth-bound, the whole GPU),
+    // then the persistent K2 over all layers; stream order is the dependency
+    int rc = e->select_batch(0, L, q_true, q_pred, step, par, st);
     if (rc != SCOUT_OK) return rc;
     std::vector<const float*> q(L), co(L), cml(L);
     std::vector<float*> o(L), ml(L);
@@ -381,10 +395,9 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const float* 
         o[i] = out_o + i * qd;
         ml[i] = out_ml + i * md;
     }
-    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, st)) != SCOUT_OK)
+    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, false, st)) != SCOUT_OK)
         return rc;
-    if ((rc = e->issue_recalls(step)) != SCOUT_OK) return rc;
-    return e->end_step(st);
+    return e->issue_recalls(step);
 }
 
 extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const float* h_q_true, const float* h_q_pred,
@@ -423,19 +436,20 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
         CU(cudaEventRecord(e->chunk_ev[c], e->h2d));
         if ((rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
     }
-    // ---- K1 stream, layer by layer as the chunks land; CPU-side ids out right after
-    for (int i = 0; i < L; ++i) {
-        if (i % CH == 0) CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[i / CH], 0));
-        if ((rc = e->select(i, i == 0 ? d_qt : d_qp + i * qd, step, par, e->k1s)) != SCOUT_OK) return rc;
+    // ---- K1 stream: one launch per input chunk as it lands (each layer publishes
+    // a device flag); the CPU-side ids go out right after
+    for (int c = 0; c < nch; ++c) {
+        const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
+        CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[c], 0));
+        if ((rc = e->select_batch(lo, n, d_qt, d_qp, step, par, e->k1s)) != SCOUT_OK) return rc;
         if (h_cpu_ids) {
-            // the host co-attention worker needs layer i's CPU-side ids as soon as K1(i) is done
-            CU(cudaEventRecord(e->ev_k1[i], e->k1s));
-            CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[i], 0));
-            CU(cudaMemcpyAsync(h_cpu_ids + e->lk(i), e->I(e->cpu_ids[par]) + e->lk(i),
-                               static_cast<size_t>(e->U) * e->cfg.k * 4, cudaMemcpyDeviceToHost, e->d2h));
+            CU(cudaEventRecord(e->ev_k1[c], e->k1s));
+            CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[c], 0));
+            CU(cudaMemcpyAsync(h_cpu_ids + e->lk(lo), e->I(e->cpu_ids[par]) + e->lk(lo),
+                               static_cast<size_t>(n) * e->U * e->cfg.k * 4, cudaMemcpyDeviceToHost, e->d2h));
             if (h_n_cpu)
-                CU(cudaMemcpyAsync(h_n_cpu + e->lu(i), e->I(e->n_cpu[par]) + e->lu(i), static_cast<size_t>(e->U) * 4,
-                                   cudaMemcpyDeviceToHost, e->d2h));
+                CU(cudaMemcpyAsync(h_n_cpu + e->lu(lo), e->I(e->n_cpu[par]) + e->lu(lo),
+                                   static_cast<size_t>(n) * e->U * 4, cudaMemcpyDeviceToHost, e->d2h));
         }
     }
     // ---- K2: one launch; layer i waits for its input chunk's flag on the device
@@ -450,7 +464,8 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
         ml[i] = d_oml + i * md;
         inflag[i] = e->in_flag + i / CH;
     }
-    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), st)) != SCOUT_OK)
+    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), true, st)) !=
+        SCOUT_OK)
         return rc;
     if ((rc = e->issue_recalls(step)) != SCOUT_OK) return rc;
     // ---- outputs: each chunk leaves once every CTA finished its last layer

@@ -1,0 +1,15 @@
+// Internal: one K1 launch over many layers (grid = units x layers); the
+// per-layer arguments travel by value in the kernel parameters.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "../../include/scout_b200.h"
+
+constexpr int K1_MAX_LAYERS = 96;
+
+struct K1Batch {
+    int n;
+    scout_topk_args a[K1_MAX_LAYERS];
+};
+
+int scout_k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st);

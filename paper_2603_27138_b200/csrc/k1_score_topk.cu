@@ -25,6 +25,12 @@ using namespace scout_dev;
 namespace {
 
 constexpr int K1_THREADS = 256;
+
+}  // namespace
+
+#include "k1_batch.h"
+
+namespace {
 constexpr int K1_WARPS = K1_THREADS / 32;
 
 __device__ __forceinline__ uint64_t score_key(double s) {
@@ -222,7 +228,8 @@ __device__ void radix_kth(int nb, int k, KeyF keyf, CandF candf, SelScratch& S, 
 enum : uint8_t { CLS_OUT = 0, CLS_IN = 1, CLS_Z = 2 };
 
 template <typename DigT, int G, int MODE>
-__global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk_args a) {
+__global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const K1Batch batch) {
+    const scout_topk_args& a = batch.a[blockIdx.y];  // layer of this CTA (one launch can cover many)
     extern __shared__ __align__(16) uint8_t k1_smem[];
     double* qs = reinterpret_cast<double*>(k1_smem);            // [D][G] stacked order
     double2* pn = reinterpret_cast<double2*>(qs + D * G);       // [D] (sum q>=0, sum q<0)
@@ -495,7 +502,8 @@ __global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const scout_topk
 }
 
 template <typename DigT, int MODE>
-int launch_g(const scout_topk_args& a, cudaStream_t st) {
+int launch_g(const K1Batch& b, cudaStream_t st) {
+    const scout_topk_args& a = b.a[0];
     // qs | pn | pna | max(keys + cls, part_s[P][nb] + part_a[P][nb]) with P*nb <= max(4*K1_THREADS+12, nbs)
     const size_t nbs = static_cast<size_t>(a.nb_stride);
     const size_t pmax = 4 * K1_THREADS + 12;  // P * nq <= K1_THREADS
@@ -504,7 +512,7 @@ int launch_g(const scout_topk_args& a, cudaStream_t st) {
     const size_t smem = static_cast<size_t>(D) * a.group * 8 + static_cast<size_t>(D) * 24 + tail;
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
-        scout_host::launch(kern, dim3(a.n_units), dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, a);
+        scout_host::launch(kern, dim3(a.n_units, b.n), dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
     };
     switch (a.group) {
         case 1: go(score_topk_kernel<DigT, 1, MODE>); break;
@@ -516,15 +524,8 @@ int launch_g(const scout_topk_args& a, cudaStream_t st) {
     return 0;
 }
 
-}  // namespace
-
-extern "C" int scout_score_topk_split(const scout_topk_args* args, void* stream) {
+int validate(const scout_topk_args& a) {
     using namespace scout_host;
-    if (!args) {
-        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_score_topk_split: null args");
-        return SCOUT_ERR_INVALID_ARGUMENT;
-    }
-    const scout_topk_args& a = *args;
     if (a.k == 0) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "select_topk: k must be >= 1");
         return SCOUT_ERR_INVALID_ARGUMENT;
@@ -543,19 +544,23 @@ extern "C" int scout_score_topk_split(const scout_topk_args* args, void* stream)
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_score_topk_split: group %d not in {1,2,4,8}", a.group);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
-    if (a.n_units == 0) return SCOUT_OK;
-    if (!a.q || !a.digests || !a.n_tokens) {
+    if (a.n_units > 0 && (!a.q || !a.digests || !a.n_tokens)) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_score_topk_split: null q/digests/n_tokens");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
-    auto st = static_cast<cudaStream_t>(stream);
+    return SCOUT_OK;
+}
+
+int launch_batch(const K1Batch& b, cudaStream_t st) {
+    using namespace scout_host;
+    const scout_topk_args& a = b.a[0];
     int rc = -1;
     if (a.method == SCOUT_DIGEST_MINMAX) {
-        if (a.digest_dtype == SCOUT_BF16) rc = launch_g<__nv_bfloat16, 0>(a, st);
-        else if (a.digest_dtype == SCOUT_F32) rc = launch_g<float, 0>(a, st);
-        else if (a.digest_dtype == SCOUT_F64) rc = launch_g<double, 1>(a, st);
+        if (a.digest_dtype == SCOUT_BF16) rc = launch_g<__nv_bfloat16, 0>(b, st);
+        else if (a.digest_dtype == SCOUT_F32) rc = launch_g<float, 0>(b, st);
+        else if (a.digest_dtype == SCOUT_F64) rc = launch_g<double, 1>(b, st);
     } else if (a.method == SCOUT_DIGEST_MEAN) {
-        if (a.digest_dtype == SCOUT_F64) rc = launch_g<double, 2>(a, st);
+        if (a.digest_dtype == SCOUT_F64) rc = launch_g<double, 2>(b, st);
     }
     if (rc != 0) {
         set_error(SCOUT_ERR_UNSUPPORTED, "scout_score_topk_split: method %d with digest dtype %d unsupported",
@@ -563,4 +568,44 @@ extern "C" int scout_score_topk_split(const scout_topk_args* args, void* stream)
         return SCOUT_ERR_UNSUPPORTED;
     }
     return check_launch("scout_score_topk_split");
+}
+
+}  // namespace
+
+extern "C" int scout_score_topk_split(const scout_topk_args* args, void* stream) {
+    using namespace scout_host;
+    if (!args) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_score_topk_split: null args");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    const int rc = validate(*args);
+    if (rc != SCOUT_OK) return rc;
+    if (args->n_units == 0) return SCOUT_OK;
+    static thread_local K1Batch b;  // kernel parameters (copied at launch)
+    b.n = 1;
+    b.a[0] = *args;
+    return launch_batch(b, static_cast<cudaStream_t>(stream));
+}
+
+int scout_k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st) {
+    using namespace scout_host;
+    if (n < 1 || n > K1_MAX_LAYERS) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "K1 batch: %d layers (max %d)", n, K1_MAX_LAYERS);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    for (int i = 0; i < n; ++i) {
+        const int rc = validate(layers[i]);
+        if (rc != SCOUT_OK) return rc;
+        if (layers[i].n_units != layers[0].n_units || layers[i].group != layers[0].group ||
+            layers[i].nb_stride != layers[0].nb_stride || layers[i].digest_dtype != layers[0].digest_dtype ||
+            layers[i].method != layers[0].method) {
+            set_error(SCOUT_ERR_INVALID_ARGUMENT, "K1 batch: layers must share shape / dtype / method");
+            return SCOUT_ERR_INVALID_ARGUMENT;
+        }
+    }
+    if (layers[0].n_units == 0) return SCOUT_OK;
+    static thread_local K1Batch b;
+    b.n = n;
+    for (int i = 0; i < n; ++i) b.a[i] = layers[i];
+    return launch_batch(b, st);
 }
