@@ -151,6 +151,9 @@ typedef struct scout_topk_args {
 } scout_topk_args;
 
 int scout_score_topk_split(const scout_topk_args* args, void* stream);
+/* The same for n layers in ONE launch (grid = units x layers): every
+ * args[i] must share n_units, group, nb_stride, digest dtype and method. */
+int scout_score_topk_split_batch(const scout_topk_args* args, int n, void* stream);
 
 /* ------------------------------------------------------------------ K2 --
  * Block-sparse flash-decode over the GPU-resident selected blocks of every

@@ -1,20 +1,21 @@
 // Host-side decode-step orchestration in C++ (the GPU side of
 // ScoutEngine::decode_step, reference proj/include/scout/engine.hpp:205-314).
 //
-// One decode step = two concurrent streams plus two copy streams:
-//   K1 stream : K1(0) (true query; layer 0 is pinned resident, engine.hpp:227-233)
-//               then K1(i) for i >= 1 with the predicted query (engine.hpp:236-251),
-//               each publishing a device flag when its lists are written;
-//   caller's stream : ONE persistent K2 launch that walks all layers, polling
-//               the K1 flag of layer i before planning it (K1 CTAs co-reside
-//               with the K2 CTAs, so the two overlap on every SM);
-//   side stream : per-layer recall copies (copy engines) gated on the layer's
-//               K2 completion counter via cuStreamWaitValue32 (issued after the
-//               layer's attention, kv_store.hpp:175-197) and publishing a
-//               recall flag the next step's K2 waits on before it streams the
-//               layer (visible at (m+1, i), kv_store.hpp:201-218);
-//   h2d / d2h : the host-buffer path's pipelined input / output copies, also
-//               flag-gated per layer chunk.
+// A decode step (device path, scout_engine_decode_step):
+//   1. K1 for every layer in ONE launch (grid units x layers): K1(0) with the
+//      true query (layer 0 is pinned resident, engine.hpp:227-233), K1(i>=1)
+//      with the predicted query (engine.hpp:236-251);
+//   2. ONE persistent K2 launch that walks all layers (per-layer launch cost
+//      and pipeline drain gone);
+//   3. side stream: per-layer recall copies (copy engines) gated on the
+//      layer's K2 completion counter via cuStreamWaitValue32 (issued after the
+//      layer's attention, kv_store.hpp:175-197), each publishing a recall flag
+//      the next step's K2 waits on before it streams the layer (visible at
+//      (m+1, i), kv_store.hpp:201-218).
+// Host-buffer path (scout_engine_decode_step_host): q_pred lands first, chunk
+// by chunk, each chunk releasing a K1 launch; K2 starts once K1 is done and
+// polls per-chunk input flags for q_true / CPU partials still in flight; the
+// outputs and the host worker's CPU-side ids leave as soon as they exist.
 // K1 outputs are double-buffered by step parity; K2 workspaces are per layer.
 // Nothing here allocates or synchronises the host inside a step.
 #include <cuda.h>
@@ -422,22 +423,30 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
     float* d_oml = d_o + L * qd;
     int rc = e->begin_step(st, par);
     if (rc != SCOUT_OK) return rc;
-    // ---- inputs: chunked H2D; each chunk publishes a flag (K2) and an event (K1)
+    // ---- inputs, in the order the device needs them: q_true of layer 0 and
+    // q_pred (K1's inputs) by chunk first, each chunk releasing a K1 launch on
+    // the whole GPU; then q_true / CPU partials by chunk, each publishing a
+    // flag the (already running) persistent K2 polls before planning a layer
     if (e->stage_recorded[par]) CU(cudaStreamWaitEvent(e->h2d, e->stage_free[par], 0));
     CU(cudaStreamWaitEvent(e->h2d, e->ev_start, 0));
+    CU(cudaMemcpyAsync(d_qt, h_q_true, qd * 4, cudaMemcpyHostToDevice, e->h2d));
     for (int c = 0; c < nch; ++c) {
         const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
-        CU(cudaMemcpyAsync(d_qt + lo * qd, h_q_true + lo * qd, n * qd * 4, cudaMemcpyHostToDevice, e->h2d));
         CU(cudaMemcpyAsync(d_qp + lo * qd, h_q_pred + lo * qd, n * qd * 4, cudaMemcpyHostToDevice, e->h2d));
+        CU(cudaEventRecord(e->chunk_ev[c], e->h2d));
+    }
+    for (int c = 0; c < nch; ++c) {
+        const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
+        const int lq = c == 0 ? 1 : lo;  // layer 0's q_true went first
+        CU(cudaMemcpyAsync(d_qt + lq * qd, h_q_true + lq * qd, (lo + n - lq) * qd * 4, cudaMemcpyHostToDevice, e->h2d));
         if (h_cpu_o) {
             CU(cudaMemcpyAsync(d_co + lo * qd, h_cpu_o + lo * qd, n * qd * 4, cudaMemcpyHostToDevice, e->h2d));
             CU(cudaMemcpyAsync(d_cm + lo * md, h_cpu_ml + lo * md, n * md * 4, cudaMemcpyHostToDevice, e->h2d));
         }
-        CU(cudaEventRecord(e->chunk_ev[c], e->h2d));
         if ((rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
     }
-    // ---- K1 stream: one launch per input chunk as it lands (each layer publishes
-    // a device flag); the CPU-side ids go out right after
+    // ---- K1 per q_pred chunk, on the whole GPU (before K2 starts); the
+    // CPU-side ids go out to the host worker right after each chunk
     for (int c = 0; c < nch; ++c) {
         const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
         CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[c], 0));
@@ -452,6 +461,8 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
                                    static_cast<size_t>(n) * e->U * 4, cudaMemcpyDeviceToHost, e->d2h));
         }
     }
+    CU(cudaEventRecord(e->ev_k1_end, e->k1s));
+    CU(cudaStreamWaitEvent(st, e->ev_k1_end, 0));
     // ---- K2: one launch; layer i waits for its input chunk's flag on the device
     std::vector<const float*> q(L), co(L), cml(L);
     std::vector<float*> o(L), ml(L);
@@ -464,7 +475,7 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
         ml[i] = d_oml + i * md;
         inflag[i] = e->in_flag + i / CH;
     }
-    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), true, st)) !=
+    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), false, st)) !=
         SCOUT_OK)
         return rc;
     if ((rc = e->issue_recalls(step)) != SCOUT_OK) return rc;

@@ -24,7 +24,19 @@ using namespace scout_dev;
 
 namespace {
 
-constexpr int K1_THREADS = 256;
+// 128 threads x 12 CTAs/SM: many small CTAs hide the latency-bound selection
+// phases best (64-layer batch: 1.14 ms vs 1.35 at 256 x 4, 1.63 at 512 x 1)
+#ifndef SCOUT_K1_THREADS
+#define SCOUT_K1_THREADS 128
+#endif
+#ifndef SCOUT_K1_PMAX
+#define SCOUT_K1_PMAX 1
+#endif
+#ifndef SCOUT_K1_MINB
+#define SCOUT_K1_MINB 12
+#endif
+constexpr int K1_THREADS = SCOUT_K1_THREADS;
+constexpr int K1_PMAX = SCOUT_K1_PMAX;  // channel parts per block quad in the fast score
 
 }  // namespace
 
@@ -228,7 +240,7 @@ __device__ void radix_kth(int nb, int k, KeyF keyf, CandF candf, SelScratch& S, 
 enum : uint8_t { CLS_OUT = 0, CLS_IN = 1, CLS_Z = 2 };
 
 template <typename DigT, int G, int MODE>
-__global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const K1Batch batch) {
+__global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(const K1Batch batch) {
     const scout_topk_args& a = batch.a[blockIdx.y];  // layer of this CTA (one launch can cover many)
     extern __shared__ __align__(16) uint8_t k1_smem[];
     double* qs = reinterpret_cast<double*>(k1_smem);            // [D][G] stacked order
@@ -293,7 +305,7 @@ __global__ void __launch_bounds__(K1_THREADS) score_topk_kernel(const K1Batch ba
             // are summed in a fixed order afterwards (order is free: approximate).
             const int nq = (nb + 3) >> 2;
             int P = 1;
-            while (P < 2 && nq * P * 2 <= K1_THREADS) P *= 2;
+            while (P < K1_PMAX && nq * P * 2 <= K1_THREADS) P *= 2;
             const int cper = D / P;
             // [P][nb] partials overlay keys/cls (P*nq <= K1_THREADS, so P*nb <= max(4*K1_THREADS+12,
             // nb_stride): sized at launch; small so K1 can co-reside with a K2 CTA)
@@ -608,4 +620,12 @@ int scout_k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st)
     b.n = n;
     for (int i = 0; i < n; ++i) b.a[i] = layers[i];
     return launch_batch(b, st);
+}
+
+extern "C" int scout_score_topk_split_batch(const scout_topk_args* args, int n, void* stream) {
+    if (!args) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_score_topk_split_batch: null args");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    return scout_k1_launch_batch(args, n, static_cast<cudaStream_t>(stream));
 }
