@@ -202,13 +202,9 @@ def dist_setup():
 
 
 def max_over_ranks(x, ws, dev):
-    if ws == 1:
-        return x
-    import torch.distributed as dist
+    from paper_2603_27138_b200.sharding import max_over_ranks as m
 
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    return m(x, dev) if ws > 1 else x
 
 
 def barrier(ws):
@@ -329,7 +325,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="scout", choices=["scout", "reference"])
     ap.add_argument("--config", default="qwen3-32b-32k", choices=sorted(CONFIGS))
-    ap.add_argument("--batch", type=int, default=0, help="requests per GPU (default: config)")
+    ap.add_argument("--batch", type=int, default=0, help="requests per GPU (default: config; weak scaling)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="total requests split across ranks (strong scaling, e.g. config 4: 128)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline")
@@ -338,6 +336,12 @@ def main():
     if args.batch:
         cfg["batch"] = args.batch
     ws, rank, local = dist_setup()
+    scaling = "weak"
+    if args.global_batch:
+        from paper_2603_27138_b200.sharding import request_shard
+
+        cfg["batch"] = request_shard(args.global_batch, ws, rank)[1]
+        scaling = "strong"
     if args.impl == "reference":
         run_reference(args, cfg, ws, rank)
         barrier(ws)
@@ -389,7 +393,12 @@ def main():
     eng.set_timing(False)
     k2_ms = [k2_total / max(k2_n, 1)] * k2_n
     ms_step = ms / args.steps
-    tok_s = cfg["batch"] * ws / (ms_step / 1000.0)
+    global_batch = args.global_batch or cfg["batch"] * ws
+    tok_s = global_batch / (ms_step / 1000.0)
+    # verification only (outside the timed region): every rank's output checksum
+    from paper_2603_27138_b200.sharding import gather_checksums
+
+    checksums = gather_checksums(wl.out_o[-1]) if ws > 1 else None
     # ---- roofline for K2 (dominant kernel)
     # one persistent K2 launch covers all layers of a step
     k2_avg = float(np.mean(k2_ms))
@@ -414,7 +423,7 @@ def main():
     # ---- e2e through host buffers
     e2e = None
     if not args.profile:
-        e2e = run_e2e(wl, args.e2e_steps, dev, ws)
+        e2e = run_e2e(wl, args.e2e_steps, dev, ws, global_batch)
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
@@ -426,10 +435,10 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init KV, digests, queries, CPU partials)",
             "config": {"workload": args.config, "model_shape": "Qwen3-32B" if cfg["hq"] == 64 else "Qwen3-8B",
-                       "batch_per_gpu": cfg["batch"], "global_batch": cfg["batch"] * ws, "context": cfg["ctx"],
+                       "batch_per_gpu": cfg["batch"], "global_batch": global_batch, "context": cfg["ctx"],
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "head_dim": D,
                        "block": BS, "top_k": cfg["k"], "gpu_cache_blocks_per_unit": cfg["capacity"],
                        "cpu_blocks_per_unit": wl.cpu_per_unit, "recall_every": cfg["recall"],
@@ -442,6 +451,7 @@ def main():
                          "share_of_step": k2_share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"},
             "clocks": clk,
             "gpu_launches": launches,
+            "verify": {"rank_output_checksums": checksums} if checksums else None,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
@@ -449,7 +459,7 @@ def main():
     barrier(ws)
 
 
-def run_e2e(wl: Workload, steps, dev, ws):
+def run_e2e(wl: Workload, steps, dev, ws, global_batch):
     """Same step through the C++ engine with pinned HOST inputs/outputs
     (scout_engine_decode_step_host): H2D of q_true / q_pred / CPU partials in
     layer chunks on a copy stream, D2H of the attention output and of each
@@ -486,7 +496,7 @@ def run_e2e(wl: Workload, steps, dev, ws):
     ok = bool(torch.allclose(h_out[L - 1], wl.out_o[L - 1].cpu(), rtol=0, atol=0))
     h2d_bytes = sum(x.numel() * x.element_size() for x in (h_qt, h_qp, h_co, h_cm))
     d2h_bytes = sum(x.numel() * x.element_size() for x in (h_out, h_oml, h_cpu_ids, h_n_cpu))
-    return {"value": wl.cfg["batch"] * ws / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms,
+    return {"value": global_batch / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes, "matches_device_path": ok,
             "path": "C ABI scout_engine_decode_step_host (csrc/engine.cpp), pinned host buffers"}
 

@@ -1,0 +1,66 @@
+"""Multi-process (gloo, world_size 2, CPU) coverage of the N>1 host path:
+request sharding, max-over-ranks timing, checksum gather."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_27138_b200.sharding import gather_checksums, max_over_ranks, request_shard, unit_range
+
+
+@pytest.mark.parametrize("gb,world", [(128, 2), (128, 8), (7, 3), (1, 4), (0, 2)])
+def test_request_shard_partitions(gb, world):
+    seen = []
+    for r in range(world):
+        s, n = request_shard(gb, world, r)
+        seen += list(range(s, s + n))
+    assert seen == list(range(gb))
+    counts = [request_shard(gb, world, r)[1] for r in range(world)]
+    assert max(counts) - min(counts) <= 1
+
+
+def test_unit_range_and_errors():
+    assert unit_range(128, 8, 4, 1) == (32 * 8, 32 * 8)
+    with pytest.raises(ValueError):
+        request_shard(4, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        s, n = request_shard(128, world, rank)
+        t = max_over_ranks(10.0 + rank)               # the slowest rank sets the step time
+        out = torch.full((n, 4), float(rank + 1))      # this rank's attention outputs
+        sums = gather_checksums(out)
+        q.put((rank, s, n, t, sums))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_ranks():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [(r[1], r[2]) for r in res] == [(0, 64), (64, 64)]
+    assert all(r[3] == 11.0 for r in res)
+    assert all(r[4] == [64 * 4 * 1.0, 64 * 4 * 2.0] for r in res)
