@@ -33,9 +33,26 @@ namespace {
 #define SCOUT_K1_PMAX 1
 #endif
 #ifndef SCOUT_K1_MINB
-#define SCOUT_K1_MINB 12
+#define SCOUT_K1_MINB 4
 #endif
 constexpr int K1_THREADS = SCOUT_K1_THREADS;
+static_assert(K1_THREADS >= 128, "one thread per channel when staging the query sums");
+#ifndef SCOUT_K1_NBUF
+#define SCOUT_K1_NBUF 2
+#endif
+constexpr int K1_NBUF = SCOUT_K1_NBUF;          // digest chunk buffers (bulk-copy ring)
+constexpr int K1_CHUNK_BYTES = 16384;           // lo + hi rows of one chunk
+
+__host__ __device__ inline size_t k1_stage_offset(int G, int nbs) {
+    const size_t head = static_cast<size_t>(D) * G * 8 + static_cast<size_t>(D) * 24 + static_cast<size_t>(nbs) * 21;
+    return (head + 127) / 128 * 128;
+}
+__host__ __device__ inline size_t k1_smem_bytes(int G, int nbs, int esz) {
+    // the chunk is at least one channel of lo + hi rows
+    const size_t one = static_cast<size_t>(nbs) * 2 * esz;
+    const size_t chunk = one > static_cast<size_t>(K1_CHUNK_BYTES) ? one : K1_CHUNK_BYTES;
+    return k1_stage_offset(G, nbs) + K1_NBUF * chunk;
+}
 constexpr int K1_PMAX = SCOUT_K1_PMAX;  // channel parts per block quad in the fast score
 
 }  // namespace
@@ -247,7 +264,11 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
     double2* pn = reinterpret_cast<double2*>(qs + D * G);       // [D] (sum q>=0, sum q<0)
     float2* pna = reinterpret_cast<float2*>(pn + D);            // [D] abs sums, rounded up
     uint64_t* keys = reinterpret_cast<uint64_t*>(pna + D);      // [nb_stride]
-    uint8_t* cls = reinterpret_cast<uint8_t*>(keys + a.nb_stride);  // [nb_stride]
+    double* s_acc = reinterpret_cast<double*>(keys + a.nb_stride);  // [nb_stride] running fast scores
+    float* a_acc = reinterpret_cast<float*>(s_acc + a.nb_stride);   // [nb_stride] running sum |terms|
+    uint8_t* cls = reinterpret_cast<uint8_t*>(a_acc + a.nb_stride); // [nb_stride]
+    uint8_t* stagebuf = k1_smem + k1_stage_offset(G, a.nb_stride);  // K1_NBUF x chunk (MODE 0)
+    __shared__ uint64_t s_full[K1_NBUF];
     __shared__ SelScratch S;
     __shared__ int warp_tot[K1_WARPS];
     __shared__ int s_tok[2];
@@ -300,76 +321,79 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
         }
         __syncthreads();
         if (!take_all || a.scores_out) {
-            // thread -> (block quad j, channel part p): P parts of 128/P channels so
-            // every thread streams digests (memory-level parallelism); the parts
-            // are summed in a fixed order afterwards (order is free: approximate).
+            // Digests stream through shared memory with 1-D bulk copies (TMA
+            // engine): chunks of `cpc` channels (lo rows + hi rows, 16 KiB at
+            // 512 blocks), K1_NBUF-deep, so loads hold no registers and every
+            // CTA keeps a chunk in flight while it computes the previous one.
+            // thread -> block quads j = tid, tid + K1_THREADS, ...; the running
+            // sums live in shared memory (order-free: the score is approximate).
             const int nq = (nb + 3) >> 2;
-            int P = 1;
-            while (P < K1_PMAX && nq * P * 2 <= K1_THREADS) P *= 2;
-            const int cper = D / P;
-            // [P][nb] partials overlay keys/cls (P*nq <= K1_THREADS, so P*nb <= max(4*K1_THREADS+12,
-            // nb_stride): sized at launch; small so K1 can co-reside with a K2 CTA)
-            double* part_s = reinterpret_cast<double*>(keys);
-            float* part_a = reinterpret_cast<float*>(part_s + P * nb);
-            for (int t = tid; t < nq * P; t += K1_THREADS) {
-                const int j = t % nq, p = t / nq;
-                const int b0 = 4 * j;
-                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-                float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-                const int c0 = p * cper;
-#pragma unroll 8
-                for (int c = c0; c < c0 + cper; ++c) {
-                    float l[4], h[4];
-                    if constexpr (sizeof(DigT) == 2) {
-                        const uint2 lv = __ldg(reinterpret_cast<const uint2*>(lo + c * ns + b0));
-                        const uint2 hv = __ldg(reinterpret_cast<const uint2*>(hi + c * ns + b0));
-                        l[0] = __uint_as_float(lv.x << 16); l[1] = __uint_as_float(lv.x & 0xFFFF0000u);
-                        l[2] = __uint_as_float(lv.y << 16); l[3] = __uint_as_float(lv.y & 0xFFFF0000u);
-                        h[0] = __uint_as_float(hv.x << 16); h[1] = __uint_as_float(hv.x & 0xFFFF0000u);
-                        h[2] = __uint_as_float(hv.y << 16); h[3] = __uint_as_float(hv.y & 0xFFFF0000u);
-                    } else {
-                        const float4 lv = __ldg(reinterpret_cast<const float4*>(lo + c * ns + b0));
-                        const float4 hv = __ldg(reinterpret_cast<const float4*>(hi + c * ns + b0));
-                        l[0] = lv.x; l[1] = lv.y; l[2] = lv.z; l[3] = lv.w;
-                        h[0] = hv.x; h[1] = hv.y; h[2] = hv.z; h[3] = hv.w;
-                    }
-                    const double2 pv = pn[c];
-                    const float2 pa = pna[c];
-                    s0 = fma(static_cast<double>(h[0]), pv.x, s0); s0 = fma(static_cast<double>(l[0]), pv.y, s0);
-                    s1 = fma(static_cast<double>(h[1]), pv.x, s1); s1 = fma(static_cast<double>(l[1]), pv.y, s1);
-                    s2 = fma(static_cast<double>(h[2]), pv.x, s2); s2 = fma(static_cast<double>(l[2]), pv.y, s2);
-                    s3 = fma(static_cast<double>(h[3]), pv.x, s3); s3 = fma(static_cast<double>(l[3]), pv.y, s3);
-                    a0 = fmaf(fabsf(h[0]), pa.x, fmaf(fabsf(l[0]), pa.y, a0));
-                    a1 = fmaf(fabsf(h[1]), pa.x, fmaf(fabsf(l[1]), pa.y, a1));
-                    a2 = fmaf(fabsf(h[2]), pa.x, fmaf(fabsf(l[2]), pa.y, a2));
-                    a3 = fmaf(fabsf(h[3]), pa.x, fmaf(fabsf(l[3]), pa.y, a3));
-                }
-                const double sv[4] = {s0, s1, s2, s3};
-                const float av[4] = {a0, a1, a2, a3};
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    if (b0 + i < nb) {
-                        part_s[p * nb + b0 + i] = sv[i];
-                        part_a[p * nb + b0 + i] = av[i];
-                    }
+            constexpr int esz = static_cast<int>(sizeof(DigT));
+            const int cpc = max(1, min(D, K1_CHUNK_BYTES / (2 * static_cast<int>(ns) * esz)));
+            const int nchunks = (D + cpc - 1) / cpc;
+            const uint32_t lo_bytes = static_cast<uint32_t>(cpc * ns * esz);  // one half of a chunk buffer
+            for (int i = tid; i < nq * 4; i += K1_THREADS) { s_acc[i] = 0.0; a_acc[i] = 0.f; }
+            if (tid == 0) {
+                for (int i = 0; i < K1_NBUF; ++i) mbar_init(&s_full[i], 1);
+                fence_mbar_init();
             }
             __syncthreads();
-            // fold the parts (fixed order) -> approximate keys; keys overlay part 0
-            float amax = 0.f;
-            double sfold[16];
-            int nmine = 0;
-            for (int b = tid; b < nb; b += K1_THREADS) {
-                double sv = part_s[b];
-                float av = part_a[b];
-                for (int p = 1; p < P; ++p) { sv += part_s[p * nb + b]; av += part_a[p * nb + b]; }
-                if (nmine < 16) sfold[nmine] = sv;
-                ++nmine;
-                amax = fmaxf(amax, av * 1.0001f);
+            auto issue = [&](int c) {
+                const int ch0 = c * cpc, nch = min(cpc, D - ch0);
+                const uint32_t bytes = static_cast<uint32_t>(nch * ns * esz);
+                uint8_t* buf = stagebuf + static_cast<size_t>(c % K1_NBUF) * 2 * lo_bytes;
+                mbar_arrive_expect_tx(&s_full[c % K1_NBUF], 2 * bytes);
+                bulk_g2s(buf, lo + ch0 * ns, bytes, &s_full[c % K1_NBUF]);
+                bulk_g2s(buf + lo_bytes, hi + ch0 * ns, bytes, &s_full[c % K1_NBUF]);
+            };
+            if (tid == 0)
+                for (int c = 0; c < K1_NBUF && c < nchunks; ++c) issue(c);
+            for (int c = 0; c < nchunks; ++c) {
+                mbar_wait(&s_full[c % K1_NBUF], (c / K1_NBUF) & 1);
+                const int ch0 = c * cpc, nch = min(cpc, D - ch0);
+                const DigT* blo = reinterpret_cast<const DigT*>(stagebuf + static_cast<size_t>(c % K1_NBUF) * 2 * lo_bytes);
+                const DigT* bhi = reinterpret_cast<const DigT*>(reinterpret_cast<const uint8_t*>(blo) + lo_bytes);
+                for (int j = tid; j < nq; j += K1_THREADS) {
+                    const int b0 = 4 * j;
+                    double s0 = s_acc[b0], s1 = s_acc[b0 + 1], s2 = s_acc[b0 + 2], s3 = s_acc[b0 + 3];
+                    float a0 = a_acc[b0], a1 = a_acc[b0 + 1], a2 = a_acc[b0 + 2], a3 = a_acc[b0 + 3];
+#pragma unroll 4
+                    for (int cl = 0; cl < nch; ++cl) {
+                        float l[4], h[4];
+                        if constexpr (sizeof(DigT) == 2) {
+                            const uint2 lv = *reinterpret_cast<const uint2*>(blo + cl * ns + b0);
+                            const uint2 hv = *reinterpret_cast<const uint2*>(bhi + cl * ns + b0);
+                            l[0] = __uint_as_float(lv.x << 16); l[1] = __uint_as_float(lv.x & 0xFFFF0000u);
+                            l[2] = __uint_as_float(lv.y << 16); l[3] = __uint_as_float(lv.y & 0xFFFF0000u);
+                            h[0] = __uint_as_float(hv.x << 16); h[1] = __uint_as_float(hv.x & 0xFFFF0000u);
+                            h[2] = __uint_as_float(hv.y << 16); h[3] = __uint_as_float(hv.y & 0xFFFF0000u);
+                        } else {
+                            const float4 lv = *reinterpret_cast<const float4*>(blo + cl * ns + b0);
+                            const float4 hv = *reinterpret_cast<const float4*>(bhi + cl * ns + b0);
+                            l[0] = lv.x; l[1] = lv.y; l[2] = lv.z; l[3] = lv.w;
+                            h[0] = hv.x; h[1] = hv.y; h[2] = hv.z; h[3] = hv.w;
+                        }
+                        const double2 pv = pn[ch0 + cl];
+                        const float2 pa = pna[ch0 + cl];
+                        s0 = fma(static_cast<double>(h[0]), pv.x, s0); s0 = fma(static_cast<double>(l[0]), pv.y, s0);
+                        s1 = fma(static_cast<double>(h[1]), pv.x, s1); s1 = fma(static_cast<double>(l[1]), pv.y, s1);
+                        s2 = fma(static_cast<double>(h[2]), pv.x, s2); s2 = fma(static_cast<double>(l[2]), pv.y, s2);
+                        s3 = fma(static_cast<double>(h[3]), pv.x, s3); s3 = fma(static_cast<double>(l[3]), pv.y, s3);
+                        a0 = fmaf(fabsf(h[0]), pa.x, fmaf(fabsf(l[0]), pa.y, a0));
+                        a1 = fmaf(fabsf(h[1]), pa.x, fmaf(fabsf(l[1]), pa.y, a1));
+                        a2 = fmaf(fabsf(h[2]), pa.x, fmaf(fabsf(l[2]), pa.y, a2));
+                        a3 = fmaf(fabsf(h[3]), pa.x, fmaf(fabsf(l[3]), pa.y, a3));
+                    }
+                    s_acc[b0] = s0; s_acc[b0 + 1] = s1; s_acc[b0 + 2] = s2; s_acc[b0 + 3] = s3;
+                    a_acc[b0] = a0; a_acc[b0 + 1] = a1; a_acc[b0 + 2] = a2; a_acc[b0 + 3] = a3;
+                }
+                __syncthreads();  // buffer drained by every thread: refill it
+                if (tid == 0 && c + K1_NBUF < nchunks) issue(c + K1_NBUF);
             }
-            __syncthreads();  // all parts read before keys overwrite them
-            {
-                int i = 0;
-                for (int b = tid; b < nb; b += K1_THREADS, ++i) keys[b] = score_key(sfold[i]);
+            float amax = 0.f;
+            for (int b = tid; b < nb; b += K1_THREADS) {
+                keys[b] = score_key(s_acc[b]);
+                amax = fmaxf(amax, a_acc[b] * 1.0001f);
             }
 #pragma unroll
             for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -516,12 +540,9 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
 template <typename DigT, int MODE>
 int launch_g(const K1Batch& b, cudaStream_t st) {
     const scout_topk_args& a = b.a[0];
-    // qs | pn | pna | max(keys + cls, part_s[P][nb] + part_a[P][nb]) with P*nb <= max(4*K1_THREADS+12, nbs)
-    const size_t nbs = static_cast<size_t>(a.nb_stride);
-    const size_t pmax = 4 * K1_THREADS + 12;  // P * nq <= K1_THREADS
-    const size_t pnb = nbs > pmax ? nbs : pmax;
-    const size_t tail = nbs * 9 > pnb * 12 ? nbs * 9 : pnb * 12;
-    const size_t smem = static_cast<size_t>(D) * a.group * 8 + static_cast<size_t>(D) * 24 + tail;
+    // qs | pn | pna | keys | s_acc | a_acc | cls | digest chunk ring (MODE 0)
+    const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)))
+                                  : k1_stage_offset(a.group, a.nb_stride);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
         scout_host::launch(kern, dim3(a.n_units, b.n), dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
