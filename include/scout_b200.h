@@ -259,7 +259,10 @@ int scout_engine_decode_step(scout_engine* eng, int step, const float* q_true, c
  * D2H of the outputs plus each layer's CPU-side block ids (h_cpu_ids
  * [L][U][k], h_n_cpu [L][U], the host co-attention worker's input) are
  * pipelined by layer chunks on copy streams. Completion is ordered on
- * `stream`: synchronise it before reading the host outputs. */
+ * `stream`: synchronise it before reading the host outputs. As with
+ * cudaMemcpyAsync, the input copies start as soon as the call is made (they
+ * overlap the previous step's attention), so the host inputs must be final
+ * at the call and stay unchanged until `stream` completes the step. */
 int scout_engine_decode_step_host(scout_engine* eng, int step, const float* h_q_true, const float* h_q_pred,
                                   const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o, float* h_out_ml,
                                   int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream);

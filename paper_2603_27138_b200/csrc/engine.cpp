@@ -426,9 +426,11 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
     // ---- inputs, in the order the device needs them: q_true of layer 0 and
     // q_pred (K1's inputs) by chunk first, each chunk releasing a K1 launch on
     // the whole GPU; then q_true / CPU partials by chunk, each publishing a
-    // flag the (already running) persistent K2 polls before planning a layer
+    // flag the (already running) persistent K2 polls before planning a layer.
+    // The sources are host memory, so the copies only wait for this parity's
+    // staging to be free (step n-2 fully done): step n's inputs stream in
+    // while step n-1's K2 still runs.
     if (e->stage_recorded[par]) CU(cudaStreamWaitEvent(e->h2d, e->stage_free[par], 0));
-    CU(cudaStreamWaitEvent(e->h2d, e->ev_start, 0));
     CU(cudaMemcpyAsync(d_qt, h_q_true, qd * 4, cudaMemcpyHostToDevice, e->h2d));
     for (int c = 0; c < nch; ++c) {
         const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
