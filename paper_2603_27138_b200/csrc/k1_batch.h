@@ -9,6 +9,8 @@ constexpr int K1_MAX_LAYERS = 96;
 
 struct K1Batch {
     int n;
+    int nbuf;   // digest ring depth (set at launch)
+    int chunk;  // digest chunk bytes (set at launch)
     scout_topk_args a[K1_MAX_LAYERS];
 };
 

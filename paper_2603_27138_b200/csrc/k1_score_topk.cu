@@ -20,40 +20,44 @@
 // comparisons do), with equal scores ranked by block id through a block scan.
 #include "scout_common.cuh"
 
+#include <cstdlib>
+
 using namespace scout_dev;
 
 namespace {
 
-// 128 threads x 12 CTAs/SM: many small CTAs hide the latency-bound selection
-// phases best (64-layer batch: 1.14 ms vs 1.35 at 256 x 4, 1.63 at 512 x 1)
+// 128 threads, ~30 KB of shared memory, 72 registers: 7 CTAs per SM. Many
+// small CTAs hide the latency-bound selection phases best; a deeper digest ring
+// costs more (fewer CTAs) than it buys (64-layer batch, tools/gpu/k1_sweep.sh:
+// 2 x 8 KiB 0.78 ms, 1 x 16 KiB 0.78, 3 x 8 KiB 0.86, 2 x 32 KiB 1.16)
 #ifndef SCOUT_K1_THREADS
 #define SCOUT_K1_THREADS 128
-#endif
-#ifndef SCOUT_K1_PMAX
-#define SCOUT_K1_PMAX 1
 #endif
 #ifndef SCOUT_K1_MINB
 #define SCOUT_K1_MINB 4
 #endif
 constexpr int K1_THREADS = SCOUT_K1_THREADS;
 static_assert(K1_THREADS >= 128, "one thread per channel when staging the query sums");
-#ifndef SCOUT_K1_NBUF
-#define SCOUT_K1_NBUF 2
-#endif
-constexpr int K1_NBUF = SCOUT_K1_NBUF;          // digest chunk buffers (bulk-copy ring)
-constexpr int K1_CHUNK_BYTES = 16384;           // lo + hi rows of one chunk
+constexpr int K1_MAXBUF = 4;                    // digest chunk buffers (bulk-copy ring), runtime depth <= this
+constexpr int K1_CHUNK_BYTES = 8192;            // lo + hi rows of one chunk (default; SCOUT_K1_CHUNK)
+constexpr int K1_REG_BLOCKS = 4 * K1_THREADS;   // nb_stride up to this: running scores live in registers
 
+// qs [D*G] f64 | pn [D] float2 | keys [nbs] u64 | cls [nbs] u8 | (nbs > K1_REG_BLOCKS:
+// s_acc [nbs] f64 | a_acc [nbs] f32) | digest chunk ring (MODE 0)
 __host__ __device__ inline size_t k1_stage_offset(int G, int nbs) {
-    const size_t head = static_cast<size_t>(D) * G * 8 + static_cast<size_t>(D) * 24 + static_cast<size_t>(nbs) * 21;
+    size_t head = static_cast<size_t>(D) * G * 8 + static_cast<size_t>(D) * 8 + static_cast<size_t>(nbs) * 9;
+    head = (head + 15) / 16 * 16;
+    if (nbs > K1_REG_BLOCKS) head += static_cast<size_t>(nbs) * 12;
     return (head + 127) / 128 * 128;
 }
-__host__ __device__ inline size_t k1_smem_bytes(int G, int nbs, int esz) {
+__host__ __device__ inline size_t k1_chunk_bytes(int nbs, int esz, int chunk) {
     // the chunk is at least one channel of lo + hi rows
     const size_t one = static_cast<size_t>(nbs) * 2 * esz;
-    const size_t chunk = one > static_cast<size_t>(K1_CHUNK_BYTES) ? one : K1_CHUNK_BYTES;
-    return k1_stage_offset(G, nbs) + K1_NBUF * chunk;
+    return one > static_cast<size_t>(chunk) ? one : chunk;
 }
-constexpr int K1_PMAX = SCOUT_K1_PMAX;  // channel parts per block quad in the fast score
+__host__ __device__ inline size_t k1_smem_bytes(int G, int nbs, int esz, int nbuf, int chunk) {
+    return k1_stage_offset(G, nbs) + nbuf * k1_chunk_bytes(nbs, esz, chunk);
+}
 
 }  // namespace
 
@@ -160,37 +164,72 @@ __device__ __forceinline__ double key_to_double(uint64_t k) {
 struct SelScratch {
     uint32_t hist[256];
     uint64_t cand[32];
+    uint64_t wmax[K1_WARPS], wmin[K1_WARPS];
     uint64_t prefix;
     int krem;
     int count;
     int n;
 };
 
-// k-th largest key among the candidates (radix select, 8-bit digits, MSB
-// first; once <= 32 candidates share the prefix one warp finishes by rank).
-// Returns thr and need_eq = how many candidates equal to thr belong to the
-// top k (the lowest ids among them, digest.hpp:108-111). k <= #candidates.
+// k-th largest key among the candidates: radix select with 8-bit digits, MSB
+// first, starting at the highest bit in which the candidates differ (a
+// max / min reduction skips the common prefix, so the first histogram already
+// spreads the keys instead of piling them into one bin); once <= 32
+// candidates share the prefix one warp finishes by rank. Returns thr and
+// need_eq = how many candidates equal to thr belong to the top k (the lowest
+// ids among them, digest.hpp:108-111). k <= #candidates.
 template <class KeyF, class CandF>
 __device__ void radix_kth(int nb, int k, KeyF keyf, CandF candf, SelScratch& S, uint64_t& thr, int& need_eq) {
-    const int tid = threadIdx.x;
-    uint64_t prefix = 0, mask = 0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t kmax = 0, kmin = ~0ull;
+    for (int b = tid; b < nb; b += K1_THREADS) {
+        if (!candf(b)) continue;
+        const uint64_t key = keyf(b);
+        kmax = key > kmax ? key : kmax;
+        kmin = key < kmin ? key : kmin;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const uint64_t x = __shfl_xor_sync(0xffffffffu, kmax, o), y = __shfl_xor_sync(0xffffffffu, kmin, o);
+        kmax = x > kmax ? x : kmax;
+        kmin = y < kmin ? y : kmin;
+    }
+    if (lane == 0) { S.wmax[warp] = kmax; S.wmin[warp] = kmin; }
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < K1_WARPS; ++w) {
+        kmax = S.wmax[w] > kmax ? S.wmax[w] : kmax;
+        kmin = S.wmin[w] < kmin ? S.wmin[w] : kmin;
+    }
+    if (kmax == kmin) {  // every candidate equal (k <= #candidates)
+        thr = kmax;
+        need_eq = k;
+        __syncthreads();
+        return;
+    }
+    int hi = 63 - __clzll(static_cast<long long>(kmax ^ kmin));  // highest differing bit
+    uint64_t mask = hi == 63 ? 0ull : ~((2ull << hi) - 1ull);      // bits above hi: shared by all
+    uint64_t prefix = kmax & mask;
     int krem = k;
-    for (int pass = 0; pass < 8; ++pass) {
-        const int shift = 56 - 8 * pass;
+    while (hi >= 0) {
+        const int w = hi + 1 < 8 ? hi + 1 : 8;
+        const int shift = hi - w + 1;
+        const uint32_t nbin = 1u << w;
         for (int i = tid; i < 256; i += K1_THREADS) S.hist[i] = 0;
         __syncthreads();
         for (int b = tid; b < nb; b += K1_THREADS) {
             if (!candf(b)) continue;
             const uint64_t key = keyf(b);
-            if ((key & mask) == prefix) atomicAdd(&S.hist[(key >> shift) & 255u], 1u);
+            if ((key & mask) == prefix) atomicAdd(&S.hist[(key >> shift) & (nbin - 1u)], 1u);
         }
         __syncthreads();
         if (tid < 32) {
+            // lane l scans bins 255-8l .. 248-8l (bins >= nbin are empty)
             uint32_t cnt[8];
             uint32_t local = 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                cnt[i] = S.hist[255 - 8 * tid - i];  // lane l: bins 255-8l .. 248-8l
+                cnt[i] = S.hist[255 - 8 * tid - i];
                 local += cnt[i];
             }
             uint32_t incl = local;
@@ -217,8 +256,9 @@ __device__ void radix_kth(int nb, int k, KeyF keyf, CandF candf, SelScratch& S, 
         __syncthreads();
         prefix = S.prefix;
         krem = S.krem;
-        mask |= 0xFFull << shift;
-        if (pass < 7 && S.count <= 32) {
+        mask |= static_cast<uint64_t>(nbin - 1u) << shift;
+        hi = shift - 1;
+        if (hi >= 0 && S.count <= 32) {
             // few candidates left: gather them and rank inside one warp
             if (tid == 0) S.n = 0;
             __syncthreads();
@@ -252,23 +292,62 @@ __device__ void radix_kth(int nb, int k, KeyF keyf, CandF candf, SelScratch& S, 
     }
     thr = prefix;
     need_eq = krem;
+    __syncthreads();
 }
 
 enum : uint8_t { CLS_OUT = 0, CLS_IN = 1, CLS_Z = 2 };
+
+// Fast score of one 4-block quad over one chunk of channels (MODE 0): products
+// and the running sum in fp32, flushed to the f64 accumulators every 8
+// channels (<= 16 terms per fp32 chain); a_acc gathers sum |terms| for the band.
+template <typename DigT>
+__device__ __forceinline__ void fast_quad(const DigT* blo, const DigT* bhi, int ns, int b0, int nch, const float2* pn,
+                                          int ch0, double (&s)[4], float (&a)[4]) {
+    for (int c0 = 0; c0 < nch; c0 += 8) {
+        const int c1 = min(nch, c0 + 8);
+        float t[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+        for (int cl = c0; cl < c1; ++cl) {
+            float l[4], h[4];
+            if constexpr (sizeof(DigT) == 2) {
+                const uint2 lv = *reinterpret_cast<const uint2*>(blo + cl * ns + b0);
+                const uint2 hv = *reinterpret_cast<const uint2*>(bhi + cl * ns + b0);
+                l[0] = __uint_as_float(lv.x << 16); l[1] = __uint_as_float(lv.x & 0xFFFF0000u);
+                l[2] = __uint_as_float(lv.y << 16); l[3] = __uint_as_float(lv.y & 0xFFFF0000u);
+                h[0] = __uint_as_float(hv.x << 16); h[1] = __uint_as_float(hv.x & 0xFFFF0000u);
+                h[2] = __uint_as_float(hv.y << 16); h[3] = __uint_as_float(hv.y & 0xFFFF0000u);
+            } else {
+                const float4 lv = *reinterpret_cast<const float4*>(blo + cl * ns + b0);
+                const float4 hv = *reinterpret_cast<const float4*>(bhi + cl * ns + b0);
+                l[0] = lv.x; l[1] = lv.y; l[2] = lv.z; l[3] = lv.w;
+                h[0] = hv.x; h[1] = hv.y; h[2] = hv.z; h[3] = hv.w;
+            }
+            const float2 pv = pn[ch0 + cl];  // (P_c, N_c): sums of the non-negative / negative q_g[c]
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                t[e] = fmaf(h[e], pv.x, fmaf(l[e], pv.y, t[e]));
+                a[e] = fmaf(fabsf(h[e]), pv.x, fmaf(fabsf(l[e]), -pv.y, a[e]));
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[e] += static_cast<double>(t[e]);
+    }
+}
 
 template <typename DigT, int G, int MODE>
 __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(const K1Batch batch) {
     const scout_topk_args& a = batch.a[blockIdx.y];  // layer of this CTA (one launch can cover many)
     extern __shared__ __align__(16) uint8_t k1_smem[];
-    double* qs = reinterpret_cast<double*>(k1_smem);            // [D][G] stacked order
-    double2* pn = reinterpret_cast<double2*>(qs + D * G);       // [D] (sum q>=0, sum q<0)
-    float2* pna = reinterpret_cast<float2*>(pn + D);            // [D] abs sums, rounded up
-    uint64_t* keys = reinterpret_cast<uint64_t*>(pna + D);      // [nb_stride]
-    double* s_acc = reinterpret_cast<double*>(keys + a.nb_stride);  // [nb_stride] running fast scores
-    float* a_acc = reinterpret_cast<float*>(s_acc + a.nb_stride);   // [nb_stride] running sum |terms|
-    uint8_t* cls = reinterpret_cast<uint8_t*>(a_acc + a.nb_stride); // [nb_stride]
-    uint8_t* stagebuf = k1_smem + k1_stage_offset(G, a.nb_stride);  // K1_NBUF x chunk (MODE 0)
-    __shared__ uint64_t s_full[K1_NBUF];
+    const size_t ns = static_cast<size_t>(a.nb_stride);
+    double* qs = reinterpret_cast<double*>(k1_smem);             // [D][G] stacked order
+    float2* pn = reinterpret_cast<float2*>(qs + D * G);          // [D] (sum q>=0, sum q<0) rounded to f32
+    uint64_t* keys = reinterpret_cast<uint64_t*>(pn + D);        // [nb_stride]
+    uint8_t* cls = reinterpret_cast<uint8_t*>(keys + ns);        // [nb_stride]
+    uint8_t* big = k1_smem + (static_cast<size_t>(D) * G * 8 + D * 8 + ns * 9 + 15) / 16 * 16;
+    double* s_acc = reinterpret_cast<double*>(big);              // [nb_stride] (nb_stride > K1_REG_BLOCKS)
+    float* a_acc = reinterpret_cast<float*>(s_acc + ns);         // [nb_stride]
+    uint8_t* stagebuf = k1_smem + k1_stage_offset(G, a.nb_stride);  // nbuf x chunk (MODE 0)
+    __shared__ uint64_t s_full[K1_MAXBUF];
     __shared__ SelScratch S;
     __shared__ int warp_tot[K1_WARPS];
     __shared__ int s_tok[2];
@@ -277,6 +356,32 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
 
     const int u = blockIdx.x;
     const int tid = threadIdx.x;
+    const int nbuf = batch.nbuf;
+    const DigT* lo = static_cast<const DigT*>(a.digests) + static_cast<size_t>(u) * 2 * D * ns;
+    const DigT* hi = lo + D * ns;
+    // digest chunk ring: chunks of `cpc` channels (lo rows + hi rows, 16 KiB at
+    // 512 blocks) stream through shared memory with 1-D bulk copies (TMA
+    // engine). The first copies go out before anything else so the query
+    // staging below hides under them.
+    constexpr int esz = static_cast<int>(sizeof(DigT));
+    const int cpc = max(1, min(D, batch.chunk / (2 * static_cast<int>(ns) * esz)));
+    const int nchunks = (D + cpc - 1) / cpc;
+    const uint32_t lo_bytes = static_cast<uint32_t>(cpc * ns * esz);  // one half of a chunk buffer
+    auto issue = [&](int c) {
+        const int ch0 = c * cpc, nch = min(cpc, D - ch0);
+        const uint32_t bytes = static_cast<uint32_t>(nch * ns * esz);
+        uint8_t* buf = stagebuf + static_cast<size_t>(c % nbuf) * 2 * lo_bytes;
+        mbar_arrive_expect_tx(&s_full[c % nbuf], 2 * bytes);
+        bulk_g2s(buf, lo + ch0 * ns, bytes, &s_full[c % nbuf]);
+        bulk_g2s(buf + lo_bytes, hi + ch0 * ns, bytes, &s_full[c % nbuf]);
+    };
+    if constexpr (MODE == 0) {
+        if (tid == 0) {
+            for (int i = 0; i < nbuf; ++i) mbar_init(&s_full[i], 1);
+            fence_mbar_init();
+            for (int c = 0; c < nbuf && c < nchunks; ++c) issue(c);
+        }
+    }
     // PDL: the next kernel may launch now; this one only reads inputs until it
     // publishes its lists (griddep_wait below orders those writes).
     griddep_launch_dependents();
@@ -285,7 +390,6 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
     ntok = max(0, min(ntok, a.nb_stride * BS));
     const int nb = (ntok + BS - 1) / BS;
     const int tail = ntok - (nb - 1) * BS;
-    const size_t ns = static_cast<size_t>(a.nb_stride);
 
     for (int i = tid; i < D * G; i += K1_THREADS) {
         const int g = i / D, c = i % D;
@@ -300,105 +404,75 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
 
     const int k = a.k;
     const bool take_all = nb <= k;
-    const DigT* lo = static_cast<const DigT*>(a.digests) + static_cast<size_t>(u) * 2 * D * ns;
-    const DigT* hi = lo + D * ns;
 
     if constexpr (MODE == 0) {
-        // ---- fast score: s~_b = sum_c hi_c * P_c + lo_c * N_c  (P_c / N_c = sums of
-        // the non-negative / negative q_g[c]); |s~ - s_ref| <= ~1300 u A_b with
-        // A_b = sum |terms|; eps_b = A_b * 2^-40 covers it with a 6x margin.
+        // ---- fast score s~_b = sum_c hi_c * P_c + lo_c * N_c in fp32 chains of <= 16
+        // terms summed in f64 (P_c / N_c: sums of the non-negative / negative q_g[c],
+        // rounded to f32). Error vs the reference's sequential double sum:
+        //   |s~ - s_ref| <= (16 + 1) u32 A_b + 2^-43 A_b + underflow < A_b 2^-19 + 2^-126
+        // with A_b = sum |terms| (fp32, rounded up by 1.0001). Blocks within the
+        // band of the k-th score are decided exactly below.
         if (tid < D) {
             double P = 0.0, N = 0.0;
-            float Pa = 0.f, Na = 0.f;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
                 const double qv = qs[tid * G + g];
-                if (qv >= 0.0) { P += qv; Pa += static_cast<float>(qv); }
-                else { N += qv; Na -= static_cast<float>(qv); }
+                if (qv >= 0.0) P += qv;
+                else N += qv;
             }
-            pn[tid] = make_double2(P, N);
-            pna[tid] = make_float2(Pa * 1.0001f, Na * 1.0001f);
+            pn[tid] = make_float2(static_cast<float>(P), static_cast<float>(N));
+            // f32-subnormal sums lose the relative bound: decide the unit exactly
+            if ((P != 0.0 && P < 0x1p-126) || (N != 0.0 && N > -0x1p-126))
+                atomicMax(reinterpret_cast<int*>(&s_amax), 0x7f800000);
         }
-        __syncthreads();
-        if (!take_all || a.scores_out) {
-            // Digests stream through shared memory with 1-D bulk copies (TMA
-            // engine): chunks of `cpc` channels (lo rows + hi rows, 16 KiB at
-            // 512 blocks), K1_NBUF-deep, so loads hold no registers and every
-            // CTA keeps a chunk in flight while it computes the previous one.
-            // thread -> block quads j = tid, tid + K1_THREADS, ...; the running
-            // sums live in shared memory (order-free: the score is approximate).
-            const int nq = (nb + 3) >> 2;
-            constexpr int esz = static_cast<int>(sizeof(DigT));
-            const int cpc = max(1, min(D, K1_CHUNK_BYTES / (2 * static_cast<int>(ns) * esz)));
-            const int nchunks = (D + cpc - 1) / cpc;
-            const uint32_t lo_bytes = static_cast<uint32_t>(cpc * ns * esz);  // one half of a chunk buffer
+        const int nq = (nb + 3) >> 2;
+        const bool regs = ns <= static_cast<size_t>(K1_REG_BLOCKS);  // one quad per thread at most
+        if (!regs)
             for (int i = tid; i < nq * 4; i += K1_THREADS) { s_acc[i] = 0.0; a_acc[i] = 0.f; }
-            if (tid == 0) {
-                for (int i = 0; i < K1_NBUF; ++i) mbar_init(&s_full[i], 1);
-                fence_mbar_init();
-            }
-            __syncthreads();
-            auto issue = [&](int c) {
-                const int ch0 = c * cpc, nch = min(cpc, D - ch0);
-                const uint32_t bytes = static_cast<uint32_t>(nch * ns * esz);
-                uint8_t* buf = stagebuf + static_cast<size_t>(c % K1_NBUF) * 2 * lo_bytes;
-                mbar_arrive_expect_tx(&s_full[c % K1_NBUF], 2 * bytes);
-                bulk_g2s(buf, lo + ch0 * ns, bytes, &s_full[c % K1_NBUF]);
-                bulk_g2s(buf + lo_bytes, hi + ch0 * ns, bytes, &s_full[c % K1_NBUF]);
-            };
-            if (tid == 0)
-                for (int c = 0; c < K1_NBUF && c < nchunks; ++c) issue(c);
-            for (int c = 0; c < nchunks; ++c) {
-                mbar_wait(&s_full[c % K1_NBUF], (c / K1_NBUF) & 1);
-                const int ch0 = c * cpc, nch = min(cpc, D - ch0);
-                const DigT* blo = reinterpret_cast<const DigT*>(stagebuf + static_cast<size_t>(c % K1_NBUF) * 2 * lo_bytes);
-                const DigT* bhi = reinterpret_cast<const DigT*>(reinterpret_cast<const uint8_t*>(blo) + lo_bytes);
+        __syncthreads();
+        double rs[4] = {0.0, 0.0, 0.0, 0.0};
+        float ra[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int c = 0; c < nchunks; ++c) {
+            mbar_wait(&s_full[c % nbuf], (c / nbuf) & 1);
+            const int ch0 = c * cpc, nch = min(cpc, D - ch0);
+            const DigT* blo = reinterpret_cast<const DigT*>(stagebuf + static_cast<size_t>(c % nbuf) * 2 * lo_bytes);
+            const DigT* bhi = reinterpret_cast<const DigT*>(reinterpret_cast<const uint8_t*>(blo) + lo_bytes);
+            if (regs) {
+                if (tid < nq) fast_quad<DigT>(blo, bhi, static_cast<int>(ns), 4 * tid, nch, pn, ch0, rs, ra);
+            } else {
                 for (int j = tid; j < nq; j += K1_THREADS) {
-                    const int b0 = 4 * j;
-                    double s0 = s_acc[b0], s1 = s_acc[b0 + 1], s2 = s_acc[b0 + 2], s3 = s_acc[b0 + 3];
-                    float a0 = a_acc[b0], a1 = a_acc[b0 + 1], a2 = a_acc[b0 + 2], a3 = a_acc[b0 + 3];
-#pragma unroll 4
-                    for (int cl = 0; cl < nch; ++cl) {
-                        float l[4], h[4];
-                        if constexpr (sizeof(DigT) == 2) {
-                            const uint2 lv = *reinterpret_cast<const uint2*>(blo + cl * ns + b0);
-                            const uint2 hv = *reinterpret_cast<const uint2*>(bhi + cl * ns + b0);
-                            l[0] = __uint_as_float(lv.x << 16); l[1] = __uint_as_float(lv.x & 0xFFFF0000u);
-                            l[2] = __uint_as_float(lv.y << 16); l[3] = __uint_as_float(lv.y & 0xFFFF0000u);
-                            h[0] = __uint_as_float(hv.x << 16); h[1] = __uint_as_float(hv.x & 0xFFFF0000u);
-                            h[2] = __uint_as_float(hv.y << 16); h[3] = __uint_as_float(hv.y & 0xFFFF0000u);
-                        } else {
-                            const float4 lv = *reinterpret_cast<const float4*>(blo + cl * ns + b0);
-                            const float4 hv = *reinterpret_cast<const float4*>(bhi + cl * ns + b0);
-                            l[0] = lv.x; l[1] = lv.y; l[2] = lv.z; l[3] = lv.w;
-                            h[0] = hv.x; h[1] = hv.y; h[2] = hv.z; h[3] = hv.w;
-                        }
-                        const double2 pv = pn[ch0 + cl];
-                        const float2 pa = pna[ch0 + cl];
-                        s0 = fma(static_cast<double>(h[0]), pv.x, s0); s0 = fma(static_cast<double>(l[0]), pv.y, s0);
-                        s1 = fma(static_cast<double>(h[1]), pv.x, s1); s1 = fma(static_cast<double>(l[1]), pv.y, s1);
-                        s2 = fma(static_cast<double>(h[2]), pv.x, s2); s2 = fma(static_cast<double>(l[2]), pv.y, s2);
-                        s3 = fma(static_cast<double>(h[3]), pv.x, s3); s3 = fma(static_cast<double>(l[3]), pv.y, s3);
-                        a0 = fmaf(fabsf(h[0]), pa.x, fmaf(fabsf(l[0]), pa.y, a0));
-                        a1 = fmaf(fabsf(h[1]), pa.x, fmaf(fabsf(l[1]), pa.y, a1));
-                        a2 = fmaf(fabsf(h[2]), pa.x, fmaf(fabsf(l[2]), pa.y, a2));
-                        a3 = fmaf(fabsf(h[3]), pa.x, fmaf(fabsf(l[3]), pa.y, a3));
-                    }
-                    s_acc[b0] = s0; s_acc[b0 + 1] = s1; s_acc[b0 + 2] = s2; s_acc[b0 + 3] = s3;
-                    a_acc[b0] = a0; a_acc[b0 + 1] = a1; a_acc[b0 + 2] = a2; a_acc[b0 + 3] = a3;
-                }
-                __syncthreads();  // buffer drained by every thread: refill it
-                if (tid == 0 && c + K1_NBUF < nchunks) issue(c + K1_NBUF);
-            }
-            float amax = 0.f;
-            for (int b = tid; b < nb; b += K1_THREADS) {
-                keys[b] = score_key(s_acc[b]);
-                amax = fmaxf(amax, a_acc[b] * 1.0001f);
-            }
+                    double s4[4];
+                    float a4[4];
 #pragma unroll
-            for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-            if ((tid & 31) == 0) atomicMax(reinterpret_cast<int*>(&s_amax), __float_as_int(amax));
+                    for (int e = 0; e < 4; ++e) { s4[e] = s_acc[e * nq + j]; a4[e] = a_acc[e * nq + j]; }
+                    fast_quad<DigT>(blo, bhi, static_cast<int>(ns), 4 * j, nch, pn, ch0, s4, a4);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) { s_acc[e * nq + j] = s4[e]; a_acc[e * nq + j] = a4[e]; }
+                }
+            }
+            __syncthreads();  // buffer drained by every thread: refill it
+            if (tid == 0 && c + nbuf < nchunks) issue(c + nbuf);
         }
+        float amax = 0.f;
+        if (regs) {
+            if (tid < nq)
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (4 * tid + e < nb) {
+                        keys[4 * tid + e] = score_key(rs[e]);
+                        amax = fmaxf(amax, ra[e] * 1.0001f);
+                    }
+        } else {
+            for (int b = tid; b < nb; b += K1_THREADS) {
+                keys[b] = score_key(s_acc[(b & 3) * nq + (b >> 2)]);
+                amax = fmaxf(amax, a_acc[(b & 3) * nq + (b >> 2)] * 1.0001f);
+            }
+        }
+        // NaN / inf (fp32 overflow) -> an infinite band: every block is decided exactly
+        if (!(amax <= 3.0e38f)) amax = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        if ((tid & 31) == 0) atomicMax(reinterpret_cast<int*>(&s_amax), __float_as_int(amax));
         if (a.scores_out)  // exact reference-order scores (tests / diagnostics only)
             for (int b = tid; b < nb; b += K1_THREADS)
                 a.scores_out[u * ns + b] = exact_score_minmax<DigT, G>(lo, hi, ns, b, qs);
@@ -429,7 +503,7 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
         int dummy;
         radix_kth(nb, k, [&](int b) { return keys[b]; }, [](int) { return true; }, S, tkey, dummy);
         const double T = key_to_double(tkey);
-        const double band = 2.0 * static_cast<double>(s_amax) * 0x1p-40;
+        const double band = 2.0 * (static_cast<double>(s_amax) * 0x1p-19 + 0x1p-126);
         int nin = 0, nz = 0;
         for (int b = tid; b < nb; b += K1_THREADS) {
             const double v = key_to_double(keys[b]);
@@ -538,10 +612,23 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
 }
 
 template <typename DigT, int MODE>
-int launch_g(const K1Batch& b, cudaStream_t st) {
+int launch_g(K1Batch& b, cudaStream_t st) {
     const scout_topk_args& a = b.a[0];
-    // qs | pn | pna | keys | s_acc | a_acc | cls | digest chunk ring (MODE 0)
-    const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)))
+    // digest ring depth (tuning knob SCOUT_K1_NBUF, 1..K1_MAXBUF)
+    // and chunk bytes (SCOUT_K1_CHUNK, 4096..65536)
+    static const int nbuf_env = [] {
+        const char* e = getenv("SCOUT_K1_NBUF");
+        const int v = e ? atoi(e) : 2;
+        return v < 1 ? 1 : (v > K1_MAXBUF ? K1_MAXBUF : v);
+    }();
+    static const int chunk_env = [] {
+        const char* e = getenv("SCOUT_K1_CHUNK");
+        const int v = e ? atoi(e) : K1_CHUNK_BYTES;
+        return v < 4096 ? 4096 : (v > 65536 ? 65536 : v);
+    }();
+    b.nbuf = nbuf_env;
+    b.chunk = chunk_env;
+    const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)), b.nbuf, b.chunk)
                                   : k1_stage_offset(a.group, a.nb_stride);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
@@ -584,7 +671,7 @@ int validate(const scout_topk_args& a) {
     return SCOUT_OK;
 }
 
-int launch_batch(const K1Batch& b, cudaStream_t st) {
+int launch_batch(K1Batch& b, cudaStream_t st) {
     using namespace scout_host;
     const scout_topk_args& a = b.a[0];
     int rc = -1;
