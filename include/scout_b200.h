@@ -93,6 +93,20 @@ int scout_digest_build(const void* kv_pool, int kv_dtype, int method, int n, con
                        const int32_t* block_rows, const int32_t* units, const int32_t* block_ids,
                        void* digests, int nb_stride, void* stream);
 
+/* Decode-time append (append_token kv_store.hpp:90-117, one layer, data
+ * side): for every unit u, the f32 rows k_rows[u] / v_rows[u] ([n_units][128])
+ * go to row n_tokens[u] % 64 of pool slot open_slot[u] (the caller hands a
+ * fresh slot when that row is 0, i.e. a new block opens), and the digest column
+ * of block n_tokens[u] / 64 is updated in place: minmax continues the
+ * reference's min/max fold by one row (bit-identical to rebuilding the open
+ * block, kv_store.hpp:108); mean recomputes the sequential double column sum
+ * of the stored rows / rows (f64 digests). advance != 0 also increments
+ * n_tokens[u] (set it on the last layer appended: n_tokens is shared by the
+ * layers). A block is sealed when n_tokens becomes a multiple of 64.        */
+int scout_kv_append(void* kv_pool, int kv_dtype, int method, int n_units, const int32_t* open_slot,
+                    int32_t* n_tokens, const float* k_rows, const float* v_rows, void* digests, int nb_stride,
+                    int advance, void* stream);
+
 /* ------------------------------------------------------------------ K1 --
  * Score + top-k + resident/CPU split for n_units units of one layer
  * (digest_score digest.hpp:62-72, select_topk :101-118, set_intersection /

@@ -26,7 +26,7 @@ BLOCK_SIZE = 64
 # every extern "C" symbol of include/scout_b200.h
 EXPORTED = (
     "scout_last_error", "scout_version", "scout_slot_bytes",
-    "scout_kv_write_tokens", "scout_kv_read_tokens", "scout_digest_build",
+    "scout_kv_write_tokens", "scout_kv_read_tokens", "scout_digest_build", "scout_kv_append",
     "scout_score_topk_split", "scout_score_topk_split_batch", "scout_sparse_decode_workspace_bytes",
     "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather", "scout_recall_copy",
     "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
@@ -96,6 +96,7 @@ def lib() -> C.CDLL:
         L.scout_kv_write_tokens.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_kv_read_tokens.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_digest_build.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]
+        L.scout_kv_append.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_score_topk_split.argtypes = [C.POINTER(TopkArgs), _vp]
         L.scout_score_topk_split_batch.argtypes = [C.POINTER(TopkArgs), C.c_int, _vp]
         L.scout_sparse_decode_workspace_bytes.restype = C.c_size_t

@@ -35,6 +35,12 @@ __device__ __forceinline__ float from_f32<float>(float x) {
 __device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
 __device__ __forceinline__ float to_f32(float x) { return x; }
 
+// std::min / std::max as build_digest folds them (digest.hpp:45-46): the
+// running value is kept unless the new row compares strictly below / above,
+// so signed zeros and NaNs fold exactly as in the reference.
+__device__ __forceinline__ float ref_min(float acc, float v) { return v < acc ? v : acc; }
+__device__ __forceinline__ float ref_max(float acc, float v) { return acc < v ? v : acc; }
+
 // One CTA of 128 threads per token row: thread = channel.
 template <typename T>
 __global__ void kv_write_kernel(uint8_t* pool, const int32_t* slots, const int32_t* rows,
@@ -75,8 +81,8 @@ __global__ void digest_minmax_kernel(const uint8_t* pool, int n, const int32_t* 
     float hi = lo;
     for (int r = 1; r < rows; ++r) {
         const float v = to_f32(k[elem_index<T>(r, c)]);
-        lo = fminf(lo, v);
-        hi = fmaxf(hi, v);
+        lo = ref_min(lo, v);
+        hi = ref_max(hi, v);
     }
     T* dig = digests + static_cast<size_t>(units[i]) * 2 * D * nb_stride;
     dig[static_cast<size_t>(c) * nb_stride + block_ids[i]] = from_f32<T>(lo);
@@ -98,7 +104,80 @@ __global__ void digest_mean_kernel(const uint8_t* pool, int n, const int32_t* sl
     digests[static_cast<size_t>(units[i]) * D * nb_stride + static_cast<size_t>(c) * nb_stride + block_ids[i]] = s;
 }
 
+// Append one token to the open block of each unit (append_token,
+// kv_store.hpp:90-117, one layer): the row lands at row n_tokens[u] % 64 of
+// slot open_slot[u]; the digest column of block n_tokens[u] / 64 continues the
+// reference's fold by one row (minmax: the fold of build_digest over the rows
+// so far, bit-identical to rebuilding the open block as kv_store.hpp:108 does;
+// mean: sequential double column sum over the stored rows / rows).
+// Thread = channel, CTA = unit.
+template <typename T, int METHOD>
+__global__ void kv_append_kernel(uint8_t* pool, const int32_t* open_slot, int32_t* n_tokens, const float* k_rows,
+                                 const float* v_rows, void* digests, int nb_stride, int advance) {
+    const int u = blockIdx.x, c = threadIdx.x;
+    const int pos = n_tokens[u];
+    const int r = pos % BS, blk = pos / BS;
+    const size_t tile = BS * D;
+    T* base = reinterpret_cast<T*>(pool + static_cast<size_t>(open_slot[u]) * (2 * tile * sizeof(T)));
+    const size_t off = elem_index<T>(r, c);
+    const T kq = from_f32<T>(k_rows[static_cast<size_t>(u) * D + c]);
+    base[off] = kq;
+    base[tile + off] = from_f32<T>(v_rows[static_cast<size_t>(u) * D + c]);
+    if constexpr (METHOD == SCOUT_DIGEST_MINMAX) {
+        T* dig = static_cast<T*>(digests) + static_cast<size_t>(u) * 2 * D * nb_stride;
+        T& lo = dig[static_cast<size_t>(c) * nb_stride + blk];
+        T& hi = dig[static_cast<size_t>(D + c) * nb_stride + blk];
+        const float v = to_f32(kq);
+        if (r == 0) {
+            lo = kq;
+            hi = kq;
+        } else {
+            lo = from_f32<T>(ref_min(to_f32(lo), v));
+            hi = from_f32<T>(ref_max(to_f32(hi), v));
+        }
+    } else {
+        // the row just written is read back with the others (same stream order)
+        __syncthreads();
+        double s = 0.0;
+        for (int rr = 0; rr <= r; ++rr) s = __dadd_rn(s, static_cast<double>(to_f32(base[elem_index<T>(rr, c)])));
+        static_cast<double*>(digests)[static_cast<size_t>(u) * D * nb_stride + static_cast<size_t>(c) * nb_stride + blk] =
+            __ddiv_rn(s, static_cast<double>(r + 1));
+    }
+    if (advance) {
+        __syncthreads();
+        if (c == 0) n_tokens[u] = pos + 1;
+    }
+}
+
 }  // namespace
+
+extern "C" int scout_kv_append(void* kv_pool, int kv_dtype, int method, int n_units, const int32_t* open_slot,
+                               int32_t* n_tokens, const float* k_rows, const float* v_rows, void* digests,
+                               int nb_stride, int advance, void* stream) {
+    using namespace scout_host;
+    if (n_units < 0 || nb_stride <= 0 ||
+        (n_units > 0 && (!kv_pool || !open_slot || !n_tokens || !k_rows || !v_rows || !digests))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "append_token: bad arguments");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (n_units == 0) return SCOUT_OK;
+    auto st = static_cast<cudaStream_t>(stream);
+    auto pool = static_cast<uint8_t*>(kv_pool);
+    const int adv = advance ? 1 : 0;
+    if (method == SCOUT_DIGEST_MINMAX && kv_dtype == SCOUT_BF16)
+        kv_append_kernel<__nv_bfloat16, SCOUT_DIGEST_MINMAX><<<n_units, D, 0, st>>>(pool, open_slot, n_tokens, k_rows, v_rows, digests, nb_stride, adv);
+    else if (method == SCOUT_DIGEST_MINMAX && kv_dtype == SCOUT_F32)
+        kv_append_kernel<float, SCOUT_DIGEST_MINMAX><<<n_units, D, 0, st>>>(pool, open_slot, n_tokens, k_rows, v_rows, digests, nb_stride, adv);
+    else if (method == SCOUT_DIGEST_MEAN && kv_dtype == SCOUT_BF16)
+        kv_append_kernel<__nv_bfloat16, SCOUT_DIGEST_MEAN><<<n_units, D, 0, st>>>(pool, open_slot, n_tokens, k_rows, v_rows, digests, nb_stride, adv);
+    else if (method == SCOUT_DIGEST_MEAN && kv_dtype == SCOUT_F32)
+        kv_append_kernel<float, SCOUT_DIGEST_MEAN><<<n_units, D, 0, st>>>(pool, open_slot, n_tokens, k_rows, v_rows, digests, nb_stride, adv);
+    else {
+        set_error(SCOUT_ERR_UNSUPPORTED, "scout_kv_append: method %d / kv dtype %d unsupported", method, kv_dtype);
+        return SCOUT_ERR_UNSUPPORTED;
+    }
+    return check_launch("scout_kv_append");
+}
 
 extern "C" int scout_kv_write_tokens(void* kv_pool, int kv_dtype, const int32_t* slots, const int32_t* rows,
                                      const float* k_rows, const float* v_rows, int n, void* stream) {

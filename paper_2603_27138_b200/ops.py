@@ -77,6 +77,19 @@ def digest_build(pool, kv_dtype, method, slots, block_rows, units, block_ids, di
                                        _stream()))
 
 
+def kv_append(pool, kv_dtype, method, open_slot, n_tokens, k_rows, v_rows, digests, nb_stride, advance=True):
+    """append_token (kv_store.hpp:90-117) for one layer of every unit: rows to
+    the open block, digest column updated in place, n_tokens advanced."""
+    dev = pool.device
+    open_slot = _i32(open_slot, dev)
+    assert n_tokens.dtype == torch.int32 and n_tokens.device == dev
+    k_rows = torch.as_tensor(k_rows, dtype=torch.float32, device=dev).contiguous()
+    v_rows = torch.as_tensor(v_rows, dtype=torch.float32, device=dev).contiguous()
+    A.check(A.lib().scout_kv_append(_p(pool), dtype_code(kv_dtype), int(method), int(open_slot.numel()),
+                                    _p(open_slot), _p(n_tokens), _p(k_rows), _p(v_rows), _p(digests),
+                                    int(nb_stride), int(bool(advance)), _stream()))
+
+
 def score_topk_split(q, digests, n_tokens, k, group, *, method=A.SCOUT_DIGEST_MINMAX, block_table=None, step=0,
                      k_stride=None, want_scores=False, last_selected=None, out=None):
     """K1. q [units*G][128] (f32, or f64 for f64 digests); digests [units][2|1][128][nb_stride].

@@ -49,6 +49,22 @@ def make_digests(rng, U, nbs, kind="iid", dtype=np.float32):
                 perm = rng.permutation(D)
                 w = rng.integers(0, 3)
                 a[u, :, j], b[u, :, j] = base[u, w, 0, perm], base[u, w, 1, perm]
+    elif kind == "ulp":
+        # one base digest per unit; every block moves 1-3 channels by one bf16
+        # ulp, so scores differ by ~2^-18 of sum |terms|: inside K1's fp32 band
+        base = bf16_round(rng.standard_normal((U, 2, D)).astype(np.float32))
+        a = np.repeat(base[:, 0, :, None], nbs, axis=2).copy()
+        b = np.repeat(base[:, 1, :, None], nbs, axis=2).copy()
+        for u in range(U):
+            for j in range(nbs):
+                for c in rng.integers(0, D, size=rng.integers(1, 4)):
+                    for arr in (a, b):
+                        bits = int(np.array([arr[u, c, j]], np.float32).view(np.uint32)[0])
+                        bits = (bits + int(rng.choice([1, -1])) * 65536) & 0xFFFFFFFF
+                        arr[u, c, j] = np.array([bits], np.uint32).view(np.float32)[0]
+    elif kind == "huge":  # products overflow fp32 (K1 falls back to the exact path)
+        a = (rng.standard_normal((U, D, nbs)) * 1e36).astype(np.float32)
+        b = (rng.standard_normal((U, D, nbs)) * 1e36).astype(np.float32)
     else:
         a = rng.standard_normal((U, D, nbs)).astype(np.float32)
         b = rng.standard_normal((U, D, nbs)).astype(np.float32)
@@ -61,4 +77,8 @@ def make_queries(rng, U, G, kind="iid"):
         return rng.integers(-1, 2, size=(U * G, D)).astype(np.float32)
     if kind == "perm":  # constant over channels (per head) so channel permutations keep the term multiset
         return np.repeat(rng.standard_normal((U * G, 1)), D, axis=1).astype(np.float32)
+    if kind == "tinyq":  # query sums below the f32 normal range (K1's relative bound does not hold)
+        return (rng.standard_normal((U * G, D)) * 1e-39).astype(np.float32)
+    if kind == "huge":
+        return (rng.standard_normal((U * G, D)) * 1e4).astype(np.float32)
     return rng.standard_normal((U * G, D)).astype(np.float32)

@@ -97,3 +97,74 @@ def test_recall_copy_engine_path(cuda, dtype):
     for src, d in ((8, 5), (0, 1), (3, 2)):
         assert torch.equal(p[d * sb:(d + 1) * sb], host[src * sb:(src + 1) * sb])
     assert torch.count_nonzero(p[:sb]) == 0
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("method", [0, 1])
+def test_kv_append_incremental_digest(cuda, dtype, method):
+    """append_token (kv_store.hpp:90-117) on the GPU: after every append the
+    open block's digest equals build_digest over its rows (digest.hpp:34-60),
+    bit for bit, sealed blocks keep theirs, and the rows read back exactly."""
+    rng = np.random.default_rng(17 + method)
+    dev = torch.device("cuda")
+    U, nbs, steps = 5, 8, 140
+    start = np.array([0, 63, 64, 130, 7], np.int32)
+    n_slots = U * nbs
+    pool = ops.alloc_pool(n_slots, dtype)
+    ddt = torch.float64 if method == 1 else dtype
+    digests = torch.zeros((U, 1 if method == 1 else 2, D, nbs), dtype=ddt, device=dev)
+    rows_k = [[] for _ in range(U)]  # per unit, per block: list of K rows (kv-dtype rounded, f64)
+    rows_v = [[] for _ in range(U)]
+    slot_of = np.full((U, nbs), -1, np.int64)
+    free = list(range(n_slots))[::-1]
+    rnd = (lambda x: torch.from_numpy(x).to(dtype).double().numpy()) if dtype == torch.bfloat16 else \
+        (lambda x: x.astype(np.float64))
+    # prefill: the open block state before the first decode append
+    n_tok = torch.zeros(U, dtype=torch.int32, device=dev)
+    for u in range(U):
+        for t in range(start[u]):
+            b = t // 64
+            if t % 64 == 0:
+                slot_of[u, b] = free.pop()
+                rows_k[u].append([]), rows_v[u].append([])
+            kr, vr = rng.standard_normal(D).astype(np.float32), rng.standard_normal(D).astype(np.float32)
+            rows_k[u][b].append(rnd(kr)), rows_v[u][b].append(rnd(vr))
+            ops.kv_write_tokens(pool, dtype, [slot_of[u, b]], [t % 64], torch.from_numpy(kr)[None],
+                                torch.from_numpy(vr)[None])
+        for b in range(len(rows_k[u])):
+            ops.digest_build(pool, dtype, method, [slot_of[u, b]], [len(rows_k[u][b])], [u], [b], digests, nbs)
+    n_tok.copy_(torch.from_numpy(start))
+    for _ in range(steps):
+        pos = n_tok.cpu().numpy()
+        open_slot = np.zeros(U, np.int32)
+        for u in range(U):
+            b = pos[u] // 64
+            if pos[u] % 64 == 0:
+                slot_of[u, b] = free.pop()
+                rows_k[u].append([]), rows_v[u].append([])
+            open_slot[u] = slot_of[u, b]
+        kr = rng.standard_normal((U, D)).astype(np.float32)
+        vr = rng.standard_normal((U, D)).astype(np.float32)
+        ops.kv_append(pool, dtype, method, open_slot, n_tok, torch.from_numpy(kr), torch.from_numpy(vr), digests, nbs)
+        dg = digests.double().cpu().numpy()
+        for u in range(U):
+            b = pos[u] // 64
+            rows_k[u][b].append(rnd(kr[u])), rows_v[u][b].append(rnd(vr[u]))
+            want = P.build_digest(np.array(rows_k[u][b]), method)
+            if method == 0:
+                assert np.array_equal(dg[u, 0, :, b].view(np.uint64), want[0].view(np.uint64))
+                assert np.array_equal(dg[u, 1, :, b].view(np.uint64), want[1].view(np.uint64))
+            else:
+                assert np.array_equal(dg[u, 0, :, b].view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(n_tok.cpu().numpy(), start + steps)
+    # every block (sealed and open) digest and rows intact at the end
+    dg = digests.double().cpu().numpy()
+    for u in range(U):
+        for b in range(len(rows_k[u])):
+            want = P.build_digest(np.array(rows_k[u][b]), method)
+            got = dg[u, 0, :, b] if method == 1 else np.stack([dg[u, 0, :, b], dg[u, 1, :, b]])
+            assert np.array_equal(np.asarray(got).view(np.uint64), np.asarray(want).view(np.uint64))
+            n = len(rows_k[u][b])
+            k2, v2 = ops.kv_read_tokens(pool, dtype, [slot_of[u, b]] * n, list(range(n)))
+            assert np.array_equal(k2.cpu().double().numpy(), np.array(rows_k[u][b]))
+            assert np.array_equal(v2.cpu().double().numpy(), np.array(rows_v[u][b]))

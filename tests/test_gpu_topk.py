@@ -70,6 +70,26 @@ def test_topk_split_vs_oracle(cuda, G, kind, dtype):
             assert np.array_equal(got["scores"][u, :nb].view(np.uint64), want["scores"][u, :nb].view(np.uint64))
 
 
+@pytest.mark.parametrize("G", [1, 8])
+@pytest.mark.parametrize("kind", ["ulp", "tinyq", "huge"])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+def test_topk_band_edges_vs_oracle(cuda, G, kind, dtype):
+    """Inputs aimed at K1's fast-score band: ulp-level score gaps (exact path
+    decides), f32-subnormal query sums and fp32 overflow (whole unit exact)."""
+    rng = np.random.default_rng(hash(("edge", G, kind, str(dtype))) % 2**32)
+    U, nbs = 12, nbs_for(200)
+    n_tokens = np.full(U, 64 * 200 - 17, np.int32)
+    dig = make_digests(rng, U, nbs, "ulp" if kind == "ulp" else ("huge" if kind == "huge" else "iid"))
+    q = make_queries(rng, U, G, kind if kind != "ulp" else "iid")
+    for k in (1, 16, 64):
+        want = P.score_topk_split(q, dig, n_tokens, k, G, k_stride=k)
+        got = _gpu_topk(q, dig, n_tokens, k, G, dtype=dtype)
+        for u in range(U):
+            ns = want["n_sel"][u]
+            assert got["n_sel"][u] == ns
+            assert np.array_equal(got["sel_ids"][u, :ns], want["sel_ids"][u, :ns]), (kind, u, k)
+
+
 def test_topk_generic_f64_paths(cuda):
     """Arbitrary doubles (the drop-in wrapper's path): minmax and mean, no fma."""
     rng = np.random.default_rng(7)
