@@ -228,6 +228,67 @@ int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host_blocks,
 int scout_recall_copy(void* kv_pool, int kv_dtype, const void* host_blocks, const int64_t* src_index,
                       const int32_t* dst_slots, int n, void* stream);
 
+/* ------------------------------------------------------------------ K5 --
+ * Device-resident tier bookkeeping: the GPU mirror of TieredKvCache's
+ * per-layer state (kv_store.hpp:296-305) for n_units units of ONE layer, so
+ * residency planning, LRU eviction and recall tickets never leave the device.
+ * Clock ticks encode the reference's (step, layer) pairs as
+ * step * n_layers + layer (pair order == integer order).
+ * All arrays are device memory, row stride nb_stride blocks ([U][nb_stride])
+ * or slots_per_unit (free stack); zero-initialise tier, fill table / ready
+ * with -1, and push the (layer, unit)'s pool slots onto free_slots.        */
+typedef struct scout_tier_layer {
+    int32_t* table;       /* [U][nbs] pool slot of a fast or in-flight block, -1 otherwise */
+    uint8_t* tier;        /* [U][nbs] 1 = fast, 0 = slow (Tier, kv_store.hpp:19) */
+    int32_t* last_sel;    /* [U][nbs] last_selected step (K1 writes it: mark_selected) */
+    int32_t* ready;       /* [U][nbs] ready tick of an in-flight recall, -1 none */
+    int32_t* ticket;      /* [U][nbs] issue number of that recall (apply order) */
+    int32_t* free_slots;  /* [U][slots_per_unit] stack of free pool slots */
+    int32_t* n_free;      /* [U] */
+    int32_t* err;         /* [U] sticky first error of the unit (0 none): 1 invalid
+                             argument (reference throws std::invalid_argument), 2 out of slots */
+    int capacity;         /* sealed fast blocks per unit; <= 0: pinned layer (pin_layer) */
+    int slots_per_unit;
+} scout_tier_layer;
+
+/* append_token's bookkeeping (kv_store.hpp:95-115), n_tokens = count BEFORE
+ * the append: a new block takes a free slot, is fast and marked clock_step;
+ * the append that fills a block seals it (mark = clock_step) and enforces
+ * capacity (LRU victim, ties -> lower id, kv_store.hpp:333-345). open_slot[u]
+ * receives the slot to hand scout_kv_append; sealed_id[u] the block sealed by
+ * this append or -1 (its image goes to the host tier: write-through).     */
+int scout_tier_append(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
+                      int clock_step, int32_t* open_slot, int32_t* sealed_id, void* stream);
+/* begin_layer's application for this layer (kv_store.hpp:201-218): blocks
+ * whose recall is ready at or before due_tick become fast, ticket by ticket,
+ * each followed by enforce_capacity. n_applied[u] (optional) counts them.  */
+int scout_tier_apply(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
+                     int due_tick, int32_t* n_applied, void* stream);
+/* schedule_recall (kv_store.hpp:175-197) per unit: ids[u][0..n_ids[u]) an
+ * ascending set of sealed, slow, not-in-flight blocks (else the unit's ticket
+ * is rejected: err = 1, dst_slots = -1); n_ids[u] == 0 skips the unit.
+ * Accepted blocks get a free pool slot, written to dst_slots[u][i] (the copy
+ * engines' destination), and ready_tick / ticket.                          */
+int scout_tier_schedule_recall(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
+                               const int32_t* ids, const int32_t* n_ids, int k_stride, int ready_tick, int ticket,
+                               int32_t* dst_slots, void* stream);
+/* residency_set (kv_store.hpp:156-170) as K1's block table [U][nb_stride]:
+ * the slot of every fast block and of every in-flight block ready by
+ * next_tick (= next_run_of(layer), kv_store.hpp:328-331), -1 elsewhere.    */
+int scout_tier_plan(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
+                    int next_tick, int32_t* block_table, void* stream);
+/* mark_selected (kv_store.hpp:222-228) for explicit ascending id lists
+ * (K1 marks its own selections through scout_topk_args.last_selected).     */
+int scout_tier_mark(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* ids,
+                    const int32_t* n_ids, int k_stride, int step, void* stream);
+/* place_after_prefill (kv_store.hpp:271-283): keep[u] = ascending ids of the
+ * top-capacity sealed blocks (K1 over the sealed blocks, k = capacity); the
+ * other sealed blocks go slow and free their slots; a kept block that was
+ * slow takes a free slot, returned in fill_slots[u][i] (optional, else -1)
+ * so the caller copies its image in. No-op for pinned layers.              */
+int scout_tier_place(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
+                     const int32_t* keep, const int32_t* n_keep, int k_stride, int32_t* fill_slots, void* stream);
+
 /* ------------------------------------------------------------- engine --
  * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,
  * engine.hpp:205-314, GPU side): per layer i, K1 for layer i+1 with the

@@ -76,6 +76,20 @@ def ref():
             L.ref_cpu_baseline.argtypes = [C.c_int] * 6 + [_dp, _dp, _ip, _dp, _ip, C.c_int, C.c_int, C.c_int,
                                                            C.POINTER(dbl)]
             L.ref_cpu_baseline.restype = dbl
+            ll, vp = C.c_longlong, C.c_void_p
+            L.ref_cache_new.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, ll]
+            L.ref_cache_new.restype = vp
+            L.ref_cache_free.argtypes = [vp]
+            L.ref_cache_pin.argtypes = [vp, C.c_int]
+            L.ref_cache_append.argtypes = [vp, C.c_int, _dp, _dp, C.c_int]
+            L.ref_cache_append.restype = ll
+            L.ref_cache_begin_layer.argtypes = [vp, ll, C.c_int]
+            L.ref_cache_schedule_recall.argtypes = [vp, C.c_int, _ip, C.c_int, ll, C.c_int]
+            L.ref_cache_mark_selected.argtypes = [vp, C.c_int, _ip, C.c_int, ll]
+            L.ref_cache_residency.argtypes = [vp, C.c_int, _ip]
+            L.ref_cache_state.argtypes = [vp, C.c_int, _ip, _lp, _ip]
+            L.ref_cache_place.argtypes = [vp, C.c_int, _dp, C.c_int]
+            L.ref_cache_digests.argtypes = [vp, C.c_int, C.c_int, C.c_int, _dp]
         _c["r"] = L
     return _c["r"]
 
@@ -203,3 +217,59 @@ def finalize(p: Partial, lib=None):
     if fn(d, f64(p.o_acc), p.denom, p.count, out) != 0:
         raise ValueError("finalize: empty partial")
     return out
+
+
+class RefCache:
+    """The reference TieredKvCache (kv_store.hpp) behind oracle/_ref (checker only)."""
+
+    def __init__(self, layers, head_dim, capacity, block_size=64, method=0):
+        self.L = ref()
+        if self.L is None:
+            raise RuntimeError("oracle/_ref/libscout_ref.so not built")
+        self.h = self.L.ref_cache_new(layers, block_size, head_dim, method, capacity)
+        self.d = head_dim
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_cache_free(self.h)
+
+    def pin_layer(self, layer):
+        self.L.ref_cache_pin(self.h, layer)
+
+    def append_token(self, layer, k, v):
+        r = self.L.ref_cache_append(self.h, layer, f64(k), f64(v), self.d)
+        if r == -2:
+            raise ValueError("append_token")
+        return None if r < 0 else int(r)
+
+    def begin_layer(self, step, layer):
+        return self.L.ref_cache_begin_layer(self.h, step, layer)
+
+    def schedule_recall(self, layer, ids, issue_step, issue_layer):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        if self.L.ref_cache_schedule_recall(self.h, layer, ids, len(ids), issue_step, issue_layer) != 0:
+            raise ValueError("schedule_recall")
+
+    def mark_selected(self, layer, ids, step):
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        if self.L.ref_cache_mark_selected(self.h, layer, ids, len(ids), step) != 0:
+            raise ValueError("mark_selected")
+
+    def residency_set(self, layer, max_blocks=8192):
+        out = np.zeros(max_blocks, np.int32)
+        n = self.L.ref_cache_residency(self.h, layer, out)
+        return out[:n]
+
+    def state(self, layer, max_blocks=8192):
+        t, ls, fl = np.zeros(max_blocks, np.int32), np.zeros(max_blocks, np.int64), np.zeros(max_blocks, np.int32)
+        n = self.L.ref_cache_state(self.h, layer, t, ls, fl)
+        return t[:n], ls[:n], fl[:n]
+
+    def place_after_prefill(self, layer, q):
+        if self.L.ref_cache_place(self.h, layer, f64(q), self.d) != 0:
+            raise ValueError("place_after_prefill")
+
+    def digests(self, layer, nb_stride):
+        out = np.zeros((2, self.d, nb_stride))
+        n = self.L.ref_cache_digests(self.h, layer, self.d, nb_stride, out)
+        return out, n

@@ -292,4 +292,90 @@ double ref_cpu_baseline(int samples, int hq, int hkv, int d, int nb, int k, cons
     return secs;
 }
 
+// ---- TieredKvCache (kv_store.hpp) driven through a handle: the oracle of the
+// device tier bookkeeping (K5). Values of K/V rows do not matter for the tier
+// state except through place_after_prefill, which scores the digests.
+void* ref_cache_new(int layers, int block_size, int head_dim, int method, long long capacity) {
+    try {
+        return new scout::TieredKvCache(static_cast<size_t>(layers), static_cast<size_t>(block_size),
+                                        static_cast<size_t>(head_dim),
+                                        method == 0 ? scout::DigestMethod::minmax : scout::DigestMethod::mean,
+                                        static_cast<size_t>(capacity));
+    } catch (const std::invalid_argument&) {
+        return nullptr;
+    }
+}
+void ref_cache_free(void* c) { delete static_cast<scout::TieredKvCache*>(c); }
+void ref_cache_pin(void* c, int layer) { static_cast<scout::TieredKvCache*>(c)->pin_layer(static_cast<size_t>(layer)); }
+// returns the sealed block id, -1 if the append sealed nothing, -2 on invalid_argument
+long long ref_cache_append(void* c, int layer, const double* k, const double* v, int d) {
+    try {
+        const auto r = static_cast<scout::TieredKvCache*>(c)->append_token(static_cast<size_t>(layer), Vec(k, k + d),
+                                                                            Vec(v, v + d));
+        return r ? static_cast<long long>(*r) : -1;
+    } catch (const std::invalid_argument&) {
+        return -2;
+    }
+}
+// number of tickets applied
+int ref_cache_begin_layer(void* c, long long step, int layer) {
+    return static_cast<int>(
+        static_cast<scout::TieredKvCache*>(c)->begin_layer(static_cast<size_t>(step), static_cast<size_t>(layer)).size());
+}
+int ref_cache_schedule_recall(void* c, int layer, const int32_t* ids, int n, long long issue_step, int issue_layer) {
+    try {
+        BlockIdSet s(ids, ids + n);
+        static_cast<scout::TieredKvCache*>(c)->schedule_recall(static_cast<size_t>(layer), s,
+                                                               static_cast<size_t>(issue_step),
+                                                               static_cast<size_t>(issue_layer));
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+int ref_cache_mark_selected(void* c, int layer, const int32_t* ids, int n, long long step) {
+    try {
+        BlockIdSet s(ids, ids + n);
+        static_cast<scout::TieredKvCache*>(c)->mark_selected(static_cast<size_t>(layer), s, static_cast<size_t>(step));
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+int ref_cache_residency(void* c, int layer, int32_t* out) {
+    const BlockIdSet r = static_cast<scout::TieredKvCache*>(c)->residency_set(static_cast<size_t>(layer));
+    for (size_t i = 0; i < r.size(); ++i) out[i] = static_cast<int32_t>(r[i]);
+    return static_cast<int>(r.size());
+}
+// per block: tier (1 fast), last_selected, in flight (1/0); returns the block count
+int ref_cache_state(void* c, int layer, int32_t* tier, int64_t* last_sel, int32_t* in_flight) {
+    const auto* kc = static_cast<scout::TieredKvCache*>(c);
+    const size_t L = static_cast<size_t>(layer);
+    const size_t n = kc->block_count(L);
+    for (size_t id = 0; id < n; ++id) {
+        tier[id] = kc->tier_of(L, id) == scout::Tier::fast ? 1 : 0;
+        last_sel[id] = static_cast<int64_t>(kc->last_selected(L, id));
+        in_flight[id] = kc->is_in_flight(L, id) ? 1 : 0;
+    }
+    return static_cast<int>(n);
+}
+int ref_cache_place(void* c, int layer, const double* q, int d) {
+    try {
+        static_cast<scout::TieredKvCache*>(c)->place_after_prefill(static_cast<size_t>(layer), Vec(q, q + d));
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
+}
+// the layer's digests as [2][d][nb_stride] (minmax) for the GPU side of a place test
+int ref_cache_digests(void* c, int layer, int d, int nb_stride, double* out) {
+    const auto& ds = static_cast<scout::TieredKvCache*>(c)->digests(static_cast<size_t>(layer));
+    for (size_t b = 0; b < ds.size(); ++b)
+        for (int ch = 0; ch < d; ++ch) {
+            out[static_cast<size_t>(ch) * nb_stride + b] = ds[b].lo[ch];
+            out[static_cast<size_t>(d + ch) * nb_stride + b] = ds[b].hi[ch];
+        }
+    return static_cast<int>(ds.size());
+}
+
 }  // extern "C"

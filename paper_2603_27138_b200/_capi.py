@@ -31,10 +31,18 @@ EXPORTED = (
     "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather", "scout_recall_copy",
     "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
     "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k1_outputs",
+    "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
+    "scout_tier_place",
 )
 
 _vp = C.c_void_p
 _i32p = C.c_void_p  # device pointers travel as void*
+
+
+class TierLayer(C.Structure):
+    _fields_ = [("table", _vp), ("tier", _vp), ("last_sel", _vp), ("ready", _vp), ("ticket", _vp),
+                ("free_slots", _vp), ("n_free", _vp), ("err", _vp), ("capacity", C.c_int),
+                ("slots_per_unit", C.c_int)]
 
 
 class TopkArgs(C.Structure):
@@ -96,6 +104,14 @@ def lib() -> C.CDLL:
         L.scout_kv_write_tokens.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_kv_read_tokens.argtypes = [_vp, C.c_int, _vp, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_digest_build.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]
+        _tl = C.POINTER(TierLayer)
+        L.scout_tier_append.argtypes = [_tl, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp, _vp]
+        L.scout_tier_apply.argtypes = [_tl, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp]
+        L.scout_tier_schedule_recall.argtypes = [_tl, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, C.c_int, C.c_int,
+                                                 _vp, _vp]
+        L.scout_tier_plan.argtypes = [_tl, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp]
+        L.scout_tier_mark.argtypes = [_tl, C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int, _vp]
+        L.scout_tier_place.argtypes = [_tl, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp]
         L.scout_kv_append.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_score_topk_split.argtypes = [C.POINTER(TopkArgs), _vp]
         L.scout_score_topk_split_batch.argtypes = [C.POINTER(TopkArgs), C.c_int, _vp]

@@ -1,0 +1,423 @@
+// K5 — device-resident tier bookkeeping.
+//
+// The GPU mirror of TieredKvCache's per-layer state (reference
+// proj/include/scout/kv_store.hpp:296-305): tier flag, last_selected mark,
+// in-flight recall ticket and the pool slot of every block of every unit,
+// plus a per-(layer, unit) stack of free pool slots. It replaces the
+// reference's host bookkeeping on the decode path:
+//   append_token's block open / seal        kv_store.hpp:90-117
+//   residency_set (the planning view)       kv_store.hpp:156-170
+//   schedule_recall                         kv_store.hpp:175-197
+//   begin_layer (apply due recalls)         kv_store.hpp:201-218
+//   enforce_capacity (LRU, ties -> lower id) kv_store.hpp:333-345
+//   place_after_prefill                     kv_store.hpp:271-283
+// mark_selected (kv_store.hpp:222-228) is K1's last_selected output.
+// One CTA per unit; the LRU victim search is a block-wide argmin over the
+// (last_selected, id) key, one round per evicted block (the excess is the
+// handful of blocks a recall or a seal adds, so rounds are few).
+#include "scout_common.cuh"
+
+#include <climits>
+
+using namespace scout_dev;
+
+namespace {
+
+constexpr int TT = 128;  // threads per unit
+constexpr int TW = TT / 32;
+
+struct TierSm {
+    unsigned long long red[TW];
+    int cnt[TW];
+    int n_free;
+    int err;
+};
+
+__device__ __forceinline__ int n_blocks_of(int ntok) { return (ntok + BS - 1) / BS; }
+// a block is sealed once it holds B rows (kv_store.hpp:111)
+__device__ __forceinline__ bool sealed(int id, int ntok) { return (id + 1) * BS <= ntok; }
+
+__device__ int block_sum(int v, TierSm& S) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) S.cnt[w] = v;
+    __syncthreads();
+    int t = 0;
+#pragma unroll
+    for (int i = 0; i < TW; ++i) t += S.cnt[i];
+    __syncthreads();
+    return t;
+}
+
+__device__ unsigned long long block_min(unsigned long long v, TierSm& S) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y < v ? y : v;
+    }
+    if (lane == 0) S.red[w] = v;
+    __syncthreads();
+    unsigned long long t = S.red[0];
+#pragma unroll
+    for (int i = 1; i < TW; ++i) t = S.red[i] < t ? S.red[i] : t;
+    __syncthreads();
+    return t;
+}
+
+struct Unit {
+    int32_t* table;
+    uint8_t* tier;
+    int32_t* last_sel;
+    int32_t* ready;
+    int32_t* ticket;
+    int32_t* free_slots;
+    int32_t* n_free;
+    int32_t* err;
+};
+
+__device__ Unit unit_of(const scout_tier_layer& L, int u, int nbs) {
+    const size_t o = static_cast<size_t>(u) * nbs;
+    return Unit{L.table + o, L.tier + o, L.last_sel + o, L.ready + o, L.ticket + o,
+                L.free_slots + static_cast<size_t>(u) * L.slots_per_unit, L.n_free + u, L.err + u};
+}
+
+__device__ void set_err(Unit& U, int code) {
+    if (*U.err == 0) *U.err = code;
+}
+
+// enforce_capacity (kv_store.hpp:333-345): while more sealed fast blocks than
+// capacity, demote the least recently selected one (ties -> lower id) and
+// return its slot to the free stack.
+__device__ void enforce_capacity(const scout_tier_layer& L, Unit& U, int nb, int ntok, TierSm& S) {
+    if (L.capacity <= 0) return;  // pinned layer
+    int mine = 0;
+    for (int b = threadIdx.x; b < nb; b += TT) mine += (U.tier[b] && sealed(b, ntok));
+    int excess = block_sum(mine, S) - L.capacity;
+    while (excess > 0) {
+        unsigned long long key = ~0ull;
+        for (int b = threadIdx.x; b < nb; b += TT)
+            if (U.tier[b] && sealed(b, ntok)) {
+                const unsigned long long k =
+                    (static_cast<unsigned long long>(static_cast<uint32_t>(U.last_sel[b])) << 32) | static_cast<uint32_t>(b);
+                key = k < key ? k : key;
+            }
+        key = block_min(key, S);
+        if (threadIdx.x == 0) {
+            const int v = static_cast<int>(key & 0xFFFFFFFFu);
+            U.tier[v] = 0;
+            const int n = *U.n_free;
+            if (n < L.slots_per_unit) {
+                U.free_slots[n] = U.table[v];
+                *U.n_free = n + 1;
+            }
+            U.table[v] = -1;
+        }
+        __syncthreads();
+        --excess;
+    }
+}
+
+// append_token's bookkeeping (kv_store.hpp:95-115) for one layer: n_tokens is
+// the count BEFORE the append. A new block takes a slot from the free stack,
+// is fast and marked with the clock step; the append that fills it seals it
+// (mark = clock step again) and enforces capacity.
+__global__ void __launch_bounds__(TT) tier_append_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
+                                                         int clock_step, int32_t* open_slot, int32_t* sealed_id) {
+    __shared__ TierSm S;
+    const int u = blockIdx.x;
+    Unit U = unit_of(L, u, nbs);
+    const int pos = n_tokens[u];
+    const int id = pos / BS;
+    if (threadIdx.x == 0) {
+        if (id >= nbs) {
+            set_err(U, SCOUT_ERR_INVALID_ARGUMENT);
+            S.err = 1;
+        } else {
+            S.err = 0;
+            if (pos % BS == 0) {
+                const int n = *U.n_free;
+                if (n <= 0) {
+                    set_err(U, SCOUT_ERR_LOGIC);  // no pool slot for the new open block
+                    S.err = 1;
+                } else {
+                    U.table[id] = U.free_slots[n - 1];
+                    *U.n_free = n - 1;
+                    U.tier[id] = 1;
+                    U.ready[id] = -1;
+                    U.last_sel[id] = clock_step;
+                }
+            }
+        }
+        if (open_slot) open_slot[u] = S.err ? -1 : U.table[id];
+        if (sealed_id) sealed_id[u] = (!S.err && (pos + 1) % BS == 0) ? id : -1;
+    }
+    __syncthreads();
+    if (S.err || (pos + 1) % BS != 0) return;
+    if (threadIdx.x == 0) U.last_sel[id] = clock_step;
+    __syncthreads();
+    enforce_capacity(L, U, id + 1, pos + 1, S);
+}
+
+// begin_layer's application for one layer (kv_store.hpp:201-218): every
+// in-flight block whose ready tick <= due_tick becomes fast; tickets are
+// applied in issue order (ticket number), each followed by enforce_capacity.
+__global__ void __launch_bounds__(TT) tier_apply_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
+                                                        int due_tick, int32_t* n_applied) {
+    __shared__ TierSm S;
+    const int u = blockIdx.x;
+    Unit U = unit_of(L, u, nbs);
+    const int ntok = n_tokens[u];
+    const int nb = min(n_blocks_of(ntok), nbs);
+    int applied = 0;
+    for (;;) {
+        unsigned long long t = ~0ull;
+        for (int b = threadIdx.x; b < nb; b += TT)
+            if (U.ready[b] >= 0 && U.ready[b] <= due_tick) {
+                const unsigned long long k = static_cast<uint32_t>(U.ticket[b]);
+                t = k < t ? k : t;
+            }
+        t = block_min(t, S);
+        if (t == ~0ull) break;
+        int mine = 0;
+        for (int b = threadIdx.x; b < nb; b += TT)
+            if (U.ready[b] >= 0 && U.ready[b] <= due_tick && static_cast<uint32_t>(U.ticket[b]) == t) {
+                U.tier[b] = 1;
+                U.ready[b] = -1;
+                ++mine;
+            }
+        applied += block_sum(mine, S);
+        enforce_capacity(L, U, nb, ntok, S);
+    }
+    if (threadIdx.x == 0 && n_applied) n_applied[u] = applied;
+}
+
+// schedule_recall (kv_store.hpp:175-197): ids must be sealed, slow and not in
+// flight, else the unit's whole ticket is rejected (the reference throws
+// before changing anything). Accepted blocks get a pool slot (the H2D
+// destination, dst_slots) and the ready tick; n_ids[u] == 0 skips the unit.
+__global__ void __launch_bounds__(TT) tier_recall_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
+                                                         const int32_t* ids, const int32_t* n_ids, int k_stride,
+                                                         int ready_tick, int ticket, int32_t* dst_slots) {
+    __shared__ TierSm S;
+    const int u = blockIdx.x;
+    Unit U = unit_of(L, u, nbs);
+    const int n = n_ids[u];
+    if (n <= 0) return;
+    const int ntok = n_tokens[u];
+    const int nb = min(n_blocks_of(ntok), nbs);
+    const int32_t* my = ids + static_cast<size_t>(u) * k_stride;
+    int bad = 0;
+    for (int i = threadIdx.x; i < n; i += TT) {
+        const int id = my[i];
+        if (id < 0 || id >= nb || !sealed(id, ntok) || U.tier[id] || U.ready[id] >= 0 ||
+            (i > 0 && my[i - 1] >= id))  // ids must be a sorted set
+            bad = 1;
+    }
+    bad = block_sum(bad, S);
+    if (threadIdx.x == 0) {
+        S.err = 0;
+        if (bad) {
+            set_err(U, SCOUT_ERR_INVALID_ARGUMENT);
+            S.err = 1;
+        } else if (*U.n_free < n) {
+            set_err(U, SCOUT_ERR_LOGIC);  // not enough free pool slots for the ticket
+            S.err = 1;
+        } else {
+            S.n_free = *U.n_free;
+            *U.n_free = S.n_free - n;
+        }
+    }
+    __syncthreads();
+    if (S.err) {
+        for (int i = threadIdx.x; i < n; i += TT) dst_slots[static_cast<size_t>(u) * k_stride + i] = -1;
+        return;
+    }
+    for (int i = threadIdx.x; i < n; i += TT) {
+        const int id = my[i];
+        const int slot = U.free_slots[S.n_free - 1 - i];
+        U.table[id] = slot;
+        U.ready[id] = ready_tick;
+        U.ticket[id] = ticket;
+        dst_slots[static_cast<size_t>(u) * k_stride + i] = slot;
+    }
+}
+
+// residency_set (kv_store.hpp:156-170) as K1's block table: the slot of every
+// fast block and of every in-flight block ready by the layer's next run.
+__global__ void __launch_bounds__(TT) tier_plan_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
+                                                       int next_tick, int32_t* block_table) {
+    const int u = blockIdx.x;
+    const size_t o = static_cast<size_t>(u) * nbs;
+    const int nb = min(n_blocks_of(n_tokens[u]), nbs);
+    for (int b = threadIdx.x; b < nbs; b += TT) {
+        int v = -1;
+        if (b < nb) {
+            const int r = L.ready[o + b];
+            if (L.tier[o + b] || (r >= 0 && r <= next_tick)) v = L.table[o + b];
+        }
+        block_table[o + b] = v;
+    }
+}
+
+// place_after_prefill (kv_store.hpp:271-283): sealed blocks in keep (K1's
+// top-capacity selection over the sealed blocks, ascending ids) are fast, the
+// other sealed blocks go slow and free their slots; a kept block that was slow
+// takes a free slot, reported in fill_slots[u][i] (else -1) for the H2D fill
+// of its image. Pinned layers keep all.
+__global__ void __launch_bounds__(TT) tier_place_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
+                                                        const int32_t* keep, const int32_t* n_keep, int k_stride,
+                                                        int32_t* fill_slots) {
+    __shared__ TierSm S;
+    if (L.capacity <= 0) return;
+    const int u = blockIdx.x;
+    Unit U = unit_of(L, u, nbs);
+    const int ntok = n_tokens[u];
+    const int nb = min(n_blocks_of(ntok), nbs);
+    const int32_t* kp = keep + static_cast<size_t>(u) * k_stride;
+    const int nk = n_keep[u];
+    if (threadIdx.x == 0) S.n_free = *U.n_free;
+    __syncthreads();
+    // demote the sealed blocks outside keep
+    for (int b = threadIdx.x; b < nb; b += TT) {
+        if (!sealed(b, ntok)) continue;
+        int lo = 0, hi = nk;  // binary search in the ascending keep list
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (kp[mid] < b) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo < nk && kp[lo] == b) continue;
+        if (U.tier[b] && U.table[b] >= 0) {
+            const int i = atomicAdd(&S.n_free, 1);
+            if (i < L.slots_per_unit) U.free_slots[i] = U.table[b];
+        }
+        U.table[b] = -1;
+        U.tier[b] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        S.n_free = min(S.n_free, L.slots_per_unit);
+        S.err = 0;
+    }
+    __syncthreads();
+    // promote the kept blocks that were slow
+    for (int i = threadIdx.x; i < nk; i += TT) {
+        const int b = kp[i];
+        int fill = -1;
+        if (b >= 0 && b < nb && !U.tier[b]) {
+            const int top = atomicSub(&S.n_free, 1);
+            if (top > 0) {
+                fill = U.free_slots[top - 1];
+                U.table[b] = fill;
+                U.tier[b] = 1;
+                U.ready[b] = -1;
+            } else {
+                S.err = 1;
+            }
+        }
+        if (fill_slots) fill_slots[static_cast<size_t>(u) * k_stride + i] = fill;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *U.n_free = max(S.n_free, 0);
+        if (S.err) set_err(U, SCOUT_ERR_LOGIC);
+    }
+}
+
+// mark_selected (kv_store.hpp:222-228) for explicit id lists (K1 marks its
+// own selections through last_selected).
+__global__ void __launch_bounds__(TT) tier_mark_kernel(const scout_tier_layer L, int nbs, const int32_t* ids,
+                                                       const int32_t* n_ids, int k_stride, int step) {
+    const int u = blockIdx.x;
+    const int n = n_ids[u];
+    for (int i = threadIdx.x; i < n; i += TT) {
+        const int id = ids[static_cast<size_t>(u) * k_stride + i];
+        if (id >= 0 && id < nbs) L.last_sel[static_cast<size_t>(u) * nbs + id] = step;
+    }
+}
+
+int check_layer(const scout_tier_layer* L, int n_units, int nbs, const char* what) {
+    using namespace scout_host;
+    if (!L || n_units < 0 || nbs <= 0 ||
+        (n_units > 0 && (!L->table || !L->tier || !L->last_sel || !L->ready || !L->ticket || !L->free_slots ||
+                         !L->n_free || !L->err || L->slots_per_unit <= 0))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "%s: bad tier layer", what);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    return SCOUT_OK;
+}
+
+}  // namespace
+
+extern "C" int scout_tier_append(const scout_tier_layer* L, int n_units, int nb_stride, const int32_t* n_tokens,
+                                 int clock_step, int32_t* open_slot, int32_t* sealed_id, void* stream) {
+    int rc = check_layer(L, n_units, nb_stride, "scout_tier_append");
+    if (rc != SCOUT_OK || n_units == 0) return rc;
+    tier_append_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, n_tokens, clock_step,
+                                                                              open_slot, sealed_id);
+    return scout_host::check_launch("scout_tier_append");
+}
+
+extern "C" int scout_tier_apply(const scout_tier_layer* L, int n_units, int nb_stride, const int32_t* n_tokens,
+                                int due_tick, int32_t* n_applied, void* stream) {
+    int rc = check_layer(L, n_units, nb_stride, "scout_tier_apply");
+    if (rc != SCOUT_OK || n_units == 0) return rc;
+    tier_apply_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, n_tokens, due_tick,
+                                                                             n_applied);
+    return scout_host::check_launch("scout_tier_apply");
+}
+
+extern "C" int scout_tier_schedule_recall(const scout_tier_layer* L, int n_units, int nb_stride,
+                                          const int32_t* n_tokens, const int32_t* ids, const int32_t* n_ids,
+                                          int k_stride, int ready_tick, int ticket, int32_t* dst_slots, void* stream) {
+    int rc = check_layer(L, n_units, nb_stride, "schedule_recall");
+    if (rc != SCOUT_OK || n_units == 0) return rc;
+    if (!ids || !n_ids || !dst_slots || k_stride <= 0 || ready_tick < 0 || ticket < 0) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "schedule_recall: bad arguments");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    tier_recall_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, n_tokens, ids, n_ids,
+                                                                              k_stride, ready_tick, ticket, dst_slots);
+    return scout_host::check_launch("scout_tier_schedule_recall");
+}
+
+extern "C" int scout_tier_plan(const scout_tier_layer* L, int n_units, int nb_stride, const int32_t* n_tokens,
+                               int next_tick, int32_t* block_table, void* stream) {
+    int rc = check_layer(L, n_units, nb_stride, "residency_set");
+    if (rc != SCOUT_OK || n_units == 0) return rc;
+    if (!block_table) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "residency_set: null block table");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    tier_plan_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, n_tokens, next_tick,
+                                                                            block_table);
+    return scout_host::check_launch("scout_tier_plan");
+}
+
+extern "C" int scout_tier_place(const scout_tier_layer* L, int n_units, int nb_stride, const int32_t* n_tokens,
+                                const int32_t* keep, const int32_t* n_keep, int k_stride, int32_t* fill_slots,
+                                void* stream) {
+    int rc = check_layer(L, n_units, nb_stride, "place_after_prefill");
+    if (rc != SCOUT_OK || n_units == 0) return rc;
+    if (!keep || !n_keep || k_stride <= 0) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "place_after_prefill: bad keep list");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    tier_place_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, n_tokens, keep, n_keep,
+                                                                             k_stride, fill_slots);
+    return scout_host::check_launch("scout_tier_place");
+}
+
+extern "C" int scout_tier_mark(const scout_tier_layer* L, int n_units, int nb_stride, const int32_t* ids,
+                               const int32_t* n_ids, int k_stride, int step, void* stream) {
+    int rc = check_layer(L, n_units, nb_stride, "mark_selected");
+    if (rc != SCOUT_OK || n_units == 0) return rc;
+    if (!ids || !n_ids || k_stride <= 0) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "mark_selected: bad id lists");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    tier_mark_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, ids, n_ids, k_stride, step);
+    return scout_host::check_launch("scout_tier_mark");
+}

@@ -1,0 +1,159 @@
+"""Device-resident TieredKvCache (the host-side mirror of the reference class
+over the K5 C ABI).
+
+`DeviceTieredCache` keeps the reference's API (proj/include/scout/kv_store.hpp:
+append_token :90, residency_set :156, schedule_recall :175, begin_layer :201,
+mark_selected :222, place_after_prefill :271, pin_layer :79) for n_units units
+at once ("unit" = (request, KV head)); every unit is one reference cache and
+all of them share the writer clock. The tier state lives in HBM and is only
+touched by the K5 kernels; the host keeps the two things the reference keeps
+on its clock side: the (step, layer) clock and the ledger of in-flight
+tickets per layer (which layers begin_layer must visit).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _capi as A
+from . import ops
+
+BS = A.BLOCK_SIZE
+
+
+class DeviceTieredCache:
+    def __init__(self, layers: int, n_units: int, nb_stride: int, capacity: int, slots_per_unit: int,
+                 device="cuda", slot_base: int = 0):
+        self.L, self.U, self.nbs = layers, n_units, nb_stride
+        self.spu = slots_per_unit
+        self.dev = torch.device(device)
+        dev, U, nbs = self.dev, n_units, nb_stride
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.table = torch.full((layers, U, nbs), -1, **i32)
+        self.tier = torch.zeros((layers, U, nbs), dtype=torch.uint8, device=dev)
+        self.last_sel = torch.zeros((layers, U, nbs), **i32)
+        self.ready = torch.full((layers, U, nbs), -1, **i32)
+        self.ticket = torch.zeros((layers, U, nbs), **i32)
+        # layer l, unit u owns pool slots slot_base + (l*U + u)*spu + [0, spu); stack top = lowest slot
+        base = slot_base + torch.arange(layers * U, **i32).view(layers, U, 1) * slots_per_unit
+        self.free_slots = (base + torch.arange(slots_per_unit - 1, -1, -1, **i32).view(1, 1, -1)).contiguous()
+        self.n_free = torch.full((layers, U), slots_per_unit, **i32)
+        self.err = torch.zeros((layers, U), **i32)
+        self.n_tokens = torch.zeros((layers, U), **i32)
+        self.capacity = [capacity] * layers
+        self.clock_step, self.clock_layer = 0, 0
+        self.pending: list[list[int]] = [[] for _ in range(layers)]  # ready ticks of in-flight tickets
+        self.n_tickets = 0
+
+    # -------------------------------------------------------------- helpers
+    def tick(self, step: int, layer: int) -> int:
+        return step * self.L + layer
+
+    def layer_desc(self, layer: int) -> A.TierLayer:
+        d = A.TierLayer()
+        for name in ("table", "tier", "last_sel", "ready", "ticket", "free_slots", "n_free", "err"):
+            setattr(d, name, getattr(self, name)[layer].data_ptr())
+        d.capacity = self.capacity[layer]
+        d.slots_per_unit = self.spu
+        return d
+
+    def next_run_of(self, layer: int) -> int:  # kv_store.hpp:328-331
+        if self.clock_layer <= layer:
+            return self.tick(self.clock_step, layer)
+        return self.tick(self.clock_step + 1, layer)
+
+    def check(self, layer: int):
+        """Raise like the reference would (std::invalid_argument / logic errors
+        surface as the units' sticky error codes)."""
+        e = self.err[layer]
+        bad = torch.nonzero(e).flatten().tolist()
+        if bad:
+            code = int(e[bad[0]])
+            self.err[layer].zero_()
+            if code == A.SCOUT_ERR_INVALID_ARGUMENT:
+                raise ValueError(f"tier layer {layer}: invalid argument in units {bad}")
+            raise RuntimeError(f"tier layer {layer}: out of pool slots in units {bad}")
+
+    # ------------------------------------------------------------- reference API
+    def pin_layer(self, layer: int):
+        self.capacity[layer] = 0
+
+    def append_token(self, layer: int, k_rows=None, v_rows=None, pool=None, kv_dtype=None, digests=None,
+                     method=0):
+        """One token for every unit. Without a pool only the bookkeeping runs."""
+        lib, st = A.lib(), torch.cuda.current_stream(self.dev).cuda_stream
+        open_slot = torch.empty(self.U, dtype=torch.int32, device=self.dev)
+        sealed = torch.empty(self.U, dtype=torch.int32, device=self.dev)
+        nt = self.n_tokens[layer]
+        desc = self.layer_desc(layer)
+        A.check(lib.scout_tier_append(C.byref(desc), self.U, self.nbs, nt.data_ptr(), self.clock_step,
+                                      open_slot.data_ptr(), sealed.data_ptr(), st))
+        if pool is not None:
+            ops.kv_append(pool, kv_dtype, method, open_slot, nt, k_rows, v_rows, digests, self.nbs, advance=True)
+        else:
+            nt.add_(1)
+        return open_slot, sealed
+
+    def begin_layer(self, step: int, layer: int) -> int:
+        """Advance the clock and apply every due ticket (kv_store.hpp:201-218)."""
+        self.clock_step, self.clock_layer = step, layer
+        now = self.tick(step, layer)
+        lib, st = A.lib(), torch.cuda.current_stream(self.dev).cuda_stream
+        applied = 0
+        for l in range(self.L):
+            due = [t for t in self.pending[l] if t <= now]
+            if not due:
+                continue
+            self.pending[l] = [t for t in self.pending[l] if t > now]
+            desc = self.layer_desc(l)
+            A.check(lib.scout_tier_apply(C.byref(desc), self.U, self.nbs, self.n_tokens[l].data_ptr(), now, None, st))
+            applied += len(due)
+        return applied
+
+    def schedule_recall(self, layer: int, ids: torch.Tensor, n_ids: torch.Tensor, issue_step: int,
+                        issue_layer: int) -> torch.Tensor:
+        """ids [U][k] ascending per unit (n_ids[u] valid; 0 = no recall for the
+        unit). Returns the destination pool slots [U][k] for the H2D copies."""
+        ids = ids.to(device=self.dev, dtype=torch.int32).contiguous()
+        n_ids = n_ids.to(device=self.dev, dtype=torch.int32).contiguous()
+        k = ids.shape[1]
+        dst = torch.empty_like(ids)
+        ready = self.tick(issue_step + 1, issue_layer)
+        desc = self.layer_desc(layer)
+        A.check(A.lib().scout_tier_schedule_recall(C.byref(desc), self.U, self.nbs, self.n_tokens[layer].data_ptr(),
+                                                   ids.data_ptr(), n_ids.data_ptr(), k, ready, self.n_tickets,
+                                                   dst.data_ptr(), torch.cuda.current_stream(self.dev).cuda_stream))
+        self.n_tickets += 1
+        self.pending[layer].append(ready)
+        return dst
+
+    def mark_selected(self, layer: int, ids: torch.Tensor, n_ids: torch.Tensor, step: int):
+        ids = ids.to(device=self.dev, dtype=torch.int32).contiguous()
+        n_ids = n_ids.to(device=self.dev, dtype=torch.int32).contiguous()
+        desc = self.layer_desc(layer)
+        A.check(A.lib().scout_tier_mark(C.byref(desc), self.U, self.nbs, ids.data_ptr(), n_ids.data_ptr(),
+                                        ids.shape[1], step, torch.cuda.current_stream(self.dev).cuda_stream))
+
+    def residency_table(self, layer: int) -> torch.Tensor:
+        """residency_set (kv_store.hpp:156-170) as K1's block table [U][nb_stride]."""
+        out = torch.empty((self.U, self.nbs), dtype=torch.int32, device=self.dev)
+        desc = self.layer_desc(layer)
+        A.check(A.lib().scout_tier_plan(C.byref(desc), self.U, self.nbs, self.n_tokens[layer].data_ptr(),
+                                        self.next_run_of(layer), out.data_ptr(),
+                                        torch.cuda.current_stream(self.dev).cuda_stream))
+        return out
+
+    def place_after_prefill(self, layer: int, q: torch.Tensor, digests: torch.Tensor, group: int, kv_dtype=None):
+        """Keep the top-capacity sealed blocks of every unit fast (kv_store.hpp:271-283):
+        K1 over the sealed blocks (n_tokens rounded down to whole blocks)."""
+        if self.capacity[layer] <= 0:
+            return
+        sealed_tok = (self.n_tokens[layer] // BS) * BS
+        r = ops.score_topk_split(q, digests, sealed_tok.contiguous(), self.capacity[layer], group)
+        desc = self.layer_desc(layer)
+        fill = torch.empty_like(r["sel_ids"])
+        A.check(A.lib().scout_tier_place(C.byref(desc), self.U, self.nbs, self.n_tokens[layer].data_ptr(),
+                                         r["sel_ids"].data_ptr(), r["n_sel"].data_ptr(), r["sel_ids"].shape[1],
+                                         fill.data_ptr(), torch.cuda.current_stream(self.dev).cuda_stream))
+        return r["sel_ids"], fill
