@@ -126,6 +126,8 @@ class Workload:
         noise = torch.randn(L, U * G, D, generator=g, device=dev)
         qp = self.q_true + 0.33 * noise
         self.q_pred = qp * (self.q_true.norm(dim=-1, keepdim=True) / qp.norm(dim=-1, keepdim=True))
+        # queries in the model's dtype (q_dtype bf16: what a bf16 Qwen3 projection emits)
+        self.q_true, self.q_pred = self.q_true.to(cfg["q_dtype"]), self.q_pred.to(cfg["q_dtype"])
         self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev)
         m = torch.randn(L, U * G, generator=g, device=dev)
         l = torch.rand(L, U * G, generator=g, device=dev) * 40 + 1
@@ -176,7 +178,8 @@ class Workload:
         self.layer_states = layers
         self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=pool,
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
-                                   recall_interval=cfg["recall"], host_tier=self.host_tier, host_staging=True)
+                                   recall_interval=cfg["recall"], host_tier=self.host_tier, host_staging=True,
+                                   q_dtype=cfg["q_dtype"])
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
 
@@ -331,8 +334,11 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline")
+    ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
+                    help="query dtype (q_true / q_pred); bf16 = the model's projection output")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    cfg["q_dtype"] = torch.bfloat16 if args.q_dtype == "bf16" else torch.float32
     if args.batch:
         cfg["batch"] = args.batch
     ws, rank, local = dist_setup()
@@ -442,7 +448,7 @@ def main():
             "config": {"workload": args.config, "model_shape": "Qwen3-32B" if cfg["hq"] == 64 else "Qwen3-8B",
                        "batch_per_gpu": cfg["batch"], "global_batch": global_batch, "context": cfg["ctx"],
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "head_dim": D,
-                       "block": BS, "top_k": cfg["k"], "gpu_cache_blocks_per_unit": cfg["capacity"],
+                       "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "gpu_cache_blocks_per_unit": cfg["capacity"],
                        "cpu_blocks_per_unit": wl.cpu_per_unit, "recall_every": cfg["recall"],
                        "parallelism": f"request-sharded x{ws}, no collective",
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},

@@ -29,7 +29,9 @@
  *   digests    : per unit [2][128][nb_stride] (lo then hi, channel-major, block
  *                id fastest) in the KV dtype for minmax; [128][nb_stride] f64
  *                for the mean method.
- *   queries    : [req][Hq][128] f32 (f64 for the generic f64 scoring path).
+ *   queries    : [req][Hq][128] f32 (f64 for the generic f64 scoring path), or
+ *                bf16 where a q_dtype field says SCOUT_BF16 (the model's own
+ *                query dtype: half the bytes, products still exact in K1).
  *   partials   : o [req][Hq][128] f32 (normalised) + ml [req][Hq][2] f32
  *                = (max logit, denominator); empty partial = (0, -inf, 0).
  */
@@ -162,6 +164,7 @@ typedef struct scout_topk_args {
     unsigned* done_flag;
     unsigned* done_ctr;
     unsigned done_token;
+    int q_dtype;    /* minmax bf16/f32 digests: SCOUT_F32 (0, default) or SCOUT_BF16 queries */
 } scout_topk_args;
 
 int scout_score_topk_split(const scout_topk_args* args, void* stream);
@@ -188,7 +191,7 @@ typedef struct scout_decode_args {
     int kv_dtype;
     int k_stride;
     float scale;
-    const float* q;
+    const void* q;  /* f32 (or bf16, see q_dtype) */
     const void* kv_pool;
     const int32_t* res_slots;
     const int32_t* res_ids;
@@ -202,6 +205,7 @@ typedef struct scout_decode_args {
     size_t workspace_bytes;
     int max_ctas; /* 0 = one persistent CTA per SM */
     int flags;    /* SCOUT_LAUNCH_PDL: programmatic dependent launch */
+    int q_dtype;  /* bf16 KV: SCOUT_F32 (0, default) or SCOUT_BF16 queries (q then points to bf16) */
 } scout_decode_args;
 
 size_t scout_sparse_decode_workspace_bytes(int n_units, int group, int max_ctas);
@@ -320,15 +324,17 @@ typedef struct scout_engine_config {
     int host_staging;          /* 1: allocate device staging for decode_step_host */
     int chunk_layers;          /* layers per H2D/D2H chunk of the host path (0 = 8) */
     int recall_mode;           /* 0: copy engines (scout_recall_copy), 1: SM gather kernel (K4) */
+    int q_dtype;               /* q_true / q_pred element type: SCOUT_F32 (0) or SCOUT_BF16 */
 } scout_engine_config;
 
 typedef struct scout_engine scout_engine;
 
 int scout_engine_create(const scout_engine_config* cfg, const scout_layer_desc* layers, scout_engine** out);
 int scout_engine_destroy(scout_engine* eng);
-/* One decode step, device-resident inputs: q_true / q_pred / cpu_o [L][U*G][128],
- * cpu_ml [L][U*G][2] f32; outputs out_o [L][U*G][128], out_ml [L][U*G][2]. */
-int scout_engine_decode_step(scout_engine* eng, int step, const float* q_true, const float* q_pred,
+/* One decode step, device-resident inputs: q_true / q_pred [L][U*G][128] in
+ * cfg.q_dtype, cpu_o [L][U*G][128], cpu_ml [L][U*G][2] f32; outputs out_o
+ * [L][U*G][128], out_ml [L][U*G][2] f32. */
+int scout_engine_decode_step(scout_engine* eng, int step, const void* q_true, const void* q_pred,
                              const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml, void* stream);
 /* Same step from pinned HOST buffers (same layouts): H2D of the inputs and
  * D2H of the outputs plus each layer's CPU-side block ids (h_cpu_ids
@@ -338,7 +344,7 @@ int scout_engine_decode_step(scout_engine* eng, int step, const float* q_true, c
  * cudaMemcpyAsync, the input copies start as soon as the call is made (they
  * overlap the previous step's attention), so the host inputs must be final
  * at the call and stay unchanged until `stream` completes the step. */
-int scout_engine_decode_step_host(scout_engine* eng, int step, const float* h_q_true, const float* h_q_pred,
+int scout_engine_decode_step_host(scout_engine* eng, int step, const void* h_q_true, const void* h_q_pred,
                                   const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o, float* h_out_ml,
                                   int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream);
 /* Order all outstanding side-stream work (recalls) before `stream`. */

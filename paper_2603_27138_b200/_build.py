@@ -46,13 +46,13 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
         if force or _stale(obj, [src] + hdrs):
             cmd = [NVCC, *ARCH, *NVFLAGS, "-c", str(src), "-o", str(obj)]
             if src.suffix == ".cpp":  # host-only C++: the system compiler
-                cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-Wall", f"-I{CUDA_INC}", f"-I{ROOT / 'include'}",
+                cmd = [CXX, "-O3", "-std=c++17", "-fPIC", "-Wall", "-pthread", f"-I{CUDA_INC}", f"-I{ROOT / 'include'}",
                        "-c", str(src), "-o", str(obj)]
             if verbose:
                 print(" ".join(cmd))
             subprocess.run(cmd, check=True)
     if force or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static", "-Xcompiler", "-pthread"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

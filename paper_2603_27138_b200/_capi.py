@@ -53,7 +53,7 @@ class TopkArgs(C.Structure):
         ("sel_ids", _vp), ("n_sel", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
         ("cpu_ids", _vp), ("n_cpu", _vp), ("res_tokens", _vp), ("cpu_tokens", _vp),
         ("last_selected", _vp), ("scores_out", _vp), ("flags", C.c_int),
-        ("done_flag", _vp), ("done_ctr", _vp), ("done_token", C.c_uint),
+        ("done_flag", _vp), ("done_ctr", _vp), ("done_token", C.c_uint), ("q_dtype", C.c_int),
     ]
 
 
@@ -64,6 +64,7 @@ class DecodeArgs(C.Structure):
         ("q", _vp), ("kv_pool", _vp), ("res_slots", _vp), ("res_ids", _vp), ("n_res", _vp),
         ("n_tokens", _vp), ("cpu_o", _vp), ("cpu_ml", _vp), ("o", _vp), ("ml", _vp),
         ("workspace", _vp), ("workspace_bytes", C.c_size_t), ("max_ctas", C.c_int), ("flags", C.c_int),
+        ("q_dtype", C.c_int),
     ]
 
 
@@ -78,6 +79,7 @@ class EngineConfig(C.Structure):
         ("nb_stride", C.c_int), ("kv_dtype", C.c_int), ("scale", C.c_float), ("recall_interval", C.c_int),
         ("kv_pool", _vp), ("n_tokens", _vp), ("host_tier", _vp), ("max_ctas", C.c_int),
         ("host_staging", C.c_int), ("chunk_layers", C.c_int), ("recall_mode", C.c_int),
+        ("q_dtype", C.c_int),
     ]
 
 

@@ -12,18 +12,25 @@
 //      layer's attention, kv_store.hpp:175-197), each publishing a recall flag
 //      the next step's K2 waits on before it streams the layer (visible at
 //      (m+1, i), kv_store.hpp:201-218).
-// Host-buffer path (scout_engine_decode_step_host): q_pred lands first, chunk
-// by chunk, each chunk releasing a K1 launch; K2 starts once K1 is done and
-// polls per-chunk input flags for q_true / CPU partials still in flight; the
-// outputs and the host worker's CPU-side ids leave as soon as they exist.
+// Host-buffer path (scout_engine_decode_step_host): q_pred lands first and
+// releases one K1 launch over all layers; K2 starts once K1 is done and polls
+// per-chunk input flags for q_true / CPU partials still in flight; the outputs
+// (4 layers at a time) and the host worker's CPU-side ids leave as soon as they
+// exist. A step's input copies start at the call, so in steady state they run
+// under the previous step's K2.
 // K1 outputs are double-buffered by step parity; K2 workspaces are per layer.
 // Nothing here allocates or synchronises the host inside a step.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <cstdio>
 #include <cstring>
+#include <deque>
+#include <mutex>
 #include <new>
+#include <thread>
 #include <vector>
 
 #include "../../include/scout_b200.h"
@@ -119,6 +126,17 @@ struct scout_engine {
     Buf stage[2];
     cudaEvent_t stage_free[2] = {nullptr, nullptr};
     bool stage_recorded[2] = {false, false};
+    // recall issuer thread: a layer's recall is ~1300 block copies whose
+    // descriptors cost the CPU ~0.6 us each; a worker enqueues them on the side
+    // stream so the caller's thread goes straight on to the next step
+    int device = 0;
+    std::thread rc_thread;
+    std::mutex rc_mu;
+    std::condition_variable rc_cv, rc_idle;
+    std::deque<std::pair<int, unsigned>> rc_jobs;  // (layer, token)
+    bool rc_stop = false, rc_busy = false;
+    int rc_err = SCOUT_OK;
+    char rc_msg[256] = {0};
     // instrumentation
     bool timing = false;
     std::vector<cudaEvent_t> tev;
@@ -130,6 +148,7 @@ struct scout_engine {
     int32_t* I(const Buf& b) const { return static_cast<int32_t*>(b.p); }
 
     ~scout_engine() {
+        stop_recalls();
         for (cudaStream_t s : {k1s, side, h2d, d2h})
             if (s) cudaStreamDestroy(s);
         for (cudaEvent_t e : {ev_start, ev_k1_end, ev_tmp, ev_k2[0], ev_k2[1], stage_free[0], stage_free[1]})
@@ -140,7 +159,13 @@ struct scout_engine {
     }
 
     // ---------------------------------------------------------------- K1
-    scout_topk_args k1_args(int layer, const float* q, int step, int par) {
+    size_t qbytes() const { return cfg.q_dtype == SCOUT_BF16 ? 2 : 4; }
+    // layer l's query block of a [L][U*G][128] query array
+    const void* qlayer(const void* q, int l) const {
+        return static_cast<const uint8_t*>(q) + static_cast<size_t>(l) * UG * SCOUT_HEAD_DIM * qbytes();
+    }
+
+    scout_topk_args k1_args(int layer, const void* q, int step, int par) {
         scout_topk_args a{};
         a.n_units = U;
         a.group = G;
@@ -166,23 +191,23 @@ struct scout_engine {
         a.done_flag = k1_flag + layer;
         a.done_ctr = k1_ctr + layer;
         a.done_token = token;
+        a.q_dtype = cfg.q_dtype;
         return a;
     }
     // K1 over layers [l0, l0+n) in one launch (grid units x layers): layer 0
     // selects with the true query, the others with the predicted one
-    int select_batch(int l0, int n, const float* q_true, const float* q_pred, int step, int par, cudaStream_t st) {
-        const size_t qd = static_cast<size_t>(UG) * SCOUT_HEAD_DIM;
+    int select_batch(int l0, int n, const void* q_true, const void* q_pred, int step, int par, cudaStream_t st) {
         std::vector<scout_topk_args> v(n);
         for (int i = 0; i < n; ++i) {
             const int l = l0 + i;
-            v[i] = k1_args(l, l == 0 ? q_true : q_pred + l * qd, step, par);
+            v[i] = k1_args(l, l == 0 ? q_true : qlayer(q_pred, l), step, par);
         }
         ++launches;
         return scout_k1_launch_batch(v.data(), n, st);
     }
 
     // ---------------------------------------------------------------- K2
-    int launch_k2(int par, const float* const* q, const float* const* co, const float* const* cml, float* const* o,
+    int launch_k2(int par, const void* const* q, const float* const* co, const float* const* cml, float* const* o,
                   float* const* ml, const unsigned* const* inflag, bool poll_k1, cudaStream_t st) {
         K2StepArgs a{};
         a.n_units = U;
@@ -199,6 +224,7 @@ struct scout_engine {
         a.layer_done = layer_done;
         a.token = token;
         a.max_ctas = cfg.max_ctas;
+        a.q_bf16 = cfg.q_dtype == SCOUT_BF16;
         for (int i = 0; i < cfg.layers; ++i)
             a.layers[i] = K2Layer{q[i], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
                                   co[i], cml[i], o[i], ml[i], inflag ? inflag[i] : nullptr, rc_token[i], 0u};
@@ -227,25 +253,74 @@ struct scout_engine {
     // the copy waits for every CTA to finish layer i of this launch
     int issue_recalls(int step) {
         if (cfg.recall_interval <= 0) return SCOUT_OK;
+        {
+            std::lock_guard<std::mutex> lk(rc_mu);
+            if (rc_err != SCOUT_OK) {
+                scout_host::set_error(rc_err, "recall issuer: %s", rc_msg);
+                return rc_err;
+            }
+        }
+        bool any = false;
         for (int i = 0; i < cfg.layers; ++i) {
             const scout_layer_desc& L = layers[i];
             if (L.recall_n <= 0 || rc_src[i].empty() || (step + i) % cfg.recall_interval != 0) continue;
-            int rc = wait_value(side, layer_done + i, token * static_cast<unsigned>(grid));
-            if (rc != SCOUT_OK) return rc;
-            if (cfg.recall_mode == 1) {
-                ++launches;
-                const int64_t* src = static_cast<const int64_t*>(rc_dev[i].p);
-                const int32_t* dst = reinterpret_cast<const int32_t*>(src + L.recall_n);
-                rc = scout_recall_gather(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, src, dst, L.recall_n, side);
-            } else {
-                rc = scout_recall_copy(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, rc_src[i].data(), rc_dst[i].data(),
-                                       L.recall_n, side);
-            }
-            if (rc != SCOUT_OK) return rc;
-            if ((rc = write_value(side, recall_flag + i, token)) != SCOUT_OK) return rc;
             rc_token[i] = token;  // the next step's K2 waits for it before streaming layer i
+            std::lock_guard<std::mutex> lk(rc_mu);
+            rc_jobs.emplace_back(i, token);
+            any = true;
         }
+        if (any) rc_cv.notify_one();
         return SCOUT_OK;
+    }
+    // one layer's recall on the side stream (issuer thread)
+    int run_recall(int i, unsigned tok) {
+        const scout_layer_desc& L = layers[i];
+        int rc = wait_value(side, layer_done + i, tok * static_cast<unsigned>(grid));
+        if (rc != SCOUT_OK) return rc;
+        if (cfg.recall_mode == 1) {
+            const int64_t* src = static_cast<const int64_t*>(rc_dev[i].p);
+            const int32_t* dst = reinterpret_cast<const int32_t*>(src + L.recall_n);
+            rc = scout_recall_gather(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, src, dst, L.recall_n, side);
+        } else {
+            rc = scout_recall_copy(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, rc_src[i].data(), rc_dst[i].data(),
+                                   L.recall_n, side);
+        }
+        if (rc != SCOUT_OK) return rc;
+        return write_value(side, recall_flag + i, tok);
+    }
+    void recall_loop() {
+        cudaSetDevice(device);
+        std::unique_lock<std::mutex> lk(rc_mu);
+        for (;;) {
+            rc_cv.wait(lk, [&] { return rc_stop || !rc_jobs.empty(); });
+            if (rc_jobs.empty()) break;  // stopping and drained
+            const auto job = rc_jobs.front();
+            rc_jobs.pop_front();
+            rc_busy = true;
+            lk.unlock();
+            const int rc = run_recall(job.first, job.second);
+            lk.lock();
+            rc_busy = false;
+            if (rc != SCOUT_OK && rc_err == SCOUT_OK) {
+                rc_err = rc;
+                std::snprintf(rc_msg, sizeof(rc_msg), "%s", scout_last_error());
+            }
+            if (rc_jobs.empty()) rc_idle.notify_all();
+        }
+    }
+    // every queued recall enqueued on the side stream
+    void drain_recalls() {
+        std::unique_lock<std::mutex> lk(rc_mu);
+        rc_idle.wait(lk, [&] { return rc_jobs.empty() && !rc_busy; });
+    }
+    void stop_recalls() {
+        if (!rc_thread.joinable()) return;
+        {
+            std::lock_guard<std::mutex> lk(rc_mu);
+            rc_stop = true;
+        }
+        rc_cv.notify_all();
+        rc_thread.join();
     }
 
     // K1 lists of this parity were read by the K2 two steps back: wait for it;
@@ -272,7 +347,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     }
     const scout_engine_config& c = *cfg;
     if (c.layers <= 0 || c.layers > K2_MAX_LAYERS || c.batch <= 0 || c.hkv <= 0 || c.hq % c.hkv != 0 || c.k <= 0 ||
-        c.nb_stride <= 0 || !c.kv_pool || !c.n_tokens || !(c.scale > 0.f) || c.kv_dtype != SCOUT_BF16) {
+        c.nb_stride <= 0 || !c.kv_pool || !c.n_tokens || !(c.scale > 0.f) || c.kv_dtype != SCOUT_BF16 ||
+        (c.q_dtype != SCOUT_F32 && c.q_dtype != SCOUT_BF16)) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 KV)", K2_MAX_LAYERS);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
@@ -311,7 +387,9 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
                  cudaMemset(e->flags.p, 0, nflags * 4) != cudaSuccess))
         bad = 1;
     if (!bad && c.host_staging) {
-        const size_t per = static_cast<size_t>(c.layers) * e->UG * (4 * SCOUT_HEAD_DIM + 4) * 4;
+        // q_true | q_pred (q dtype) | cpu_o | cpu_ml | out_o | out_ml (f32)
+        const size_t qb = c.q_dtype == SCOUT_BF16 ? 2 : 4;
+        const size_t per = static_cast<size_t>(c.layers) * e->UG * (2 * SCOUT_HEAD_DIM * qb + (2 * SCOUT_HEAD_DIM + 4) * 4);
         bad |= e->stage[0].alloc(per) | e->stage[1].alloc(per);
     }
     if (bad) {
@@ -350,6 +428,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     for (cudaEvent_t* ev : {&e->ev_start, &e->ev_k1_end, &e->ev_tmp, &e->ev_k2[0], &e->ev_k2[1], &e->stage_free[0],
                             &e->stage_free[1]})
         cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    cudaGetDevice(&e->device);
+    if (c.recall_interval > 0) e->rc_thread = std::thread([e] { e->recall_loop(); });
     e->ev_k1.resize(c.layers);
     for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     e->chunk_ev.resize(e->nch);
@@ -365,12 +445,15 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
 }
 
 extern "C" int scout_engine_destroy(scout_engine* eng) {
-    if (eng) cudaDeviceSynchronize();  // flags / copies still reference engine memory
+    if (eng) {
+        eng->stop_recalls();     // drains the queued recalls first
+        cudaDeviceSynchronize();  // flags / copies still reference engine memory
+    }
     delete eng;
     return SCOUT_OK;
 }
 
-extern "C" int scout_engine_decode_step(scout_engine* e, int step, const float* q_true, const float* q_pred,
+extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q_true, const void* q_pred,
                                         const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml,
                                         void* stream) {
     if (!e || !q_true || !q_pred || !out_o || !out_ml || ((cpu_o == nullptr) != (cpu_ml == nullptr))) {
@@ -387,10 +470,11 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const float* 
     // then the persistent K2 over all layers; stream order is the dependency
     int rc = e->select_batch(0, L, q_true, q_pred, step, par, st);
     if (rc != SCOUT_OK) return rc;
-    std::vector<const float*> q(L), co(L), cml(L);
+    std::vector<const void*> q(L);
+    std::vector<const float*> co(L), cml(L);
     std::vector<float*> o(L), ml(L);
     for (int i = 0; i < L; ++i) {
-        q[i] = q_true + i * qd;
+        q[i] = e->qlayer(q_true, i);
         co[i] = cpu_o ? cpu_o + i * qd : nullptr;
         cml[i] = cpu_ml ? cpu_ml + i * md : nullptr;
         o[i] = out_o + i * qd;
@@ -401,7 +485,7 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const float* 
     return e->issue_recalls(step);
 }
 
-extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const float* h_q_true, const float* h_q_pred,
+extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred,
                                              const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o,
                                              float* h_out_ml, int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream) {
     if (!e || !e->stage[0].p || !h_q_true || !h_q_pred || !h_out_o || !h_out_ml ||
@@ -415,12 +499,15 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
     const unsigned token = ++e->token;
     const int par = token & 1;
-    float* d_qt = static_cast<float*>(e->stage[par].p);
-    float* d_qp = d_qt + L * qd;
-    float* d_co = d_qp + L * qd;
+    const size_t qb = e->qbytes();  // query element bytes
+    uint8_t* d_qt = static_cast<uint8_t*>(e->stage[par].p);
+    uint8_t* d_qp = d_qt + L * qd * qb;
+    float* d_co = reinterpret_cast<float*>(d_qp + L * qd * qb);
     float* d_cm = d_co + L * qd;
     float* d_o = d_cm + L * md;
     float* d_oml = d_o + L * qd;
+    const uint8_t* hq_t = static_cast<const uint8_t*>(h_q_true);
+    const uint8_t* hq_p = static_cast<const uint8_t*>(h_q_pred);
     int rc = e->begin_step(st, par);
     if (rc != SCOUT_OK) return rc;
     // ---- inputs, in the order the device needs them: q_true of layer 0 and
@@ -431,46 +518,43 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
     // staging to be free (step n-2 fully done): step n's inputs stream in
     // while step n-1's K2 still runs.
     if (e->stage_recorded[par]) CU(cudaStreamWaitEvent(e->h2d, e->stage_free[par], 0));
-    CU(cudaMemcpyAsync(d_qt, h_q_true, qd * 4, cudaMemcpyHostToDevice, e->h2d));
-    for (int c = 0; c < nch; ++c) {
-        const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
-        CU(cudaMemcpyAsync(d_qp + lo * qd, h_q_pred + lo * qd, n * qd * 4, cudaMemcpyHostToDevice, e->h2d));
-        CU(cudaEventRecord(e->chunk_ev[c], e->h2d));
-    }
+    CU(cudaMemcpyAsync(d_qt, hq_t, qd * qb, cudaMemcpyHostToDevice, e->h2d));
+    CU(cudaMemcpyAsync(d_qp + qd * qb, hq_p + qd * qb, (L - 1) * qd * qb, cudaMemcpyHostToDevice, e->h2d));
+    CU(cudaEventRecord(e->chunk_ev[0], e->h2d));
     for (int c = 0; c < nch; ++c) {
         const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
         const int lq = c == 0 ? 1 : lo;  // layer 0's q_true went first
-        CU(cudaMemcpyAsync(d_qt + lq * qd, h_q_true + lq * qd, (lo + n - lq) * qd * 4, cudaMemcpyHostToDevice, e->h2d));
+        CU(cudaMemcpyAsync(d_qt + lq * qd * qb, hq_t + lq * qd * qb, (lo + n - lq) * qd * qb, cudaMemcpyHostToDevice,
+                           e->h2d));
         if (h_cpu_o) {
             CU(cudaMemcpyAsync(d_co + lo * qd, h_cpu_o + lo * qd, n * qd * 4, cudaMemcpyHostToDevice, e->h2d));
             CU(cudaMemcpyAsync(d_cm + lo * md, h_cpu_ml + lo * md, n * md * 4, cudaMemcpyHostToDevice, e->h2d));
         }
         if ((rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
     }
-    // ---- K1 per q_pred chunk, on the whole GPU (before K2 starts); the
-    // CPU-side ids go out to the host worker right after each chunk
-    for (int c = 0; c < nch; ++c) {
-        const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
-        CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[c], 0));
-        if ((rc = e->select_batch(lo, n, d_qt, d_qp, step, par, e->k1s)) != SCOUT_OK) return rc;
-        if (h_cpu_ids) {
-            CU(cudaEventRecord(e->ev_k1[c], e->k1s));
-            CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[c], 0));
-            CU(cudaMemcpyAsync(h_cpu_ids + e->lk(lo), e->I(e->cpu_ids[par]) + e->lk(lo),
-                               static_cast<size_t>(n) * e->U * e->cfg.k * 4, cudaMemcpyDeviceToHost, e->d2h));
-            if (h_n_cpu)
-                CU(cudaMemcpyAsync(h_n_cpu + e->lu(lo), e->I(e->n_cpu[par]) + e->lu(lo),
-                                   static_cast<size_t>(n) * e->U * 4, cudaMemcpyDeviceToHost, e->d2h));
-        }
+    // ---- K1 for every layer in one launch once q_pred landed (in steady state
+    // it was copied while the previous step's K2 ran); the CPU-side ids then
+    // go out to the host worker
+    CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[0], 0));
+    if ((rc = e->select_batch(0, L, d_qt, d_qp, step, par, e->k1s)) != SCOUT_OK) return rc;
+    if (h_cpu_ids) {
+        CU(cudaEventRecord(e->ev_k1[0], e->k1s));
+        CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[0], 0));
+        CU(cudaMemcpyAsync(h_cpu_ids, e->I(e->cpu_ids[par]), static_cast<size_t>(L) * e->U * e->cfg.k * 4,
+                           cudaMemcpyDeviceToHost, e->d2h));
+        if (h_n_cpu)
+            CU(cudaMemcpyAsync(h_n_cpu, e->I(e->n_cpu[par]), static_cast<size_t>(L) * e->U * 4, cudaMemcpyDeviceToHost,
+                               e->d2h));
     }
     CU(cudaEventRecord(e->ev_k1_end, e->k1s));
     CU(cudaStreamWaitEvent(st, e->ev_k1_end, 0));
     // ---- K2: one launch; layer i waits for its input chunk's flag on the device
-    std::vector<const float*> q(L), co(L), cml(L);
+    std::vector<const void*> q(L);
+    std::vector<const float*> co(L), cml(L);
     std::vector<float*> o(L), ml(L);
     std::vector<const unsigned*> inflag(L);
     for (int i = 0; i < L; ++i) {
-        q[i] = d_qt + i * qd;
+        q[i] = d_qt + i * qd * qb;
         co[i] = h_cpu_o ? d_co + i * qd : nullptr;
         cml[i] = h_cpu_ml ? d_cm + i * md : nullptr;
         o[i] = d_o + i * qd;
@@ -481,9 +565,11 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
         SCOUT_OK)
         return rc;
     if ((rc = e->issue_recalls(step)) != SCOUT_OK) return rc;
-    // ---- outputs: each chunk leaves once every CTA finished its last layer
-    for (int c = 0; c < nch; ++c) {
-        const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
+    // ---- outputs: OUT_CH layers at a time, each group leaving once every CTA
+    // finished its last layer (a short tail after K2 ends)
+    constexpr int OUT_CH = 4;
+    for (int lo = 0; lo < L; lo += OUT_CH) {
+        const int n = lo + OUT_CH > L ? L - lo : OUT_CH;
         if ((rc = wait_value(e->d2h, e->layer_done + lo + n - 1, token * static_cast<unsigned>(e->grid))) != SCOUT_OK)
             return rc;
         CU(cudaMemcpyAsync(h_out_o + lo * qd, d_o + lo * qd, n * qd * 4, cudaMemcpyDeviceToHost, e->d2h));
@@ -500,6 +586,7 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const fl
 extern "C" int scout_engine_sync(scout_engine* e, void* stream) {
     if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
+    e->drain_recalls();
     CU(cudaEventRecord(e->ev_tmp, e->side));
     CU(cudaStreamWaitEvent(st, e->ev_tmp, 0));
     return SCOUT_OK;

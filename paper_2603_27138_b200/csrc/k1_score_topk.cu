@@ -394,8 +394,11 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
     for (int i = tid; i < D * G; i += K1_THREADS) {
         const int g = i / D, c = i % D;
         double v;
-        if constexpr (MODE == 0) v = static_cast<const float*>(a.q)[(static_cast<size_t>(u) * G + g) * D + c];
-        else v = static_cast<const double*>(a.q)[(static_cast<size_t>(u) * G + g) * D + c];
+        const size_t qi = (static_cast<size_t>(u) * G + g) * D + c;
+        if constexpr (MODE == 0)
+            v = a.q_dtype == SCOUT_BF16 ? static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(a.q)[qi]))
+                                        : static_cast<const float*>(a.q)[qi];
+        else v = static_cast<const double*>(a.q)[qi];
         qs[c * G + g] = v;
     }
     if (tid < 2) { s_tok[tid] = 0; s_cnt[tid] = 0; }
@@ -662,6 +665,11 @@ int validate(const scout_topk_args& a) {
     }
     if (a.group != 1 && a.group != 2 && a.group != 4 && a.group != 8) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_score_topk_split: group %d not in {1,2,4,8}", a.group);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (a.q_dtype != SCOUT_F32 && !(a.q_dtype == SCOUT_BF16 && a.digest_dtype != SCOUT_F64)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_score_topk_split: q dtype %d unsupported with digest dtype %d",
+                  a.q_dtype, a.digest_dtype);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     if (a.n_units > 0 && (!a.q || !a.digests || !a.n_tokens)) {

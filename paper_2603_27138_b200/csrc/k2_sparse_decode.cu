@@ -325,17 +325,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
             uint32_t bh[8][2], bl[8][2];
             {
                 const bool live = g < G;
-                const float* qh = io.q + (static_cast<size_t>(u) * G + (live ? g : 0)) * D;
+                const size_t qoff = (static_cast<size_t>(u) * G + (live ? g : 0)) * D;
+                if (a.q_bf16) {  // the query is bf16 already: lo part zero
+                    const uint32_t* qb = reinterpret_cast<const uint32_t*>(static_cast<const __nv_bfloat16*>(io.q) + qoff);
 #pragma unroll
-                for (int kk = 0; kk < 8; ++kk) {
+                    for (int kk = 0; kk < 8; ++kk)
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        float2 v = live ? *reinterpret_cast<const float2*>(qh + 16 * kk + 8 * half + 2 * t)
-                                        : make_float2(0.f, 0.f);
-                        const __nv_bfloat162 hv = __floats2bfloat162_rn(v.x, v.y);
-                        const float2 hf = __bfloat1622float2(hv);
-                        bh[kk][half] = *reinterpret_cast<const uint32_t*>(&hv);
-                        bl[kk][half] = pack_bf16(v.x - hf.x, v.y - hf.y);
+                        for (int half = 0; half < 2; ++half) {
+                            bh[kk][half] = live ? qb[(16 * kk + 8 * half + 2 * t) >> 1] : 0u;
+                            bl[kk][half] = 0u;
+                        }
+                } else {
+                    const float* qh = static_cast<const float*>(io.q) + qoff;
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            float2 v = live ? *reinterpret_cast<const float2*>(qh + 16 * kk + 8 * half + 2 * t)
+                                            : make_float2(0.f, 0.f);
+                            const __nv_bfloat162 hv = __floats2bfloat162_rn(v.x, v.y);
+                            const float2 hf = __bfloat1622float2(hv);
+                            bh[kk][half] = *reinterpret_cast<const uint32_t*>(&hv);
+                            bl[kk][half] = pack_bf16(v.x - hf.x, v.y - hf.y);
+                        }
                     }
                 }
             }
@@ -387,7 +399,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                         uint32_t a0, a1, a2, a3;
                         ldsm_x4(addr, a0, a1, a2, a3);
                         mma_bf16(sh[mt], a0, a1, a2, a3, bh[kk][0], bh[kk][1]);
-                        mma_bf16(slo[mt], a0, a1, a2, a3, bl[kk][0], bl[kk][1]);
+                        if (!a.q_bf16) mma_bf16(slo[mt], a0, a1, a2, a3, bl[kk][0], bl[kk][1]);
                     }
                 }
                 // ---- online softmax (columns = heads 2t, 2t+1; rows = tokens)
@@ -602,7 +614,7 @@ __global__ void __launch_bounds__(NW * 32) decode_f32_kernel(const scout_decode_
     float qv[G][4];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-        const float4 x = *reinterpret_cast<const float4*>(a.q + (static_cast<size_t>(u) * G + g) * D + 4 * lane);
+        const float4 x = *reinterpret_cast<const float4*>(static_cast<const float*>(a.q) + (static_cast<size_t>(u) * G + g) * D + 4 * lane);
         qv[g][0] = x.x; qv[g][1] = x.y; qv[g][2] = x.z; qv[g][3] = x.w;
     }
     float m2[G], l[G], o[G][4];
@@ -757,6 +769,11 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_sparse_decode: group %d not in {1,2,4,8}", a.group);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
+    if (a.q_dtype != SCOUT_F32 && !(a.q_dtype == SCOUT_BF16 && a.kv_dtype == SCOUT_BF16)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_sparse_decode: q dtype %d unsupported with kv dtype %d",
+                  a.q_dtype, a.kv_dtype);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
     if (a.n_units == 0) return SCOUT_OK;
     if (!a.q || !a.kv_pool || !a.res_slots || !a.res_ids || !a.n_res || !a.n_tokens || !a.o || !a.ml ||
         !a.workspace || ((a.cpu_o == nullptr) != (a.cpu_ml == nullptr))) {
@@ -781,6 +798,7 @@ extern "C" int scout_sparse_decode(const scout_decode_args* args, void* stream) 
         k.workspace = a.workspace;
         k.ws_layer_bytes = a.workspace_bytes;
         k.max_ctas = a.max_ctas;
+        k.q_bf16 = a.q_dtype == SCOUT_BF16;
         k.layers[0] = K2Layer{a.q, a.res_slots, a.res_ids, a.n_res, a.cpu_o, a.cpu_ml, a.o, a.ml, nullptr, 0u, 0u};
         return scout_k2_launch(k, st, (a.flags & SCOUT_LAUNCH_PDL) != 0);
     } else if (a.kv_dtype == SCOUT_F32) {

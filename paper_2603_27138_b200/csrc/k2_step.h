@@ -8,7 +8,7 @@
 constexpr int K2_MAX_LAYERS = 96;  // kernel parameters carry the per-layer I/O by value
 
 struct K2Layer {
-    const float* q;          // [U*G][128] true query of the layer
+    const void* q;           // [U*G][128] true query of the layer (f32, or bf16 if q_bf16)
     const int32_t* res_slots;
     const int32_t* res_ids;
     const int32_t* n_res;
@@ -33,6 +33,7 @@ struct K2StepArgs {
     unsigned* layer_done;     // optional [n_layers]: += 1 per CTA when its share of layer L is written
     unsigned token;
     int max_ctas;
+    int q_bf16;               // queries are bf16 (else f32)
     K2Layer layers[K2_MAX_LAYERS];
 };
 

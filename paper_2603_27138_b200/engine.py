@@ -32,7 +32,7 @@ def _p(t):
 class DecodeEngine:
     def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
                  recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
-                 recall_mode=0):
+                 recall_mode=0, q_dtype=torch.float32):
         self.L, self.batch, self.hq, self.hkv, self.G, self.k = layers, batch, hq, hkv, hq // hkv, k
         self.U = batch * hkv
         self.layer_states = layer_states  # keep tensors alive
@@ -47,6 +47,8 @@ class DecodeEngine:
         cfg.kv_pool, cfg.n_tokens, cfg.host_tier = _p(pool), _p(n_tokens), _p(host_tier)
         cfg.max_ctas, cfg.host_staging, cfg.chunk_layers = int(max_ctas), int(host_staging), int(chunk_layers)
         cfg.recall_mode = int(recall_mode)
+        cfg.q_dtype = ops.dtype_code(q_dtype)
+        self.q_dtype = q_dtype
         descs = (A.LayerDesc * layers)()
         for i, st in enumerate(layer_states):
             descs[i].digests, descs[i].block_table = _p(st.digests), _p(st.table)

@@ -92,7 +92,7 @@ def kv_append(pool, kv_dtype, method, open_slot, n_tokens, k_rows, v_rows, diges
 
 def score_topk_split(q, digests, n_tokens, k, group, *, method=A.SCOUT_DIGEST_MINMAX, block_table=None, step=0,
                      k_stride=None, want_scores=False, last_selected=None, out=None):
-    """K1. q [units*G][128] (f32, or f64 for f64 digests); digests [units][2|1][128][nb_stride].
+    """K1. q [units*G][128] (f32 or bf16, or f64 for f64 digests); digests [units][2|1][128][nb_stride].
 
     Returns a dict of device tensors: sel_ids/n_sel, and when block_table is given
     res_slots/res_ids/n_res, cpu_ids/n_cpu, res_tokens/cpu_tokens (+ scores)."""
@@ -111,6 +111,7 @@ def score_topk_split(q, digests, n_tokens, k, group, *, method=A.SCOUT_DIGEST_MI
     args.n_units, args.group, args.digest_dtype, args.method = n_units, int(group), dtype_code(digests.dtype), int(method)
     args.k, args.k_stride, args.nb_stride, args.step = int(k), ks, nb_stride, int(step)
     args.q, args.digests, args.n_tokens = _p(q), _p(digests), _p(n_tokens)
+    args.q_dtype = A.SCOUT_BF16 if q.dtype == torch.bfloat16 else A.SCOUT_F32
     args.sel_ids, args.n_sel = _p(buf("sel_ids", (n_units, ks))), _p(buf("n_sel", (n_units,)))
     if block_table is not None:
         args.block_table = _p(block_table)
@@ -152,6 +153,7 @@ def sparse_decode(q, pool, kv_dtype, res_slots, res_ids, n_res, n_tokens, group,
     args.n_units, args.group, args.kv_dtype, args.k_stride = n_units, int(group), dtype_code(kv_dtype), int(res_slots.shape[-1])
     args.scale = float(scale)
     args.q, args.kv_pool, args.res_slots, args.res_ids = _p(q), _p(pool), _p(res_slots), _p(res_ids)
+    args.q_dtype = A.SCOUT_BF16 if q.dtype == torch.bfloat16 else A.SCOUT_F32
     args.n_res, args.n_tokens, args.cpu_o, args.cpu_ml = _p(n_res), _p(n_tokens), _p(cpu_o), _p(cpu_ml)
     args.o, args.ml = _p(o), _p(ml)
     args.workspace, args.workspace_bytes, args.max_ctas = _p(workspace.buf), workspace.buf.numel(), int(max_ctas)

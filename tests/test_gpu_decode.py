@@ -131,6 +131,26 @@ def test_sparse_decode_merges_cpu_partial(cuda, dtype):
     check(o, ml, *oracle_outputs(c, U, G, dtype, cpu=(cpu_o, cpu_ml)), dtype)
 
 
+@pytest.mark.parametrize("G", [1, 8])
+def test_sparse_decode_bf16_queries(cuda, G):
+    """bf16 queries (q_dtype = SCOUT_BF16) against the oracle on the same
+    bf16-rounded query values, with a CPU partial merge."""
+    rng = np.random.default_rng(500 + G)
+    U = 9
+    nb_list = [int(x) for x in rng.integers(1, 30, size=U)]
+    n_res = [int(rng.integers(0, nb + 1)) for nb in nb_list]
+    c = build_case(rng, U, G, nb_list, n_res, torch.bfloat16)
+    c["q"] = torch.from_numpy(c["q"]).bfloat16().float().numpy()
+    cpu_o = rng.standard_normal((U * G, D)).astype(np.float32)
+    cpu_ml = np.stack([rng.standard_normal(U * G), rng.random(U * G) * 10 + 0.5], axis=1).astype(np.float32)
+    d = c["dev"]
+    o, ml = ops.sparse_decode(d["q"].bfloat16(), c["pool"], torch.bfloat16, d["res_slots"], d["res_ids"], d["n_res"],
+                              d["n_tokens"], G, cpu_o=torch.as_tensor(cpu_o, device="cuda"),
+                              cpu_ml=torch.as_tensor(cpu_ml, device="cuda"), max_ctas=5)
+    torch.cuda.synchronize()
+    check(o, ml, *oracle_outputs(c, U, G, torch.bfloat16, cpu=(cpu_o, cpu_ml)), torch.bfloat16)
+
+
 def test_sparse_decode_large_logits_bf16(cuda):
     """Keys scaled x8: logits of tens, exercises the online-softmax rescaling."""
     rng = np.random.default_rng(9)

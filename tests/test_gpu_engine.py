@@ -14,7 +14,7 @@ from paper_2603_27138_b200.engine import DecodeEngine, LayerState
 pytestmark = pytest.mark.gpu
 
 
-def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True):
+def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True, q_dtype=torch.float32):
     dev = torch.device("cuda")
     U = batch * hkv
     nbs = ((nb + 7) // 8) * 8
@@ -42,9 +42,9 @@ def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True):
     eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=n_tokens, pool=pool,
                        kv_dtype=torch.bfloat16, layer_states=layers, scale=1 / math.sqrt(D),
                        recall_interval=2 if recall else 0, host_tier=host if recall else None, host_staging=True,
-                       chunk_layers=2)
-    q_true = torch.randn(L, U * G, D, device=dev)
-    q_pred = torch.randn(L, U * G, D, device=dev)
+                       chunk_layers=2, q_dtype=q_dtype)
+    q_true = torch.randn(L, U * G, D, device=dev).to(q_dtype)
+    q_pred = torch.randn(L, U * G, D, device=dev).to(q_dtype)
     cpu_o = torch.randn(L, U * G, D, device=dev)
     cpu_ml = torch.stack([torch.randn(L, U * G, device=dev), torch.rand(L, U * G, device=dev) * 5 + 0.5], -1).contiguous()
     return dict(eng=eng, pool=pool, layers=layers, n_tokens=n_tokens, q_true=q_true, q_pred=q_pred, cpu_o=cpu_o,
@@ -65,10 +65,11 @@ def reference_step(c):
     return outs
 
 
-def test_engine_device_step_matches_per_layer_ops(cuda):
-    c = build(np.random.default_rng(11), recall=False)
+@pytest.mark.parametrize("q_dtype", [torch.float32, torch.bfloat16])
+def test_engine_device_step_matches_per_layer_ops(cuda, q_dtype):
+    c = build(np.random.default_rng(11), recall=False, q_dtype=q_dtype)
     want = reference_step(c)
-    out_o = torch.empty_like(c["q_true"])
+    out_o = torch.empty(c["q_true"].shape, device="cuda")
     out_ml = torch.empty(c["L"], c["U"] * c["G"], 2, device="cuda")
     for step in (1, 2, 3):  # several launches: tokens / parities advance
         c["eng"].decode_step(step, c["q_true"], c["q_pred"], c["cpu_o"], c["cpu_ml"], out_o, out_ml)
@@ -78,12 +79,13 @@ def test_engine_device_step_matches_per_layer_ops(cuda):
             assert torch.equal(out_ml[li], want[li][1]), (step, li)
 
 
-def test_engine_host_path_matches_device_path(cuda):
-    c = build(np.random.default_rng(12), recall=False)
+@pytest.mark.parametrize("q_dtype", [torch.float32, torch.bfloat16])
+def test_engine_host_path_matches_device_path(cuda, q_dtype):
+    c = build(np.random.default_rng(12), recall=False, q_dtype=q_dtype)
     want = reference_step(c)
     pin = lambda t: t.cpu().pin_memory()  # noqa: E731
     h = [pin(c[n]) for n in ("q_true", "q_pred", "cpu_o", "cpu_ml")]
-    h_out = torch.empty(c["q_true"].shape).pin_memory()
+    h_out = torch.empty(c["q_true"].shape, dtype=torch.float32).pin_memory()
     h_ml = torch.empty(c["L"], c["U"] * c["G"], 2).pin_memory()
     h_ids = torch.full((c["L"], c["U"], c["k"]), -1, dtype=torch.int32).pin_memory()
     h_ncpu = torch.full((c["L"], c["U"]), -1, dtype=torch.int32).pin_memory()
@@ -106,7 +108,7 @@ def test_engine_host_path_matches_device_path(cuda):
 
 def test_engine_recall_moves_blocks_after_attention(cuda):
     c = build(np.random.default_rng(13), recall=True)
-    out_o = torch.empty_like(c["q_true"])
+    out_o = torch.empty(c["q_true"].shape, device="cuda")
     out_ml = torch.empty(c["L"], c["U"] * c["G"], 2, device="cuda")
     eng, sb = c["eng"], c["sb"]
     for step in (1, 2, 3, 4):

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 import py_oracle as P
-from helpers import D, from_bf16, load_golden, make_digests, make_queries, nbs_for
+from helpers import D, bf16_round, from_bf16, load_golden, make_digests, make_queries, nbs_for
 from paper_2603_27138_b200 import ops
 
 pytestmark = pytest.mark.gpu
@@ -88,6 +88,33 @@ def test_topk_band_edges_vs_oracle(cuda, G, kind, dtype):
             ns = want["n_sel"][u]
             assert got["n_sel"][u] == ns
             assert np.array_equal(got["sel_ids"][u, :ns], want["sel_ids"][u, :ns]), (kind, u, k)
+
+
+@pytest.mark.parametrize("G", [1, 4, 8])
+@pytest.mark.parametrize("kind", ["iid", "perm"])
+def test_topk_bf16_queries_vs_oracle(cuda, G, kind):
+    """bf16 queries (the model's own dtype; q_dtype = SCOUT_BF16): the oracle
+    sees the same bf16-rounded values, selection and scores stay bit-exact."""
+    rng = np.random.default_rng(hash(("bf16q", G, kind)) % 2**32)
+    U, nbs = 16, nbs_for(260)
+    n_tokens = rng.integers(1, 64 * 260, size=U).astype(np.int32)
+    dig = make_digests(rng, U, nbs, kind)
+    q = bf16_round(make_queries(rng, U, G, kind))
+    table = np.where(rng.random((U, nbs)) < 0.8, rng.integers(0, 10**6, size=(U, nbs)), -1).astype(np.int32)
+    dev = torch.device("cuda")
+    for k in (1, 33, 64):
+        want = P.score_topk_split(q, dig, n_tokens, k, G, table=table, k_stride=k)
+        r = ops.score_topk_split(torch.from_numpy(q).to(dev).bfloat16(), torch.from_numpy(dig).to(dev).bfloat16(),
+                                 torch.from_numpy(n_tokens).to(dev), k, G,
+                                 block_table=torch.from_numpy(table).to(dev), want_scores=True)
+        got = {k_: v.cpu().numpy() for k_, v in r.items()}
+        for u in range(U):
+            ns, nr = want["n_sel"][u], want["n_res"][u]
+            assert got["n_sel"][u] == ns and got["n_res"][u] == nr
+            assert np.array_equal(got["sel_ids"][u, :ns], want["sel_ids"][u, :ns]), (u, k)
+            assert np.array_equal(got["res_slots"][u, :nr], want["res_slots"][u, :nr])
+            nb = (n_tokens[u] + 63) // 64
+            assert np.array_equal(got["scores"][u, :nb].view(np.uint64), want["scores"][u, :nb].view(np.uint64))
 
 
 def test_topk_generic_f64_paths(cuda):
