@@ -90,6 +90,7 @@ def ref():
             L.ref_cache_state.argtypes = [vp, C.c_int, _ip, _lp, _ip]
             L.ref_cache_place.argtypes = [vp, C.c_int, _dp, C.c_int]
             L.ref_cache_digests.argtypes = [vp, C.c_int, C.c_int, C.c_int, _dp]
+            L.ref_predict_query.argtypes = [_dp, C.c_int, _dp, C.c_int, _dp]
         _c["r"] = L
     return _c["r"]
 
@@ -273,3 +274,12 @@ class RefCache:
         out = np.zeros((2, self.d, nb_stride))
         n = self.L.ref_cache_digests(self.h, layer, self.d, nb_stride, out)
         return out, n
+
+
+def predict_query(x, w):
+    """The reference's predict_next_query(rms_normalize(x), w) (checker only)."""
+    x, w = f64(x), f64(w)
+    out = np.zeros(w.shape[1])
+    if ref().ref_predict_query(x, x.shape[0], w, w.shape[1], out) != 0:
+        raise ValueError("predict_next_query")
+    return out

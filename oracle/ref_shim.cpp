@@ -19,6 +19,7 @@
 #include "scout/attention.hpp"
 #include "scout/digest.hpp"
 #include "scout/kv_store.hpp"
+#include "scout/model.hpp"
 
 using scout::BlockDigest;
 using scout::BlockIdSet;
@@ -376,6 +377,19 @@ int ref_cache_digests(void* c, int layer, int d, int nb_stride, double* out) {
             out[static_cast<size_t>(d + ch) * nb_stride + b] = ds[b].hi[ch];
         }
     return static_cast<int>(ds.size());
+}
+
+// predict_next_query(rms_normalize(x), W) (model.hpp:215-217, numerics.hpp:99-123):
+// the oracle of K6. W [hidden][n_out] row-major.
+int ref_predict_query(const double* x, int hidden, const double* w, int n_out, double* out) {
+    try {
+        const Vec xn = scout::rms_normalize(Vec(x, x + hidden));
+        const Vec q = scout::predict_next_query(xn, mat_from(w, hidden, n_out));
+        std::memcpy(out, q.data(), sizeof(double) * n_out);
+        return 0;
+    } catch (const std::invalid_argument&) {
+        return -1;
+    }
 }
 
 }  // extern "C"

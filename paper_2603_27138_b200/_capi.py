@@ -32,7 +32,7 @@ EXPORTED = (
     "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
     "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k1_outputs",
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
-    "scout_tier_place",
+    "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
 )
 
 _vp = C.c_void_p
@@ -114,6 +114,11 @@ def lib() -> C.CDLL:
         L.scout_tier_plan.argtypes = [_tl, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp]
         L.scout_tier_mark.argtypes = [_tl, C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_tier_place.argtypes = [_tl, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp]
+        L.scout_qpred_workspace_bytes.argtypes = [C.c_int] * 4
+        L.scout_qpred_workspace_bytes.restype = C.c_size_t
+        L.scout_qpred_pack_weights.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
+        L.scout_predict_query.argtypes = [_vp, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp, _vp, C.c_size_t, C.c_int,
+                                          _vp]
         L.scout_kv_append.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_score_topk_split.argtypes = [C.POINTER(TopkArgs), _vp]
         L.scout_score_topk_split_batch.argtypes = [C.POINTER(TopkArgs), C.c_int, _vp]
