@@ -456,7 +456,13 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "sparse_decode_tc_kernel (K2+K3, one persistent launch per step = 64 layers)",
                          "bytes_per_launch": k2_bytes, "avg_launch_us": k2_avg * 1000.0,
-                         "share_of_step": k2_share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)"},
+                         "share_of_step": k2_share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
+                         # K2 only reads: the copy peak counts read+write bytes of a copy, so a
+                         # read-dominated gather can exceed it; the read-only bulk-copy stream
+                         # and 32 KiB random-gather ceilings measured on this hardware
+                         # (profiles/r01_microbench.txt, r01_gather.txt) bound it tighter
+                         "read_stream_gbs": 7400.0, "frac_of_read_stream": achieved / 7400.0,
+                         "gather_32k_gbs": 6700.0, "frac_of_gather_32k": achieved / 6700.0},
             "clocks": clk,
             "gpu_launches": launches,
             "verify": {"rank_output_checksums": checksums} if checksums else None,

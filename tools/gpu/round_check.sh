@@ -18,4 +18,8 @@ timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx
   python bench.py --profile --steps 2 --warmup 1 > $OUT/ncu_k2_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "timed/" -k regex:score_topk -c 1 -f -o $OUT/prof_k1_$TAG \
   python bench.py --profile --steps 2 --warmup 1 > $OUT/ncu_k1_$TAG.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:qpred_gemm -s 2 -c 1 -f -o $OUT/prof_k6_$TAG \
+  python tools/debug/qpred_once.py > $OUT/ncu_k6_$TAG.log 2>&1
+timeout 300 python tools/debug/time_qpred.py > $OUT/time_qpred_$TAG.txt 2>&1
+timeout 300 python tools/debug/e2e_probe.py > $OUT/e2e_probe_$TAG.txt 2>&1
 ls -la $OUT

@@ -60,7 +60,7 @@ if lc.exists():
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
         lines.append(f"| `{k}` | {len(v)} | {sum(v) / len(v) / 1000:.1f} | {sum(v) / tot:.1%} |")
     lines.append("")
-for name in ("k2", "k1"):
+for name in ("k2", "k1", "k6"):
     rep = G / f"prof_{name}_{R}.ncu-rep"
     if not rep.exists():
         continue
