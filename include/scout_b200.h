@@ -299,15 +299,16 @@ int scout_tier_place(const scout_tier_layer* layer, int n_units, int nb_stride, 
  * (model.hpp:215-217, numerics.hpp:99-123, called at engine.hpp:237).
  * W [hidden][n_out] bf16 (the reference's hidden x out layout) is packed once
  * into UMMA core-matrix tiles (w_packed: hidden*n_out bf16). x [batch][hidden]
- * f32, batch <= 256, hidden % 64 == 0, n_out % 128 == 0. Outputs q_pred
+ * f32, batch <= 256, hidden % 128 == 0, n_out % 128 == 0. Outputs q_pred
  * [batch][n_out] as f32 and/or bf16 (either may be NULL): fp32 accumulation of
- * bf16 products. workspace: scout_qpred_workspace_bytes(), zeroed once (the
- * kernel leaves its counters zeroed). ksplit: K splits per 128-feature tile
- * (0 = 2), reduced in split order (deterministic).                          */
-size_t scout_qpred_workspace_bytes(int hidden, int n_out, int batch, int ksplit);
+ * bf16 products. Stream-K over (128-feature tile, 64-wide K chunk) units on
+ * max_ctas CTAs (0 = one per SM); a tile shared by several CTAs is summed in
+ * CTA order (deterministic). workspace: scout_qpred_workspace_bytes() for the
+ * same max_ctas, zeroed once (the kernel leaves its counters zeroed).      */
+size_t scout_qpred_workspace_bytes(int hidden, int n_out, int batch, int max_ctas);
 int scout_qpred_pack_weights(const void* w, int hidden, int n_out, void* w_packed, void* stream);
 int scout_predict_query(const float* x, int batch, int hidden, const void* w_packed, int n_out, float* out_f32,
-                        void* out_bf16, void* workspace, size_t workspace_bytes, int ksplit, void* stream);
+                        void* out_bf16, void* workspace, size_t workspace_bytes, int max_ctas, void* stream);
 
 /* ------------------------------------------------------------- engine --
  * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,

@@ -191,14 +191,14 @@ class QueryPredictor:
     on the tcgen05 tensor cores. W [hidden][n_out] (the reference's layout) is
     packed once at construction."""
 
-    def __init__(self, w: torch.Tensor, batch: int, ksplit: int = 2):
+    def __init__(self, w: torch.Tensor, batch: int, max_ctas: int = 0):
         self.hidden, self.n_out = int(w.shape[0]), int(w.shape[1])
         self.dev = w.device
         w = w.to(torch.bfloat16).contiguous()
         self.w_packed = torch.empty_like(w)
         A.check(A.lib().scout_qpred_pack_weights(_p(w), self.hidden, self.n_out, _p(self.w_packed), _stream()))
-        self.batch, self.ksplit = batch, ksplit
-        nbytes = int(A.lib().scout_qpred_workspace_bytes(self.hidden, self.n_out, batch, ksplit))
+        self.batch, self.max_ctas = batch, max_ctas
+        nbytes = int(A.lib().scout_qpred_workspace_bytes(self.hidden, self.n_out, batch, max_ctas))
         self.ws = torch.zeros(nbytes, dtype=torch.uint8, device=self.dev)
 
     def __call__(self, x: torch.Tensor, out_f32=None, out_bf16=None, want=("f32",)):
@@ -210,5 +210,5 @@ class QueryPredictor:
         if out_bf16 is None and "bf16" in want:
             out_bf16 = torch.empty(b, self.n_out, dtype=torch.bfloat16, device=self.dev)
         A.check(A.lib().scout_predict_query(_p(x), b, self.hidden, _p(self.w_packed), self.n_out, _p(out_f32),
-                                            _p(out_bf16), _p(self.ws), self.ws.numel(), self.ksplit, _stream()))
+                                            _p(out_bf16), _p(self.ws), self.ws.numel(), self.max_ctas, _stream()))
         return out_f32 if out_bf16 is None else (out_bf16 if out_f32 is None else (out_f32, out_bf16))

@@ -13,13 +13,15 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("hidden,n_out", [(256, 256), (640, 384)])
 @pytest.mark.parametrize("batch", [1, 5, 32, 40])
-@pytest.mark.parametrize("ksplit", [1, 2, 3])
-def test_predict_query_vs_reference(cuda, hidden, n_out, batch, ksplit):
-    rng = np.random.default_rng(hidden + n_out + batch + 7 * ksplit)
+@pytest.mark.parametrize("max_ctas", [0, 2, 5])
+def test_predict_query_vs_reference(cuda, hidden, n_out, batch, max_ctas):
+    """max_ctas 0: one CTA per SM (tiles shared by several CTAs); 2 / 5: the
+    minimum grid (= tiles: whole tiles) and a grid that splits tiles unevenly."""
+    rng = np.random.default_rng(hidden + n_out + batch + 7 * max_ctas)
     w = torch.from_numpy(rng.standard_normal((hidden, n_out)).astype(np.float32) / np.sqrt(hidden)).bfloat16()
     x = rng.standard_normal((batch, hidden)).astype(np.float32) * 3.0
     x[0, :] = 0.0 if batch > 2 else x[0, :]  # rms == 0 row: rms_normalize returns x unchanged
-    qp = ops.QueryPredictor(w.cuda(), batch, ksplit=ksplit)
+    qp = ops.QueryPredictor(w.cuda(), batch, max_ctas=max_ctas)
     q32, qbf = qp(torch.from_numpy(x), want=("f32", "bf16"))
     torch.cuda.synchronize()
     q32, qbf = q32.cpu(), qbf.cpu()

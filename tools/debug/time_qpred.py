@@ -14,8 +14,8 @@ hidden, n_out, batch = 5120, 8192, 32
 w = (torch.randn(hidden, n_out, device="cuda") / hidden ** 0.5).bfloat16()
 x = torch.randn(batch, hidden, device="cuda")
 peak = json.load(open("MEASURED_PEAKS.json")).get("hbm_gbs", 6537.0)
-for ks in (1, 2, 4):
-    qp = ops.QueryPredictor(w, batch, ksplit=ks)
+for ks in (0, 148, 296):
+    qp = ops.QueryPredictor(w, batch, max_ctas=ks)
     o = torch.empty(batch, n_out, device="cuda")
     for _ in range(5):
         qp(x, out_f32=o)
@@ -34,4 +34,4 @@ for ks in (1, 2, 4):
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) / 100 * 1000
     byts = hidden * n_out * 2 + batch * hidden * 4 + batch * n_out * 4
-    print(f"ksplit {ks}: {us:.1f} us per layer, {byts / us / 1e3:.0f} GB/s ({byts / us / 1e3 / peak:.2f} of {peak:.0f})")
+    print(f"max_ctas {ks}: {us:.1f} us per layer, {byts / us / 1e3:.0f} GB/s ({byts / us / 1e3 / peak:.2f} of {peak:.0f})")
