@@ -21,6 +21,7 @@
 #include "scout_common.cuh"
 
 #include <cstdlib>
+#include <type_traits>
 
 using namespace scout_dev;
 
@@ -40,7 +41,8 @@ constexpr int K1_THREADS = SCOUT_K1_THREADS;
 static_assert(K1_THREADS >= 128, "one thread per channel when staging the query sums");
 constexpr int K1_MAXBUF = 4;                    // digest chunk buffers (bulk-copy ring), runtime depth <= this
 constexpr int K1_CHUNK_BYTES = 8192;            // lo + hi rows of one chunk (default; SCOUT_K1_CHUNK)
-constexpr int K1_REG_BLOCKS = 4 * K1_THREADS;   // nb_stride up to this: running scores live in registers
+constexpr int K1_REG_BLOCKS = 16 * K1_THREADS;  // nb_stride up to this: running scores live in registers
+                                                // (up to 4 block quads per thread)
 
 // qs [D*G] f64 | pn [D] float2 | keys [nbs] u64 | cls [nbs] u8 | (nbs > K1_REG_BLOCKS:
 // s_acc [nbs] f64 | a_acc [nbs] f32) | digest chunk ring (MODE 0)
@@ -334,7 +336,9 @@ __device__ __forceinline__ void fast_quad(const DigT* blo, const DigT* bhi, int 
     }
 }
 
-template <typename DigT, int G, int MODE>
+// QPT: block quads per thread whose running scores live in registers (1: up
+// to 512 blocks, 4: up to 2048); 0: shared-memory accumulators (any size).
+template <typename DigT, int G, int MODE, int QPT>
 __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(const K1Batch batch) {
     const scout_topk_args& a = batch.a[blockIdx.y];  // layer of this CTA (one launch can cover many)
     extern __shared__ __align__(16) uint8_t k1_smem[];
@@ -429,19 +433,28 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
                 atomicMax(reinterpret_cast<int*>(&s_amax), 0x7f800000);
         }
         const int nq = (nb + 3) >> 2;
-        const bool regs = ns <= static_cast<size_t>(K1_REG_BLOCKS);  // one quad per thread at most
+        constexpr bool regs = QPT > 0;
         if (!regs)
             for (int i = tid; i < nq * 4; i += K1_THREADS) { s_acc[i] = 0.0; a_acc[i] = 0.f; }
         __syncthreads();
-        double rs[4] = {0.0, 0.0, 0.0, 0.0};
-        float ra[4] = {0.f, 0.f, 0.f, 0.f};
+        constexpr int RQ = QPT > 0 ? QPT : 1;
+        double rs[RQ][4];
+        float ra[RQ][4];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) { rs[q][e] = 0.0; ra[q][e] = 0.f; }
         for (int c = 0; c < nchunks; ++c) {
             mbar_wait(&s_full[c % nbuf], (c / nbuf) & 1);
             const int ch0 = c * cpc, nch = min(cpc, D - ch0);
             const DigT* blo = reinterpret_cast<const DigT*>(stagebuf + static_cast<size_t>(c % nbuf) * 2 * lo_bytes);
             const DigT* bhi = reinterpret_cast<const DigT*>(reinterpret_cast<const uint8_t*>(blo) + lo_bytes);
-            if (regs) {
-                if (tid < nq) fast_quad<DigT>(blo, bhi, static_cast<int>(ns), 4 * tid, nch, pn, ch0, rs, ra);
+            if constexpr (regs) {
+#pragma unroll
+                for (int q = 0; q < QPT; ++q) {
+                    const int j = tid + q * K1_THREADS;
+                    if (j < nq) fast_quad<DigT>(blo, bhi, static_cast<int>(ns), 4 * j, nch, pn, ch0, rs[q], ra[q]);
+                }
             } else {
                 for (int j = tid; j < nq; j += K1_THREADS) {
                     double s4[4];
@@ -457,14 +470,17 @@ __global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(c
             if (tid == 0 && c + nbuf < nchunks) issue(c + nbuf);
         }
         float amax = 0.f;
-        if (regs) {
-            if (tid < nq)
+        if constexpr (regs) {
+#pragma unroll
+            for (int q = 0; q < QPT; ++q) {
+                const int j = tid + q * K1_THREADS;
 #pragma unroll
                 for (int e = 0; e < 4; ++e)
-                    if (4 * tid + e < nb) {
-                        keys[4 * tid + e] = score_key(rs[e]);
-                        amax = fmaxf(amax, ra[e] * 1.0001f);
+                    if (4 * j + e < nb) {
+                        keys[4 * j + e] = score_key(rs[q][e]);
+                        amax = fmaxf(amax, ra[q][e] * 1.0001f);
                     }
+            }
         } else {
             for (int b = tid; b < nb; b += K1_THREADS) {
                 keys[b] = score_key(s_acc[(b & 3) * nq + (b >> 2)]);
@@ -631,17 +647,32 @@ int launch_g(K1Batch& b, cudaStream_t st) {
     }();
     b.nbuf = nbuf_env;
     b.chunk = chunk_env;
+    // many blocks per unit: at least 4 channels per chunk (fewer ring round trips)
+    if (MODE == 0 && a.nb_stride > 512) {
+        const int four = 4 * a.nb_stride * 2 * static_cast<int>(sizeof(DigT));
+        const int want = four < 32768 ? four : 32768;
+        if (b.chunk < want) b.chunk = want;
+    }
     const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)), b.nbuf, b.chunk)
                                   : k1_stage_offset(a.group, a.nb_stride);
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
         scout_host::launch(kern, dim3(a.n_units, b.n), dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
     };
+    const int qpt = MODE != 0 ? 1 : (a.nb_stride <= 4 * K1_THREADS ? 1 : (a.nb_stride <= K1_REG_BLOCKS ? 4 : 0));
+    auto pick = [&](auto g) {
+        constexpr int Gv = decltype(g)::value;
+        if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1>);
+        else if constexpr (MODE == 0) {
+            if (qpt == 4) go(score_topk_kernel<DigT, Gv, MODE, 4>);
+            else go(score_topk_kernel<DigT, Gv, MODE, 0>);
+        }
+    };
     switch (a.group) {
-        case 1: go(score_topk_kernel<DigT, 1, MODE>); break;
-        case 2: go(score_topk_kernel<DigT, 2, MODE>); break;
-        case 4: go(score_topk_kernel<DigT, 4, MODE>); break;
-        case 8: go(score_topk_kernel<DigT, 8, MODE>); break;
+        case 1: pick(std::integral_constant<int, 1>{}); break;
+        case 2: pick(std::integral_constant<int, 2>{}); break;
+        case 4: pick(std::integral_constant<int, 4>{}); break;
+        case 8: pick(std::integral_constant<int, 8>{}); break;
         default: return -1;
     }
     return 0;

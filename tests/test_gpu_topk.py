@@ -117,6 +117,24 @@ def test_topk_bf16_queries_vs_oracle(cuda, G, kind):
             assert np.array_equal(got["scores"][u, :nb].view(np.uint64), want["scores"][u, :nb].view(np.uint64))
 
 
+@pytest.mark.parametrize("nb", [1000, 2048, 2600])
+def test_topk_many_blocks_vs_oracle(cuda, nb):
+    """Long contexts: running scores in registers (4 quads per thread, <= 2048
+    blocks) and in shared memory (> 2048), 4-channel digest chunks."""
+    rng = np.random.default_rng(nb)
+    U, G, nbs = 4, 8, nbs_for(nb)
+    n_tokens = np.array([64 * nb, 64 * nb - 63, 64 * (nb // 2) + 5, 64 * nb - 1], np.int32)
+    dig = make_digests(rng, U, nbs)
+    q = make_queries(rng, U, G)
+    for k in (128, 512):
+        want = P.score_topk_split(q, dig, n_tokens, k, G, k_stride=k)
+        got = _gpu_topk(q, dig, n_tokens, k, G)
+        for u in range(U):
+            ns = want["n_sel"][u]
+            assert got["n_sel"][u] == ns
+            assert np.array_equal(got["sel_ids"][u, :ns], want["sel_ids"][u, :ns]), (u, k)
+
+
 def test_topk_generic_f64_paths(cuda):
     """Arbitrary doubles (the drop-in wrapper's path): minmax and mean, no fma."""
     rng = np.random.default_rng(7)
