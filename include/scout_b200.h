@@ -310,6 +310,21 @@ int scout_qpred_pack_weights(const void* w, int hidden, int n_out, void* w_packe
 int scout_predict_query(const float* x, int batch, int hidden, const void* w_packed, int n_out, float* out_f32,
                         void* out_bf16, void* workspace, size_t workspace_bytes, int max_ctas, void* stream);
 
+/* Device-driven tier data movement. Host tier layout: the image of block
+ * (layer, unit, id) at index host_base + unit * nb_stride + id, with
+ * host_base = layer * n_units * nb_stride, modulo host_blocks when > 0 (a
+ * bounded synthetic tier whose images alias) (pinned, device-mapped memory).
+ * scout_recall_gather_ids: unit u's blocks ids[u][0..n_ids[u]) (e.g. K1's
+ * CPU-side ids) into the slots K5 assigned (dst_slots, -1 = skipped), SM
+ * loads over PCIe / C2C, ctas_per_unit CTAs per unit (0 = 2).
+ * scout_kv_writeback: write-through of the blocks scout_tier_append sealed
+ * (sealed_id[u] >= 0 at slot open_slot[u]) into their host images.        */
+int scout_recall_gather_ids(void* kv_pool, int kv_dtype, const void* host_tier, long long host_base, int nb_stride,
+                            long long host_blocks, int n_units, const int32_t* ids, const int32_t* n_ids, const int32_t* dst_slots,
+                            int k_stride, int ctas_per_unit, void* stream);
+int scout_kv_writeback(const void* kv_pool, int kv_dtype, void* host_tier, long long host_base, int nb_stride,
+                       long long host_blocks, int n_units, const int32_t* open_slot, const int32_t* sealed_id, void* stream);
+
 /* ------------------------------------------------------------- engine --
  * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,
  * engine.hpp:205-314, GPU side): per layer i, K1 for layer i+1 with the
@@ -342,6 +357,17 @@ typedef struct scout_engine_config {
     int chunk_layers;          /* layers per H2D/D2H chunk of the host path (0 = 8) */
     int recall_mode;           /* 0: copy engines (scout_recall_copy), 1: SM gather kernel (K4) */
     int q_dtype;               /* q_true / q_pred element type: SCOUT_F32 (0) or SCOUT_BF16 */
+    /* device tier mode (optional): per-layer K5 state (host array of `layers`
+     * descs over device arrays). Residency is then planned on the device
+     * (layers[].block_table and recall plans are ignored), decode steps take
+     * the new token's K/V (scout_engine_decode_step_kv) and append it, seal
+     * blocks with write-through to host_tier, evict LRU, and recall each
+     * layer's CPU-side selected blocks every recall_interval steps straight
+     * from K1's lists (no host round trip). host_tier holds block images at
+     * ((layer * U + unit) * nb_stride + id) % host_blocks (host_blocks <= 0:
+     * no wrap; the bench bounds it and lets images alias).                 */
+    const scout_tier_layer* tier;
+    long long host_blocks;
 } scout_engine_config;
 
 typedef struct scout_engine scout_engine;
@@ -364,6 +390,14 @@ int scout_engine_decode_step(scout_engine* eng, int step, const void* q_true, co
 int scout_engine_decode_step_host(scout_engine* eng, int step, const void* h_q_true, const void* h_q_pred,
                                   const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o, float* h_out_ml,
                                   int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream);
+/* Device tier mode: one decode step with the token's new K/V rows k_new /
+ * v_new [L][U][128] f32 appended after each layer's attention (the order of
+ * engine.hpp:220-307: plan, select + mark, begin_layer's ticket application,
+ * attention + merge, append, recall). The other arguments as
+ * scout_engine_decode_step. n_tokens (cfg) advances by one per step.      */
+int scout_engine_decode_step_kv(scout_engine* eng, int step, const void* q_true, const void* q_pred,
+                                const float* cpu_o, const float* cpu_ml, const float* k_new, const float* v_new,
+                                float* out_o, float* out_ml, void* stream);
 /* Order all outstanding side-stream work (recalls) before `stream`. */
 int scout_engine_sync(scout_engine* eng, void* stream);
 /* Instrumentation: when enabled, CUDA events bracket every K2 launch (on the

@@ -33,6 +33,7 @@ EXPORTED = (
     "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k1_outputs",
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
+    "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv",
 )
 
 _vp = C.c_void_p
@@ -80,6 +81,7 @@ class EngineConfig(C.Structure):
         ("kv_pool", _vp), ("n_tokens", _vp), ("host_tier", _vp), ("max_ctas", C.c_int),
         ("host_staging", C.c_int), ("chunk_layers", C.c_int), ("recall_mode", C.c_int),
         ("q_dtype", C.c_int),
+    ("tier", _vp), ("host_blocks", C.c_longlong),
     ]
 
 
@@ -119,6 +121,10 @@ def lib() -> C.CDLL:
         L.scout_qpred_pack_weights.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
         L.scout_predict_query.argtypes = [_vp, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp, _vp, C.c_size_t, C.c_int,
                                           _vp]
+        L.scout_recall_gather_ids.argtypes = [_vp, C.c_int, _vp, C.c_longlong, C.c_int, C.c_longlong, C.c_int, _vp,
+                                              _vp, _vp, C.c_int, C.c_int, _vp]
+        L.scout_kv_writeback.argtypes = [_vp, C.c_int, _vp, C.c_longlong, C.c_int, C.c_longlong, C.c_int, _vp, _vp,
+                                         _vp]
         L.scout_kv_append.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_score_topk_split.argtypes = [C.POINTER(TopkArgs), _vp]
         L.scout_score_topk_split_batch.argtypes = [C.POINTER(TopkArgs), C.c_int, _vp]
@@ -131,6 +137,7 @@ def lib() -> C.CDLL:
         L.scout_engine_create.argtypes = [C.POINTER(EngineConfig), C.POINTER(LayerDesc), C.POINTER(_vp)]
         L.scout_engine_destroy.argtypes = [_vp]
         L.scout_engine_decode_step.argtypes = [_vp, C.c_int] + [_vp] * 6 + [_vp]
+        L.scout_engine_decode_step_kv.argtypes = [_vp, C.c_int] + [_vp] * 8 + [_vp]
         L.scout_engine_decode_step_host.argtypes = [_vp, C.c_int] + [_vp] * 8 + [_vp]
         L.scout_engine_sync.argtypes = [_vp, _vp]
         L.scout_engine_set_timing.argtypes = [_vp, C.c_int]

@@ -137,6 +137,17 @@ struct scout_engine {
     bool rc_stop = false, rc_busy = false;
     int rc_err = SCOUT_OK;
     char rc_msg[256] = {0};
+    // device tier mode (cfg.tier != nullptr)
+    bool tier_mode = false;
+    std::vector<scout_tier_layer> tier;
+    Buf plan_tab;                  // [L][U][nbs] residency planning view (K1's block tables)
+    Buf open_slot, sealed_id;      // [L][U] append bookkeeping
+    Buf tier_dst;                  // [L][U][k] recall destination slots
+    std::vector<int> pending;      // per layer: ready tick of its in-flight recall ticket, -1 none
+    int n_tickets = 0;
+    cudaEvent_t ev_side_end = nullptr;
+    bool side_recorded = false;
+    int tick(int step, int layer) const { return step * cfg.layers + layer; }
     // instrumentation
     bool timing = false;
     std::vector<cudaEvent_t> tev;
@@ -151,7 +162,7 @@ struct scout_engine {
         stop_recalls();
         for (cudaStream_t s : {k1s, side, h2d, d2h})
             if (s) cudaStreamDestroy(s);
-        for (cudaEvent_t e : {ev_start, ev_k1_end, ev_tmp, ev_k2[0], ev_k2[1], stage_free[0], stage_free[1]})
+        for (cudaEvent_t e : {ev_start, ev_k1_end, ev_tmp, ev_k2[0], ev_k2[1], stage_free[0], stage_free[1], ev_side_end})
             if (e) cudaEventDestroy(e);
         for (auto e : ev_k1) cudaEventDestroy(e);
         for (auto e : chunk_ev) cudaEventDestroy(e);
@@ -178,7 +189,8 @@ struct scout_engine {
         a.q = q;
         a.digests = layers[layer].digests;
         a.n_tokens = cfg.n_tokens;
-        a.block_table = layers[layer].block_table;
+        a.block_table = tier_mode ? I(plan_tab) + static_cast<size_t>(layer) * U * cfg.nb_stride : layers[layer].block_table;
+        if (tier_mode) a.last_selected = tier[layer].last_sel;  // mark_selected (kv_store.hpp:222-228)
         a.sel_ids = I(sel_ids[par]) + lk(layer);
         a.n_sel = I(n_sel[par]) + lu(layer);
         a.res_slots = I(res_slots[par]) + lk(layer);
@@ -352,7 +364,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 KV)", K2_MAX_LAYERS);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
-    if (c.recall_interval > 0 && !c.host_tier) {
+    if ((c.recall_interval > 0 || c.tier) && !c.host_tier) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: recall needs a host tier");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
@@ -428,8 +440,20 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     for (cudaEvent_t* ev : {&e->ev_start, &e->ev_k1_end, &e->ev_tmp, &e->ev_k2[0], &e->ev_k2[1], &e->stage_free[0],
                             &e->stage_free[1]})
         cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    if (c.tier) {
+        e->tier_mode = true;
+        e->tier.assign(c.tier, c.tier + c.layers);
+        const size_t lu = static_cast<size_t>(c.layers) * e->U;
+        if (e->plan_tab.alloc(lu * c.nb_stride * 4) || e->open_slot.alloc(lu * 4) || e->sealed_id.alloc(lu * 4) ||
+            e->tier_dst.alloc(lu * c.k * 4) || cudaEventCreateWithFlags(&e->ev_side_end, cudaEventDisableTiming)) {
+            delete e;
+            set_error(SCOUT_ERR_CUDA, "scout_engine_create: tier-mode allocation failed");
+            return SCOUT_ERR_CUDA;
+        }
+        e->pending.assign(c.layers, -1);
+    }
     cudaGetDevice(&e->device);
-    if (c.recall_interval > 0) e->rc_thread = std::thread([e] { e->recall_loop(); });
+    if (c.recall_interval > 0 && !c.tier) e->rc_thread = std::thread([e] { e->recall_loop(); });
     e->ev_k1.resize(c.layers);
     for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     e->chunk_ev.resize(e->nch);
@@ -580,6 +604,92 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const vo
     if ((rc = e->end_step(st)) != SCOUT_OK) return rc;
     CU(cudaEventRecord(e->stage_free[par], st));
     e->stage_recorded[par] = true;
+    return SCOUT_OK;
+}
+
+extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void* q_true, const void* q_pred,
+                                           const float* cpu_o, const float* cpu_ml, const float* k_new,
+                                           const float* v_new, float* out_o, float* out_ml, void* stream) {
+    using scout_host::set_error;
+    if (!e || !e->tier_mode || !q_true || !q_pred || !k_new || !v_new || !out_o || !out_ml ||
+        ((cpu_o == nullptr) != (cpu_ml == nullptr))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_decode_step_kv: null buffer or engine without tier state");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    const int L = e->cfg.layers, U = e->U, nbs = e->cfg.nb_stride, k = e->cfg.k;
+    const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
+    const unsigned token = ++e->token;
+    const int par = token & 1;
+    int rc;
+    // the previous step's appends / recalls (tier state, digests, n_tokens) first
+    if (e->side_recorded) CU(cudaStreamWaitEvent(st, e->ev_side_end, 0));
+    // 1. residency planning view of every layer at this step (residency_set at
+    //    (step, i-1) == at step start: later ops of the step touch other layers)
+    for (int i = 0; i < L; ++i)
+        if ((rc = scout_tier_plan(&e->tier[i], U, nbs, e->cfg.n_tokens, e->tick(step, i),
+                                  e->I(e->plan_tab) + static_cast<size_t>(i) * U * nbs, st)) != SCOUT_OK)
+            return rc;
+    // 2. select + split + mark_selected for every layer (one launch)
+    if ((rc = e->select_batch(0, L, q_true, q_pred, step, par, st)) != SCOUT_OK) return rc;
+    // 3. begin_layer: tickets due at (step, i), applied after the marks
+    for (int i = 0; i < L; ++i) {
+        if (e->pending[i] < 0 || e->pending[i] > e->tick(step, i)) continue;
+        if ((rc = scout_tier_apply(&e->tier[i], U, nbs, e->cfg.n_tokens, e->tick(step, i), nullptr, st)) != SCOUT_OK)
+            return rc;
+        e->pending[i] = -1;
+    }
+    // 4. attention + merge over all layers (one persistent launch)
+    std::vector<const void*> q(L);
+    std::vector<const float*> co(L), cml(L);
+    std::vector<float*> o(L), ml(L);
+    for (int i = 0; i < L; ++i) {
+        q[i] = e->qlayer(q_true, i);
+        co[i] = cpu_o ? cpu_o + i * qd : nullptr;
+        cml[i] = cpu_ml ? cpu_ml + i * md : nullptr;
+        o[i] = out_o + i * qd;
+        ml[i] = out_ml + i * md;
+    }
+    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, false, st)) != SCOUT_OK)
+        return rc;
+    // 5. per layer, once every CTA finished it: append the token (open / seal,
+    //    LRU eviction, write-through) and, when due, recall the layer's
+    //    CPU-side selected blocks (maybe_schedule_recall, recall.hpp:114-126)
+    CU(cudaEventRecord(e->ev_tmp, st));
+    CU(cudaStreamWaitEvent(e->side, e->ev_tmp, 0));
+    const size_t sb = scout_slot_bytes(e->cfg.kv_dtype);
+    (void)sb;
+    for (int i = 0; i < L; ++i) {
+        if ((rc = wait_value(e->side, e->layer_done + i, token * static_cast<unsigned>(e->grid))) != SCOUT_OK) return rc;
+        int32_t* os = e->I(e->open_slot) + static_cast<size_t>(i) * U;
+        int32_t* sid = e->I(e->sealed_id) + static_cast<size_t>(i) * U;
+        const long long hbase = static_cast<long long>(i) * U * nbs;
+        if ((rc = scout_tier_append(&e->tier[i], U, nbs, e->cfg.n_tokens, step, os, sid, e->side)) != SCOUT_OK) return rc;
+        if ((rc = scout_kv_append(e->cfg.kv_pool, e->cfg.kv_dtype, SCOUT_DIGEST_MINMAX, U, os, const_cast<int32_t*>(e->cfg.n_tokens),
+                                  k_new + static_cast<size_t>(i) * U * SCOUT_HEAD_DIM,
+                                  v_new + static_cast<size_t>(i) * U * SCOUT_HEAD_DIM,
+                                  const_cast<void*>(e->layers[i].digests), nbs, i == L - 1, e->side)) != SCOUT_OK)
+            return rc;
+        if ((rc = scout_kv_writeback(e->cfg.kv_pool, e->cfg.kv_dtype, const_cast<void*>(e->cfg.host_tier), hbase, nbs,
+                                     e->cfg.host_blocks, U, os, sid, e->side)) != SCOUT_OK)
+            return rc;
+        if (e->cfg.recall_interval > 0 && (step + i) % e->cfg.recall_interval == 0) {
+            const int32_t* ids = e->I(e->cpu_ids[par]) + e->lk(i);
+            const int32_t* nids = e->I(e->n_cpu[par]) + e->lu(i);
+            int32_t* dst = e->I(e->tier_dst) + e->lk(i);
+            if ((rc = scout_tier_schedule_recall(&e->tier[i], U, nbs, e->cfg.n_tokens, ids, nids, k,
+                                                 e->tick(step + 1, i), e->n_tickets++, dst, e->side)) != SCOUT_OK)
+                return rc;
+            if ((rc = scout_recall_gather_ids(e->cfg.kv_pool, e->cfg.kv_dtype, e->cfg.host_tier, hbase, nbs,
+                                              e->cfg.host_blocks, U, ids, nids, dst, k, 1, e->side)) != SCOUT_OK)
+                return rc;
+            if ((rc = write_value(e->side, e->recall_flag + i, token)) != SCOUT_OK) return rc;
+            e->rc_token[i] = token;  // the next step's K2 waits for it before streaming layer i
+            e->pending[i] = e->tick(step + 1, i);
+        }
+    }
+    CU(cudaEventRecord(e->ev_side_end, e->side));
+    e->side_recorded = true;
     return SCOUT_OK;
 }
 

@@ -145,3 +145,109 @@ extern "C" int scout_recall_copy(void* kv_pool, int kv_dtype, const void* host_b
     }
     return SCOUT_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Device-driven tier data movement (the engine's device-tier mode): the block
+// lists live in HBM (K1's CPU-side ids, K5's slots), so the copies are issued
+// by kernels instead of host copy descriptors.
+//   host tier layout: block (layer, unit, id) at index (layer * n_units + unit) * nb_stride + id,
+//   modulo host_blocks when host_blocks > 0 (a bounded synthetic tier: images alias)
+namespace {
+
+// recall: unit u's n_ids[u] blocks ids[u][i] -> pool slots dst[u][i] (-1: rejected ticket)
+__device__ __forceinline__ long long host_index(long long base, int u, int nb_stride, int id, long long host_blocks) {
+    const long long i = base + static_cast<long long>(u) * nb_stride + id;
+    return host_blocks > 0 ? i % host_blocks : i;
+}
+
+__global__ void __launch_bounds__(256) recall_ids_kernel(uint8_t* pool, const uint8_t* host, long long host_base,
+                                                         int nb_stride, long long host_blocks, const int32_t* ids,
+                                                         const int32_t* n_ids, const int32_t* dst, int k_stride,
+                                                         size_t slot_bytes) {
+    const int u = blockIdx.y;
+    const int n = n_ids[u];
+    const int nvec = static_cast<int>(slot_bytes / 16);
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const int slot = dst[static_cast<size_t>(u) * k_stride + i];
+        if (slot < 0) continue;
+        const long long hb = host_index(host_base, u, nb_stride, ids[static_cast<size_t>(u) * k_stride + i], host_blocks);
+        const int4* s = reinterpret_cast<const int4*>(host + static_cast<size_t>(hb) * slot_bytes);
+        int4* d = reinterpret_cast<int4*>(pool + static_cast<size_t>(slot) * slot_bytes);
+        for (int base = threadIdx.x; base < nvec; base += 4 * blockDim.x) {
+            int4 v[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int idx = base + k * blockDim.x;
+                if (idx < nvec) v[k] = __ldcv(s + idx);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int idx = base + k * blockDim.x;
+                if (idx < nvec) d[idx] = v[k];
+            }
+        }
+    }
+}
+
+// seal write-through: the block unit u sealed (sealed_id[u] >= 0, slot
+// open_slot[u]) is copied to its host-tier image, which becomes the slow copy
+__global__ void __launch_bounds__(256) writeback_kernel(const uint8_t* pool, uint8_t* host, long long host_base,
+                                                        int nb_stride, long long host_blocks, const int32_t* open_slot,
+                                                        const int32_t* sealed_id, size_t slot_bytes) {
+    const int u = blockIdx.x;
+    const int id = sealed_id[u];
+    if (id < 0) return;
+    const int4* s = reinterpret_cast<const int4*>(pool + static_cast<size_t>(open_slot[u]) * slot_bytes);
+    int4* d = reinterpret_cast<int4*>(host + static_cast<size_t>(host_index(host_base, u, nb_stride, id, host_blocks)) *
+                                      slot_bytes);
+    const int nvec = static_cast<int>(slot_bytes / 16);
+    for (int i = threadIdx.x; i < nvec; i += blockDim.x) d[i] = __ldcg(s + i);
+}
+
+const void* device_view(const void* host) {
+    void* dv = nullptr;
+    if (cudaHostGetDevicePointer(&dv, const_cast<void*>(host), 0) == cudaSuccess && dv) return dv;
+    cudaGetLastError();
+    return host;
+}
+
+}  // namespace
+
+extern "C" int scout_recall_gather_ids(void* kv_pool, int kv_dtype, const void* host_tier, long long host_base,
+                                       int nb_stride, long long host_blocks, int n_units, const int32_t* ids, const int32_t* n_ids,
+                                       const int32_t* dst_slots, int k_stride, int ctas_per_unit, void* stream) {
+    using namespace scout_host;
+    if (kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32) {
+        set_error(SCOUT_ERR_UNSUPPORTED, "scout_recall_gather_ids: kv dtype %d unsupported", kv_dtype);
+        return SCOUT_ERR_UNSUPPORTED;
+    }
+    if (n_units < 0 || nb_stride <= 0 || k_stride <= 0 ||
+        (n_units > 0 && (!kv_pool || !host_tier || !ids || !n_ids || !dst_slots))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_recall_gather_ids: bad arguments");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (n_units == 0) return SCOUT_OK;
+    const int cpu = ctas_per_unit > 0 ? ctas_per_unit : 2;
+    recall_ids_kernel<<<dim3(cpu, n_units), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<uint8_t*>(kv_pool), static_cast<const uint8_t*>(device_view(host_tier)), host_base, nb_stride,
+        host_blocks, ids, n_ids, dst_slots, k_stride, slot_bytes(kv_dtype));
+    return check_launch("scout_recall_gather_ids");
+}
+
+extern "C" int scout_kv_writeback(const void* kv_pool, int kv_dtype, void* host_tier, long long host_base, int nb_stride,
+                                  long long host_blocks, int n_units, const int32_t* open_slot, const int32_t* sealed_id, void* stream) {
+    using namespace scout_host;
+    if (kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32) {
+        set_error(SCOUT_ERR_UNSUPPORTED, "scout_kv_writeback: kv dtype %d unsupported", kv_dtype);
+        return SCOUT_ERR_UNSUPPORTED;
+    }
+    if (n_units < 0 || nb_stride <= 0 || (n_units > 0 && (!kv_pool || !host_tier || !open_slot || !sealed_id))) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_kv_writeback: bad arguments");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (n_units == 0) return SCOUT_OK;
+    writeback_kernel<<<n_units, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint8_t*>(kv_pool), static_cast<uint8_t*>(const_cast<void*>(device_view(host_tier))), host_base,
+        nb_stride, host_blocks, open_slot, sealed_id, slot_bytes(kv_dtype));
+    return check_launch("scout_kv_writeback");
+}

@@ -32,7 +32,10 @@ def _p(t):
 class DecodeEngine:
     def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
                  recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
-                 recall_mode=0, q_dtype=torch.float32):
+                 recall_mode=0, q_dtype=torch.float32, tier=None, host_blocks=0):
+        """tier: a tier.DeviceTieredCache whose state the engine drives on the
+        device (device tier mode: decode_step_kv); host_tier then holds block
+        images at ((layer*U + unit)*nb_stride + id) % host_blocks."""
         self.L, self.batch, self.hq, self.hkv, self.G, self.k = layers, batch, hq, hkv, hq // hkv, k
         self.U = batch * hkv
         self.layer_states = layer_states  # keep tensors alive
@@ -48,6 +51,11 @@ class DecodeEngine:
         cfg.max_ctas, cfg.host_staging, cfg.chunk_layers = int(max_ctas), int(host_staging), int(chunk_layers)
         cfg.recall_mode = int(recall_mode)
         cfg.q_dtype = ops.dtype_code(q_dtype)
+        self.tier = tier
+        if tier is not None:
+            self._tier_descs = (A.TierLayer * layers)(*[tier.layer_desc(i) for i in range(layers)])
+            cfg.tier = C.cast(self._tier_descs, C.c_void_p)
+            cfg.host_blocks = int(host_blocks)
         self.q_dtype = q_dtype
         descs = (A.LayerDesc * layers)()
         for i, st in enumerate(layer_states):
@@ -74,6 +82,11 @@ class DecodeEngine:
         """Device tensors: q_true/q_pred/cpu_o/out_o [L][U*G][128] f32, cpu_ml/out_ml [L][U*G][2]."""
         A.check(A.lib().scout_engine_decode_step(self._h, int(step), _p(q_true), _p(q_pred), _p(cpu_o), _p(cpu_ml),
                                                  _p(out_o), _p(out_ml), self._stream()))
+
+    def decode_step_kv(self, step, q_true, q_pred, cpu_o, cpu_ml, k_new, v_new, out_o, out_ml):
+        """Device tier mode: the step appends k_new / v_new [L][U][128] f32."""
+        A.check(A.lib().scout_engine_decode_step_kv(self._h, int(step), _p(q_true), _p(q_pred), _p(cpu_o), _p(cpu_ml),
+                                                    _p(k_new), _p(v_new), _p(out_o), _p(out_ml), self._stream()))
 
     def decode_step_host(self, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, h_out_o, h_out_ml, h_cpu_ids=None,
                          h_n_cpu=None):

@@ -80,8 +80,10 @@ class DeviceTieredCache:
         self.capacity[layer] = 0
 
     def append_token(self, layer: int, k_rows=None, v_rows=None, pool=None, kv_dtype=None, digests=None,
-                     method=0):
-        """One token for every unit. Without a pool only the bookkeeping runs."""
+                     method=0, host_tier=None, host_blocks=0):
+        """One token for every unit. Without a pool only the bookkeeping runs;
+        with host_tier, sealed blocks are written through to their host images
+        ((layer*U + unit)*nb_stride + id, modulo host_blocks)."""
         lib, st = A.lib(), torch.cuda.current_stream(self.dev).cuda_stream
         open_slot = torch.empty(self.U, dtype=torch.int32, device=self.dev)
         sealed = torch.empty(self.U, dtype=torch.int32, device=self.dev)
@@ -91,6 +93,10 @@ class DeviceTieredCache:
                                       open_slot.data_ptr(), sealed.data_ptr(), st))
         if pool is not None:
             ops.kv_append(pool, kv_dtype, method, open_slot, nt, k_rows, v_rows, digests, self.nbs, advance=True)
+            if host_tier is not None:
+                A.check(lib.scout_kv_writeback(pool.data_ptr(), ops.dtype_code(kv_dtype), host_tier.data_ptr(),
+                                               layer * self.U * self.nbs, self.nbs, int(host_blocks), self.U,
+                                               open_slot.data_ptr(), sealed.data_ptr(), st))
         else:
             nt.add_(1)
         return open_slot, sealed

@@ -1,0 +1,109 @@
+"""Device tier mode of the C++ engine (scout_engine_decode_step_kv): a whole
+decode step on the device in the order of ScoutEngine::decode_step
+(engine.hpp:220-307): planning view, select + mark, begin_layer's ticket
+application, attention + merge, append (open / seal / LRU eviction,
+write-through), periodic recall of the CPU-side selected blocks. Compared,
+step after step, with a replay of the reference's per-layer order through the
+validated single ops and the DeviceTieredCache mirror (itself bit-exact
+against the reference TieredKvCache, test_gpu_tier.py)."""
+import ctypes as C
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2603_27138_b200 import _capi as A
+from paper_2603_27138_b200 import ops
+from paper_2603_27138_b200.engine import DecodeEngine, LayerState
+from paper_2603_27138_b200.tier import DeviceTieredCache
+
+pytestmark = pytest.mark.gpu
+D, BS = 128, 64
+
+
+class Side:
+    """One side of the comparison: its own pool, digests, host tier and tier state."""
+
+    def __init__(self, L, U, nbs, cap, kv, seed_rows):
+        dev = torch.device("cuda")
+        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=nbs)
+        self.tier.pin_layer(0)
+        self.pool = ops.alloc_pool(L * U * nbs, kv)
+        self.dig = [torch.zeros(U, 2, D, nbs, dtype=kv, device=dev) for _ in range(L)]
+        self.host = torch.zeros(L * U * nbs * ops.slot_bytes(kv), dtype=torch.uint8).pin_memory()
+        self.n_tokens = torch.zeros(U, dtype=torch.int32, device=dev)
+        self.kv = kv
+        for layer in range(L):  # prefill: appends that seal (and evict: capacity holds during prefill)
+            for k_rows, v_rows in seed_rows[layer]:
+                self.tier.append_token(layer, k_rows, v_rows, self.pool, kv, self.dig[layer], host_tier=self.host)
+        self.n_tokens.copy_(self.tier.n_tokens[0])
+
+
+@pytest.mark.parametrize("recall", [3, 0])
+def test_engine_tier_mode_matches_reference_order_replay(cuda, recall):
+    rng = np.random.default_rng(21 + recall)
+    L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 70
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 12 + 40
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    eng_side, rep = Side(L, U, nbs, cap, kv, seed_rows), Side(L, U, nbs, cap, kv, seed_rows)
+    layers = [LayerState(eng_side.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda"))
+              for i in range(L)]
+    eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=eng_side.n_tokens,
+                       pool=eng_side.pool, kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D),
+                       recall_interval=recall, host_tier=eng_side.host, tier=eng_side.tier, host_blocks=0,
+                       q_dtype=torch.bfloat16)
+    out_o = torch.empty(L, U * G, D, device="cuda")
+    out_ml = torch.empty(L, U * G, 2, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    rt = rep.tier
+    for step in range(1, steps + 1):
+        q_true = torch.randn(L, U * G, D, device="cuda").bfloat16()
+        q_pred = (q_true.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).bfloat16()
+        cpu_o = torch.randn(L, U * G, D, device="cuda")
+        cpu_ml = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
+        k_new = torch.randn(L, U, D, device="cuda")
+        v_new = torch.randn(L, U, D, device="cuda")
+        eng.decode_step_kv(step, q_true, q_pred, cpu_o, cpu_ml, k_new, v_new, out_o, out_ml)
+        # ---- replay in the reference's per-layer order
+        sel = [None] * L
+        want = []
+        for i in range(L):
+            rt.begin_layer(step, i)
+            targets = ([0] if i == 0 else []) + ([i + 1] if i + 1 < L else [])
+            for t in targets:
+                q = q_true[0] if t == 0 else q_pred[t]
+                sel[t] = ops.score_topk_split(q, rep.dig[t], rep.n_tokens, k, G, block_table=rt.residency_table(t),
+                                              step=step, last_selected=rt.last_sel[t], k_stride=k)
+            r = sel[i]
+            o, ml = ops.sparse_decode(q_true[i], rep.pool, kv, r["res_slots"], r["res_ids"], r["n_res"], rep.n_tokens,
+                                      G, cpu_o=cpu_o[i], cpu_ml=cpu_ml[i])
+            want.append((o, ml))
+            rt.append_token(i, k_new[i], v_new[i], rep.pool, kv, rep.dig[i], host_tier=rep.host)
+            if recall and (step + i) % recall == 0:
+                dst = rt.schedule_recall(i, r["cpu_ids"], r["n_cpu"], step, i)
+                A.check(A.lib().scout_recall_gather_ids(rep.pool.data_ptr(), ops.dtype_code(kv), rep.host.data_ptr(),
+                                                        i * U * nbs, nbs, 0, U, r["cpu_ids"].data_ptr(),
+                                                        r["n_cpu"].data_ptr(), dst.data_ptr(), k, 1, st))
+                rt.check(i)
+        rep.n_tokens.copy_(rt.n_tokens[0])
+        eng.sync()
+        torch.cuda.synchronize()
+        for i in range(L):
+            assert torch.equal(out_o[i], want[i][0]), (step, i)
+            assert torch.equal(out_ml[i], want[i][1]), (step, i)
+        assert torch.equal(eng_side.n_tokens, rep.n_tokens)
+        for name in ("tier", "last_sel"):
+            assert torch.equal(getattr(eng_side.tier, name), getattr(rt, name)), (step, name)
+        assert torch.equal(eng_side.tier.ready >= 0, rt.ready >= 0), step
+        assert int(eng_side.tier.err.abs().sum()) == 0
+    # the run crossed seals (evictions) and, with recall, flipped tiers back
+    assert int(eng_side.n_tokens[0]) == T0 + steps
+    nb = (T0 + steps + BS - 1) // BS
+    assert int((eng_side.tier.tier[1:, :, :nb - 1] == 0).sum()) > 0  # sealed blocks on the slow tier
+    assert (rt.n_tickets > 0) == (recall > 0)
+    # digests (incrementally maintained) equal on both sides and the pools hold the same live blocks
+    for i in range(L):
+        assert torch.equal(eng_side.dig[i], rep.dig[i])
