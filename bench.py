@@ -1,6 +1,13 @@
 #!/usr/bin/env python
 """Benchmark: ScoutAttention GPU-side sparse decode at Qwen3-32B shape, 32K context.
 
+Default (--tier device): the complete decode step of ScoutEngine::decode_step
+(engine.hpp:220-307) on the device: residency planning, select + mark,
+begin_layer's ticket application, attention + LSE merge, append of the
+token's K/V with digest refresh (seal write-through, LRU eviction), and the
+periodic recall of each layer's CPU-side selected blocks. --tier static is
+the kernel view: residency fixed at the paper's 8.2% CPU share, no appends.
+
 Workload (BASELINE.json configs[2], the metric's config): 64 layers, 64 query /
 8 KV heads, head_dim 128, batch 32 per GPU, 32K-token context (512 blocks of
 64 tokens per (request, KV head)), top-64 block selection, bf16 KV, layer-ahead
@@ -193,6 +200,118 @@ class Workload:
         return res_tokens_total * 2 * D * 2 + UG * (D * 4 + (D + 2) * 4 + (D + 2) * 4)
 
 
+class TierWorkload:
+    """Device tier mode (--tier device): the full decode step of the reference
+    (plan, select + mark, ticket application, attention + merge, append of the
+    token's K/V with seal write-through and LRU eviction, periodic recall of
+    the CPU-side selected blocks), all bookkeeping on the device (K5). Same
+    shape and synthetic data as Workload; the initial placement keeps the
+    selected blocks minus the CPU share resident, like Workload's table.
+    Queries stay stationary, so recalls pull the CPU share in and the
+    resident fraction grows over the run (reported)."""
+
+    def __init__(self, cfg, dev, seed, max_steps):
+        from paper_2603_27138_b200 import ops
+        from paper_2603_27138_b200.engine import DecodeEngine, LayerState
+        from paper_2603_27138_b200.tier import DeviceTieredCache
+
+        self.cfg = cfg
+        L, hq, hkv, B = cfg["layers"], cfg["hq"], cfg["hkv"], cfg["batch"]
+        G = hq // hkv
+        U = B * hkv
+        nb = cfg["ctx"] // BS
+        nbs = ((nb + (max_steps + BS - 1) // BS + 1 + 7) // 8) * 8  # room for the appended tokens
+        k, cap = cfg["k"], cfg["capacity"]
+        self.L, self.U, self.G, self.nb, self.k = L, U, G, nb, k
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        gcpu = torch.Generator().manual_seed(seed)
+        kv_dt = torch.bfloat16
+        spu = [nbs] + [cap + cfg["headroom"] + 8] * (L - 1)  # pinned layer 0; capacity + in-flight + open block
+        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=spu, device=dev)
+        self.tier.pin_layer(0)
+        self.pool = ops.alloc_pool(self.tier.n_slots, kv_dt, dev)
+        pv = self.pool.view(torch.bfloat16)
+        for s0 in range(0, pv.numel(), 1 << 28):
+            pv[s0:min(pv.numel(), s0 + (1 << 28))].normal_(generator=g)
+        # requests differ in length (by < one block), so seals (and their
+        # write-through) spread over steps instead of all units at once
+        lens = cfg["ctx"] - 2 * (torch.arange(B, device=dev, dtype=torch.int32) % 32)
+        self.n_tokens = lens.repeat_interleave(hkv).contiguous()
+        # decode drift: the queries move along a closed loop, one point per step
+        # (n_path points, all precomputed in HBM), so selections change a little
+        # every step and the CPU share settles where recalls balance it
+        n_path = cfg.get("drift_points", 32)
+        radius = cfg.get("drift", 0.0)
+        q0 = torch.randn(L, U * G, D, generator=g, device=dev)
+        du = torch.randn(L, U * G, D, generator=g, device=dev)
+        dv = torch.randn(L, U * G, D, generator=g, device=dev)
+        noise = torch.randn(L, U * G, D, generator=g, device=dev)
+        self.q_path_t, self.q_path_p = [], []
+        for j in range(n_path if radius > 0 else 1):
+            th = 2 * math.pi * j / n_path
+            qt = q0 + radius * (math.cos(th) * du + math.sin(th) * dv)
+            qp = qt + 0.33 * noise
+            qp = qp * (qt.norm(dim=-1, keepdim=True) / qp.norm(dim=-1, keepdim=True))
+            self.q_path_t.append(qt.to(cfg["q_dtype"]))
+            self.q_path_p.append(qp.to(cfg["q_dtype"]))
+        self.q_true, self.q_pred = self.q_path_t[0], self.q_path_p[0]
+        self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev)
+        m = torch.randn(L, U * G, generator=g, device=dev)
+        l = torch.rand(L, U * G, generator=g, device=dev) * 40 + 1
+        self.cpu_ml = torch.stack([m, l], dim=-1).contiguous()
+        self.k_new = torch.randn(L, U, D, generator=g, device=dev)
+        self.v_new = torch.randn(L, U, D, generator=g, device=dev)
+        self.out_o = torch.empty(L, U * G, D, device=dev)
+        self.out_ml = torch.empty(L, U * G, 2, device=dev)
+        self.host_blocks = 8192
+        sb = ops.slot_bytes(kv_dt)
+        self.host_tier = torch.empty(self.host_blocks * sb, dtype=torch.uint8).pin_memory()
+        self.host_tier.view(torch.bfloat16).normal_(generator=gcpu)
+        cpu_per_unit = int(round(cfg["cpu_frac"] * k))
+        layers = []
+        for li in range(L):
+            a = torch.randn(U, D, nbs, generator=g, device=dev).to(kv_dt)
+            b = torch.randn(U, D, nbs, generator=g, device=dev).to(kv_dt)
+            dig = torch.stack([torch.minimum(a, b), torch.maximum(a, b)], dim=1).contiguous()
+            dig[..., nb:] = 0  # blocks still to be appended
+            del a, b
+            base = self.tier.layer_base[li] + torch.arange(U, device=dev, dtype=torch.int32)[:, None] * spu[li]
+            ids = torch.arange(nbs, device=dev, dtype=torch.int32)[None]
+            if li == 0:  # pinned: every block resident
+                table = torch.where(ids < nb, base + ids, -1)
+            else:
+                r = ops.score_topk_split(self.q_pred[li], dig, self.n_tokens, k, G)
+                sel = r["sel_ids"][:, :k].long()
+                score = torch.rand(U, nbs, generator=g, device=dev)
+                score[:, nb:] = -1
+                score.scatter_(1, sel, 2.0)
+                drop = torch.rand(U, k, generator=g, device=dev).argsort(dim=1)[:, :cpu_per_unit]
+                score.scatter_(1, torch.gather(sel, 1, drop), -0.5)
+                score[self.n_tokens % BS != 0, nb - 1] = 3.0  # an open block is always fast (kv_store.hpp:60-63)
+                keep = score.argsort(dim=1, descending=True)[:, :cap]
+                table = torch.full((U, nbs), -1, dtype=torch.int32, device=dev)
+                table.scatter_(1, keep, (base + torch.arange(cap, device=dev, dtype=torch.int32)[None]).to(torch.int32))
+            self.tier.adopt(li, table.contiguous(), self.n_tokens)
+            layers.append(LayerState(dig, torch.full((U, nbs), -1, dtype=torch.int32, device=dev)))
+        self.layer_states = layers
+        self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=self.pool,
+                                   kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
+                                   recall_interval=cfg["recall"], host_tier=self.host_tier, q_dtype=cfg["q_dtype"],
+                                   tier=self.tier, host_blocks=self.host_blocks, host_staging=True)
+        self.cpu_per_unit = cpu_per_unit
+        self.digest_bytes_layer = U * 2 * D * nb * 2
+
+    def step(self, s):
+        j = s % len(self.q_path_t)
+        self.engine.decode_step_kv(s, self.q_path_t[j], self.q_path_p[j], self.cpu_o, self.cpu_ml, self.k_new,
+                                   self.v_new, self.out_o, self.out_ml)
+
+    def k2_bytes(self, res_tokens_total):
+        UG = self.U * self.G
+        return res_tokens_total * 2 * D * 2 + UG * (D * 4 + (D + 2) * 4 + (D + 2) * 4)
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -334,11 +453,18 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline")
+    ap.add_argument("--tier", default="device", choices=["static", "device"],
+                    help="device (default): the full decode step -- append + digest refresh, device tier "
+                         "bookkeeping (LRU eviction, recall tickets), recalls (scout_engine_decode_step_kv); "
+                         "static: residency fixed at the paper's 8.2%% CPU share, no appends (kernel view)")
+    ap.add_argument("--drift", type=float, default=0.0,
+                    help="device tier mode: radius of the closed query path (0 = stationary queries)")
     ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
                     help="query dtype (q_true / q_pred); bf16 = the model's projection output")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     cfg["q_dtype"] = torch.bfloat16 if args.q_dtype == "bf16" else torch.float32
+    cfg["drift"] = args.drift
     if args.batch:
         cfg["batch"] = args.batch
     ws, rank, local = dist_setup()
@@ -358,7 +484,9 @@ def main():
 
     lib()  # native library must be present: no fallback
     t0 = time.time()
-    wl = Workload(cfg, dev, seed=1234 + rank)
+    tier_mode = args.tier == "device"
+    wl = (TierWorkload(cfg, dev, seed=1234 + rank, max_steps=args.warmup + args.steps + 8) if tier_mode
+          else Workload(cfg, dev, seed=1234 + rank))
     torch.cuda.synchronize(dev)
     log(f"workload ready in {time.time() - t0:.1f}s: pool {wl.pool.numel() / 2**30:.1f} GiB")
     eng = wl.engine
@@ -368,7 +496,7 @@ def main():
     torch.cuda.synchronize(dev)
     # resident token count per K2 launch (stationary across steps)
     res_tok_layers = []
-    for li in range(wl.L):
+    for li in range(0 if tier_mode else wl.L):
         st = wl.layer_states[li]
         q = wl.q_true[0] if li == 0 else wl.q_pred[li]
         from paper_2603_27138_b200 import ops
@@ -398,6 +526,15 @@ def main():
     ms = start.elapsed_time(end)
     ms = max_over_ranks(ms, ws, dev)
     k2_total, k2_n, launches = eng.stats()
+    tier_info = None
+    if tier_mode:  # the residency evolves: bytes from the last timed step's K1 lists
+        k1o = eng.k1_outputs()
+        res_tok_layers = [int(x) for x in k1o["res_tokens"].sum(1).tolist()]
+        cpu_tok = int(k1o["cpu_tokens"].sum())
+        tier_info = {"mode": "device (scout_engine_decode_step_kv)", "resident_token_frac_last_step":
+                     sum(res_tok_layers) / max(sum(res_tok_layers) + cpu_tok, 1),
+                     "tokens_at_end": int(wl.n_tokens[0]), "host_tier_blocks": wl.host_blocks,
+                     "note": "stationary queries: recalls pull the CPU share in, so residency grows over the run"}
     eng.set_timing(False)
     k2_ms = [k2_total / max(k2_n, 1)] * k2_n
     ms_step = ms / args.steps
@@ -431,7 +568,7 @@ def main():
     # ---- e2e through host buffers
     e2e = None
     if not args.profile:
-        e2e = run_e2e(wl, args.e2e_steps, dev, ws, global_batch)
+        e2e = run_e2e(wl, args.e2e_steps, dev, ws, global_batch, tier_mode)
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
@@ -466,6 +603,7 @@ def main():
             "clocks": clk,
             "gpu_launches": launches,
             "verify": {"rank_output_checksums": checksums} if checksums else None,
+            "tier": tier_info,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
@@ -473,7 +611,7 @@ def main():
     barrier(ws)
 
 
-def run_e2e(wl: Workload, steps, dev, ws, global_batch):
+def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False):
     """Same step through the C++ engine with pinned HOST inputs/outputs
     (scout_engine_decode_step_host): H2D of q_true / q_pred / CPU partials in
     layer chunks on a copy stream, D2H of the attention output and of each
@@ -490,29 +628,39 @@ def run_e2e(wl: Workload, steps, dev, ws, global_batch):
     h_cpu_ids = torch.empty(L, wl.U, wl.k, dtype=torch.int32).pin_memory()
     h_n_cpu = torch.empty(L, wl.U, dtype=torch.int32).pin_memory()
 
-    def one(s):
-        eng.decode_step_host(s, h_qt, h_qp, h_co, h_cm, h_out, h_oml, h_cpu_ids, h_n_cpu)
+    h_kv = [wl.k_new.cpu().pin_memory(), wl.v_new.cpu().pin_memory()] if tier_mode else []
 
+    def one(s):
+        if tier_mode:
+            eng.decode_step_kv_host(s, h_qt, h_qp, h_co, h_cm, *h_kv, h_out, h_oml, h_cpu_ids, h_n_cpu)
+        else:
+            eng.decode_step_host(s, h_qt, h_qp, h_co, h_cm, h_out, h_oml, h_cpu_ids, h_n_cpu)
+
+    s0 = 10000  # after the device-path steps: the tier clock keeps moving forward
     for s in range(3):
-        one(1000 + s)
+        one(s0 + s)
     eng.sync()
     torch.cuda.synchronize(dev)
     barrier(ws)
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for s in range(steps):
-        one(2000 + s)
+        one(s0 + 3 + s)
     eng.sync()
     b.record()
     torch.cuda.synchronize(dev)
     ms = max_over_ranks(a.elapsed_time(b), ws, dev) / steps
     # the host output must equal the device path's output for the same inputs
-    ok = bool(torch.allclose(h_out[L - 1], wl.out_o[L - 1].cpu(), rtol=0, atol=0))
-    h2d_bytes = sum(x.numel() * x.element_size() for x in (h_qt, h_qp, h_co, h_cm))
+    # static residency: the host output must equal the device path's for the same inputs
+    # (tier mode: residency moved on since the device-path run, so the check is the
+    # bit-exact host-vs-device test in tests/test_gpu_engine_tier.py instead)
+    ok = None if tier_mode else bool(torch.allclose(h_out[L - 1], wl.out_o[L - 1].cpu(), rtol=0, atol=0))
+    h2d_bytes = sum(x.numel() * x.element_size() for x in (h_qt, h_qp, h_co, h_cm, *h_kv))
     d2h_bytes = sum(x.numel() * x.element_size() for x in (h_out, h_oml, h_cpu_ids, h_n_cpu))
     return {"value": global_batch / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes, "matches_device_path": ok,
-            "path": "C ABI scout_engine_decode_step_host (csrc/engine.cpp), pinned host buffers"}
+            "path": "C ABI scout_engine_decode_step_%s (csrc/engine.cpp), pinned host buffers" %
+                    ("kv_host" if tier_mode else "host")}
 
 
 if __name__ == "__main__":

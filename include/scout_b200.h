@@ -398,6 +398,12 @@ int scout_engine_decode_step_host(scout_engine* eng, int step, const void* h_q_t
 int scout_engine_decode_step_kv(scout_engine* eng, int step, const void* q_true, const void* q_pred,
                                 const float* cpu_o, const float* cpu_ml, const float* k_new, const float* v_new,
                                 float* out_o, float* out_ml, void* stream);
+/* Device tier mode from pinned HOST buffers (the pipeline of
+ * scout_engine_decode_step_host plus h_k_new / h_v_new [L][U][128] f32). */
+int scout_engine_decode_step_kv_host(scout_engine* eng, int step, const void* h_q_true, const void* h_q_pred,
+                                     const float* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
+                                     const float* h_v_new, float* h_out_o, float* h_out_ml, int32_t* h_cpu_ids,
+                                     int32_t* h_n_cpu, void* stream);
 /* Order all outstanding side-stream work (recalls) before `stream`. */
 int scout_engine_sync(scout_engine* eng, void* stream);
 /* Instrumentation: when enabled, CUDA events bracket every K2 launch (on the

@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -36,6 +37,7 @@
 #include "../../include/scout_b200.h"
 #include "k1_batch.h"
 #include "k2_step.h"
+#include "k5_batch.h"
 
 namespace scout_host {
 void set_error(int code, const char* fmt, ...);
@@ -143,9 +145,11 @@ struct scout_engine {
     Buf plan_tab;                  // [L][U][nbs] residency planning view (K1's block tables)
     Buf open_slot, sealed_id;      // [L][U] append bookkeeping
     Buf tier_dst;                  // [L][U][k] recall destination slots
+    Buf tier_dev;                  // [L] scout_tier_layer (device copy for the multi-layer launches)
+    uint8_t* host_dev = nullptr;   // device view of the pinned host tier
     std::vector<int> pending;      // per layer: ready tick of its in-flight recall ticket, -1 none
     int n_tickets = 0;
-    cudaEvent_t ev_side_end = nullptr;
+    cudaEvent_t ev_side_end = nullptr, ev_kvin = nullptr;
     bool side_recorded = false;
     int tick(int step, int layer) const { return step * cfg.layers + layer; }
     // instrumentation
@@ -162,7 +166,7 @@ struct scout_engine {
         stop_recalls();
         for (cudaStream_t s : {k1s, side, h2d, d2h})
             if (s) cudaStreamDestroy(s);
-        for (cudaEvent_t e : {ev_start, ev_k1_end, ev_tmp, ev_k2[0], ev_k2[1], stage_free[0], stage_free[1], ev_side_end})
+        for (cudaEvent_t e : {ev_start, ev_k1_end, ev_tmp, ev_k2[0], ev_k2[1], stage_free[0], stage_free[1], ev_side_end, ev_kvin})
             if (e) cudaEventDestroy(e);
         for (auto e : ev_k1) cudaEventDestroy(e);
         for (auto e : chunk_ev) cudaEventDestroy(e);
@@ -335,6 +339,73 @@ struct scout_engine {
         rc_thread.join();
     }
 
+    // ------------------------------------------------------- device tier mode
+    // 1. residency planning view of every layer at this step (residency_set at
+    //    (step, i-1) == at step start: the step's later ops touch other layers);
+    // 2. select + split + mark_selected for every layer (one launch);
+    // 3. begin_layer: tickets due at (step, i), applied after the marks
+    int tier_pre(int step, int par, const void* q_true, const void* q_pred, cudaStream_t s) {
+        const int L = cfg.layers, nbs = cfg.nb_stride;
+        int rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(tier_dev.p), L, U, nbs, cfg.n_tokens, step,
+                                        I(plan_tab), s);
+        if (rc != SCOUT_OK) return rc;
+        if ((rc = select_batch(0, L, q_true, q_pred, step, par, s)) != SCOUT_OK) return rc;
+        for (int i = 0; i < L; ++i) {
+            if (pending[i] < 0 || pending[i] > tick(step, i)) continue;
+            if ((rc = scout_tier_apply(&tier[i], U, nbs, cfg.n_tokens, tick(step, i), nullptr, s)) != SCOUT_OK) return rc;
+            pending[i] = -1;
+        }
+        return SCOUT_OK;
+    }
+    // 5. after the attention, every layer in one launch: append the token
+    //    (open / seal + LRU eviction, write-through) and, when due, schedule the
+    //    recall of the layer's CPU-side selected blocks (maybe_schedule_recall,
+    //    recall.hpp:114-126); n_tokens advances;
+    // 6. the recall copies on the side stream; the next step's K2 waits for a
+    //    layer's flag before streaming it (visible at (m+1, i))
+    int tier_post(int step, int par, unsigned tok, const float* k_new, const float* v_new, cudaStream_t s) {
+        const int L = cfg.layers, nbs = cfg.nb_stride;
+        TierPostArgs pa{};
+        pa.layers = static_cast<const scout_tier_layer*>(tier_dev.p);
+        pa.n_layers = L;
+        pa.nbs = nbs;
+        pa.k = cfg.k;
+        pa.step = step;
+        pa.ticket_base = n_tickets;
+        n_tickets += L;
+        pa.n_tokens = cfg.n_tokens;
+        pa.pool = static_cast<uint8_t*>(cfg.kv_pool);
+        pa.k_new = k_new;
+        pa.v_new = v_new;
+        for (int i = 0; i < L; ++i) pa.digests[i] = const_cast<void*>(layers[i].digests);
+        pa.host_tier = host_dev;
+        pa.host_blocks = cfg.host_blocks;
+        pa.cpu_ids = I(cpu_ids[par]);
+        pa.n_cpu = I(n_cpu[par]);
+        pa.dst = I(tier_dst);
+        bool any_recall = false;
+        for (int i = 0; i < L; ++i) {
+            pa.recall_due[i] = cfg.recall_interval > 0 && (step + i) % cfg.recall_interval == 0;
+            any_recall |= pa.recall_due[i] != 0;
+        }
+        int rc = scout_tier_post_layers(pa, U, s);
+        if (rc != SCOUT_OK) return rc;
+        if (!any_recall) return SCOUT_OK;
+        CU(cudaEventRecord(ev_tmp, s));
+        CU(cudaStreamWaitEvent(side, ev_tmp, 0));
+        for (int i = 0; i < L; ++i) {
+            if (!pa.recall_due[i]) continue;
+            if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, static_cast<long long>(i) * U * nbs,
+                                              nbs, cfg.host_blocks, U, pa.cpu_ids + lk(i), pa.n_cpu + lu(i), pa.dst + lk(i),
+                                              cfg.k, 1, side)) != SCOUT_OK)
+                return rc;
+            if ((rc = write_value(side, recall_flag + i, tok)) != SCOUT_OK) return rc;
+            rc_token[i] = tok;
+            pending[i] = tick(step + 1, i);
+        }
+        return SCOUT_OK;
+    }
+
     // K1 lists of this parity were read by the K2 two steps back: wait for it;
     // inputs recorded on `st` before the step are visible to the K1 stream
     int begin_step(cudaStream_t st, int par) {
@@ -401,7 +472,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     if (!bad && c.host_staging) {
         // q_true | q_pred (q dtype) | cpu_o | cpu_ml | out_o | out_ml (f32)
         const size_t qb = c.q_dtype == SCOUT_BF16 ? 2 : 4;
-        const size_t per = static_cast<size_t>(c.layers) * e->UG * (2 * SCOUT_HEAD_DIM * qb + (2 * SCOUT_HEAD_DIM + 4) * 4);
+        size_t per = static_cast<size_t>(c.layers) * e->UG * (2 * SCOUT_HEAD_DIM * qb + (2 * SCOUT_HEAD_DIM + 4) * 4);
+        if (c.tier) per += static_cast<size_t>(c.layers) * e->U * SCOUT_HEAD_DIM * 4 * 2;  // k_new | v_new (device tier mode)
         bad |= e->stage[0].alloc(per) | e->stage[1].alloc(per);
     }
     if (bad) {
@@ -445,12 +517,26 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         e->tier.assign(c.tier, c.tier + c.layers);
         const size_t lu = static_cast<size_t>(c.layers) * e->U;
         if (e->plan_tab.alloc(lu * c.nb_stride * 4) || e->open_slot.alloc(lu * 4) || e->sealed_id.alloc(lu * 4) ||
-            e->tier_dst.alloc(lu * c.k * 4) || cudaEventCreateWithFlags(&e->ev_side_end, cudaEventDisableTiming)) {
+            e->tier_dst.alloc(lu * c.k * 4) || cudaEventCreateWithFlags(&e->ev_side_end, cudaEventDisableTiming) ||
+            cudaEventCreateWithFlags(&e->ev_kvin, cudaEventDisableTiming)) {
             delete e;
             set_error(SCOUT_ERR_CUDA, "scout_engine_create: tier-mode allocation failed");
             return SCOUT_ERR_CUDA;
         }
         e->pending.assign(c.layers, -1);
+        if (c.layers > K5_MAX_LAYERS || e->tier_dev.alloc(sizeof(scout_tier_layer) * c.layers) ||
+            cudaMemcpy(e->tier_dev.p, c.tier, sizeof(scout_tier_layer) * c.layers, cudaMemcpyHostToDevice) != cudaSuccess) {
+            delete e;
+            set_error(SCOUT_ERR_CUDA, "scout_engine_create: tier descriptors (layers <= %d)", K5_MAX_LAYERS);
+            return SCOUT_ERR_CUDA;
+        }
+        void* hv = nullptr;
+        if (cudaHostGetDevicePointer(&hv, const_cast<void*>(c.host_tier), 0) != cudaSuccess || !hv) {
+            delete e;
+            set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: host_tier must be pinned, device-mapped memory");
+            return SCOUT_ERR_INVALID_ARGUMENT;
+        }
+        e->host_dev = static_cast<uint8_t*>(hv);
     }
     cudaGetDevice(&e->device);
     if (c.recall_interval > 0 && !c.tier) e->rc_thread = std::thread([e] { e->recall_loop(); });
@@ -509,9 +595,38 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q
     return e->issue_recalls(step);
 }
 
+static int host_step(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred, const float* h_cpu_o,
+                     const float* h_cpu_ml, const float* h_k_new, const float* h_v_new, float* h_out_o, float* h_out_ml,
+                     int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream);
+
 extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred,
                                              const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o,
                                              float* h_out_ml, int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream) {
+    if (e && e->tier_mode) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT,
+                              "scout_engine_decode_step_host: device tier engine: use scout_engine_decode_step_kv_host");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    return host_step(e, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, nullptr, nullptr, h_out_o, h_out_ml, h_cpu_ids,
+                     h_n_cpu, stream);
+}
+
+extern "C" int scout_engine_decode_step_kv_host(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred,
+                                                const float* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
+                                                const float* h_v_new, float* h_out_o, float* h_out_ml,
+                                                int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream) {
+    if (!e || !e->tier_mode || !h_k_new || !h_v_new) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT,
+                              "scout_engine_decode_step_kv_host: needs a device tier engine and the new K/V rows");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    return host_step(e, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, h_k_new, h_v_new, h_out_o, h_out_ml, h_cpu_ids,
+                     h_n_cpu, stream);
+}
+
+static int host_step(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred, const float* h_cpu_o,
+                     const float* h_cpu_ml, const float* h_k_new, const float* h_v_new, float* h_out_o, float* h_out_ml,
+                     int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream) {
     if (!e || !e->stage[0].p || !h_q_true || !h_q_pred || !h_out_o || !h_out_ml ||
         ((h_cpu_o == nullptr) != (h_cpu_ml == nullptr))) {
         scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT,
@@ -530,6 +645,9 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const vo
     float* d_cm = d_co + L * qd;
     float* d_o = d_cm + L * md;
     float* d_oml = d_o + L * qd;
+    float* d_kn = d_oml + L * md;  // device tier mode: the token's K/V rows
+    float* d_vn = d_kn + static_cast<size_t>(L) * e->U * SCOUT_HEAD_DIM;
+    const size_t kvn = static_cast<size_t>(L) * e->U * SCOUT_HEAD_DIM * 4;
     const uint8_t* hq_t = static_cast<const uint8_t*>(h_q_true);
     const uint8_t* hq_p = static_cast<const uint8_t*>(h_q_pred);
     int rc = e->begin_step(st, par);
@@ -556,11 +674,19 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const vo
         }
         if ((rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
     }
+    if (e->tier_mode) {  // the token's K/V, needed after the attention
+        CU(cudaMemcpyAsync(d_kn, h_k_new, kvn, cudaMemcpyHostToDevice, e->h2d));
+        CU(cudaMemcpyAsync(d_vn, h_v_new, kvn, cudaMemcpyHostToDevice, e->h2d));
+        CU(cudaEventRecord(e->ev_kvin, e->h2d));
+    }
     // ---- K1 for every layer in one launch once q_pred landed (in steady state
     // it was copied while the previous step's K2 ran); the CPU-side ids then
-    // go out to the host worker
+    // go out to the host worker. Device tier mode: planning view + K1 + ticket
+    // application (the previous step's bookkeeping is ordered by ev_start)
     CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[0], 0));
-    if ((rc = e->select_batch(0, L, d_qt, d_qp, step, par, e->k1s)) != SCOUT_OK) return rc;
+    if (e->tier_mode) rc = e->tier_pre(step, par, d_qt, d_qp, e->k1s);
+    else rc = e->select_batch(0, L, d_qt, d_qp, step, par, e->k1s);
+    if (rc != SCOUT_OK) return rc;
     if (h_cpu_ids) {
         CU(cudaEventRecord(e->ev_k1[0], e->k1s));
         CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[0], 0));
@@ -588,7 +714,12 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const vo
     if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), false, st)) !=
         SCOUT_OK)
         return rc;
-    if ((rc = e->issue_recalls(step)) != SCOUT_OK) return rc;
+    if (e->tier_mode) {
+        CU(cudaStreamWaitEvent(st, e->ev_kvin, 0));
+        if ((rc = e->tier_post(step, par, token, d_kn, d_vn, st)) != SCOUT_OK) return rc;
+    } else if ((rc = e->issue_recalls(step)) != SCOUT_OK) {
+        return rc;
+    }
     // ---- outputs: OUT_CH layers at a time, each group leaving once every CTA
     // finished its last layer (a short tail after K2 ends)
     constexpr int OUT_CH = 4;
@@ -617,28 +748,20 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     auto st = static_cast<cudaStream_t>(stream);
-    const int L = e->cfg.layers, U = e->U, nbs = e->cfg.nb_stride, k = e->cfg.k;
+    const int L = e->cfg.layers;
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
     const unsigned token = ++e->token;
     const int par = token & 1;
     int rc;
-    // the previous step's appends / recalls (tier state, digests, n_tokens) first
-    if (e->side_recorded) CU(cudaStreamWaitEvent(st, e->ev_side_end, 0));
-    // 1. residency planning view of every layer at this step (residency_set at
-    //    (step, i-1) == at step start: later ops of the step touch other layers)
-    for (int i = 0; i < L; ++i)
-        if ((rc = scout_tier_plan(&e->tier[i], U, nbs, e->cfg.n_tokens, e->tick(step, i),
-                                  e->I(e->plan_tab) + static_cast<size_t>(i) * U * nbs, st)) != SCOUT_OK)
-            return rc;
-    // 2. select + split + mark_selected for every layer (one launch)
-    if ((rc = e->select_batch(0, L, q_true, q_pred, step, par, st)) != SCOUT_OK) return rc;
-    // 3. begin_layer: tickets due at (step, i), applied after the marks
-    for (int i = 0; i < L; ++i) {
-        if (e->pending[i] < 0 || e->pending[i] > e->tick(step, i)) continue;
-        if ((rc = scout_tier_apply(&e->tier[i], U, nbs, e->cfg.n_tokens, e->tick(step, i), nullptr, st)) != SCOUT_OK)
-            return rc;
-        e->pending[i] = -1;
-    }
+    // debug: SCOUT_ENGINE_PHASES=1 prints per-phase device times (synchronises)
+    static const bool phases = getenv("SCOUT_ENGINE_PHASES") != nullptr;
+    cudaEvent_t pe[4] = {};
+    if (phases)
+        for (auto& ev : pe) cudaEventCreate(&ev);
+    if (phases) cudaEventRecord(pe[0], st);
+    // 1-3. planning view, select + split + mark, begin_layer's ticket application
+    if ((rc = e->tier_pre(step, par, q_true, q_pred, st)) != SCOUT_OK) return rc;
+    if (phases) cudaEventRecord(pe[1], st);
     // 4. attention + merge over all layers (one persistent launch)
     std::vector<const void*> q(L);
     std::vector<const float*> co(L), cml(L);
@@ -652,44 +775,17 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
     }
     if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, false, st)) != SCOUT_OK)
         return rc;
-    // 5. per layer, once every CTA finished it: append the token (open / seal,
-    //    LRU eviction, write-through) and, when due, recall the layer's
-    //    CPU-side selected blocks (maybe_schedule_recall, recall.hpp:114-126)
-    CU(cudaEventRecord(e->ev_tmp, st));
-    CU(cudaStreamWaitEvent(e->side, e->ev_tmp, 0));
-    const size_t sb = scout_slot_bytes(e->cfg.kv_dtype);
-    (void)sb;
-    for (int i = 0; i < L; ++i) {
-        if ((rc = wait_value(e->side, e->layer_done + i, token * static_cast<unsigned>(e->grid))) != SCOUT_OK) return rc;
-        int32_t* os = e->I(e->open_slot) + static_cast<size_t>(i) * U;
-        int32_t* sid = e->I(e->sealed_id) + static_cast<size_t>(i) * U;
-        const long long hbase = static_cast<long long>(i) * U * nbs;
-        if ((rc = scout_tier_append(&e->tier[i], U, nbs, e->cfg.n_tokens, step, os, sid, e->side)) != SCOUT_OK) return rc;
-        if ((rc = scout_kv_append(e->cfg.kv_pool, e->cfg.kv_dtype, SCOUT_DIGEST_MINMAX, U, os, const_cast<int32_t*>(e->cfg.n_tokens),
-                                  k_new + static_cast<size_t>(i) * U * SCOUT_HEAD_DIM,
-                                  v_new + static_cast<size_t>(i) * U * SCOUT_HEAD_DIM,
-                                  const_cast<void*>(e->layers[i].digests), nbs, i == L - 1, e->side)) != SCOUT_OK)
-            return rc;
-        if ((rc = scout_kv_writeback(e->cfg.kv_pool, e->cfg.kv_dtype, const_cast<void*>(e->cfg.host_tier), hbase, nbs,
-                                     e->cfg.host_blocks, U, os, sid, e->side)) != SCOUT_OK)
-            return rc;
-        if (e->cfg.recall_interval > 0 && (step + i) % e->cfg.recall_interval == 0) {
-            const int32_t* ids = e->I(e->cpu_ids[par]) + e->lk(i);
-            const int32_t* nids = e->I(e->n_cpu[par]) + e->lu(i);
-            int32_t* dst = e->I(e->tier_dst) + e->lk(i);
-            if ((rc = scout_tier_schedule_recall(&e->tier[i], U, nbs, e->cfg.n_tokens, ids, nids, k,
-                                                 e->tick(step + 1, i), e->n_tickets++, dst, e->side)) != SCOUT_OK)
-                return rc;
-            if ((rc = scout_recall_gather_ids(e->cfg.kv_pool, e->cfg.kv_dtype, e->cfg.host_tier, hbase, nbs,
-                                              e->cfg.host_blocks, U, ids, nids, dst, k, 1, e->side)) != SCOUT_OK)
-                return rc;
-            if ((rc = write_value(e->side, e->recall_flag + i, token)) != SCOUT_OK) return rc;
-            e->rc_token[i] = token;  // the next step's K2 waits for it before streaming layer i
-            e->pending[i] = e->tick(step + 1, i);
-        }
+    if (phases) cudaEventRecord(pe[2], st);
+    // 5-6. append + write-through + recall scheduling, then the recall copies
+    if ((rc = e->tier_post(step, par, token, k_new, v_new, st)) != SCOUT_OK) return rc;
+    if (phases) {
+        cudaEventRecord(pe[3], e->side);
+        cudaEventSynchronize(pe[3]);
+        float t[3];
+        for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], pe[i], pe[i + 1]);
+        fprintf(stderr, "step %d: plan+K1+apply %.3f K2 %.3f post+recalls %.3f ms\n", step, t[0], t[1], t[2]);
+        for (auto& ev : pe) cudaEventDestroy(ev);
     }
-    CU(cudaEventRecord(e->ev_side_end, e->side));
-    e->side_recorded = true;
     return SCOUT_OK;
 }
 

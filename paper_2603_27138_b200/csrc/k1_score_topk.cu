@@ -337,9 +337,9 @@ __device__ __forceinline__ void fast_quad(const DigT* blo, const DigT* bhi, int 
 }
 
 // QPT: block quads per thread whose running scores live in registers (1: up
-// to 512 blocks, 4: up to 2048); 0: shared-memory accumulators (any size).
+// to 512 blocks, 2: up to 1024, 4: up to 2048); 0: shared-memory accumulators.
 template <typename DigT, int G, int MODE, int QPT>
-__global__ void __launch_bounds__(K1_THREADS, SCOUT_K1_MINB) score_topk_kernel(const K1Batch batch) {
+__global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT_K1_MINB) score_topk_kernel(const K1Batch batch) {
     const scout_topk_args& a = batch.a[blockIdx.y];  // layer of this CTA (one launch can cover many)
     extern __shared__ __align__(16) uint8_t k1_smem[];
     const size_t ns = static_cast<size_t>(a.nb_stride);
@@ -659,12 +659,14 @@ int launch_g(K1Batch& b, cudaStream_t st) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
         scout_host::launch(kern, dim3(a.n_units, b.n), dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
     };
-    const int qpt = MODE != 0 ? 1 : (a.nb_stride <= 4 * K1_THREADS ? 1 : (a.nb_stride <= K1_REG_BLOCKS ? 4 : 0));
+    const int ns = a.nb_stride;
+    const int qpt = MODE != 0 ? 1 : (ns <= 4 * K1_THREADS ? 1 : (ns <= 8 * K1_THREADS ? 2 : (ns <= K1_REG_BLOCKS ? 4 : 0)));
     auto pick = [&](auto g) {
         constexpr int Gv = decltype(g)::value;
         if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1>);
         else if constexpr (MODE == 0) {
-            if (qpt == 4) go(score_topk_kernel<DigT, Gv, MODE, 4>);
+            if (qpt == 2) go(score_topk_kernel<DigT, Gv, MODE, 2>);
+            else if (qpt == 4) go(score_topk_kernel<DigT, Gv, MODE, 4>);
             else go(score_topk_kernel<DigT, Gv, MODE, 0>);
         }
     };

@@ -1,0 +1,29 @@
+// Internal (engine <-> K5) multi-layer launches of the device tier mode. Not
+// part of the public C ABI: the engine drives them for a whole decode step.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/scout_b200.h"
+
+constexpr int K5_MAX_LAYERS = 96;
+
+struct TierPostArgs {
+    const scout_tier_layer* layers;  // device array [n_layers]
+    int n_layers, nbs, k, step, ticket_base;
+    const int32_t* n_tokens;         // count before the append (advanced after the launch)
+    uint8_t* pool;                   // bf16 KV pool
+    const float* k_new;              // [L][U][128]
+    const float* v_new;
+    void* digests[K5_MAX_LAYERS];    // per layer [U][2][128][nbs] bf16
+    uint8_t* host_tier;              // device view of the pinned host tier (nullptr: no write-through)
+    long long host_blocks;
+    const int32_t* cpu_ids;          // [L][U][k] K1's CPU-side ids of this step
+    const int32_t* n_cpu;            // [L][U]
+    int32_t* dst;                    // [L][U][k] recall destination slots
+    uint8_t recall_due[K5_MAX_LAYERS];
+};
+
+int scout_tier_plan_layers(const scout_tier_layer* layers_dev, int n_layers, int n_units, int nb_stride,
+                           const int32_t* n_tokens, int step, int32_t* tables, cudaStream_t st);
+int scout_tier_post_layers(const TierPostArgs& a, int n_units, cudaStream_t st);

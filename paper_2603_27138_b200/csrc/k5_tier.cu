@@ -421,3 +421,167 @@ extern "C" int scout_tier_mark(const scout_tier_layer* L, int n_units, int nb_st
     tier_mark_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, ids, n_ids, k_stride, step);
     return scout_host::check_launch("scout_tier_mark");
 }
+
+// ===========================================================================
+// Engine-internal multi-layer launches (device tier mode, k5_batch.h): the
+// per-layer bookkeeping of a whole decode step in two launches instead of
+// ~4 per layer (tiny kernels cost ~10 us each behind the persistent K2).
+#include "k5_batch.h"
+
+namespace {
+
+// residency_set of every layer (grid units x layers): next run of layer l at step = tick(step, l)
+__global__ void __launch_bounds__(TT) tier_plan_layers_kernel(const scout_tier_layer* Ls, int nbs,
+                                                              const int32_t* n_tokens, int step, int n_layers,
+                                                              int32_t* tables) {
+    const int u = blockIdx.x, l = blockIdx.y;
+    const scout_tier_layer& L = Ls[l];
+    const size_t o = static_cast<size_t>(u) * nbs;
+    const int nb = min(n_blocks_of(n_tokens[u]), nbs);
+    const int next_tick = step * n_layers + l;
+    int32_t* out = tables + static_cast<size_t>(l) * gridDim.x * nbs + o;
+    for (int b = threadIdx.x; b < nbs; b += TT) {
+        int v = -1;
+        if (b < nb) {
+            const int r = L.ready[o + b];
+            if (L.tier[o + b] || (r >= 0 && r <= next_tick)) v = L.table[o + b];
+        }
+        out[b] = v;
+    }
+}
+
+// After the step's attention, per (unit, layer): append the token (open /
+// seal + enforce_capacity, row write, digest fold), write a sealed block
+// through to the host tier, and when the layer is due, schedule the recall of
+// K1's CPU-side ids (validation, slot assignment). n_tokens is read as the
+// count before the append; the caller advances it afterwards.
+__global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs a) {
+    __shared__ TierSm S;
+    __shared__ int s_slot, s_sealed;
+    const int u = blockIdx.x, l = blockIdx.y, c = threadIdx.x;
+    const scout_tier_layer& L = a.layers[l];
+    Unit U = unit_of(L, u, a.nbs);
+    const int pos = a.n_tokens[u];
+    const int id = pos / BS, r = pos % BS;
+    // ---- append bookkeeping (tier_append_kernel's logic)
+    if (c == 0) {
+        S.err = 0;
+        if (id >= a.nbs) {
+            set_err(U, SCOUT_ERR_INVALID_ARGUMENT);
+            S.err = 1;
+        } else if (r == 0) {
+            const int n = *U.n_free;
+            if (n <= 0) {
+                set_err(U, SCOUT_ERR_LOGIC);
+                S.err = 1;
+            } else {
+                U.table[id] = U.free_slots[n - 1];
+                *U.n_free = n - 1;
+                U.tier[id] = 1;
+                U.ready[id] = -1;
+                U.last_sel[id] = a.step;
+            }
+        }
+        s_slot = S.err ? -1 : U.table[id];
+        s_sealed = (!S.err && (pos + 1) % BS == 0) ? id : -1;
+    }
+    __syncthreads();
+    const int slot = s_slot, sealed_blk = s_sealed;
+    if (slot >= 0) {
+        // ---- row write + digest fold (scout_kv_append, bf16 KV, minmax)
+        __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(a.pool + static_cast<size_t>(slot) * BF16_SLOT_BYTES);
+        const int off = bf16_tile_offset(r, c);
+        const size_t row = (static_cast<size_t>(l) * gridDim.x + u) * D + c;
+        const __nv_bfloat16 kq = __float2bfloat16_rn(a.k_new[row]);
+        base[off] = kq;
+        base[BS * D + off] = __float2bfloat16_rn(a.v_new[row]);
+        __nv_bfloat16* dig = static_cast<__nv_bfloat16*>(a.digests[l]) + static_cast<size_t>(u) * 2 * D * a.nbs;
+        __nv_bfloat16& lo = dig[static_cast<size_t>(c) * a.nbs + id];
+        __nv_bfloat16& hi = dig[static_cast<size_t>(D + c) * a.nbs + id];
+        const float v = __bfloat162float(kq);
+        if (r == 0) {
+            lo = kq;
+            hi = kq;
+        } else {  // std::min / std::max fold (digest.hpp:45-46)
+            const float lf = __bfloat162float(lo), hf = __bfloat162float(hi);
+            if (v < lf) lo = kq;
+            if (hf < v) hi = kq;
+        }
+    }
+    if (sealed_blk >= 0) {
+        // ---- seal: mark, write-through of the block image, enforce capacity
+        __syncthreads();  // the row just written belongs to the image
+        if (c == 0) U.last_sel[sealed_blk] = a.step;
+        if (a.host_tier) {
+            long long hi = (static_cast<long long>(l) * gridDim.x + u) * a.nbs + sealed_blk;
+            if (a.host_blocks > 0) hi %= a.host_blocks;
+            const int4* src = reinterpret_cast<const int4*>(a.pool + static_cast<size_t>(slot) * BF16_SLOT_BYTES);
+            int4* dst = reinterpret_cast<int4*>(a.host_tier + static_cast<size_t>(hi) * BF16_SLOT_BYTES);
+            for (int i = c; i < static_cast<int>(BF16_SLOT_BYTES / 16); i += TT) dst[i] = __ldcg(src + i);
+        }
+        __syncthreads();
+        enforce_capacity(L, U, id + 1, pos + 1, S);
+    }
+    // ---- recall of the layer's CPU-side selected blocks (tier_recall_kernel's logic)
+    if (!a.recall_due[l]) return;
+    const int n = a.n_cpu[static_cast<size_t>(l) * gridDim.x + u];
+    if (n <= 0) return;
+    const int ntok = pos + 1;  // after this step's append
+    const int nb = min(n_blocks_of(ntok), a.nbs);
+    const int32_t* my = a.cpu_ids + (static_cast<size_t>(l) * gridDim.x + u) * a.k;
+    int32_t* dst = a.dst + (static_cast<size_t>(l) * gridDim.x + u) * a.k;
+    int bad = 0;
+    for (int i = c; i < n; i += TT) {
+        const int b = my[i];
+        if (b < 0 || b >= nb || !sealed(b, ntok) || U.tier[b] || U.ready[b] >= 0 || (i > 0 && my[i - 1] >= b)) bad = 1;
+    }
+    bad = block_sum(bad, S);
+    if (c == 0) {
+        S.err = 0;
+        if (bad) {
+            set_err(U, SCOUT_ERR_INVALID_ARGUMENT);
+            S.err = 1;
+        } else if (*U.n_free < n) {
+            set_err(U, SCOUT_ERR_LOGIC);
+            S.err = 1;
+        } else {
+            S.n_free = *U.n_free;
+            *U.n_free = S.n_free - n;
+        }
+    }
+    __syncthreads();
+    for (int i = c; i < n; i += TT) {
+        if (S.err) {
+            dst[i] = -1;
+            continue;
+        }
+        const int b = my[i];
+        const int s2 = U.free_slots[S.n_free - 1 - i];
+        U.table[b] = s2;
+        U.ready[b] = (a.step + 1) * a.n_layers + l;
+        U.ticket[b] = a.ticket_base + l;
+        dst[i] = s2;
+    }
+}
+
+__global__ void advance_tokens_kernel(int32_t* n_tokens, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) n_tokens[i] += 1;
+}
+
+}  // namespace
+
+int scout_tier_plan_layers(const scout_tier_layer* layers_dev, int n_layers, int n_units, int nb_stride,
+                           const int32_t* n_tokens, int step, int32_t* tables, cudaStream_t st) {
+    tier_plan_layers_kernel<<<dim3(n_units, n_layers), TT, 0, st>>>(layers_dev, nb_stride, n_tokens, step, n_layers,
+                                                                    tables);
+    return scout_host::check_launch("tier plan (all layers)");
+}
+
+int scout_tier_post_layers(const TierPostArgs& a, int n_units, cudaStream_t st) {
+    tier_post_layers_kernel<<<dim3(n_units, a.n_layers), TT, 0, st>>>(a);
+    int rc = scout_host::check_launch("tier post-attention (all layers)");
+    if (rc != SCOUT_OK) return rc;
+    advance_tokens_kernel<<<(n_units + 255) / 256, 256, 0, st>>>(const_cast<int32_t*>(a.n_tokens), n_units);
+    return scout_host::check_launch("advance n_tokens");
+}

@@ -88,6 +88,13 @@ class DecodeEngine:
         A.check(A.lib().scout_engine_decode_step_kv(self._h, int(step), _p(q_true), _p(q_pred), _p(cpu_o), _p(cpu_ml),
                                                     _p(k_new), _p(v_new), _p(out_o), _p(out_ml), self._stream()))
 
+    def decode_step_kv_host(self, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, h_k_new, h_v_new, h_out_o, h_out_ml,
+                            h_cpu_ids=None, h_n_cpu=None):
+        """Device tier mode from pinned host tensors (+ the token's K/V rows)."""
+        A.check(A.lib().scout_engine_decode_step_kv_host(self._h, int(step), _p(h_q_true), _p(h_q_pred), _p(h_cpu_o),
+                                                         _p(h_cpu_ml), _p(h_k_new), _p(h_v_new), _p(h_out_o),
+                                                         _p(h_out_ml), _p(h_cpu_ids), _p(h_n_cpu), self._stream()))
+
     def decode_step_host(self, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, h_out_o, h_out_ml, h_cpu_ids=None,
                          h_n_cpu=None):
         """Pinned host tensors, same layouts; h_cpu_ids [L][U][k], h_n_cpu [L][U] int32."""

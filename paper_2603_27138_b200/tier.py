@@ -23,10 +23,15 @@ BS = A.BLOCK_SIZE
 
 
 class DeviceTieredCache:
-    def __init__(self, layers: int, n_units: int, nb_stride: int, capacity: int, slots_per_unit: int,
+    def __init__(self, layers: int, n_units: int, nb_stride: int, capacity: int, slots_per_unit,
                  device="cuda", slot_base: int = 0):
+        """slots_per_unit: pool slots each (layer, unit) owns, an int or one per
+        layer (a pinned layer needs every block, the others capacity plus
+        room for in-flight recalls and the open block)."""
         self.L, self.U, self.nbs = layers, n_units, nb_stride
-        self.spu = slots_per_unit
+        spu = [int(slots_per_unit)] * layers if isinstance(slots_per_unit, int) else [int(x) for x in slots_per_unit]
+        self.spu_l = spu
+        self.spu = max(spu)
         self.dev = torch.device(device)
         dev, U, nbs = self.dev, n_units, nb_stride
         i32 = dict(dtype=torch.int32, device=dev)
@@ -35,10 +40,14 @@ class DeviceTieredCache:
         self.last_sel = torch.zeros((layers, U, nbs), **i32)
         self.ready = torch.full((layers, U, nbs), -1, **i32)
         self.ticket = torch.zeros((layers, U, nbs), **i32)
-        # layer l, unit u owns pool slots slot_base + (l*U + u)*spu + [0, spu); stack top = lowest slot
-        base = slot_base + torch.arange(layers * U, **i32).view(layers, U, 1) * slots_per_unit
-        self.free_slots = (base + torch.arange(slots_per_unit - 1, -1, -1, **i32).view(1, 1, -1)).contiguous()
-        self.n_free = torch.full((layers, U), slots_per_unit, **i32)
+        # layer l, unit u owns pool slots layer_base[l] + u*spu[l] + [0, spu[l]); stack top = lowest slot
+        self.layer_base = [slot_base + U * sum(spu[:l]) for l in range(layers)]
+        self.free_slots = torch.zeros((layers, U, self.spu), **i32)
+        for l in range(layers):
+            base = self.layer_base[l] + torch.arange(U, **i32).view(U, 1) * spu[l]
+            self.free_slots[l, :, :spu[l]] = base + torch.arange(spu[l] - 1, -1, -1, **i32).view(1, -1)
+        self.n_free = torch.tensor(spu, **i32).view(layers, 1).repeat(1, U).contiguous()
+        self.n_slots = U * sum(spu)
         self.err = torch.zeros((layers, U), **i32)
         self.n_tokens = torch.zeros((layers, U), **i32)
         self.capacity = [capacity] * layers
@@ -55,7 +64,7 @@ class DeviceTieredCache:
         for name in ("table", "tier", "last_sel", "ready", "ticket", "free_slots", "n_free", "err"):
             setattr(d, name, getattr(self, name)[layer].data_ptr())
         d.capacity = self.capacity[layer]
-        d.slots_per_unit = self.spu
+        d.slots_per_unit = self.spu_l[layer]
         return d
 
     def next_run_of(self, layer: int) -> int:  # kv_store.hpp:328-331
@@ -74,6 +83,30 @@ class DeviceTieredCache:
             if code == A.SCOUT_ERR_INVALID_ARGUMENT:
                 raise ValueError(f"tier layer {layer}: invalid argument in units {bad}")
             raise RuntimeError(f"tier layer {layer}: out of pool slots in units {bad}")
+
+    def adopt(self, layer: int, table: torch.Tensor, n_tokens: torch.Tensor):
+        """Start a layer from a placed state (a prefill done elsewhere): the
+        blocks with a slot in table [U][nbs] are fast, the rest of the first
+        n_tokens' blocks slow; every slot of the (layer, unit) range not in
+        table goes on the free stack. Marks start at 0."""
+        U, spu = self.U, self.spu_l[layer]
+        table = table.to(device=self.dev, dtype=torch.int32)
+        self.table[layer].copy_(table)
+        self.tier[layer].copy_((table >= 0).to(torch.uint8))
+        self.last_sel[layer].zero_()
+        self.ready[layer].fill_(-1)
+        self.n_tokens[layer].copy_(n_tokens)
+        base = self.layer_base[layer] + torch.arange(U, device=self.dev, dtype=torch.int32).view(U, 1) * spu
+        cand = base + torch.arange(spu - 1, -1, -1, device=self.dev, dtype=torch.int32).view(1, -1)  # [U][spu]
+        used = torch.zeros((U, spu), dtype=torch.bool, device=self.dev)
+        rel = table - base
+        ok = (table >= 0) & (rel >= 0) & (rel < spu)
+        uu, bb = ok.nonzero(as_tuple=True)
+        used[uu, (spu - 1 - rel[uu, bb]).long()] = True
+        # free slots first, in the stack's (descending) order
+        order = torch.sort(used.to(torch.int32), dim=1, stable=True).indices
+        self.free_slots[layer, :, :spu] = cand.gather(1, order)
+        self.n_free[layer] = (~used).sum(1).to(torch.int32)
 
     # ------------------------------------------------------------- reference API
     def pin_layer(self, layer: int):

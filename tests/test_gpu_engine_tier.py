@@ -107,3 +107,39 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, recall):
     # digests (incrementally maintained) equal on both sides and the pools hold the same live blocks
     for i in range(L):
         assert torch.equal(eng_side.dig[i], rep.dig[i])
+
+
+def test_engine_tier_host_path_matches_device_path(cuda):
+    """scout_engine_decode_step_kv_host (pinned host inputs and outputs,
+    pipelined copies) against scout_engine_decode_step_kv on an identical
+    second cache: same outputs, same tier state, step after step."""
+    rng = np.random.default_rng(5)
+    L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 40
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 11 + 50
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    sides = [Side(L, U, nbs, cap, kv, seed_rows) for _ in range(2)]
+    engs = []
+    for sd in sides:
+        layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+        engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
+                                 kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=4,
+                                 host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, host_staging=True,
+                                 chunk_layers=2))
+    out = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
+    h_out = [torch.empty(L, U * G, D).pin_memory(), torch.empty(L, U * G, 2).pin_memory()]
+    for step in range(1, steps + 1):
+        ins = [torch.randn(L, U * G, D, device="cuda").bfloat16(), torch.randn(L, U * G, D, device="cuda").bfloat16(),
+               torch.randn(L, U * G, D, device="cuda"),
+               torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous(),
+               torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")]
+        engs[0].decode_step_kv(step, *ins, *out)
+        h_ins = [t.cpu().pin_memory() for t in ins]
+        engs[1].decode_step_kv_host(step, *h_ins, *h_out)
+        for e in engs:
+            e.sync()
+        torch.cuda.synchronize()
+        assert torch.equal(h_out[0], out[0].cpu()) and torch.equal(h_out[1], out[1].cpu()), step
+        for name in ("tier", "last_sel", "table"):
+            assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
