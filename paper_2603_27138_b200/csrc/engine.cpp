@@ -346,12 +346,14 @@ struct scout_engine {
     // 3. begin_layer: tickets due at (step, i), applied after the marks
     int tier_pre(int step, int par, const void* q_true, const void* q_pred, cudaStream_t s) {
         const int L = cfg.layers, nbs = cfg.nb_stride;
+        ++launches;
         int rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(tier_dev.p), L, U, nbs, cfg.n_tokens, step,
                                         I(plan_tab), s);
         if (rc != SCOUT_OK) return rc;
         if ((rc = select_batch(0, L, q_true, q_pred, step, par, s)) != SCOUT_OK) return rc;
         for (int i = 0; i < L; ++i) {
             if (pending[i] < 0 || pending[i] > tick(step, i)) continue;
+            ++launches;
             if ((rc = scout_tier_apply(&tier[i], U, nbs, cfg.n_tokens, tick(step, i), nullptr, s)) != SCOUT_OK) return rc;
             pending[i] = -1;
         }
@@ -388,6 +390,7 @@ struct scout_engine {
             pa.recall_due[i] = cfg.recall_interval > 0 && (step + i) % cfg.recall_interval == 0;
             any_recall |= pa.recall_due[i] != 0;
         }
+        launches += 2;  // post-attention bookkeeping + n_tokens advance
         int rc = scout_tier_post_layers(pa, U, s);
         if (rc != SCOUT_OK) return rc;
         if (!any_recall) return SCOUT_OK;
@@ -395,6 +398,7 @@ struct scout_engine {
         CU(cudaStreamWaitEvent(side, ev_tmp, 0));
         for (int i = 0; i < L; ++i) {
             if (!pa.recall_due[i]) continue;
+            ++launches;
             if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, static_cast<long long>(i) * U * nbs,
                                               nbs, cfg.host_blocks, U, pa.cpu_ids + lk(i), pa.n_cpu + lu(i), pa.dst + lk(i),
                                               cfg.k, 1, side)) != SCOUT_OK)
