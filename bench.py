@@ -400,6 +400,36 @@ class RefBaseline:
                     sample=f"{n} " + self.sample)
 
 
+def measure_cpu_worker(wl, cfg, seconds=4.0):
+    """The CPU co-attention worker (scout_cpu_partial_attention, AVX-512, all
+    host threads) on this box over the workload's CPU share: each unit attends
+    over cpu_blocks_per_unit block images of the host tier with its G heads.
+    Reports blocks/s and the CPU time one decode step's CPU share would take
+    (the GPU step does not wait for it here: the bench pre-stages partials)."""
+    from paper_2603_27138_b200 import ops
+
+    U, G = wl.U, wl.G
+    nc = max(int(round(cfg["cpu_frac"] * cfg["k"])), 1)
+    hb = wl.host_tier.numel() // ops.slot_bytes(torch.bfloat16)
+    rng = np.random.default_rng(7)
+    idx = torch.from_numpy(rng.integers(0, hb, size=(U, nc)).astype(np.int64))
+    nb = torch.full((U,), nc, dtype=torch.int32)
+    q = torch.randn(U * G, D)
+    ops.cpu_partial_attention(wl.host_tier, torch.bfloat16, idx, nb, q, G)  # warm
+    n, t0 = 0, time.time()
+    while time.time() - t0 < seconds:
+        ops.cpu_partial_attention(wl.host_tier, torch.bfloat16, idx, nb, q, G)
+        n += 1
+    dt = time.time() - t0
+    bps = n * U * nc / dt
+    per_step = nc * U * (wl.L - 1)
+    return {"blocks_per_s": bps, "threads": os.cpu_count(), "blocks_per_step": per_step,
+            "ms_per_step": 1000.0 * per_step / bps, "gb_per_s": bps * ops.slot_bytes(torch.bfloat16) / 1e9,
+            "kernel": "scout_cpu_partial_attention (csrc/cpu_coattn.cpp, AVX-512 fp32)",
+            "note": "CPU share of one step (cpu_blocks_per_unit x units x layers 1..L-1); the bench pre-stages "
+                    "the CPU partials, so this is reported beside the GPU step, not inside it"}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -577,6 +607,9 @@ def main():
         if r is not None:
             cpu = {"value": r["tok_s"], "unit": "tokens/s", "cores": r["threads"], "kind": "reference",
                    "sample": r["sample"] + f"; {cpu_model()}"}
+    cpu_worker = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
+        cpu_worker = measure_cpu_worker(wl, cfg)
     if rank == 0:
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
@@ -606,6 +639,7 @@ def main():
             "tier": tier_info,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "cpu_coattention": cpu_worker,
         }
         print(json.dumps(line), flush=True)
     barrier(ws)

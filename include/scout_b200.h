@@ -325,6 +325,20 @@ int scout_recall_gather_ids(void* kv_pool, int kv_dtype, const void* host_tier, 
 int scout_kv_writeback(const void* kv_pool, int kv_dtype, void* host_tier, long long host_base, int nb_stride,
                        long long host_blocks, int n_units, const int32_t* open_slot, const int32_t* sealed_id, void* stream);
 
+/* ------------------------------------------------------------- host CPU --
+ * CPU co-attention worker (the reference's PrecomputeWorker
+ * engine.hpp:88-150 running partial_attention attention.hpp:73-95 on the
+ * CPU-side blocks): HOST memory throughout. Unit u's G heads
+ * q[(u*G+g)*128] (f32) attend over n_blocks[u] block images
+ * host_tier + host_index[u*k_stride+i] * slot_bytes (the pool's layout: bf16
+ * swizzled tiles or f32 rows), block_rows[u*k_stride+i] valid rows (NULL: 64).
+ * Writes o [(u*G+g)][128] normalised and ml [(u*G+g)][2] = (max logit, denom),
+ * empty = (0, -inf, 0): K2's CPU-partial input. fp32 arithmetic, AVX-512 when
+ * the CPU has it; `threads` workers (0 = all hardware threads).            */
+int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, const int64_t* host_index,
+                                const int32_t* block_rows, const int32_t* n_blocks, int k_stride, const float* q,
+                                int group, float scale, int n_units, float* o, float* ml, int threads);
+
 /* ------------------------------------------------------------- engine --
  * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,
  * engine.hpp:205-314, GPU side): per layer i, K1 for layer i+1 with the

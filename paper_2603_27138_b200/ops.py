@@ -212,3 +212,23 @@ class QueryPredictor:
         A.check(A.lib().scout_predict_query(_p(x), b, self.hidden, _p(self.w_packed), self.n_out, _p(out_f32),
                                             _p(out_bf16), _p(self.ws), self.ws.numel(), self.max_ctas, _stream()))
         return out_f32 if out_bf16 is None else (out_bf16 if out_f32 is None else (out_f32, out_bf16))
+
+
+def cpu_partial_attention(host_tier, kv_dtype, host_index, n_blocks, q, group, scale=None, block_rows=None,
+                          threads=0):
+    """CPU co-attention worker (host tensors): unit u's heads over its blocks
+    host_index[u, :n_blocks[u]] of the host tier. Returns (o, ml) host f32."""
+    host_index = torch.as_tensor(host_index, dtype=torch.int64).contiguous()
+    n_blocks = torch.as_tensor(n_blocks, dtype=torch.int32).contiguous()
+    q = torch.as_tensor(q, dtype=torch.float32).contiguous()
+    n_units = int(n_blocks.numel())
+    if scale is None:
+        scale = 1.0 / math.sqrt(A.HEAD_DIM)
+    rows = None if block_rows is None else torch.as_tensor(block_rows, dtype=torch.int32).contiguous()
+    o = torch.empty(n_units * group, A.HEAD_DIM, dtype=torch.float32)
+    ml = torch.empty(n_units * group, 2, dtype=torch.float32)
+    A.check(A.lib().scout_cpu_partial_attention(host_tier.data_ptr(), dtype_code(kv_dtype), host_index.data_ptr(),
+                                                None if rows is None else rows.data_ptr(), n_blocks.data_ptr(),
+                                                int(host_index.shape[1]), q.data_ptr(), int(group), float(scale),
+                                                n_units, o.data_ptr(), ml.data_ptr(), int(threads)))
+    return o, ml
