@@ -5,10 +5,11 @@
 // attention.hpp:73-95, on the CPU-side blocks of layer i+1 with the predicted
 // query) by a multi-threaded AVX-512 kernel over the host tier's block images
 // (the pool's bf16 swizzled tile layout, or f32 row-major). One unit's G query
-// heads share a pass over its blocks (GQA), as on the GPU: per block,
-// S = K (64 x 128) . Q^T (128 x G) in fp32, an online softmax per head, and
-// O += P^T V. The result is K2's CPU-partial input: o normalised plus
-// (max logit, denominator), empty partials (0, -inf, 0) (attention.hpp:24-36).
+// heads share a pass over its blocks (GQA), as on the GPU: per block, the
+// rows are decoded once, S = K (64 x 128) . Q^T (128 x G) in fp32, a
+// block-wise online softmax per head, and O += P^T V. The result is K2's
+// CPU-partial input: o normalised plus (max logit, denominator), empty
+// partials (0, -inf, 0) (attention.hpp:24-36).
 #include <immintrin.h>
 
 #include <algorithm>
@@ -105,17 +106,24 @@ struct Job {
     float* ml;
 };
 
+// Per block: the block's rows are decoded once (K and V into fp32), then for
+// each head: 64 scores, one block maximum, 64 exponentials and the weighted V
+// sum; the running state is rescaled once per block (same result as the
+// per-row online softmax of accumulate_token, attention.hpp:38-50, up to fp32
+// rounding).
 template <bool AVX>
 void run_unit(const Job& j, int u) {
     const int G = j.G;
-    float m[GMAX], l[GMAX], acc[GMAX][D];
+    float m[GMAX], l[GMAX];
+    alignas(64) float acc[GMAX][D];
+    alignas(64) float kb[BS][D], vb[BS][D];
+    float sc[BS];
     for (int g = 0; g < G; ++g) {
         m[g] = -std::numeric_limits<float>::infinity();
         l[g] = 0.f;
         std::memset(acc[g], 0, sizeof(acc[g]));
     }
     const float* qu = j.q + static_cast<size_t>(u) * G * D;
-    float krow[D], vrow[D];
     const int nb = j.n_blocks[u];
     for (int i = 0; i < nb; ++i) {
         const size_t idx = static_cast<size_t>(u) * j.k_stride + i;
@@ -124,21 +132,35 @@ void run_unit(const Job& j, int u) {
         const int rows = j.rows ? j.rows[idx] : BS;
         for (int r = 0; r < rows; ++r) {
             if (AVX) {
-                load_row_avx512(kt, j.kv_dtype, r, krow);
-                load_row_avx512(vt, j.kv_dtype, r, vrow);
+                load_row_avx512(kt, j.kv_dtype, r, kb[r]);
+                load_row_avx512(vt, j.kv_dtype, r, vb[r]);
             } else {
-                load_row_scalar(kt, j.kv_dtype, r, krow);
-                load_row_scalar(vt, j.kv_dtype, r, vrow);
+                load_row_scalar(kt, j.kv_dtype, r, kb[r]);
+                load_row_scalar(vt, j.kv_dtype, r, vb[r]);
             }
-            for (int g = 0; g < G; ++g) {
-                // online softmax (accumulate_token, attention.hpp:38-50)
-                const float s = (AVX ? dot128_avx512(krow, qu + g * D) : dot128_scalar(krow, qu + g * D)) * j.scale;
-                const float mn = std::max(m[g], s);
-                const float alpha = std::exp(m[g] - mn), p = std::exp(s - mn);
-                m[g] = mn;
-                l[g] = l[g] * alpha + p;
-                if (AVX) axpy128_avx512(acc[g], p, vrow, alpha);
-                else axpy128_scalar(acc[g], p, vrow, alpha);
+        }
+        for (int g = 0; g < G; ++g) {
+            const float* qg = qu + g * D;
+            float mx = -std::numeric_limits<float>::infinity();
+            for (int r = 0; r < rows; ++r) {
+                sc[r] = (AVX ? dot128_avx512(kb[r], qg) : dot128_scalar(kb[r], qg)) * j.scale;
+                mx = std::max(mx, sc[r]);
+            }
+            const float mn = std::max(m[g], mx);
+            const float alpha = std::exp(m[g] - mn);
+            float lsum = 0.f;
+            for (int r = 0; r < rows; ++r) {
+                sc[r] = std::exp(sc[r] - mn);
+                lsum += sc[r];
+            }
+            l[g] = l[g] * alpha + lsum;
+            m[g] = mn;
+            if (AVX) {
+                axpy128_avx512(acc[g], 0.f, vb[0], alpha);  // acc *= alpha
+                for (int r = 0; r < rows; ++r) axpy128_avx512(acc[g], sc[r], vb[r], 1.f);
+            } else {
+                axpy128_scalar(acc[g], 0.f, vb[0], alpha);
+                for (int r = 0; r < rows; ++r) axpy128_scalar(acc[g], sc[r], vb[r], 1.f);
             }
         }
     }
