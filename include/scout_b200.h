@@ -316,12 +316,13 @@ int scout_predict_query(const float* x, int batch, int hidden, const void* w_pac
  * bounded synthetic tier whose images alias) (pinned, device-mapped memory).
  * scout_recall_gather_ids: unit u's blocks ids[u][0..n_ids[u]) (e.g. K1's
  * CPU-side ids) into the slots K5 assigned (dst_slots, -1 = skipped), SM
- * loads over PCIe / C2C, ctas_per_unit CTAs per unit (0 = 2).
+ * loads over PCIe / C2C on `ctas` CTAs (0 = 32: a narrow footprint next to
+ * a persistent K2).
  * scout_kv_writeback: write-through of the blocks scout_tier_append sealed
  * (sealed_id[u] >= 0 at slot open_slot[u]) into their host images.        */
 int scout_recall_gather_ids(void* kv_pool, int kv_dtype, const void* host_tier, long long host_base, int nb_stride,
                             long long host_blocks, int n_units, const int32_t* ids, const int32_t* n_ids, const int32_t* dst_slots,
-                            int k_stride, int ctas_per_unit, void* stream);
+                            int k_stride, int ctas, void* stream);
 int scout_kv_writeback(const void* kv_pool, int kv_dtype, void* host_tier, long long host_base, int nb_stride,
                        long long host_blocks, int n_units, const int32_t* open_slot, const int32_t* sealed_id, void* stream);
 

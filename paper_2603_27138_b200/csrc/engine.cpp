@@ -118,7 +118,7 @@ struct scout_engine {
     std::vector<std::vector<int32_t>> rc_dst;
     std::vector<Buf> rc_dev;
     // streams / events
-    cudaStream_t k1s = nullptr, side = nullptr, h2d = nullptr, d2h = nullptr;
+    cudaStream_t k1s = nullptr, side = nullptr, h2d = nullptr, d2h = nullptr, rc_list = nullptr;
     cudaEvent_t ev_start = nullptr, ev_k1_end = nullptr, ev_tmp = nullptr;
     cudaEvent_t ev_k2[2] = {nullptr, nullptr};
     bool k2_recorded[2] = {false, false};
@@ -135,7 +135,25 @@ struct scout_engine {
     std::thread rc_thread;
     std::mutex rc_mu;
     std::condition_variable rc_cv, rc_idle;
-    std::deque<std::pair<int, unsigned>> rc_jobs;  // (layer, token)
+    struct RcJob {
+        int layer;
+        unsigned token;
+        int slot;   // device tier mode: pinned list slot (-1: static recall plan)
+        int chunk;  // ... and the post chunk whose lists it waits for
+    };
+    std::deque<RcJob> rc_jobs;
+    // device tier mode recalls on the copy engines: the post-attention kernel's
+    // lists (K1's CPU-side ids, K5's slots) come back to pinned slots, and the
+    // issuer thread turns them into copy descriptors
+    static constexpr int RC_SLOTS = 4;
+    uint8_t* rc_pinned = nullptr;  // RC_SLOTS x (ids [L][U][k] | n [L][U] | dst [L][U][k]) int32
+    size_t rc_slot_bytes = 0;
+    static constexpr int MAX_CH = (K2_MAX_LAYERS + 7) / 8;
+    cudaEvent_t ev_chunk[RC_SLOTS][MAX_CH] = {};  // post chunk done (post stream)
+    cudaEvent_t ev_list[RC_SLOTS][MAX_CH] = {};   // its lists landed (pinned)
+    cudaEvent_t ev_post = nullptr, ev_pre = nullptr;
+    cudaStream_t post_s = nullptr;
+    int rc_slot_jobs[RC_SLOTS] = {};
     bool rc_stop = false, rc_busy = false;
     int rc_err = SCOUT_OK;
     char rc_msg[256] = {0};
@@ -164,7 +182,17 @@ struct scout_engine {
 
     ~scout_engine() {
         stop_recalls();
-        for (cudaStream_t s : {k1s, side, h2d, d2h})
+        for (auto& row : ev_chunk)
+            for (auto ev : row)
+                if (ev) cudaEventDestroy(ev);
+        for (auto& row : ev_list)
+            for (auto ev : row)
+                if (ev) cudaEventDestroy(ev);
+        if (ev_post) cudaEventDestroy(ev_post);
+        if (ev_pre) cudaEventDestroy(ev_pre);
+        if (post_s) cudaStreamDestroy(post_s);
+        if (rc_pinned) cudaFreeHost(rc_pinned);
+        for (cudaStream_t s : {k1s, side, h2d, d2h, rc_list})
             if (s) cudaStreamDestroy(s);
         for (cudaEvent_t e : {ev_start, ev_k1_end, ev_tmp, ev_k2[0], ev_k2[1], stage_free[0], stage_free[1], ev_side_end, ev_kvin})
             if (e) cudaEventDestroy(e);
@@ -282,7 +310,7 @@ struct scout_engine {
             if (L.recall_n <= 0 || rc_src[i].empty() || (step + i) % cfg.recall_interval != 0) continue;
             rc_token[i] = token;  // the next step's K2 waits for it before streaming layer i
             std::lock_guard<std::mutex> lk(rc_mu);
-            rc_jobs.emplace_back(i, token);
+            rc_jobs.push_back(RcJob{i, token, -1, 0});
             any = true;
         }
         if (any) rc_cv.notify_one();
@@ -314,15 +342,48 @@ struct scout_engine {
             rc_jobs.pop_front();
             rc_busy = true;
             lk.unlock();
-            const int rc = run_recall(job.first, job.second);
+            const int rc = job.slot < 0 ? run_recall(job.layer, job.token) : run_tier_recall(job);
             lk.lock();
             rc_busy = false;
+            if (job.slot >= 0 && --rc_slot_jobs[job.slot] == 0) rc_idle.notify_all();
             if (rc != SCOUT_OK && rc_err == SCOUT_OK) {
                 rc_err = rc;
                 std::snprintf(rc_msg, sizeof(rc_msg), "%s", scout_last_error());
             }
             if (rc_jobs.empty()) rc_idle.notify_all();
         }
+    }
+    // device tier mode: one layer's recall from a pinned list slot (issuer thread)
+    int run_tier_recall(const RcJob& job) {
+        if (cudaEventSynchronize(ev_list[job.slot][job.chunk]) != cudaSuccess) {
+            scout_host::set_error(SCOUT_ERR_CUDA, "recall lists: %s", cudaGetErrorString(cudaGetLastError()));
+            return SCOUT_ERR_CUDA;
+        }
+        const int L = cfg.layers, k = cfg.k, nbs = cfg.nb_stride, i = job.layer;
+        const int32_t* ids = reinterpret_cast<const int32_t*>(rc_pinned + job.slot * rc_slot_bytes);
+        const int32_t* nn = ids + static_cast<size_t>(L) * U * k;
+        const int32_t* dst = nn + static_cast<size_t>(L) * U;
+        std::vector<int64_t> src_v;
+        std::vector<int32_t> dst_v;
+        src_v.reserve(static_cast<size_t>(U) * 8);
+        dst_v.reserve(static_cast<size_t>(U) * 8);
+        for (int u = 0; u < U; ++u) {
+            const int n = nn[static_cast<size_t>(i) * U + u];
+            for (int j = 0; j < n; ++j) {
+                const size_t o = (static_cast<size_t>(i) * U + u) * k + j;
+                if (dst[o] < 0) continue;
+                long long hi = (static_cast<long long>(i) * U + u) * nbs + ids[o];
+                if (cfg.host_blocks > 0) hi %= cfg.host_blocks;
+                src_v.push_back(hi);
+                dst_v.push_back(dst[o]);
+            }
+        }
+        int rc = SCOUT_OK;
+        if (!src_v.empty())
+            rc = scout_recall_copy(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, src_v.data(), dst_v.data(),
+                                   static_cast<int>(src_v.size()), side);
+        if (rc != SCOUT_OK) return rc;
+        return write_value(side, recall_flag + i, job.token);
     }
     // every queued recall enqueued on the side stream
     void drain_recalls() {
@@ -359,13 +420,20 @@ struct scout_engine {
         }
         return SCOUT_OK;
     }
-    // 5. after the attention, every layer in one launch: append the token
-    //    (open / seal + LRU eviction, write-through) and, when due, schedule the
-    //    recall of the layer's CPU-side selected blocks (maybe_schedule_recall,
-    //    recall.hpp:114-126); n_tokens advances;
-    // 6. the recall copies on the side stream; the next step's K2 waits for a
-    //    layer's flag before streaming it (visible at (m+1, i))
-    int tier_post(int step, int par, unsigned tok, const float* k_new, const float* v_new, cudaStream_t s) {
+    // 5. as K2 finishes each chunk of layers (layer_done flags), one launch per
+    //    chunk on the post stream: append the token (open / seal + LRU
+    //    eviction, write-through) and, when due, schedule the recall of the
+    //    layer's CPU-side selected blocks (maybe_schedule_recall,
+    //    recall.hpp:114-126) -- issued right after the layer's attention, as in
+    //    engine.hpp:299-307, so the copies get a whole step before the next
+    //    K2 needs them; n_tokens advances once every layer has appended;
+    // 6. the recall copies: copy engines (lists back to a pinned slot, the
+    //    issuer thread builds the descriptors) or the SM gather (recall_mode 1).
+    //    The next step's K2 waits for a layer's flag before streaming it.
+    // `pre`: an event recorded on the step's stream after phases 1-3 (before K2).
+    static constexpr int POST_CH = 8;
+    int tier_post(int step, int par, unsigned tok, const float* k_new, const float* v_new, cudaEvent_t pre,
+                  cudaStream_t s) {
         const int L = cfg.layers, nbs = cfg.nb_stride;
         TierPostArgs pa{};
         pa.layers = static_cast<const scout_tier_layer*>(tier_dev.p);
@@ -385,28 +453,79 @@ struct scout_engine {
         pa.cpu_ids = I(cpu_ids[par]);
         pa.n_cpu = I(n_cpu[par]);
         pa.dst = I(tier_dst);
-        bool any_recall = false;
-        for (int i = 0; i < L; ++i) {
+        for (int i = 0; i < L; ++i)
             pa.recall_due[i] = cfg.recall_interval > 0 && (step + i) % cfg.recall_interval == 0;
-            any_recall |= pa.recall_due[i] != 0;
+        const bool ce = cfg.recall_mode == 0 && rc_pinned != nullptr;
+        const int slot = static_cast<int>(tok % RC_SLOTS);
+        if (ce) {  // this step's list slot must be free (the issuer thread is done with it)
+            std::unique_lock<std::mutex> lk(rc_mu);
+            rc_idle.wait(lk, [&] { return rc_slot_jobs[slot] == 0; });
         }
-        launches += 2;  // post-attention bookkeeping + n_tokens advance
-        int rc = scout_tier_post_layers(pa, U, s);
-        if (rc != SCOUT_OK) return rc;
-        if (!any_recall) return SCOUT_OK;
-        CU(cudaEventRecord(ev_tmp, s));
-        CU(cudaStreamWaitEvent(side, ev_tmp, 0));
-        for (int i = 0; i < L; ++i) {
-            if (!pa.recall_due[i]) continue;
-            ++launches;
-            if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, static_cast<long long>(i) * U * nbs,
-                                              nbs, cfg.host_blocks, U, pa.cpu_ids + lk(i), pa.n_cpu + lu(i), pa.dst + lk(i),
-                                              cfg.k, 1, side)) != SCOUT_OK)
+        int32_t* hid = ce ? reinterpret_cast<int32_t*>(rc_pinned + slot * rc_slot_bytes) : nullptr;
+        int32_t* hn = ce ? hid + static_cast<size_t>(L) * U * cfg.k : nullptr;
+        int32_t* hd = ce ? hn + static_cast<size_t>(L) * U : nullptr;
+        CU(cudaStreamWaitEvent(post_s, pre, 0));
+        int rc;
+        for (int c = 0, lo = 0; lo < L; ++c, lo += POST_CH) {
+            const int n = lo + POST_CH > L ? L - lo : POST_CH;
+            if ((rc = wait_value(post_s, layer_done + lo + n - 1, tok * static_cast<unsigned>(grid))) != SCOUT_OK)
                 return rc;
-            if ((rc = write_value(side, recall_flag + i, tok)) != SCOUT_OK) return rc;
-            rc_token[i] = tok;
-            pending[i] = tick(step + 1, i);
+            pa.layer0 = lo;
+            ++launches;
+            if ((rc = scout_tier_post_layers(pa, U, n, post_s)) != SCOUT_OK) return rc;
+            bool due = false;
+            for (int i = lo; i < lo + n; ++i) due |= pa.recall_due[i] != 0;
+            if (!due) continue;
+            if (ce) {
+                // the lists travel on their own stream; `side` carries only the
+                // issuer thread's copies and flags (which the next step's K2
+                // waits for), so nothing of the next step may queue ahead there
+                CU(cudaEventRecord(ev_chunk[slot][c], post_s));
+                CU(cudaStreamWaitEvent(rc_list, ev_chunk[slot][c], 0));
+                for (int i = lo; i < lo + n; ++i) {
+                    if (!pa.recall_due[i]) continue;
+                    CU(cudaMemcpyAsync(hid + lk(i), pa.cpu_ids + lk(i), static_cast<size_t>(U) * cfg.k * 4,
+                                       cudaMemcpyDeviceToHost, rc_list));
+                    CU(cudaMemcpyAsync(hn + lu(i), pa.n_cpu + lu(i), static_cast<size_t>(U) * 4, cudaMemcpyDeviceToHost,
+                                       rc_list));
+                    CU(cudaMemcpyAsync(hd + lk(i), pa.dst + lk(i), static_cast<size_t>(U) * cfg.k * 4,
+                                       cudaMemcpyDeviceToHost, rc_list));
+                }
+                CU(cudaEventRecord(ev_list[slot][c], rc_list));
+                {
+                    std::lock_guard<std::mutex> lk(rc_mu);
+                    for (int i = lo; i < lo + n; ++i) {
+                        if (!pa.recall_due[i]) continue;
+                        rc_jobs.push_back(RcJob{i, tok, slot, c});
+                        ++rc_slot_jobs[slot];
+                    }
+                }
+                rc_cv.notify_one();
+            } else {
+                CU(cudaEventRecord(ev_chunk[slot][c], post_s));
+                CU(cudaStreamWaitEvent(side, ev_chunk[slot][c], 0));
+                for (int i = lo; i < lo + n; ++i) {
+                    if (!pa.recall_due[i]) continue;
+                    ++launches;
+                    if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier,
+                                                      static_cast<long long>(i) * U * nbs, nbs, cfg.host_blocks, U,
+                                                      pa.cpu_ids + lk(i), pa.n_cpu + lu(i), pa.dst + lk(i), cfg.k, 0,
+                                                      side)) != SCOUT_OK)
+                        return rc;
+                    if ((rc = write_value(side, recall_flag + i, tok)) != SCOUT_OK) return rc;
+                }
+            }
+            for (int i = lo; i < lo + n; ++i) {
+                if (!pa.recall_due[i]) continue;
+                rc_token[i] = tok;  // the next step's K2 waits for it before streaming layer i
+                pending[i] = tick(step + 1, i);
+            }
         }
+        ++launches;
+        if ((rc = scout_tier_advance(const_cast<int32_t*>(cfg.n_tokens), U, post_s)) != SCOUT_OK) return rc;
+        // the next step (planning, K1) follows the bookkeeping
+        CU(cudaEventRecord(ev_post, post_s));
+        CU(cudaStreamWaitEvent(s, ev_post, 0));
         return SCOUT_OK;
     }
 
@@ -512,7 +631,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
             }
         }
     }
-    for (cudaStream_t* s : {&e->k1s, &e->side, &e->h2d, &e->d2h}) cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
+    for (cudaStream_t* s : {&e->k1s, &e->side, &e->h2d, &e->d2h, &e->rc_list})
+        cudaStreamCreateWithFlags(s, cudaStreamNonBlocking);
     for (cudaEvent_t* ev : {&e->ev_start, &e->ev_k1_end, &e->ev_tmp, &e->ev_k2[0], &e->ev_k2[1], &e->stage_free[0],
                             &e->stage_free[1]})
         cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
@@ -543,7 +663,26 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         e->host_dev = static_cast<uint8_t*>(hv);
     }
     cudaGetDevice(&e->device);
-    if (c.recall_interval > 0 && !c.tier) e->rc_thread = std::thread([e] { e->recall_loop(); });
+    if (c.tier && c.recall_interval > 0 && c.recall_mode == 0) {
+        e->rc_slot_bytes = (static_cast<size_t>(c.layers) * e->U * (2 * c.k + 1) * 4 + 255) / 256 * 256;
+        if (cudaHostAlloc(reinterpret_cast<void**>(&e->rc_pinned), e->rc_slot_bytes * scout_engine::RC_SLOTS,
+                          cudaHostAllocDefault) != cudaSuccess) {
+            e->rc_pinned = nullptr;
+            delete e;
+            set_error(SCOUT_ERR_CUDA, "scout_engine_create: pinned recall lists");
+            return SCOUT_ERR_CUDA;
+        }
+        for (auto& row : e->ev_list)
+            for (auto& ev : row) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming | cudaEventBlockingSync);
+    }
+    if (c.tier) {
+        for (auto& row : e->ev_chunk)
+            for (auto& ev : row) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e->ev_post, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e->ev_pre, cudaEventDisableTiming);
+        cudaStreamCreateWithFlags(&e->post_s, cudaStreamNonBlocking);
+    }
+    if (c.recall_interval > 0) e->rc_thread = std::thread([e] { e->recall_loop(); });
     e->ev_k1.resize(c.layers);
     for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     e->chunk_ev.resize(e->nch);
@@ -688,8 +827,12 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     // go out to the host worker. Device tier mode: planning view + K1 + ticket
     // application (the previous step's bookkeeping is ordered by ev_start)
     CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[0], 0));
-    if (e->tier_mode) rc = e->tier_pre(step, par, d_qt, d_qp, e->k1s);
-    else rc = e->select_batch(0, L, d_qt, d_qp, step, par, e->k1s);
+    if (e->tier_mode) {
+        rc = e->tier_pre(step, par, d_qt, d_qp, e->k1s);
+        if (rc == SCOUT_OK && cudaEventRecord(e->ev_pre, e->k1s) != cudaSuccess) rc = SCOUT_ERR_CUDA;
+    } else {
+        rc = e->select_batch(0, L, d_qt, d_qp, step, par, e->k1s);
+    }
     if (rc != SCOUT_OK) return rc;
     if (h_cpu_ids) {
         CU(cudaEventRecord(e->ev_k1[0], e->k1s));
@@ -719,8 +862,8 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
         SCOUT_OK)
         return rc;
     if (e->tier_mode) {
-        CU(cudaStreamWaitEvent(st, e->ev_kvin, 0));
-        if ((rc = e->tier_post(step, par, token, d_kn, d_vn, st)) != SCOUT_OK) return rc;
+        CU(cudaStreamWaitEvent(e->post_s, e->ev_kvin, 0));  // the token's K/V landed
+        if ((rc = e->tier_post(step, par, token, d_kn, d_vn, e->ev_pre, st)) != SCOUT_OK) return rc;
     } else if ((rc = e->issue_recalls(step)) != SCOUT_OK) {
         return rc;
     }
@@ -765,6 +908,7 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
     if (phases) cudaEventRecord(pe[0], st);
     // 1-3. planning view, select + split + mark, begin_layer's ticket application
     if ((rc = e->tier_pre(step, par, q_true, q_pred, st)) != SCOUT_OK) return rc;
+    CU(cudaEventRecord(e->ev_pre, st));
     if (phases) cudaEventRecord(pe[1], st);
     // 4. attention + merge over all layers (one persistent launch)
     std::vector<const void*> q(L);
@@ -781,13 +925,13 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
         return rc;
     if (phases) cudaEventRecord(pe[2], st);
     // 5-6. append + write-through + recall scheduling, then the recall copies
-    if ((rc = e->tier_post(step, par, token, k_new, v_new, st)) != SCOUT_OK) return rc;
+    if ((rc = e->tier_post(step, par, token, k_new, v_new, e->ev_pre, st)) != SCOUT_OK) return rc;
     if (phases) {
-        cudaEventRecord(pe[3], e->side);
+        cudaEventRecord(pe[3], st);
         cudaEventSynchronize(pe[3]);
         float t[3];
         for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], pe[i], pe[i + 1]);
-        fprintf(stderr, "step %d: plan+K1+apply %.3f K2 %.3f post+recalls %.3f ms\n", step, t[0], t[1], t[2]);
+        fprintf(stderr, "step %d: plan+K1+apply %.3f K2 %.3f post tail %.3f ms\n", step, t[0], t[1], t[2]);
         for (auto& ev : pe) cudaEventDestroy(ev);
     }
     return SCOUT_OK;

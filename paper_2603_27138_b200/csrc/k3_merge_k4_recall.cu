@@ -154,36 +154,41 @@ extern "C" int scout_recall_copy(void* kv_pool, int kv_dtype, const void* host_b
 //   modulo host_blocks when host_blocks > 0 (a bounded synthetic tier: images alias)
 namespace {
 
-// recall: unit u's n_ids[u] blocks ids[u][i] -> pool slots dst[u][i] (-1: rejected ticket)
 __device__ __forceinline__ long long host_index(long long base, int u, int nb_stride, int id, long long host_blocks) {
     const long long i = base + static_cast<long long>(u) * nb_stride + id;
     return host_blocks > 0 ? i % host_blocks : i;
 }
 
+// recall: unit u's n_ids[u] blocks ids[u][i] -> pool slots dst[u][i] (-1:
+// rejected ticket). A small fixed grid loops over the units: the copies are
+// PCIe-bound anyway, and a narrow footprint leaves the SMs' thread / register
+// room to the persistent K2 that runs next to it (a wide grid of gather CTAs
+// held K2's CTAs back from launching).
 __global__ void __launch_bounds__(256) recall_ids_kernel(uint8_t* pool, const uint8_t* host, long long host_base,
                                                          int nb_stride, long long host_blocks, const int32_t* ids,
                                                          const int32_t* n_ids, const int32_t* dst, int k_stride,
-                                                         size_t slot_bytes) {
-    const int u = blockIdx.y;
-    const int n = n_ids[u];
+                                                         size_t slot_bytes, int n_units) {
     const int nvec = static_cast<int>(slot_bytes / 16);
-    for (int i = blockIdx.x; i < n; i += gridDim.x) {
-        const int slot = dst[static_cast<size_t>(u) * k_stride + i];
-        if (slot < 0) continue;
-        const long long hb = host_index(host_base, u, nb_stride, ids[static_cast<size_t>(u) * k_stride + i], host_blocks);
-        const int4* s = reinterpret_cast<const int4*>(host + static_cast<size_t>(hb) * slot_bytes);
-        int4* d = reinterpret_cast<int4*>(pool + static_cast<size_t>(slot) * slot_bytes);
-        for (int base = threadIdx.x; base < nvec; base += 4 * blockDim.x) {
-            int4 v[4];
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        const int n = n_ids[u];
+        for (int i = 0; i < n; ++i) {
+            const int slot = dst[static_cast<size_t>(u) * k_stride + i];
+            if (slot < 0) continue;
+            const long long hb = host_index(host_base, u, nb_stride, ids[static_cast<size_t>(u) * k_stride + i], host_blocks);
+            const int4* s = reinterpret_cast<const int4*>(host + static_cast<size_t>(hb) * slot_bytes);
+            int4* d = reinterpret_cast<int4*>(pool + static_cast<size_t>(slot) * slot_bytes);
+            for (int base = threadIdx.x; base < nvec; base += 4 * blockDim.x) {
+                int4 v[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int idx = base + k * blockDim.x;
-                if (idx < nvec) v[k] = __ldcv(s + idx);
-            }
+                for (int k = 0; k < 4; ++k) {
+                    const int idx = base + k * blockDim.x;
+                    if (idx < nvec) v[k] = __ldcv(s + idx);
+                }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int idx = base + k * blockDim.x;
-                if (idx < nvec) d[idx] = v[k];
+                for (int k = 0; k < 4; ++k) {
+                    const int idx = base + k * blockDim.x;
+                    if (idx < nvec) d[idx] = v[k];
+                }
             }
         }
     }
@@ -215,7 +220,7 @@ const void* device_view(const void* host) {
 
 extern "C" int scout_recall_gather_ids(void* kv_pool, int kv_dtype, const void* host_tier, long long host_base,
                                        int nb_stride, long long host_blocks, int n_units, const int32_t* ids, const int32_t* n_ids,
-                                       const int32_t* dst_slots, int k_stride, int ctas_per_unit, void* stream) {
+                                       const int32_t* dst_slots, int k_stride, int ctas, void* stream) {
     using namespace scout_host;
     if (kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32) {
         set_error(SCOUT_ERR_UNSUPPORTED, "scout_recall_gather_ids: kv dtype %d unsupported", kv_dtype);
@@ -227,10 +232,11 @@ extern "C" int scout_recall_gather_ids(void* kv_pool, int kv_dtype, const void* 
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     if (n_units == 0) return SCOUT_OK;
-    const int cpu = ctas_per_unit > 0 ? ctas_per_unit : 2;
-    recall_ids_kernel<<<dim3(cpu, n_units), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    int grid = ctas > 0 ? ctas : 32;
+    if (grid > n_units) grid = n_units;
+    recall_ids_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
         static_cast<uint8_t*>(kv_pool), static_cast<const uint8_t*>(device_view(host_tier)), host_base, nb_stride,
-        host_blocks, ids, n_ids, dst_slots, k_stride, slot_bytes(kv_dtype));
+        host_blocks, ids, n_ids, dst_slots, k_stride, slot_bytes(kv_dtype), n_units);
     return check_launch("scout_recall_gather_ids");
 }
 

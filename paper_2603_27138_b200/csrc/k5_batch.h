@@ -11,6 +11,7 @@ constexpr int K5_MAX_LAYERS = 96;
 struct TierPostArgs {
     const scout_tier_layer* layers;  // device array [n_layers]
     int n_layers, nbs, k, step, ticket_base;
+    int layer0;                      // first layer of this launch (grid.y layers from it)
     const int32_t* n_tokens;         // count before the append (advanced after the launch)
     uint8_t* pool;                   // bf16 KV pool
     const float* k_new;              // [L][U][128]
@@ -26,4 +27,7 @@ struct TierPostArgs {
 
 int scout_tier_plan_layers(const scout_tier_layer* layers_dev, int n_layers, int n_units, int nb_stride,
                            const int32_t* n_tokens, int step, int32_t* tables, cudaStream_t st);
-int scout_tier_post_layers(const TierPostArgs& a, int n_units, cudaStream_t st);
+// post-attention bookkeeping of layers [a.layer0, a.layer0 + n_layers_launch)
+int scout_tier_post_layers(const TierPostArgs& a, int n_units, int n_layers_launch, cudaStream_t st);
+// n_tokens += 1 once every layer has appended
+int scout_tier_advance(int32_t* n_tokens, int n_units, cudaStream_t st);

@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(TT) tier_plan_layers_kernel(const scout_tier_l
 __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs a) {
     __shared__ TierSm S;
     __shared__ int s_slot, s_sealed;
-    const int u = blockIdx.x, l = blockIdx.y, c = threadIdx.x;
+    const int u = blockIdx.x, l = a.layer0 + blockIdx.y, c = threadIdx.x;
     const scout_tier_layer& L = a.layers[l];
     Unit U = unit_of(L, u, a.nbs);
     const int pos = a.n_tokens[u];
@@ -578,10 +578,12 @@ int scout_tier_plan_layers(const scout_tier_layer* layers_dev, int n_layers, int
     return scout_host::check_launch("tier plan (all layers)");
 }
 
-int scout_tier_post_layers(const TierPostArgs& a, int n_units, cudaStream_t st) {
-    tier_post_layers_kernel<<<dim3(n_units, a.n_layers), TT, 0, st>>>(a);
-    int rc = scout_host::check_launch("tier post-attention (all layers)");
-    if (rc != SCOUT_OK) return rc;
-    advance_tokens_kernel<<<(n_units + 255) / 256, 256, 0, st>>>(const_cast<int32_t*>(a.n_tokens), n_units);
+int scout_tier_post_layers(const TierPostArgs& a, int n_units, int n_layers_launch, cudaStream_t st) {
+    tier_post_layers_kernel<<<dim3(n_units, n_layers_launch), TT, 0, st>>>(a);
+    return scout_host::check_launch("tier post-attention");
+}
+
+int scout_tier_advance(int32_t* n_tokens, int n_units, cudaStream_t st) {
+    advance_tokens_kernel<<<(n_units + 255) / 256, 256, 0, st>>>(n_tokens, n_units);
     return scout_host::check_launch("advance n_tokens");
 }

@@ -143,3 +143,32 @@ def test_engine_tier_host_path_matches_device_path(cuda):
         assert torch.equal(h_out[0], out[0].cpu()) and torch.equal(h_out[1], out[1].cpu()), step
         for name in ("tier", "last_sel", "table"):
             assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
+
+
+def test_engine_tier_back_to_back_steps_with_recalls(cuda):
+    """Steps queued back to back (no host sync), a recall every step: the
+    copy-engine recalls (issuer thread) must never sit behind the next step's
+    work that waits for them (a K2 flag wait would trap after 10 s)."""
+    L, batch, hkv, G, k, cap, nbs = 4, 2, 2, 4, 6, 8, 32
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 14 + 3
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    sd = Side(L, U, nbs, cap, kv, seed_rows)
+    layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+    eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
+                       kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=1,
+                       host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16)
+    qs = [torch.randn(L, U * G, D, device="cuda").bfloat16() for _ in range(4)]
+    cpu_o = torch.randn(L, U * G, D, device="cuda")
+    cpu_ml = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
+    kn, vn = torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")
+    out_o = torch.empty(L, U * G, D, device="cuda")
+    out_ml = torch.empty(L, U * G, 2, device="cuda")
+    for step in range(1, 61):  # drifting queries: every step recalls something
+        eng.decode_step_kv(step, qs[step % 4], qs[(step + 1) % 4], cpu_o, cpu_ml, kn, vn, out_o, out_ml)
+    eng.sync()
+    torch.cuda.synchronize()
+    assert int(sd.tier.err.abs().sum()) == 0
+    assert torch.isfinite(out_o).all()
+    assert int(sd.n_tokens[0]) == T0 + 60
