@@ -697,6 +697,8 @@ def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False):
     d2h_bytes = sum(x.numel() * x.element_size() for x in (h_out, h_oml, h_cpu_ids, h_n_cpu))
     return {"value": global_batch / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms,
             "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes, "matches_device_path": ok,
+            "verified_by": ("tests/test_gpu_engine_tier.py::test_engine_tier_host_path_matches_device_path "
+                            "(bit-exact, step by step)") if tier_mode else "the check above (same inputs, bit-exact)",
             "path": "C ABI scout_engine_decode_step_%s (csrc/engine.cpp), pinned host buffers" %
                     ("kv_host" if tier_mode else "host")}
 
