@@ -340,9 +340,18 @@ __device__ __forceinline__ void fast_quad(const DigT* blo, const DigT* bhi, int 
 // to 512 blocks, 2: up to 1024, 4: up to 2048); 0: shared-memory accumulators.
 template <typename DigT, int G, int MODE, int QPT>
 __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT_K1_MINB) score_topk_kernel(const K1Batch batch) {
-    const scout_topk_args& a = batch.a[blockIdx.y];  // layer of this CTA (one launch can cover many)
+    // Work items are (layer, unit) pairs, flattened layer-major. Classic grid
+    // (units x layers): one item per CTA. Persistent grid (batch.persist): CTA
+    // c takes items c, c + grid, ... and the digest ring keeps streaming across
+    // item boundaries, so one item's latency-bound selection phase overlaps
+    // the next item's first digest chunks.
+    const int n_units = batch.a[0].n_units;
+    const long long total_items = static_cast<long long>(n_units) * batch.n;
+    const long long first = batch.persist ? blockIdx.x : static_cast<long long>(blockIdx.y) * n_units + blockIdx.x;
+    const long long stride = batch.persist ? gridDim.x : total_items;
+    const int n_my = first < total_items ? static_cast<int>((total_items - first + stride - 1) / stride) : 0;
     extern __shared__ __align__(16) uint8_t k1_smem[];
-    const size_t ns = static_cast<size_t>(a.nb_stride);
+    const size_t ns = static_cast<size_t>(batch.a[0].nb_stride);
     double* qs = reinterpret_cast<double*>(k1_smem);             // [D][G] stacked order
     float2* pn = reinterpret_cast<float2*>(qs + D * G);          // [D] (sum q>=0, sum q<0) rounded to f32
     uint64_t* keys = reinterpret_cast<uint64_t*>(pn + D);        // [nb_stride]
@@ -350,7 +359,7 @@ __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT
     uint8_t* big = k1_smem + (static_cast<size_t>(D) * G * 8 + D * 8 + ns * 9 + 15) / 16 * 16;
     double* s_acc = reinterpret_cast<double*>(big);              // [nb_stride] (nb_stride > K1_REG_BLOCKS)
     float* a_acc = reinterpret_cast<float*>(s_acc + ns);         // [nb_stride]
-    uint8_t* stagebuf = k1_smem + k1_stage_offset(G, a.nb_stride);  // nbuf x chunk (MODE 0)
+    uint8_t* stagebuf = k1_smem + k1_stage_offset(G, static_cast<int>(ns));  // nbuf x chunk (MODE 0)
     __shared__ uint64_t s_full[K1_MAXBUF];
     __shared__ SelScratch S;
     __shared__ int warp_tot[K1_WARPS];
@@ -358,37 +367,58 @@ __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT
     __shared__ int s_cnt[2];
     __shared__ float s_amax;
 
-    const int u = blockIdx.x;
     const int tid = threadIdx.x;
     const int nbuf = batch.nbuf;
-    const DigT* lo = static_cast<const DigT*>(a.digests) + static_cast<size_t>(u) * 2 * D * ns;
-    const DigT* hi = lo + D * ns;
-    // digest chunk ring: chunks of `cpc` channels (lo rows + hi rows, 16 KiB at
-    // 512 blocks) stream through shared memory with 1-D bulk copies (TMA
-    // engine). The first copies go out before anything else so the query
-    // staging below hides under them.
+    // digest chunk ring: chunks of `cpc` channels (lo rows + hi rows) stream
+    // through shared memory with 1-D bulk copies (TMA engine); global chunk
+    // numbers run across this CTA's items. The first copies go out before
+    // anything else so the query staging hides under them.
     constexpr int esz = static_cast<int>(sizeof(DigT));
     const int cpc = max(1, min(D, batch.chunk / (2 * static_cast<int>(ns) * esz)));
     const int nchunks = (D + cpc - 1) / cpc;
     const uint32_t lo_bytes = static_cast<uint32_t>(cpc * ns * esz);  // one half of a chunk buffer
-    auto issue = [&](int c) {
-        const int ch0 = c * cpc, nch = min(cpc, D - ch0);
+    const long long total_chunks = static_cast<long long>(n_my) * nchunks;
+    // issuer state (thread 0): next global chunk and the item it belongs to
+    long long g_iss = 0;
+    int iss_item = 0, iss_chunk = 0;
+    const DigT* iss_lo = nullptr;
+    auto item_digests = [&](int local) {
+        const long long it = first + static_cast<long long>(local) * stride;
+        const scout_topk_args& ai = batch.a[it / n_units];
+        return static_cast<const DigT*>(ai.digests) + static_cast<size_t>(it % n_units) * 2 * D * ns;
+    };
+    auto issue_next = [&]() {
+        if (iss_chunk == 0) iss_lo = item_digests(iss_item);
+        const int ch0 = iss_chunk * cpc, nch = min(cpc, D - ch0);
         const uint32_t bytes = static_cast<uint32_t>(nch * ns * esz);
-        uint8_t* buf = stagebuf + static_cast<size_t>(c % nbuf) * 2 * lo_bytes;
-        mbar_arrive_expect_tx(&s_full[c % nbuf], 2 * bytes);
-        bulk_g2s(buf, lo + ch0 * ns, bytes, &s_full[c % nbuf]);
-        bulk_g2s(buf + lo_bytes, hi + ch0 * ns, bytes, &s_full[c % nbuf]);
+        const int slot = static_cast<int>(g_iss % nbuf);
+        uint8_t* buf = stagebuf + static_cast<size_t>(slot) * 2 * lo_bytes;
+        mbar_arrive_expect_tx(&s_full[slot], 2 * bytes);
+        bulk_g2s(buf, iss_lo + ch0 * ns, bytes, &s_full[slot]);
+        bulk_g2s(buf + lo_bytes, iss_lo + (D + ch0) * ns, bytes, &s_full[slot]);
+        ++g_iss;
+        if (++iss_chunk == nchunks) {
+            iss_chunk = 0;
+            ++iss_item;
+        }
     };
     if constexpr (MODE == 0) {
         if (tid == 0) {
             for (int i = 0; i < nbuf; ++i) mbar_init(&s_full[i], 1);
             fence_mbar_init();
-            for (int c = 0; c < nbuf && c < nchunks; ++c) issue(c);
+            while (g_iss < nbuf && g_iss < total_chunks) issue_next();
         }
     }
     // PDL: the next kernel may launch now; this one only reads inputs until it
     // publishes its lists (griddep_wait below orders those writes).
     griddep_launch_dependents();
+    long long g_cons = 0;  // chunks consumed (uniform across threads)
+    for (int item = 0; item < n_my; ++item) {
+    const long long it = first + static_cast<long long>(item) * stride;
+    const scout_topk_args& a = batch.a[it / n_units];
+    const int u = static_cast<int>(it % n_units);
+    const DigT* lo = static_cast<const DigT*>(a.digests) + static_cast<size_t>(u) * 2 * D * ns;
+    const DigT* hi = lo + D * ns;
     if (a.scores_out) griddep_wait();
     int ntok = a.n_tokens[u];
     ntok = max(0, min(ntok, a.nb_stride * BS));
@@ -444,10 +474,11 @@ __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT
         for (int q = 0; q < RQ; ++q)
 #pragma unroll
             for (int e = 0; e < 4; ++e) { rs[q][e] = 0.0; ra[q][e] = 0.f; }
-        for (int c = 0; c < nchunks; ++c) {
-            mbar_wait(&s_full[c % nbuf], (c / nbuf) & 1);
+        for (int c = 0; c < nchunks; ++c, ++g_cons) {
+            const int slot = static_cast<int>(g_cons % nbuf);
+            mbar_wait(&s_full[slot], static_cast<uint32_t>((g_cons / nbuf) & 1));
             const int ch0 = c * cpc, nch = min(cpc, D - ch0);
-            const DigT* blo = reinterpret_cast<const DigT*>(stagebuf + static_cast<size_t>(c % nbuf) * 2 * lo_bytes);
+            const DigT* blo = reinterpret_cast<const DigT*>(stagebuf + static_cast<size_t>(slot) * 2 * lo_bytes);
             const DigT* bhi = reinterpret_cast<const DigT*>(reinterpret_cast<const uint8_t*>(blo) + lo_bytes);
             if constexpr (regs) {
 #pragma unroll
@@ -466,8 +497,8 @@ __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT
                     for (int e = 0; e < 4; ++e) { s_acc[e * nq + j] = s4[e]; a_acc[e * nq + j] = a4[e]; }
                 }
             }
-            __syncthreads();  // buffer drained by every thread: refill it
-            if (tid == 0 && c + nbuf < nchunks) issue(c + nbuf);
+            __syncthreads();  // buffer drained by every thread: refill it (possibly with the next item's chunks)
+            if (tid == 0 && g_iss < total_chunks) issue_next();
         }
         float amax = 0.f;
         if constexpr (regs) {
@@ -617,16 +648,18 @@ __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT
             if (a.cpu_tokens) a.cpu_tokens[u] = s_tok[1];
         }
         if (a.done_flag) {
-            // grid-wide completion: the last CTA publishes the flag a
-            // concurrently running K2 polls (ld.acquire) before reading the lists
+            // layer-wide completion: the last item of the layer publishes the
+            // flag a concurrently running K2 polls (ld.acquire) before reading
             __threadfence();
             const unsigned old = atomicAdd(a.done_ctr, 1u);
-            if (old == gridDim.x - 1) {
+            if (old == static_cast<unsigned>(n_units) - 1u) {
                 *a.done_ctr = 0u;
                 __threadfence();
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done_flag), "r"(a.done_token) : "memory");
             }
         }
+    }
+    __syncthreads();  // shared state is reused by the next item
     }
 }
 
@@ -655,9 +688,27 @@ int launch_g(K1Batch& b, cudaStream_t st) {
     }
     const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)), b.nbuf, b.chunk)
                                   : k1_stage_offset(a.group, a.nb_stride);
+    // persistent grid (SCOUT_K1_PERSIST=1): measured slower than the classic
+    // one-item-per-CTA grid at config 3 (0.93 vs 0.86 ms per 64 layers), whose
+    // freshly started CTAs overlap their prologue with other CTAs' selection
+    // phases as well as a continuous ring does; kept opt-in and tested
+    static const bool persist_env = [] {
+        const char* e = getenv("SCOUT_K1_PERSIST");
+        return e ? atoi(e) != 0 : false;
+    }();
     auto go = [&](auto kern) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
-        scout_host::launch(kern, dim3(a.n_units, b.n), dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
+        // persistent grid: resident CTAs x SMs, when the items outnumber them
+        const long long items = static_cast<long long>(a.n_units) * b.n;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K1_THREADS, smem);
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const long long slots = static_cast<long long>(per_sm > 0 ? per_sm : 1) * sms;
+        b.persist = MODE == 0 && persist_env && items > slots;
+        const dim3 grid = b.persist ? dim3(static_cast<unsigned>(slots)) : dim3(a.n_units, b.n);
+        scout_host::launch(kern, grid, dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
     };
     const int ns = a.nb_stride;
     const int qpt = MODE != 0 ? 1 : (ns <= 4 * K1_THREADS ? 1 : (ns <= 8 * K1_THREADS ? 2 : (ns <= K1_REG_BLOCKS ? 4 : 0)));

@@ -177,3 +177,60 @@ def test_topk_empty_unit(cuda):
     rng = np.random.default_rng(5)
     r = _gpu_topk(make_queries(rng, 2, 1), make_digests(rng, 2, 8), [0, 128], 3, 1)
     assert r["n_sel"][0] == 0 and r["n_sel"][1] == 2
+
+
+def test_topk_batch_persistent_grid_matches_single_launches(cuda):
+    """scout_score_topk_split_batch over more (layer, unit) items than resident
+    CTAs, on the persistent grid (SCOUT_K1_PERSIST=1, read once per process:
+    run in a subprocess) and the classic one: every layer's lists equal the
+    one-layer launches bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(__file__)
+    for persist in ("1", "0"):
+        env = dict(os.environ, SCOUT_K1_PERSIST=persist)
+        code = ("import sys; sys.path[:0] = ['../oracle', '..', '.']; "
+                "import test_gpu_topk as t; t._batch_vs_single()")
+        r = subprocess.run([sys.executable, "-c", code], cwd=here, env=env, capture_output=True, text=True,
+                           timeout=300)
+        assert r.returncode == 0, r.stdout + r.stderr
+
+
+def _batch_vs_single():
+    from paper_2603_27138_b200 import _capi as A
+
+    rng = np.random.default_rng(99)
+    L, U, G, nb, k = 3, 700, 4, 96, 16  # 2100 items > 148 x 7 resident CTAs
+    nbs = nbs_for(nb)
+    dev = torch.device("cuda")
+    digs = [torch.from_numpy(make_digests(rng, U, nbs, "perm" if l == 1 else "iid")).to(dev).bfloat16().contiguous()
+            for l in range(L)]
+    qs = [torch.from_numpy(make_queries(rng, U, G, "perm" if l == 1 else "iid")).to(dev) for l in range(L)]
+    nt = torch.from_numpy(rng.integers(64 * 40, 64 * nb + 1, size=U).astype(np.int32)).to(dev)
+    tabs = [torch.from_numpy(np.where(rng.random((U, nbs)) < 0.7, rng.integers(0, 10**6, size=(U, nbs)), -1)
+                             .astype(np.int32)).to(dev) for _ in range(L)]
+    outs = {n: torch.full((L, U, k), -7, dtype=torch.int32, device=dev) for n in ("sel", "rs", "ri", "ci")}
+    cnts = {n: torch.full((L, U), -7, dtype=torch.int32, device=dev) for n in ("ns", "nr", "nc", "rt", "ct")}
+    arr = (A.TopkArgs * L)()
+    for i in range(L):
+        a = arr[i]
+        a.n_units, a.group, a.digest_dtype, a.method, a.k, a.k_stride, a.nb_stride = U, G, A.SCOUT_BF16, 0, k, k, nbs
+        a.q, a.digests, a.n_tokens, a.block_table = qs[i].data_ptr(), digs[i].data_ptr(), nt.data_ptr(), tabs[i].data_ptr()
+        a.sel_ids, a.res_slots, a.res_ids, a.cpu_ids = (outs[n][i].data_ptr() for n in ("sel", "rs", "ri", "ci"))
+        a.n_sel, a.n_res, a.n_cpu, a.res_tokens, a.cpu_tokens = (cnts[n][i].data_ptr() for n in ("ns", "nr", "nc", "rt", "ct"))
+    A.check(A.lib().scout_score_topk_split_batch(arr, L, torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    for i in range(L):
+        r = ops.score_topk_split(qs[i], digs[i], nt, k, G, block_table=tabs[i], k_stride=k)
+        torch.cuda.synchronize()
+        ns_ = r["n_sel"]
+        assert torch.equal(cnts["ns"][i], ns_) and torch.equal(cnts["nr"][i], r["n_res"])
+        assert torch.equal(cnts["rt"][i], r["res_tokens"]) and torch.equal(cnts["ct"][i], r["cpu_tokens"])
+        for u in range(0, U, 7):
+            n = int(ns_[u])
+            assert torch.equal(outs["sel"][i, u, :n], r["sel_ids"][u, :n]), (i, u)
+            nr = int(r["n_res"][u])
+            assert torch.equal(outs["rs"][i, u, :nr], r["res_slots"][u, :nr])
+            assert torch.equal(outs["ci"][i, u, :n - nr], r["cpu_ids"][u, :n - nr])
