@@ -414,7 +414,11 @@ int scout_engine_decode_step_kv(scout_engine* eng, int step, const void* q_true,
                                 const float* cpu_o, const float* cpu_ml, const float* k_new, const float* v_new,
                                 float* out_o, float* out_ml, void* stream);
 /* Device tier mode from pinned HOST buffers (the pipeline of
- * scout_engine_decode_step_host plus h_k_new / h_v_new [L][U][128] f32). */
+ * scout_engine_decode_step_host plus h_k_new / h_v_new [L][U][128] f32).
+ * The step's selection follows the previous step's engine work, not other
+ * work the caller queued on `stream` after it: the engine owns every device
+ * buffer it reads, and the previous step's output copies need not finish
+ * before the next step's selection starts. */
 int scout_engine_decode_step_kv_host(scout_engine* eng, int step, const void* h_q_true, const void* h_q_pred,
                                      const float* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
                                      const float* h_v_new, float* h_out_o, float* h_out_ml, int32_t* h_cpu_ids,

@@ -152,6 +152,7 @@ struct scout_engine {
     cudaEvent_t ev_chunk[RC_SLOTS][MAX_CH] = {};  // post chunk done (post stream)
     cudaEvent_t ev_list[RC_SLOTS][MAX_CH] = {};   // its lists landed (pinned)
     cudaEvent_t ev_post = nullptr, ev_pre = nullptr;
+    bool post_recorded = false;
     cudaStream_t post_s = nullptr;
     int rc_slot_jobs[RC_SLOTS] = {};
     bool rc_stop = false, rc_busy = false;
@@ -525,15 +526,24 @@ struct scout_engine {
         if ((rc = scout_tier_advance(const_cast<int32_t*>(cfg.n_tokens), U, post_s)) != SCOUT_OK) return rc;
         // the next step (planning, K1) follows the bookkeeping
         CU(cudaEventRecord(ev_post, post_s));
+        post_recorded = true;
         CU(cudaStreamWaitEvent(s, ev_post, 0));
         return SCOUT_OK;
     }
 
     // K1 lists of this parity were read by the K2 two steps back: wait for it;
     // inputs recorded on `st` before the step are visible to the K1 stream
+    // Device tier mode: the engine owns every buffer K1 reads, so K1 follows
+    // the previous step's bookkeeping (ev_post) instead of everything queued on
+    // the caller's stream -- in particular not the previous step's output
+    // copies, whose tail would otherwise sit in front of every step.
     int begin_step(cudaStream_t st, int par) {
-        CU(cudaEventRecord(ev_start, st));
-        CU(cudaStreamWaitEvent(k1s, ev_start, 0));
+        if (tier_mode) {
+            if (post_recorded) CU(cudaStreamWaitEvent(k1s, ev_post, 0));
+        } else {
+            CU(cudaEventRecord(ev_start, st));
+            CU(cudaStreamWaitEvent(k1s, ev_start, 0));
+        }
         if (k2_recorded[par]) CU(cudaStreamWaitEvent(k1s, ev_k2[par], 0));
         return SCOUT_OK;
     }
