@@ -64,7 +64,7 @@ namespace tc {
 constexpr int NPAIR = 3;
 constexpr int NC = 2 * NPAIR;               // consumer warps
 constexpr int NCT = NC * 32;                // consumer threads
-constexpr int NTHREADS = NCT + 32;          // + 1 producer / planner warp
+constexpr int NTHREADS = NCT + 64;          // + 1 producer warp + 1 planner warp
 constexpr int NST = 2 * NPAIR;              // ring stages
 constexpr int STAGE_BYTES = 32768;          // one block: K tile (16 KiB) + V tile (16 KiB)
 constexpr int MAXSEG = 64;                  // units touched by one CTA range
@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&sm.plan_full[i], 1);
-            mbar_init(&sm.plan_empty[i], 1);
+            mbar_init(&sm.plan_empty[i], 2);  // the consumers and the producer release a plan
         }
         fence_mbar_init();
     }
@@ -270,10 +270,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
     griddep_launch_dependents();
     __syncthreads();
 
-    if (warp == NC) {
-        // ======================================== planner + producer warp
-        const uint64_t pol = policy_evict_first();
-        const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
+    if (warp == NC + 1) {
+        // ======================================== planner warp: layer L's plan
+        // while the producer still streams layer L-1 (a plan costs a few
+        // dependent global round trips: inline in the producer it left the
+        // ring draining at every layer boundary, ~20% at config 2)
         int j = 0;  // CTA-global block stream index (continues across layers)
         for (int L = 0; L < a.n_layers; ++L) {
             const int b = L & 1;
@@ -286,21 +287,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
             }
             __syncwarp();
             make_plan(a, io, sm.plan[b], j, lane);
+            j += sm.plan[b].nblk;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sm.plan_full[b]);
+        }
+        return;
+    }
+    if (warp == NC) {
+        // ======================================== producer warp (lane 0)
+        if (lane != 0) return;
+        const uint64_t pol = policy_evict_first();
+        const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
+        int j = 0;
+        for (int L = 0; L < a.n_layers; ++L) {
+            const int b = L & 1;
+            const K2Layer& io = a.layers[L];
+            mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
             const int nblk = sm.plan[b].nblk;
-            if (lane == 0) {
-                mbar_arrive(&sm.plan_full[b]);
-                // blocks recalled for this layer one step ago must have landed
-                if (io.recall_token && a.recall_flag) wait_flag(a.recall_flag + L, io.recall_token);
-                for (int f = 0; f < nblk; ++f, ++j) {
-                    const int s = stage_of(j);
-                    if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
-                    mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
-                    bulk_g2s_evict_first(stages + s * STAGE_BYTES,
-                                         pool + static_cast<size_t>(sm.plan[b].blk_slot[f]) * BF16_SLOT_BYTES,
-                                         STAGE_BYTES, &sm.full[s], pol);
-                }
+            // blocks recalled for this layer one step ago must have landed
+            if (io.recall_token && a.recall_flag) wait_flag(a.recall_flag + L, io.recall_token);
+            for (int f = 0; f < nblk; ++f, ++j) {
+                const int s = stage_of(j);
+                if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
+                mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
+                bulk_g2s_evict_first(stages + s * STAGE_BYTES,
+                                     pool + static_cast<size_t>(sm.plan[b].blk_slot[f]) * BF16_SLOT_BYTES,
+                                     STAGE_BYTES, &sm.full[s], pol);
             }
-            j = __shfl_sync(0xffffffffu, j, 0);
+            mbar_arrive(&sm.plan_empty[b]);  // the producer is done reading this plan
         }
         return;
     }
@@ -561,16 +575,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                 }
             }
             if (sg.nseg != 1) {
-                __threadfence();
+                // publish the segment partial: the barrier orders every consumer
+                // thread's stores before thread 0's gpu-scope fence (cumulative),
+                // which precedes the counter update; only one thread fences (a
+                // fence per warp cost an L1 invalidation each: 15% of K2's
+                // stall samples at config 2)
                 named_bar_sync(1, NCT);
                 if (ctid == 0) {
+                    __threadfence();
                     const int old = atomicAdd(&ctr[u], 1);
-                    sm.last_flag = (old == sg.nseg - 1);
+                    const bool last = old == sg.nseg - 1;
+                    if (last) __threadfence();  // acquire: the other segments' partials are visible
+                    sm.last_flag = last;
                 }
                 named_bar_sync(1, NCT);
                 if (sm.last_flag) {
                     // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
-                    __threadfence();
+                    // (partials read with ld.global.cg: L2, never a stale L1 line)
                     finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, sg.cfirst + u, sg.nseg, ctid);
                     if (ctid == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
                 }
@@ -582,11 +603,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
             finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, ctid);
         }
         // layer done in this CTA: release the plan buffer, count the CTA in
-        __threadfence();
+        // (outputs ordered before the counter by the barrier + thread 0's fence)
         named_bar_sync(1, NCT);
         if (ctid == 0) {
             mbar_arrive(&sm.plan_empty[b]);
-            if (a.layer_done) atomicAdd(a.layer_done + L, 1u);
+            if (a.layer_done) {
+                __threadfence();
+                atomicAdd(a.layer_done + L, 1u);
+            }
         }
     }
 }
