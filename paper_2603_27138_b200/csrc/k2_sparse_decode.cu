@@ -79,11 +79,13 @@ struct Seg {
 
 // A layer's work list for this CTA, built by the planner warp one layer ahead
 // (double-buffered), consumed by the consumer warps.
+constexpr int ZMAX = 16;  // units without a resident block this CTA finalizes, listed in the plan
 struct Plan {
     Seg segs[MAXSEG];
     int blk_slot[MAXB];      // resident blocks in stream order: pool slot
     int16_t blk_rows[MAXB];  // valid rows (64, or the open block's fill)
-    int nsegs, nblk, jbase, pad;
+    int zero_units[ZMAX];    // units u == blockIdx.x (mod grid) with no resident block
+    int nsegs, nblk, jbase, nzero;  // nzero > ZMAX: scan n_res instead
 };
 
 struct Smem {
@@ -179,8 +181,19 @@ __device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int j
     const int nunits = a.n_units;
     long long T = 0;
     {
-        int loc = 0;
-        for (int u = lane; u < nunits; u += 32) loc += io.n_res[u];
+        int loc = 0, nz = 0;
+        for (int base = 0; base < nunits; base += 32) {
+            const int u = base + lane;
+            const int n = u < nunits ? io.n_res[u] : 0;
+            loc += n;
+            // units with no resident block that this CTA finalizes (CPU partial or zeros)
+            const bool z = u < nunits && n == 0 && u % static_cast<int>(gridDim.x) == static_cast<int>(blockIdx.x);
+            const unsigned bz = __ballot_sync(0xffffffffu, z);
+            const int pos = nz + __popc(bz & ((1u << lane) - 1u));
+            if (z && pos < ZMAX) P.zero_units[pos] = u;
+            nz += __popc(bz);
+        }
+        if (lane == 0) P.nzero = nz;
 #pragma unroll
         for (int o = 16; o; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
         T = loc;
@@ -226,6 +239,18 @@ __device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int j
     nseg = min(nseg, MAXSEG);
     const int nblk = min(static_cast<int>(hi - lo), MAXB);
     __syncwarp();
+    // the consumers load each segment's query at its start: pull the rows
+    // into L2 now, a layer ahead (one 128-byte line per lane and step)
+    {
+        const int qbytes = a.group * D * (a.q_bf16 ? 2 : 4);
+        const int lines = (qbytes + 127) / 128;
+        for (int i = lane; i < nseg * lines; i += 32) {
+            const int si = i / lines, li = i % lines;
+            const uint8_t* qp = static_cast<const uint8_t*>(io.q) +
+                                static_cast<size_t>(P.segs[si].unit) * qbytes + static_cast<size_t>(li) * 128;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
+        }
+    }
     for (int f = lane; f < nblk; f += 32) {
         int si = 0;
         while (si + 1 < nseg && P.segs[si + 1].f0 <= f) ++si;
@@ -597,10 +622,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                 }
             }
         }
-        // ---- units with no resident block: output = CPU partial (or empty)
-        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-            if (io.n_res[u] != 0) continue;
-            finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, ctid);
+        // ---- units with no resident block: output = CPU partial (or empty),
+        // listed by the planner (no n_res read on this path)
+        if (P.nzero <= ZMAX) {
+            for (int i = 0; i < P.nzero; ++i)
+                finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, P.zero_units[i], parts, 0, 0, ctid);
+        } else {
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                if (io.n_res[u] != 0) continue;
+                finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, ctid);
+            }
         }
         // layer done in this CTA: release the plan buffer, count the CTA in
         // (outputs ordered before the counter by the barrier + thread 0's fence)
