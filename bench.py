@@ -401,9 +401,10 @@ class RefBaseline:
 
 
 def measure_cpu_worker(wl, cfg, seconds=4.0):
-    """The CPU co-attention worker (scout_cpu_partial_attention, AVX-512, all
-    host threads) on this box over the workload's CPU share: each unit attends
-    over cpu_blocks_per_unit block images of the host tier with its G heads.
+    """The CPU co-attention worker (scout_cpu_partial_attention: AMX-BF16 tiles
+    where the CPU has them, else AVX-512; all host threads) on this box over
+    the workload's CPU share: each unit attends over cpu_blocks_per_unit block
+    images of the host tier with its G heads.
     Reports blocks/s and the CPU time one decode step's CPU share would take
     (the GPU step does not wait for it here: the bench pre-stages partials)."""
     from paper_2603_27138_b200 import ops
@@ -415,17 +416,29 @@ def measure_cpu_worker(wl, cfg, seconds=4.0):
     idx = torch.from_numpy(rng.integers(0, hb, size=(U, nc)).astype(np.int64))
     nb = torch.full((U,), nc, dtype=torch.int32)
     q = torch.randn(U * G, D)
-    ops.cpu_partial_attention(wl.host_tier, torch.bfloat16, idx, nb, q, G)  # warm
-    n, t0 = 0, time.time()
-    while time.time() - t0 < seconds:
-        ops.cpu_partial_attention(wl.host_tier, torch.bfloat16, idx, nb, q, G)
-        n += 1
-    dt = time.time() - t0
-    bps = n * U * nc / dt
+
+    def rate(secs):
+        ops.cpu_partial_attention(wl.host_tier, torch.bfloat16, idx, nb, q, G)  # warm
+        n, t0 = 0, time.time()
+        while time.time() - t0 < secs:
+            ops.cpu_partial_attention(wl.host_tier, torch.bfloat16, idx, nb, q, G)
+            n += 1
+        return n * U * nc / (time.time() - t0)
+
+    bps = rate(seconds)
+    kernel = ops.cpu_coattn_kernel(torch.bfloat16)
+    bps_avx = None
+    if kernel == "amx-bf16":  # the AVX-512 fp32 kernel beside it, for reference
+        os.environ["SCOUT_CPU_AMX"] = "0"
+        try:
+            bps_avx = rate(seconds / 4)
+        finally:
+            del os.environ["SCOUT_CPU_AMX"]
     per_step = nc * U * (wl.L - 1)
     return {"blocks_per_s": bps, "threads": os.cpu_count(), "blocks_per_step": per_step,
             "ms_per_step": 1000.0 * per_step / bps, "gb_per_s": bps * ops.slot_bytes(torch.bfloat16) / 1e9,
-            "kernel": "scout_cpu_partial_attention (csrc/cpu_coattn.cpp, AVX-512 fp32)",
+            "kernel": f"scout_cpu_partial_attention (csrc/cpu_coattn.cpp, {kernel})",
+            "blocks_per_s_avx512": bps_avx,
             "note": "CPU share of one step (cpu_blocks_per_unit x units x layers 1..L-1); the bench pre-stages "
                     "the CPU partials, so this is reported beside the GPU step, not inside it"}
 

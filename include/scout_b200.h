@@ -334,11 +334,16 @@ int scout_kv_writeback(const void* kv_pool, int kv_dtype, void* host_tier, long 
  * host_tier + host_index[u*k_stride+i] * slot_bytes (the pool's layout: bf16
  * swizzled tiles or f32 rows), block_rows[u*k_stride+i] valid rows (NULL: 64).
  * Writes o [(u*G+g)][128] normalised and ml [(u*G+g)][2] = (max logit, denom),
- * empty = (0, -inf, 0): K2's CPU-partial input. fp32 arithmetic, AVX-512 when
- * the CPU has it; `threads` workers (0 = all hardware threads).            */
+ * empty = (0, -inf, 0): K2's CPU-partial input. bf16 images on an AMX-BF16
+ * CPU: tile products (q split bf16 hi + lo, P rounded to bf16 as in K2);
+ * otherwise fp32 AVX-512 (SCOUT_CPU_AMX=0 forces this). `threads` workers of
+ * a persistent pool (0 = all hardware threads).                           */
 int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, const int64_t* host_index,
                                 const int32_t* block_rows, const int32_t* n_blocks, int k_stride, const float* q,
                                 int group, float scale, int n_units, float* o, float* ml, int threads);
+/* Which kernel scout_cpu_partial_attention runs for kv_dtype on this CPU now:
+ * 2 = AMX-BF16 tiles, 1 = AVX-512 fp32, 0 = scalar.                        */
+int scout_cpu_coattn_kernel(int kv_dtype);
 
 /* ------------------------------------------------------------- engine --
  * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,

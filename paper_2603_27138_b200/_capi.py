@@ -34,7 +34,7 @@ EXPORTED = (
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv",
-    "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention",
+    "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel",
 )
 
 _vp = C.c_void_p
@@ -128,6 +128,7 @@ def lib() -> C.CDLL:
                                          _vp]
         L.scout_cpu_partial_attention.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, C.c_float,
                                                   C.c_int, _vp, _vp, C.c_int]
+        L.scout_cpu_coattn_kernel.argtypes = [C.c_int]
         L.scout_kv_append.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_score_topk_split.argtypes = [C.POINTER(TopkArgs), _vp]
         L.scout_score_topk_split_batch.argtypes = [C.POINTER(TopkArgs), C.c_int, _vp]

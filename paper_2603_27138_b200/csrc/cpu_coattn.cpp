@@ -1,5 +1,12 @@
 // CPU co-attention worker: the host half of ScoutAttention.
 //
+// Two kernels: on CPUs with AMX-BF16 (Sapphire Rapids and later), bf16 block
+// images go through the tile unit (run_unit_amx: S = K.Q^T and O += P.V as
+// TDPBF16PS tile products, the query split into bf16 hi + lo so scores keep
+// ~16 mantissa bits, P rounded to bf16 as K2 does on the GPU); otherwise, and
+// for f32 images, an AVX-512 fp32 kernel (run_unit). SCOUT_CPU_AMX=0 forces the
+// latter. A persistent thread pool runs the units.
+//
 // Replaces the reference's scalar-double PrecomputeWorker path
 // (proj/include/scout/engine.hpp:88-150, which calls partial_attention,
 // attention.hpp:73-95, on the CPU-side blocks of layer i+1 with the predicted
@@ -12,12 +19,19 @@
 // partials (0, -inf, 0) (attention.hpp:24-36).
 #include <immintrin.h>
 
+#include <sys/syscall.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <limits>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -173,6 +187,383 @@ void run_unit(const Job& j, int u) {
     }
 }
 
+// ---------------------------------------------------------------- AMX path --
+struct alignas(64) TileCfg {
+    uint8_t palette, start_row;
+    uint8_t rsv[14];
+    uint16_t colsb[16];
+    uint8_t rows[16];
+};
+
+// per-thread scratch of the AMX kernel: one chunk of up to CH blocks (~320 KB, L2)
+constexpr int CH = 8;
+struct alignas(64) AmxScratch {
+    uint16_t kb[CH][BS][D];         // K rows, unswizzled (A operand of S = K.Q^T)
+    uint16_t vv[CH][BS / 2][D][2];  // V in VNNI pairs (B operand of O += P.V)
+    float sb[CH][BS][16];           // S: cols 0-7 hi heads, 8-15 lo heads
+    float pf[BS][GMAX];             // one block's P (bf16-exact fp32), token-major
+    uint16_t pa[CH][2][16][32];     // P head-major per 32-token half (A operand; rows >= G zero)
+    float ob[16][D];                // the chunk's P.V (rows >= G zero)
+    float o[GMAX][D];             // running O
+    uint16_t bq[4][16][32];       // Q^T in VNNI, per 32-channel step (hi | lo columns)
+};
+
+// qword permutations: a 128-byte slab row whose 16-byte chunk c sits at
+// position c ^ x -> channel order (x = row & 7), as (first 64 B, second 64 B)
+struct UnswizzleIdx {
+    alignas(64) int64_t lo[8][8], hi[8][8];
+    UnswizzleIdx() {
+        for (int x = 0; x < 8; ++x)
+            for (int q = 0; q < 8; ++q) {
+                lo[x][q] = ((((q >> 1) ^ x) << 1) | (q & 1));
+                hi[x][q] = (((((q + 8) >> 1) ^ x) << 1) | (q & 1));
+            }
+    }
+};
+const UnswizzleIdx kUnsw;
+
+inline uint16_t bf16_rne(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7f800000u) == 0x7f800000u) return static_cast<uint16_t>(u >> 16);  // inf / nan
+    return static_cast<uint16_t>((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+}
+inline float bf16_f(uint16_t h) {
+    const uint32_t u = static_cast<uint32_t>(h) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+#ifdef SCOUT_CPU_PROF
+#include <x86intrin.h>
+thread_local unsigned long long g_prof[8];
+#define PROF_MARK(i) do { _mm_mfence(); const unsigned long long t_ = __rdtsc(); g_prof[i] += t_ - t_prev; t_prev = t_; } while (0)
+#define PROF_START unsigned long long t_prev = __rdtsc()
+#else
+#define PROF_MARK(i) do {} while (0)
+#define PROF_START do {} while (0)
+#endif
+
+#define SCOUT_AMX_TARGET __attribute__((target("amx-tile,amx-bf16,avx512f,avx512bw,avx512bf16")))
+
+// row r of a swizzled bf16 tile -> four zmm of 32 channels each
+SCOUT_AMX_TARGET inline void unswizzle_row(const uint16_t* t, int r, __m512i out[4]) {
+    const int h = r >> 5, rr = r & 31, x = rr & 7;
+    const __m512i il = _mm512_load_si512(kUnsw.lo[x]), ih = _mm512_load_si512(kUnsw.hi[x]);
+    for (int j = 0; j < 2; ++j) {
+        const uint16_t* row = t + ((h * 2 + j) * 32 + rr) * 64;
+        const __m512i a = _mm512_loadu_si512(row), b = _mm512_loadu_si512(row + 32);
+        out[2 * j] = _mm512_permutex2var_epi64(a, il, b);
+        out[2 * j + 1] = _mm512_permutex2var_epi64(a, ih, b);
+    }
+}
+
+// tokens t, t + 1 of a score tile (hi + lo columns) as one vector: lanes 0-7
+// token t, 8-15 token t + 1; rows past the fill -> -inf
+SCOUT_AMX_TARGET inline __m512 score_pair(const float* s0, const float* s1, int t, int rows, __m512i pick_hi,
+                                          __m512i pick_lo, __m512 ninf) {
+    const __m512 a = _mm512_load_ps(s0), c = _mm512_load_ps(s1);
+    const __m512 v = _mm512_add_ps(_mm512_permutex2var_ps(a, pick_hi, c), _mm512_permutex2var_ps(a, pick_lo, c));
+    const __mmask16 ok = static_cast<__mmask16>((t < rows ? 0x00ffu : 0u) | (t + 1 < rows ? 0xff00u : 0u));
+    return _mm512_mask_blend_ps(ok, ninf, v);
+}
+
+SCOUT_AMX_TARGET inline __m512 exp2_ps(__m512 x) {
+    x = _mm512_max_ps(x, _mm512_set1_ps(-200.f));  // -inf -> 0 after scalef
+    const __m512 xi = _mm512_roundscale_ps(x, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
+    const __m512 f = _mm512_sub_ps(x, xi);  // [-0.5, 0.5]
+    __m512 p = _mm512_set1_ps(1.5403530e-4f);
+    p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(1.3333558e-3f));
+    p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(9.6181291e-3f));
+    p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(5.5504109e-2f));
+    p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(2.4022651e-1f));
+    p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(6.9314718e-1f));
+    p = _mm512_fmadd_ps(p, f, _mm512_set1_ps(1.f));
+    return _mm512_scalef_ps(p, xi);
+}
+
+SCOUT_AMX_TARGET void amx_config(int G) {
+    TileCfg c{};
+    c.palette = 1;
+    (void)G;
+    for (int t = 0; t < 8; ++t) { c.rows[t] = 16; c.colsb[t] = 64; }
+    _tile_loadconfig(&c);
+}
+
+// One unit on the tile unit. Scores are in log2 units (the query is scaled by
+// scale * log2(e) before the hi/lo split); the result is K2's CPU-partial
+// format. The blocks go in chunks of up to CH: all of a chunk's operands are
+// staged first (AVX-512), then one tile burst computes every block's S, the
+// softmax runs over the whole chunk (one rescale per chunk), and a second
+// burst accumulates the chunk's P.V in the tile registers. The tile unit pays
+// a wake-up of several hundred cycles after each stretch of vector work, so
+// two bursts per chunk instead of two per block matter (measured: an S burst
+// of 16 tile products costs ~220 TSC back to back, ~900 after 1200 cycles of
+// other work).
+SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
+    const int G = j.G;
+    constexpr float LOG2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
+    // ---- Q^T -> VNNI B tiles: column n < 8 = hi of head n, 8 + n = lo of head n;
+    // a VNNI word is the (2i, 2i+1) channel pair of one column
+    std::memset(w.bq, 0, sizeof(w.bq));
+    const float* qu = j.q + static_cast<size_t>(u) * G * D;
+    const __m512 qs = _mm512_set1_ps(j.scale * LOG2E);
+    const __m512i col = _mm512_mullo_epi32(_mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15),
+                                           _mm512_set1_epi32(16));
+    for (int g = 0; g < G; ++g)
+        for (int ks = 0; ks < 4; ++ks) {
+            const __m512 v0 = _mm512_mul_ps(_mm512_loadu_ps(qu + g * D + 32 * ks), qs);
+            const __m512 v1 = _mm512_mul_ps(_mm512_loadu_ps(qu + g * D + 32 * ks + 16), qs);
+            const __m512i hi = (__m512i)_mm512_cvtne2ps_pbh(v1, v0);
+            const __m512 h0 = _mm512_castsi512_ps(_mm512_slli_epi32(_mm512_cvtepu16_epi32(_mm512_castsi512_si256(hi)), 16));
+            const __m512 h1 = _mm512_castsi512_ps(
+                _mm512_slli_epi32(_mm512_cvtepu16_epi32(_mm512_extracti64x4_epi64(hi, 1)), 16));
+            const __m512i lo = (__m512i)_mm512_cvtne2ps_pbh(_mm512_sub_ps(v1, h1), _mm512_sub_ps(v0, h0));
+            int* base = reinterpret_cast<int*>(w.bq[ks]);
+            _mm512_i32scatter_epi32(base + g, col, hi, 4);
+            _mm512_i32scatter_epi32(base + 8 + g, col, lo, 4);
+        }
+    std::memset(w.o, 0, sizeof(w.o));
+    std::memset(w.pa, 0, sizeof(w.pa));  // rows >= G stay zero
+    const __m512 ninf = _mm512_set1_ps(-std::numeric_limits<float>::infinity());
+    __m512 m = ninf, l = _mm512_setzero_ps();  // lanes g and 8 + g: head g
+    const __m512i pick_hi = _mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 16, 17, 18, 19, 20, 21, 22, 23);
+    const __m512i pick_lo = _mm512_setr_epi32(8, 9, 10, 11, 12, 13, 14, 15, 24, 25, 26, 27, 28, 29, 30, 31);
+    const __m512i vp0 = _mm512_setr_epi64(0, 1, 8, 9, 2, 3, 10, 11);
+    const __m512i vp1 = _mm512_setr_epi64(4, 5, 12, 13, 6, 7, 14, 15);
+    const __m512i gidx = _mm512_mullo_epi32(_mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15),
+                                            _mm512_set1_epi32(GMAX));
+    const int nb = j.n_blocks[u];
+    for (int c0 = 0; c0 < nb; c0 += CH) {
+        const int nc = std::min(CH, nb - c0);
+        int rows[CH];
+        PROF_START;
+        // ---- stage: K rows -> kb, V row pairs -> vv (rows past the fill are
+        // zero: stale bytes may be NaN)
+        for (int b = 0; b < nc; ++b) {
+            const size_t idx = static_cast<size_t>(u) * j.k_stride + c0 + b;
+            const uint16_t* kt =
+                reinterpret_cast<const uint16_t*>(j.host + static_cast<size_t>(j.index[idx]) * j.slot_bytes);
+            const uint16_t* vt = kt + j.slot_bytes / 4;
+            rows[b] = std::max(0, std::min(BS, j.rows ? static_cast<int>(j.rows[idx]) : BS));
+            for (int r = 0; r < BS; ++r) {
+                __m512i z[4];
+                if (r < rows[b]) unswizzle_row(kt, r, z);
+                else z[0] = z[1] = z[2] = z[3] = _mm512_setzero_si512();
+                for (int q = 0; q < 4; ++q) _mm512_store_si512(&w.kb[b][r][32 * q], z[q]);
+            }
+            for (int p = 0; p < BS / 2; ++p) {
+                __m512i a[4], c[4];
+                if (2 * p < rows[b]) unswizzle_row(vt, 2 * p, a);
+                else a[0] = a[1] = a[2] = a[3] = _mm512_setzero_si512();
+                if (2 * p + 1 < rows[b]) unswizzle_row(vt, 2 * p + 1, c);
+                else c[0] = c[1] = c[2] = c[3] = _mm512_setzero_si512();
+                for (int q = 0; q < 4; ++q) {
+                    const __m512i lo = _mm512_unpacklo_epi16(a[q], c[q]), hi = _mm512_unpackhi_epi16(a[q], c[q]);
+                    _mm512_store_si512(&w.vv[b][p][32 * q][0], _mm512_permutex2var_epi64(lo, vp0, hi));
+                    _mm512_store_si512(&w.vv[b][p][32 * q + 16][0], _mm512_permutex2var_epi64(lo, vp1, hi));
+                }
+            }
+        }
+        PROF_MARK(0);
+        // ---- burst 1: S = K . Q^T per block, four 16-token accumulators
+        // (tmm0-3), Q^T two 32-channel steps at a time in tmm6/7, K via tmm4/5
+#define SCOUT_S_STEP(mt, ks, A, QB)                                 \
+    _tile_loadd(A, &w.kb[b][16 * (mt)][32 * (ks)], 2 * D);          \
+    _tile_dpbf16ps(mt, A, QB)
+        for (int b = 0; b < nc; ++b) {
+            _tile_zero(0);
+            _tile_zero(1);
+            _tile_zero(2);
+            _tile_zero(3);
+            for (int kp = 0; kp < 2; ++kp) {
+                _tile_loadd(6, w.bq[2 * kp], 64);
+                _tile_loadd(7, w.bq[2 * kp + 1], 64);
+                SCOUT_S_STEP(0, 2 * kp, 4, 6);
+                SCOUT_S_STEP(1, 2 * kp, 5, 6);
+                SCOUT_S_STEP(2, 2 * kp, 4, 6);
+                SCOUT_S_STEP(3, 2 * kp, 5, 6);
+                SCOUT_S_STEP(0, 2 * kp + 1, 4, 7);
+                SCOUT_S_STEP(1, 2 * kp + 1, 5, 7);
+                SCOUT_S_STEP(2, 2 * kp + 1, 4, 7);
+                SCOUT_S_STEP(3, 2 * kp + 1, 5, 7);
+            }
+            _tile_stored(0, &w.sb[b][0][0], 64);
+            _tile_stored(1, &w.sb[b][16][0], 64);
+            _tile_stored(2, &w.sb[b][32][0], 64);
+            _tile_stored(3, &w.sb[b][48][0], 64);
+        }
+#undef SCOUT_S_STEP
+        PROF_MARK(1);
+        // ---- softmax over the chunk, two tokens per vector (lanes 0-7: token
+        // t, 8-15: t + 1): pass 1 the maximum, pass 2 the bf16-rounded weights
+#define score(b, p) score_pair(w.sb[b][2 * (p)], w.sb[b][2 * (p) + 1], 2 * (p), rows[b], pick_hi, pick_lo, ninf)
+        __m512 mx = ninf;
+        for (int b = 0; b < nc; ++b)
+            for (int p = 0; p < BS / 2; ++p) mx = _mm512_max_ps(mx, score(b, p));
+        mx = _mm512_max_ps(mx, _mm512_shuffle_f32x4(mx, mx, 0x4e));
+        const __m512 mn = _mm512_max_ps(m, mx);
+        const __m512 alpha = exp2_ps(_mm512_sub_ps(m, mn));
+        m = mn;
+        __m512 ls = _mm512_setzero_ps();
+        for (int b = 0; b < nc; ++b) {
+            for (int p = 0; p < BS / 2; ++p) {
+                const __m512 e = exp2_ps(_mm512_sub_ps(score(b, p), mn));
+                // round to bf16 once: the sum uses the same weights the tile product sees
+                const __m512 pr = _mm512_castsi512_ps(
+                    _mm512_slli_epi32(_mm512_cvtepu16_epi32((__m256i)_mm512_cvtneps_pbh(e)), 16));
+                ls = _mm512_add_ps(ls, pr);
+                _mm512_store_ps(&w.pf[2 * p][0], pr);
+            }
+            // P -> head-major bf16 (A operand), one row per head
+            for (int g = 0; g < G; ++g)
+                for (int h = 0; h < 2; ++h) {
+                    const __m512 p0 = _mm512_i32gather_ps(gidx, &w.pf[32 * h][g], 4);
+                    const __m512 p1 = _mm512_i32gather_ps(gidx, &w.pf[32 * h + 16][g], 4);
+                    _mm512_store_si512(w.pa[b][h][g], (__m512i)_mm512_cvtne2ps_pbh(p1, p0));
+                }
+        }
+#undef score
+        ls = _mm512_add_ps(ls, _mm512_shuffle_f32x4(ls, ls, 0x4e));
+        l = _mm512_fmadd_ps(l, alpha, ls);
+        PROF_MARK(2);
+        // ---- burst 2: the chunk's P.V, four 16-channel accumulators (tmm0-3)
+        // per pass over the blocks, P in tmm4/5 (token halves), V via tmm6/7
+#define SCOUT_PV_STEP(c, kt, A, B)                                          \
+    _tile_loadd(B, &w.vv[b][16 * (kt)][16 * (cg0 + (c))][0], D * 4);        \
+    _tile_dpbf16ps(c, A, B)
+        for (int cg0 = 0; cg0 < D / 16; cg0 += 4) {
+            _tile_zero(0);
+            _tile_zero(1);
+            _tile_zero(2);
+            _tile_zero(3);
+            for (int b = 0; b < nc; ++b) {
+                _tile_loadd(4, w.pa[b][0], 64);
+                _tile_loadd(5, w.pa[b][1], 64);
+                SCOUT_PV_STEP(0, 0, 4, 6);
+                SCOUT_PV_STEP(1, 0, 4, 7);
+                SCOUT_PV_STEP(2, 0, 4, 6);
+                SCOUT_PV_STEP(3, 0, 4, 7);
+                SCOUT_PV_STEP(0, 1, 5, 6);
+                SCOUT_PV_STEP(1, 1, 5, 7);
+                SCOUT_PV_STEP(2, 1, 5, 6);
+                SCOUT_PV_STEP(3, 1, 5, 7);
+            }
+            _tile_stored(0, &w.ob[0][16 * cg0], D * 4);
+            _tile_stored(1, &w.ob[0][16 * cg0 + 16], D * 4);
+            _tile_stored(2, &w.ob[0][16 * cg0 + 32], D * 4);
+            _tile_stored(3, &w.ob[0][16 * cg0 + 48], D * 4);
+        }
+#undef SCOUT_PV_STEP
+        PROF_MARK(3);
+        // ---- O = O * alpha + P.V
+        alignas(64) float al[16];
+        _mm512_store_ps(al, alpha);
+        for (int g = 0; g < G; ++g) {
+            const __m512 a = _mm512_set1_ps(al[g]);
+            for (int c = 0; c < D; c += 16)
+                _mm512_store_ps(&w.o[g][c], _mm512_fmadd_ps(a, _mm512_load_ps(&w.o[g][c]), _mm512_load_ps(&w.ob[g][c])));
+        }
+        PROF_MARK(4);
+    }
+    alignas(64) float mm[16], ll[16];
+    _mm512_store_ps(mm, m);
+    _mm512_store_ps(ll, l);
+    for (int g = 0; g < G; ++g) {
+        const size_t h = static_cast<size_t>(u) * G + g;
+        const float inv = ll[g] > 0.f ? 1.f / ll[g] : 0.f;
+        for (int d = 0; d < D; ++d) j.o[h * D + d] = w.o[g][d] * inv;
+        j.ml[h * 2] = ll[g] > 0.f ? mm[g] * LN2 : -std::numeric_limits<float>::infinity();
+        j.ml[h * 2 + 1] = ll[g];
+    }
+}
+
+SCOUT_AMX_TARGET void amx_work(const Job& j, std::atomic<int>& next, int n_units) {
+    static thread_local AmxScratch* scratch = nullptr;
+    if (!scratch) scratch = static_cast<AmxScratch*>(std::aligned_alloc(64, sizeof(AmxScratch)));
+    amx_config(j.G);
+    for (int u; (u = next.fetch_add(1)) < n_units;) run_unit_amx(j, u, *scratch);
+    _tile_release();
+}
+
+// AMX-BF16 present and the kernel granted the tile state (arch_prctl)
+bool amx_ready() {
+    static const int v = [] {
+        if (!__builtin_cpu_supports("avx512bf16")) return 0;
+        unsigned a, b, c, d;
+        __asm__ volatile("cpuid" : "=a"(a), "=b"(b), "=c"(c), "=d"(d) : "a"(7), "c"(0));
+        if (!((d >> 22) & 1u) || !((d >> 24) & 1u)) return 0;  // AMX-BF16, AMX-TILE
+        constexpr long ARCH_REQ_XCOMP_PERM = 0x1023, XFEATURE_XTILEDATA = 18;
+        return syscall(SYS_arch_prctl, ARCH_REQ_XCOMP_PERM, XFEATURE_XTILEDATA) == 0 ? 1 : 0;
+    }();
+    return v != 0;
+}
+
+// ----------------------------------------------------------- thread pool --
+// Persistent workers (a decode step calls the worker once per layer: thread
+// creation per call would cost more than a layer's CPU share).
+class Pool {
+public:
+    void run(int T, const std::function<void()>& fn) {
+        std::lock_guard<std::mutex> call(call_mu_);
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            while (static_cast<int>(workers_.size()) < T - 1) {
+                const int id = static_cast<int>(workers_.size());
+                workers_.emplace_back([this, id] { loop(id); });
+            }
+            fn_ = &fn;
+            want_ = T - 1;
+            pending_ = T - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn();
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+    ~Pool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+private:
+    void loop(int id) {
+        uint64_t seen = 0;
+        for (;;) {
+            const std::function<void()>* fn;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || (gen_ != seen && id < want_); });
+                if (stop_) return;
+                seen = gen_;
+                fn = fn_;
+            }
+            (*fn)();
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::mutex call_mu_, mu_;
+    std::condition_variable cv_, done_;
+    std::vector<std::thread> workers_;
+    const std::function<void()>* fn_ = nullptr;
+    uint64_t gen_ = 0;
+    int want_ = 0, pending_ = 0;
+    bool stop_ = false;
+};
+
+Pool& pool() {
+    static Pool p;
+    return p;
+}
+
 bool has_avx512() {
     static const int v = __builtin_cpu_supports("avx512f") ? 1 : 0;
     return v != 0;
@@ -197,22 +588,27 @@ extern "C" int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, 
     int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
     if (T < 1) T = 1;
     if (T > n_units) T = n_units;
+    const char* env = std::getenv("SCOUT_CPU_AMX");
+    const bool amx = kv_dtype == SCOUT_BF16 && !(env && env[0] == '0') && amx_ready();
     const bool avx = has_avx512();
     std::atomic<int> next{0};
-    auto work = [&] {
+    const std::function<void()> work = [&] {
+        if (amx) {
+            amx_work(j, next, n_units);
+            return;
+        }
         for (int u; (u = next.fetch_add(1)) < n_units;) {
             if (avx) run_unit<true>(j, u);
             else run_unit<false>(j, u);
         }
     };
-    if (T == 1) {
-        work();
-        return SCOUT_OK;
-    }
-    std::vector<std::thread> pool;
-    pool.reserve(T - 1);
-    for (int t = 1; t < T; ++t) pool.emplace_back(work);
-    work();
-    for (auto& th : pool) th.join();
+    if (T == 1) work();
+    else pool().run(T, work);
     return SCOUT_OK;
+}
+
+extern "C" int scout_cpu_coattn_kernel(int kv_dtype) {
+    const char* env = std::getenv("SCOUT_CPU_AMX");
+    if (kv_dtype == SCOUT_BF16 && !(env && env[0] == '0') && amx_ready()) return 2;
+    return has_avx512() ? 1 : 0;
 }

@@ -71,7 +71,6 @@ constexpr int MAXSEG = 64;                  // units touched by one CTA range
 constexpr int MAXB = 384;                   // blocks per CTA range per layer
 constexpr int CB_ROW = D + 4;               // combine rows (bank-conflict pad)
 constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES;
-static_assert(8 * CB_ROW * 4 + 64 <= HALF_BYTES_BF16, "a warp's combine area must fit in its K half");
 
 struct Seg {
     int unit, j0, j1, nseg, cfirst, f0;  // f0: first block of the segment in the layer's CTA list
@@ -94,7 +93,12 @@ struct Smem {
     uint64_t plan_full[2];
     uint64_t plan_empty[2];
     Plan plan[2];
-    int warp_area[NC];   // byte offset of a warp's combine area, -1: no state
+    int warp_area[NC];   // 1: the warp left a state in wstate, -1: no state
+    // per-warp segment states (o^T rows, m, l): in their own area so a warp
+    // hands its ring stage back as soon as its last block is consumed, not
+    // after the 6-warp merge (the held stages used to shrink the ring at
+    // every segment end)
+    alignas(16) float wstate[NC][8 * CB_ROW + 16];
     int last_flag;
 };
 
@@ -494,17 +498,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                     }
                 }
             }
-            // ---- warp state -> its combine area: the K half it read of the pair's
-            // last stage (the partner reads only the other half of that stage)
+            // ---- warp state -> its combine area; the stage goes back right away
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 lp[0] += __shfl_xor_sync(0xffffffffu, lp[0], o);
                 lp[1] += __shfl_xor_sync(0xffffffffu, lp[1], o);
             }
             __syncwarp();
-            const int area = (held >= 0 && any) ? held * STAGE_BYTES + hsel * HALF_BYTES_BF16 : -1;
+            const int area = (held >= 0 && any) ? 1 : -1;
+            if (held >= 0) {  // all lanes are past their last ldmatrix of the stage
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.empty[held]);
+            }
             if (area >= 0) {
-                float* cb = reinterpret_cast<float*>(stages + area);
+                float* cb = sm.wstate[warp];
 #pragma unroll
                 for (int md = 0; md < 8; ++md) {
                     cb[(2 * t) * CB_ROW + 16 * md + g] = oacc[md][0];
@@ -533,16 +540,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                 float M = -CUDART_INF_F;
 #pragma unroll
                 for (int w = 0; w < NC; ++w) {
-                    const int ar = sm.warp_area[w];
-                    if (ar >= 0) M = fmaxf(M, reinterpret_cast<const float*>(stages + ar)[8 * CB_ROW + hh]);
+                    if (sm.warp_area[w] >= 0) M = fmaxf(M, sm.wstate[w][8 * CB_ROW + hh]);
                 }
                 float Lsum = 0.f;
                 float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int w = 0; w < NC; ++w) {
-                    const int ar = sm.warp_area[w];
-                    if (ar < 0) continue;
-                    const float* wb = reinterpret_cast<const float*>(stages + ar);
+                    if (sm.warp_area[w] < 0) continue;
+                    const float* wb = sm.wstate[w];
                     const float l = wb[8 * CB_ROW + 8 + hh];
                     if (!(l > 0.f)) continue;
                     const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
@@ -552,11 +557,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                 }
                 Ms[r] = M; Ls[r] = Lsum; accs[r] = acc;
             }
-            named_bar_sync(1, NCT);  // every combine area read: stages can go back
-            if (held >= 0) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[held]);
-            }
+            named_bar_sync(1, NCT);  // every combine area read before the next segment writes them
 #pragma unroll
             for (int r = 0; r < 2; ++r) {
                 const int idx = ctid + r * NCT;

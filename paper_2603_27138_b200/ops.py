@@ -161,6 +161,11 @@ def sparse_decode(q, pool, kv_dtype, res_slots, res_ids, n_res, n_tokens, group,
     return o, ml
 
 
+def cpu_coattn_kernel(kv_dtype=torch.bfloat16):
+    """The CPU worker's kernel for kv_dtype here: "amx-bf16", "avx512-f32" or "scalar"."""
+    return {2: "amx-bf16", 1: "avx512-f32", 0: "scalar"}[A.lib().scout_cpu_coattn_kernel(dtype_code(kv_dtype))]
+
+
 def merge_partials(a_o, a_ml, b_o, b_ml, out_o=None, out_ml=None):
     n = int(a_o.shape[0])
     out_o = torch.empty_like(a_o) if out_o is None else out_o
