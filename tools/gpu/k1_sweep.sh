@@ -1,6 +1,7 @@
 #!/bin/bash
 # K1 ring depth / chunk size sweep (64-layer batch, config-3 shape)
 OUT=gpurun_out; mkdir -p $OUT
-for nb in 1 2 3 4; do for ch in 8192 16384 32768; do
-  echo "NBUF=$nb CHUNK=$ch: $(SCOUT_K1_NBUF=$nb SCOUT_K1_CHUNK=$ch timeout 120 python tools/debug/time_k1.py 2>&1 | grep batch)"
-done; done
+for cfg in "2 8192" "2 4096" "3 4096" "3 8192" "4 4096" "4 8192" "3 16384" "2 16384"; do
+  set -- $cfg
+  echo "NBUF=$1 CHUNK=$2: $(SCOUT_K1_NBUF=$1 SCOUT_K1_CHUNK=$2 timeout 120 python tools/debug/time_k1.py 2>&1 | grep batch)"
+done
