@@ -181,8 +181,29 @@ struct scout_engine {
     size_t lu(int layer) const { return static_cast<size_t>(layer) * U; }
     int32_t* I(const Buf& b) const { return static_cast<int32_t*>(b.p); }
 
+    // SCOUT_K2_PROF diagnostics: [grid][16] cycle sums (producer: total, plan
+    // waits, free-stage waits, blocks; consumers, summed over the warps: data
+    // waits, Q loads, segment ends, plans + layer ends; combiner: waiting, busy)
+    unsigned long long* k2_prof = nullptr;
+    void report_k2_prof() {
+        std::vector<unsigned long long> h(static_cast<size_t>(grid) * 16);
+        if (cudaMemcpy(h.data(), k2_prof, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+        double s[16] = {0};
+        for (int c = 0; c < grid; ++c)
+            for (int i = 0; i < 16; ++i) s[i] += static_cast<double>(h[static_cast<size_t>(c) * 16 + i]);
+        const double tot = s[0] > 0 ? s[0] : 1.0, nw = 6.0;
+        fprintf(stderr,
+                "[k2 prof] %d CTAs, %.0f blocks/CTA, %.0f cycles/block | producer: plan wait %.1f%%, stage wait "
+                "%.1f%% | consumers: data wait %.1f%%, Q load %.1f%%, segment end %.1f%%, plan+layer end %.1f%% | "
+                "combiner: waiting %.1f%%, busy %.1f%%\n",
+                grid, s[3] / grid, s[0] / (s[3] > 0 ? s[3] : 1), 100 * s[1] / tot, 100 * s[2] / tot,
+                100 * s[4] / nw / tot, 100 * s[5] / nw / tot, 100 * s[6] / nw / tot, 100 * s[7] / nw / tot,
+                100 * s[8] / tot, 100 * s[9] / tot);
+    }
+
     ~scout_engine() {
         stop_recalls();
+        if (k2_prof) cudaFree(k2_prof);
         for (auto& row : ev_chunk)
             for (auto ev : row)
                 if (ev) cudaEventDestroy(ev);
@@ -270,6 +291,7 @@ struct scout_engine {
         a.token = token;
         a.max_ctas = cfg.max_ctas;
         a.q_bf16 = cfg.q_dtype == SCOUT_BF16;
+        a.prof = k2_prof;
         for (int i = 0; i < cfg.layers; ++i)
             a.layers[i] = K2Layer{q[i], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
                                   co[i], cml[i], o[i], ml[i], inflag ? inflag[i] : nullptr, rc_token[i], 0u};
@@ -588,6 +610,11 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     e->G = c.hq / c.hkv;
     e->UG = e->U * e->G;
     e->grid = scout_k2_grid(e->U, c.k, c.max_ctas);
+    if (const char* pe = getenv("SCOUT_K2_PROF"); pe && atoi(pe) != 0) {
+        // diagnostics: K2 cycle accounting, summed over every launch, printed at destroy
+        CU(cudaMalloc(&e->k2_prof, static_cast<size_t>(e->grid) * 16 * sizeof(unsigned long long)));
+        CU(cudaMemset(e->k2_prof, 0, static_cast<size_t>(e->grid) * 16 * sizeof(unsigned long long)));
+    }
     e->nch = (c.layers + e->cfg.chunk_layers - 1) / e->cfg.chunk_layers;
     const size_t lk = static_cast<size_t>(c.layers) * e->U * c.k * 4, lu = static_cast<size_t>(c.layers) * e->U * 4;
     int bad = 0;
@@ -711,6 +738,7 @@ extern "C" int scout_engine_destroy(scout_engine* eng) {
     if (eng) {
         eng->stop_recalls();     // drains the queued recalls first
         cudaDeviceSynchronize();  // flags / copies still reference engine memory
+        if (eng->k2_prof) eng->report_k2_prof();
     }
     delete eng;
     return SCOUT_OK;

@@ -64,7 +64,7 @@ namespace tc {
 constexpr int NPAIR = 3;
 constexpr int NC = 2 * NPAIR;               // consumer warps
 constexpr int NCT = NC * 32;                // consumer threads
-constexpr int NTHREADS = NCT + 64;          // + 1 producer warp + 1 planner warp
+constexpr int NTHREADS = NCT + 96;          // + 1 producer warp + 1 planner warp + 1 combiner warp
 constexpr int NST = 2 * NPAIR;              // ring stages
 constexpr int STAGE_BYTES = 32768;          // one block: K tile (16 KiB) + V tile (16 KiB)
 constexpr int MAXSEG = 64;                  // units touched by one CTA range
@@ -92,14 +92,13 @@ struct Smem {
     uint64_t empty[NST];
     uint64_t plan_full[2];
     uint64_t plan_empty[2];
+    uint64_t seg_full;   // the NC consumer warps left their segment states
+    uint64_t seg_empty;  // the combiner has read them
     Plan plan[2];
     int warp_area[NC];   // 1: the warp left a state in wstate, -1: no state
-    // per-warp segment states (o^T rows, m, l): in their own area so a warp
-    // hands its ring stage back as soon as its last block is consumed, not
-    // after the 6-warp merge (the held stages used to shrink the ring at
-    // every segment end)
+    // per-warp segment states (o^T rows, m, l), merged by the combiner warp
+    // while the consumers go on with the next segment
     alignas(16) float wstate[NC][8 * CB_ROW + 16];
-    int last_flag;
 };
 
 __device__ __forceinline__ int stage_of(int j) { return (j % NPAIR) + NPAIR * ((j / NPAIR) & 1); }
@@ -172,6 +171,80 @@ __device__ void finalize_unit(const float* cpu_o, const float* cpu_ml, float* ou
         if ((idx & 31) == 0) {
             out_ml[head * 2] = L > 0.f ? M * LN2 : -CUDART_INF_F;
             out_ml[head * 2 + 1] = L;
+        }
+    }
+}
+
+// finalize_unit for one warp (the combiner): lane owns channels 4*lane.. of
+// every head, and each phase issues all of its loads before using them, so a
+// unit costs ~2 L2 round trips per partial slot rather than one per head.
+template <int G>
+__device__ void finalize_unit_warp(const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml, int u,
+                                   const float* parts, int first_slot, int nslots, int lane) {
+    const int d0 = lane * 4;
+    float M[G], cm[G], cl[G], L[G];
+    float4 acc[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        M[h] = -CUDART_INF_F; cm[h] = -CUDART_INF_F; cl[h] = 0.f; L[h] = 0.f;
+        acc[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (cpu_ml) {
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            const size_t head = static_cast<size_t>(u) * G + h;
+            cm[h] = cpu_ml[head * 2] * LOG2E;
+            cl[h] = cpu_ml[head * 2 + 1];
+        }
+    }
+    for (int i = 0; i < nslots; ++i) {
+        const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE;
+#pragma unroll
+        for (int h = 0; h < G; ++h) M[h] = fmaxf(M[h], __ldcg(p + h * HEAD_STRIDE + D));
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h)
+        if (cl[h] > 0.f) M[h] = fmaxf(M[h], cm[h]);
+    for (int i = 0; i < nslots; ++i) {
+        const float* p = parts + static_cast<size_t>(first_slot + i) * PART_STRIDE;
+        float pm[G], pl[G];
+        float4 px[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            pm[h] = __ldcg(p + h * HEAD_STRIDE + D);
+            pl[h] = __ldcg(p + h * HEAD_STRIDE + D + 1);
+            px[h] = __ldcg(reinterpret_cast<const float4*>(p + h * HEAD_STRIDE + d0));
+        }
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            if (M[h] == -CUDART_INF_F || !(pl[h] > 0.f)) continue;
+            const float w = pl[h] * exp2f(pm[h] - M[h]);
+            L[h] += w;
+            acc[h].x += w * px[h].x; acc[h].y += w * px[h].y; acc[h].z += w * px[h].z; acc[h].w += w * px[h].w;
+        }
+    }
+    if (cpu_ml) {
+        float4 co[G];
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+            co[h] = *reinterpret_cast<const float4*>(cpu_o + (static_cast<size_t>(u) * G + h) * D + d0);
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            if (M[h] == -CUDART_INF_F || !(cl[h] > 0.f)) continue;
+            const float w = cl[h] * exp2f(cm[h] - M[h]);
+            L[h] += w;
+            acc[h].x += w * co[h].x; acc[h].y += w * co[h].y; acc[h].z += w * co[h].z; acc[h].w += w * co[h].w;
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        const size_t head = static_cast<size_t>(u) * G + h;
+        const float inv = L[h] > 0.f ? 1.f / L[h] : 0.f;
+        *reinterpret_cast<float4*>(out_o + head * D + d0) =
+            make_float4(acc[h].x * inv, acc[h].y * inv, acc[h].z * inv, acc[h].w * inv);
+        if (lane == 0) {
+            out_ml[head * 2] = L[h] > 0.f ? M[h] * LN2 : -CUDART_INF_F;
+            out_ml[head * 2 + 1] = L[h];
         }
     }
 }
@@ -289,8 +362,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&sm.plan_full[i], 1);
-            mbar_init(&sm.plan_empty[i], 2);  // the consumers and the producer release a plan
+            mbar_init(&sm.plan_empty[i], NC + 2);  // every consumer warp, the producer and the combiner release a plan
         }
+        mbar_init(&sm.seg_full, NC);
+        mbar_init(&sm.seg_empty, 1);
         fence_mbar_init();
     }
     // PDL (single-layer launches): inputs from the preceding kernel are
@@ -328,22 +403,187 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
         const uint64_t pol = policy_evict_first();
         const uint8_t* pool = static_cast<const uint8_t*>(a.kv_pool);
         int j = 0;
+        long long t_plan = 0, t_empty = 0;  // SCOUT_K2_PROF: cycles blocked on a plan / a free stage
+        const long long t_start = clock64();
         for (int L = 0; L < a.n_layers; ++L) {
             const int b = L & 1;
             const K2Layer& io = a.layers[L];
+            long long t0 = a.prof ? clock64() : 0;
             mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
-            const int nblk = sm.plan[b].nblk;
             // blocks recalled for this layer one step ago must have landed
             if (io.recall_token && a.recall_flag) wait_flag(a.recall_flag + L, io.recall_token);
+            if (a.prof) t_plan += clock64() - t0;
+            const int nblk = sm.plan[b].nblk;
             for (int f = 0; f < nblk; ++f, ++j) {
                 const int s = stage_of(j);
+                if (a.prof) t0 = clock64();
                 if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
+                if (a.prof) t_empty += clock64() - t0;
                 mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
                 bulk_g2s_evict_first(stages + s * STAGE_BYTES,
                                      pool + static_cast<size_t>(sm.plan[b].blk_slot[f]) * BF16_SLOT_BYTES,
                                      STAGE_BYTES, &sm.full[s], pol);
             }
             mbar_arrive(&sm.plan_empty[b]);  // the producer is done reading this plan
+        }
+        if (a.prof) {
+            unsigned long long* pr = a.prof + blockIdx.x * 16;
+            atomicAdd(pr + 0, static_cast<unsigned long long>(clock64() - t_start));
+            atomicAdd(pr + 1, static_cast<unsigned long long>(t_plan));
+            atomicAdd(pr + 2, static_cast<unsigned long long>(t_empty));
+            atomicAdd(pr + 3, static_cast<unsigned long long>(j));
+        }
+        return;
+    }
+
+    if (warp == NC + 2) {
+        // ======================================== combiner warp: merges each
+        // segment's NC warp states, writes the unit's output (nseg == 1) or its
+        // partial (+ the cross-CTA finalize when last), the units without a
+        // resident block and the layer-done count, off the consumers' path
+        long long k_wait = 0, k_busy = 0, tq = 0;
+        int segidx = 0;
+        for (int L = 0; L < a.n_layers; ++L) {
+            const int b = L & 1;
+            const K2Layer& io = a.layers[L];
+            int* ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(a.workspace) + static_cast<size_t>(L) * a.ws_layer_bytes);
+            float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ctr) + ctr_bytes(nunits));
+            mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
+            const Plan& P = sm.plan[b];
+            for (int si = 0; si < P.nsegs; ++si, ++segidx) {
+                const Seg sg = P.segs[si];
+                const int u = sg.unit;
+                if (a.prof) tq = clock64();
+                mbar_wait(&sm.seg_full, segidx & 1);
+                if (a.prof) { const long long t1 = clock64(); k_wait += t1 - tq; tq = t1; }
+                // lane: channels 4*lane..4*lane+3 of every head
+                const int d0 = lane * 4;
+                float Ms[8], Ls[8];
+                float4 accs[8];
+#pragma unroll
+                for (int hh = 0; hh < 8; ++hh) {
+                    float M = -CUDART_INF_F;
+#pragma unroll
+                    for (int w = 0; w < NC; ++w)
+                        if (sm.warp_area[w] >= 0) M = fmaxf(M, sm.wstate[w][8 * CB_ROW + hh]);
+                    float Lsum = 0.f;
+                    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int w = 0; w < NC; ++w) {
+                        if (sm.warp_area[w] < 0) continue;
+                        const float* wb = sm.wstate[w];
+                        const float l = wb[8 * CB_ROW + 8 + hh];
+                        if (!(l > 0.f)) continue;
+                        const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
+                        Lsum += l * fct;
+                        const float4 x = *reinterpret_cast<const float4*>(wb + hh * CB_ROW + d0);
+                        acc.x += fct * x.x; acc.y += fct * x.y; acc.z += fct * x.z; acc.w += fct * x.w;
+                    }
+                    Ms[hh] = M; Ls[hh] = Lsum; accs[hh] = acc;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sm.seg_empty);  // states read: the consumers may overwrite them
+                // the unit's CPU partial, all heads' loads in flight at once (nseg == 1)
+                float cms[G], cls[G];
+                float4 cos_[G];
+#pragma unroll
+                for (int hh = 0; hh < G; ++hh) {
+                    cms[hh] = -CUDART_INF_F; cls[hh] = 0.f; cos_[hh] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (sg.nseg == 1 && io.cpu_ml) {
+                        const size_t head = static_cast<size_t>(u) * G + hh;
+                        cms[hh] = io.cpu_ml[head * 2] * LOG2E;
+                        cls[hh] = io.cpu_ml[head * 2 + 1];
+                        cos_[hh] = *reinterpret_cast<const float4*>(io.cpu_o + head * D + d0);
+                    }
+                }
+#pragma unroll
+                for (int hh = 0; hh < 8; ++hh) {
+                    if (hh >= G) continue;
+                    const float M = Ms[hh], Lsum = Ls[hh];
+                    const float4 acc = accs[hh];
+                    const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+                    if (sg.nseg == 1) {
+                        // the whole unit is here: merge with the CPU partial and write out
+                        const size_t head = static_cast<size_t>(u) * G + hh;
+                        const float cm = cms[hh], cl = cls[hh];
+                        float Mt = M, wa = 1.f, wb = 0.f, Lt = Lsum;
+                        if (cl > 0.f) {
+                            Mt = fmaxf(M, cm);
+                            wa = Lsum > 0.f ? exp2f(M - Mt) : 0.f;
+                            wb = cl * exp2f(cm - Mt);
+                            Lt = Lsum * wa + wb;
+                        }
+                        const float invt = Lt > 0.f ? 1.f / Lt : 0.f;
+                        float4 res;
+                        if (cl > 0.f) {
+                            const float4 co = cos_[hh];
+                            res = make_float4((acc.x * wa + wb * co.x) * invt, (acc.y * wa + wb * co.y) * invt,
+                                              (acc.z * wa + wb * co.z) * invt, (acc.w * wa + wb * co.w) * invt);
+                        } else {
+                            res = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                        }
+                        *reinterpret_cast<float4*>(io.o + head * D + d0) = res;
+                        if (lane == 0) {
+                            io.ml[head * 2] = Lt > 0.f ? Mt * LN2 : -CUDART_INF_F;
+                            io.ml[head * 2 + 1] = Lt;
+                        }
+                    } else {
+                        // this segment's partial (o normalised, m2, l) -> slot c+u
+                        float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
+                        *reinterpret_cast<float4*>(p + d0) =
+                            make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
+                        if (lane == 0) { p[D] = M; p[D + 1] = Lsum; }
+                    }
+                }
+                if (sg.nseg != 1) {
+                    // publish the partial: __syncwarp orders the lanes' stores
+                    // before lane 0's gpu-scope fence, which precedes the counter
+                    __syncwarp();
+                    int last = 0;
+                    if (lane == 0) {
+                        __threadfence();
+                        const int old = atomicAdd(&ctr[u], 1);
+                        last = old == sg.nseg - 1;
+                        if (last) __threadfence();  // acquire: the other segments' partials are visible
+                    }
+                    last = __shfl_sync(0xffffffffu, last, 0);
+                    if (last) {
+                        // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
+                        // (partials read with ld.global.cg: L2, never a stale L1 line)
+                        finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, sg.cfirst + u, sg.nseg, lane);
+                        if (lane == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
+                    }
+                }
+                if (a.prof) k_busy += clock64() - tq;
+            }
+            if (a.prof) tq = clock64();
+            // ---- units with no resident block: output = CPU partial (or empty),
+            // listed by the planner (no n_res read on this path)
+            if (P.nzero <= ZMAX) {
+                for (int i = 0; i < P.nzero; ++i)
+                    finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, P.zero_units[i], parts, 0, 0, lane);
+            } else {
+                for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                    if (io.n_res[u] != 0) continue;
+                    finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, lane);
+                }
+            }
+            // layer done in this CTA: release the plan buffer, count the CTA in
+            // (the lanes' outputs ordered before the counter by __syncwarp + lane 0's fence)
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&sm.plan_empty[b]);
+                if (a.layer_done) {
+                    __threadfence();
+                    atomicAdd(a.layer_done + L, 1u);
+                }
+            }
+            if (a.prof) k_busy += clock64() - tq;
+        }
+        if (a.prof && lane == 0) {
+            unsigned long long* pr = a.prof + blockIdx.x * 16;
+            atomicAdd(pr + 8, static_cast<unsigned long long>(k_wait));
+            atomicAdd(pr + 9, static_cast<unsigned long long>(k_busy));
         }
         return;
     }
@@ -352,18 +592,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
     const int g = lane >> 2, t = lane & 3;
     const int pair = warp >> 1, hsel = warp & 1;
     const float sl2 = a.scale * LOG2E;
-    const int ctid = tid;  // 0 .. NCT-1
+    // SCOUT_K2_PROF: cycles waiting for data, loading Q, in segment ends, on plans / layer ends
+    long long c_full = 0, c_q = 0, c_end = 0, c_plan = 0, tp = 0;
+    int segidx = 0;  // CTA-global segment count (the state buffer's phase)
     for (int L = 0; L < a.n_layers; ++L) {
         const int b = L & 1;
         const K2Layer& io = a.layers[L];
-        int* ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(a.workspace) + static_cast<size_t>(L) * a.ws_layer_bytes);
-        float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ctr) + ctr_bytes(nunits));
+        if (a.prof) tp = clock64();
         mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
+        if (a.prof) c_plan += clock64() - tp;
         const Plan& P = sm.plan[b];
         const int nsegs = P.nsegs, jbase = P.jbase;
         for (int si = 0; si < nsegs; ++si) {
             const Seg sg = P.segs[si];
             const int u = sg.unit;
+            if (a.prof) tp = clock64();
             // Q^T fragments (hi/lo split), heads >= G are zero
             uint32_t bh[8][2], bl[8][2];
             {
@@ -394,6 +637,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                     }
                 }
             }
+            if (a.prof) { __syncwarp(); c_q += clock64() - tp; }
             float m2[2] = {-CUDART_INF_F, -CUDART_INF_F};
             float lp[2] = {0.f, 0.f};
             float oacc[8][4];
@@ -413,8 +657,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                 const int s = stage_of(jj);
                 held = s;
                 const int valid = min(HALF_ROWS, static_cast<int>(P.blk_rows[f]) - hsel * HALF_ROWS);
+                if (a.prof) tp = clock64();
                 mbar_wait(&sm.full[s], (jj / NST) & 1);
                 __syncwarp();  // lanes may leave the try_wait loop apart: reconverge before .aligned ops
+                if (a.prof) c_full += clock64() - tp;
                 if (valid <= 0) continue;  // open block with one half: the other warp idles
                 any = true;
                 const uint32_t kbase = smem_u32(stages + s * STAGE_BYTES) + hsel * HALF_BYTES_BF16;
@@ -498,7 +744,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                     }
                 }
             }
-            // ---- warp state -> its combine area; the stage goes back right away
+            if (a.prof) tp = clock64();
+            // ---- warp state -> the combiner; the stage goes back right away
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
                 lp[0] += __shfl_xor_sync(0xffffffffu, lp[0], o);
@@ -506,10 +753,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
             }
             __syncwarp();
             const int area = (held >= 0 && any) ? 1 : -1;
-            if (held >= 0) {  // all lanes are past their last ldmatrix of the stage
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sm.empty[held]);
-            }
+            if (held >= 0 && lane == 0) mbar_arrive(&sm.empty[held]);  // all lanes are past their last ldmatrix
+            // the combiner has read the previous segment's states
+            if (segidx > 0) mbar_wait(&sm.seg_empty, (segidx - 1) & 1);
             if (area >= 0) {
                 float* cb = sm.wstate[warp];
 #pragma unroll
@@ -527,123 +773,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
                 }
             }
             if (lane == 0) sm.warp_area[warp] = area;
-            named_bar_sync(1, NCT);
-            // ---- merge the NC warp states (8 heads x 32 lanes x 4 channels)
-            float Ms[2], Ls[2];
-            float4 accs[2];
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int idx = ctid + r * NCT;
-                Ms[r] = -CUDART_INF_F; Ls[r] = 0.f; accs[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (idx >= 256) continue;
-                const int hh = idx >> 5, d0 = (idx & 31) * 4;
-                float M = -CUDART_INF_F;
-#pragma unroll
-                for (int w = 0; w < NC; ++w) {
-                    if (sm.warp_area[w] >= 0) M = fmaxf(M, sm.wstate[w][8 * CB_ROW + hh]);
-                }
-                float Lsum = 0.f;
-                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int w = 0; w < NC; ++w) {
-                    if (sm.warp_area[w] < 0) continue;
-                    const float* wb = sm.wstate[w];
-                    const float l = wb[8 * CB_ROW + 8 + hh];
-                    if (!(l > 0.f)) continue;
-                    const float fct = exp2f(wb[8 * CB_ROW + hh] - M);
-                    Lsum += l * fct;
-                    const float4 x = *reinterpret_cast<const float4*>(wb + hh * CB_ROW + d0);
-                    acc.x += fct * x.x; acc.y += fct * x.y; acc.z += fct * x.z; acc.w += fct * x.w;
-                }
-                Ms[r] = M; Ls[r] = Lsum; accs[r] = acc;
-            }
-            named_bar_sync(1, NCT);  // every combine area read before the next segment writes them
-#pragma unroll
-            for (int r = 0; r < 2; ++r) {
-                const int idx = ctid + r * NCT;
-                if (idx >= 256) continue;
-                const int hh = idx >> 5, d0 = (idx & 31) * 4;
-                const float M = Ms[r], Lsum = Ls[r];
-                const float4 acc = accs[r];
-                const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
-                if (sg.nseg == 1) {
-                    // the whole unit is here: merge with the CPU partial and write out
-                    if (hh >= G) continue;
-                    const size_t head = static_cast<size_t>(u) * G + hh;
-                    float cm = -CUDART_INF_F, cl = 0.f;
-                    if (io.cpu_ml) { cm = io.cpu_ml[head * 2] * LOG2E; cl = io.cpu_ml[head * 2 + 1]; }
-                    float Mt = M, wa = 1.f, wb = 0.f, Lt = Lsum;
-                    if (cl > 0.f) {
-                        Mt = fmaxf(M, cm);
-                        wa = Lsum > 0.f ? exp2f(M - Mt) : 0.f;
-                        wb = cl * exp2f(cm - Mt);
-                        Lt = Lsum * wa + wb;
-                    }
-                    const float invt = Lt > 0.f ? 1.f / Lt : 0.f;
-                    float4 res;
-                    if (cl > 0.f) {
-                        const float4 co = *reinterpret_cast<const float4*>(io.cpu_o + head * D + d0);
-                        res = make_float4((acc.x * wa + wb * co.x) * invt, (acc.y * wa + wb * co.y) * invt,
-                                          (acc.z * wa + wb * co.z) * invt, (acc.w * wa + wb * co.w) * invt);
-                    } else {
-                        res = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-                    }
-                    *reinterpret_cast<float4*>(io.o + head * D + d0) = res;
-                    if ((idx & 31) == 0) {
-                        io.ml[head * 2] = Lt > 0.f ? Mt * LN2 : -CUDART_INF_F;
-                        io.ml[head * 2 + 1] = Lt;
-                    }
-                } else {
-                    // this segment's partial (o normalised, m2, l) -> slot c+u
-                    float* p = parts + (static_cast<size_t>(blockIdx.x) + u) * PART_STRIDE + hh * HEAD_STRIDE;
-                    *reinterpret_cast<float4*>(p + d0) = make_float4(acc.x * inv, acc.y * inv, acc.z * inv, acc.w * inv);
-                    if ((idx & 31) == 0) { p[D] = M; p[D + 1] = Lsum; }
-                }
-            }
-            if (sg.nseg != 1) {
-                // publish the segment partial: the barrier orders every consumer
-                // thread's stores before thread 0's gpu-scope fence (cumulative),
-                // which precedes the counter update; only one thread fences (a
-                // fence per warp cost an L1 invalidation each: 15% of K2's
-                // stall samples at config 2)
-                named_bar_sync(1, NCT);
-                if (ctid == 0) {
-                    __threadfence();
-                    const int old = atomicAdd(&ctr[u], 1);
-                    const bool last = old == sg.nseg - 1;
-                    if (last) __threadfence();  // acquire: the other segments' partials are visible
-                    sm.last_flag = last;
-                }
-                named_bar_sync(1, NCT);
-                if (sm.last_flag) {
-                    // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
-                    // (partials read with ld.global.cg: L2, never a stale L1 line)
-                    finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, sg.cfirst + u, sg.nseg, ctid);
-                    if (ctid == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
-                }
-            }
+            __syncwarp();  // every lane's state stores before lane 0's (release) arrive
+            if (lane == 0) mbar_arrive(&sm.seg_full);
+            ++segidx;
+            if (a.prof) c_end += clock64() - tp;
         }
-        // ---- units with no resident block: output = CPU partial (or empty),
-        // listed by the planner (no n_res read on this path)
-        if (P.nzero <= ZMAX) {
-            for (int i = 0; i < P.nzero; ++i)
-                finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, P.zero_units[i], parts, 0, 0, ctid);
-        } else {
-            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-                if (io.n_res[u] != 0) continue;
-                finalize_unit<G, NCT>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, ctid);
-            }
-        }
-        // layer done in this CTA: release the plan buffer, count the CTA in
-        // (outputs ordered before the counter by the barrier + thread 0's fence)
-        named_bar_sync(1, NCT);
-        if (ctid == 0) {
-            mbar_arrive(&sm.plan_empty[b]);
-            if (a.layer_done) {
-                __threadfence();
-                atomicAdd(a.layer_done + L, 1u);
-            }
-        }
+        // this warp is done with layer L's plan
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sm.plan_empty[b]);
+    }
+    if (a.prof && lane == 0) {
+        unsigned long long* pr = a.prof + blockIdx.x * 16;
+        atomicAdd(pr + 4, static_cast<unsigned long long>(c_full));
+        atomicAdd(pr + 5, static_cast<unsigned long long>(c_q));
+        atomicAdd(pr + 6, static_cast<unsigned long long>(c_end));
+        atomicAdd(pr + 7, static_cast<unsigned long long>(c_plan));
     }
 }
 

@@ -34,6 +34,7 @@ struct K2StepArgs {
     unsigned token;
     int max_ctas;
     int q_bf16;               // queries are bf16 (else f32)
+    unsigned long long* prof; // optional [grid][16] cycle counters (SCOUT_K2_PROF diagnostics)
     K2Layer layers[K2_MAX_LAYERS];
 };
 
