@@ -292,6 +292,11 @@ struct scout_engine {
         a.max_ctas = cfg.max_ctas;
         a.q_bf16 = cfg.q_dtype == SCOUT_BF16;
         a.prof = k2_prof;
+        static const int l2pf = [] {
+            const char* e = getenv("SCOUT_K2_L2PF");
+            return e ? atoi(e) : 0;
+        }();
+        a.l2_prefetch = l2pf;
         for (int i = 0; i < cfg.layers; ++i)
             a.layers[i] = K2Layer{q[i], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
                                   co[i], cml[i], o[i], ml[i], inflag ? inflag[i] : nullptr, rc_token[i], 0u};
@@ -434,7 +439,9 @@ struct scout_engine {
         int rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(tier_dev.p), L, U, nbs, cfg.n_tokens, step,
                                         I(plan_tab), s);
         if (rc != SCOUT_OK) return rc;
+        if (ph_ev[0]) cudaEventRecord(ph_ev[0], s);
         if ((rc = select_batch(0, L, q_true, q_pred, step, par, s)) != SCOUT_OK) return rc;
+        if (ph_ev[1]) cudaEventRecord(ph_ev[1], s);
         for (int i = 0; i < L; ++i) {
             if (pending[i] < 0 || pending[i] > tick(step, i)) continue;
             ++launches;
@@ -455,6 +462,7 @@ struct scout_engine {
     //    The next step's K2 waits for a layer's flag before streaming it.
     // `pre`: an event recorded on the step's stream after phases 1-3 (before K2).
     static constexpr int POST_CH = 8;
+    cudaEvent_t ph_ev[2] = {};  // SCOUT_ENGINE_PHASES: after the plan, after K1
     int tier_post(int step, int par, unsigned tok, const float* k_new, const float* v_new, cudaEvent_t pre,
                   cudaStream_t s) {
         const int L = cfg.layers, nbs = cfg.nb_stride;
@@ -941,8 +949,11 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
     // debug: SCOUT_ENGINE_PHASES=1 prints per-phase device times (synchronises)
     static const bool phases = getenv("SCOUT_ENGINE_PHASES") != nullptr;
     cudaEvent_t pe[4] = {};
-    if (phases)
+    if (phases) {
         for (auto& ev : pe) cudaEventCreate(&ev);
+        for (auto& ev : e->ph_ev)
+            if (!ev) cudaEventCreate(&ev);
+    }
     if (phases) cudaEventRecord(pe[0], st);
     // 1-3. planning view, select + split + mark, begin_layer's ticket application
     if ((rc = e->tier_pre(step, par, q_true, q_pred, st)) != SCOUT_OK) return rc;
@@ -967,9 +978,12 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
     if (phases) {
         cudaEventRecord(pe[3], st);
         cudaEventSynchronize(pe[3]);
-        float t[3];
+        float t[3], tp = 0.f, tk = 0.f;
         for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&t[i], pe[i], pe[i + 1]);
-        fprintf(stderr, "step %d: plan+K1+apply %.3f K2 %.3f post tail %.3f ms\n", step, t[0], t[1], t[2]);
+        cudaEventElapsedTime(&tp, pe[0], e->ph_ev[0]);
+        cudaEventElapsedTime(&tk, e->ph_ev[0], e->ph_ev[1]);
+        fprintf(stderr, "step %d: plan %.3f K1 %.3f apply %.3f K2 %.3f post tail %.3f ms\n", step, tp, tk,
+                t[0] - tp - tk, t[1], t[2]);
         for (auto& ev : pe) cudaEventDestroy(ev);
     }
     return SCOUT_OK;

@@ -346,8 +346,15 @@ __device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int j
     __syncwarp();
 }
 
+// Register cap: a warp's registers come from its SM sub-partition's 16K file
+// (warp w -> SMSP w % 4), and with nine warps SMSP 0 hosts three of them. At
+// the 168 registers ptxas picks by itself, SMSP 0 had 256 registers left and
+// no 4-warp kernel (the tier bookkeeping that runs beside K2 on the post
+// stream) could launch next to K2 until it exited: the recalls then landed a
+// step late and K2 waited for them (tier mode 6.05 -> 7.1 ms per step). 144
+// leaves room for two 32-register warps on SMSP 0 and does not spill.
 template <int G>
-__global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2StepArgs a) {
+__global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
     extern __shared__ __align__(1024) uint8_t dsmem[];
     __shared__ Smem sm;
     uint8_t* stages = dsmem;
@@ -414,8 +421,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) sparse_decode_tc_kernel(const K2S
             if (io.recall_token && a.recall_flag) wait_flag(a.recall_flag + L, io.recall_token);
             if (a.prof) t_plan += clock64() - t0;
             const int nblk = sm.plan[b].nblk;
+            // L2 prefetch runs K2_PF blocks ahead of the ring: the ring's 6
+            // stages alone keep ~4 us of this SM's share of HBM bandwidth in
+            // flight, which the loaded latency eats (SCOUT_K2_PROF: producer on
+            // a full ring while the consumers wait for data)
+            const int pf = a.l2_prefetch;
+            for (int f = 0; f < min(pf, nblk); ++f)
+                bulk_prefetch_l2(pool + static_cast<size_t>(sm.plan[b].blk_slot[f]) * BF16_SLOT_BYTES, STAGE_BYTES);
             for (int f = 0; f < nblk; ++f, ++j) {
                 const int s = stage_of(j);
+                if (f + pf < nblk)
+                    bulk_prefetch_l2(pool + static_cast<size_t>(sm.plan[b].blk_slot[f + pf]) * BF16_SLOT_BYTES,
+                                     STAGE_BYTES);
                 if (a.prof) t0 = clock64();
                 if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
                 if (a.prof) t_empty += clock64() - t0;

@@ -35,6 +35,7 @@ struct K2StepArgs {
     int max_ctas;
     int q_bf16;               // queries are bf16 (else f32)
     unsigned long long* prof; // optional [grid][16] cycle counters (SCOUT_K2_PROF diagnostics)
+    int l2_prefetch;          // blocks the producer prefetches into L2 ahead of the ring (0: none)
     K2Layer layers[K2_MAX_LAYERS];
 };
 

@@ -37,15 +37,32 @@ __global__ void gather(const uint8_t* src, const long long* off, int n_per_cta, 
     if (acc == 1234.5f) out[0] = acc;
 }
 template <int NST, int PIECES, int PB>
-int run(const uint8_t* src, size_t bytes, bool random, int sms, float* dout, const char* name) {
+int run(const uint8_t* src, size_t bytes, int mode, int sms, float* dout, const char* name) {
+    // mode 0: random slots; 1: sequential; 2: unit-clustered (each CTA walks
+    // units of 512 contiguous slots = 16 MB, taking 64 random slots of each in
+    // ascending order: K2's access pattern if a unit's blocks were allocated
+    // together)
     const int per = 200;  // items per CTA
     const int grid = sms;
     const int nitems = grid * per;
     std::vector<long long> off((size_t)nitems * PIECES);
     std::mt19937_64 rng(1);
     const long long nslots = bytes / 32768;
+    std::vector<long long> unit_slots;
     for (int i = 0; i < nitems; ++i) {
-        long long slot = random ? (long long)(rng() % nslots) : (long long)i % nslots;
+        long long slot;
+        if (mode == 2) {
+            if (i % 64 == 0) {  // next unit: 64 of its 512 slots, ascending
+                const long long base = (long long)(rng() % (nslots / 512)) * 512;
+                std::vector<char> pick(512, 0);
+                for (int c = 0; c < 64;) { int r = (int)(rng() % 512); if (!pick[r]) { pick[r] = 1; ++c; } }
+                unit_slots.clear();
+                for (int r = 0; r < 512; ++r) if (pick[r]) unit_slots.push_back(base + r);
+            }
+            slot = unit_slots[i % 64];
+        } else {
+            slot = mode == 0 ? (long long)(rng() % nslots) : (long long)i % nslots;
+        }
         for (int p = 0; p < PIECES; ++p) off[(size_t)i * PIECES + p] = slot * 32768 + (long long)p * (PIECES == 2 ? 16384 : PB);
     }
     long long* doff; CK(cudaMalloc(&doff, off.size() * 8)); CK(cudaMemcpy(doff, off.data(), off.size() * 8, cudaMemcpyHostToDevice));
@@ -64,12 +81,14 @@ int main() {
     size_t bytes = (size_t)40 << 30;
     uint8_t* src; CK(cudaMalloc(&src, bytes)); CK(cudaMemset(src, 1, bytes));
     float* dout; CK(cudaMalloc(&dout, 64));
-    run<13, 2, 8192>(src, bytes, true, sms, dout, "random slot, K+V halves (2x8KB)");
-    run<13, 2, 8192>(src, bytes, false, sms, dout, "sequential slot, K+V halves");
-    run<13, 1, 16384>(src, bytes, true, sms, dout, "random 16KB contiguous");
-    run<6, 1, 32768>(src, bytes, true, sms, dout, "random 32KB contiguous");
-    run<26, 1, 8192>(src, bytes, true, sms, dout, "random 8KB");
-    run<13, 4, 4096>(src, bytes, true, sms, dout, "random 4x4KB");
-    run<12, 1, 16384>(src, bytes, false, sms, dout, "sequential 16KB");
+    run<13, 2, 8192>(src, bytes, 0, sms, dout, "random slot, K+V halves (2x8KB)");
+    run<13, 2, 8192>(src, bytes, 1, sms, dout, "sequential slot, K+V halves");
+    run<13, 1, 16384>(src, bytes, 0, sms, dout, "random 16KB contiguous");
+    run<6, 1, 32768>(src, bytes, 0, sms, dout, "random 32KB contiguous");
+    run<6, 1, 32768>(src, bytes, 2, sms, dout, "unit-clustered 32KB (64 of 512)");
+    run<6, 1, 32768>(src, bytes, 1, sms, dout, "sequential 32KB");
+    run<26, 1, 8192>(src, bytes, 0, sms, dout, "random 8KB");
+    run<13, 4, 4096>(src, bytes, 0, sms, dout, "random 4x4KB");
+    run<12, 1, 16384>(src, bytes, 1, sms, dout, "sequential 16KB");
     return 0;
 }
