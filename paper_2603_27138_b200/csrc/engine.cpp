@@ -148,7 +148,7 @@ struct scout_engine {
     static constexpr int RC_SLOTS = 4;
     uint8_t* rc_pinned = nullptr;  // RC_SLOTS x (ids [L][U][k] | n [L][U] | dst [L][U][k]) int32
     size_t rc_slot_bytes = 0;
-    static constexpr int MAX_CH = (K2_MAX_LAYERS + 7) / 8;
+    static constexpr int MAX_CH = (K2_MAX_LAYERS + 7) / 8 + 1;  // post chunks (+ the short tail chunk)
     cudaEvent_t ev_chunk[RC_SLOTS][MAX_CH] = {};  // post chunk done (post stream)
     cudaEvent_t ev_list[RC_SLOTS][MAX_CH] = {};   // its lists landed (pinned)
     cudaEvent_t ev_post = nullptr, ev_pre = nullptr;
@@ -433,20 +433,37 @@ struct scout_engine {
     //    (step, i-1) == at step start: the step's later ops touch other layers);
     // 2. select + split + mark_selected for every layer (one launch);
     // 3. begin_layer: tickets due at (step, i), applied after the marks
+    //    The planning view is usually written already: the previous step's
+    //    post-attention launches compute it for `step` as each layer's
+    //    bookkeeping ends (planned_step); a step number out of sequence (or the
+    //    first step) plans here.
+    int planned_step = -1;
     int tier_pre(int step, int par, const void* q_true, const void* q_pred, cudaStream_t s) {
         const int L = cfg.layers, nbs = cfg.nb_stride;
-        ++launches;
-        int rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(tier_dev.p), L, U, nbs, cfg.n_tokens, step,
-                                        I(plan_tab), s);
-        if (rc != SCOUT_OK) return rc;
+        int rc;
+        if (planned_step != step) {
+            ++launches;
+            if ((rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(tier_dev.p), L, U, nbs, cfg.n_tokens,
+                                             step, I(plan_tab), s)) != SCOUT_OK)
+                return rc;
+        }
         if (ph_ev[0]) cudaEventRecord(ph_ev[0], s);
         if ((rc = select_batch(0, L, q_true, q_pred, step, par, s)) != SCOUT_OK) return rc;
         if (ph_ev[1]) cudaEventRecord(ph_ev[1], s);
+        TierApplyArgs ap{};
+        ap.layers = static_cast<const scout_tier_layer*>(tier_dev.p);
+        ap.nbs = nbs;
+        ap.n_tokens = cfg.n_tokens;
         for (int i = 0; i < L; ++i) {
             if (pending[i] < 0 || pending[i] > tick(step, i)) continue;
-            ++launches;
-            if ((rc = scout_tier_apply(&tier[i], U, nbs, cfg.n_tokens, tick(step, i), nullptr, s)) != SCOUT_OK) return rc;
+            ap.layer[ap.n] = i;
+            ap.due_tick[ap.n] = tick(step, i);
+            ++ap.n;
             pending[i] = -1;
+        }
+        if (ap.n > 0) {  // every due layer in one launch (independent layer states)
+            ++launches;
+            if ((rc = scout_tier_apply_layers(ap, U, s)) != SCOUT_OK) return rc;
         }
         return SCOUT_OK;
     }
@@ -461,7 +478,7 @@ struct scout_engine {
     //    issuer thread builds the descriptors) or the SM gather (recall_mode 1).
     //    The next step's K2 waits for a layer's flag before streaming it.
     // `pre`: an event recorded on the step's stream after phases 1-3 (before K2).
-    static constexpr int POST_CH = 8;
+    static constexpr int POST_CH = 8, POST_TAIL = 2;
     cudaEvent_t ph_ev[2] = {};  // SCOUT_ENGINE_PHASES: after the plan, after K1
     int tier_post(int step, int par, unsigned tok, const float* k_new, const float* v_new, cudaEvent_t pre,
                   cudaStream_t s) {
@@ -486,6 +503,8 @@ struct scout_engine {
         pa.dst = I(tier_dst);
         for (int i = 0; i < L; ++i)
             pa.recall_due[i] = cfg.recall_interval > 0 && (step + i) % cfg.recall_interval == 0;
+        pa.plan_out = I(plan_tab);  // the next step's planning view (K1 of this step has read its own)
+        pa.plan_step = step + 1;
         const bool ce = cfg.recall_mode == 0 && rc_pinned != nullptr;
         const int slot = static_cast<int>(tok % RC_SLOTS);
         if (ce) {  // this step's list slot must be free (the issuer thread is done with it)
@@ -497,8 +516,10 @@ struct scout_engine {
         int32_t* hd = ce ? hn + static_cast<size_t>(L) * U : nullptr;
         CU(cudaStreamWaitEvent(post_s, pre, 0));
         int rc;
-        for (int c = 0, lo = 0; lo < L; ++c, lo += POST_CH) {
-            const int n = lo + POST_CH > L ? L - lo : POST_CH;
+        // chunks of POST_CH layers, the last one only POST_TAIL long: it runs
+        // after K2 has ended, on the critical path to the next step
+        for (int c = 0, lo = 0, n = 0; lo < L; ++c, lo += n) {
+            n = L - lo <= POST_TAIL ? L - lo : std::min(POST_CH, L - lo - POST_TAIL);
             if ((rc = wait_value(post_s, layer_done + lo + n - 1, tok * static_cast<unsigned>(grid))) != SCOUT_OK)
                 return rc;
             pa.layer0 = lo;
@@ -554,6 +575,7 @@ struct scout_engine {
         }
         ++launches;
         if ((rc = scout_tier_advance(const_cast<int32_t*>(cfg.n_tokens), U, post_s)) != SCOUT_OK) return rc;
+        planned_step = step + 1;
         // the next step (planning, K1) follows the bookkeeping
         CU(cudaEventRecord(ev_post, post_s));
         post_recorded = true;

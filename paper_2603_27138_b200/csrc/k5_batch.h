@@ -22,12 +22,24 @@ struct TierPostArgs {
     const int32_t* cpu_ids;          // [L][U][k] K1's CPU-side ids of this step
     const int32_t* n_cpu;            // [L][U]
     int32_t* dst;                    // [L][U][k] recall destination slots
+    int32_t* plan_out;               // optional [L][U][nbs]: the planning view of step plan_step,
+    int plan_step;                   //   written once the layer's bookkeeping is done
     uint8_t recall_due[K5_MAX_LAYERS];
+};
+
+// begin_layer's ticket application for several layers in one launch
+struct TierApplyArgs {
+    const scout_tier_layer* layers;  // device array [n_layers]
+    int nbs, n;
+    const int32_t* n_tokens;
+    int layer[K5_MAX_LAYERS];        // the layers with a ticket due
+    int due_tick[K5_MAX_LAYERS];
 };
 
 int scout_tier_plan_layers(const scout_tier_layer* layers_dev, int n_layers, int n_units, int nb_stride,
                            const int32_t* n_tokens, int step, int32_t* tables, cudaStream_t st);
 // post-attention bookkeeping of layers [a.layer0, a.layer0 + n_layers_launch)
 int scout_tier_post_layers(const TierPostArgs& a, int n_units, int n_layers_launch, cudaStream_t st);
+int scout_tier_apply_layers(const TierApplyArgs& a, int n_units, cudaStream_t st);
 // n_tokens += 1 once every layer has appended
 int scout_tier_advance(int32_t* n_tokens, int n_units, cudaStream_t st);

@@ -163,10 +163,8 @@ __global__ void __launch_bounds__(TT) tier_append_kernel(const scout_tier_layer 
 // begin_layer's application for one layer (kv_store.hpp:201-218): every
 // in-flight block whose ready tick <= due_tick becomes fast; tickets are
 // applied in issue order (ticket number), each followed by enforce_capacity.
-__global__ void __launch_bounds__(TT) tier_apply_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
-                                                        int due_tick, int32_t* n_applied) {
-    __shared__ TierSm S;
-    const int u = blockIdx.x;
+__device__ void apply_unit(const scout_tier_layer& L, int u, int nbs, const int32_t* n_tokens, int due_tick,
+                           int32_t* n_applied, TierSm& S) {
     Unit U = unit_of(L, u, nbs);
     const int ntok = n_tokens[u];
     const int nb = min(n_blocks_of(ntok), nbs);
@@ -191,6 +189,12 @@ __global__ void __launch_bounds__(TT) tier_apply_kernel(const scout_tier_layer L
         enforce_capacity(L, U, nb, ntok, S);
     }
     if (threadIdx.x == 0 && n_applied) n_applied[u] = applied;
+}
+
+__global__ void __launch_bounds__(TT) tier_apply_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
+                                                        int due_tick, int32_t* n_applied) {
+    __shared__ TierSm S;
+    apply_unit(L, blockIdx.x, nbs, n_tokens, due_tick, n_applied, S);
 }
 
 // schedule_recall (kv_store.hpp:175-197): ids must be sealed, slow and not in
@@ -450,6 +454,9 @@ __global__ void __launch_bounds__(TT) tier_plan_layers_kernel(const scout_tier_l
     }
 }
 
+__device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Unit& U, int u, int l, int pos, int n,
+                            TierSm& S);
+
 // After the step's attention, per (unit, layer): append the token (open /
 // seal + enforce_capacity, row write, digest fold), write a sealed block
 // through to the host tier, and when the layer is due, schedule the recall of
@@ -523,9 +530,31 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
         enforce_capacity(L, U, id + 1, pos + 1, S);
     }
     // ---- recall of the layer's CPU-side selected blocks (tier_recall_kernel's logic)
-    if (!a.recall_due[l]) return;
-    const int n = a.n_cpu[static_cast<size_t>(l) * gridDim.x + u];
-    if (n <= 0) return;
+    const int n = a.recall_due[l] ? a.n_cpu[static_cast<size_t>(l) * gridDim.x + u] : 0;
+    if (n > 0) post_recall(a, L, U, u, l, pos, n, S);
+    // ---- the layer's planning view for the next step (tier_plan_layers_kernel's
+    // logic): nothing touches this layer's state between here and that step's
+    // plan, so the view is the same and the step need not wait for a plan launch
+    if (a.plan_out) {
+        __syncthreads();  // this CTA's append / seal / eviction / recall writes first
+        const size_t o = static_cast<size_t>(u) * a.nbs;
+        const int nbn = min(n_blocks_of(pos + 1), a.nbs);
+        const int next_tick = a.plan_step * a.n_layers + l;
+        int32_t* out = a.plan_out + static_cast<size_t>(l) * gridDim.x * a.nbs + o;
+        for (int b = c; b < a.nbs; b += TT) {
+            int v = -1;
+            if (b < nbn) {
+                const int rd = L.ready[o + b];
+                if (L.tier[o + b] || (rd >= 0 && rd <= next_tick)) v = L.table[o + b];
+            }
+            out[b] = v;
+        }
+    }
+}
+
+__device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Unit& U, int u, int l, int pos, int n,
+                            TierSm& S) {
+    const int c = threadIdx.x;
     const int ntok = pos + 1;  // after this step's append
     const int nb = min(n_blocks_of(ntok), a.nbs);
     const int32_t* my = a.cpu_ids + (static_cast<size_t>(l) * gridDim.x + u) * a.k;
@@ -564,6 +593,12 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
     }
 }
 
+__global__ void __launch_bounds__(TT) tier_apply_layers_kernel(const TierApplyArgs a) {
+    __shared__ TierSm S;
+    const int l = a.layer[blockIdx.y];
+    apply_unit(a.layers[l], blockIdx.x, a.nbs, a.n_tokens, a.due_tick[blockIdx.y], nullptr, S);
+}
+
 __global__ void advance_tokens_kernel(int32_t* n_tokens, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) n_tokens[i] += 1;
@@ -581,6 +616,12 @@ int scout_tier_plan_layers(const scout_tier_layer* layers_dev, int n_layers, int
 int scout_tier_post_layers(const TierPostArgs& a, int n_units, int n_layers_launch, cudaStream_t st) {
     tier_post_layers_kernel<<<dim3(n_units, n_layers_launch), TT, 0, st>>>(a);
     return scout_host::check_launch("tier post-attention");
+}
+
+int scout_tier_apply_layers(const TierApplyArgs& a, int n_units, cudaStream_t st) {
+    if (a.n <= 0) return SCOUT_OK;
+    tier_apply_layers_kernel<<<dim3(n_units, a.n), TT, 0, st>>>(a);
+    return scout_host::check_launch("tier apply (due layers)");
 }
 
 int scout_tier_advance(int32_t* n_tokens, int n_units, cudaStream_t st) {
