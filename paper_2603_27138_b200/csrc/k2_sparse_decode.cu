@@ -387,10 +387,13 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
         // dependent global round trips: inline in the producer it left the
         // ring draining at every layer boundary, ~20% at config 2)
         int j = 0;  // CTA-global block stream index (continues across layers)
+        long long w_empty = 0, w_plan = 0, tq = 0;  // SCOUT_K2_PROF: waiting for a free plan buffer, planning
         for (int L = 0; L < a.n_layers; ++L) {
             const int b = L & 1;
             const K2Layer& io = a.layers[L];
+            if (a.prof) tq = clock64();
             if (L >= 2) mbar_wait(&sm.plan_empty[b], ((L >> 1) - 1) & 1);
+            if (a.prof) { const long long t1 = clock64(); w_empty += t1 - tq; tq = t1; }
             if (lane == 0) {
                 // K1 published layer L's lists / the layer's inputs landed
                 if (a.k1_flag) wait_flag(a.k1_flag + L, a.token);
@@ -401,6 +404,12 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             j += sm.plan[b].nblk;
             __syncwarp();
             if (lane == 0) mbar_arrive(&sm.plan_full[b]);
+            if (a.prof) w_plan += clock64() - tq;
+        }
+        if (a.prof && lane == 0) {
+            unsigned long long* pr = a.prof + blockIdx.x * 16;
+            atomicAdd(pr + 10, static_cast<unsigned long long>(w_empty));
+            atomicAdd(pr + 11, static_cast<unsigned long long>(w_plan));
         }
         return;
     }
@@ -475,10 +484,10 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                 if (a.prof) { const long long t1 = clock64(); k_wait += t1 - tq; tq = t1; }
                 // lane: channels 4*lane..4*lane+3 of every head
                 const int d0 = lane * 4;
-                float Ms[8], Ls[8];
-                float4 accs[8];
+                float Ms[G], Ls[G];
+                float4 accs[G];
 #pragma unroll
-                for (int hh = 0; hh < 8; ++hh) {
+                for (int hh = 0; hh < G; ++hh) {  // heads >= G carry nothing
                     float M = -CUDART_INF_F;
 #pragma unroll
                     for (int w = 0; w < NC; ++w)
@@ -514,8 +523,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                     }
                 }
 #pragma unroll
-                for (int hh = 0; hh < 8; ++hh) {
-                    if (hh >= G) continue;
+                for (int hh = 0; hh < G; ++hh) {
                     const float M = Ms[hh], Lsum = Ls[hh];
                     const float4 acc = accs[hh];
                     const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;

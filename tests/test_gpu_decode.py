@@ -192,3 +192,32 @@ def test_decode_vs_reference_golden(cuda, case):
     ml = ml.cpu().double().numpy()[0]
     lse = ml[0] + math.log(ml[1])
     assert abs(lse - (g["merged_m"] + math.log(g["merged_l"]))) < 5e-3
+
+
+@pytest.mark.parametrize("case", ["one_cta_many_units", "few_units_many_ctas"])
+def test_sparse_decode_segment_edges(cuda, case):
+    """K2's combine paths: one CTA holding 40 units (40 segments handed to the
+    combiner warp back to back, 22 units without a resident block: more than
+    the plan lists, so the combiner scans n_res) and two long units spread
+    over 60 CTAs (the cross-CTA finalize of many partial slots), each with a
+    CPU partial to merge."""
+    rng = np.random.default_rng(4242 + (case == "few_units_many_ctas"))
+    G = 8
+    if case == "one_cta_many_units":
+        U, max_ctas = 40, 1
+        nb_list = [int(x) for x in rng.integers(1, 6, size=U)]
+        n_res = [0 if u % 2 == 0 or u > 34 else int(rng.integers(1, nb_list[u] + 1)) for u in range(U)]
+    else:
+        U, max_ctas = 2, 60
+        nb_list = [200, 150]
+        n_res = [200, 131]
+    c = build_case(rng, U, G, nb_list, n_res, torch.bfloat16)
+    cpu_o = rng.standard_normal((U * G, D)).astype(np.float32)
+    cpu_ml = np.stack([rng.standard_normal(U * G), rng.random(U * G) * 10 + 0.5], axis=1).astype(np.float32)
+    cpu_ml[:G] = (-np.inf, 0.0)  # unit 0: no CPU side
+    d = c["dev"]
+    o, ml = ops.sparse_decode(d["q"], c["pool"], torch.bfloat16, d["res_slots"], d["res_ids"], d["n_res"],
+                              d["n_tokens"], G, cpu_o=torch.as_tensor(cpu_o, device="cuda"),
+                              cpu_ml=torch.as_tensor(cpu_ml, device="cuda"), max_ctas=max_ctas)
+    torch.cuda.synchronize()
+    check(o, ml, *oracle_outputs(c, U, G, torch.bfloat16, cpu=(cpu_o, cpu_ml)), torch.bfloat16)
