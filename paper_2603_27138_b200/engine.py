@@ -68,11 +68,18 @@ class DecodeEngine:
         A.check(A.lib().scout_engine_create(C.byref(cfg), descs, C.byref(h)))
         self._h = h
 
-    def __del__(self):
+    def close(self):
+        """Destroy the engine (drains its recall thread); idempotent."""
         h = getattr(self, "_h", None)
         if h:
-            A.lib().scout_engine_destroy(h)
             self._h = None
+            A.lib().scout_engine_destroy(h)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown: the module globals may be gone already
+            pass
 
     @staticmethod
     def _stream():
