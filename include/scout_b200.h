@@ -430,6 +430,11 @@ int scout_engine_decode_step_kv_host(scout_engine* eng, int step, const void* h_
                                      int32_t* h_n_cpu, void* stream);
 /* Order all outstanding side-stream work (recalls) before `stream`. */
 int scout_engine_sync(scout_engine* eng, void* stream);
+/* Device tier mode: the caller changed the K5 state outside the engine
+ * between steps (e.g. scout_tier_place for a newly admitted request). Each
+ * step's post-attention launch writes the next step's planning view; this
+ * makes the next step plan again from the current state instead. */
+int scout_engine_tier_changed(scout_engine* eng);
 /* Instrumentation: when enabled, CUDA events bracket every K2 launch (on the
  * launching stream). scout_engine_stats synchronises, reports the summed K2
  * event time, K2 count and the number of kernels launched since the last

@@ -34,7 +34,7 @@ EXPORTED = (
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv",
-    "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel",
+    "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
 )
 
 _vp = C.c_void_p
@@ -145,6 +145,7 @@ def lib() -> C.CDLL:
         L.scout_engine_decode_step_kv_host.argtypes = [_vp, C.c_int] + [_vp] * 10 + [_vp]
         L.scout_engine_decode_step_host.argtypes = [_vp, C.c_int] + [_vp] * 8 + [_vp]
         L.scout_engine_sync.argtypes = [_vp, _vp]
+        L.scout_engine_tier_changed.argtypes = [_vp]
         L.scout_engine_set_timing.argtypes = [_vp, C.c_int]
         L.scout_engine_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]
         L.scout_engine_k1_outputs.argtypes = [_vp] + [C.POINTER(_vp)] * 7

@@ -1020,6 +1020,12 @@ extern "C" int scout_engine_sync(scout_engine* e, void* stream) {
     return SCOUT_OK;
 }
 
+extern "C" int scout_engine_tier_changed(scout_engine* e) {
+    if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
+    e->planned_step = -1;
+    return SCOUT_OK;
+}
+
 extern "C" int scout_engine_set_timing(scout_engine* e, int enable) {
     if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
     e->timing = enable != 0;

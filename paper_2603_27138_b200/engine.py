@@ -109,6 +109,10 @@ class DecodeEngine:
                                                       _p(h_cpu_ml), _p(h_out_o), _p(h_out_ml), _p(h_cpu_ids),
                                                       _p(h_n_cpu), self._stream()))
 
+    def tier_changed(self):
+        """The tier state was changed outside the engine: plan the next step afresh."""
+        A.check(A.lib().scout_engine_tier_changed(self._h))
+
     def sync(self):
         A.check(A.lib().scout_engine_sync(self._h, self._stream()))
 

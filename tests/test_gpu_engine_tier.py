@@ -40,8 +40,12 @@ class Side:
         self.n_tokens.copy_(self.tier.n_tokens[0])
 
 
-@pytest.mark.parametrize("recall", [3, 0])
-def test_engine_tier_mode_matches_reference_order_replay(cuda, recall):
+@pytest.mark.parametrize("recall,external", [(3, False), (0, False), (0, True)])
+def test_engine_tier_mode_matches_reference_order_replay(cuda, recall, external):
+    """external: between two steps the caller re-places layer 1's fast set
+    (place_after_prefill) on both sides and tells the engine
+    (scout_engine_tier_changed), whose next planning view must then come from
+    the new state, not from the view the previous step's post launch wrote."""
     rng = np.random.default_rng(21 + recall)
     L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 70
     U = batch * hkv
@@ -99,6 +103,15 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, recall):
             assert torch.equal(getattr(eng_side.tier, name), getattr(rt, name)), (step, name)
         assert torch.equal(eng_side.tier.ready >= 0, rt.ready >= 0), step
         assert int(eng_side.tier.err.abs().sum()) == 0
+        if external and step == steps // 2:
+            qx = torch.randn(U * G, D, device="cuda")
+            for i in range(L):  # the engine advanced its own token counts, not the mirror's
+                eng_side.tier.n_tokens[i].copy_(eng_side.n_tokens)
+            for side in (eng_side, rep):
+                side.tier.place_after_prefill(1, qx, side.dig[1], G, kv)
+            torch.cuda.synchronize()
+            assert torch.equal(eng_side.tier.tier, rt.tier)
+            eng.tier_changed()
     # the run crossed seals (evictions) and, with recall, flipped tiers back
     assert int(eng_side.n_tokens[0]) == T0 + steps
     nb = (T0 + steps + BS - 1) // BS
