@@ -12,6 +12,7 @@ struct K1Batch {
     int nbuf;   // digest ring depth (set at launch)
     int chunk;  // digest chunk bytes (set at launch)
     int persist;  // persistent grid over (layer, unit) items (set at launch)
+    int direct;   // bf16 digests read straight from global memory, no ring (set at launch)
     scout_topk_args a[K1_MAX_LAYERS];
 };
 

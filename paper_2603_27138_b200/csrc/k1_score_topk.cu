@@ -336,10 +336,72 @@ __device__ __forceinline__ void fast_quad(const DigT* blo, const DigT* bhi, int 
     }
 }
 
+// fast_quad over all 128 channels straight from global memory (bf16 digests):
+// each thread streams its quad's lo / hi words of 4 channels per batch with
+// evict-first loads, the next batch in flight while this one is summed; no
+// shared-memory ring, no per-chunk barrier. Chains of 8 channels, as above.
+#ifndef SCOUT_K1_DCB
+#define SCOUT_K1_DCB 4  // channels per direct-load batch (two batches in flight)
+#endif
+#ifndef SCOUT_K1_DMINB
+#define SCOUT_K1_DMINB 6   // CTAs per SM the direct QPT=2 variant is compiled for (80 registers)
+#endif
+#ifndef SCOUT_K1_DMINB1
+#define SCOUT_K1_DMINB1 8  // ... and the QPT=1 variant (64 registers)
+#endif
+constexpr int DCB = SCOUT_K1_DCB;
+__device__ __forceinline__ void ld_quad4(const __nv_bfloat16* lo, const __nv_bfloat16* hi, size_t ns, int b0, int c0,
+                                         uint2 (&L)[DCB], uint2 (&H)[DCB]) {
+#pragma unroll
+    for (int i = 0; i < DCB; ++i) {
+        L[i] = __ldcs(reinterpret_cast<const uint2*>(lo + static_cast<size_t>(c0 + i) * ns + b0));
+        H[i] = __ldcs(reinterpret_cast<const uint2*>(hi + static_cast<size_t>(c0 + i) * ns + b0));
+    }
+}
+__device__ __forceinline__ void sum_quad4(const uint2 (&L)[DCB], const uint2 (&H)[DCB], const float2* pn, int c0,
+                                          float (&t)[4], float (&a)[4]) {
+#pragma unroll
+    for (int i = 0; i < DCB; ++i) {
+        float l[4], h[4];
+        l[0] = __uint_as_float(L[i].x << 16); l[1] = __uint_as_float(L[i].x & 0xFFFF0000u);
+        l[2] = __uint_as_float(L[i].y << 16); l[3] = __uint_as_float(L[i].y & 0xFFFF0000u);
+        h[0] = __uint_as_float(H[i].x << 16); h[1] = __uint_as_float(H[i].x & 0xFFFF0000u);
+        h[2] = __uint_as_float(H[i].y << 16); h[3] = __uint_as_float(H[i].y & 0xFFFF0000u);
+        const float2 pv = pn[c0 + i];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            t[e] = fmaf(h[e], pv.x, fmaf(l[e], pv.y, t[e]));
+            a[e] = fmaf(fabsf(h[e]), pv.x, fmaf(fabsf(l[e]), -pv.y, a[e]));
+        }
+    }
+}
+__device__ __forceinline__ void fast_quad_direct(const __nv_bfloat16* lo, const __nv_bfloat16* hi, size_t ns, int b0,
+                                                 const float2* pn, double (&s)[4], float (&a)[4]) {
+    static_assert(DCB == 4 || DCB == 8, "8-channel fp32 chains: batches of 4 (two per chain) or 8");
+    uint2 L0[DCB], H0[DCB], L1[DCB], H1[DCB];
+    ld_quad4(lo, hi, ns, b0, 0, L0, H0);
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 2 * DCB) {
+        float t[4] = {0.f, 0.f, 0.f, 0.f};
+        ld_quad4(lo, hi, ns, b0, c0 + DCB, L1, H1);
+        sum_quad4(L0, H0, pn, c0, t, a);
+        if (DCB == 8) {  // one chain per batch
+#pragma unroll
+            for (int e = 0; e < 4; ++e) { s[e] += static_cast<double>(t[e]); t[e] = 0.f; }
+        }
+        if (c0 + 2 * DCB < D) ld_quad4(lo, hi, ns, b0, c0 + 2 * DCB, L0, H0);
+        sum_quad4(L1, H1, pn, c0 + DCB, t, a);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) s[e] += static_cast<double>(t[e]);
+    }
+}
+
 // QPT: block quads per thread whose running scores live in registers (1: up
 // to 512 blocks, 2: up to 1024, 4: up to 2048); 0: shared-memory accumulators.
-template <typename DigT, int G, int MODE, int QPT>
-__global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT_K1_MINB) score_topk_kernel(const K1Batch batch) {
+template <typename DigT, int G, int MODE, int QPT, bool DIRECT = false>
+__global__ void __launch_bounds__(K1_THREADS, DIRECT ? (QPT == 1 ? SCOUT_K1_DMINB1 : (QPT == 2 ? SCOUT_K1_DMINB : 4))
+                                                      : ((QPT == 1 || QPT == 2) ? 7 : SCOUT_K1_MINB))
+    score_topk_kernel(const K1Batch batch) {
     // Work items are (layer, unit) pairs, flattened layer-major. Classic grid
     // (units x layers): one item per CTA. Persistent grid (batch.persist): CTA
     // c takes items c, c + grid, ... and the digest ring keeps streaming across
@@ -402,8 +464,10 @@ __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT
             ++iss_item;
         }
     };
+    constexpr bool can_direct = DIRECT && MODE == 0 && QPT > 0 && sizeof(DigT) == 2;
+    constexpr bool direct = can_direct;
     if constexpr (MODE == 0) {
-        if (tid == 0) {
+        if (tid == 0 && !direct) {
             for (int i = 0; i < nbuf; ++i) mbar_init(&s_full[i], 1);
             fence_mbar_init();
             while (g_iss < nbuf && g_iss < total_chunks) issue_next();
@@ -474,7 +538,18 @@ __global__ void __launch_bounds__(K1_THREADS, (QPT == 1 || QPT == 2) ? 7 : SCOUT
         for (int q = 0; q < RQ; ++q)
 #pragma unroll
             for (int e = 0; e < 4; ++e) { rs[q][e] = 0.0; ra[q][e] = 0.f; }
-        for (int c = 0; c < nchunks; ++c, ++g_cons) {
+        if constexpr (can_direct) {
+            if (direct) {
+#pragma unroll
+                for (int q = 0; q < RQ; ++q) {
+                    const int j = tid + q * K1_THREADS;
+                    if (j < nq)
+                        fast_quad_direct(reinterpret_cast<const __nv_bfloat16*>(lo),
+                                         reinterpret_cast<const __nv_bfloat16*>(hi), ns, 4 * j, pn, rs[q], ra[q]);
+                }
+            }
+        }
+        for (int c = 0; c < (direct ? 0 : nchunks); ++c, ++g_cons) {
             const int slot = static_cast<int>(g_cons % nbuf);
             mbar_wait(&s_full[slot], static_cast<uint32_t>((g_cons / nbuf) & 1));
             const int ch0 = c * cpc, nch = min(cpc, D - ch0);
@@ -686,7 +761,13 @@ int launch_g(K1Batch& b, cudaStream_t st) {
         const int want = four < 32768 ? four : 32768;
         if (b.chunk < want) b.chunk = want;
     }
-    const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)), b.nbuf, b.chunk)
+    static const bool direct_env = [] {
+        const char* e = getenv("SCOUT_K1_DIRECT");
+        return e ? atoi(e) != 0 : true;
+    }();
+    b.direct = MODE == 0 && sizeof(DigT) == 2 && direct_env && a.nb_stride <= K1_REG_BLOCKS;  // QPT 1 / 2 / 4
+    const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)),
+                                                  b.direct ? 0 : b.nbuf, b.chunk)
                                   : k1_stage_offset(a.group, a.nb_stride);
     // persistent grid (SCOUT_K1_PERSIST=1): measured slower than the classic
     // one-item-per-CTA grid at config 3 (0.93 vs 0.86 ms per 64 layers), whose
@@ -714,6 +795,14 @@ int launch_g(K1Batch& b, cudaStream_t st) {
     const int qpt = MODE != 0 ? 1 : (ns <= 4 * K1_THREADS ? 1 : (ns <= 8 * K1_THREADS ? 2 : (ns <= K1_REG_BLOCKS ? 4 : 0)));
     auto pick = [&](auto g) {
         constexpr int Gv = decltype(g)::value;
+        if constexpr (MODE == 0 && sizeof(DigT) == 2) {
+            if (b.direct) {
+                if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1, true>);
+                else if (qpt == 2) go(score_topk_kernel<DigT, Gv, MODE, 2, true>);
+                else go(score_topk_kernel<DigT, Gv, MODE, 4, true>);
+                return;
+            }
+        }
         if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1>);
         else if constexpr (MODE == 0) {
             if (qpt == 2) go(score_topk_kernel<DigT, Gv, MODE, 2>);
