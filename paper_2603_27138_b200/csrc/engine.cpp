@@ -195,10 +195,10 @@ struct scout_engine {
         fprintf(stderr,
                 "[k2 prof] %d CTAs, %.0f blocks/CTA, %.0f cycles/block | producer: plan wait %.1f%%, stage wait "
                 "%.1f%% | consumers: data wait %.1f%%, Q load %.1f%%, segment end %.1f%%, plan+layer end %.1f%% | "
-                "combiner: waiting %.1f%%, busy %.1f%% | planner: buffer wait %.1f%%, planning %.1f%%\n",
+                "combiners (each): waiting %.1f%%, busy %.1f%% | planner: buffer wait %.1f%%, planning %.1f%%\n",
                 grid, s[3] / grid, s[0] / (s[3] > 0 ? s[3] : 1), 100 * s[1] / tot, 100 * s[2] / tot,
                 100 * s[4] / nw / tot, 100 * s[5] / nw / tot, 100 * s[6] / nw / tot, 100 * s[7] / nw / tot,
-                100 * s[8] / tot, 100 * s[9] / tot, 100 * s[10] / tot, 100 * s[11] / tot);
+                100 * s[8] / 2 / tot, 100 * s[9] / 2 / tot, 100 * s[10] / tot, 100 * s[11] / tot);
     }
 
     ~scout_engine() {

@@ -64,12 +64,13 @@ namespace tc {
 constexpr int NPAIR = 3;
 constexpr int NC = 2 * NPAIR;               // consumer warps
 constexpr int NCT = NC * 32;                // consumer threads
-constexpr int NTHREADS = NCT + 96;          // + 1 producer warp + 1 planner warp + 1 combiner warp
+constexpr int NCOMB = 2;                    // combiner warps (segments alternate between them)
+constexpr int NTHREADS = NCT + 32 * (2 + NCOMB);  // + producer, planner and combiner warps
 constexpr int NST = 2 * NPAIR;              // ring stages
 constexpr int STAGE_BYTES = 32768;          // one block: K tile (16 KiB) + V tile (16 KiB)
 constexpr int MAXSEG = 64;                  // units touched by one CTA range
 constexpr int MAXB = 384;                   // blocks per CTA range per layer
-constexpr int CB_ROW = D + 4;               // combine rows (bank-conflict pad)
+constexpr int CB_ROW = D;  // combine rows (no pad: the conflicted state stores are once per segment)
 constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES;
 
 struct Seg {
@@ -92,8 +93,9 @@ struct Smem {
     uint64_t empty[NST];
     uint64_t plan_full[2];
     uint64_t plan_empty[2];
-    uint64_t seg_full;   // the NC consumer warps left their segment states
-    uint64_t seg_empty;  // the combiner has read them
+    uint64_t seg_full[NCOMB];  // the NC consumer warps left a segment's states (segment s: combiner s % NCOMB)
+    uint64_t seg_empty;        // its combiner has read them
+    int layer_fin[K2_MAX_LAYERS];  // combiners done with layer L (the last one counts the CTA in)
     Plan plan[2];
     int warp_area[NC];   // 1: the warp left a state in wstate, -1: no state
     // per-warp segment states (o^T rows, m, l), merged by the combiner warp
@@ -362,6 +364,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int nunits = a.n_units;
 
+    for (int i = tid; i < K2_MAX_LAYERS; i += NTHREADS) sm.layer_fin[i] = 0;
     if (tid == 0) {
         for (int i = 0; i < NST; ++i) {
             mbar_init(&sm.full[i], 1);
@@ -369,9 +372,9 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&sm.plan_full[i], 1);
-            mbar_init(&sm.plan_empty[i], NC + 2);  // every consumer warp, the producer and the combiner release a plan
+            mbar_init(&sm.plan_empty[i], NC + 1 + NCOMB);  // every consumer warp, the producer and the combiners
         }
-        mbar_init(&sm.seg_full, NC);
+        for (int i = 0; i < NCOMB; ++i) mbar_init(&sm.seg_full[i], NC);
         mbar_init(&sm.seg_empty, 1);
         fence_mbar_init();
     }
@@ -462,11 +465,15 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
         return;
     }
 
-    if (warp == NC + 2) {
-        // ======================================== combiner warp: merges each
-        // segment's NC warp states, writes the unit's output (nseg == 1) or its
-        // partial (+ the cross-CTA finalize when last), the units without a
-        // resident block and the layer-done count, off the consumers' path
+    if (warp >= NC + 2) {
+        // ======================================== combiner warps: each merges
+        // every NCOMB-th segment's NC warp states and writes the unit's output
+        // (nseg == 1) or its partial (+ the cross-CTA finalize when last), off
+        // the consumers' path; they share the units without a resident block,
+        // and the last to finish a layer counts the CTA in. One combiner kept
+        // up at config 3 but not where segments are short (config 2: busy 81%,
+        // consumers waiting for it 19% of their time)
+        const int cw = warp - (NC + 2);
         long long k_wait = 0, k_busy = 0, tq = 0;
         int segidx = 0;
         for (int L = 0; L < a.n_layers; ++L) {
@@ -477,10 +484,11 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
             const Plan& P = sm.plan[b];
             for (int si = 0; si < P.nsegs; ++si, ++segidx) {
+                if (segidx % NCOMB != cw) continue;
                 const Seg sg = P.segs[si];
                 const int u = sg.unit;
                 if (a.prof) tq = clock64();
-                mbar_wait(&sm.seg_full, segidx & 1);
+                mbar_wait(&sm.seg_full[cw], (segidx / NCOMB) & 1);
                 if (a.prof) { const long long t1 = clock64(); k_wait += t1 - tq; tq = t1; }
                 // lane: channels 4*lane..4*lane+3 of every head
                 const int d0 = lane * 4;
@@ -585,22 +593,27 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             // ---- units with no resident block: output = CPU partial (or empty),
             // listed by the planner (no n_res read on this path)
             if (P.nzero <= ZMAX) {
-                for (int i = 0; i < P.nzero; ++i)
+                for (int i = cw; i < P.nzero; i += NCOMB)
                     finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, P.zero_units[i], parts, 0, 0, lane);
             } else {
-                for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                for (int u = blockIdx.x + cw * gridDim.x; u < nunits; u += NCOMB * gridDim.x) {
                     if (io.n_res[u] != 0) continue;
                     finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, lane);
                 }
             }
-            // layer done in this CTA: release the plan buffer, count the CTA in
-            // (the lanes' outputs ordered before the counter by __syncwarp + lane 0's fence)
+            // done with layer L: release the plan buffer; the last combiner counts
+            // the CTA in. Each orders its lanes' outputs (__syncwarp) before its
+            // gpu-scope fence, the fence before its shared-memory count, and the
+            // last one's fence after that count precedes the layer counter.
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&sm.plan_empty[b]);
                 if (a.layer_done) {
                     __threadfence();
-                    atomicAdd(a.layer_done + L, 1u);
+                    if (atomicAdd(&sm.layer_fin[L], 1) == NCOMB - 1) {
+                        __threadfence();
+                        atomicAdd(a.layer_done + L, 1u);
+                    }
                 }
             }
             if (a.prof) k_busy += clock64() - tq;
@@ -799,7 +812,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             }
             if (lane == 0) sm.warp_area[warp] = area;
             __syncwarp();  // every lane's state stores before lane 0's (release) arrive
-            if (lane == 0) mbar_arrive(&sm.seg_full);
+            if (lane == 0) mbar_arrive(&sm.seg_full[segidx % NCOMB]);
             ++segidx;
             if (a.prof) c_end += clock64() - tp;
         }
