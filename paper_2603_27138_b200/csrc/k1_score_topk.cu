@@ -375,13 +375,15 @@ __device__ __forceinline__ void sum_quad4(const uint2 (&L)[DCB], const uint2 (&H
         }
     }
 }
+// channels [cb, ce) (multiples of 2 * DCB)
 __device__ __forceinline__ void fast_quad_direct(const __nv_bfloat16* lo, const __nv_bfloat16* hi, size_t ns, int b0,
-                                                 const float2* pn, double (&s)[4], float (&a)[4]) {
+                                                 const float2* pn, double (&s)[4], float (&a)[4], int cb = 0,
+                                                 int ce = D) {
     static_assert(DCB == 4 || DCB == 8, "8-channel fp32 chains: batches of 4 (two per chain) or 8");
     uint2 L0[DCB], H0[DCB], L1[DCB], H1[DCB];
-    ld_quad4(lo, hi, ns, b0, 0, L0, H0);
+    ld_quad4(lo, hi, ns, b0, cb, L0, H0);
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 2 * DCB) {
+    for (int c0 = cb; c0 < ce; c0 += 2 * DCB) {
         float t[4] = {0.f, 0.f, 0.f, 0.f};
         ld_quad4(lo, hi, ns, b0, c0 + DCB, L1, H1);
         sum_quad4(L0, H0, pn, c0, t, a);
@@ -389,7 +391,7 @@ __device__ __forceinline__ void fast_quad_direct(const __nv_bfloat16* lo, const 
 #pragma unroll
             for (int e = 0; e < 4; ++e) { s[e] += static_cast<double>(t[e]); t[e] = 0.f; }
         }
-        if (c0 + 2 * DCB < D) ld_quad4(lo, hi, ns, b0, c0 + 2 * DCB, L0, H0);
+        if (c0 + 2 * DCB < ce) ld_quad4(lo, hi, ns, b0, c0 + 2 * DCB, L0, H0);
         sum_quad4(L1, H1, pn, c0 + DCB, t, a);
 #pragma unroll
         for (int e = 0; e < 4; ++e) s[e] += static_cast<double>(t[e]);
@@ -539,13 +541,41 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (QPT == 1 ? SCOUT_K1_DMIN
 #pragma unroll
             for (int e = 0; e < 4; ++e) { rs[q][e] = 0.0; ra[q][e] = 0.f; }
         if constexpr (can_direct) {
-            if (direct) {
+            const __nv_bfloat16* dlo = reinterpret_cast<const __nv_bfloat16*>(lo);
+            const __nv_bfloat16* dhi = reinterpret_cast<const __nv_bfloat16*>(hi);
+            const int ntail = nq - K1_THREADS;  // quads past the first pass
+            if (QPT == 2 && ntail > 0 && ntail <= 32) {
+                // a stride just above 4 * K1_THREADS blocks (tier mode: room for
+                // appended blocks): the few tail quads would leave one thread each
+                // streaming all 128 channels while the CTA waits. Instead every
+                // warp takes a quarter of the channels of every tail quad, and
+                // warp 0 adds the four partials (f64 sums of the same <= 8-channel
+                // fp32 chains: the error bound is unchanged).
+                if (tid < nq) fast_quad_direct(dlo, dhi, ns, 4 * tid, pn, rs[0], ra[0]);
+                double* ps = reinterpret_cast<double*>(stagebuf);        // [K1_WARPS][32][4]
+                float* pa = reinterpret_cast<float*>(ps + K1_WARPS * 128);  // [K1_WARPS][32][4]
+                const int w = tid >> 5, l = tid & 31;
+                if (l < ntail) {
+                    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+                    float a4[4] = {0.f, 0.f, 0.f, 0.f};
+                    const int cq = D / K1_WARPS;
+                    fast_quad_direct(dlo, dhi, ns, 4 * (K1_THREADS + l), pn, s4, a4, w * cq, (w + 1) * cq);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) { ps[(w * 32 + l) * 4 + e] = s4[e]; pa[(w * 32 + l) * 4 + e] = a4[e]; }
+                }
+                __syncthreads();
+                if (tid < ntail)
+                    for (int ww = 0; ww < K1_WARPS; ++ww)
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            rs[RQ - 1][e] += ps[(ww * 32 + tid) * 4 + e];
+                            ra[RQ - 1][e] += pa[(ww * 32 + tid) * 4 + e];
+                        }
+            } else if (direct) {
 #pragma unroll
                 for (int q = 0; q < RQ; ++q) {
                     const int j = tid + q * K1_THREADS;
-                    if (j < nq)
-                        fast_quad_direct(reinterpret_cast<const __nv_bfloat16*>(lo),
-                                         reinterpret_cast<const __nv_bfloat16*>(hi), ns, 4 * j, pn, rs[q], ra[q]);
+                    if (j < nq) fast_quad_direct(dlo, dhi, ns, 4 * j, pn, rs[q], ra[q]);
                 }
             }
         }
@@ -766,8 +796,10 @@ int launch_g(K1Batch& b, cudaStream_t st) {
         return e ? atoi(e) != 0 : true;
     }();
     b.direct = MODE == 0 && sizeof(DigT) == 2 && direct_env && a.nb_stride <= K1_REG_BLOCKS;  // QPT 1 / 2 / 4
-    const size_t smem = MODE == 0 ? k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)),
-                                                  b.direct ? 0 : b.nbuf, b.chunk)
+    // direct loads: no ring; the 2-quad variant keeps a tail-quad scratch there (K1_WARPS x 32 x 4 x (8 + 4) B)
+    const size_t smem = MODE == 0 ? (b.direct ? k1_stage_offset(a.group, a.nb_stride) + K1_WARPS * 32 * 4 * 12
+                                              : k1_smem_bytes(a.group, a.nb_stride, static_cast<int>(sizeof(DigT)),
+                                                              b.nbuf, b.chunk))
                                   : k1_stage_offset(a.group, a.nb_stride);
     // persistent grid (SCOUT_K1_PERSIST=1): measured slower than the classic
     // one-item-per-CTA grid at config 3 (0.93 vs 0.86 ms per 64 layers), whose

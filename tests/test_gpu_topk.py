@@ -117,10 +117,12 @@ def test_topk_bf16_queries_vs_oracle(cuda, G, kind):
             assert np.array_equal(got["scores"][u, :nb].view(np.uint64), want["scores"][u, :nb].view(np.uint64))
 
 
-@pytest.mark.parametrize("nb", [1000, 2048, 2600])
+@pytest.mark.parametrize("nb", [513, 520, 640, 700, 1000, 2048, 2600])
 def test_topk_many_blocks_vs_oracle(cuda, nb):
-    """Long contexts: running scores in registers (4 quads per thread, <= 2048
-    blocks) and in shared memory (> 2048), 4-channel digest chunks."""
+    """Long contexts: running scores in registers (2 quads per thread <= 1024
+    blocks, 4 <= 2048) and in shared memory (> 2048). 513-640 blocks: the
+    direct-load path's tail quads split over the warps' channel quarters;
+    700: one tail quad per thread."""
     rng = np.random.default_rng(nb)
     U, G, nbs = 4, 8, nbs_for(nb)
     n_tokens = np.array([64 * nb, 64 * nb - 63, 64 * (nb // 2) + 5, 64 * nb - 1], np.int32)
