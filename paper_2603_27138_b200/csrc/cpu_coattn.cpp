@@ -31,6 +31,7 @@
 #include <cstring>
 #include <functional>
 #include <limits>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -480,8 +481,19 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
 }
 
 SCOUT_AMX_TARGET void amx_work(const Job& j, std::atomic<int>& next, int n_units) {
-    static thread_local AmxScratch* scratch = nullptr;
-    if (!scratch) scratch = static_cast<AmxScratch*>(std::aligned_alloc(64, sizeof(AmxScratch)));
+    // per-thread scratch, freed when the thread exits (callers' own threads run units too)
+    struct Free {
+        void operator()(AmxScratch* p) const { std::free(p); }
+    };
+    static thread_local std::unique_ptr<AmxScratch, Free> owned;
+    if (!owned) {
+        owned.reset(static_cast<AmxScratch*>(std::aligned_alloc(64, sizeof(AmxScratch))));
+        if (!owned) {  // no memory for the tile staging: this thread takes the AVX-512 kernel
+            for (int u; (u = next.fetch_add(1)) < n_units;) run_unit<true>(j, u);
+            return;
+        }
+    }
+    AmxScratch* scratch = owned.get();
     amx_config(j.G);
     for (int u; (u = next.fetch_add(1)) < n_units;) run_unit_amx(j, u, *scratch);
     _tile_release();
