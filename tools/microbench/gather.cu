@@ -86,6 +86,8 @@ int main() {
     run<13, 1, 16384>(src, bytes, 0, sms, dout, "random 16KB contiguous");
     run<6, 1, 32768>(src, bytes, 0, sms, dout, "random 32KB contiguous");
     run<6, 1, 32768>(src, bytes, 2, sms, dout, "unit-clustered 32KB (64 of 512)");
+    run<5, 1, 32768>(src, bytes, 0, sms, dout, "random 32KB, 5 stages");
+    run<7, 1, 32768>(src, bytes, 0, sms, dout, "random 32KB, 7 stages (224 KB)");
     run<6, 1, 32768>(src, bytes, 1, sms, dout, "sequential 32KB");
     run<26, 1, 8192>(src, bytes, 0, sms, dout, "random 8KB");
     run<13, 4, 4096>(src, bytes, 0, sms, dout, "random 4x4KB");
