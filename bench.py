@@ -632,7 +632,7 @@ def main():
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init KV, digests, queries, CPU partials)",
-            "config": {"workload": args.config, "model_shape": "Qwen3-32B" if cfg["hq"] == 64 else "Qwen3-8B",
+            "config": {"workload": args.config, "attention_shape": "Qwen3-32B" if cfg["hq"] == 64 else "Qwen3-8B",
                        "batch_per_gpu": cfg["batch"], "global_batch": global_batch, "context": cfg["ctx"],
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "head_dim": D,
                        "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "gpu_cache_blocks_per_unit": cfg["capacity"],
