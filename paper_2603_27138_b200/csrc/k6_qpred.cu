@@ -140,6 +140,7 @@ struct QpArgs {
     float* partial;           // [grid][2][128][n_pad]: a CTA's partial of its first / second tile
     int* counters;            // [n_out / 128], zero; left zeroed
     int hidden, n_out, batch, n_pad, nst;
+    int pair;                 // 1: cluster pairs, CTA 2t+r holds K half r of tile t; halves meet in shared memory
 };
 
 // CTA holding unit u when T units are cut into `grid` equal ranges
@@ -265,7 +266,53 @@ __global__ void __launch_bounds__(QP_THREADS, 1) qpred_gemm_kernel(const QpArgs 
         for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
     };
     const int ngrp = (a.n_pad + 31) / 32;
-    for (int seg = 0; seg < nseg; ++seg) {
+    if (a.pair) {
+        // ---- cluster pair: rank 1 drops its accumulator into rank 0's shared
+        // memory (past the ring), a cluster barrier publishes it, rank 0 adds
+        // its own and writes the tile. Replaces the partials' round trip through
+        // L2 (store, fence, counter, reload) for the default 2-CTAs-per-tile grid.
+        uint32_t rank;
+        asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+        float* recv = reinterpret_cast<float*>(qsm + static_cast<size_t>(nst) * stage_bytes);  // [128][n_pad]
+        const int row = warp * 32 + lane;
+        mbar_wait(&tfull[0], 0);
+        __syncwarp();
+        tc_fence_after();
+        if (rank == 1) {
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(recv + row * a.n_pad)));
+            for (int grp = 0; grp < ngrp; ++grp) {
+                float f[32];
+                tmem_load(static_cast<uint32_t>(grp * 32), f);
+                const int ncol = min(32, a.n_pad - grp * 32);
+#pragma unroll
+                for (int j = 0; j < 32; j += 4)
+                    if (j < ncol)
+                        asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote + 4u * (grp * 32 + j)),
+                                     "f"(f[j]), "f"(f[j + 1]), "f"(f[j + 2]), "f"(f[j + 3])
+                                     : "memory");
+            }
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (rank == 0) {
+            const int feat = mt0 * QP_M + row;
+            for (int grp = 0; grp < ngrp; ++grp) {
+                float f[32];
+                tmem_load(static_cast<uint32_t>(grp * 32), f);
+                const float* rp = recv + row * a.n_pad + grp * 32;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int bcol = grp * 32 + j;
+                    if (bcol < a.batch) {
+                        const float v = f[j] + rp[j];  // K half 0 + K half 1: the same order for every call
+                        if (a.out_f32) a.out_f32[static_cast<size_t>(bcol) * a.n_out + feat] = v;
+                        if (a.out_bf16) a.out_bf16[static_cast<size_t>(bcol) * a.n_out + feat] = __float2bfloat16_rn(v);
+                    }
+                }
+            }
+        }
+    }
+    for (int seg = 0; seg < (a.pair ? 0 : nseg); ++seg) {
         const int mt = mt0 + seg;
         const int feat = mt * QP_M + warp * 32 + lane;
         const long long t0 = static_cast<long long>(mt) * nkc, t1 = t0 + nkc;  // the tile's units
@@ -404,15 +451,23 @@ extern "C" int scout_predict_query(const float* x, int batch, int hidden, const 
     auto* part = reinterpret_cast<float*>(ws + xb_bytes + ctr_bytes);
     qpred_pack_x_kernel<<<n_pad, 256, 0, st>>>(x, hidden, batch, n_pad, xb);
     QpArgs a{static_cast<const __nv_bfloat16*>(w_packed), xb, out_f32, static_cast<__nv_bfloat16*>(out_bf16), part, ctr,
-             hidden, n_out, batch, n_pad, 0};
+             hidden, n_out, batch, n_pad, 0, 0};
+    // cluster pairs when every tile is exactly two K halves (the default grid)
+    static const bool pair_env = [] {
+        const char* e = getenv("SCOUT_QP_PAIR");
+        return e ? atoi(e) != 0 : true;
+    }();
+    a.pair = pair_env && grid == 2 * tiles && nkc % 2 == 0 && n_pad <= 64;
     const uint32_t stage = QP_A_BYTES + static_cast<uint32_t>(n_pad) * QP_KC * 2;
+    const uint32_t recv = a.pair ? static_cast<uint32_t>(QP_M) * n_pad * 4 : 0u;
     int nst = static_cast<int>((200u * 1024u) / stage);
     if (const char* e = getenv("SCOUT_QP_NST")) nst = atoi(e);  // tuning
     if (nst > 8) nst = 8;
+    while (nst > 2 && static_cast<size_t>(nst) * stage + recv > 224u * 1024u) --nst;
     if (nst < 2) nst = 2;
     a.nst = nst;
-    const size_t smem = static_cast<size_t>(nst) * stage;
+    const size_t smem = static_cast<size_t>(nst) * stage + recv;
     ensure_smem(reinterpret_cast<const void*>(qpred_gemm_kernel), smem);
-    launch(qpred_gemm_kernel, dim3(grid), dim3(QP_THREADS), smem, st, true, a);
+    launch(qpred_gemm_kernel, dim3(grid), dim3(QP_THREADS), smem, st, true, a, a.pair ? 2 : 1);
     return check_launch("scout_predict_query");
 }
