@@ -493,7 +493,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="requests per GPU (default: config; weak scaling)")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="total requests split across ranks (strong scaling, e.g. config 4: 128)")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline")
     ap.add_argument("--tier", default="device", choices=["static", "device"],
@@ -530,7 +530,7 @@ def main():
     lib()  # native library must be present: no fallback
     t0 = time.time()
     tier_mode = args.tier == "device"
-    wl = (TierWorkload(cfg, dev, seed=1234 + rank, max_steps=args.warmup + args.steps + 8) if tier_mode
+    wl = (TierWorkload(cfg, dev, seed=1234 + rank, max_steps=args.warmup + args.steps + args.e2e_steps + 16) if tier_mode
           else Workload(cfg, dev, seed=1234 + rank))
     torch.cuda.synchronize(dev)
     log(f"workload ready in {time.time() - t0:.1f}s: pool {wl.pool.numel() / 2**30:.1f} GiB")
@@ -615,7 +615,7 @@ def main():
     # ---- e2e through host buffers
     e2e = None
     if not args.profile:
-        e2e = run_e2e(wl, args.e2e_steps, dev, ws, global_batch, tier_mode)
+        e2e = run_e2e(wl, args.e2e_steps, dev, ws, global_batch, tier_mode, first_step=args.warmup + args.steps + 1)
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
@@ -662,7 +662,7 @@ def main():
     barrier(ws)
 
 
-def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False):
+def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False, first_step=10000):
     """Same step through the C++ engine with pinned HOST inputs/outputs
     (scout_engine_decode_step_host): H2D of q_true / q_pred / CPU partials in
     layer chunks on a copy stream, D2H of the attention output and of each
@@ -687,8 +687,9 @@ def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False):
         else:
             eng.decode_step_host(s, h_qt, h_qp, h_co, h_cm, h_out, h_oml, h_cpu_ids, h_n_cpu)
 
-    s0 = 10000  # after the device-path steps: the tier clock keeps moving forward
-    for s in range(3):
+    s0 = first_step  # right after the device-path steps: the tier clock moves on without a jump
+    warm = 5
+    for s in range(warm):
         one(s0 + s)
     eng.sync()
     torch.cuda.synchronize(dev)
@@ -696,7 +697,7 @@ def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     for s in range(steps):
-        one(s0 + 3 + s)
+        one(s0 + warm + s)
     eng.sync()
     b.record()
     torch.cuda.synchronize(dev)
