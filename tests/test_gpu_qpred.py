@@ -11,12 +11,14 @@ from paper_2603_27138_b200 import ops
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("hidden,n_out", [(256, 256), (640, 384)])
+@pytest.mark.parametrize("hidden,n_out", [(256, 256), (640, 384), (512, 256)])
 @pytest.mark.parametrize("batch", [1, 5, 32, 40])
-@pytest.mark.parametrize("max_ctas", [0, 2, 5])
+@pytest.mark.parametrize("max_ctas", [0, 2, 4, 5])
 def test_predict_query_vs_reference(cuda, hidden, n_out, batch, max_ctas):
     """max_ctas 0: one CTA per SM (tiles shared by several CTAs); 2 / 5: the
-    minimum grid (= tiles: whole tiles) and a grid that splits tiles unevenly."""
+    minimum grid (= tiles: whole tiles) and a grid that splits tiles unevenly;
+    4 with (512, 256): two CTAs per tile with an even chunk count, the cluster
+    pairs whose K halves meet in shared memory."""
     rng = np.random.default_rng(hidden + n_out + batch + 7 * max_ctas)
     w = torch.from_numpy(rng.standard_normal((hidden, n_out)).astype(np.float32) / np.sqrt(hidden)).bfloat16()
     x = rng.standard_normal((batch, hidden)).astype(np.float32) * 3.0
