@@ -349,7 +349,7 @@ __device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int j
 }
 
 // Register cap: a warp's registers come from its SM sub-partition's 16K file
-// (warp w -> SMSP w % 4), and with nine warps SMSP 0 hosts three of them. At
+// (warp w -> SMSP w % 4), and with nine or ten warps SMSP 0 hosts three. At
 // the 168 registers ptxas picks by itself, SMSP 0 had 256 registers left and
 // no 4-warp kernel (the tier bookkeeping that runs beside K2 on the post
 // stream) could launch next to K2 until it exited: the recalls then landed a
