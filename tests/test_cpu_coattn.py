@@ -30,7 +30,7 @@ def bf16_tile(x: np.ndarray) -> np.ndarray:
 
 @pytest.mark.parametrize("kernel", ["auto", "avx512"])
 @pytest.mark.parametrize("kv", ["bf16", "f32"])
-@pytest.mark.parametrize("G", [1, 4, 8])
+@pytest.mark.parametrize("G", [1, 2, 4, 8])
 def test_cpu_partial_attention_vs_oracle(kv, G, kernel, monkeypatch):
     if kernel == "avx512":
         if kv == "f32":

@@ -236,3 +236,21 @@ def _batch_vs_single():
             nr = int(r["n_res"][u])
             assert torch.equal(outs["rs"][i, u, :nr], r["res_slots"][u, :nr])
             assert torch.equal(outs["ci"][i, u, :n - nr], r["cpu_ids"][u, :n - nr])
+
+
+def test_topk_ring_path_parity(cuda):
+    """The bulk-copy ring (SCOUT_K1_DIRECT=0, read once per process) is no
+    longer the default for bf16 digests: run the oracle parity cases through it
+    in a subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("SCOUT_K1_DIRECT") == "0":
+        pytest.skip("already on the ring path")
+    here = os.path.dirname(__file__)
+    env = dict(os.environ, SCOUT_K1_DIRECT="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "test_gpu_topk.py", "-k",
+                        "split_vs_oracle or band_edges or many_blocks or bf16_queries"],
+                       cwd=here, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
