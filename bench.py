@@ -135,7 +135,7 @@ class Workload:
         self.q_pred = qp * (self.q_true.norm(dim=-1, keepdim=True) / qp.norm(dim=-1, keepdim=True))
         # queries in the model's dtype (q_dtype bf16: what a bf16 Qwen3 projection emits)
         self.q_true, self.q_pred = self.q_true.to(cfg["q_dtype"]), self.q_pred.to(cfg["q_dtype"])
-        self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev)
+        self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev).to(cfg.get("cpu_dtype", torch.float32))
         m = torch.randn(L, U * G, generator=g, device=dev)
         l = torch.rand(L, U * G, generator=g, device=dev) * 40 + 1
         self.cpu_ml = torch.stack([m, l], dim=-1).contiguous()
@@ -186,7 +186,7 @@ class Workload:
         self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=pool,
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
                                    recall_interval=cfg["recall"], host_tier=self.host_tier, host_staging=True,
-                                   q_dtype=cfg["q_dtype"])
+                                   q_dtype=cfg["q_dtype"], cpu_dtype=cfg.get("cpu_dtype", torch.float32))
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
 
@@ -197,7 +197,8 @@ class Workload:
         """Algorithmic bytes of one K2 launch: resident selected K+V rows, q in,
         CPU partial in, output out."""
         UG = self.U * self.G
-        return res_tokens_total * 2 * D * 2 + UG * (D * 4 + (D + 2) * 4 + (D + 2) * 4)
+        qb, cb = self.q_true.element_size(), self.cpu_o.element_size()
+        return res_tokens_total * 2 * D * 2 + UG * (D * qb + (D * cb + 8) + (D + 2) * 4)
 
 
 class TierWorkload:
@@ -256,7 +257,7 @@ class TierWorkload:
             self.q_path_t.append(qt.to(cfg["q_dtype"]))
             self.q_path_p.append(qp.to(cfg["q_dtype"]))
         self.q_true, self.q_pred = self.q_path_t[0], self.q_path_p[0]
-        self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev)
+        self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev).to(cfg.get("cpu_dtype", torch.float32))
         m = torch.randn(L, U * G, generator=g, device=dev)
         l = torch.rand(L, U * G, generator=g, device=dev) * 40 + 1
         self.cpu_ml = torch.stack([m, l], dim=-1).contiguous()
@@ -298,7 +299,8 @@ class TierWorkload:
         self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=self.pool,
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
                                    recall_interval=cfg["recall"], host_tier=self.host_tier, q_dtype=cfg["q_dtype"],
-                                   tier=self.tier, host_blocks=self.host_blocks, host_staging=True)
+                                   tier=self.tier, host_blocks=self.host_blocks, host_staging=True,
+                                   cpu_dtype=cfg.get("cpu_dtype", torch.float32))
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
 
@@ -309,7 +311,8 @@ class TierWorkload:
 
     def k2_bytes(self, res_tokens_total):
         UG = self.U * self.G
-        return res_tokens_total * 2 * D * 2 + UG * (D * 4 + (D + 2) * 4 + (D + 2) * 4)
+        qb, cb = self.q_path_t[0].element_size(), self.cpu_o.element_size()
+        return res_tokens_total * 2 * D * 2 + UG * (D * qb + (D * cb + 8) + (D + 2) * 4)
 
 
 def dist_setup():
@@ -506,9 +509,12 @@ def main():
                          "(PAPER.md:251), with every layer's recall moving real blocks each interval")
     ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
                     help="query dtype (q_true / q_pred); bf16 = the model's projection output")
+    ap.add_argument("--cpu-dtype", default="bf16", choices=["bf16", "f32"],
+                    help="CPU-partial o as the host worker hands it over (bf16 halves the largest H2D stream)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     cfg["q_dtype"] = torch.bfloat16 if args.q_dtype == "bf16" else torch.float32
+    cfg["cpu_dtype"] = torch.bfloat16 if args.cpu_dtype == "bf16" else torch.float32
     cfg["drift"] = args.drift
     if args.batch:
         cfg["batch"] = args.batch
@@ -635,7 +641,7 @@ def main():
             "config": {"workload": args.config, "attention_shape": "Qwen3-32B" if cfg["hq"] == 64 else "Qwen3-8B",
                        "batch_per_gpu": cfg["batch"], "global_batch": global_batch, "context": cfg["ctx"],
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "head_dim": D,
-                       "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "gpu_cache_blocks_per_unit": cfg["capacity"],
+                       "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "cpu_partial_dtype": args.cpu_dtype, "gpu_cache_blocks_per_unit": cfg["capacity"],
                        "cpu_blocks_per_unit": wl.cpu_per_unit, "recall_every": cfg["recall"],
                        "parallelism": f"request-sharded x{ws}, no collective",
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},

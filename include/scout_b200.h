@@ -388,6 +388,8 @@ typedef struct scout_engine_config {
      * no wrap; the bench bounds it and lets images alias).                 */
     const scout_tier_layer* tier;
     long long host_blocks;
+    int cpu_dtype;             /* CPU-partial o element type: SCOUT_F32 (0) or SCOUT_BF16 (half the
+                                * host-path bytes; its (max, denominator) pairs stay f32)        */
 } scout_engine_config;
 
 typedef struct scout_engine scout_engine;
@@ -395,10 +397,10 @@ typedef struct scout_engine scout_engine;
 int scout_engine_create(const scout_engine_config* cfg, const scout_layer_desc* layers, scout_engine** out);
 int scout_engine_destroy(scout_engine* eng);
 /* One decode step, device-resident inputs: q_true / q_pred [L][U*G][128] in
- * cfg.q_dtype, cpu_o [L][U*G][128], cpu_ml [L][U*G][2] f32; outputs out_o
+ * cfg.q_dtype, cpu_o [L][U*G][128] in cfg.cpu_dtype, cpu_ml [L][U*G][2] f32; outputs out_o
  * [L][U*G][128], out_ml [L][U*G][2] f32. */
 int scout_engine_decode_step(scout_engine* eng, int step, const void* q_true, const void* q_pred,
-                             const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml, void* stream);
+                             const void* cpu_o, const float* cpu_ml, float* out_o, float* out_ml, void* stream);
 /* Same step from pinned HOST buffers (same layouts): H2D of the inputs and
  * D2H of the outputs plus each layer's CPU-side block ids (h_cpu_ids
  * [L][U][k], h_n_cpu [L][U], the host co-attention worker's input) are
@@ -408,7 +410,7 @@ int scout_engine_decode_step(scout_engine* eng, int step, const void* q_true, co
  * overlap the previous step's attention), so the host inputs must be final
  * at the call and stay unchanged until `stream` completes the step. */
 int scout_engine_decode_step_host(scout_engine* eng, int step, const void* h_q_true, const void* h_q_pred,
-                                  const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o, float* h_out_ml,
+                                  const void* h_cpu_o, const float* h_cpu_ml, float* h_out_o, float* h_out_ml,
                                   int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream);
 /* Device tier mode: one decode step with the token's new K/V rows k_new /
  * v_new [L][U][128] f32 appended after each layer's attention (the order of
@@ -416,7 +418,7 @@ int scout_engine_decode_step_host(scout_engine* eng, int step, const void* h_q_t
  * attention + merge, append, recall). The other arguments as
  * scout_engine_decode_step. n_tokens (cfg) advances by one per step.      */
 int scout_engine_decode_step_kv(scout_engine* eng, int step, const void* q_true, const void* q_pred,
-                                const float* cpu_o, const float* cpu_ml, const float* k_new, const float* v_new,
+                                const void* cpu_o, const float* cpu_ml, const float* k_new, const float* v_new,
                                 float* out_o, float* out_ml, void* stream);
 /* Device tier mode from pinned HOST buffers (the pipeline of
  * scout_engine_decode_step_host plus h_k_new / h_v_new [L][U][128] f32).
@@ -425,7 +427,7 @@ int scout_engine_decode_step_kv(scout_engine* eng, int step, const void* q_true,
  * buffer it reads, and the previous step's output copies need not finish
  * before the next step's selection starts. */
 int scout_engine_decode_step_kv_host(scout_engine* eng, int step, const void* h_q_true, const void* h_q_pred,
-                                     const float* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
+                                     const void* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
                                      const float* h_v_new, float* h_out_o, float* h_out_ml, int32_t* h_cpu_ids,
                                      int32_t* h_n_cpu, void* stream);
 /* Order all outstanding side-stream work (recalls) before `stream`. */

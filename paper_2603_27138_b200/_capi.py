@@ -82,7 +82,7 @@ class EngineConfig(C.Structure):
         ("kv_pool", _vp), ("n_tokens", _vp), ("host_tier", _vp), ("max_ctas", C.c_int),
         ("host_staging", C.c_int), ("chunk_layers", C.c_int), ("recall_mode", C.c_int),
         ("q_dtype", C.c_int),
-    ("tier", _vp), ("host_blocks", C.c_longlong),
+        ("tier", _vp), ("host_blocks", C.c_longlong), ("cpu_dtype", C.c_int),
     ]
 
 

@@ -225,6 +225,7 @@ struct scout_engine {
 
     // ---------------------------------------------------------------- K1
     size_t qbytes() const { return cfg.q_dtype == SCOUT_BF16 ? 2 : 4; }
+    size_t cbytes() const { return cfg.cpu_dtype == SCOUT_BF16 ? 2 : 4; }  // CPU-partial o element bytes
     // layer l's query block of a [L][U*G][128] query array
     const void* qlayer(const void* q, int l) const {
         return static_cast<const uint8_t*>(q) + static_cast<size_t>(l) * UG * SCOUT_HEAD_DIM * qbytes();
@@ -273,7 +274,7 @@ struct scout_engine {
     }
 
     // ---------------------------------------------------------------- K2
-    int launch_k2(int par, const void* const* q, const float* const* co, const float* const* cml, float* const* o,
+    int launch_k2(int par, const void* const* q, const void* const* co, const float* const* cml, float* const* o,
                   float* const* ml, const unsigned* const* inflag, bool poll_k1, cudaStream_t st) {
         K2StepArgs a{};
         a.n_units = U;
@@ -291,6 +292,7 @@ struct scout_engine {
         a.token = token;
         a.max_ctas = cfg.max_ctas;
         a.q_bf16 = cfg.q_dtype == SCOUT_BF16;
+        a.cpu_bf16 = cfg.cpu_dtype == SCOUT_BF16;
         a.prof = k2_prof;
         static const int l2pf = [] {
             const char* e = getenv("SCOUT_K2_L2PF");
@@ -616,7 +618,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     const scout_engine_config& c = *cfg;
     if (c.layers <= 0 || c.layers > K2_MAX_LAYERS || c.batch <= 0 || c.hkv <= 0 || c.hq % c.hkv != 0 || c.k <= 0 ||
         c.nb_stride <= 0 || !c.kv_pool || !c.n_tokens || !(c.scale > 0.f) || c.kv_dtype != SCOUT_BF16 ||
-        (c.q_dtype != SCOUT_F32 && c.q_dtype != SCOUT_BF16)) {
+        (c.q_dtype != SCOUT_F32 && c.q_dtype != SCOUT_BF16) || (c.cpu_dtype != SCOUT_F32 && c.cpu_dtype != SCOUT_BF16)) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 KV)", K2_MAX_LAYERS);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
@@ -775,7 +777,7 @@ extern "C" int scout_engine_destroy(scout_engine* eng) {
 }
 
 extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q_true, const void* q_pred,
-                                        const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml,
+                                        const void* cpu_o, const float* cpu_ml, float* out_o, float* out_ml,
                                         void* stream) {
     if (!e || !q_true || !q_pred || !out_o || !out_ml || ((cpu_o == nullptr) != (cpu_ml == nullptr))) {
         scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_decode_step: null buffer");
@@ -792,11 +794,12 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q
     int rc = e->select_batch(0, L, q_true, q_pred, step, par, st);
     if (rc != SCOUT_OK) return rc;
     std::vector<const void*> q(L);
-    std::vector<const float*> co(L), cml(L);
+    std::vector<const void*> co(L);
+    std::vector<const float*> cml(L);
     std::vector<float*> o(L), ml(L);
     for (int i = 0; i < L; ++i) {
         q[i] = e->qlayer(q_true, i);
-        co[i] = cpu_o ? cpu_o + i * qd : nullptr;
+        co[i] = cpu_o ? static_cast<const uint8_t*>(cpu_o) + i * qd * e->cbytes() : nullptr;
         cml[i] = cpu_ml ? cpu_ml + i * md : nullptr;
         o[i] = out_o + i * qd;
         ml[i] = out_ml + i * md;
@@ -806,12 +809,12 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q
     return e->issue_recalls(step);
 }
 
-static int host_step(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred, const float* h_cpu_o,
+static int host_step(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred, const void* h_cpu_o,
                      const float* h_cpu_ml, const float* h_k_new, const float* h_v_new, float* h_out_o, float* h_out_ml,
                      int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream);
 
 extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred,
-                                             const float* h_cpu_o, const float* h_cpu_ml, float* h_out_o,
+                                             const void* h_cpu_o, const float* h_cpu_ml, float* h_out_o,
                                              float* h_out_ml, int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream) {
     if (e && e->tier_mode) {
         scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT,
@@ -823,7 +826,7 @@ extern "C" int scout_engine_decode_step_host(scout_engine* e, int step, const vo
 }
 
 extern "C" int scout_engine_decode_step_kv_host(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred,
-                                                const float* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
+                                                const void* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
                                                 const float* h_v_new, float* h_out_o, float* h_out_ml,
                                                 int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream) {
     if (!e || !e->tier_mode || !h_k_new || !h_v_new) {
@@ -835,7 +838,7 @@ extern "C" int scout_engine_decode_step_kv_host(scout_engine* e, int step, const
                      h_n_cpu, stream);
 }
 
-static int host_step(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred, const float* h_cpu_o,
+static int host_step(scout_engine* e, int step, const void* h_q_true, const void* h_q_pred, const void* h_cpu_o,
                      const float* h_cpu_ml, const float* h_k_new, const float* h_v_new, float* h_out_o, float* h_out_ml,
                      int32_t* h_cpu_ids, int32_t* h_n_cpu, void* stream) {
     if (!e || !e->stage[0].p || !h_q_true || !h_q_pred || !h_out_o || !h_out_ml ||
@@ -852,8 +855,9 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     const size_t qb = e->qbytes();  // query element bytes
     uint8_t* d_qt = static_cast<uint8_t*>(e->stage[par].p);
     uint8_t* d_qp = d_qt + L * qd * qb;
-    float* d_co = reinterpret_cast<float*>(d_qp + L * qd * qb);
-    float* d_cm = d_co + L * qd;
+    uint8_t* d_co = d_qp + L * qd * qb;  // CPU-partial o (cfg.cpu_dtype); sized for f32
+    const size_t cb = e->cbytes();
+    float* d_cm = reinterpret_cast<float*>(d_co + L * qd * 4);
     float* d_o = d_cm + L * md;
     float* d_oml = d_o + L * qd;
     float* d_kn = d_oml + L * md;  // device tier mode: the token's K/V rows
@@ -880,7 +884,8 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
         CU(cudaMemcpyAsync(d_qt + lq * qd * qb, hq_t + lq * qd * qb, (lo + n - lq) * qd * qb, cudaMemcpyHostToDevice,
                            e->h2d));
         if (h_cpu_o) {
-            CU(cudaMemcpyAsync(d_co + lo * qd, h_cpu_o + lo * qd, n * qd * 4, cudaMemcpyHostToDevice, e->h2d));
+            CU(cudaMemcpyAsync(d_co + lo * qd * cb, static_cast<const uint8_t*>(h_cpu_o) + lo * qd * cb, n * qd * cb,
+                               cudaMemcpyHostToDevice, e->h2d));
             CU(cudaMemcpyAsync(d_cm + lo * md, h_cpu_ml + lo * md, n * md * 4, cudaMemcpyHostToDevice, e->h2d));
         }
         if ((rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
@@ -915,12 +920,13 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     CU(cudaStreamWaitEvent(st, e->ev_k1_end, 0));
     // ---- K2: one launch; layer i waits for its input chunk's flag on the device
     std::vector<const void*> q(L);
-    std::vector<const float*> co(L), cml(L);
+    std::vector<const void*> co(L);
+    std::vector<const float*> cml(L);
     std::vector<float*> o(L), ml(L);
     std::vector<const unsigned*> inflag(L);
     for (int i = 0; i < L; ++i) {
         q[i] = d_qt + i * qd * qb;
-        co[i] = h_cpu_o ? d_co + i * qd : nullptr;
+        co[i] = h_cpu_o ? d_co + i * qd * cb : nullptr;
         cml[i] = h_cpu_ml ? d_cm + i * md : nullptr;
         o[i] = d_o + i * qd;
         ml[i] = d_oml + i * md;
@@ -954,7 +960,7 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
 }
 
 extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void* q_true, const void* q_pred,
-                                           const float* cpu_o, const float* cpu_ml, const float* k_new,
+                                           const void* cpu_o, const float* cpu_ml, const float* k_new,
                                            const float* v_new, float* out_o, float* out_ml, void* stream) {
     using scout_host::set_error;
     if (!e || !e->tier_mode || !q_true || !q_pred || !k_new || !v_new || !out_o || !out_ml ||
@@ -983,11 +989,12 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
     if (phases) cudaEventRecord(pe[1], st);
     // 4. attention + merge over all layers (one persistent launch)
     std::vector<const void*> q(L);
-    std::vector<const float*> co(L), cml(L);
+    std::vector<const void*> co(L);
+    std::vector<const float*> cml(L);
     std::vector<float*> o(L), ml(L);
     for (int i = 0; i < L; ++i) {
         q[i] = e->qlayer(q_true, i);
-        co[i] = cpu_o ? cpu_o + i * qd : nullptr;
+        co[i] = cpu_o ? static_cast<const uint8_t*>(cpu_o) + i * qd * e->cbytes() : nullptr;
         cml[i] = cpu_ml ? cpu_ml + i * md : nullptr;
         o[i] = out_o + i * qd;
         ml[i] = out_ml + i * md;

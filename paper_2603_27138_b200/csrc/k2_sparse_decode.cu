@@ -177,12 +177,22 @@ __device__ void finalize_unit(const float* cpu_o, const float* cpu_ml, float* ou
     }
 }
 
+// four channels d0..d0+3 of a CPU-partial row, f32 or bf16
+__device__ __forceinline__ float4 load_co(const void* cpu_o, size_t off, bool bf16) {
+    if (bf16) {
+        const uint2 w = *reinterpret_cast<const uint2*>(static_cast<const __nv_bfloat16*>(cpu_o) + off);
+        return make_float4(__uint_as_float(w.x << 16), __uint_as_float(w.x & 0xFFFF0000u), __uint_as_float(w.y << 16),
+                           __uint_as_float(w.y & 0xFFFF0000u));
+    }
+    return *reinterpret_cast<const float4*>(static_cast<const float*>(cpu_o) + off);
+}
+
 // finalize_unit for one warp (the combiner): lane owns channels 4*lane.. of
 // every head, and each phase issues all of its loads before using them, so a
 // unit costs ~2 L2 round trips per partial slot rather than one per head.
 template <int G>
-__device__ void finalize_unit_warp(const float* cpu_o, const float* cpu_ml, float* out_o, float* out_ml, int u,
-                                   const float* parts, int first_slot, int nslots, int lane) {
+__device__ void finalize_unit_warp(const void* cpu_o, bool co_bf16, const float* cpu_ml, float* out_o, float* out_ml,
+                                   int u, const float* parts, int first_slot, int nslots, int lane) {
     const int d0 = lane * 4;
     float M[G], cm[G], cl[G], L[G];
     float4 acc[G];
@@ -229,7 +239,7 @@ __device__ void finalize_unit_warp(const float* cpu_o, const float* cpu_ml, floa
         float4 co[G];
 #pragma unroll
         for (int h = 0; h < G; ++h)
-            co[h] = *reinterpret_cast<const float4*>(cpu_o + (static_cast<size_t>(u) * G + h) * D + d0);
+            co[h] = load_co(cpu_o, (static_cast<size_t>(u) * G + h) * D + d0, co_bf16);
 #pragma unroll
         for (int h = 0; h < G; ++h) {
             if (M[h] == -CUDART_INF_F || !(cl[h] > 0.f)) continue;
@@ -527,7 +537,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                         const size_t head = static_cast<size_t>(u) * G + hh;
                         cms[hh] = io.cpu_ml[head * 2] * LOG2E;
                         cls[hh] = io.cpu_ml[head * 2 + 1];
-                        cos_[hh] = *reinterpret_cast<const float4*>(io.cpu_o + head * D + d0);
+                        cos_[hh] = load_co(io.cpu_o, head * D + d0, a.cpu_bf16 != 0);
                     }
                 }
 #pragma unroll
@@ -583,7 +593,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                     if (last) {
                         // last CTA for unit u: its segments are CTAs cfirst..cfirst+nseg-1 at slots c+u
                         // (partials read with ld.global.cg: L2, never a stale L1 line)
-                        finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, sg.cfirst + u, sg.nseg, lane);
+                        finalize_unit_warp<G>(io.cpu_o, a.cpu_bf16 != 0, io.cpu_ml, io.o, io.ml, u, parts, sg.cfirst + u, sg.nseg, lane);
                         if (lane == 0) ctr[u] = 0;  // leave the counter zeroed for the next launch
                     }
                 }
@@ -594,11 +604,11 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             // listed by the planner (no n_res read on this path)
             if (P.nzero <= ZMAX) {
                 for (int i = cw; i < P.nzero; i += NCOMB)
-                    finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, P.zero_units[i], parts, 0, 0, lane);
+                    finalize_unit_warp<G>(io.cpu_o, a.cpu_bf16 != 0, io.cpu_ml, io.o, io.ml, P.zero_units[i], parts, 0, 0, lane);
             } else {
                 for (int u = blockIdx.x + cw * gridDim.x; u < nunits; u += NCOMB * gridDim.x) {
                     if (io.n_res[u] != 0) continue;
-                    finalize_unit_warp<G>(io.cpu_o, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, lane);
+                    finalize_unit_warp<G>(io.cpu_o, a.cpu_bf16 != 0, io.cpu_ml, io.o, io.ml, u, parts, 0, 0, lane);
                 }
             }
             // done with layer L: release the plan buffer; the last combiner counts

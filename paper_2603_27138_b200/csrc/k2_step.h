@@ -12,7 +12,7 @@ struct K2Layer {
     const int32_t* res_slots;
     const int32_t* res_ids;
     const int32_t* n_res;
-    const float* cpu_o;      // optional CPU partial
+    const void* cpu_o;       // optional CPU partial (f32, or bf16 when K2StepArgs::cpu_bf16)
     const float* cpu_ml;
     float* o;
     float* ml;
@@ -34,6 +34,7 @@ struct K2StepArgs {
     unsigned token;
     int max_ctas;
     int q_bf16;               // queries are bf16 (else f32)
+    int cpu_bf16;             // CPU partial o is bf16 (else f32); its (m, l) stay f32
     unsigned long long* prof; // optional [grid][16] cycle counters (SCOUT_K2_PROF diagnostics)
     int l2_prefetch;          // blocks the producer prefetches into L2 ahead of the ring (0: none)
     K2Layer layers[K2_MAX_LAYERS];

@@ -32,7 +32,7 @@ def _p(t):
 class DecodeEngine:
     def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
                  recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
-                 recall_mode=0, q_dtype=torch.float32, tier=None, host_blocks=0):
+                 recall_mode=0, q_dtype=torch.float32, tier=None, host_blocks=0, cpu_dtype=torch.float32):
         """tier: a tier.DeviceTieredCache whose state the engine drives on the
         device (device tier mode: decode_step_kv); host_tier then holds block
         images at ((layer*U + unit)*nb_stride + id) % host_blocks."""
@@ -51,12 +51,14 @@ class DecodeEngine:
         cfg.max_ctas, cfg.host_staging, cfg.chunk_layers = int(max_ctas), int(host_staging), int(chunk_layers)
         cfg.recall_mode = int(recall_mode)
         cfg.q_dtype = ops.dtype_code(q_dtype)
+        cfg.cpu_dtype = ops.dtype_code(cpu_dtype)  # CPU-partial o: f32 or bf16
         self.tier = tier
         if tier is not None:
             self._tier_descs = (A.TierLayer * layers)(*[tier.layer_desc(i) for i in range(layers)])
             cfg.tier = C.cast(self._tier_descs, C.c_void_p)
             cfg.host_blocks = int(host_blocks)
         self.q_dtype = q_dtype
+        self.cpu_dtype = cpu_dtype
         descs = (A.LayerDesc * layers)()
         for i, st in enumerate(layer_states):
             descs[i].digests, descs[i].block_table = _p(st.digests), _p(st.table)

@@ -14,7 +14,8 @@ from paper_2603_27138_b200.engine import DecodeEngine, LayerState
 pytestmark = pytest.mark.gpu
 
 
-def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True, q_dtype=torch.float32):
+def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True, q_dtype=torch.float32,
+          cpu_dtype=torch.float32):
     dev = torch.device("cuda")
     U = batch * hkv
     nbs = ((nb + 7) // 8) * 8
@@ -42,10 +43,10 @@ def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True, q_dtyp
     eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=n_tokens, pool=pool,
                        kv_dtype=torch.bfloat16, layer_states=layers, scale=1 / math.sqrt(D),
                        recall_interval=2 if recall else 0, host_tier=host if recall else None, host_staging=True,
-                       chunk_layers=2, q_dtype=q_dtype)
+                       chunk_layers=2, q_dtype=q_dtype, cpu_dtype=cpu_dtype)
     q_true = torch.randn(L, U * G, D, device=dev).to(q_dtype)
     q_pred = torch.randn(L, U * G, D, device=dev).to(q_dtype)
-    cpu_o = torch.randn(L, U * G, D, device=dev)
+    cpu_o = torch.randn(L, U * G, D, device=dev).to(cpu_dtype)
     cpu_ml = torch.stack([torch.randn(L, U * G, device=dev), torch.rand(L, U * G, device=dev) * 5 + 0.5], -1).contiguous()
     return dict(eng=eng, pool=pool, layers=layers, n_tokens=n_tokens, q_true=q_true, q_pred=q_pred, cpu_o=cpu_o,
                 cpu_ml=cpu_ml, L=L, U=U, G=G, k=k, host=host, sb=sb)
@@ -60,14 +61,17 @@ def reference_step(c):
         r = ops.score_topk_split(q_sel, st.digests, c["n_tokens"], c["k"], c["G"], block_table=st.table,
                                  k_stride=c["k"])
         o, ml = ops.sparse_decode(c["q_true"][li], c["pool"], torch.bfloat16, r["res_slots"], r["res_ids"],
-                                  r["n_res"], c["n_tokens"], c["G"], cpu_o=c["cpu_o"][li], cpu_ml=c["cpu_ml"][li])
+                                  r["n_res"], c["n_tokens"], c["G"], cpu_o=c["cpu_o"][li].float(), cpu_ml=c["cpu_ml"][li])
         outs.append((o, ml))
     return outs
 
 
+@pytest.mark.parametrize("cpu_dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("q_dtype", [torch.float32, torch.bfloat16])
-def test_engine_device_step_matches_per_layer_ops(cuda, q_dtype):
-    c = build(np.random.default_rng(11), recall=False, q_dtype=q_dtype)
+def test_engine_device_step_matches_per_layer_ops(cuda, q_dtype, cpu_dtype):
+    """cpu_dtype bf16: the CPU partial's o arrives as bf16 (K2 widens it exactly);
+    the per-layer reference gets the same values in f32."""
+    c = build(np.random.default_rng(11), recall=False, q_dtype=q_dtype, cpu_dtype=cpu_dtype)
     want = reference_step(c)
     out_o = torch.empty(c["q_true"].shape, device="cuda")
     out_ml = torch.empty(c["L"], c["U"] * c["G"], 2, device="cuda")
@@ -79,9 +83,10 @@ def test_engine_device_step_matches_per_layer_ops(cuda, q_dtype):
             assert torch.equal(out_ml[li], want[li][1]), (step, li)
 
 
+@pytest.mark.parametrize("cpu_dtype", [torch.float32, torch.bfloat16])
 @pytest.mark.parametrize("q_dtype", [torch.float32, torch.bfloat16])
-def test_engine_host_path_matches_device_path(cuda, q_dtype):
-    c = build(np.random.default_rng(12), recall=False, q_dtype=q_dtype)
+def test_engine_host_path_matches_device_path(cuda, q_dtype, cpu_dtype):
+    c = build(np.random.default_rng(12), recall=False, q_dtype=q_dtype, cpu_dtype=cpu_dtype)
     want = reference_step(c)
     pin = lambda t: t.cpu().pin_memory()  # noqa: E731
     h = [pin(c[n]) for n in ("q_true", "q_pred", "cpu_o", "cpu_ml")]

@@ -122,10 +122,12 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, recall, external)
         assert torch.equal(eng_side.dig[i], rep.dig[i])
 
 
-def test_engine_tier_host_path_matches_device_path(cuda):
+@pytest.mark.parametrize("cpu_dtype", [torch.float32, torch.bfloat16])
+def test_engine_tier_host_path_matches_device_path(cuda, cpu_dtype):
     """scout_engine_decode_step_kv_host (pinned host inputs and outputs,
     pipelined copies) against scout_engine_decode_step_kv on an identical
-    second cache: same outputs, same tier state, step after step."""
+    second cache: same outputs, same tier state, step after step (CPU
+    partials in f32 and in bf16, the bench's setting)."""
     rng = np.random.default_rng(5)
     L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 40
     U = batch * hkv
@@ -139,12 +141,12 @@ def test_engine_tier_host_path_matches_device_path(cuda):
         engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
                                  kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=4,
                                  host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, host_staging=True,
-                                 chunk_layers=2))
+                                 chunk_layers=2, cpu_dtype=cpu_dtype))
     out = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
     h_out = [torch.empty(L, U * G, D).pin_memory(), torch.empty(L, U * G, 2).pin_memory()]
     for step in range(1, steps + 1):
         ins = [torch.randn(L, U * G, D, device="cuda").bfloat16(), torch.randn(L, U * G, D, device="cuda").bfloat16(),
-               torch.randn(L, U * G, D, device="cuda"),
+               torch.randn(L, U * G, D, device="cuda").to(cpu_dtype),
                torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous(),
                torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")]
         engs[0].decode_step_kv(step, *ins, *out)
