@@ -186,7 +186,8 @@ class Workload:
         self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=pool,
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
                                    recall_interval=cfg["recall"], host_tier=self.host_tier, host_staging=True,
-                                   q_dtype=cfg["q_dtype"], cpu_dtype=cfg.get("cpu_dtype", torch.float32))
+                                   q_dtype=cfg["q_dtype"], cpu_dtype=cfg.get("cpu_dtype", torch.float32),
+                                   recall_stagger=cfg.get("recall_policy") == "stagger")
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
 
@@ -300,7 +301,8 @@ class TierWorkload:
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
                                    recall_interval=cfg["recall"], host_tier=self.host_tier, q_dtype=cfg["q_dtype"],
                                    tier=self.tier, host_blocks=self.host_blocks, host_staging=True,
-                                   cpu_dtype=cfg.get("cpu_dtype", torch.float32))
+                                   cpu_dtype=cfg.get("cpu_dtype", torch.float32),
+                                   recall_stagger=cfg.get("recall_policy") == "stagger")
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
 
@@ -509,6 +511,10 @@ def main():
                          "(PAPER.md:251), with every layer's recall moving real blocks each interval")
     ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
                     help="query dtype (q_true / q_pred); bf16 = the model's projection output")
+    ap.add_argument("--recall-policy", default="reference", choices=["reference", "stagger"],
+                    help="reference (default): every layer is due when step - last_recall >= 16 "
+                         "(recall.hpp:114-126), so all layers recall at steps 16, 32, ...; stagger: layer i "
+                         "recalls when (step + i) %% 16 == 0 (the same volume spread over the steps)")
     ap.add_argument("--cpu-dtype", default="bf16", choices=["bf16", "f32"],
                     help="CPU-partial o as the host worker hands it over (bf16 halves the largest H2D stream)")
     args = ap.parse_args()
@@ -516,6 +522,7 @@ def main():
     cfg["q_dtype"] = torch.bfloat16 if args.q_dtype == "bf16" else torch.float32
     cfg["cpu_dtype"] = torch.bfloat16 if args.cpu_dtype == "bf16" else torch.float32
     cfg["drift"] = args.drift
+    cfg["recall_policy"] = args.recall_policy
     if args.batch:
         cfg["batch"] = args.batch
     ws, rank, local = dist_setup()
@@ -643,6 +650,7 @@ def main():
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "head_dim": D,
                        "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "cpu_partial_dtype": args.cpu_dtype, "gpu_cache_blocks_per_unit": cfg["capacity"],
                        "cpu_blocks_per_unit": wl.cpu_per_unit, "recall_every": cfg["recall"],
+                       "recall_policy": args.recall_policy,
                        "parallelism": f"request-sharded x{ws}, no collective",
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},
             "step_gbs": step_gbs,

@@ -25,7 +25,8 @@
  *   KV pool    : slot-major array of blocks. Slot s holds K then V of one block
  *                (64 tokens x 128 channels). bf16 slots are 32 KiB, stored in the
  *                "half/slab/row" 128B-swizzled order (scout_kv_write_tokens
- *                writes it); f32 slots are 64 KiB, plain row-major.
+ *                writes it); f32 slots are 64 KiB, plain row-major. Slot
+                indices are < 2^26.
  *   digests    : per unit [2][128][nb_stride] (lo then hi, channel-major, block
  *                id fastest) in the KV dtype for minmax; [128][nb_stride] f64
  *                for the mean method.
@@ -59,6 +60,7 @@ enum scout_status {
 };
 
 enum scout_dtype { SCOUT_F32 = 0, SCOUT_BF16 = 1, SCOUT_F64 = 2 };
+#define SCOUT_TIER_ERR_SPLIT 3 /* scout_tier_layer.err: check_split failed (std::logic_error) */
 
 /* Launch flags. SCOUT_LAUNCH_PDL launches with programmatic stream
  * serialization: K1 scores before waiting on the preceding kernel (it only
@@ -209,6 +211,10 @@ typedef struct scout_decode_args {
 } scout_decode_args;
 
 size_t scout_sparse_decode_workspace_bytes(int n_units, int group, int max_ctas);
+/* CTAs the bf16 launch uses: max_ctas, or one persistent CTA per SM when 0
+ * (capped at 1024), whatever the unit count or list length: a CTA plans a
+ * range of any size in chunks. */
+int scout_sparse_decode_grid(int n_units, int k_stride, int max_ctas);
 int scout_sparse_decode(const scout_decode_args* args, void* stream);
 
 /* ------------------------------------------------------------------ K3 --
@@ -250,7 +256,8 @@ typedef struct scout_tier_layer {
     int32_t* free_slots;  /* [U][slots_per_unit] stack of free pool slots */
     int32_t* n_free;      /* [U] */
     int32_t* err;         /* [U] sticky first error of the unit (0 none): 1 invalid
-                             argument (reference throws std::invalid_argument), 2 out of slots */
+                             argument (reference throws std::invalid_argument), 2 out of slots,
+                             3 (engine) K1's split broke check_split (engine.hpp:317-329) */
     int capacity;         /* sealed fast blocks per unit; <= 0: pinned layer (pin_layer) */
     int slots_per_unit;
 } scout_tier_layer;
@@ -351,11 +358,11 @@ int scout_cpu_coattn_kernel(int kv_dtype);
  * predicted query (layer 0: K1 with the true query, pinned resident,
  * engine.hpp:227-233), K2+K3 for layer i with the true query over the
  * resident share chosen during layer i-1, merged with layer i's CPU partial;
- * then, every recall_interval steps (staggered: layer i recalls when
- * (step + i) % interval == 0), K4 moves that layer's recall plan host->device
- * on a side stream; layer i's next attention waits for it (issue (m, i) ->
- * visible (m+1, i), kv_store.hpp:175-218). The tier policy (which blocks go
- * where) stays with the caller: it owns the tables and recall plans.       */
+ * then, when layer i is due for a recall (the cadence below), K4 moves that
+ * layer's recall host->device on a side stream; layer i's next attention
+ * waits for it (issue (m, i) -> visible (m+1, i), kv_store.hpp:175-218).
+ * Static mode: the caller owns the tables and the recall plans. Device tier
+ * mode (cfg.tier): the engine runs the reference's policy on the device. */
 typedef struct scout_layer_desc {
     const void* digests;         /* [U][2][128][nb_stride] in kv dtype */
     const int32_t* block_table;  /* [U][nb_stride] slot or -1 (planning view) */
@@ -390,6 +397,27 @@ typedef struct scout_engine_config {
     long long host_blocks;
     int cpu_dtype;             /* CPU-partial o element type: SCOUT_F32 (0) or SCOUT_BF16 (half the
                                 * host-path bytes; its (max, denominator) pairs stay f32)        */
+    /* Recall cadence (engine.hpp:35, recall.hpp:97-126). recall_intervals
+     * (optional host array [layers], each >= 1; copied at create) gives each
+     * layer its calibrated interval; NULL: recall_interval for every layer.
+     * Layer i is due at step s when s - last_recall(i) >= interval(i), with
+     * last_recall = 0 at prefill (so at steps n, 2n, ...), and a due trigger
+     * resets the cadence even when it moves nothing. recall_stagger = 1 keeps
+     * round 1's staggered cadence instead ((s + i) % interval == 0, one
+     * interval for all layers): it spreads the PCIe traffic over the steps. */
+    const int32_t* recall_intervals;
+    int recall_stagger;
+    /* In-engine CPU co-attention (the reference's PrecomputeWorker,
+     * engine.hpp:88-150, 243-271), device tier mode host path only: 1 = the
+     * engine itself computes every step's CPU partials on cpu_threads host
+     * threads (0 = all) over the host tier, from the CPU-side ids K1 selects
+     * in THIS step and the step's predicted queries (layer i's partial with
+     * q_pred[i]), and publishes them layer chunk by layer chunk to the running
+     * K2, which merges each layer as soon as its chunk landed. The decode
+     * calls' cpu_o / cpu_ml inputs must then be NULL. 0 = the caller supplies
+     * the partials. */
+    int cpu_worker;
+    int cpu_threads;
 } scout_engine_config;
 
 typedef struct scout_engine scout_engine;
@@ -430,6 +458,12 @@ int scout_engine_decode_step_kv_host(scout_engine* eng, int step, const void* h_
                                      const void* h_cpu_o, const float* h_cpu_ml, const float* h_k_new,
                                      const float* h_v_new, float* h_out_o, float* h_out_ml, int32_t* h_cpu_ids,
                                      int32_t* h_n_cpu, void* stream);
+/* Device tier mode: the tier state's sticky per-unit errors (a rejected
+ * recall ticket, out of pool slots, a split that broke check_split,
+ * engine.hpp:317-329, checked after every step). Synchronises; returns
+ * SCOUT_OK, or SCOUT_ERR_INVALID_ARGUMENT / SCOUT_ERR_LOGIC naming the first
+ * (layer, unit) with an error. */
+int scout_engine_check_state(scout_engine* eng);
 /* Order all outstanding side-stream work (recalls) before `stream`. */
 int scout_engine_sync(scout_engine* eng, void* stream);
 /* Device tier mode: the caller changed the K5 state outside the engine
@@ -443,6 +477,9 @@ int scout_engine_tier_changed(scout_engine* eng);
  * call, then resets. */
 int scout_engine_set_timing(scout_engine* eng, int enable);
 int scout_engine_stats(scout_engine* eng, double* k2_ms_total, int* k2_count, long long* launches);
+/* In-engine CPU worker (cfg.cpu_worker): the wall time its partials took
+ * on the host pool, summed over the steps since the last call, then reset. */
+int scout_engine_worker_stats(scout_engine* eng, double* cpu_ms_total, int* steps);
 /* Device views of the engine's per-layer K1 outputs ([L][U][k] / [L][U]). */
 int scout_engine_k1_outputs(scout_engine* eng, int32_t** res_slots, int32_t** res_ids, int32_t** n_res,
                             int32_t** cpu_ids, int32_t** n_cpu, int32_t** res_tokens, int32_t** cpu_tokens);

@@ -91,6 +91,13 @@ def ref():
             L.ref_cache_place.argtypes = [vp, C.c_int, _dp, C.c_int]
             L.ref_cache_digests.argtypes = [vp, C.c_int, C.c_int, C.c_int, _dp]
             L.ref_predict_query.argtypes = [_dp, C.c_int, _dp, C.c_int, _dp]
+            if hasattr(L, "ref_recompute_layer_attention"):
+                L.ref_recompute_layer_attention.argtypes = [C.c_int, C.c_int, _dp, _dp, C.c_int, C.c_int, C.c_int, _dp,
+                                                            _dp, _ip, C.c_int, _ip, C.c_int, dbl, _dp]
+            L.ref_recall_new.argtypes = [C.c_int, C.c_int, _ip, dbl]
+            L.ref_recall_new.restype = vp
+            L.ref_recall_free.argtypes = [vp]
+            L.ref_maybe_schedule_recall.argtypes = [vp, C.c_int, C.c_int, ll, _ip, C.c_int, _ip, C.c_int, _ip]
         _c["r"] = L
     return _c["r"]
 
@@ -274,6 +281,51 @@ class RefCache:
         out = np.zeros((2, self.d, nb_stride))
         n = self.L.ref_cache_digests(self.h, layer, self.d, nb_stride, out)
         return out, n
+
+
+def recompute_layer_attention(keys, values, tokens_at_attention, q_true, q_pred, res_ids, cpu_ids, scale,
+                              block_size=64):
+    """The reference's hybrid-query oracle (harness.hpp:318-329) for G heads of
+    one unit: keys/values [n_rows][d] = the layer's whole K/V stream,
+    q_true/q_pred [G][d]. Returns [G][d] (checker only)."""
+    L = ref()
+    if L is None or not hasattr(L, "ref_recompute_layer_attention"):
+        raise RuntimeError("oracle/_ref built without harness.hpp (json.hpp missing)")
+    keys, values = f64(keys), f64(values)
+    qt, qp = f64(np.atleast_2d(q_true)), f64(np.atleast_2d(q_pred))
+    G, d = qt.shape
+    r = np.ascontiguousarray(res_ids, dtype=np.int32)
+    c = np.ascontiguousarray(cpu_ids, dtype=np.int32)
+    out = np.zeros((G, d))
+    if L.ref_recompute_layer_attention(d, block_size, keys, values, keys.shape[0], int(tokens_at_attention), G, qt, qp,
+                                       r, len(r), c, len(c), float(scale), out) != 0:
+        raise ValueError("recompute_layer_attention")
+    return out
+
+
+class RefRecall:
+    """The reference recall policy (recall.hpp:69-126: RecallSchedule +
+    maybe_schedule_recall) for n_units independent engines behind oracle/_ref
+    (checker only)."""
+
+    def __init__(self, n_units, intervals, beta=0.12):
+        self.L = ref()
+        if self.L is None:
+            raise RuntimeError("oracle/_ref/libscout_ref.so not built")
+        iv = np.ascontiguousarray(intervals, dtype=np.int32)
+        self.h = self.L.ref_recall_new(n_units, len(iv), iv, beta)
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_recall_free(self.h)
+
+    def maybe_schedule_recall(self, unit, layer, step, predicted, residency):
+        """None when the layer is not due, else set_difference(predicted, residency)."""
+        p = np.ascontiguousarray(predicted, dtype=np.int32)
+        r = np.ascontiguousarray(residency, dtype=np.int32)
+        out = np.zeros(max(len(p), 1), np.int32)
+        n = self.L.ref_maybe_schedule_recall(self.h, unit, layer, step, p, len(p), r, len(r), out)
+        return None if n < 0 else out[:n]
 
 
 def predict_query(x, w):

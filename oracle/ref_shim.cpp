@@ -20,6 +20,10 @@
 #include "scout/digest.hpp"
 #include "scout/kv_store.hpp"
 #include "scout/model.hpp"
+#include "scout/recall.hpp"
+#ifdef SCOUT_REF_HARNESS
+#include "scout/harness.hpp"  // recompute_layer_attention (needs nlohmann json.hpp on the include path)
+#endif
 
 using scout::BlockDigest;
 using scout::BlockIdSet;
@@ -391,5 +395,70 @@ int ref_predict_query(const double* x, int hidden, const double* w, int n_out, d
         return -1;
     }
 }
+
+// ---- recall policy (recall.hpp:69-126) for n_units independent reference
+// engines sharing one schedule: the oracle of the device tier mode's cadence
+// and recall set. intervals: [layers], each >= 1.
+struct RefRecall {
+    scout::RecallSchedule schedule;
+    std::vector<scout::RecallPolicyState> state;  // one per unit
+};
+void* ref_recall_new(int n_units, int layers, const int32_t* intervals, double beta) {
+    auto* r = new RefRecall();
+    r->schedule.intervals.assign(intervals, intervals + layers);
+    r->schedule.beta = beta;
+    r->state.assign(static_cast<size_t>(n_units), scout::RecallPolicyState(static_cast<size_t>(layers)));
+    return r;
+}
+void ref_recall_free(void* h) { delete static_cast<RefRecall*>(h); }
+// maybe_schedule_recall for one unit: -1 when the layer is not due (nullopt),
+// else the number of ids of set_difference(predicted, residency) written to out
+int ref_maybe_schedule_recall(void* h, int unit, int layer, long long step, const int32_t* pred, int n_pred,
+                              const int32_t* res, int n_res, int32_t* out) {
+    auto* r = static_cast<RefRecall*>(h);
+    const BlockIdSet p(pred, pred + n_pred), rs(res, res + n_res);
+    const auto ids = scout::maybe_schedule_recall(r->schedule, r->state.at(static_cast<size_t>(unit)),
+                                                  static_cast<size_t>(layer), static_cast<size_t>(step), p, rs);
+    if (!ids) return -1;
+    for (size_t i = 0; i < ids->size(); ++i) out[i] = static_cast<int32_t>((*ids)[i]);
+    return static_cast<int>(ids->size());
+}
+
+#ifdef SCOUT_REF_HARNESS
+// recompute_layer_attention (harness.hpp:318-329), the reference's hybrid-query
+// oracle of one decode layer, for the G query heads of one unit: the layer's
+// whole final K/V stream (n_rows rows, block_size-row blocks) goes into a
+// one-layer TieredKvCache; blocks that grew after the attention are truncated
+// back to tokens_at_attention; q_true over the resident set, q_pred over the
+// CPU set, merged and finalised (both empty -> zeros). out: [G][d]. Returns 0,
+// or -1 if the reference threw.
+int ref_recompute_layer_attention(int d, int block_size, const double* keys, const double* values, int n_rows,
+                                  int tokens_at_attention, int G, const double* q_true, const double* q_pred,
+                                  const int32_t* res_ids, int n_res, const int32_t* cpu_ids, int n_cpu, double scale,
+                                  double* out) {
+    try {
+        scout::TieredKvCache cache(1, static_cast<size_t>(block_size), static_cast<size_t>(d), scout::DigestMethod::minmax,
+                                   1u << 20);
+        for (int r = 0; r < n_rows; ++r)
+            cache.append_token(0, Vec(keys + static_cast<size_t>(r) * d, keys + static_cast<size_t>(r + 1) * d),
+                               Vec(values + static_cast<size_t>(r) * d, values + static_cast<size_t>(r + 1) * d));
+        scout::LayerMetrics lm;
+        lm.layer = 0;
+        lm.resident_set.assign(res_ids, res_ids + n_res);
+        lm.cpu_set.assign(cpu_ids, cpu_ids + n_cpu);
+        lm.tokens_at_attention = static_cast<size_t>(tokens_at_attention);
+        lm.attn_out.assign(static_cast<size_t>(d), 0.0);
+        for (int g = 0; g < G; ++g) {
+            lm.q_true.assign(q_true + static_cast<size_t>(g) * d, q_true + static_cast<size_t>(g + 1) * d);
+            lm.q_pred.assign(q_pred + static_cast<size_t>(g) * d, q_pred + static_cast<size_t>(g + 1) * d);
+            const Vec o = scout::recompute_layer_attention(cache, scale, lm);
+            std::memcpy(out + static_cast<size_t>(g) * d, o.data(), sizeof(double) * d);
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+#endif
 
 }  // extern "C"

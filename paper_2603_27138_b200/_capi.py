@@ -28,6 +28,7 @@ EXPORTED = (
     "scout_last_error", "scout_version", "scout_slot_bytes",
     "scout_kv_write_tokens", "scout_kv_read_tokens", "scout_digest_build", "scout_kv_append",
     "scout_score_topk_split", "scout_score_topk_split_batch", "scout_sparse_decode_workspace_bytes",
+    "scout_sparse_decode_grid",
     "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather", "scout_recall_copy",
     "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
     "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k1_outputs",
@@ -35,6 +36,7 @@ EXPORTED = (
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv",
     "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
+    "scout_engine_worker_stats", "scout_engine_check_state",
 )
 
 _vp = C.c_void_p
@@ -83,6 +85,7 @@ class EngineConfig(C.Structure):
         ("host_staging", C.c_int), ("chunk_layers", C.c_int), ("recall_mode", C.c_int),
         ("q_dtype", C.c_int),
         ("tier", _vp), ("host_blocks", C.c_longlong), ("cpu_dtype", C.c_int),
+        ("recall_intervals", _vp), ("recall_stagger", C.c_int), ("cpu_worker", C.c_int), ("cpu_threads", C.c_int),
     ]
 
 
@@ -134,6 +137,7 @@ def lib() -> C.CDLL:
         L.scout_score_topk_split_batch.argtypes = [C.POINTER(TopkArgs), C.c_int, _vp]
         L.scout_sparse_decode_workspace_bytes.restype = C.c_size_t
         L.scout_sparse_decode_workspace_bytes.argtypes = [C.c_int, C.c_int, C.c_int]
+        L.scout_sparse_decode_grid.argtypes = [C.c_int, C.c_int, C.c_int]
         L.scout_sparse_decode.argtypes = [C.POINTER(DecodeArgs), _vp]
         L.scout_merge_partials.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, C.c_int, _vp]
         L.scout_recall_gather.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp]
@@ -149,6 +153,8 @@ def lib() -> C.CDLL:
         L.scout_engine_set_timing.argtypes = [_vp, C.c_int]
         L.scout_engine_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]
         L.scout_engine_k1_outputs.argtypes = [_vp] + [C.POINTER(_vp)] * 7
+        L.scout_engine_worker_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]
+        L.scout_engine_check_state.argtypes = [_vp]
         _lib = L
     return _lib
 

@@ -37,6 +37,7 @@
 #include <vector>
 
 #include "../../include/scout_b200.h"
+#include "cpu_coattn.h"
 
 namespace scout_host {
 void set_error(int code, const char* fmt, ...);
@@ -116,10 +117,42 @@ struct Job {
     const int32_t* n_blocks;
     int k_stride, G;
     float scale;
-    const float* q;
-    float* o;
+    const void* q;   // f32, or bf16 when q_bf16
+    void* o;         // f32, or bf16 when o_bf16
     float* ml;
+    bool q_bf16, o_bf16;
 };
+
+inline float bf16_to_f(uint16_t h) {
+    const uint32_t u = static_cast<uint32_t>(h) << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+inline uint16_t f_to_bf16(float f) {  // round to nearest even (finite values)
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7F800000u) == 0x7F800000u) return static_cast<uint16_t>(u >> 16);  // inf / nan
+    return static_cast<uint16_t>((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+// unit u's G query rows as f32 (bf16 queries widened exactly into scratch)
+inline const float* unit_query(const Job& j, int u, float* scratch) {
+    const size_t off = static_cast<size_t>(u) * j.G * D;
+    if (!j.q_bf16) return static_cast<const float*>(j.q) + off;
+    const uint16_t* qb = static_cast<const uint16_t*>(j.q) + off;
+    for (int i = 0; i < j.G * D; ++i) scratch[i] = bf16_to_f(qb[i]);
+    return scratch;
+}
+// head h's normalised output row (K2's CPU-partial o) in the job's o dtype
+inline void store_o(const Job& j, size_t h, const float* acc, float inv) {
+    if (j.o_bf16) {
+        uint16_t* o = static_cast<uint16_t*>(j.o) + h * D;
+        for (int d = 0; d < D; ++d) o[d] = f_to_bf16(acc[d] * inv);
+    } else {
+        float* o = static_cast<float*>(j.o) + h * D;
+        for (int d = 0; d < D; ++d) o[d] = acc[d] * inv;
+    }
+}
 
 // Per block: the block's rows are decoded once (K and V into fp32), then for
 // each head: 64 scores, one block maximum, 64 exponentials and the weighted V
@@ -138,7 +171,8 @@ void run_unit(const Job& j, int u) {
         l[g] = 0.f;
         std::memset(acc[g], 0, sizeof(acc[g]));
     }
-    const float* qu = j.q + static_cast<size_t>(u) * G * D;
+    alignas(64) float qscratch[GMAX * D];
+    const float* qu = unit_query(j, u, qscratch);
     const int nb = j.n_blocks[u];
     for (int i = 0; i < nb; ++i) {
         const size_t idx = static_cast<size_t>(u) * j.k_stride + i;
@@ -182,7 +216,7 @@ void run_unit(const Job& j, int u) {
     for (int g = 0; g < G; ++g) {
         const size_t h = static_cast<size_t>(u) * G + g;
         const float inv = l[g] > 0.f ? 1.f / l[g] : 0.f;
-        for (int d = 0; d < D; ++d) j.o[h * D + d] = acc[g][d] * inv;
+        store_o(j, h, acc[g], inv);
         j.ml[h * 2] = l[g] > 0.f ? m[g] : -std::numeric_limits<float>::infinity();
         j.ml[h * 2 + 1] = l[g];
     }
@@ -308,7 +342,8 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
     // ---- Q^T -> VNNI B tiles: column n < 8 = hi of head n, 8 + n = lo of head n;
     // a VNNI word is the (2i, 2i+1) channel pair of one column
     std::memset(w.bq, 0, sizeof(w.bq));
-    const float* qu = j.q + static_cast<size_t>(u) * G * D;
+    alignas(64) float qscratch[GMAX * D];
+    const float* qu = unit_query(j, u, qscratch);
     const __m512 qs = _mm512_set1_ps(j.scale * LOG2E);
     const __m512i col = _mm512_mullo_epi32(_mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15),
                                            _mm512_set1_epi32(16));
@@ -474,7 +509,7 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
     for (int g = 0; g < G; ++g) {
         const size_t h = static_cast<size_t>(u) * G + g;
         const float inv = ll[g] > 0.f ? 1.f / ll[g] : 0.f;
-        for (int d = 0; d < D; ++d) j.o[h * D + d] = w.o[g][d] * inv;
+        store_o(j, h, w.o[g], inv);
         j.ml[h * 2] = ll[g] > 0.f ? mm[g] * LN2 : -std::numeric_limits<float>::infinity();
         j.ml[h * 2 + 1] = ll[g];
     }
@@ -583,25 +618,25 @@ bool has_avx512() {
 
 }  // namespace
 
-extern "C" int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, const int64_t* host_index,
-                                           const int32_t* block_rows, const int32_t* n_blocks, int k_stride,
-                                           const float* q, int group, float scale, int n_units, float* o, float* ml,
-                                           int threads) {
+int scout_cpu_coattn_run(const CpuCoattnArgs& a) {
     using scout_host::set_error;
-    if (n_units < 0 || k_stride <= 0 || group < 1 || group > GMAX || !(scale > 0.f) ||
-        (kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32) ||
-        (n_units > 0 && (!host_tier || !host_index || !n_blocks || !q || !o || !ml))) {
+    if (a.n_units < 0 || a.k_stride <= 0 || a.group < 1 || a.group > GMAX || !(a.scale > 0.f) ||
+        (a.kv_dtype != SCOUT_BF16 && a.kv_dtype != SCOUT_F32) || (a.q_dtype != SCOUT_F32 && a.q_dtype != SCOUT_BF16) ||
+        (a.o_dtype != SCOUT_F32 && a.o_dtype != SCOUT_BF16) ||
+        (a.n_units > 0 && (!a.host_tier || !a.host_index || !a.n_blocks || !a.q || !a.o || !a.ml))) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_cpu_partial_attention: bad arguments");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
-    if (n_units == 0) return SCOUT_OK;
-    const Job j{static_cast<const uint8_t*>(host_tier), kv_dtype, scout_slot_bytes(kv_dtype), host_index, block_rows,
-                n_blocks, k_stride, group, scale, q, o, ml};
-    int T = threads > 0 ? threads : static_cast<int>(std::thread::hardware_concurrency());
+    if (a.n_units == 0) return SCOUT_OK;
+    const Job j{static_cast<const uint8_t*>(a.host_tier), a.kv_dtype, scout_slot_bytes(a.kv_dtype), a.host_index,
+                a.block_rows, a.n_blocks, a.k_stride, a.group, a.scale, a.q, a.o, a.ml,
+                a.q_dtype == SCOUT_BF16, a.o_dtype == SCOUT_BF16};
+    const int n_units = a.n_units;
+    int T = a.threads > 0 ? a.threads : static_cast<int>(std::thread::hardware_concurrency());
     if (T < 1) T = 1;
     if (T > n_units) T = n_units;
     const char* env = std::getenv("SCOUT_CPU_AMX");
-    const bool amx = kv_dtype == SCOUT_BF16 && !(env && env[0] == '0') && amx_ready();
+    const bool amx = a.kv_dtype == SCOUT_BF16 && !(env && env[0] == '0') && amx_ready();
     const bool avx = has_avx512();
     std::atomic<int> next{0};
     const std::function<void()> work = [&] {
@@ -617,6 +652,29 @@ extern "C" int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, 
     if (T == 1) work();
     else pool().run(T, work);
     return SCOUT_OK;
+}
+
+extern "C" int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, const int64_t* host_index,
+                                           const int32_t* block_rows, const int32_t* n_blocks, int k_stride,
+                                           const float* q, int group, float scale, int n_units, float* o, float* ml,
+                                           int threads) {
+    CpuCoattnArgs a{};
+    a.host_tier = host_tier;
+    a.kv_dtype = kv_dtype;
+    a.host_index = host_index;
+    a.block_rows = block_rows;
+    a.n_blocks = n_blocks;
+    a.k_stride = k_stride;
+    a.q = q;
+    a.q_dtype = SCOUT_F32;
+    a.group = group;
+    a.scale = scale;
+    a.n_units = n_units;
+    a.o = o;
+    a.o_dtype = SCOUT_F32;
+    a.ml = ml;
+    a.threads = threads;
+    return scout_cpu_coattn_run(a);
 }
 
 extern "C" int scout_cpu_coattn_kernel(int kv_dtype) {

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
@@ -35,6 +36,7 @@
 #include <vector>
 
 #include "../../include/scout_b200.h"
+#include "cpu_coattn.h"
 #include "k1_batch.h"
 #include "k2_step.h"
 #include "k5_batch.h"
@@ -113,6 +115,9 @@ struct scout_engine {
     unsigned *k1_flag = nullptr, *k1_ctr = nullptr, *recall_flag = nullptr, *layer_done = nullptr, *in_flag = nullptr;
     unsigned token = 0;  // number of steps launched
     std::vector<unsigned> rc_token;  // per layer: token of its last recall (0: none)
+    // recall cadence (engine.hpp:35, recall.hpp:97-126): per-layer interval
+    // (0: never) and the step of the layer's last trigger (0: prefill)
+    std::vector<int> rc_int, last_recall;
     // recall plans (host arrays for the copy engines, device for the SM kernel)
     std::vector<std::vector<int64_t>> rc_src;
     std::vector<std::vector<int32_t>> rc_dst;
@@ -164,6 +169,7 @@ struct scout_engine {
     Buf plan_tab;                  // [L][U][nbs] residency planning view (K1's block tables)
     Buf open_slot, sealed_id;      // [L][U] append bookkeeping
     Buf tier_dst;                  // [L][U][k] recall destination slots
+    Buf tier_rc_ids, tier_rc_n;    // [L][U][k] / [L][U] the recalled ids (predicted \ residency)
     Buf tier_dev;                  // [L] scout_tier_layer (device copy for the multi-layer launches)
     uint8_t* host_dev = nullptr;   // device view of the pinned host tier
     std::vector<int> pending;      // per layer: ready tick of its in-flight recall ticket, -1 none
@@ -171,6 +177,35 @@ struct scout_engine {
     cudaEvent_t ev_side_end = nullptr, ev_kvin = nullptr;
     bool side_recorded = false;
     int tick(int step, int layer) const { return step * cfg.layers + layer; }
+    // ---- in-engine CPU co-attention worker (cfg.cpu_worker; the reference's
+    // PrecomputeWorker, engine.hpp:88-150): per step, once K1 has selected
+    // and its CPU-side ids are on the host, a worker thread computes layer
+    // chunk c's partials (q_pred over the host tier images) on the CPU pool,
+    // copies them into the step's device staging and publishes in_flag[c];
+    // the running K2 merges each chunk's layers as they land.
+    bool cw_on = false;
+    std::thread cw_thread;
+    std::mutex cw_mu;
+    std::condition_variable cw_cv, cw_done_cv;
+    struct CwJob {
+        unsigned token;
+        int par;
+        const void* h_q_pred;
+    };
+    std::deque<CwJob> cw_jobs;
+    bool cw_stop = false;
+    unsigned cw_done = 0;  // token of the last finished job
+    int cw_err = SCOUT_OK;
+    char cw_msg[256] = {0};
+    uint8_t* cw_pinned = nullptr;  // per parity: ids [L][U][k] | n [L][U] | o [L][UG][128] | ml [L][UG][2]
+    size_t cw_par_bytes = 0, cw_off_o = 0, cw_off_ml = 0;
+    cudaStream_t cw_s = nullptr;
+    cudaEvent_t cw_ids_ev[2] = {}, cw_qt_ev[2] = {}, cw_copy_ev[2] = {};
+    bool cw_copy_rec[2] = {false, false};  // worker thread only
+    std::vector<int64_t> cw_index;         // worker thread only: [L][U][k] host image indices
+    double cw_ms = 0.0;                    // CPU time of the worker's partials (summed, reset by stats)
+    int cw_steps = 0;
+
     // instrumentation
     bool timing = false;
     std::vector<cudaEvent_t> tev;
@@ -202,7 +237,13 @@ struct scout_engine {
     }
 
     ~scout_engine() {
+        stop_worker();
         stop_recalls();
+        if (cw_pinned) cudaFreeHost(cw_pinned);
+        if (cw_s) cudaStreamDestroy(cw_s);
+        for (auto* evs : {cw_ids_ev, cw_qt_ev, cw_copy_ev})
+            for (int i = 0; i < 2; ++i)
+                if (evs[i]) cudaEventDestroy(evs[i]);
         if (k2_prof) cudaFree(k2_prof);
         for (auto& row : ev_chunk)
             for (auto ev : row)
@@ -323,21 +364,34 @@ struct scout_engine {
     }
 
     // ---------------------------------------------------------------- K4
-    // recalls of this step: layer i recalls when (step + i) % interval == 0;
-    // the copy waits for every CTA to finish layer i of this launch
+    // Is layer i due for a recall at this step? The reference's trigger
+    // (maybe_schedule_recall, recall.hpp:114-126): step - last_recall >=
+    // interval, which resets the cadence even when nothing moves; or, opt-in,
+    // round 1's stagger (step + i) % interval == 0. Call once per (step, layer).
+    bool recall_due(int step, int i) {
+        const int n = rc_int[i];
+        if (n <= 0) return false;
+        if (cfg.recall_stagger) return (step + i) % n == 0;
+        if (step - last_recall[i] < n) return false;
+        last_recall[i] = step;
+        return true;
+    }
+    // A failure of the recall issuer thread (reported by the next call, before
+    // anything of that call is launched: the failed layer's flag was still
+    // published, so no K2 waits for it forever)
+    int issuer_status() {
+        std::lock_guard<std::mutex> lk(rc_mu);
+        if (rc_err == SCOUT_OK) return SCOUT_OK;
+        scout_host::set_error(rc_err, "recall issuer: %s", rc_msg);
+        return rc_err;
+    }
+    // static mode: the due layers' recall plans; the copy waits for every CTA
+    // to finish layer i of this launch
     int issue_recalls(int step) {
-        if (cfg.recall_interval <= 0) return SCOUT_OK;
-        {
-            std::lock_guard<std::mutex> lk(rc_mu);
-            if (rc_err != SCOUT_OK) {
-                scout_host::set_error(rc_err, "recall issuer: %s", rc_msg);
-                return rc_err;
-            }
-        }
         bool any = false;
         for (int i = 0; i < cfg.layers; ++i) {
             const scout_layer_desc& L = layers[i];
-            if (L.recall_n <= 0 || rc_src[i].empty() || (step + i) % cfg.recall_interval != 0) continue;
+            if (L.recall_n <= 0 || rc_src[i].empty() || !recall_due(step, i)) continue;
             rc_token[i] = token;  // the next step's K2 waits for it before streaming layer i
             std::lock_guard<std::mutex> lk(rc_mu);
             rc_jobs.push_back(RcJob{i, token, -1, 0});
@@ -373,6 +427,8 @@ struct scout_engine {
             rc_busy = true;
             lk.unlock();
             const int rc = job.slot < 0 ? run_recall(job.layer, job.token) : run_tier_recall(job);
+            if (rc != SCOUT_OK)  // publish the flag anyway: the next K2 must not wait for it forever
+                write_value(side, recall_flag + job.layer, job.token);
             lk.lock();
             rc_busy = false;
             if (job.slot >= 0 && --rc_slot_jobs[job.slot] == 0) rc_idle.notify_all();
@@ -428,6 +484,137 @@ struct scout_engine {
         }
         rc_cv.notify_all();
         rc_thread.join();
+    }
+
+    // ------------------------------------------------------ host staging
+    struct Stage {
+        uint8_t *qt, *qp, *co;
+        float *cm, *o, *oml, *kn, *vn;
+    };
+    // device staging of one step parity: q_true | q_pred (q dtype) | cpu_o
+    // (cpu dtype, sized for f32) | cpu_ml | out_o | out_ml | k_new | v_new
+    Stage stage_of(int par) const {
+        const size_t qd = static_cast<size_t>(UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(UG) * 2;
+        const size_t L = static_cast<size_t>(cfg.layers), qb = qbytes();
+        Stage g{};
+        g.qt = static_cast<uint8_t*>(stage[par].p);
+        g.qp = g.qt + L * qd * qb;
+        g.co = g.qp + L * qd * qb;
+        g.cm = reinterpret_cast<float*>(g.co + L * qd * 4);
+        g.o = g.cm + L * md;
+        g.oml = g.o + L * qd;
+        g.kn = g.oml + L * md;
+        g.vn = g.kn + L * U * SCOUT_HEAD_DIM;
+        return g;
+    }
+
+    // ------------------------------------------------------ CPU worker
+    int32_t* cw_ids(int par) const { return reinterpret_cast<int32_t*>(cw_pinned + par * cw_par_bytes); }
+    int32_t* cw_n(int par) const { return cw_ids(par) + static_cast<size_t>(cfg.layers) * U * cfg.k; }
+    uint8_t* cw_o(int par) const { return cw_pinned + par * cw_par_bytes + cw_off_o; }
+    float* cw_ml(int par) const { return reinterpret_cast<float*>(cw_pinned + par * cw_par_bytes + cw_off_ml); }
+    int worker_status() {
+        std::lock_guard<std::mutex> lk(cw_mu);
+        if (cw_err == SCOUT_OK) return SCOUT_OK;
+        scout_host::set_error(cw_err, "CPU co-attention worker: %s", cw_msg);
+        return cw_err;
+    }
+    void cw_loop() {
+        cudaSetDevice(device);
+        std::unique_lock<std::mutex> lk(cw_mu);
+        for (;;) {
+            cw_cv.wait(lk, [&] { return cw_stop || !cw_jobs.empty(); });
+            if (cw_jobs.empty()) break;  // stopping and drained
+            const CwJob job = cw_jobs.front();
+            cw_jobs.pop_front();
+            lk.unlock();
+            const int rc = cw_run(job);
+            lk.lock();
+            if (rc != SCOUT_OK && cw_err == SCOUT_OK) {
+                cw_err = rc;
+                std::snprintf(cw_msg, sizeof(cw_msg), "%s", scout_last_error());
+            }
+            cw_done = job.token;
+            cw_done_cv.notify_all();
+        }
+    }
+    // One step's CPU share, chunk by chunk (engine.hpp:243-251: layer i's task
+    // covers cpu[i] = predicted[i] \ residency with q_pred[i]). A failure still
+    // publishes the flags (with whatever the partials hold) so no K2 waits
+    // forever; the error is reported by the next call.
+    int cw_run(const CwJob& job) {
+        const int par = job.par, L = cfg.layers, CH = cfg.chunk_layers, k = cfg.k, nbs = cfg.nb_stride;
+        int rc = SCOUT_OK;
+        if (cudaEventSynchronize(cw_ids_ev[par]) != cudaSuccess ||
+            (cw_copy_rec[par] && cudaEventSynchronize(cw_copy_ev[par]) != cudaSuccess)) {
+            scout_host::set_error(SCOUT_ERR_CUDA, "CPU worker: %s", cudaGetErrorString(cudaGetLastError()));
+            rc = SCOUT_ERR_CUDA;
+        }
+        const Stage g = stage_of(par);
+        const size_t qd = static_cast<size_t>(UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(UG) * 2;
+        const int32_t* ids = cw_ids(par);
+        const int32_t* nn = cw_n(par);
+        double ms = 0.0;
+        for (int c = 0, lo = 0; lo < L; ++c, lo += CH) {
+            const int n = std::min(CH, L - lo);
+            if (rc == SCOUT_OK) {
+                const auto t0 = std::chrono::steady_clock::now();
+                for (int l = lo; l < lo + n; ++l)
+                    for (int u = 0; u < U; ++u) {
+                        const size_t row = (static_cast<size_t>(l) * U + u) * k;
+                        const long long base = (static_cast<long long>(l) * U + u) * nbs;
+                        for (int i = 0; i < nn[static_cast<size_t>(l) * U + u]; ++i) {
+                            long long hi = base + ids[row + i];
+                            if (cfg.host_blocks > 0) hi %= cfg.host_blocks;
+                            cw_index[row + i] = hi;
+                        }
+                    }
+                CpuCoattnArgs a{};
+                a.host_tier = cfg.host_tier;
+                a.kv_dtype = cfg.kv_dtype;
+                a.host_index = cw_index.data() + lk(lo);
+                a.n_blocks = nn + lu(lo);
+                a.k_stride = k;
+                a.q = static_cast<const uint8_t*>(job.h_q_pred) + lo * qd * qbytes();
+                a.q_dtype = cfg.q_dtype;
+                a.group = G;
+                a.scale = cfg.scale;
+                a.n_units = n * U;
+                a.o = cw_o(par) + lo * qd * cbytes();
+                a.o_dtype = cfg.cpu_dtype;
+                a.ml = cw_ml(par) + lo * md;
+                a.threads = cfg.cpu_threads;
+                rc = scout_cpu_coattn_run(a);
+                ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            }
+            if (cudaMemcpyAsync(g.co + lo * qd * cbytes(), cw_o(par) + lo * qd * cbytes(), n * qd * cbytes(),
+                                cudaMemcpyHostToDevice, cw_s) != cudaSuccess ||
+                cudaMemcpyAsync(g.cm + lo * md, cw_ml(par) + lo * md, n * md * 4, cudaMemcpyHostToDevice, cw_s) !=
+                    cudaSuccess) {
+                if (rc == SCOUT_OK) {
+                    scout_host::set_error(SCOUT_ERR_CUDA, "CPU worker copies: %s", cudaGetErrorString(cudaGetLastError()));
+                    rc = SCOUT_ERR_CUDA;
+                }
+            }
+            const int wr = write_value(cw_s, in_flag + c, job.token);
+            if (rc == SCOUT_OK) rc = wr;
+        }
+        if (cudaEventRecord(cw_copy_ev[par], cw_s) == cudaSuccess) cw_copy_rec[par] = true;
+        {
+            std::lock_guard<std::mutex> l(cw_mu);
+            cw_ms += ms;
+            ++cw_steps;
+        }
+        return rc;
+    }
+    void stop_worker() {
+        if (!cw_thread.joinable()) return;
+        {
+            std::lock_guard<std::mutex> lk(cw_mu);
+            cw_stop = true;
+        }
+        cw_cv.notify_all();
+        cw_thread.join();
     }
 
     // ------------------------------------------------------- device tier mode
@@ -500,11 +687,18 @@ struct scout_engine {
         for (int i = 0; i < L; ++i) pa.digests[i] = const_cast<void*>(layers[i].digests);
         pa.host_tier = host_dev;
         pa.host_blocks = cfg.host_blocks;
+        pa.sel_ids = I(sel_ids[par]);
+        pa.n_sel = I(n_sel[par]);
+        pa.rc_ids = I(tier_rc_ids);
+        pa.rc_n = I(tier_rc_n);
+        pa.dst = I(tier_dst);
+        pa.res_ids = I(res_ids[par]);
+        pa.n_res = I(n_res[par]);
         pa.cpu_ids = I(cpu_ids[par]);
         pa.n_cpu = I(n_cpu[par]);
-        pa.dst = I(tier_dst);
-        for (int i = 0; i < L; ++i)
-            pa.recall_due[i] = cfg.recall_interval > 0 && (step + i) % cfg.recall_interval == 0;
+        pa.res_tok = I(res_tok[par]);
+        pa.cpu_tok = I(cpu_tok[par]);
+        for (int i = 0; i < L; ++i) pa.recall_due[i] = recall_due(step, i);
         pa.plan_out = I(plan_tab);  // the next step's planning view (K1 of this step has read its own)
         pa.plan_step = step + 1;
         const bool ce = cfg.recall_mode == 0 && rc_pinned != nullptr;
@@ -538,9 +732,9 @@ struct scout_engine {
                 CU(cudaStreamWaitEvent(rc_list, ev_chunk[slot][c], 0));
                 for (int i = lo; i < lo + n; ++i) {
                     if (!pa.recall_due[i]) continue;
-                    CU(cudaMemcpyAsync(hid + lk(i), pa.cpu_ids + lk(i), static_cast<size_t>(U) * cfg.k * 4,
+                    CU(cudaMemcpyAsync(hid + lk(i), pa.rc_ids + lk(i), static_cast<size_t>(U) * cfg.k * 4,
                                        cudaMemcpyDeviceToHost, rc_list));
-                    CU(cudaMemcpyAsync(hn + lu(i), pa.n_cpu + lu(i), static_cast<size_t>(U) * 4, cudaMemcpyDeviceToHost,
+                    CU(cudaMemcpyAsync(hn + lu(i), pa.rc_n + lu(i), static_cast<size_t>(U) * 4, cudaMemcpyDeviceToHost,
                                        rc_list));
                     CU(cudaMemcpyAsync(hd + lk(i), pa.dst + lk(i), static_cast<size_t>(U) * cfg.k * 4,
                                        cudaMemcpyDeviceToHost, rc_list));
@@ -563,7 +757,7 @@ struct scout_engine {
                     ++launches;
                     if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier,
                                                       static_cast<long long>(i) * U * nbs, nbs, cfg.host_blocks, U,
-                                                      pa.cpu_ids + lk(i), pa.n_cpu + lu(i), pa.dst + lk(i), cfg.k, 0,
+                                                      pa.rc_ids + lk(i), pa.rc_n + lu(i), pa.dst + lk(i), cfg.k, 0,
                                                       side)) != SCOUT_OK)
                         return rc;
                     if ((rc = write_value(side, recall_flag + i, tok)) != SCOUT_OK) return rc;
@@ -617,12 +811,36 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     }
     const scout_engine_config& c = *cfg;
     if (c.layers <= 0 || c.layers > K2_MAX_LAYERS || c.batch <= 0 || c.hkv <= 0 || c.hq % c.hkv != 0 || c.k <= 0 ||
-        c.nb_stride <= 0 || !c.kv_pool || !c.n_tokens || !(c.scale > 0.f) || c.kv_dtype != SCOUT_BF16 ||
-        (c.q_dtype != SCOUT_F32 && c.q_dtype != SCOUT_BF16) || (c.cpu_dtype != SCOUT_F32 && c.cpu_dtype != SCOUT_BF16)) {
-        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 KV)", K2_MAX_LAYERS);
+        c.k > SCOUT_MAX_K || c.nb_stride <= 0 || !c.kv_pool || !c.n_tokens || !(c.scale > 0.f) ||
+        c.kv_dtype != SCOUT_BF16 || (c.q_dtype != SCOUT_F32 && c.q_dtype != SCOUT_BF16) ||
+        (c.cpu_dtype != SCOUT_F32 && c.cpu_dtype != SCOUT_BF16) || c.recall_interval < 0) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 KV, k 1..%d)",
+                  K2_MAX_LAYERS, SCOUT_MAX_K);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
-    if ((c.recall_interval > 0 || c.tier) && !c.host_tier) {
+    if (const int G = c.hq / c.hkv; G != 1 && G != 2 && G != 4 && G != 8) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: GQA group %d not in {1,2,4,8}", G);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (c.recall_intervals)
+        for (int l = 0; l < c.layers; ++l)
+            if (c.recall_intervals[l] < 1) {  // engine.hpp:177-178
+                set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: recall interval of layer %d must be >= 1", l);
+                return SCOUT_ERR_INVALID_ARGUMENT;
+            }
+    if (c.tier && c.tier[0].capacity > 0) {
+        // layer 0 is pinned resident (engine.hpp:181): its begin_layer tickets are
+        // applied after the step's selection, which only a pinned layer allows
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: device tier mode needs layer 0 pinned (capacity <= 0)");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    const bool any_recall = c.recall_interval > 0 || c.recall_intervals != nullptr;
+    if (c.cpu_worker && (!c.tier || !c.host_staging || !c.host_tier || c.cpu_threads < 0)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT,
+                  "scout_engine_create: cpu_worker needs device tier mode, host_staging and a host tier");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if ((any_recall || c.tier) && !c.host_tier) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: recall needs a host tier");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
@@ -680,6 +898,9 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     e->layer_done = f + 3 * c.layers;
     e->in_flag = f + 4 * c.layers;
     e->rc_token.assign(c.layers, 0u);
+    e->rc_int.assign(c.layers, 0);
+    for (int l = 0; l < c.layers; ++l) e->rc_int[l] = c.recall_intervals ? c.recall_intervals[l] : c.recall_interval;
+    e->last_recall.assign(c.layers, 0);
     e->rc_src.resize(c.layers);
     e->rc_dst.resize(c.layers);
     e->rc_dev = std::vector<Buf>(c.layers);
@@ -710,7 +931,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         e->tier.assign(c.tier, c.tier + c.layers);
         const size_t lu = static_cast<size_t>(c.layers) * e->U;
         if (e->plan_tab.alloc(lu * c.nb_stride * 4) || e->open_slot.alloc(lu * 4) || e->sealed_id.alloc(lu * 4) ||
-            e->tier_dst.alloc(lu * c.k * 4) || cudaEventCreateWithFlags(&e->ev_side_end, cudaEventDisableTiming) ||
+            e->tier_dst.alloc(lu * c.k * 4) || e->tier_rc_ids.alloc(lu * c.k * 4) || e->tier_rc_n.alloc(lu * 4) ||
+            cudaEventCreateWithFlags(&e->ev_side_end, cudaEventDisableTiming) ||
             cudaEventCreateWithFlags(&e->ev_kvin, cudaEventDisableTiming)) {
             delete e;
             set_error(SCOUT_ERR_CUDA, "scout_engine_create: tier-mode allocation failed");
@@ -732,7 +954,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         e->host_dev = static_cast<uint8_t*>(hv);
     }
     cudaGetDevice(&e->device);
-    if (c.tier && c.recall_interval > 0 && c.recall_mode == 0) {
+    if (c.tier && any_recall && c.recall_mode == 0) {
         e->rc_slot_bytes = (static_cast<size_t>(c.layers) * e->U * (2 * c.k + 1) * 4 + 255) / 256 * 256;
         if (cudaHostAlloc(reinterpret_cast<void**>(&e->rc_pinned), e->rc_slot_bytes * scout_engine::RC_SLOTS,
                           cudaHostAllocDefault) != cudaSuccess) {
@@ -751,7 +973,32 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         cudaEventCreateWithFlags(&e->ev_pre, cudaEventDisableTiming);
         cudaStreamCreateWithFlags(&e->post_s, cudaStreamNonBlocking);
     }
-    if (c.recall_interval > 0) e->rc_thread = std::thread([e] { e->recall_loop(); });
+    if (any_recall) e->rc_thread = std::thread([e] { e->recall_loop(); });
+    if (c.cpu_worker) {
+        const size_t L = c.layers, U = e->U, UG = e->UG, D = SCOUT_HEAD_DIM;
+        auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+        e->cw_off_o = up(L * U * c.k * 4 + L * U * 4);
+        e->cw_off_ml = e->cw_off_o + up(L * UG * D * e->cbytes());
+        e->cw_par_bytes = e->cw_off_ml + up(L * UG * 2 * 4);
+        bool ok = cudaHostAlloc(reinterpret_cast<void**>(&e->cw_pinned), 2 * e->cw_par_bytes, cudaHostAllocDefault) ==
+                  cudaSuccess;
+        if (!ok) e->cw_pinned = nullptr;
+        ok = ok && cudaStreamCreateWithFlags(&e->cw_s, cudaStreamNonBlocking) == cudaSuccess;
+        for (int i = 0; i < 2 && ok; ++i)
+            ok = cudaEventCreateWithFlags(&e->cw_ids_ev[i], cudaEventDisableTiming | cudaEventBlockingSync) ==
+                     cudaSuccess &&
+                 cudaEventCreateWithFlags(&e->cw_qt_ev[i], cudaEventDisableTiming) == cudaSuccess &&
+                 cudaEventCreateWithFlags(&e->cw_copy_ev[i], cudaEventDisableTiming | cudaEventBlockingSync) ==
+                     cudaSuccess;
+        if (!ok) {
+            delete e;
+            set_error(SCOUT_ERR_CUDA, "scout_engine_create: CPU worker buffers");
+            return SCOUT_ERR_CUDA;
+        }
+        e->cw_index.assign(L * U * c.k, 0);
+        e->cw_on = true;
+        e->cw_thread = std::thread([e] { e->cw_loop(); });
+    }
     e->ev_k1.resize(c.layers);
     for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     e->chunk_ev.resize(e->nch);
@@ -768,6 +1015,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
 
 extern "C" int scout_engine_destroy(scout_engine* eng) {
     if (eng) {
+        eng->stop_worker();      // finishes the queued CPU partials (their flags) first
         eng->stop_recalls();     // drains the queued recalls first
         cudaDeviceSynchronize();  // flags / copies still reference engine memory
         if (eng->k2_prof) eng->report_k2_prof();
@@ -783,12 +1031,16 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q
         scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_decode_step: null buffer");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
+    if (e->cw_on) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "cpu_worker engine: use scout_engine_decode_step_kv_host");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
     auto st = static_cast<cudaStream_t>(stream);
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
     const int L = e->cfg.layers;
+    if (const int rc = e->issuer_status(); rc != SCOUT_OK) return rc;
     const unsigned token = ++e->token;
     const int par = token & 1;
-    (void)token;
     // K1 for every layer in one wide launch (bandwidth-bound, the whole GPU),
     // then the persistent K2 over all layers; stream order is the dependency
     int rc = e->select_batch(0, L, q_true, q_pred, step, par, st);
@@ -847,24 +1099,32 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
                               "scout_engine_decode_step_host: null buffer or engine created without host_staging");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
+    if (e->cw_on && h_cpu_o) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT,
+                              "scout_engine_decode_step_kv_host: the engine computes the CPU partials (cpu_worker): "
+                              "pass h_cpu_o = h_cpu_ml = NULL");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (const int rc = e->issuer_status(); rc != SCOUT_OK) return rc;
+    if (e->cw_on)
+        if (const int rc = e->worker_status(); rc != SCOUT_OK) return rc;
     auto st = static_cast<cudaStream_t>(stream);
     const int L = e->cfg.layers, CH = e->cfg.chunk_layers, nch = e->nch;
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
     const unsigned token = ++e->token;
     const int par = token & 1;
     const size_t qb = e->qbytes();  // query element bytes
-    uint8_t* d_qt = static_cast<uint8_t*>(e->stage[par].p);
-    uint8_t* d_qp = d_qt + L * qd * qb;
-    uint8_t* d_co = d_qp + L * qd * qb;  // CPU-partial o (cfg.cpu_dtype); sized for f32
     const size_t cb = e->cbytes();
-    float* d_cm = reinterpret_cast<float*>(d_co + L * qd * 4);
-    float* d_o = d_cm + L * md;
-    float* d_oml = d_o + L * qd;
-    float* d_kn = d_oml + L * md;  // device tier mode: the token's K/V rows
-    float* d_vn = d_kn + static_cast<size_t>(L) * e->U * SCOUT_HEAD_DIM;
+    const scout_engine::Stage g = e->stage_of(par);
     const size_t kvn = static_cast<size_t>(L) * e->U * SCOUT_HEAD_DIM * 4;
     const uint8_t* hq_t = static_cast<const uint8_t*>(h_q_true);
     const uint8_t* hq_p = static_cast<const uint8_t*>(h_q_pred);
+    if (e->cw_on) {
+        // the worker's pinned buffers and events of this parity belong to the
+        // step two back until its job is done
+        std::unique_lock<std::mutex> lk(e->cw_mu);
+        e->cw_done_cv.wait(lk, [&] { return token < 3 || e->cw_done + 2 >= token; });
+    }
     int rc = e->begin_step(st, par);
     if (rc != SCOUT_OK) return rc;
     // ---- inputs, in the order the device needs them: q_true of layer 0 and
@@ -873,26 +1133,31 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     // flag the (already running) persistent K2 polls before planning a layer.
     // The sources are host memory, so the copies only wait for this parity's
     // staging to be free (step n-2 fully done): step n's inputs stream in
-    // while step n-1's K2 still runs.
+    // while step n-1's K2 still runs. With the in-engine CPU worker the
+    // partials come from the worker, which publishes the chunk flags.
     if (e->stage_recorded[par]) CU(cudaStreamWaitEvent(e->h2d, e->stage_free[par], 0));
-    CU(cudaMemcpyAsync(d_qt, hq_t, qd * qb, cudaMemcpyHostToDevice, e->h2d));
-    CU(cudaMemcpyAsync(d_qp + qd * qb, hq_p + qd * qb, (L - 1) * qd * qb, cudaMemcpyHostToDevice, e->h2d));
+    CU(cudaMemcpyAsync(g.qt, hq_t, qd * qb, cudaMemcpyHostToDevice, e->h2d));
+    CU(cudaMemcpyAsync(g.qp + qd * qb, hq_p + qd * qb, (L - 1) * qd * qb, cudaMemcpyHostToDevice, e->h2d));
     CU(cudaEventRecord(e->chunk_ev[0], e->h2d));
     for (int c = 0; c < nch; ++c) {
         const int lo = c * CH, n = (c + 1) * CH > L ? L - lo : CH;
         const int lq = c == 0 ? 1 : lo;  // layer 0's q_true went first
-        CU(cudaMemcpyAsync(d_qt + lq * qd * qb, hq_t + lq * qd * qb, (lo + n - lq) * qd * qb, cudaMemcpyHostToDevice,
+        CU(cudaMemcpyAsync(g.qt + lq * qd * qb, hq_t + lq * qd * qb, (lo + n - lq) * qd * qb, cudaMemcpyHostToDevice,
                            e->h2d));
         if (h_cpu_o) {
-            CU(cudaMemcpyAsync(d_co + lo * qd * cb, static_cast<const uint8_t*>(h_cpu_o) + lo * qd * cb, n * qd * cb,
+            CU(cudaMemcpyAsync(g.co + lo * qd * cb, static_cast<const uint8_t*>(h_cpu_o) + lo * qd * cb, n * qd * cb,
                                cudaMemcpyHostToDevice, e->h2d));
-            CU(cudaMemcpyAsync(d_cm + lo * md, h_cpu_ml + lo * md, n * md * 4, cudaMemcpyHostToDevice, e->h2d));
+            CU(cudaMemcpyAsync(g.cm + lo * md, h_cpu_ml + lo * md, n * md * 4, cudaMemcpyHostToDevice, e->h2d));
         }
-        if ((rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
+        if (!e->cw_on && (rc = write_value(e->h2d, e->in_flag + c, token)) != SCOUT_OK) return rc;
+    }
+    if (e->cw_on) {  // the worker's flags follow every q_true copy of the step
+        CU(cudaEventRecord(e->cw_qt_ev[par], e->h2d));
+        CU(cudaStreamWaitEvent(e->cw_s, e->cw_qt_ev[par], 0));
     }
     if (e->tier_mode) {  // the token's K/V, needed after the attention
-        CU(cudaMemcpyAsync(d_kn, h_k_new, kvn, cudaMemcpyHostToDevice, e->h2d));
-        CU(cudaMemcpyAsync(d_vn, h_v_new, kvn, cudaMemcpyHostToDevice, e->h2d));
+        CU(cudaMemcpyAsync(g.kn, h_k_new, kvn, cudaMemcpyHostToDevice, e->h2d));
+        CU(cudaMemcpyAsync(g.vn, h_v_new, kvn, cudaMemcpyHostToDevice, e->h2d));
         CU(cudaEventRecord(e->ev_kvin, e->h2d));
     }
     // ---- K1 for every layer in one launch once q_pred landed (in steady state
@@ -901,35 +1166,46 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     // application (the previous step's bookkeeping is ordered by ev_start)
     CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[0], 0));
     if (e->tier_mode) {
-        rc = e->tier_pre(step, par, d_qt, d_qp, e->k1s);
+        rc = e->tier_pre(step, par, g.qt, g.qp, e->k1s);
         if (rc == SCOUT_OK && cudaEventRecord(e->ev_pre, e->k1s) != cudaSuccess) rc = SCOUT_ERR_CUDA;
     } else {
-        rc = e->select_batch(0, L, d_qt, d_qp, step, par, e->k1s);
+        rc = e->select_batch(0, L, g.qt, g.qp, step, par, e->k1s);
     }
     if (rc != SCOUT_OK) return rc;
-    if (h_cpu_ids) {
+    const size_t id_bytes = static_cast<size_t>(L) * e->U * e->cfg.k * 4, n_bytes = static_cast<size_t>(L) * e->U * 4;
+    if (h_cpu_ids || e->cw_on) {
         CU(cudaEventRecord(e->ev_k1[0], e->k1s));
         CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[0], 0));
-        CU(cudaMemcpyAsync(h_cpu_ids, e->I(e->cpu_ids[par]), static_cast<size_t>(L) * e->U * e->cfg.k * 4,
-                           cudaMemcpyDeviceToHost, e->d2h));
-        if (h_n_cpu)
-            CU(cudaMemcpyAsync(h_n_cpu, e->I(e->n_cpu[par]), static_cast<size_t>(L) * e->U * 4, cudaMemcpyDeviceToHost,
-                               e->d2h));
+    }
+    if (e->cw_on) {  // the worker's input: this step's CPU-side ids, then the job
+        CU(cudaMemcpyAsync(e->cw_ids(par), e->I(e->cpu_ids[par]), id_bytes, cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaMemcpyAsync(e->cw_n(par), e->I(e->n_cpu[par]), n_bytes, cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaEventRecord(e->cw_ids_ev[par], e->d2h));
+        {
+            std::lock_guard<std::mutex> lk(e->cw_mu);
+            e->cw_jobs.push_back(scout_engine::CwJob{token, par, h_q_pred});
+        }
+        e->cw_cv.notify_one();
+    }
+    if (h_cpu_ids) {
+        CU(cudaMemcpyAsync(h_cpu_ids, e->I(e->cpu_ids[par]), id_bytes, cudaMemcpyDeviceToHost, e->d2h));
+        if (h_n_cpu) CU(cudaMemcpyAsync(h_n_cpu, e->I(e->n_cpu[par]), n_bytes, cudaMemcpyDeviceToHost, e->d2h));
     }
     CU(cudaEventRecord(e->ev_k1_end, e->k1s));
     CU(cudaStreamWaitEvent(st, e->ev_k1_end, 0));
     // ---- K2: one launch; layer i waits for its input chunk's flag on the device
+    const bool have_cpu = h_cpu_o != nullptr || e->cw_on;
     std::vector<const void*> q(L);
     std::vector<const void*> co(L);
     std::vector<const float*> cml(L);
     std::vector<float*> o(L), ml(L);
     std::vector<const unsigned*> inflag(L);
     for (int i = 0; i < L; ++i) {
-        q[i] = d_qt + i * qd * qb;
-        co[i] = h_cpu_o ? d_co + i * qd * cb : nullptr;
-        cml[i] = h_cpu_ml ? d_cm + i * md : nullptr;
-        o[i] = d_o + i * qd;
-        ml[i] = d_oml + i * md;
+        q[i] = g.qt + i * qd * qb;
+        co[i] = have_cpu ? g.co + i * qd * cb : nullptr;
+        cml[i] = have_cpu ? g.cm + i * md : nullptr;
+        o[i] = g.o + i * qd;
+        ml[i] = g.oml + i * md;
         inflag[i] = e->in_flag + i / CH;
     }
     if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), false, st)) !=
@@ -937,7 +1213,7 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
         return rc;
     if (e->tier_mode) {
         CU(cudaStreamWaitEvent(e->post_s, e->ev_kvin, 0));  // the token's K/V landed
-        if ((rc = e->tier_post(step, par, token, d_kn, d_vn, e->ev_pre, st)) != SCOUT_OK) return rc;
+        if ((rc = e->tier_post(step, par, token, g.kn, g.vn, e->ev_pre, st)) != SCOUT_OK) return rc;
     } else if ((rc = e->issue_recalls(step)) != SCOUT_OK) {
         return rc;
     }
@@ -948,8 +1224,8 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
         const int n = lo + OUT_CH > L ? L - lo : OUT_CH;
         if ((rc = wait_value(e->d2h, e->layer_done + lo + n - 1, token * static_cast<unsigned>(e->grid))) != SCOUT_OK)
             return rc;
-        CU(cudaMemcpyAsync(h_out_o + lo * qd, d_o + lo * qd, n * qd * 4, cudaMemcpyDeviceToHost, e->d2h));
-        CU(cudaMemcpyAsync(h_out_ml + lo * md, d_oml + lo * md, n * md * 4, cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaMemcpyAsync(h_out_o + lo * qd, g.o + lo * qd, n * qd * 4, cudaMemcpyDeviceToHost, e->d2h));
+        CU(cudaMemcpyAsync(h_out_ml + lo * md, g.oml + lo * md, n * md * 4, cudaMemcpyDeviceToHost, e->d2h));
     }
     CU(cudaEventRecord(e->ev_tmp, e->d2h));
     CU(cudaStreamWaitEvent(st, e->ev_tmp, 0));
@@ -968,6 +1244,11 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_decode_step_kv: null buffer or engine without tier state");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
+    if (e->cw_on) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "cpu_worker engine: use scout_engine_decode_step_kv_host");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (const int rc = e->issuer_status(); rc != SCOUT_OK) return rc;
     auto st = static_cast<cudaStream_t>(stream);
     const int L = e->cfg.layers;
     const size_t qd = static_cast<size_t>(e->UG) * SCOUT_HEAD_DIM, md = static_cast<size_t>(e->UG) * 2;
@@ -1021,10 +1302,19 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
 extern "C" int scout_engine_sync(scout_engine* e, void* stream) {
     if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
     auto st = static_cast<cudaStream_t>(stream);
+    if (e->cw_on) {  // every queued CPU share computed and its copies enqueued
+        std::unique_lock<std::mutex> lk(e->cw_mu);
+        e->cw_done_cv.wait(lk, [&] { return e->cw_jobs.empty() && e->cw_done == e->token; });
+    }
     e->drain_recalls();
     CU(cudaEventRecord(e->ev_tmp, e->side));
     CU(cudaStreamWaitEvent(st, e->ev_tmp, 0));
-    return SCOUT_OK;
+    if (e->cw_on) {
+        CU(cudaEventRecord(e->ev_tmp, e->cw_s));
+        CU(cudaStreamWaitEvent(st, e->ev_tmp, 0));
+        if (const int rc = e->worker_status(); rc != SCOUT_OK) return rc;
+    }
+    return e->issuer_status();
 }
 
 extern "C" int scout_engine_tier_changed(scout_engine* e) {
@@ -1054,6 +1344,36 @@ extern "C" int scout_engine_stats(scout_engine* e, double* k2_ms_total, int* k2_
     if (launches) *launches = e->launches;
     e->tev_used = 0;
     e->launches = 0;
+    return SCOUT_OK;
+}
+
+extern "C" int scout_engine_check_state(scout_engine* e) {
+    if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
+    if (!e->tier_mode) return SCOUT_OK;
+    CU(cudaDeviceSynchronize());
+    std::vector<int32_t> err(static_cast<size_t>(e->U));
+    for (int l = 0; l < e->cfg.layers; ++l) {
+        CU(cudaMemcpy(err.data(), e->tier[l].err, err.size() * 4, cudaMemcpyDeviceToHost));
+        for (int u = 0; u < e->U; ++u) {
+            if (err[u] == 0) continue;
+            const char* what = err[u] == SCOUT_ERR_INVALID_ARGUMENT ? "recall ticket rejected (schedule_recall)"
+                               : err[u] == SCOUT_TIER_ERR_SPLIT   ? "split broke check_split (engine.hpp:317-329)"
+                                                                  : "out of pool slots";
+            const int code = err[u] == SCOUT_ERR_INVALID_ARGUMENT ? SCOUT_ERR_INVALID_ARGUMENT : SCOUT_ERR_LOGIC;
+            scout_host::set_error(code, "tier state: layer %d unit %d: %s", l, u, what);
+            return code;
+        }
+    }
+    return SCOUT_OK;
+}
+
+extern "C" int scout_engine_worker_stats(scout_engine* e, double* cpu_ms_total, int* steps) {
+    if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(e->cw_mu);
+    if (cpu_ms_total) *cpu_ms_total = e->cw_ms;
+    if (steps) *steps = e->cw_steps;
+    e->cw_ms = 0.0;
+    e->cw_steps = 0;
     return SCOUT_OK;
 }
 

@@ -68,24 +68,39 @@ constexpr int NCOMB = 2;                    // combiner warps (segments alternat
 constexpr int NTHREADS = NCT + 32 * (2 + NCOMB);  // + producer, planner and combiner warps
 constexpr int NST = 2 * NPAIR;              // ring stages
 constexpr int STAGE_BYTES = 32768;          // one block: K tile (16 KiB) + V tile (16 KiB)
-constexpr int MAXSEG = 64;                  // units touched by one CTA range
-constexpr int MAXB = 384;                   // blocks per CTA range per layer
+constexpr int MAXSEG = 64;                  // segments per plan chunk
+constexpr int MAXB = 384;                   // blocks per plan chunk
 constexpr int CB_ROW = D;  // combine rows (no pad: the conflicted state stores are once per segment)
 constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES;
 
+// A segment piece: blocks [j0, j1) of unit `unit`'s resident list. A CTA's
+// segment of a unit that does not fit the rest of a plan chunk is split over
+// consecutive chunks; the consumers carry its softmax state in registers from
+// a piece marked SEG_CONT_NEXT to the next one (marked SEG_CONT_PREV).
+constexpr int SEG_CONT_PREV = 1, SEG_CONT_NEXT = 2;
 struct Seg {
-    int unit, j0, j1, nseg, cfirst, f0;  // f0: first block of the segment in the layer's CTA list
+    int unit, j0, j1, nseg, cfirst, f0;  // f0: first block of the piece in the chunk's block list
+    int cont;
 };
 
-// A layer's work list for this CTA, built by the planner warp one layer ahead
-// (double-buffered), consumed by the consumer warps.
+// One plan chunk: a piece of this CTA's share of one layer (at most MAXSEG
+// segment pieces and MAXB blocks; a layer's share is one or more chunks, so a
+// range of any length or unit count is planned whole). Built by the planner
+// warp ahead of the consumers (double-buffered).
 constexpr int ZMAX = 16;  // units without a resident block this CTA finalizes, listed in the plan
+constexpr int CH_FIRST = 1, CH_LAST = 2;  // first / last chunk of its layer
+// A plan entry packs the pool slot (< 2^26: 2 TiB of 32 KiB slots, more than
+// any device holds) with the block's valid rows - 1 (0..63).
+constexpr int BLK_ROWS_SHIFT = 26;
+constexpr uint32_t BLK_SLOT_MASK = (1u << BLK_ROWS_SHIFT) - 1u;
+__device__ __forceinline__ size_t blk_slot(uint32_t e) { return e & BLK_SLOT_MASK; }
+__device__ __forceinline__ int blk_rows(uint32_t e) { return static_cast<int>(e >> BLK_ROWS_SHIFT) + 1; }
 struct Plan {
     Seg segs[MAXSEG];
-    int blk_slot[MAXB];      // resident blocks in stream order: pool slot
-    int16_t blk_rows[MAXB];  // valid rows (64, or the open block's fill)
-    int zero_units[ZMAX];    // units u == blockIdx.x (mod grid) with no resident block
+    uint32_t blk[MAXB];      // resident blocks in stream order: pool slot | (valid rows - 1) << 26
+    int zero_units[ZMAX];    // first chunk: units u == blockIdx.x (mod grid) with no resident block
     int nsegs, nblk, jbase, nzero;  // nzero > ZMAX: scan n_res instead
+    int layer, flags;
 };
 
 struct Smem {
@@ -109,11 +124,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
-}
-__device__ __forceinline__ unsigned long long global_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
 }
 // Spin until *p >= token (wrap-safe). A flag that never arrives (a producer
 // that cannot be scheduled) traps after 10 s instead of hanging the device.
@@ -261,13 +271,70 @@ __device__ void finalize_unit_warp(const void* cpu_o, bool co_bf16, const float*
     }
 }
 
-// Planner (one warp): this CTA's share of layer io's resident blocks.
+// ---------------------------------------------------------------- planner
+// The plan buffer of chunk c, once every role has released its previous use.
+__device__ __forceinline__ Plan& plan_acquire(Smem& sm, int c, long long& waited, bool prof) {
+    const long long t0 = prof ? clock64() : 0;
+    if (c >= 2) mbar_wait(&sm.plan_empty[c & 1], ((c >> 1) - 1) & 1);
+    if (prof) waited += clock64() - t0;
+    return sm.plan[c & 1];
+}
+
+// Finish chunk c (its segment pieces are written): pull the query rows of the
+// segments starting here into L2, fill the block list (pool slot, valid rows)
+// and publish it to the producer, consumers and combiners.
+__device__ void plan_publish(const K2StepArgs& a, const K2Layer& io, Smem& sm, int c, int nseg, int nblk, int jbase,
+                             int layer, int flags, int lane) {
+    Plan& P = sm.plan[c & 1];
+    __syncwarp();  // lane 0's segment records
+    {
+        const int qbytes = a.group * D * (a.q_bf16 ? 2 : 4);
+        const int lines = (qbytes + 127) / 128;
+        for (int i = lane; i < nseg * lines; i += 32) {
+            const int si = i / lines, li = i % lines;
+            if (P.segs[si].cont & SEG_CONT_PREV) continue;
+            const uint8_t* qp = static_cast<const uint8_t*>(io.q) +
+                                static_cast<size_t>(P.segs[si].unit) * qbytes + static_cast<size_t>(li) * 128;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
+        }
+    }
+    for (int f = lane; f < nblk; f += 32) {
+        int lo = 0, hi = nseg - 1;  // the last piece with f0 <= f (f0 ascending)
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (P.segs[mid].f0 <= f) lo = mid;
+            else hi = mid - 1;
+        }
+        const Seg sg = P.segs[lo];
+        const size_t idx = static_cast<size_t>(sg.unit) * a.k_stride + sg.j0 + (f - sg.f0);
+        const int nt = a.n_tokens[sg.unit];
+        const int nb = (nt + BS - 1) / BS;
+        const int rows = (io.res_ids[idx] == nb - 1) ? nt - (nb - 1) * BS : BS;  // the open block's fill
+        P.blk[f] = static_cast<uint32_t>(io.res_slots[idx]) | (static_cast<uint32_t>(rows - 1) << BLK_ROWS_SHIFT);
+    }
+    if (lane == 0) {
+        P.nsegs = nseg;
+        P.nblk = nblk;
+        P.jbase = jbase;
+        P.layer = layer;
+        P.flags = flags;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.plan_full[c & 1]);
+}
+
+// Planner (one warp): this CTA's share of layer `layer`'s resident blocks, as
+// one or more plan chunks (c: chunk counter, j: CTA-global block stream index).
 // Stream-K: the concatenation of every unit's resident block list is cut into
 // geff = min(grid, T) equal ranges (every range non-empty, so a unit's segment
 // count is the number of CTAs between the ones holding its first and last
-// block); segment (cta c, unit u) owns partial slot c+u.
-__device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int jbase, int lane) {
+// block); segment (cta c, unit u) owns partial slot c+u. A range may touch any
+// number of units and hold any number of blocks: pieces go into chunks of at
+// most MAXSEG pieces / MAXB blocks, a segment split at a chunk boundary.
+__device__ void plan_layer(const K2StepArgs& a, const K2Layer& io, Smem& sm, int layer, int& c, int& j, int lane,
+                           long long& waited) {
     const int nunits = a.n_units;
+    Plan* P = &plan_acquire(sm, c, waited, a.prof != nullptr);
     long long T = 0;
     {
         int loc = 0, nz = 0;
@@ -279,21 +346,20 @@ __device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int j
             const bool z = u < nunits && n == 0 && u % static_cast<int>(gridDim.x) == static_cast<int>(blockIdx.x);
             const unsigned bz = __ballot_sync(0xffffffffu, z);
             const int pos = nz + __popc(bz & ((1u << lane) - 1u));
-            if (z && pos < ZMAX) P.zero_units[pos] = u;
+            if (z && pos < ZMAX) P->zero_units[pos] = u;
             nz += __popc(bz);
         }
-        if (lane == 0) P.nzero = nz;
+        if (lane == 0) P->nzero = nz;
 #pragma unroll
         for (int o = 16; o; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
         T = loc;
     }
     const long long grid = T < static_cast<long long>(gridDim.x) ? (T > 0 ? T : 1) : gridDim.x;
-    const long long c = blockIdx.x;
-    const long long lo = c < grid ? T * c / grid : T, hi = c < grid ? T * (c + 1) / grid : T;
+    const long long cta = blockIdx.x;
+    const long long lo = cta < grid ? T * cta / grid : T, hi = cta < grid ? T * (cta + 1) / grid : T;
     long long run = 0;
-    int nseg = 0, frun = 0;
-    const unsigned lt = (1u << lane) - 1u;
-    for (int base = 0; base < nunits; base += 32) {
+    int nseg = 0, nblk = 0, jb = j, first = CH_FIRST;
+    for (int base = 0; base < nunits && run < hi; base += 32) {
         const int u = base + lane;
         const int n = u < nunits ? io.n_res[u] : 0;
         int incl = n;
@@ -305,57 +371,48 @@ __device__ void make_plan(const K2StepArgs& a, const K2Layer& io, Plan& P, int j
         const long long pre = run + incl - n;
         const long long s0 = max(pre, lo), s1 = min(pre + n, hi);
         const bool has = n > 0 && s0 < s1;
-        const int len = has ? static_cast<int>(s1 - s0) : 0;
-        int lincl = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, lincl, o);
-            if (lane >= o) lincl += y;
-        }
-        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        int my_j0 = 0, my_j1 = 0, my_nseg = 0, my_cf = 0;
         if (has) {
-            const int pos = nseg + __popc(bal & lt);
+            my_j0 = static_cast<int>(s0 - pre);
+            my_j1 = static_cast<int>(s1 - pre);
             const long long cf = ((pre + 1) * grid - 1) / T;  // CTA holding position p: floor(((p+1)*grid-1)/T)
             const long long cl = ((pre + n) * grid - 1) / T;
-            if (pos < MAXSEG)
-                P.segs[pos] = Seg{u, static_cast<int>(s0 - pre), static_cast<int>(s1 - pre),
-                                  static_cast<int>(cl - cf + 1), static_cast<int>(cf), frun + lincl - len};
+            my_nseg = static_cast<int>(cl - cf + 1);
+            my_cf = static_cast<int>(cf);
         }
-        nseg += __popc(bal);
-        frun += __shfl_sync(0xffffffffu, lincl, 31);
+        unsigned bal = __ballot_sync(0xffffffffu, has);
+        while (bal) {  // this CTA's segments of the 32 units, in unit order
+            const int src = __ffs(bal) - 1;
+            bal &= bal - 1;
+            int j0 = __shfl_sync(0xffffffffu, my_j0, src);
+            const int j1 = __shfl_sync(0xffffffffu, my_j1, src);
+            const int ns = __shfl_sync(0xffffffffu, my_nseg, src);
+            const int cf = __shfl_sync(0xffffffffu, my_cf, src);
+            int cont = 0;
+            while (j0 < j1) {
+                if (nseg == MAXSEG || nblk == MAXB) {  // chunk full: publish, continue in the next
+                    plan_publish(a, io, sm, c, nseg, nblk, jb, layer, first, lane);
+                    ++c;
+                    first = 0;
+                    jb += nblk;
+                    nseg = nblk = 0;
+                    P = &plan_acquire(sm, c, waited, a.prof != nullptr);
+                    if (lane == 0) P->nzero = 0;
+                }
+                const int take = min(j1 - j0, MAXB - nblk);
+                if (lane == 0)
+                    P->segs[nseg] = Seg{base + src, j0, j0 + take, ns, cf, nblk, cont | (take < j1 - j0 ? SEG_CONT_NEXT : 0)};
+                ++nseg;
+                nblk += take;
+                j0 += take;
+                cont = SEG_CONT_PREV;
+            }
+        }
         run += __shfl_sync(0xffffffffu, incl, 31);
     }
-    nseg = min(nseg, MAXSEG);
-    const int nblk = min(static_cast<int>(hi - lo), MAXB);
-    __syncwarp();
-    // the consumers load each segment's query at its start: pull the rows
-    // into L2 now, a layer ahead (one 128-byte line per lane and step)
-    {
-        const int qbytes = a.group * D * (a.q_bf16 ? 2 : 4);
-        const int lines = (qbytes + 127) / 128;
-        for (int i = lane; i < nseg * lines; i += 32) {
-            const int si = i / lines, li = i % lines;
-            const uint8_t* qp = static_cast<const uint8_t*>(io.q) +
-                                static_cast<size_t>(P.segs[si].unit) * qbytes + static_cast<size_t>(li) * 128;
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
-        }
-    }
-    for (int f = lane; f < nblk; f += 32) {
-        int si = 0;
-        while (si + 1 < nseg && P.segs[si + 1].f0 <= f) ++si;
-        const Seg sg = P.segs[si];
-        const size_t idx = static_cast<size_t>(sg.unit) * a.k_stride + sg.j0 + (f - sg.f0);
-        const int nt = a.n_tokens[sg.unit];
-        const int nb = (nt + BS - 1) / BS;
-        P.blk_slot[f] = io.res_slots[idx];
-        P.blk_rows[f] = static_cast<int16_t>((io.res_ids[idx] == nb - 1) ? nt - (nb - 1) * BS : BS);
-    }
-    if (lane == 0) {
-        P.nsegs = nseg;
-        P.nblk = nblk;
-        P.jbase = jbase;
-    }
-    __syncwarp();
+    plan_publish(a, io, sm, c, nseg, nblk, jb, layer, first | CH_LAST, lane);
+    ++c;
+    j = jb + nblk;
 }
 
 // Register cap: a warp's registers come from its SM sub-partition's 16K file
@@ -400,25 +457,21 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
         // dependent global round trips: inline in the producer it left the
         // ring draining at every layer boundary, ~20% at config 2)
         int j = 0;  // CTA-global block stream index (continues across layers)
+        int c = 0;  // plan chunk counter (continues across layers)
         long long w_empty = 0, w_plan = 0, tq = 0;  // SCOUT_K2_PROF: waiting for a free plan buffer, planning
         for (int L = 0; L < a.n_layers; ++L) {
-            const int b = L & 1;
             const K2Layer& io = a.layers[L];
             if (a.prof) tq = clock64();
-            if (L >= 2) mbar_wait(&sm.plan_empty[b], ((L >> 1) - 1) & 1);
-            if (a.prof) { const long long t1 = clock64(); w_empty += t1 - tq; tq = t1; }
             if (lane == 0) {
                 // K1 published layer L's lists / the layer's inputs landed
                 if (a.k1_flag) wait_flag(a.k1_flag + L, a.token);
                 if (io.in_flag) wait_flag(io.in_flag, a.token);
             }
             __syncwarp();
-            make_plan(a, io, sm.plan[b], j, lane);
-            j += sm.plan[b].nblk;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sm.plan_full[b]);
+            plan_layer(a, io, sm, L, c, j, lane, w_empty);
             if (a.prof) w_plan += clock64() - tq;
         }
+        w_plan -= w_empty;
         if (a.prof && lane == 0) {
             unsigned long long* pr = a.prof + blockIdx.x * 16;
             atomicAdd(pr + 10, static_cast<unsigned long long>(w_empty));
@@ -434,13 +487,14 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
         int j = 0;
         long long t_plan = 0, t_empty = 0;  // SCOUT_K2_PROF: cycles blocked on a plan / a free stage
         const long long t_start = clock64();
-        for (int L = 0; L < a.n_layers; ++L) {
-            const int b = L & 1;
-            const K2Layer& io = a.layers[L];
+        for (int c = 0;; ++c) {
+            const int b = c & 1;
             long long t0 = a.prof ? clock64() : 0;
-            mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
+            mbar_wait(&sm.plan_full[b], (c >> 1) & 1);
+            const int L = sm.plan[b].layer, fl = sm.plan[b].flags;
+            const K2Layer& io = a.layers[L];
             // blocks recalled for this layer one step ago must have landed
-            if (io.recall_token && a.recall_flag) wait_flag(a.recall_flag + L, io.recall_token);
+            if ((fl & CH_FIRST) && io.recall_token && a.recall_flag) wait_flag(a.recall_flag + L, io.recall_token);
             if (a.prof) t_plan += clock64() - t0;
             const int nblk = sm.plan[b].nblk;
             // L2 prefetch runs K2_PF blocks ahead of the ring: the ring's 6
@@ -449,21 +503,22 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             // a full ring while the consumers wait for data)
             const int pf = a.l2_prefetch;
             for (int f = 0; f < min(pf, nblk); ++f)
-                bulk_prefetch_l2(pool + static_cast<size_t>(sm.plan[b].blk_slot[f]) * BF16_SLOT_BYTES, STAGE_BYTES);
+                bulk_prefetch_l2(pool + blk_slot(sm.plan[b].blk[f]) * BF16_SLOT_BYTES, STAGE_BYTES);
             for (int f = 0; f < nblk; ++f, ++j) {
                 const int s = stage_of(j);
                 if (f + pf < nblk)
-                    bulk_prefetch_l2(pool + static_cast<size_t>(sm.plan[b].blk_slot[f + pf]) * BF16_SLOT_BYTES,
+                    bulk_prefetch_l2(pool + blk_slot(sm.plan[b].blk[f + pf]) * BF16_SLOT_BYTES,
                                      STAGE_BYTES);
                 if (a.prof) t0 = clock64();
                 if (j >= NST) mbar_wait(&sm.empty[s], ((j / NST) - 1) & 1);
                 if (a.prof) t_empty += clock64() - t0;
                 mbar_arrive_expect_tx(&sm.full[s], STAGE_BYTES);
                 bulk_g2s_evict_first(stages + s * STAGE_BYTES,
-                                     pool + static_cast<size_t>(sm.plan[b].blk_slot[f]) * BF16_SLOT_BYTES,
+                                     pool + blk_slot(sm.plan[b].blk[f]) * BF16_SLOT_BYTES,
                                      STAGE_BYTES, &sm.full[s], pol);
             }
             mbar_arrive(&sm.plan_empty[b]);  // the producer is done reading this plan
+            if ((fl & CH_LAST) && L == a.n_layers - 1) break;
         }
         if (a.prof) {
             unsigned long long* pr = a.prof + blockIdx.x * 16;
@@ -485,20 +540,22 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
         // consumers waiting for it 19% of their time)
         const int cw = warp - (NC + 2);
         long long k_wait = 0, k_busy = 0, tq = 0;
-        int segidx = 0;
-        for (int L = 0; L < a.n_layers; ++L) {
-            const int b = L & 1;
+        int segidx = 0;  // segments flushed by the consumers (pieces ending one)
+        for (int c = 0;; ++c) {
+            const int b = c & 1;
+            mbar_wait(&sm.plan_full[b], (c >> 1) & 1);
+            const Plan& P = sm.plan[b];
+            const int L = P.layer, fl = P.flags;
             const K2Layer& io = a.layers[L];
             int* ctr = reinterpret_cast<int*>(static_cast<uint8_t*>(a.workspace) + static_cast<size_t>(L) * a.ws_layer_bytes);
             float* parts = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(ctr) + ctr_bytes(nunits));
-            mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
-            const Plan& P = sm.plan[b];
-            for (int si = 0; si < P.nsegs; ++si, ++segidx) {
-                if (segidx % NCOMB != cw) continue;
+            for (int si = 0; si < P.nsegs; ++si) {
+                if (P.segs[si].cont & SEG_CONT_NEXT) continue;  // the segment goes on in the next chunk
+                if (segidx++ % NCOMB != cw) continue;
                 const Seg sg = P.segs[si];
                 const int u = sg.unit;
                 if (a.prof) tq = clock64();
-                mbar_wait(&sm.seg_full[cw], (segidx / NCOMB) & 1);
+                mbar_wait(&sm.seg_full[cw], ((segidx - 1) / NCOMB) & 1);
                 if (a.prof) { const long long t1 = clock64(); k_wait += t1 - tq; tq = t1; }
                 // lane: channels 4*lane..4*lane+3 of every head
                 const int d0 = lane * 4;
@@ -601,8 +658,9 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             }
             if (a.prof) tq = clock64();
             // ---- units with no resident block: output = CPU partial (or empty),
-            // listed by the planner (no n_res read on this path)
-            if (P.nzero <= ZMAX) {
+            // listed by the planner in the layer's first chunk (no n_res read on this path)
+            if (!(fl & CH_FIRST)) {
+            } else if (P.nzero <= ZMAX) {
                 for (int i = cw; i < P.nzero; i += NCOMB)
                     finalize_unit_warp<G>(io.cpu_o, a.cpu_bf16 != 0, io.cpu_ml, io.o, io.ml, P.zero_units[i], parts, 0, 0, lane);
             } else {
@@ -618,7 +676,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             __syncwarp();
             if (lane == 0) {
                 mbar_arrive(&sm.plan_empty[b]);
-                if (a.layer_done) {
+                if ((fl & CH_LAST) && a.layer_done) {
                     __threadfence();
                     if (atomicAdd(&sm.layer_fin[L], 1) == NCOMB - 1) {
                         __threadfence();
@@ -627,6 +685,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                 }
             }
             if (a.prof) k_busy += clock64() - tq;
+            if ((fl & CH_LAST) && L == a.n_layers - 1) break;
         }
         if (a.prof && lane == 0) {
             unsigned long long* pr = a.prof + blockIdx.x * 16;
@@ -642,22 +701,27 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
     const float sl2 = a.scale * LOG2E;
     // SCOUT_K2_PROF: cycles waiting for data, loading Q, in segment ends, on plans / layer ends
     long long c_full = 0, c_q = 0, c_end = 0, c_plan = 0, tp = 0;
-    int segidx = 0;  // CTA-global segment count (the state buffer's phase)
-    for (int L = 0; L < a.n_layers; ++L) {
-        const int b = L & 1;
-        const K2Layer& io = a.layers[L];
+    int segidx = 0;  // CTA-global count of flushed segments (the state buffer's phase)
+    // one segment's state; a segment split over plan chunks keeps it across them
+    uint32_t bh[8][2], bl[8][2];  // Q^T fragments (hi/lo split), heads >= G are zero
+    float m2[2] = {-CUDART_INF_F, -CUDART_INF_F};
+    float lp[2] = {0.f, 0.f};
+    float oacc[8][4];
+    int held = -1;  // stage of the pair's last block: handed back at the next block or the segment end
+    bool any = false;
+    for (int c = 0;; ++c) {
+        const int b = c & 1;
         if (a.prof) tp = clock64();
-        mbar_wait(&sm.plan_full[b], (L >> 1) & 1);
+        mbar_wait(&sm.plan_full[b], (c >> 1) & 1);
         if (a.prof) c_plan += clock64() - tp;
         const Plan& P = sm.plan[b];
-        const int nsegs = P.nsegs, jbase = P.jbase;
+        const int nsegs = P.nsegs, jbase = P.jbase, L = P.layer, fl = P.flags;
+        const K2Layer& io = a.layers[L];
         for (int si = 0; si < nsegs; ++si) {
             const Seg sg = P.segs[si];
             const int u = sg.unit;
-            if (a.prof) tp = clock64();
-            // Q^T fragments (hi/lo split), heads >= G are zero
-            uint32_t bh[8][2], bl[8][2];
-            {
+            if (!(sg.cont & SEG_CONT_PREV)) {
+                if (a.prof) tp = clock64();
                 const bool live = g < G;
                 const size_t qoff = (static_cast<size_t>(u) * G + (live ? g : 0)) * D;
                 if (a.q_bf16) {  // the query is bf16 already: lo part zero
@@ -684,16 +748,15 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                         }
                     }
                 }
-            }
-            if (a.prof) { __syncwarp(); c_q += clock64() - tp; }
-            float m2[2] = {-CUDART_INF_F, -CUDART_INF_F};
-            float lp[2] = {0.f, 0.f};
-            float oacc[8][4];
+                if (a.prof) { __syncwarp(); c_q += clock64() - tp; }
+                m2[0] = m2[1] = -CUDART_INF_F;
+                lp[0] = lp[1] = 0.f;
 #pragma unroll
-            for (int i = 0; i < 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+                for (int i = 0; i < 8; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
+                held = -1;
+                any = false;
+            }
 
-            int held = -1;  // stage of the pair's last block: hosts the combine areas
-            bool any = false;
             const int f1 = sg.f0 + (sg.j1 - sg.j0);
             const int jf0 = jbase + sg.f0;
             for (int f = sg.f0 + ((pair - jf0) % NPAIR + NPAIR) % NPAIR; f < f1; f += NPAIR) {
@@ -704,7 +767,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                 const int jj = jbase + f;
                 const int s = stage_of(jj);
                 held = s;
-                const int valid = min(HALF_ROWS, static_cast<int>(P.blk_rows[f]) - hsel * HALF_ROWS);
+                const int valid = min(HALF_ROWS, blk_rows(P.blk[f]) - hsel * HALF_ROWS);
                 if (a.prof) tp = clock64();
                 mbar_wait(&sm.full[s], (jj / NST) & 1);
                 __syncwarp();  // lanes may leave the try_wait loop apart: reconverge before .aligned ops
@@ -792,6 +855,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                     }
                 }
             }
+            if (sg.cont & SEG_CONT_NEXT) continue;  // the segment goes on in the next chunk
             if (a.prof) tp = clock64();
             // ---- warp state -> the combiner; the stage goes back right away
 #pragma unroll
@@ -802,6 +866,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             __syncwarp();
             const int area = (held >= 0 && any) ? 1 : -1;
             if (held >= 0 && lane == 0) mbar_arrive(&sm.empty[held]);  // all lanes are past their last ldmatrix
+            held = -1;
             // the combiner has read the previous segment's states
             if (segidx > 0) mbar_wait(&sm.seg_empty, (segidx - 1) & 1);
             if (area >= 0) {
@@ -826,9 +891,10 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
             ++segidx;
             if (a.prof) c_end += clock64() - tp;
         }
-        // this warp is done with layer L's plan
+        // this warp is done with the chunk's plan
         __syncwarp();
         if (lane == 0) mbar_arrive(&sm.plan_empty[b]);
+        if ((fl & CH_LAST) && L == a.n_layers - 1) break;
     }
     if (a.prof && lane == 0) {
         unsigned long long* pr = a.prof + blockIdx.x * 16;
@@ -950,15 +1016,11 @@ int tc_grid(int max_ctas) {
 }  // namespace
 
 int scout_k2_grid(int n_units, int k_stride, int max_ctas) {
-    // a CTA range must not touch more than MAXSEG units nor hold more than MAXB
-    // blocks of one layer (T <= n_units * k_stride)
-    int min_grid = (n_units + tc::MAXSEG - 3) / (tc::MAXSEG - 2);
-    const long long tmax = static_cast<long long>(n_units) * k_stride;
-    const int min_grid_b = static_cast<int>((tmax + tc::MAXB - 2) / (tc::MAXB - 1));
-    if (min_grid < min_grid_b) min_grid = min_grid_b;
-    int grid = tc_grid(max_ctas);
-    if (grid < min_grid) grid = min_grid;
-    return grid > GRID_CAP ? GRID_CAP : grid;
+    // persistent: at most one CTA per SM (a CTA's range of any size is planned
+    // in chunks, so neither the unit count nor the list length raises the grid)
+    (void)n_units;
+    (void)k_stride;
+    return tc_grid(max_ctas);
 }
 
 size_t scout_k2_ws_layer_bytes(int n_units, int grid) {
@@ -981,9 +1043,16 @@ int scout_k2_launch(const K2StepArgs& a, cudaStream_t st, bool pdl) {
         case 1: go(tc::sparse_decode_tc_kernel<1>); break;
         case 2: go(tc::sparse_decode_tc_kernel<2>); break;
         case 4: go(tc::sparse_decode_tc_kernel<4>); break;
-        default: go(tc::sparse_decode_tc_kernel<8>); break;
+        case 8: go(tc::sparse_decode_tc_kernel<8>); break;
+        default:
+            set_error(SCOUT_ERR_INVALID_ARGUMENT, "K2: group %d not in {1,2,4,8}", a.group);
+            return SCOUT_ERR_INVALID_ARGUMENT;
     }
     return check_launch("scout_sparse_decode");
+}
+
+extern "C" int scout_sparse_decode_grid(int n_units, int k_stride, int max_ctas) {
+    return scout_k2_grid(n_units, k_stride, max_ctas);
 }
 
 extern "C" size_t scout_sparse_decode_workspace_bytes(int n_units, int group, int max_ctas) {

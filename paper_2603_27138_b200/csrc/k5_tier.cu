@@ -454,8 +454,37 @@ __global__ void __launch_bounds__(TT) tier_plan_layers_kernel(const scout_tier_l
     }
 }
 
-__device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Unit& U, int u, int l, int pos, int n,
+__device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Unit& U, int u, int l, int pos,
                             TierSm& S);
+
+__device__ int find_sorted(const int32_t* v, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && v[lo] == x;
+}
+
+// check_split (engine.hpp:317-329) on K1's split of this step: every
+// predicted block on exactly one side, the two sides' sizes adding up, and
+// the token accounting (resident + CPU rows = the predicted blocks' rows at
+// selection time). A violation is the unit's sticky error SCOUT_TIER_ERR_SPLIT.
+__device__ void check_split(const TierPostArgs& a, Unit& U, int u, int l, int pos, TierSm& S) {
+    const size_t lu = static_cast<size_t>(l) * gridDim.x + u, row = lu * a.k;
+    const int ns = a.n_sel[lu], nr = a.n_res[lu], nc = a.n_cpu[lu];
+    const int nb = n_blocks_of(pos);
+    int bad = 0, tok = 0;
+    for (int i = threadIdx.x; i < ns; i += TT) {
+        const int b = a.sel_ids[row + i];
+        tok += b == nb - 1 ? pos - (nb - 1) * BS : BS;
+        if (find_sorted(a.res_ids + row, nr, b) == find_sorted(a.cpu_ids + row, nc, b)) bad = 1;
+    }
+    bad = block_sum(bad, S);
+    tok = block_sum(tok, S);
+    if (threadIdx.x == 0 && (bad || nr + nc != ns || tok != a.res_tok[lu] + a.cpu_tok[lu])) set_err(U, SCOUT_TIER_ERR_SPLIT);
+}
 
 // After the step's attention, per (unit, layer): append the token (open /
 // seal + enforce_capacity, row write, digest fold), write a sealed block
@@ -470,6 +499,7 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
     Unit U = unit_of(L, u, a.nbs);
     const int pos = a.n_tokens[u];
     const int id = pos / BS, r = pos % BS;
+    if (a.res_ids) check_split(a, U, u, l, pos, S);
     // ---- append bookkeeping (tier_append_kernel's logic)
     if (c == 0) {
         S.err = 0;
@@ -529,9 +559,14 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
         __syncthreads();
         enforce_capacity(L, U, id + 1, pos + 1, S);
     }
-    // ---- recall of the layer's CPU-side selected blocks (tier_recall_kernel's logic)
-    const int n = a.recall_due[l] ? a.n_cpu[static_cast<size_t>(l) * gridDim.x + u] : 0;
-    if (n > 0) post_recall(a, L, U, u, l, pos, n, S);
+    // ---- periodic recall (engine.hpp:299-307): when the layer is due, the
+    // predicted set minus the residency evaluated after this append
+    // (maybe_schedule_recall, recall.hpp:114-126), then schedule_recall's
+    // validation and slot assignment (tier_recall_kernel's logic)
+    if (a.recall_due[l]) {
+        __syncthreads();  // the seal's eviction first
+        post_recall(a, L, U, u, l, pos, S);
+    }
     // ---- the layer's planning view for the next step (tier_plan_layers_kernel's
     // logic): nothing touches this layer's state between here and that step's
     // plan, so the view is the same and the step need not wait for a plan launch
@@ -552,13 +587,48 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
     }
 }
 
-__device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Unit& U, int u, int l, int pos, int n,
+__device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Unit& U, int u, int l, int pos,
                             TierSm& S) {
-    const int c = threadIdx.x;
+    const int c = threadIdx.x, lane = c & 31, w = c >> 5;
     const int ntok = pos + 1;  // after this step's append
     const int nb = min(n_blocks_of(ntok), a.nbs);
-    const int32_t* my = a.cpu_ids + (static_cast<size_t>(l) * gridDim.x + u) * a.k;
-    int32_t* dst = a.dst + (static_cast<size_t>(l) * gridDim.x + u) * a.k;
+    const size_t row = (static_cast<size_t>(l) * gridDim.x + u) * a.k;
+    const int32_t* pred = a.sel_ids + row;
+    const int np = a.n_sel[static_cast<size_t>(l) * gridDim.x + u];
+    int32_t* my = a.rc_ids + row;
+    int32_t* dst = a.dst + row;
+    // residency_set(l) at clock (step, l): fast blocks plus tickets ready by
+    // next_run_of(l) = (step, l) (kv_store.hpp:156-170, 328-331)
+    const int next_tick = a.step * a.n_layers + l;
+    // set_difference(predicted, residency) in id order: a block-wide
+    // order-preserving compaction of the predicted ids that are not resident
+    int n = 0;
+    for (int base = 0; base < np; base += TT) {
+        const int i = base + c;
+        int b = -1;
+        bool take = false;
+        if (i < np) {
+            b = pred[i];
+            const bool in_range = b >= 0 && b < a.nbs;
+            const int rd = in_range ? U.ready[b] : -1;
+            take = !in_range || !(U.tier[b] || (rd >= 0 && rd <= next_tick));
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, take);
+        if (lane == 0) S.cnt[w] = __popc(bal);
+        __syncthreads();
+        int off = n;
+        for (int j = 0; j < w; ++j) off += S.cnt[j];
+        int tot = 0;
+        for (int j = 0; j < TW; ++j) tot += S.cnt[j];
+        if (take) my[off + __popc(bal & ((1u << lane) - 1u))] = b;
+        n += tot;
+        __syncthreads();
+    }
+    if (c == 0) a.rc_n[static_cast<size_t>(l) * gridDim.x + u] = n;
+    __syncthreads();  // the compacted list
+    if (n == 0) return;  // nothing to move (the trigger still resets the cadence, on the host)
+    // schedule_recall (kv_store.hpp:175-197): sealed, slow, not in flight, a
+    // sorted set; else the unit's whole ticket is rejected
     int bad = 0;
     for (int i = c; i < n; i += TT) {
         const int b = my[i];

@@ -32,10 +32,18 @@ def _p(t):
 class DecodeEngine:
     def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
                  recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
-                 recall_mode=0, q_dtype=torch.float32, tier=None, host_blocks=0, cpu_dtype=torch.float32):
+                 recall_mode=0, q_dtype=torch.float32, tier=None, host_blocks=0, cpu_dtype=torch.float32,
+                 recall_intervals=None, recall_stagger=False, cpu_worker=False, cpu_threads=0):
         """tier: a tier.DeviceTieredCache whose state the engine drives on the
         device (device tier mode: decode_step_kv); host_tier then holds block
-        images at ((layer*U + unit)*nb_stride + id) % host_blocks."""
+        images at ((layer*U + unit)*nb_stride + id) % host_blocks.
+        recall_intervals: per-layer recall intervals (engine.hpp:35; default:
+        recall_interval for every layer), triggered as the reference does
+        (step - last_recall >= interval, recall.hpp:114-126); recall_stagger:
+        round 1's (step + layer) % interval cadence instead.
+        cpu_worker: the engine computes each step's CPU partials itself
+        (device tier mode, host path; the decode calls then take no cpu_o /
+        cpu_ml) on cpu_threads host threads (0 = all)."""
         self.L, self.batch, self.hq, self.hkv, self.G, self.k = layers, batch, hq, hkv, hq // hkv, k
         self.U = batch * hkv
         self.layer_states = layer_states  # keep tensors alive
@@ -52,6 +60,12 @@ class DecodeEngine:
         cfg.recall_mode = int(recall_mode)
         cfg.q_dtype = ops.dtype_code(q_dtype)
         cfg.cpu_dtype = ops.dtype_code(cpu_dtype)  # CPU-partial o: f32 or bf16
+        if recall_intervals is not None:
+            self._rc_int = (C.c_int32 * layers)(*[int(x) for x in recall_intervals])
+            cfg.recall_intervals = C.cast(self._rc_int, C.c_void_p)
+        cfg.recall_stagger = int(bool(recall_stagger))
+        cfg.cpu_worker, cfg.cpu_threads = int(bool(cpu_worker)), int(cpu_threads)
+        self.cpu_worker = bool(cpu_worker)
         self.tier = tier
         if tier is not None:
             self._tier_descs = (A.TierLayer * layers)(*[tier.layer_desc(i) for i in range(layers)])
@@ -87,19 +101,33 @@ class DecodeEngine:
     def _stream():
         return torch.cuda.current_stream().cuda_stream
 
+    def _check(self, q_true, q_pred, cpu_o, cpu_ml):
+        """The buffers' element types must be the engine's (the C ABI takes raw
+        pointers: a bf16 tensor read as f32 would be garbage, not an error)."""
+        for name, t, dt in (("q_true", q_true, self.q_dtype), ("q_pred", q_pred, self.q_dtype),
+                            ("cpu_o", cpu_o, self.cpu_dtype), ("cpu_ml", cpu_ml, torch.float32)):
+            if t is not None and t.dtype != dt:
+                raise ValueError(f"{name}: dtype {t.dtype}, the engine was configured for {dt}")
+        if self.cpu_worker and (cpu_o is not None or cpu_ml is not None):
+            raise ValueError("cpu_worker engine: the CPU partials are computed inside, pass cpu_o = cpu_ml = None")
+
     def decode_step(self, step, q_true, q_pred, cpu_o, cpu_ml, out_o, out_ml):
-        """Device tensors: q_true/q_pred/cpu_o/out_o [L][U*G][128] f32, cpu_ml/out_ml [L][U*G][2]."""
+        """Device tensors: q_true/q_pred [L][U*G][128] (q dtype), cpu_o [L][U*G][128] (cpu dtype),
+        out_o [L][U*G][128] f32, cpu_ml/out_ml [L][U*G][2] f32."""
+        self._check(q_true, q_pred, cpu_o, cpu_ml)
         A.check(A.lib().scout_engine_decode_step(self._h, int(step), _p(q_true), _p(q_pred), _p(cpu_o), _p(cpu_ml),
                                                  _p(out_o), _p(out_ml), self._stream()))
 
     def decode_step_kv(self, step, q_true, q_pred, cpu_o, cpu_ml, k_new, v_new, out_o, out_ml):
         """Device tier mode: the step appends k_new / v_new [L][U][128] f32."""
+        self._check(q_true, q_pred, cpu_o, cpu_ml)
         A.check(A.lib().scout_engine_decode_step_kv(self._h, int(step), _p(q_true), _p(q_pred), _p(cpu_o), _p(cpu_ml),
                                                     _p(k_new), _p(v_new), _p(out_o), _p(out_ml), self._stream()))
 
     def decode_step_kv_host(self, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, h_k_new, h_v_new, h_out_o, h_out_ml,
                             h_cpu_ids=None, h_n_cpu=None):
         """Device tier mode from pinned host tensors (+ the token's K/V rows)."""
+        self._check(h_q_true, h_q_pred, h_cpu_o, h_cpu_ml)
         A.check(A.lib().scout_engine_decode_step_kv_host(self._h, int(step), _p(h_q_true), _p(h_q_pred), _p(h_cpu_o),
                                                          _p(h_cpu_ml), _p(h_k_new), _p(h_v_new), _p(h_out_o),
                                                          _p(h_out_ml), _p(h_cpu_ids), _p(h_n_cpu), self._stream()))
@@ -107,6 +135,7 @@ class DecodeEngine:
     def decode_step_host(self, step, h_q_true, h_q_pred, h_cpu_o, h_cpu_ml, h_out_o, h_out_ml, h_cpu_ids=None,
                          h_n_cpu=None):
         """Pinned host tensors, same layouts; h_cpu_ids [L][U][k], h_n_cpu [L][U] int32."""
+        self._check(h_q_true, h_q_pred, h_cpu_o, h_cpu_ml)
         A.check(A.lib().scout_engine_decode_step_host(self._h, int(step), _p(h_q_true), _p(h_q_pred), _p(h_cpu_o),
                                                       _p(h_cpu_ml), _p(h_out_o), _p(h_out_ml), _p(h_cpu_ids),
                                                       _p(h_n_cpu), self._stream()))
@@ -125,6 +154,17 @@ class DecodeEngine:
         ms, n, launches = C.c_double(), C.c_int(), C.c_longlong()
         A.check(A.lib().scout_engine_stats(self._h, C.byref(ms), C.byref(n), C.byref(launches)))
         return ms.value, n.value, launches.value
+
+    def check_state(self):
+        """Raise on the tier state's sticky errors (rejected recall ticket, out of
+        slots, check_split violated); synchronises."""
+        A.check(A.lib().scout_engine_check_state(self._h))
+
+    def worker_stats(self):
+        """In-engine CPU worker: (CPU ms summed over the steps since the last call, steps)."""
+        ms, n = C.c_double(), C.c_int()
+        A.check(A.lib().scout_engine_worker_stats(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def k1_outputs(self):
         """Zero-copy torch views of the engine's per-layer K1 outputs (device)."""

@@ -40,35 +40,63 @@ class Side:
         self.n_tokens.copy_(self.tier.n_tokens[0])
 
 
-@pytest.mark.parametrize("recall,external", [(3, False), (0, False), (0, True)])
-def test_engine_tier_mode_matches_reference_order_replay(cuda, recall, external):
-    """external: between two steps the caller re-places layer 1's fast set
+POLICIES = {
+    # name: (recall intervals per layer or None, capacity, stagger, external re-placement)
+    "reference_every_3": ([3, 3, 3], 8, False, False),
+    # capacity == k with stationary queries: the fast set converges to the
+    # predicted set, so the seal at step 64 (whose open block, filled with
+    # small keys, is never predicted) evicts a block the step just predicted
+    # (LRU ties -> lower id), and the reference recalls it right away
+    # (predicted \ residency after the append)
+    "reference_per_layer_full_capacity": ([1, 2, 1], 6, False, False),
+    "no_recall": (None, 8, False, False),
+    "no_recall_external_place": (None, 8, False, True),
+    "stagger_opt_in": ([3, 3, 3], 8, True, False),
+}
+
+
+@pytest.mark.parametrize("policy", sorted(POLICIES))
+def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
+    """The engine's decode steps against a replay in the reference's per-layer
+    order (engine.hpp:219-307) through the validated single ops and the
+    DeviceTieredCache mirror, with the recall decision and the recalled set
+    coming from the reference itself: maybe_schedule_recall (recall.hpp:114-126)
+    through oracle/_ref on (predicted, residency_set after the append).
+    external: between two steps the caller re-places layer 1's fast set
     (place_after_prefill) on both sides and tells the engine
     (scout_engine_tier_changed), whose next planning view must then come from
     the new state, not from the view the previous step's post launch wrote."""
-    rng = np.random.default_rng(21 + recall)
-    L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 70
+    import py_oracle as P
+
+    intervals, cap, stagger, external = POLICIES[policy]
+    rng = np.random.default_rng(21 + len(policy))
+    torch.manual_seed(len(policy))
+    L, batch, hkv, G, k, nbs, steps = 3, 2, 2, 4, 6, 24, 70
     U = batch * hkv
     kv = torch.bfloat16
-    T0 = 64 * 12 + 40
+    stationary = policy == "reference_per_layer_full_capacity"
+    T0 = 64 * 13 if stationary else 64 * 12 + 40
     seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
     eng_side, rep = Side(L, U, nbs, cap, kv, seed_rows), Side(L, U, nbs, cap, kv, seed_rows)
     layers = [LayerState(eng_side.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda"))
               for i in range(L)]
     eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=eng_side.n_tokens,
                        pool=eng_side.pool, kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D),
-                       recall_interval=recall, host_tier=eng_side.host, tier=eng_side.tier, host_blocks=0,
-                       q_dtype=torch.bfloat16)
+                       recall_interval=0, recall_intervals=intervals, recall_stagger=stagger,
+                       host_tier=eng_side.host, tier=eng_side.tier, host_blocks=0, q_dtype=torch.bfloat16)
+    policy_ref = P.RefRecall(U, intervals) if (intervals and not stagger) else None
     out_o = torch.empty(L, U * G, D, device="cuda")
     out_ml = torch.empty(L, U * G, 2, device="cuda")
     st = torch.cuda.current_stream().cuda_stream
     rt = rep.tier
+    n_recalled = evicted_predicted = 0
+    q_fixed = torch.randn(L, U * G, D, device="cuda")
     for step in range(1, steps + 1):
-        q_true = torch.randn(L, U * G, D, device="cuda").bfloat16()
-        q_pred = (q_true.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).bfloat16()
+        q_true = (q_fixed if stationary else torch.randn(L, U * G, D, device="cuda")).bfloat16()
+        q_pred = q_true if stationary else (q_true.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).bfloat16()
         cpu_o = torch.randn(L, U * G, D, device="cuda")
         cpu_ml = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
-        k_new = torch.randn(L, U, D, device="cuda")
+        k_new = torch.randn(L, U, D, device="cuda") * (0.05 if stationary else 1.0)
         v_new = torch.randn(L, U, D, device="cuda")
         eng.decode_step_kv(step, q_true, q_pred, cpu_o, cpu_ml, k_new, v_new, out_o, out_ml)
         # ---- replay in the reference's per-layer order
@@ -86,12 +114,34 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, recall, external)
                                       G, cpu_o=cpu_o[i], cpu_ml=cpu_ml[i])
             want.append((o, ml))
             rt.append_token(i, k_new[i], v_new[i], rep.pool, kv, rep.dig[i], host_tier=rep.host)
-            if recall and (step + i) % recall == 0:
-                dst = rt.schedule_recall(i, r["cpu_ids"], r["n_cpu"], step, i)
-                A.check(A.lib().scout_recall_gather_ids(rep.pool.data_ptr(), ops.dtype_code(kv), rep.host.data_ptr(),
-                                                        i * U * nbs, nbs, 0, U, r["cpu_ids"].data_ptr(),
-                                                        r["n_cpu"].data_ptr(), dst.data_ptr(), k, 1, st))
-                rt.check(i)
+            if not intervals:
+                continue
+            # engine.hpp:299-307: maybe_schedule_recall(predicted[i], residency_set(i)) after the append
+            residency = (rt.residency_table(i) >= 0).cpu().numpy()
+            pred = [r["sel_ids"][u, :int(r["n_sel"][u])].cpu().numpy() for u in range(U)]
+            res_before = [set(r["res_ids"][u, :int(r["n_res"][u])].cpu().tolist()) for u in range(U)]
+            ids = torch.zeros(U, k, dtype=torch.int32)
+            n_ids = torch.zeros(U, dtype=torch.int32)
+            for u in range(U):
+                res_u = np.nonzero(residency[u])[0]
+                if stagger:
+                    got = np.setdiff1d(pred[u], res_u) if (step + i) % intervals[i] == 0 else None
+                else:
+                    got = policy_ref.maybe_schedule_recall(u, i, step, pred[u], res_u)
+                if got is None or len(got) == 0:
+                    continue
+                ids[u, :len(got)] = torch.from_numpy(np.asarray(got, np.int32))
+                n_ids[u] = len(got)
+                n_recalled += len(got)
+                evicted_predicted += len(set(int(x) for x in got) & res_before[u])
+            if int(n_ids.sum()) == 0:
+                continue
+            ids_d, n_d = ids.cuda(), n_ids.cuda()
+            dst = rt.schedule_recall(i, ids_d, n_d, step, i)
+            A.check(A.lib().scout_recall_gather_ids(rep.pool.data_ptr(), ops.dtype_code(kv), rep.host.data_ptr(),
+                                                    i * U * nbs, nbs, 0, U, ids_d.data_ptr(), n_d.data_ptr(),
+                                                    dst.data_ptr(), k, 1, st))
+            rt.check(i)
         rep.n_tokens.copy_(rt.n_tokens[0])
         eng.sync()
         torch.cuda.synchronize()
@@ -116,7 +166,10 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, recall, external)
     assert int(eng_side.n_tokens[0]) == T0 + steps
     nb = (T0 + steps + BS - 1) // BS
     assert int((eng_side.tier.tier[1:, :, :nb - 1] == 0).sum()) > 0  # sealed blocks on the slow tier
-    assert (rt.n_tickets > 0) == (recall > 0)
+    assert (rt.n_tickets > 0) == bool(intervals)
+    assert (n_recalled > 0) == bool(intervals)
+    if policy == "reference_per_layer_full_capacity":
+        assert evicted_predicted > 0  # a seal evicted a just-predicted block and it was recalled
     # digests (incrementally maintained) equal on both sides and the pools hold the same live blocks
     for i in range(L):
         assert torch.equal(eng_side.dig[i], rep.dig[i])
