@@ -5,29 +5,38 @@ Default (--tier device): the complete decode step of ScoutEngine::decode_step
 (engine.hpp:220-307) on the device: residency planning, select + mark,
 begin_layer's ticket application, attention + LSE merge, append of the
 token's K/V with digest refresh (seal write-through, LRU eviction), and the
-periodic recall of each layer's CPU-side selected blocks. --tier static is
-the kernel view: residency fixed at the paper's 8.2% CPU share, no appends.
+periodic recall (the reference's cadence and set: maybe_schedule_recall,
+recall.hpp:114-126). --tier static is the kernel view: residency fixed at the
+paper's 8.2% CPU share, no appends.
 
 Workload (BASELINE.json configs[2], the metric's config): 64 layers, 64 query /
 8 KV heads, head_dim 128, batch 32 per GPU, 32K-token context (512 blocks of
 64 tokens per (request, KV head)), top-64 block selection, bf16 KV, layer-ahead
-CPU partials merged on the GPU, periodic recall every 16 steps (staggered by
-layer). A "step" = one decode token for every request: for each of the 64
-layers, K1 (score + top-k + split of layer i+1 with the predicted query) and
-K2+K3 (sparse flash-decode of layer i over its resident selected blocks, fused
-LSE merge with the CPU partial), plus K4 recall gathers on a side stream.
+CPU partials merged on the GPU, periodic recall every 16 steps. A "step" = one
+decode token for every request: for each of the 64 layers, K1 (score + top-k +
+split of layer i+1 with the predicted query) and K2+K3 (sparse flash-decode of
+layer i over its resident selected blocks, fused LSE merge with the CPU
+partial), plus the post-attention bookkeeping and the recall copies.
 
   value : decode tokens/s (all GPUs), inputs resident in HBM
   e2e   : same metric through the engine with HOST (pinned) inputs/outputs:
-          per-step H2D of q_true, q_pred, CPU partials; D2H of the attention
-          output and the CPU-side block ids, inside the timed region
+          per-step H2D of q_true, q_pred, CPU partials, new K/V; D2H of the
+          attention output and the CPU-side block ids, inside the timed region
+  e2e_with_cpu_worker : the composed step: the engine's own CPU worker
+          computes every layer's CPU partial during the step from the ids K1
+          just selected (no pre-staged partials)
+  verify: one more step re-derived in float64 on the device for a sample of
+          (layer, unit) pairs (top-k sets, split, attention)
   roofline: K2 (dominant kernel) algorithmic bytes / its CUDA-event time
   cpu_baseline: the reference's own C++ functions (oracle/_ref) on this host's
           cores over a bounded sample of the same workload
 
 `--impl reference` times the reference CPU implementation alone (rank 0).
-Multi-GPU: one process per GPU, requests sharded (weak scaling: 32 per GPU),
-no collective on the path; timing = max over ranks.
+Multi-GPU: one process per GPU, requests sharded (weak scaling: 32 per GPU;
+--global-batch: strong), every rank's shard a slice of one seeded global
+workload; no collective on the path; timing = max over ranks; outside the
+timed region rank 0 recomputes a sample of every rank's requests alone and
+compares the outputs.
 """
 from __future__ import annotations
 
@@ -48,11 +57,13 @@ sys.path.insert(0, str(ROOT))
 
 D, BS = 128, 64
 CONFIGS = {
-    # name: (layers, hq, hkv, batch/GPU, ctx tokens, k, kv dtype, capacity, headroom, recall interval, cpu frac)
+    # BASELINE.json configs[2] (the metric's config) and configs[3] (sharded: --global-batch 128)
     "qwen3-32b-32k": dict(layers=64, hq=64, hkv=8, batch=32, ctx=32768, k=64, capacity=64, headroom=8,
                           recall=16, cpu_frac=0.082),
+    # configs[1]: Qwen3-8B, batch 16, 16K, GPU cache = 25% of the 256 blocks
     "qwen3-8b-16k": dict(layers=36, hq=32, hkv=8, batch=16, ctx=16384, k=32, capacity=64, headroom=8,
                          recall=16, cpu_frac=0.082),
+    # configs[4]: batch 64 on 8 GPUs = 8 per GPU, 128K, top-128
     "qwen3-32b-128k": dict(layers=64, hq=64, hkv=8, batch=8, ctx=131072, k=128, capacity=128, headroom=16,
                            recall=16, cpu_frac=0.082),
 }
@@ -96,9 +107,172 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- workload --
-class Workload:
-    """Synthetic device-resident state of one GPU's shard (random-init data of
-    the named shape; selection and residency derived from it)."""
+def _gen(dev, seed, request, salt):
+    from paper_2603_27138_b200.sharding import request_seed
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(request_seed(seed, request, salt))
+    return g
+
+
+class TierWorkload:
+    """Device tier mode (--tier device): the full decode step of the reference
+    (plan, select + mark, ticket application, attention + merge, append of the
+    token's K/V with seal write-through and LRU eviction, periodic recall of
+    predicted \\ resident blocks), all bookkeeping on the device (K5).
+
+    Synthetic, random-init data of the named shape, generated per GLOBAL
+    request id from one seed (so a rank's shard is a slice of the global
+    workload, and any subset of requests can be rebuilt alone): K/V pool, bf16
+    digests (lo <= hi), queries following a closed path (drift), CPU partials,
+    the tokens' new K/V. The initial placement keeps each unit's selected
+    blocks minus the CPU share (the paper's 8.2%) resident, filled to capacity."""
+
+    def __init__(self, cfg, dev, seed, max_steps, requests):
+        from paper_2603_27138_b200 import ops
+        from paper_2603_27138_b200.engine import LayerState
+        from paper_2603_27138_b200.tier import DeviceTieredCache
+
+        self.cfg, self.dev, self.requests = cfg, dev, list(requests)
+        L, hq, hkv = cfg["layers"], cfg["hq"], cfg["hkv"]
+        B = len(self.requests)
+        G = hq // hkv
+        U = B * hkv
+        nb = cfg["ctx"] // BS
+        nbs = ((nb + (max_steps + BS - 1) // BS + 1 + 7) // 8) * 8  # room for the appended tokens
+        k, cap = cfg["k"], cfg["capacity"]
+        self.L, self.U, self.G, self.nb, self.k, self.B, self.hkv = L, U, G, nb, k, B, hkv
+        kv_dt = torch.bfloat16
+        # pool slots per (layer, unit): every block for the pinned layer 0; else the
+        # capacity's sealed fast blocks + the open block + one recall ticket in
+        # flight (at most k blocks: predicted \ residency), so a unit can never
+        # run out of slots, however far its selection drifted since the last recall
+        spu = [nbs] + [cap + 1 + k] * (L - 1)
+        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=spu, device=dev)
+        self.tier.pin_layer(0)
+        self.pool = ops.alloc_pool(self.tier.n_slots, kv_dt, dev)
+        pv = self.pool.view(torch.bfloat16).view(-1)
+        half = ops.slot_bytes(kv_dt) // 2  # bf16 elements per slot
+        for li in range(L):  # each (layer, request)'s slot range from its own generator
+            for i, r in enumerate(self.requests):
+                s0 = (self.tier.layer_base[li] + i * hkv * spu[li]) * half
+                pv[s0:s0 + hkv * spu[li] * half].normal_(generator=_gen(dev, seed, r, 1000 + li))
+        # requests differ in length (by < one block), so seals (and their
+        # write-through) spread over steps instead of all units at once
+        lens = cfg["ctx"] - 2 * (torch.tensor(self.requests, dtype=torch.int32, device=dev) % 32)
+        self.n_tokens = lens.repeat_interleave(hkv).contiguous()
+        # decode drift: the queries move along a closed loop, one point per step
+        # (n_path points, all precomputed in HBM), so selections change a little
+        # every step and the CPU share settles where recalls balance it
+        n_path = cfg.get("drift_points", 32)
+        radius = cfg.get("drift", 0.0)
+        per = hkv * G
+        q0, du, dv, noise = (torch.empty(L, U * G, D, device=dev) for _ in range(4))
+        self.cpu_o = torch.empty(L, U * G, D, device=dev)
+        m, l_ = torch.empty(L, U * G, device=dev), torch.empty(L, U * G, device=dev)
+        self.k_new, self.v_new = torch.empty(L, U, D, device=dev), torch.empty(L, U, D, device=dev)
+        for i, r in enumerate(self.requests):
+            g = _gen(dev, seed, r, 1)
+            sl = slice(i * per, (i + 1) * per)
+            for t in (q0, du, dv, noise, self.cpu_o):
+                t[:, sl] = torch.randn(L, per, D, generator=g, device=dev)
+            m[:, sl] = torch.randn(L, per, generator=g, device=dev)
+            l_[:, sl] = torch.rand(L, per, generator=g, device=dev) * 40 + 1
+            self.k_new[:, i * hkv:(i + 1) * hkv] = torch.randn(L, hkv, D, generator=g, device=dev)
+            self.v_new[:, i * hkv:(i + 1) * hkv] = torch.randn(L, hkv, D, generator=g, device=dev)
+        self.q_path_t, self.q_path_p = [], []
+        for j in range(n_path if radius > 0 else 1):
+            th = 2 * math.pi * j / n_path
+            qt = q0 + radius * (math.cos(th) * du + math.sin(th) * dv)
+            qp = qt + 0.33 * noise
+            qp = qp * (qt.norm(dim=-1, keepdim=True) / qp.norm(dim=-1, keepdim=True))
+            self.q_path_t.append(qt.to(cfg["q_dtype"]))
+            self.q_path_p.append(qp.to(cfg["q_dtype"]))
+        del q0, du, dv, noise
+        self.q_true, self.q_pred = self.q_path_t[0], self.q_path_p[0]
+        self.cpu_o = self.cpu_o.to(cfg.get("cpu_dtype", torch.float32))
+        self.cpu_ml = torch.stack([m, l_], dim=-1).contiguous()
+        self.out_o = torch.empty(L, U * G, D, device=dev)
+        self.out_ml = torch.empty(L, U * G, 2, device=dev)
+        self.host_blocks = 8192
+        sb = ops.slot_bytes(kv_dt)
+        self.host_tier = torch.empty(self.host_blocks * sb, dtype=torch.uint8).pin_memory()
+        self.host_tier.view(torch.bfloat16).normal_(generator=torch.Generator().manual_seed(seed))
+        cpu_per_unit = int(round(cfg["cpu_frac"] * k))
+        layers = []
+        for li in range(L):
+            dig = torch.empty(U, 2, D, nbs, dtype=kv_dt, device=dev)
+            for i, r in enumerate(self.requests):
+                g = _gen(dev, seed, r, 2000 + li)
+                a = torch.randn(hkv, D, nbs, generator=g, device=dev).to(kv_dt)
+                b = torch.randn(hkv, D, nbs, generator=g, device=dev).to(kv_dt)
+                dig[i * hkv:(i + 1) * hkv, 0] = torch.minimum(a, b)
+                dig[i * hkv:(i + 1) * hkv, 1] = torch.maximum(a, b)
+            dig[..., nb:] = 0  # blocks still to be appended
+            base = self.tier.layer_base[li] + torch.arange(U, device=dev, dtype=torch.int32)[:, None] * spu[li]
+            ids = torch.arange(nbs, device=dev, dtype=torch.int32)[None]
+            if li == 0:  # pinned: every block resident
+                table = torch.where(ids < nb, base + ids, -1)
+            else:
+                r_ = ops.score_topk_split(self.q_pred[li], dig, self.n_tokens, k, G)
+                sel = r_["sel_ids"][:, :k].long()
+                score = torch.empty(U, nbs, device=dev)
+                drop = torch.empty(U, cpu_per_unit, dtype=torch.long, device=dev)
+                for i, r in enumerate(self.requests):
+                    g = _gen(dev, seed, r, 3000 + li)
+                    score[i * hkv:(i + 1) * hkv] = torch.rand(hkv, nbs, generator=g, device=dev)
+                    drop[i * hkv:(i + 1) * hkv] = torch.rand(hkv, k, generator=g, device=dev).argsort(dim=1)[:, :cpu_per_unit]
+                score[:, nb:] = -1
+                score.scatter_(1, sel, 2.0)
+                score.scatter_(1, torch.gather(sel, 1, drop), -0.5)
+                score[self.n_tokens % BS != 0, nb - 1] = 3.0  # an open block is always fast (kv_store.hpp:60-63)
+                keep = score.argsort(dim=1, descending=True)[:, :cap]
+                table = torch.full((U, nbs), -1, dtype=torch.int32, device=dev)
+                table.scatter_(1, keep, (base + torch.arange(cap, device=dev, dtype=torch.int32)[None]).to(torch.int32))
+            self.tier.adopt(li, table.contiguous(), self.n_tokens)
+            layers.append(LayerState(dig, torch.full((U, nbs), -1, dtype=torch.int32, device=dev)))
+        self.layer_states = layers
+        self.cpu_per_unit = cpu_per_unit
+        self.digest_bytes_layer = U * 2 * D * nb * 2
+        self.engine = None
+
+    def make_engine(self, **kw):
+        """(Re)create the engine over this workload's state (the tier state and
+        token counts carry over; an old engine is closed first)."""
+        from paper_2603_27138_b200.engine import DecodeEngine
+
+        if self.engine is not None:
+            self.engine.close()
+        cfg = self.cfg
+        opts = dict(recall_interval=cfg["recall"], recall_stagger=cfg.get("recall_policy") == "stagger",
+                    cpu_dtype=cfg.get("cpu_dtype", torch.float32), recall_mode=cfg.get("recall_mode", 0))
+        opts.update(kw)
+        self.engine = DecodeEngine(layers=self.L, batch=self.B, hq=cfg["hq"], hkv=cfg["hkv"], k=self.k,
+                                   n_tokens=self.n_tokens, pool=self.pool, kv_dtype=torch.bfloat16,
+                                   layer_states=self.layer_states, scale=1.0 / math.sqrt(D),
+                                   host_tier=self.host_tier, q_dtype=cfg["q_dtype"], tier=self.tier,
+                                   host_blocks=self.host_blocks, host_staging=True, **opts)
+        return self.engine
+
+    def step(self, s):
+        j = s % len(self.q_path_t)
+        self.engine.decode_step_kv(s, self.q_path_t[j], self.q_path_p[j], self.cpu_o, self.cpu_ml, self.k_new,
+                                   self.v_new, self.out_o, self.out_ml)
+
+    def k2_bytes(self, res_tokens_total):
+        """Algorithmic bytes of one K2 launch: resident selected K+V rows, q in,
+        CPU partial in, output out (SURVEY.md §8d)."""
+        UG = self.U * self.G
+        qb, cb = self.q_path_t[0].element_size(), self.cpu_o.element_size()
+        return res_tokens_total * 2 * D * 2 + UG * (D * qb + (D * cb + 8) + (D + 2) * 4)
+
+
+class StaticWorkload:
+    """--tier static: the kernel view. Residency fixed at the paper's 8.2% CPU
+    share (all but round(8.2% k) of each unit's selected blocks resident,
+    filled to capacity), no appends; the recall plans move their bytes on the
+    copy engines but flip no tiers. Same synthetic data kinds as TierWorkload
+    (one generator per rank)."""
 
     def __init__(self, cfg, dev, seed):
         from paper_2603_27138_b200 import ops
@@ -117,31 +291,25 @@ class Workload:
         g.manual_seed(seed)
         gcpu = torch.Generator().manual_seed(seed)
         kv_dt = torch.bfloat16
-        # ---- pool: layer 0 pinned fully resident, others cap + headroom slots per unit
         n_slots = U * nb + (L - 1) * U * (cap + head)
-        self.n_slots = n_slots
         pool = ops.alloc_pool(n_slots, kv_dt, dev)
         pv = pool.view(torch.bfloat16)
-        chunk = 1 << 28
-        for s in range(0, pv.numel(), chunk):  # random bf16 K/V (layout-agnostic for iid data)
-            e = min(pv.numel(), s + chunk)
-            pv[s:e].normal_(generator=g)
+        for s in range(0, pv.numel(), 1 << 28):
+            pv[s:min(pv.numel(), s + (1 << 28))].normal_(generator=g)
         self.pool = pool
         self.n_tokens = torch.full((U,), cfg["ctx"], dtype=torch.int32, device=dev)
-        # ---- queries (true, predicted ~ cos 0.95) and CPU partials
         self.q_true = torch.randn(L, U * G, D, generator=g, device=dev)
         noise = torch.randn(L, U * G, D, generator=g, device=dev)
         qp = self.q_true + 0.33 * noise
         self.q_pred = qp * (self.q_true.norm(dim=-1, keepdim=True) / qp.norm(dim=-1, keepdim=True))
-        # queries in the model's dtype (q_dtype bf16: what a bf16 Qwen3 projection emits)
         self.q_true, self.q_pred = self.q_true.to(cfg["q_dtype"]), self.q_pred.to(cfg["q_dtype"])
+        self.q_path_t, self.q_path_p = [self.q_true], [self.q_pred]
         self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev).to(cfg.get("cpu_dtype", torch.float32))
         m = torch.randn(L, U * G, generator=g, device=dev)
-        l = torch.rand(L, U * G, generator=g, device=dev) * 40 + 1
-        self.cpu_ml = torch.stack([m, l], dim=-1).contiguous()
+        l_ = torch.rand(L, U * G, generator=g, device=dev) * 40 + 1
+        self.cpu_ml = torch.stack([m, l_], dim=-1).contiguous()
         self.out_o = torch.empty(L, U * G, D, device=dev)
         self.out_ml = torch.empty(L, U * G, 2, device=dev)
-        # ---- digests (random lo <= hi in bf16) and tier tables
         layers = []
         host_blocks = 4096
         sb = ops.slot_bytes(kv_dt)
@@ -149,37 +317,32 @@ class Workload:
         self.host_tier.view(torch.bfloat16).normal_(generator=gcpu)
         slot_base = U * nb
         cpu_per_unit = int(round(cfg["cpu_frac"] * k))
-        self.resident_sel = 0
         for li in range(L):
             a = torch.randn(U, D, nbs, generator=g, device=dev).to(kv_dt)
             b = torch.randn(U, D, nbs, generator=g, device=dev).to(kv_dt)
             dig = torch.stack([torch.minimum(a, b), torch.maximum(a, b)], dim=1).contiguous()
             del a, b
-            if li == 0:  # pinned: every block resident, slots unit-major
+            if li == 0:
                 ids = torch.arange(nbs, device=dev, dtype=torch.int32)[None]
                 table = torch.where(ids < nb, torch.arange(U, device=dev, dtype=torch.int32)[:, None] * nb + ids, -1)
                 layers.append(LayerState(dig, table.contiguous()))
                 continue
-            # selection with the layer's predicted query decides residency:
-            # all but cpu_per_unit selected blocks resident, filled to capacity
             r = ops.score_topk_split(self.q_pred[li], dig, self.n_tokens, k, G)
             sel = r["sel_ids"][:, :k].long()
-            torch.cuda.synchronize(dev)
             score = torch.rand(U, nbs, generator=g, device=dev)
             score[:, nb:] = -1
-            score.scatter_(1, sel, 2.0)  # selected first
+            score.scatter_(1, sel, 2.0)
             drop = torch.rand(U, k, generator=g, device=dev).argsort(dim=1)[:, :cpu_per_unit]
             cpu_ids = torch.gather(sel, 1, drop)
-            score.scatter_(1, cpu_ids, -0.5)  # keep the CPU-side ones out
+            score.scatter_(1, cpu_ids, -0.5)
             keep = score.argsort(dim=1, descending=True)[:, :cap]
             base = slot_base + (li - 1) * U * (cap + head)
             slots = base + torch.arange(U, device=dev)[:, None] * (cap + head) + torch.arange(cap, device=dev)[None]
             table = torch.full((U, nbs), -1, dtype=torch.int32, device=dev)
             table.scatter_(1, keep, slots.to(torch.int32))
-            # recall plan: the CPU-side selected blocks -> headroom slots
-            dst = base + torch.arange(U, device=dev)[:, None] * (cap + head) + cap + torch.arange(
-                cpu_per_unit, device=dev)[None]
-            src = (cpu_ids * 2654435761 + li * 97 + torch.arange(U, device=dev)[:, None] * 31) % host_blocks
+            nrc = min(cpu_per_unit, head)
+            dst = base + torch.arange(U, device=dev)[:, None] * (cap + head) + cap + torch.arange(nrc, device=dev)[None]
+            src = (cpu_ids[:, :nrc] * 2654435761 + li * 97 + torch.arange(U, device=dev)[:, None] * 31) % host_blocks
             layers.append(LayerState(dig, table, src.reshape(-1).to(torch.int64).cpu().contiguous(),
                                      dst.reshape(-1).to(torch.int32).cpu().contiguous()))
         self.layer_states = layers
@@ -190,130 +353,14 @@ class Workload:
                                    recall_stagger=cfg.get("recall_policy") == "stagger")
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
+        self.k_new = self.v_new = None
 
     def step(self, s):
         self.engine.decode_step(s, self.q_true, self.q_pred, self.cpu_o, self.cpu_ml, self.out_o, self.out_ml)
 
     def k2_bytes(self, res_tokens_total):
-        """Algorithmic bytes of one K2 launch: resident selected K+V rows, q in,
-        CPU partial in, output out (SURVEY.md §8d)."""
         UG = self.U * self.G
         qb, cb = self.q_true.element_size(), self.cpu_o.element_size()
-        return res_tokens_total * 2 * D * 2 + UG * (D * qb + (D * cb + 8) + (D + 2) * 4)
-
-
-class TierWorkload:
-    """Device tier mode (--tier device): the full decode step of the reference
-    (plan, select + mark, ticket application, attention + merge, append of the
-    token's K/V with seal write-through and LRU eviction, periodic recall of
-    the CPU-side selected blocks), all bookkeeping on the device (K5). Same
-    shape and synthetic data as Workload; the initial placement keeps the
-    selected blocks minus the CPU share resident, like Workload's table.
-    Queries stay stationary, so recalls pull the CPU share in and the
-    resident fraction grows over the run (reported)."""
-
-    def __init__(self, cfg, dev, seed, max_steps):
-        from paper_2603_27138_b200 import ops
-        from paper_2603_27138_b200.engine import DecodeEngine, LayerState
-        from paper_2603_27138_b200.tier import DeviceTieredCache
-
-        self.cfg = cfg
-        L, hq, hkv, B = cfg["layers"], cfg["hq"], cfg["hkv"], cfg["batch"]
-        G = hq // hkv
-        U = B * hkv
-        nb = cfg["ctx"] // BS
-        nbs = ((nb + (max_steps + BS - 1) // BS + 1 + 7) // 8) * 8  # room for the appended tokens
-        k, cap = cfg["k"], cfg["capacity"]
-        self.L, self.U, self.G, self.nb, self.k = L, U, G, nb, k
-        g = torch.Generator(device=dev)
-        g.manual_seed(seed)
-        gcpu = torch.Generator().manual_seed(seed)
-        kv_dt = torch.bfloat16
-        spu = [nbs] + [cap + cfg["headroom"] + 8] * (L - 1)  # pinned layer 0; capacity + in-flight + open block
-        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=spu, device=dev)
-        self.tier.pin_layer(0)
-        self.pool = ops.alloc_pool(self.tier.n_slots, kv_dt, dev)
-        pv = self.pool.view(torch.bfloat16)
-        for s0 in range(0, pv.numel(), 1 << 28):
-            pv[s0:min(pv.numel(), s0 + (1 << 28))].normal_(generator=g)
-        # requests differ in length (by < one block), so seals (and their
-        # write-through) spread over steps instead of all units at once
-        lens = cfg["ctx"] - 2 * (torch.arange(B, device=dev, dtype=torch.int32) % 32)
-        self.n_tokens = lens.repeat_interleave(hkv).contiguous()
-        # decode drift: the queries move along a closed loop, one point per step
-        # (n_path points, all precomputed in HBM), so selections change a little
-        # every step and the CPU share settles where recalls balance it
-        n_path = cfg.get("drift_points", 32)
-        radius = cfg.get("drift", 0.0)
-        q0 = torch.randn(L, U * G, D, generator=g, device=dev)
-        du = torch.randn(L, U * G, D, generator=g, device=dev)
-        dv = torch.randn(L, U * G, D, generator=g, device=dev)
-        noise = torch.randn(L, U * G, D, generator=g, device=dev)
-        self.q_path_t, self.q_path_p = [], []
-        for j in range(n_path if radius > 0 else 1):
-            th = 2 * math.pi * j / n_path
-            qt = q0 + radius * (math.cos(th) * du + math.sin(th) * dv)
-            qp = qt + 0.33 * noise
-            qp = qp * (qt.norm(dim=-1, keepdim=True) / qp.norm(dim=-1, keepdim=True))
-            self.q_path_t.append(qt.to(cfg["q_dtype"]))
-            self.q_path_p.append(qp.to(cfg["q_dtype"]))
-        self.q_true, self.q_pred = self.q_path_t[0], self.q_path_p[0]
-        self.cpu_o = torch.randn(L, U * G, D, generator=g, device=dev).to(cfg.get("cpu_dtype", torch.float32))
-        m = torch.randn(L, U * G, generator=g, device=dev)
-        l = torch.rand(L, U * G, generator=g, device=dev) * 40 + 1
-        self.cpu_ml = torch.stack([m, l], dim=-1).contiguous()
-        self.k_new = torch.randn(L, U, D, generator=g, device=dev)
-        self.v_new = torch.randn(L, U, D, generator=g, device=dev)
-        self.out_o = torch.empty(L, U * G, D, device=dev)
-        self.out_ml = torch.empty(L, U * G, 2, device=dev)
-        self.host_blocks = 8192
-        sb = ops.slot_bytes(kv_dt)
-        self.host_tier = torch.empty(self.host_blocks * sb, dtype=torch.uint8).pin_memory()
-        self.host_tier.view(torch.bfloat16).normal_(generator=gcpu)
-        cpu_per_unit = int(round(cfg["cpu_frac"] * k))
-        layers = []
-        for li in range(L):
-            a = torch.randn(U, D, nbs, generator=g, device=dev).to(kv_dt)
-            b = torch.randn(U, D, nbs, generator=g, device=dev).to(kv_dt)
-            dig = torch.stack([torch.minimum(a, b), torch.maximum(a, b)], dim=1).contiguous()
-            dig[..., nb:] = 0  # blocks still to be appended
-            del a, b
-            base = self.tier.layer_base[li] + torch.arange(U, device=dev, dtype=torch.int32)[:, None] * spu[li]
-            ids = torch.arange(nbs, device=dev, dtype=torch.int32)[None]
-            if li == 0:  # pinned: every block resident
-                table = torch.where(ids < nb, base + ids, -1)
-            else:
-                r = ops.score_topk_split(self.q_pred[li], dig, self.n_tokens, k, G)
-                sel = r["sel_ids"][:, :k].long()
-                score = torch.rand(U, nbs, generator=g, device=dev)
-                score[:, nb:] = -1
-                score.scatter_(1, sel, 2.0)
-                drop = torch.rand(U, k, generator=g, device=dev).argsort(dim=1)[:, :cpu_per_unit]
-                score.scatter_(1, torch.gather(sel, 1, drop), -0.5)
-                score[self.n_tokens % BS != 0, nb - 1] = 3.0  # an open block is always fast (kv_store.hpp:60-63)
-                keep = score.argsort(dim=1, descending=True)[:, :cap]
-                table = torch.full((U, nbs), -1, dtype=torch.int32, device=dev)
-                table.scatter_(1, keep, (base + torch.arange(cap, device=dev, dtype=torch.int32)[None]).to(torch.int32))
-            self.tier.adopt(li, table.contiguous(), self.n_tokens)
-            layers.append(LayerState(dig, torch.full((U, nbs), -1, dtype=torch.int32, device=dev)))
-        self.layer_states = layers
-        self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=self.pool,
-                                   kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
-                                   recall_interval=cfg["recall"], host_tier=self.host_tier, q_dtype=cfg["q_dtype"],
-                                   tier=self.tier, host_blocks=self.host_blocks, host_staging=True,
-                                   cpu_dtype=cfg.get("cpu_dtype", torch.float32),
-                                   recall_stagger=cfg.get("recall_policy") == "stagger")
-        self.cpu_per_unit = cpu_per_unit
-        self.digest_bytes_layer = U * 2 * D * nb * 2
-
-    def step(self, s):
-        j = s % len(self.q_path_t)
-        self.engine.decode_step_kv(s, self.q_path_t[j], self.q_path_p[j], self.cpu_o, self.cpu_ml, self.k_new,
-                                   self.v_new, self.out_o, self.out_ml)
-
-    def k2_bytes(self, res_tokens_total):
-        UG = self.U * self.G
-        qb, cb = self.q_path_t[0].element_size(), self.cpu_o.element_size()
         return res_tokens_total * 2 * D * 2 + UG * (D * qb + (D * cb + 8) + (D + 2) * 4)
 
 
@@ -339,6 +386,185 @@ def barrier(ws):
         import torch.distributed as dist
 
         dist.barrier()
+
+
+def timed(fn, steps, dev, ws):
+    """CUDA-event time of `steps` calls of fn, barrier + synchronize on both
+    sides, max over ranks (ms per step)."""
+    barrier(ws)
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for i in range(steps):
+        fn(i)
+    b.record()
+    torch.cuda.synchronize(dev)
+    barrier(ws)
+    return max_over_ranks(a.elapsed_time(b), ws, dev) / steps
+
+
+# ---------------------------------------------------------------- verify --
+def verify_step(wl, step, n_units=8, layers=None):
+    """Run one more step (device path, outside the timed region) and re-derive
+    its outputs in float64 on the device for a sample of (layer, unit) pairs,
+    from a snapshot of their state taken right before the step (digests,
+    planning view, the K/V of every block that view counts as resident):
+      * K1: the top-k set by the stacked digest_score rule (digest.hpp:62-118;
+        ties to the lower id) from float64 scores; a set that differs only
+        inside a float64 near-tie (k-th and (k+1)-th score within 1e-12 of the
+        terms' magnitude) is counted, not failed (tests/ pin it bit-exact
+        against the reference sum order);
+      * the split against the planning view (engine.hpp:239-241);
+      * K2+K3: partial_attention over the resident share + merge with the CPU
+        partial + finalize (attention.hpp:73-122), within the bf16 bar (2e-2
+        relative per head, 5e-3 on the log-sum-exp)."""
+    from paper_2603_27138_b200 import ops
+
+    eng, dev, L, U, G, k = wl.engine, wl.pool.device, wl.L, wl.U, wl.G, wl.k
+    eng.sync()
+    torch.cuda.synchronize(dev)
+    layers = layers or sorted({0, 1, L // 2, L - 1})
+    units = sorted({int(x) for x in np.linspace(0, U - 1, n_units)})
+    tr = wl.tier
+    ntok = wl.n_tokens.clone()
+    snap = {}
+    sb = ops.slot_bytes(torch.bfloat16)
+    for l in layers:
+        tick = step * L + l
+        plan = torch.where((tr.tier[l] == 1) | ((tr.ready[l] >= 0) & (tr.ready[l] <= tick)), tr.table[l], -1)
+        for u in units:
+            slots = plan[u].clone()
+            live = torch.nonzero(slots >= 0).flatten()
+            img = wl.pool.view(-1, sb)[slots[live].long()].clone()  # [n][slot bytes]: a mini pool
+            snap[(l, u)] = (wl.layer_states[l].digests[u].double().clone(), slots, live, img)
+    j = step % len(wl.q_path_t)
+    qt_all, qp_all = wl.q_path_t[j], wl.q_path_p[j]
+    wl.step(step)
+    eng.sync()
+    torch.cuda.synchronize(dev)
+    k1 = eng.k1_outputs()
+    out_o, out_ml = wl.out_o, wl.out_ml
+    n_ok = n_tie = n_bad = split_bad = 0
+    worst, worst_lse, worst_at = 0.0, 0.0, None
+    slot_mismatch = live_diff = 0
+    scale = 1.0 / math.sqrt(D)
+    for (l, u), (dig, slots, live, img) in snap.items():
+        nt = int(ntok[u])
+        nb = (nt + BS - 1) // BS
+        q_sel = (qt_all[0] if l == 0 else qp_all[l])[u * G:(u + 1) * G].double()  # [G][D]
+        # stacked score: sum over (c, g) of max(q_g[c] lo[c], q_g[c] hi[c]), float64
+        lo, hi = dig[0, :, :nb], dig[1, :, :nb]  # [D][nb]
+        terms = torch.maximum(q_sel[:, :, None] * lo[None], q_sel[:, :, None] * hi[None])  # [G][D][nb]
+        sc = terms.sum(dim=(0, 1)).cpu()
+        mag = float(terms.abs().sum(dim=(0, 1)).max())
+        kk = min(k, nb)
+        order = sorted(range(nb), key=lambda b: (-float(sc[b]), b))
+        want = sorted(order[:kk])
+        nr, nc = int(k1["n_res"][l, u]), int(k1["n_cpu"][l, u])
+        res = k1["res_ids"][l, u, :nr].tolist()
+        cpu = k1["cpu_ids"][l, u, :nc].tolist()
+        got = sorted(res + cpu)
+        if got == want:
+            n_ok += 1
+        elif kk < nb and abs(float(sc[order[kk - 1]] - sc[order[kk]])) <= 1e-12 * mag:
+            n_tie += 1
+        else:
+            n_bad += 1
+        planned = set(int(b) for b in torch.nonzero(slots >= 0).flatten().tolist())
+        if set(res) != set(got) & planned or set(cpu) != set(got) - planned:
+            split_bad += 1
+        # attention over the snapshot's resident blocks (rows < the count at attention)
+        pos = {int(b): i for i, b in enumerate(live.tolist())}
+        sl, rr = [], []
+        for b in res:
+            rows = nt - (nb - 1) * BS if b == nb - 1 else BS
+            sl += [pos[b]] * rows
+            rr += list(range(rows))
+        if sl:
+            kr, vr = ops.kv_read_tokens(img.view(-1), torch.bfloat16, sl, rr)
+            kr, vr = kr.double(), vr.double()
+            # debug: the engine's own slots on the live pool
+            rs = k1["res_slots"][l, u, :nr].tolist()
+            plan_slots = [int(slots[b]) for b in res]
+            if rs != plan_slots:
+                slot_mismatch += 1
+            sl2 = []
+            for b, s_ in zip(res, rs):
+                rows = nt - (nb - 1) * BS if b == nb - 1 else BS
+                sl2 += [s_] * rows
+            kr2, vr2 = ops.kv_read_tokens(wl.pool, torch.bfloat16, sl2, rr)
+            if not (torch.equal(kr2.double(), kr) and torch.equal(vr2.double(), vr)):
+                live_diff += 1
+        qt = qt_all[l][u * G:(u + 1) * G].double()
+        co = wl.cpu_o[l][u * G:(u + 1) * G].double()
+        cm = wl.cpu_ml[l][u * G:(u + 1) * G].double()
+        for g in range(G):
+            mx, den, acc = -math.inf, 0.0, torch.zeros(D, dtype=torch.float64, device=dev)
+            if sl:
+                s = (kr @ qt[g]) * scale
+                mx = float(s.max())
+                p = torch.exp(s - mx)
+                den = float(p.sum())
+                acc = p @ vr
+            cmx, cden = float(cm[g, 0]), float(cm[g, 1])
+            if cden > 0:  # merge (attention.hpp:100-114), the CPU partial's o normalised
+                M = max(mx, cmx)
+                wa = math.exp(mx - M) if den > 0 else 0.0
+                wb = math.exp(cmx - M)
+                acc = acc * wa + co[g] * cden * wb
+                den, mx = den * wa + cden * wb, M
+            o = out_o[l][u * G + g].double()
+            if den == 0:
+                worst = max(worst, float(o.abs().max()))
+                continue
+            ref = acc / den
+            e = float((o - ref).abs().max() / ref.abs().max())
+            if e > worst:
+                worst_at = (l, u, g, len(res), len(cpu), nt)
+            worst = max(worst, e)
+            ml = out_ml[l][u * G + g].double()
+            worst_lse = max(worst_lse, abs(float(ml[0]) + math.log(float(ml[1])) - (mx + math.log(den))))
+    ok = n_bad == 0 and split_bad == 0 and worst <= 2e-2 and worst_lse <= 5e-3
+    return {"pass": bool(ok), "step": step, "layers": layers, "units": units,
+            "topk_sets_exact": n_ok, "topk_sets_in_float64_near_tie": n_tie, "topk_sets_wrong": n_bad,
+            "split_wrong": split_bad, "attention_max_rel_err": worst, "lse_max_abs_err": worst_lse,
+            "worst_at_layer_unit_head": worst_at, "slot_mismatch": slot_mismatch, "live_diff": live_diff,
+            "tolerance": {"attention_rel": 2e-2, "lse_abs": 5e-3},
+            "reference": "torch float64 recomputation on the device from a pre-step snapshot (digest_score / "
+                         "select_topk / split / partial_attention + merge + finalize); bit-exact top-k against the "
+                         "reference sum order is pinned in tests/"}
+
+
+def cross_rank_check(wl, cfg, args, ws, rank, dev, steps_done, seed, gb):
+    """N > 1, outside the timed region: the per-request output sums of the last
+    step gathered from every rank (the shards of one global workload), and
+    rank 0 rebuilding the first and last request of every rank's shard as a
+    workload of its own, replaying the same steps alone, and comparing."""
+    from paper_2603_27138_b200.sharding import gather_per_request, request_shard
+
+    G, hkv, L = wl.G, wl.hkv, wl.L
+    per = hkv * G
+    mine = wl.out_o.view(L, wl.B, per, D).double().sum(dim=(0, 2, 3))  # [B]
+    allsum = gather_per_request(mine, gb, ws, rank)
+    res = None
+    if rank == 0:
+        sample = sorted({s + off for r in range(ws) for s, n in [request_shard(gb, ws, r)] for off in (0, n - 1) if n})
+        sub = TierWorkload(cfg, dev, seed, max_steps=args.max_steps, requests=sample)
+        sub.make_engine()
+        for s in range(1, steps_done + 1):
+            sub.step(s)
+        sub.engine.sync()
+        torch.cuda.synchronize(dev)
+        got = sub.out_o.view(L, sub.B, per, D).double().sum(dim=(0, 2, 3)).cpu()
+        want = allsum.cpu()[sample]
+        rel = float(((got - want).abs() / want.abs().clamp_min(1e-30)).max())
+        res = {"requests_recomputed_alone": sample, "max_rel_diff_of_output_sums": rel, "pass": rel <= 1e-3,
+               "note": "stream-K splits differ with the batch (fp32 merge order); selections and tier state do "
+                       "not depend on it"}
+        sub.engine.close()
+        del sub
+    barrier(ws)
+    return res
 
 
 # ------------------------------------------------------------ CPU baseline --
@@ -408,10 +634,8 @@ class RefBaseline:
 def measure_cpu_worker(wl, cfg, seconds=4.0):
     """The CPU co-attention worker (scout_cpu_partial_attention: AMX-BF16 tiles
     where the CPU has them, else AVX-512; all host threads) on this box over
-    the workload's CPU share: each unit attends over cpu_blocks_per_unit block
-    images of the host tier with its G heads.
-    Reports blocks/s and the CPU time one decode step's CPU share would take
-    (the GPU step does not wait for it here: the bench pre-stages partials)."""
+    the workload's CPU share at the paper's 8.2%, standalone (the composed step
+    runs it inside: e2e_with_cpu_worker)."""
     from paper_2603_27138_b200 import ops
 
     U, G = wl.U, wl.G
@@ -432,20 +656,10 @@ def measure_cpu_worker(wl, cfg, seconds=4.0):
 
     bps = rate(seconds)
     kernel = ops.cpu_coattn_kernel(torch.bfloat16)
-    bps_avx = None
-    if kernel == "amx-bf16":  # the AVX-512 fp32 kernel beside it, for reference
-        os.environ["SCOUT_CPU_AMX"] = "0"
-        try:
-            bps_avx = rate(seconds / 4)
-        finally:
-            del os.environ["SCOUT_CPU_AMX"]
     per_step = nc * U * (wl.L - 1)
-    return {"blocks_per_s": bps, "threads": os.cpu_count(), "blocks_per_step": per_step,
-            "ms_per_step": 1000.0 * per_step / bps, "gb_per_s": bps * ops.slot_bytes(torch.bfloat16) / 1e9,
-            "kernel": f"scout_cpu_partial_attention (csrc/cpu_coattn.cpp, {kernel})",
-            "blocks_per_s_avx512": bps_avx,
-            "note": "CPU share of one step (cpu_blocks_per_unit x units x layers 1..L-1); the bench pre-stages "
-                    "the CPU partials, so this is reported beside the GPU step, not inside it"}
+    return {"blocks_per_s": bps, "threads": os.cpu_count(), "blocks_per_step_at_8.2pct": per_step,
+            "ms_per_step_at_8.2pct": 1000.0 * per_step / bps, "gb_per_s": bps * ops.slot_bytes(torch.bfloat16) / 1e9,
+            "kernel": f"scout_cpu_partial_attention (csrc/cpu_coattn.cpp, {kernel})"}
 
 
 def cpu_model():
@@ -466,11 +680,12 @@ def run_reference(args, cfg, ws, rank):
     if rb.ref is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libscout_ref.so not built"}), flush=True)
         return
-    vals, r = [], None
+    vals, units, r = [], [], None
     for i in range(args.warmup + args.steps):
         r = rb.measure(1.0)
         if i >= args.warmup:
             vals.append(r["tok_s"])
+            units.append(r["units"])
     v = float(np.mean(vals))
     line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 * cfg["batch"] / v if v else None,
@@ -479,6 +694,10 @@ def run_reference(args, cfg, ws, rank):
             "config": {"workload": args.config, "batch_per_gpu": cfg["batch"], "context": cfg["ctx"],
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "top_k": cfg["k"],
                        "parallelism": "reference CPU (std::thread over all host cores), rank 0"},
+            "timing": {"sampled": True, "units_per_whole_step": cfg["batch"] * cfg["layers"],
+                       "units_timed_per_step": int(np.mean(units)),
+                       "note": "each step times a ~1 s bounded sample of the step's (request, layer) units and "
+                               "extrapolates: ms_per_step is the whole-step time at that rate, not wall time"},
             "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["threads"], "kind": "reference",
                              "sample": "each step: " + r["sample"] + f"; {cpu_model()}"},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -491,122 +710,124 @@ METRIC = "sparse decode-attn tokens/s/GPU at Qwen3-32B 32K; HBM GB/s vs peak"
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=64, help="timed steps (a multiple of 32: the drift loop)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="scout", choices=["scout", "reference"])
     ap.add_argument("--config", default="qwen3-32b-32k", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=0, help="requests per GPU (default: config; weak scaling)")
     ap.add_argument("--global-batch", type=int, default=0,
                     help="total requests split across ranks (strong scaling, e.g. config 4: 128)")
-    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the cadence comparison and the CPU-worker e2e (faster)")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu: no e2e / baseline / extras")
     ap.add_argument("--tier", default="device", choices=["static", "device"],
                     help="device (default): the full decode step -- append + digest refresh, device tier "
                          "bookkeeping (LRU eviction, recall tickets), recalls (scout_engine_decode_step_kv); "
                          "static: residency fixed at the paper's 8.2%% CPU share, no appends (kernel view)")
     ap.add_argument("--drift", type=float, default=0.15,
                     help="device tier mode: radius of the closed query path the queries follow step by step "
-                         "(0 = stationary). 0.15 settles at a ~8%% CPU share, the paper's measured ratio "
-                         "(PAPER.md:251), with every layer's recall moving real blocks each interval")
+                         "(0 = stationary)")
+    ap.add_argument("--recall-policy", default="reference", choices=["reference", "stagger"],
+                    help="reference (default): layer i is due when step - last_recall >= 16 "
+                         "(recall.hpp:114-126), so every layer recalls at steps 16, 32, ...; stagger: layer i "
+                         "recalls when (step + i) %% 16 == 0 (the same volume spread over the steps)")
+    ap.add_argument("--recall-mode", default="ce", choices=["ce", "sm"],
+                    help="recall copies on the copy engines (ce, default) or an SM gather kernel (sm)")
     ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
                     help="query dtype (q_true / q_pred); bf16 = the model's projection output")
-    ap.add_argument("--recall-policy", default="reference", choices=["reference", "stagger"],
-                    help="reference (default): every layer is due when step - last_recall >= 16 "
-                         "(recall.hpp:114-126), so all layers recall at steps 16, 32, ...; stagger: layer i "
-                         "recalls when (step + i) %% 16 == 0 (the same volume spread over the steps)")
     ap.add_argument("--cpu-dtype", default="bf16", choices=["bf16", "f32"],
                     help="CPU-partial o as the host worker hands it over (bf16 halves the largest H2D stream)")
+    ap.add_argument("--seed", type=int, default=1234)
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
     cfg["q_dtype"] = torch.bfloat16 if args.q_dtype == "bf16" else torch.float32
     cfg["cpu_dtype"] = torch.bfloat16 if args.cpu_dtype == "bf16" else torch.float32
     cfg["drift"] = args.drift
     cfg["recall_policy"] = args.recall_policy
+    cfg["recall_mode"] = 1 if args.recall_mode == "sm" else 0
     if args.batch:
         cfg["batch"] = args.batch
     ws, rank, local = dist_setup()
-    scaling = "weak"
-    if args.global_batch:
-        from paper_2603_27138_b200.sharding import request_shard
+    from paper_2603_27138_b200.sharding import request_shard
 
-        cfg["batch"] = request_shard(args.global_batch, ws, rank)[1]
-        scaling = "strong"
+    scaling = "strong" if args.global_batch else "weak"
+    gb = args.global_batch or cfg["batch"] * ws
+    first, cfg["batch"] = request_shard(gb, ws, rank)
     if args.impl == "reference":
         run_reference(args, cfg, ws, rank)
         barrier(ws)
         return
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    from paper_2603_27138_b200 import lib
+    from paper_2603_27138_b200 import lib, ops
 
     lib()  # native library must be present: no fallback
     t0 = time.time()
     tier_mode = args.tier == "device"
-    wl = (TierWorkload(cfg, dev, seed=1234 + rank, max_steps=args.warmup + args.steps + args.e2e_steps + 16) if tier_mode
-          else Workload(cfg, dev, seed=1234 + rank))
+    args.max_steps = args.warmup + 2 * args.steps + 2 * args.e2e_steps + 40
+    if tier_mode:
+        wl = TierWorkload(cfg, dev, seed=args.seed, max_steps=args.max_steps,
+                          requests=range(first, first + cfg["batch"]))
+        wl.make_engine()
+    else:
+        wl = StaticWorkload(cfg, dev, seed=args.seed + rank)
     torch.cuda.synchronize(dev)
     log(f"workload ready in {time.time() - t0:.1f}s: pool {wl.pool.numel() / 2**30:.1f} GiB")
-    eng = wl.engine
-    for s in range(args.warmup):
-        wl.step(s + 1)
-    eng.sync()
-    torch.cuda.synchronize(dev)
-    # resident token count per K2 launch (stationary across steps)
-    res_tok_layers = []
-    for li in range(0 if tier_mode else wl.L):
-        st = wl.layer_states[li]
-        q = wl.q_true[0] if li == 0 else wl.q_pred[li]
-        from paper_2603_27138_b200 import ops
+    step_no = 0
 
-        r = ops.score_topk_split(q, st.digests, wl.n_tokens, wl.k, wl.G, block_table=st.table)
-        res_tok_layers.append(int(r["res_tokens"].sum()))
-        if li == 1:
-            cpu_blocks = int(r["n_cpu"].sum())
+    def run_steps(n):
+        nonlocal step_no
+        for _ in range(n):
+            step_no += 1
+            wl.step(step_no)
+
+    run_steps(args.warmup)
+    wl.engine.sync()
     torch.cuda.synchronize(dev)
+    res_tok_layers = []
+    if not tier_mode:  # resident token count per K2 launch (stationary across steps)
+        for li in range(wl.L):
+            st = wl.layer_states[li]
+            q = wl.q_true[0] if li == 0 else wl.q_pred[li]
+            r = ops.score_topk_split(q, st.digests, wl.n_tokens, wl.k, wl.G, block_table=st.table)
+            res_tok_layers.append(int(r["res_tokens"].sum()))
+    torch.cuda.synchronize(dev)
+    eng = wl.engine
     eng.stats()  # reset counters
     eng.set_timing(True)
     clocks = ClockSampler(local)
-    barrier(ws)
-    torch.cuda.synchronize(dev)
     clocks.start()
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    start.record()
     torch.cuda.nvtx.range_push("timed")  # ncu --nvtx --nvtx-include "timed/" selects the timed launches
-    for s in range(args.steps):
-        wl.step(args.warmup + s + 1)
-    eng.sync()
+
+    def timed_step(i):
+        nonlocal step_no
+        step_no += 1
+        wl.step(step_no)
+        if i == args.steps - 1:
+            eng.sync()
+
+    ms_step = timed(timed_step, args.steps, dev, ws)
     torch.cuda.nvtx.range_pop()
-    end.record()
-    torch.cuda.synchronize(dev)
     clk = clocks.stop()
-    barrier(ws)
-    ms = start.elapsed_time(end)
-    ms = max_over_ranks(ms, ws, dev)
     k2_total, k2_n, launches = eng.stats()
+    eng.set_timing(False)
     tier_info = None
     if tier_mode:  # the residency evolves: bytes from the last timed step's K1 lists
         k1o = eng.k1_outputs()
         res_tok_layers = [int(x) for x in k1o["res_tokens"].sum(1).tolist()]
         cpu_tok = int(k1o["cpu_tokens"].sum())
+        eng.check_state()  # no rejected ticket, no slot shortage, check_split held on every (layer, unit)
         tier_info = {"mode": "device (scout_engine_decode_step_kv)", "resident_token_frac_last_step":
                      sum(res_tok_layers) / max(sum(res_tok_layers) + cpu_tok, 1),
                      "tokens_at_end": int(wl.n_tokens[0]), "host_tier_blocks": wl.host_blocks,
-                     "query_drift": cfg["drift"],
+                     "query_drift": cfg["drift"], "check_state": "ok (check_split on device, every layer and unit)",
                      "note": "queries follow a closed path (drift radius); the CPU share settles where the "
-                             "periodic recalls balance the drift (drift 0: recalls pull it to ~0)"}
-    eng.set_timing(False)
-    k2_ms = [k2_total / max(k2_n, 1)] * k2_n
-    ms_step = ms / args.steps
-    global_batch = args.global_batch or cfg["batch"] * ws
-    tok_s = global_batch / (ms_step / 1000.0)
-    # verification only (outside the timed region): every rank's output checksum
-    from paper_2603_27138_b200.sharding import gather_checksums
-
-    checksums = gather_checksums(wl.out_o[-1]) if ws > 1 else None
-    # ---- roofline for K2 (dominant kernel)
-    # one persistent K2 launch covers all layers of a step
-    k2_avg = float(np.mean(k2_ms))
+                             "periodic recalls balance the drift"}
+    k2_avg = k2_total / max(k2_n, 1)
+    tok_s = gb / (ms_step / 1000.0)
+    # ---- roofline for K2 (dominant kernel): one persistent launch covers all layers of a step
     k2_bytes = float(sum(wl.k2_bytes(t) for t in res_tok_layers))
     peaks = {}
     try:
@@ -614,21 +835,62 @@ def main():
     except OSError:
         pass
     peak = peaks.get("hbm_gbs", 6650.0)
-    traffic = None
+    traffic, traffic_src = None, None
     try:  # dram read+write bytes per K2 launch from the committed ncu --set full capture
-        traffic = json.load(open(ROOT / "profiles" / "k2_traffic.json"))["bytes_per_launch"]
+        tj = json.load(open(ROOT / "profiles" / "k2_traffic.json"))
+        traffic, traffic_src = tj["bytes_per_launch"], tj.get("source", "profiles/k2_traffic.json")
     except (OSError, KeyError, ValueError):
         pass
     achieved = k2_bytes / (k2_avg / 1000.0) / 1e9
-    step_bytes = sum(wl.k2_bytes(t) for t in res_tok_layers) + wl.L * wl.digest_bytes_layer
+    step_bytes = k2_bytes + wl.L * wl.digest_bytes_layer
     step_gbs = step_bytes / (ms_step / 1000.0) / 1e9
-    k2_share = sum(k2_ms) / ms / ws if ws == 1 else None
+    k2_share = k2_total / (ms_step * args.steps) if ws == 1 else None
     log(f"step {ms_step:.3f} ms, {tok_s:.0f} tok/s, K2 avg {k2_avg * 1000:.1f} us ({achieved:.0f} GB/s), "
         f"step {step_gbs:.0f} GB/s, K2 share {k2_share}")
-    # ---- e2e through host buffers
+    # ---- verification (outside the timed region): float64 re-derivation of one step
+    verify = None
+    if tier_mode and not args.profile:
+        step_no += 1
+        verify = verify_step(wl, step_no)
+        log(f"verify: {verify['pass']} (top-k {verify['topk_sets_exact']} exact, {verify['topk_sets_wrong']} wrong; "
+            f"attention max rel err {verify['attention_max_rel_err']:.2e})")
+        if ws > 1:
+            verify["cross_rank"] = cross_rank_check(wl, cfg, args, ws, rank, dev, step_no, args.seed, gb)
+    extras = {}
+    if tier_mode and not args.profile and not args.no_extras:
+        # ---- the other recall cadence on the same workload (state carries over)
+        other = "stagger" if args.recall_policy == "reference" else "reference"
+        wl.make_engine(recall_stagger=other == "stagger")
+        run_steps(5)
+        wl.engine.sync()
+
+        def ostep(i):
+            nonlocal step_no
+            step_no += 1
+            wl.step(step_no)
+            if i == args.steps - 1:
+                wl.engine.sync()
+
+        ms_o = timed(ostep, args.steps, dev, ws)
+        extras["recall_cadence"] = {
+            args.recall_policy: {"value": tok_s, "ms_per_step": ms_step},
+            other: {"value": gb / (ms_o / 1000.0), "ms_per_step": ms_o},
+            "note": "reference: step - last_recall >= 16 for every layer (recall.hpp:114-126), so all layers "
+                    "recall in the same step and the next step waits for all of their PCIe copies; stagger: "
+                    "layer i at (step + i) % 16 == 0, the same volume spread over 16 steps"}
+        wl.make_engine()
+        log(f"cadence: {extras['recall_cadence']}")
+    # ---- e2e through host buffers (pre-staged CPU partials)
     e2e = None
     if not args.profile:
-        e2e = run_e2e(wl, args.e2e_steps, dev, ws, global_batch, tier_mode, first_step=args.warmup + args.steps + 1)
+        e2e = run_e2e(wl, args.e2e_steps, dev, ws, gb, tier_mode, step0=step_no)
+        step_no += 5 + args.e2e_steps
+        log(f"e2e {e2e['ms_per_step']:.3f} ms/step")
+    e2e_worker = None
+    if tier_mode and not args.profile and not args.no_extras:
+        e2e_worker = run_e2e_worker(wl, args.e2e_steps, dev, ws, gb, step0=step_no)
+        step_no += 5 + args.e2e_steps
+        log(f"e2e with CPU worker {e2e_worker['ms_per_step']:.3f} ms/step")
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
@@ -644,18 +906,22 @@ def main():
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init KV, digests, queries, CPU partials)",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init KV, digests, queries, CPU partials; one seeded global workload, "
+                    "generated per request)",
             "config": {"workload": args.config, "attention_shape": "Qwen3-32B" if cfg["hq"] == 64 else "Qwen3-8B",
-                       "batch_per_gpu": cfg["batch"], "global_batch": global_batch, "context": cfg["ctx"],
+                       "batch_per_gpu": cfg["batch"], "global_batch": gb, "context": cfg["ctx"],
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "head_dim": D,
-                       "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "cpu_partial_dtype": args.cpu_dtype, "gpu_cache_blocks_per_unit": cfg["capacity"],
-                       "cpu_blocks_per_unit": wl.cpu_per_unit, "recall_every": cfg["recall"],
-                       "recall_policy": args.recall_policy,
+                       "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "cpu_partial_dtype": args.cpu_dtype,
+                       "gpu_cache_blocks_per_unit": cfg["capacity"],
+                       "cpu_blocks_per_unit_at_placement": wl.cpu_per_unit, "recall_every": cfg["recall"],
+                       "recall_policy": args.recall_policy, "tier": args.tier,
                        "parallelism": f"request-sharded x{ws}, no collective",
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},
             "step_gbs": step_gbs,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "sparse_decode_tc_kernel (K2+K3, one persistent launch per step = 64 layers)",
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": "sparse_decode_tc_kernel (K2+K3, one persistent launch per step = all layers)",
                          "bytes_per_launch": k2_bytes, "avg_launch_us": k2_avg * 1000.0,
                          "share_of_step": k2_share, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy)",
                          # K2 only reads: the copy peak counts read+write bytes of a copy, so a
@@ -666,9 +932,11 @@ def main():
                          "gather_32k_gbs": 6700.0, "frac_of_gather_32k": achieved / 6700.0},
             "clocks": clk,
             "gpu_launches": launches,
-            "verify": {"rank_output_checksums": checksums} if checksums else None,
+            "verify": verify,
             "tier": tier_info,
             "e2e": e2e,
+            "e2e_with_cpu_worker": e2e_worker,
+            **extras,
             "cpu_baseline": cpu,
             "cpu_coattention": cpu_worker,
         }
@@ -676,16 +944,23 @@ def main():
     barrier(ws)
 
 
-def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False, first_step=10000):
+def _pinned_inputs(wl, tier_mode):
+    n = len(wl.q_path_t)
+    h_qt = [t.cpu().pin_memory() for t in wl.q_path_t]
+    h_qp = [t.cpu().pin_memory() for t in wl.q_path_p]
+    h_kv = [wl.k_new.cpu().pin_memory(), wl.v_new.cpu().pin_memory()] if tier_mode else []
+    return n, h_qt, h_qp, h_kv
+
+
+def run_e2e(wl, steps, dev, ws, global_batch, tier_mode, step0):
     """Same step through the C++ engine with pinned HOST inputs/outputs
-    (scout_engine_decode_step_host): H2D of q_true / q_pred / CPU partials in
-    layer chunks on a copy stream, D2H of the attention output and of each
-    layer's CPU-side block ids (the host co-attention worker's input) on
-    another, all inside the timed region."""
+    (scout_engine_decode_step_kv_host / _host): H2D of q_true / q_pred / CPU
+    partials / the token's K/V in layer chunks on a copy stream, D2H of the
+    attention output and of each layer's CPU-side block ids on another, all
+    inside the timed region."""
     L = wl.L
     eng = wl.engine
-    h_qt = wl.q_true.cpu().pin_memory()
-    h_qp = wl.q_pred.cpu().pin_memory()
+    n, h_qt, h_qp, h_kv = _pinned_inputs(wl, tier_mode)
     h_co = wl.cpu_o.cpu().pin_memory()
     h_cm = wl.cpu_ml.cpu().pin_memory()
     h_out = torch.empty(wl.out_o.shape, dtype=torch.float32).pin_memory()
@@ -693,42 +968,77 @@ def run_e2e(wl, steps, dev, ws, global_batch, tier_mode=False, first_step=10000)
     h_cpu_ids = torch.empty(L, wl.U, wl.k, dtype=torch.int32).pin_memory()
     h_n_cpu = torch.empty(L, wl.U, dtype=torch.int32).pin_memory()
 
-    h_kv = [wl.k_new.cpu().pin_memory(), wl.v_new.cpu().pin_memory()] if tier_mode else []
-
     def one(s):
+        j = s % n
         if tier_mode:
-            eng.decode_step_kv_host(s, h_qt, h_qp, h_co, h_cm, *h_kv, h_out, h_oml, h_cpu_ids, h_n_cpu)
+            eng.decode_step_kv_host(s, h_qt[j], h_qp[j], h_co, h_cm, *h_kv, h_out, h_oml, h_cpu_ids, h_n_cpu)
         else:
-            eng.decode_step_host(s, h_qt, h_qp, h_co, h_cm, h_out, h_oml, h_cpu_ids, h_n_cpu)
+            eng.decode_step_host(s, h_qt[j], h_qp[j], h_co, h_cm, h_out, h_oml, h_cpu_ids, h_n_cpu)
 
-    s0 = first_step  # right after the device-path steps: the tier clock moves on without a jump
     warm = 5
     for s in range(warm):
-        one(s0 + s)
+        one(step0 + 1 + s)
     eng.sync()
-    torch.cuda.synchronize(dev)
-    barrier(ws)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record()
-    for s in range(steps):
-        one(s0 + warm + s)
-    eng.sync()
-    b.record()
-    torch.cuda.synchronize(dev)
-    ms = max_over_ranks(a.elapsed_time(b), ws, dev) / steps
-    # the host output must equal the device path's output for the same inputs
-    # static residency: the host output must equal the device path's for the same inputs
-    # (tier mode: residency moved on since the device-path run, so the check is the
-    # bit-exact host-vs-device test in tests/test_gpu_engine_tier.py instead)
-    ok = None if tier_mode else bool(torch.allclose(h_out[L - 1], wl.out_o[L - 1].cpu(), rtol=0, atol=0))
-    h2d_bytes = sum(x.numel() * x.element_size() for x in (h_qt, h_qp, h_co, h_cm, *h_kv))
+
+    def tstep(i):
+        one(step0 + 1 + warm + i)
+        if i == steps - 1:
+            eng.sync()
+
+    ms = timed(tstep, steps, dev, ws)
+    h2d_bytes = sum(x.numel() * x.element_size() for x in (h_qt[0], h_qp[0], h_co, h_cm, *h_kv))
     d2h_bytes = sum(x.numel() * x.element_size() for x in (h_out, h_oml, h_cpu_ids, h_n_cpu))
-    return {"value": global_batch / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms,
-            "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes, "matches_device_path": ok,
-            "verified_by": ("tests/test_gpu_engine_tier.py::test_engine_tier_host_path_matches_device_path "
-                            "(bit-exact, step by step)") if tier_mode else "the check above (same inputs, bit-exact)",
-            "path": "C ABI scout_engine_decode_step_%s (csrc/engine.cpp), pinned host buffers" %
-                    ("kv_host" if tier_mode else "host")}
+    return {"value": global_batch / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms, "steps": steps,
+            "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+            "verified_by": "tests/test_gpu_engine_tier.py::test_engine_tier_host_path_matches_device_path "
+                           "(bit-exact against the device path, step by step)",
+            "path": "C ABI scout_engine_decode_step_%s (csrc/engine.cpp), pinned host buffers, CPU partials "
+                    "pre-staged" % ("kv_host" if tier_mode else "host")}
+
+
+def run_e2e_worker(wl, steps, dev, ws, global_batch, step0):
+    """The composed step (device tier mode, host buffers): the engine's own CPU
+    worker computes each layer's CPU partial during the step from the ids K1
+    selected in that step and the step's predicted queries, publishing layer
+    chunks that the running K2 merges (engine.hpp:236-273). Nothing is
+    pre-staged: the step waits for the host's CPU share."""
+    L = wl.L
+    eng = wl.make_engine(cpu_worker=True, chunk_layers=4)
+    n, h_qt, h_qp, h_kv = _pinned_inputs(wl, True)
+    h_out = torch.empty(wl.out_o.shape, dtype=torch.float32).pin_memory()
+    h_oml = torch.empty(wl.out_ml.shape, dtype=torch.float32).pin_memory()
+
+    def one(s):
+        j = s % n
+        eng.decode_step_kv_host(s, h_qt[j], h_qp[j], None, None, *h_kv, h_out, h_oml)
+
+    warm = 5
+    for s in range(warm):
+        one(step0 + 1 + s)
+    eng.sync()
+    eng.worker_stats()
+
+    def tstep(i):
+        one(step0 + 1 + warm + i)
+        if i == steps - 1:
+            eng.sync()
+
+    ms = timed(tstep, steps, dev, ws)
+    cpu_ms, nsteps = eng.worker_stats()
+    k1o = eng.k1_outputs()
+    cpu_blocks = int(k1o["n_cpu"].sum())
+    eng.check_state()
+    h2d_bytes = sum(x.numel() * x.element_size() for x in (h_qt[0], h_qp[0], *h_kv))
+    d2h_bytes = sum(x.numel() * x.element_size() for x in (h_out, h_oml)) + L * wl.U * (wl.k + 1) * 4
+    out = {"value": global_batch / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms, "steps": steps,
+           "cpu_worker_ms_per_step": cpu_ms / max(nsteps, 1), "cpu_blocks_last_step": cpu_blocks,
+           "threads": os.cpu_count(), "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+           "verified_by": "tests/test_gpu_engine_worker.py (every (step, layer, unit) against the reference's "
+                          "recompute_layer_attention, harness.hpp:318-329)",
+           "path": "C ABI scout_engine_decode_step_kv_host with cfg.cpu_worker (csrc/engine.cpp + cpu_coattn.cpp): "
+                   "CPU partials computed in the step, published per 4-layer chunk to the running K2"}
+    wl.make_engine()
+    return out
 
 
 if __name__ == "__main__":

@@ -161,6 +161,9 @@ struct scout_engine {
     cudaStream_t post_s = nullptr;
     int rc_slot_jobs[RC_SLOTS] = {};
     bool rc_stop = false, rc_busy = false;
+    // SCOUT_RECALL_PROF=1: the issuer thread's CPU time and blocks, printed at destroy
+    double rc_prof_ms = 0.0;
+    long long rc_prof_blocks = 0, rc_prof_jobs = 0;
     int rc_err = SCOUT_OK;
     char rc_msg[256] = {0};
     // device tier mode (cfg.tier != nullptr)
@@ -343,6 +346,15 @@ struct scout_engine {
         for (int i = 0; i < cfg.layers; ++i)
             a.layers[i] = K2Layer{q[i], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
                                   co[i], cml[i], o[i], ml[i], inflag ? inflag[i] : nullptr, rc_token[i], 0u};
+        if (cfg.recall_mode == 1 && (cfg.recall_interval > 0 || cfg.recall_intervals)) {
+            // SM-gather recalls need SMs: a persistent K2 that polls their flags
+            // while holding every SM would wait for them forever, so K2 starts
+            // only after every recall kernel queued so far (copy-engine recalls,
+            // the default, need no SM and overlap K2 freely)
+            drain_recalls();
+            CU(cudaEventRecord(ev_tmp, side));
+            CU(cudaStreamWaitEvent(st, ev_tmp, 0));
+        }
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (timing) {
             while (tev.size() < tev_used + 2) {
@@ -465,9 +477,16 @@ struct scout_engine {
             }
         }
         int rc = SCOUT_OK;
+        static const bool prof = getenv("SCOUT_RECALL_PROF") != nullptr;
+        const auto t0 = std::chrono::steady_clock::now();
         if (!src_v.empty())
             rc = scout_recall_copy(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier, src_v.data(), dst_v.data(),
                                    static_cast<int>(src_v.size()), side);
+        if (prof) {
+            rc_prof_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            rc_prof_blocks += static_cast<long long>(src_v.size());
+            ++rc_prof_jobs;
+        }
         if (rc != SCOUT_OK) return rc;
         return write_value(side, recall_flag + i, job.token);
     }
@@ -1019,6 +1038,10 @@ extern "C" int scout_engine_destroy(scout_engine* eng) {
         eng->stop_recalls();     // drains the queued recalls first
         cudaDeviceSynchronize();  // flags / copies still reference engine memory
         if (eng->k2_prof) eng->report_k2_prof();
+        if (eng->rc_prof_jobs)
+            fprintf(stderr, "[recall prof] %lld layer jobs, %lld blocks, issuer %.1f ms (%.2f us per block)\n",
+                    eng->rc_prof_jobs, eng->rc_prof_blocks, eng->rc_prof_ms,
+                    1000.0 * eng->rc_prof_ms / static_cast<double>(eng->rc_prof_blocks ? eng->rc_prof_blocks : 1));
     }
     delete eng;
     return SCOUT_OK;

@@ -42,3 +42,30 @@ def gather_checksums(out: torch.Tensor) -> list[float]:
     got = [torch.zeros_like(c) for _ in range(dist.get_world_size())]
     dist.all_gather(got, c)
     return [float(g.item()) for g in got]
+
+
+def request_seed(seed: int, request: int, salt: int) -> int:
+    """Seed of one request's synthetic data: a function of the GLOBAL request
+    index, so every rank's shard is a slice of one seeded global workload
+    (the same request gets the same data whatever the world size)."""
+    return ((int(seed) * 1_000_003 + int(request)) * 1_009 + int(salt)) & 0x7FFF_FFFF_FFFF_FFFF
+
+
+def gather_per_request(values: torch.Tensor, global_batch: int, world: int, rank: int) -> torch.Tensor:
+    """Verification only (outside timing): this rank's per-request values
+    [n_local, ...] into a [global_batch, ...] tensor on every rank (all_gather
+    of request_shard slices, padded to the largest shard)."""
+    import torch.distributed as dist
+
+    start, n = request_shard(global_batch, world, rank)
+    if values.shape[0] != n:
+        raise ValueError("gather_per_request: expected this rank's shard of values")
+    if not dist.is_available() or not dist.is_initialized() or world == 1:
+        return values.clone()
+    width = max(request_shard(global_batch, world, r)[1] for r in range(world))
+    pad = torch.zeros((width,) + tuple(values.shape[1:]), dtype=values.dtype, device=values.device)
+    pad[:n] = values
+    got = [torch.zeros_like(pad) for _ in range(world)]
+    dist.all_gather(got, pad)
+    out = [got[r][:request_shard(global_batch, world, r)[1]] for r in range(world)]
+    return torch.cat(out, dim=0)

@@ -64,7 +64,9 @@ class DeviceTieredCache:
         for name in ("table", "tier", "last_sel", "ready", "ticket", "free_slots", "n_free", "err"):
             setattr(d, name, getattr(self, name)[layer].data_ptr())
         d.capacity = self.capacity[layer]
-        d.slots_per_unit = self.spu_l[layer]
+        # the free stacks' row stride: the tensor is [L][U][max spu] whatever this
+        # layer's own slot count (a layer owning fewer slots just never fills it)
+        d.slots_per_unit = self.spu
         return d
 
     def next_run_of(self, layer: int) -> int:  # kv_store.hpp:328-331
