@@ -11,8 +11,11 @@
 //
 // The functions are templates over the argument types, so they take the
 // reference's own scout:: structs unchanged (any type with the same member
-// names works); scout_b200::* mirror types are provided for code that does not
-// include the reference headers. Error behaviour follows the reference:
+// names works), and their results convert to them (PartialResult,
+// DigestResult): the reference's ScoutEngine compiles with its hot-path call
+// sites swapped to scout_b200:: and nothing else changed (INTEGRATION.md §1,
+// proven by tests/cpp/test_dropin_engine.cpp); scout_b200::* mirror types are
+// provided for code that does not include the reference headers. Error behaviour follows the reference:
 // std::invalid_argument for argument errors (k == 0, scale <= 0, empty block,
 // dimension mismatch), std::runtime_error for device failures.
 //
@@ -77,6 +80,38 @@ struct PartialAttention {
         return p;
     }
     bool is_empty() const { return token_count == 0; }
+};
+
+// Results that convert to the caller's own structs: a reference call site
+// such as `const PartialAttention gpu = scout_b200::partial_attention(...)`
+// (scout::PartialAttention) or `st.digests.back() = scout_b200::build_digest(...)`
+// (scout::BlockDigest) compiles unchanged; the mirror types above are the
+// results' bases, so code without the reference headers uses them directly.
+struct PartialResult : PartialAttention {
+    PartialResult() = default;
+    explicit PartialResult(const PartialAttention& p) : PartialAttention(p) {}
+    template <class T, class = decltype(T{}.o_acc), class = decltype(T{}.token_count)>
+    operator T() const {
+        T t;
+        t.o_acc = o_acc;
+        t.max_logit = max_logit;
+        t.denom = denom;
+        t.token_count = token_count;
+        return t;
+    }
+};
+struct DigestResult : BlockDigest {
+    template <class T, class = decltype(T{}.lo), class = decltype(T{}.block_id)>
+    operator T() const {
+        T t;
+        t.method = static_cast<decltype(t.method)>(static_cast<int>(method));
+        t.lo = lo;
+        t.hi = hi;
+        t.mean = mean;
+        t.block_id = block_id;
+        t.layer = layer;
+        return t;
+    }
 };
 
 namespace detail {
@@ -180,7 +215,7 @@ inline std::vector<double> scores_and_topk(const Vec& q, const Digests& ds, std:
 
 // -------------------------------------------------------------- digest.hpp
 template <class MatT, class Method>
-inline BlockDigest build_digest(const MatT& keys, Method method, std::size_t block_id = 0, std::size_t layer = 0) {
+inline DigestResult build_digest(const MatT& keys, Method method, std::size_t block_id = 0, std::size_t layer = 0) {
     if (keys.rows == 0) throw std::invalid_argument("build_digest: empty block");
     if (keys.rows > SCOUT_BLOCK_SIZE || keys.cols > SCOUT_HEAD_DIM)
         throw std::invalid_argument("scout_b200: block larger than 64 x 128 unsupported");
@@ -205,7 +240,7 @@ inline BlockDigest build_digest(const MatT& keys, Method method, std::size_t blo
     check(scout_digest_build(pool.p, SCOUT_F32, minmax ? SCOUT_DIGEST_MINMAX : SCOUT_DIGEST_MEAN, 1, mp, mp + 1, mp + 2,
                              mp + 3, dig.p, 8, nullptr));
     cuda(cudaDeviceSynchronize(), "build_digest");
-    BlockDigest d;
+    DigestResult d;
     d.method = minmax ? DigestMethod::minmax : DigestMethod::mean;
     d.block_id = block_id;
     d.layer = layer;
@@ -318,18 +353,33 @@ inline PartialAttention partial_attention_impl(const Vec& q, const BlockPtrs& bl
 }
 
 template <class KvBlockT>
-inline PartialAttention partial_attention(const Vec& q, std::span<const KvBlockT* const> blocks, double scale) {
-    return partial_attention_impl(q, blocks, scale);
+inline PartialResult partial_attention(const Vec& q, std::span<const KvBlockT* const> blocks, double scale) {
+    return PartialResult(partial_attention_impl(q, blocks, scale));
 }
 template <class KvBlockT>
-inline PartialAttention partial_attention(const Vec& q, const std::vector<const KvBlockT*>& blocks, double scale) {
-    return partial_attention_impl(q, blocks, scale);
+inline PartialResult partial_attention(const Vec& q, const std::vector<const KvBlockT*>& blocks, double scale) {
+    return PartialResult(partial_attention_impl(q, blocks, scale));
 }
 
-template <class P>
-inline P merge(const P& a, const P& b) {
+namespace detail {
+// a partial of one struct type as another (same four fields)
+template <class P, class Q>
+inline P partial_as(const Q& q) {
+    P p{};
+    p.o_acc = q.o_acc;
+    p.max_logit = q.max_logit;
+    p.denom = q.denom;
+    p.token_count = q.token_count;
+    return p;
+}
+}  // namespace detail
+
+// merge (attention.hpp:100-114); the result has the first operand's type (the
+// operands may be a PartialResult and a plain partial, e.g. an empty one)
+template <class P, class Q>
+inline P merge(const P& a, const Q& b) {
     using namespace detail;
-    if (a.is_empty()) return b;  // exact identity (attention.hpp:101-102)
+    if (a.is_empty()) return partial_as<P>(b);  // exact identity (attention.hpp:101-102)
     if (b.is_empty()) return a;
     if (a.o_acc.size() != b.o_acc.size()) throw std::invalid_argument("merge: dimension mismatch");
     const std::size_t d = a.o_acc.size();

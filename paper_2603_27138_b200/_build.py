@@ -60,8 +60,13 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
 
 
 def build_oracle(verbose: bool = False) -> None:
-    """Build the CPU checkers under oracle/ (test infrastructure, not the product)."""
+    """Build the CPU checkers under oracle/ (test infrastructure, not the product)
+    and, where the reference headers exist, the drop-in proof binary
+    tests/cpp/_bin/test_dropin_engine (the reference engine with the
+    INTEGRATION.md §1 call swaps, linked to libscout_b200.so)."""
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True,
+                   stdout=None if verbose else subprocess.DEVNULL)
+    subprocess.run(["make", "-s", "-C", str(ROOT / "tests" / "cpp")], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
 
 

@@ -206,7 +206,7 @@ int main() {
         for (double& v : b.values.data) v = rnd(g);
         sb::Vec q(3);
         for (double& v : q) v = rnd(g);
-        const auto p = sb::partial_attention(q, std::vector<const sb::KvBlock*>{&b}, 1.0);
+        const sb::PartialAttention p = sb::partial_attention(q, std::vector<const sb::KvBlock*>{&b}, 1.0);
         const auto e = sb::PartialAttention::empty(3);
         const auto m1 = sb::merge(p, e), m2 = sb::merge(e, p);
         CHECK(m1.o_acc == p.o_acc && m1.denom == p.denom && m1.max_logit == p.max_logit && m2.o_acc == p.o_acc,

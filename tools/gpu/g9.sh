@@ -1,0 +1,2 @@
+timeout 2400 python -m pytest tests -x -q -m gpu 2>&1 | tail -15
+./tests/cpp/_bin/test_dropin_engine | tail -12
