@@ -766,7 +766,7 @@ def main():
     lib()  # native library must be present: no fallback
     t0 = time.time()
     tier_mode = args.tier == "device"
-    args.max_steps = args.warmup + 2 * args.steps + 2 * args.e2e_steps + 40
+    args.max_steps = args.warmup + 3 * args.steps + 2 * args.e2e_steps + 48
     if tier_mode:
         wl = TierWorkload(cfg, dev, seed=args.seed, max_steps=args.max_steps,
                           requests=range(first, first + cfg["batch"]))
@@ -880,6 +880,16 @@ def main():
                     "layer i at (step + i) % 16 == 0, the same volume spread over 16 steps"}
         wl.make_engine()
         log(f"cadence: {extras['recall_cadence']}")
+    # ---- layer by layer: a decoder's loop, layer i's inputs produced after layer i-1's attention
+    if tier_mode and not args.profile and not args.no_extras:
+        ms_lw = run_layerwise(wl, args.steps, dev, ws, step0=step_no)
+        step_no += 5 + args.steps
+        extras["value_layerwise"] = {
+            "value": gb / (ms_lw / 1000.0), "ms_per_step": ms_lw, "recall_policy": args.recall_policy,
+            "path": "scout_engine_decode_layer per layer (C ABI): layer i's q_true / q_pred[i+1] written by a kernel "
+                    "queued after layer i-1's attention (a decoder's data dependency), then begin_layer tickets, K1 "
+                    "of layer i+1 on the engine stream beside K2 of layer i, one K2 launch per layer, post per layer"}
+        log(f"layerwise {ms_lw:.3f} ms/step")
     # ---- e2e through host buffers (pre-staged CPU partials)
     e2e = None
     if not args.profile:
@@ -942,6 +952,40 @@ def main():
         }
         print(json.dumps(line), flush=True)
     barrier(ws)
+
+
+def run_layerwise(wl, steps, dev, ws, step0):
+    """The step as a decoder drives it: one scout_engine_decode_layer call per
+    layer, layer i's queries written into the live query buffers by a copy
+    queued after layer i-1's call (in a model they come from layer i-1's
+    output, so nothing of layer i can start earlier)."""
+    eng = wl.make_engine()
+    L = wl.L
+    qt_live = torch.empty_like(wl.q_path_t[0])
+    qp_live = torch.empty_like(wl.q_path_p[0])
+
+    def one(s):
+        j = s % len(wl.q_path_t)
+        for i in range(L):
+            qt_live[i].copy_(wl.q_path_t[j][i])
+            if i + 1 < L:
+                qp_live[i + 1].copy_(wl.q_path_p[j][i + 1])
+            eng.decode_layer(s, i, qt_live[i], qp_live[i + 1] if i + 1 < L else None, wl.cpu_o[i], wl.cpu_ml[i],
+                             wl.k_new[i], wl.v_new[i], wl.out_o[i], wl.out_ml[i])
+
+    for s in range(5):
+        one(step0 + 1 + s)
+    eng.sync()
+
+    def tstep(i):
+        one(step0 + 6 + i)
+        if i == steps - 1:
+            eng.sync()
+
+    ms = timed(tstep, steps, dev, ws)
+    eng.check_state()
+    wl.make_engine()
+    return ms
 
 
 def _pinned_inputs(wl, tier_mode):

@@ -464,6 +464,20 @@ int scout_engine_decode_step_kv_host(scout_engine* eng, int step, const void* h_
  * SCOUT_OK, or SCOUT_ERR_INVALID_ARGUMENT / SCOUT_ERR_LOGIC naming the first
  * (layer, unit) with an error. */
 int scout_engine_check_state(scout_engine* eng);
+/* Device tier mode, layer by layer: the calls a decoder makes inside its
+ * layer loop (engine.hpp:219-307 per layer), for layers 0, 1, ..., L-1 of a
+ * step in order. Layer i's call applies layer i's due recall tickets, selects
+ * layer i+1 with its predicted query q_pred_next [U*G][128] (q dtype; NULL for
+ * the last layer; layer 0 also selects itself with q_true), runs layer i's
+ * attention + merge with q_true [U*G][128] over the share selected one call
+ * earlier (cpu_o / cpu_ml: layer i's CPU partial, optional), writes out_o
+ * [U*G][128] / out_ml [U*G][2], and appends k_new / v_new [U][128] f32 after
+ * the attention. A layer's inputs need only exist at its call (they come from
+ * the previous layer's output in a decoder); the selection of layer i+1 runs
+ * on the engine's own stream beside layer i's attention. */
+int scout_engine_decode_layer(scout_engine* eng, int step, int layer, const void* q_true, const void* q_pred_next,
+                              const void* cpu_o, const float* cpu_ml, const float* k_new, const float* v_new,
+                              float* out_o, float* out_ml, void* stream);
 /* Order all outstanding side-stream work (recalls) before `stream`. */
 int scout_engine_sync(scout_engine* eng, void* stream);
 /* Device tier mode: the caller changed the K5 state outside the engine

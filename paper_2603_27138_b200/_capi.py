@@ -36,7 +36,7 @@ EXPORTED = (
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv",
     "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
-    "scout_engine_worker_stats", "scout_engine_check_state",
+    "scout_engine_worker_stats", "scout_engine_check_state", "scout_engine_decode_layer",
 )
 
 _vp = C.c_void_p
@@ -155,6 +155,7 @@ def lib() -> C.CDLL:
         L.scout_engine_k1_outputs.argtypes = [_vp] + [C.POINTER(_vp)] * 7
         L.scout_engine_worker_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.scout_engine_check_state.argtypes = [_vp]
+        L.scout_engine_decode_layer.argtypes = [_vp, C.c_int, C.c_int] + [_vp] * 8 + [_vp]
         _lib = L
     return _lib
 

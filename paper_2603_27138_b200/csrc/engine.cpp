@@ -153,7 +153,7 @@ struct scout_engine {
     static constexpr int RC_SLOTS = 4;
     uint8_t* rc_pinned = nullptr;  // RC_SLOTS x (ids [L][U][k] | n [L][U] | dst [L][U][k]) int32
     size_t rc_slot_bytes = 0;
-    static constexpr int MAX_CH = (K2_MAX_LAYERS + 7) / 8 + 1;  // post chunks (+ the short tail chunk)
+    static constexpr int MAX_CH = K2_MAX_LAYERS;  // post chunks (layer-by-layer mode: one per layer)
     cudaEvent_t ev_chunk[RC_SLOTS][MAX_CH] = {};  // post chunk done (post stream)
     cudaEvent_t ev_list[RC_SLOTS][MAX_CH] = {};   // its lists landed (pinned)
     cudaEvent_t ev_post = nullptr, ev_pre = nullptr;
@@ -208,6 +208,10 @@ struct scout_engine {
     std::vector<int64_t> cw_index;         // worker thread only: [L][U][k] host image indices
     double cw_ms = 0.0;                    // CPU time of the worker's partials (summed, reset by stats)
     int cw_steps = 0;
+
+    // layer-by-layer mode (scout_engine_decode_layer): the layer expected next
+    // and the step in progress
+    int lw_next = 0, lw_step = -1;
 
     // instrumentation
     bool timing = false;
@@ -318,21 +322,26 @@ struct scout_engine {
     }
 
     // ---------------------------------------------------------------- K2
+    // K2 over layers [l0, l0 + n) in one persistent launch (the per-layer
+    // arrays q .. inflag are indexed from l0): the whole step (0, L), or one
+    // layer in the layer-by-layer mode
     int launch_k2(int par, const void* const* q, const void* const* co, const float* const* cml, float* const* o,
-                  float* const* ml, const unsigned* const* inflag, bool poll_k1, cudaStream_t st) {
+                  float* const* ml, const unsigned* const* inflag, bool poll_k1, cudaStream_t st, int l0 = 0,
+                  int n = -1) {
+        if (n < 0) n = cfg.layers;
         K2StepArgs a{};
         a.n_units = U;
         a.group = G;
         a.k_stride = cfg.k;
-        a.n_layers = cfg.layers;
+        a.n_layers = n;
         a.scale = cfg.scale;
         a.kv_pool = cfg.kv_pool;
         a.n_tokens = cfg.n_tokens;
-        a.workspace = ws.p;
+        a.workspace = static_cast<uint8_t*>(ws.p) + static_cast<size_t>(l0) * ws_layer;
         a.ws_layer_bytes = ws_layer;
-        a.k1_flag = poll_k1 ? k1_flag : nullptr;
-        a.recall_flag = recall_flag;
-        a.layer_done = layer_done;
+        a.k1_flag = poll_k1 ? k1_flag + l0 : nullptr;
+        a.recall_flag = recall_flag + l0;
+        a.layer_done = layer_done + l0;
         a.token = token;
         a.max_ctas = cfg.max_ctas;
         a.q_bf16 = cfg.q_dtype == SCOUT_BF16;
@@ -343,9 +352,11 @@ struct scout_engine {
             return e ? atoi(e) : 0;
         }();
         a.l2_prefetch = l2pf;
-        for (int i = 0; i < cfg.layers; ++i)
-            a.layers[i] = K2Layer{q[i], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
-                                  co[i], cml[i], o[i], ml[i], inflag ? inflag[i] : nullptr, rc_token[i], 0u};
+        for (int j = 0; j < n; ++j) {
+            const int i = l0 + j;
+            a.layers[j] = K2Layer{q[j], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
+                                  co[j], cml[j], o[j], ml[j], inflag ? inflag[j] : nullptr, rc_token[i], 0u};
+        }
         if (cfg.recall_mode == 1 && (cfg.recall_interval > 0 || cfg.recall_intervals)) {
             // SM-gather recalls need SMs: a persistent K2 that polls their flags
             // while holding every SM would wait for them forever, so K2 starts
@@ -688,13 +699,22 @@ struct scout_engine {
     // `pre`: an event recorded on the step's stream after phases 1-3 (before K2).
     static constexpr int POST_CH = 8, POST_TAIL = 2;
     cudaEvent_t ph_ev[2] = {};  // SCOUT_ENGINE_PHASES: after the plan, after K1
-    int tier_post(int step, int par, unsigned tok, const float* k_new, const float* v_new, cudaEvent_t pre,
-                  cudaStream_t s) {
-        const int L = cfg.layers, nbs = cfg.nb_stride;
-        TierPostArgs pa{};
+    // The post-attention bookkeeping of one step: post_begin sets up the
+    // step's arguments and recall list slot, post_chunk handles layers
+    // [lo, lo+n) once K2 finished them, post_end advances n_tokens and orders
+    // the next step after all of it. recall_due is decided per layer as its
+    // chunk is posted (each (step, layer) once).
+    TierPostArgs pa_step{};
+    int post_slot = 0;
+    bool post_ce = false;
+    int32_t *post_hid = nullptr, *post_hn = nullptr, *post_hd = nullptr;
+    int post_begin(int step, int par, unsigned tok, const float* k_new, const float* v_new) {
+        const int L = cfg.layers;
+        TierPostArgs& pa = pa_step;
+        pa = TierPostArgs{};
         pa.layers = static_cast<const scout_tier_layer*>(tier_dev.p);
         pa.n_layers = L;
-        pa.nbs = nbs;
+        pa.nbs = cfg.nb_stride;
         pa.k = cfg.k;
         pa.step = step;
         pa.ticket_base = n_tickets;
@@ -717,78 +737,81 @@ struct scout_engine {
         pa.n_cpu = I(n_cpu[par]);
         pa.res_tok = I(res_tok[par]);
         pa.cpu_tok = I(cpu_tok[par]);
-        for (int i = 0; i < L; ++i) pa.recall_due[i] = recall_due(step, i);
         pa.plan_out = I(plan_tab);  // the next step's planning view (K1 of this step has read its own)
         pa.plan_step = step + 1;
-        const bool ce = cfg.recall_mode == 0 && rc_pinned != nullptr;
-        const int slot = static_cast<int>(tok % RC_SLOTS);
-        if (ce) {  // this step's list slot must be free (the issuer thread is done with it)
+        post_ce = cfg.recall_mode == 0 && rc_pinned != nullptr;
+        post_slot = static_cast<int>(tok % RC_SLOTS);
+        if (post_ce) {  // this step's list slot must be free (the issuer thread is done with it)
             std::unique_lock<std::mutex> lk(rc_mu);
-            rc_idle.wait(lk, [&] { return rc_slot_jobs[slot] == 0; });
+            rc_idle.wait(lk, [&] { return rc_slot_jobs[post_slot] == 0; });
         }
-        int32_t* hid = ce ? reinterpret_cast<int32_t*>(rc_pinned + slot * rc_slot_bytes) : nullptr;
-        int32_t* hn = ce ? hid + static_cast<size_t>(L) * U * cfg.k : nullptr;
-        int32_t* hd = ce ? hn + static_cast<size_t>(L) * U : nullptr;
-        CU(cudaStreamWaitEvent(post_s, pre, 0));
+        post_hid = post_ce ? reinterpret_cast<int32_t*>(rc_pinned + post_slot * rc_slot_bytes) : nullptr;
+        post_hn = post_ce ? post_hid + static_cast<size_t>(L) * U * cfg.k : nullptr;
+        post_hd = post_ce ? post_hn + static_cast<size_t>(L) * U : nullptr;
+        return SCOUT_OK;
+    }
+    int post_chunk(int step, unsigned tok, int c, int lo, int n) {
+        TierPostArgs& pa = pa_step;
+        const int nbs = cfg.nb_stride;
+        for (int i = lo; i < lo + n; ++i) pa.recall_due[i] = recall_due(step, i);
         int rc;
-        // chunks of POST_CH layers, the last one only POST_TAIL long: it runs
-        // after K2 has ended, on the critical path to the next step
-        for (int c = 0, lo = 0, n = 0; lo < L; ++c, lo += n) {
-            n = L - lo <= POST_TAIL ? L - lo : std::min(POST_CH, L - lo - POST_TAIL);
-            if ((rc = wait_value(post_s, layer_done + lo + n - 1, tok * static_cast<unsigned>(grid))) != SCOUT_OK)
-                return rc;
-            pa.layer0 = lo;
-            ++launches;
-            if ((rc = scout_tier_post_layers(pa, U, n, post_s)) != SCOUT_OK) return rc;
-            bool due = false;
-            for (int i = lo; i < lo + n; ++i) due |= pa.recall_due[i] != 0;
-            if (!due) continue;
-            if (ce) {
-                // the lists travel on their own stream; `side` carries only the
-                // issuer thread's copies and flags (which the next step's K2
-                // waits for), so nothing of the next step may queue ahead there
-                CU(cudaEventRecord(ev_chunk[slot][c], post_s));
-                CU(cudaStreamWaitEvent(rc_list, ev_chunk[slot][c], 0));
-                for (int i = lo; i < lo + n; ++i) {
-                    if (!pa.recall_due[i]) continue;
-                    CU(cudaMemcpyAsync(hid + lk(i), pa.rc_ids + lk(i), static_cast<size_t>(U) * cfg.k * 4,
-                                       cudaMemcpyDeviceToHost, rc_list));
-                    CU(cudaMemcpyAsync(hn + lu(i), pa.rc_n + lu(i), static_cast<size_t>(U) * 4, cudaMemcpyDeviceToHost,
-                                       rc_list));
-                    CU(cudaMemcpyAsync(hd + lk(i), pa.dst + lk(i), static_cast<size_t>(U) * cfg.k * 4,
-                                       cudaMemcpyDeviceToHost, rc_list));
-                }
-                CU(cudaEventRecord(ev_list[slot][c], rc_list));
-                {
-                    std::lock_guard<std::mutex> lk(rc_mu);
-                    for (int i = lo; i < lo + n; ++i) {
-                        if (!pa.recall_due[i]) continue;
-                        rc_jobs.push_back(RcJob{i, tok, slot, c});
-                        ++rc_slot_jobs[slot];
-                    }
-                }
-                rc_cv.notify_one();
-            } else {
-                CU(cudaEventRecord(ev_chunk[slot][c], post_s));
-                CU(cudaStreamWaitEvent(side, ev_chunk[slot][c], 0));
-                for (int i = lo; i < lo + n; ++i) {
-                    if (!pa.recall_due[i]) continue;
-                    ++launches;
-                    if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier,
-                                                      static_cast<long long>(i) * U * nbs, nbs, cfg.host_blocks, U,
-                                                      pa.rc_ids + lk(i), pa.rc_n + lu(i), pa.dst + lk(i), cfg.k, 0,
-                                                      side)) != SCOUT_OK)
-                        return rc;
-                    if ((rc = write_value(side, recall_flag + i, tok)) != SCOUT_OK) return rc;
-                }
-            }
+        if ((rc = wait_value(post_s, layer_done + lo + n - 1, tok * static_cast<unsigned>(grid))) != SCOUT_OK) return rc;
+        pa.layer0 = lo;
+        ++launches;
+        if ((rc = scout_tier_post_layers(pa, U, n, post_s)) != SCOUT_OK) return rc;
+        bool due = false;
+        for (int i = lo; i < lo + n; ++i) due |= pa.recall_due[i] != 0;
+        if (!due) return SCOUT_OK;
+        const int slot = post_slot;
+        if (post_ce) {
+            // the lists travel on their own stream; `side` carries only the
+            // issuer thread's copies and flags (which the next step's K2
+            // waits for), so nothing of the next step may queue ahead there
+            CU(cudaEventRecord(ev_chunk[slot][c], post_s));
+            CU(cudaStreamWaitEvent(rc_list, ev_chunk[slot][c], 0));
             for (int i = lo; i < lo + n; ++i) {
                 if (!pa.recall_due[i]) continue;
-                rc_token[i] = tok;  // the next step's K2 waits for it before streaming layer i
-                pending[i] = tick(step + 1, i);
+                CU(cudaMemcpyAsync(post_hid + lk(i), pa.rc_ids + lk(i), static_cast<size_t>(U) * cfg.k * 4,
+                                   cudaMemcpyDeviceToHost, rc_list));
+                CU(cudaMemcpyAsync(post_hn + lu(i), pa.rc_n + lu(i), static_cast<size_t>(U) * 4, cudaMemcpyDeviceToHost,
+                                   rc_list));
+                CU(cudaMemcpyAsync(post_hd + lk(i), pa.dst + lk(i), static_cast<size_t>(U) * cfg.k * 4,
+                                   cudaMemcpyDeviceToHost, rc_list));
+            }
+            CU(cudaEventRecord(ev_list[slot][c], rc_list));
+            {
+                std::lock_guard<std::mutex> lk(rc_mu);
+                for (int i = lo; i < lo + n; ++i) {
+                    if (!pa.recall_due[i]) continue;
+                    rc_jobs.push_back(RcJob{i, tok, slot, c});
+                    ++rc_slot_jobs[slot];
+                }
+            }
+            rc_cv.notify_one();
+        } else {
+            CU(cudaEventRecord(ev_chunk[slot][c], post_s));
+            CU(cudaStreamWaitEvent(side, ev_chunk[slot][c], 0));
+            for (int i = lo; i < lo + n; ++i) {
+                if (!pa.recall_due[i]) continue;
+                ++launches;
+                if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier,
+                                                  static_cast<long long>(i) * U * nbs, nbs, cfg.host_blocks, U,
+                                                  pa.rc_ids + lk(i), pa.rc_n + lu(i), pa.dst + lk(i), cfg.k, 0,
+                                                  side)) != SCOUT_OK)
+                    return rc;
+                if ((rc = write_value(side, recall_flag + i, tok)) != SCOUT_OK) return rc;
             }
         }
+        for (int i = lo; i < lo + n; ++i) {
+            if (!pa.recall_due[i]) continue;
+            rc_token[i] = tok;  // the next step's K2 waits for it before streaming layer i
+            pending[i] = tick(step + 1, i);
+        }
+        return SCOUT_OK;
+    }
+    int post_end(int step, cudaStream_t s) {
         ++launches;
+        int rc;
         if ((rc = scout_tier_advance(const_cast<int32_t*>(cfg.n_tokens), U, post_s)) != SCOUT_OK) return rc;
         planned_step = step + 1;
         // the next step (planning, K1) follows the bookkeeping
@@ -796,6 +819,21 @@ struct scout_engine {
         post_recorded = true;
         CU(cudaStreamWaitEvent(s, ev_post, 0));
         return SCOUT_OK;
+    }
+    // the whole step's bookkeeping in chunks of POST_CH layers as K2 finishes
+    // them, the last one only POST_TAIL long: it runs after K2 has ended, on
+    // the critical path to the next step
+    int tier_post(int step, int par, unsigned tok, const float* k_new, const float* v_new, cudaEvent_t pre,
+                  cudaStream_t s) {
+        const int L = cfg.layers;
+        int rc;
+        if ((rc = post_begin(step, par, tok, k_new, v_new)) != SCOUT_OK) return rc;
+        CU(cudaStreamWaitEvent(post_s, pre, 0));
+        for (int c = 0, lo = 0, n = 0; lo < L; ++c, lo += n) {
+            n = L - lo <= POST_TAIL ? L - lo : std::min(POST_CH, L - lo - POST_TAIL);
+            if ((rc = post_chunk(step, tok, c, lo, n)) != SCOUT_OK) return rc;
+        }
+        return post_end(step, s);
     }
 
     // K1 lists of this parity were read by the K2 two steps back: wait for it;
@@ -1319,6 +1357,101 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
                 t[0] - tp - tk, t[1], t[2]);
         for (auto& ev : pe) cudaEventDestroy(ev);
     }
+    return SCOUT_OK;
+}
+
+// Layer-by-layer mode (device tier mode): the calls a decoder makes inside its
+// layer loop, in the order of ScoutEngine::decode_step's body for layer i
+// (engine.hpp:219-307): begin_layer's tickets for layer i; K1 for layer i+1
+// with the predicted query (layer 0 also selects itself with the true query,
+// :227-233); K2+K3 for layer i over the share K1 chose one call earlier; the
+// append + seal/evict + recall scheduling of layer i after its attention.
+// Layer i's inputs need only exist when the call is made -- q_true[i] and
+// q_pred[i+1] come from layer i-1's output in a real decoder -- and K1(i+1)
+// may run beside K2(i), on the engine's K1 stream.
+extern "C" int scout_engine_decode_layer(scout_engine* e, int step, int layer, const void* q_true,
+                                         const void* q_pred_next, const void* cpu_o, const float* cpu_ml,
+                                         const float* k_new, const float* v_new, float* out_o, float* out_ml,
+                                         void* stream) {
+    using scout_host::set_error;
+    if (!e || !e->tier_mode || e->cw_on || !q_true || !k_new || !v_new || !out_o || !out_ml ||
+        ((cpu_o == nullptr) != (cpu_ml == nullptr)) || layer < 0 || layer >= e->cfg.layers ||
+        (layer + 1 < e->cfg.layers && !q_pred_next)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_decode_layer: bad arguments (device tier engine, "
+                                              "q_pred of the next layer unless this is the last)");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (layer != e->lw_next || (layer > 0 && step != e->lw_step)) {
+        set_error(SCOUT_ERR_LOGIC, "scout_engine_decode_layer: expected layer %d of step %d, got layer %d of step %d",
+                  e->lw_next, layer > 0 ? e->lw_step : step, layer, step);
+        return SCOUT_ERR_LOGIC;
+    }
+    if (const int rc = e->issuer_status(); rc != SCOUT_OK) return rc;
+    auto st = static_cast<cudaStream_t>(stream);
+    const int L = e->cfg.layers;
+    int rc;
+    if (layer == 0) {
+        e->token += 1;
+        e->lw_step = step;
+        const int par = e->token & 1;
+        // the previous step's bookkeeping, and the K2 that read this parity's lists
+        if (e->post_recorded) CU(cudaStreamWaitEvent(e->k1s, e->ev_post, 0));
+        if (e->k2_recorded[par]) CU(cudaStreamWaitEvent(e->k1s, e->ev_k2[par], 0));
+        if (e->planned_step != step) {
+            ++e->launches;
+            if ((rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(e->tier_dev.p), L, e->U,
+                                             e->cfg.nb_stride, e->cfg.n_tokens, step, e->I(e->plan_tab), e->k1s)) !=
+                SCOUT_OK)
+                return rc;
+        }
+        if ((rc = e->post_begin(step, par, e->token, k_new, v_new)) != SCOUT_OK) return rc;
+    }
+    const unsigned token = e->token;
+    const int par = token & 1;
+    // this call's inputs exist on the caller's stream from here on
+    CU(cudaEventRecord(e->ev_tmp, st));
+    CU(cudaStreamWaitEvent(e->k1s, e->ev_tmp, 0));
+    // begin_layer(step, layer): the layer's due tickets, after K1's marks of it (one call back)
+    if (e->pending[layer] >= 0 && e->pending[layer] <= e->tick(step, layer)) {
+        TierApplyArgs ap{};
+        ap.layers = static_cast<const scout_tier_layer*>(e->tier_dev.p);
+        ap.nbs = e->cfg.nb_stride;
+        ap.n_tokens = e->cfg.n_tokens;
+        ap.layer[0] = layer;
+        ap.due_tick[0] = e->tick(step, layer);
+        ap.n = 1;
+        e->pending[layer] = -1;
+        ++e->launches;
+        if ((rc = scout_tier_apply_layers(ap, e->U, e->k1s)) != SCOUT_OK) return rc;
+    }
+    // K1: layer 0 selects itself (true query), then layer + 1 (predicted query)
+    if (layer == 0) {
+        if ((rc = e->select_batch(0, 1, q_true, nullptr, step, par, e->k1s)) != SCOUT_OK) return rc;
+        CU(cudaEventRecord(e->ev_k1[0], e->k1s));
+    }
+    CU(cudaEventRecord(e->ev_pre, e->k1s));  // this layer's tier state is final until its post
+    if (layer + 1 < L) {
+        std::vector<scout_topk_args> v{e->k1_args(layer + 1, q_pred_next, step, par)};
+        ++e->launches;
+        if ((rc = scout_k1_launch_batch(v.data(), 1, e->k1s)) != SCOUT_OK) return rc;
+        CU(cudaEventRecord(e->ev_k1[layer + 1], e->k1s));
+    }
+    // K2 + K3 for this layer, once its lists exist
+    CU(cudaStreamWaitEvent(st, e->ev_k1[layer], 0));
+    const void* q[1] = {q_true};
+    const void* co[1] = {cpu_o};
+    const float* cml[1] = {cpu_ml};
+    float* o[1] = {out_o};
+    float* ml[1] = {out_ml};
+    if ((rc = e->launch_k2(par, q, co, cml, o, ml, nullptr, false, st, layer, 1)) != SCOUT_OK) return rc;
+    // post-attention bookkeeping of this layer (append with this call's K/V row)
+    const size_t row = static_cast<size_t>(layer) * e->U * SCOUT_HEAD_DIM;
+    e->pa_step.k_new = k_new - row;  // the post kernel indexes [layer][unit][128]
+    e->pa_step.v_new = v_new - row;
+    CU(cudaStreamWaitEvent(e->post_s, e->ev_pre, 0));
+    if ((rc = e->post_chunk(step, token, layer, layer, 1)) != SCOUT_OK) return rc;
+    e->lw_next = layer + 1 == L ? 0 : layer + 1;
+    if (layer + 1 == L) return e->post_end(step, st);
     return SCOUT_OK;
 }
 

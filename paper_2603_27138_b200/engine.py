@@ -140,6 +140,15 @@ class DecodeEngine:
                                                       _p(h_cpu_ml), _p(h_out_o), _p(h_out_ml), _p(h_cpu_ids),
                                                       _p(h_n_cpu), self._stream()))
 
+    def decode_layer(self, step, layer, q_true, q_pred_next, cpu_o, cpu_ml, k_new, v_new, out_o, out_ml):
+        """Layer-by-layer device tier mode: one layer of a step (layers 0..L-1 in
+        order); q_true [U*G][128] of this layer, q_pred_next of the next (None
+        for the last layer), k_new / v_new [U][128] f32; outputs [U*G][128] / [U*G][2]."""
+        self._check(q_true, q_pred_next, cpu_o, cpu_ml)
+        A.check(A.lib().scout_engine_decode_layer(self._h, int(step), int(layer), _p(q_true), _p(q_pred_next),
+                                                  _p(cpu_o), _p(cpu_ml), _p(k_new), _p(v_new), _p(out_o), _p(out_ml),
+                                                  self._stream()))
+
     def tier_changed(self):
         """The tier state was changed outside the engine: plan the next step afresh."""
         A.check(A.lib().scout_engine_tier_changed(self._h))

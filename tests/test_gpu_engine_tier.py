@@ -240,3 +240,48 @@ def test_engine_tier_back_to_back_steps_with_recalls(cuda):
     assert int(sd.tier.err.abs().sum()) == 0
     assert torch.isfinite(out_o).all()
     assert int(sd.n_tokens[0]) == T0 + 60
+
+
+@pytest.mark.parametrize("stagger", [False, True])
+def test_engine_layerwise_matches_fused_step(cuda, stagger):
+    """scout_engine_decode_layer (one call per layer, inputs given layer by
+    layer) against scout_engine_decode_step_kv (all layers at once) on an
+    identical second cache: the same outputs bit for bit and the same tier
+    state after every step, with recalls in both cadences."""
+    L, batch, hkv, G, k, cap, nbs, steps = 4, 2, 2, 4, 6, 8, 24, 40
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 11 + 50
+    torch.manual_seed(7)
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    sides = [Side(L, U, nbs, cap, kv, seed_rows) for _ in range(2)]
+    engs = []
+    for sd in sides:
+        layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+        engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
+                                 kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=0,
+                                 recall_intervals=[2, 3, 2, 1], recall_stagger=stagger, host_tier=sd.host,
+                                 tier=sd.tier, q_dtype=torch.bfloat16))
+    out = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
+    lw = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
+    for step in range(1, steps + 1):
+        qt = torch.randn(L, U * G, D, device="cuda").bfloat16()
+        qp = (qt.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).bfloat16()
+        co = torch.randn(L, U * G, D, device="cuda")
+        cm = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
+        kn, vn = torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")
+        engs[0].decode_step_kv(step, qt, qp, co, cm, kn, vn, *out)
+        for i in range(L):
+            engs[1].decode_layer(step, i, qt[i], qp[i + 1] if i + 1 < L else None, co[i], cm[i], kn[i], vn[i],
+                                 lw[0][i], lw[1][i])
+        for e in engs:
+            e.sync()
+        torch.cuda.synchronize()
+        assert torch.equal(out[0], lw[0]) and torch.equal(out[1], lw[1]), step
+        for name in ("tier", "last_sel", "table", "ready"):
+            assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
+        assert torch.equal(sides[0].n_tokens, sides[1].n_tokens)
+    for e in engs:
+        e.check_state()
+    with pytest.raises(RuntimeError):  # layers out of order
+        engs[1].decode_layer(steps + 1, 2, qt[2], qp[3], None, None, kn[2], vn[2], lw[0][2], lw[1][2])
