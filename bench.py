@@ -66,6 +66,14 @@ CONFIGS = {
     # configs[4]: batch 64 on 8 GPUs = 8 per GPU, 128K, top-128
     "qwen3-32b-128k": dict(layers=64, hq=64, hkv=8, batch=8, ctx=131072, k=128, capacity=128, headroom=16,
                            recall=16, cpu_frac=0.082),
+    # configs[3] at ONE GPU (batch 128): only the kernel view fits 180 GB (--tier static; the resident
+    # share = k - round(8.2% k) = 59 blocks per unit, 5 recall slots): 171 GB of pool + digests
+    "qwen3-32b-32k-b128": dict(layers=64, hq=64, hkv=8, batch=128, ctx=32768, k=64, capacity=59, headroom=5,
+                               recall=16, cpu_frac=0.082, static_only=True),
+    # configs[0]: 1 request, 1 layer, 32 Q / 8 KV heads, 4K context, top-32, fp32 KV: the C-ABI path
+    # (scout_score_topk_split + scout_sparse_decode with a CPU partial merged), no engine
+    "toy-4k-f32": dict(layers=1, hq=32, hkv=8, batch=1, ctx=4096, k=32, capacity=64, headroom=0,
+                       recall=0, cpu_frac=0.082, kv="f32"),
 }
 
 
@@ -759,13 +767,17 @@ def main():
         run_reference(args, cfg, ws, rank)
         barrier(ws)
         return
+    if cfg.get("kv") == "f32":
+        run_c_abi_f32(args, cfg, ws, rank, gb)
+        barrier(ws)
+        return
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     from paper_2603_27138_b200 import lib, ops
 
     lib()  # native library must be present: no fallback
     t0 = time.time()
-    tier_mode = args.tier == "device"
+    tier_mode = args.tier == "device" and not cfg.get("static_only")
     args.max_steps = args.warmup + 3 * args.steps + 2 * args.e2e_steps + 48
     if tier_mode:
         wl = TierWorkload(cfg, dev, seed=args.seed, max_steps=args.max_steps,
@@ -952,6 +964,95 @@ def main():
         }
         print(json.dumps(line), flush=True)
     barrier(ws)
+
+
+def run_c_abi_f32(args, cfg, ws, rank, gb):
+    """BASELINE configs[0] (fp32 KV, one layer, 1 request): the C ABI directly,
+    as a reference caller would bind it -- per step one scout_score_topk_split
+    (stacked select_topk + split against the residency table) and one
+    scout_sparse_decode (f32 CUDA-core path, merged with a CPU partial). The
+    tier holds all but round(8.2% k) selected blocks. e2e: the query and CPU
+    partial H2D and the output D2H around the two calls."""
+    from paper_2603_27138_b200 import ops
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    ops.slot_bytes(torch.float32)  # the native library must be present: no fallback
+    hq, hkv, k = cfg["hq"], cfg["hkv"], cfg["k"]
+    G, U = hq // hkv, cfg["batch"] * hkv
+    nb = cfg["ctx"] // BS
+    g = torch.Generator(device=dev).manual_seed(args.seed + rank)
+    pool = ops.alloc_pool(U * nb, torch.float32, dev)
+    pool.view(torch.float32).normal_(generator=g)
+    dig = torch.randn(U, 2, D, nb, generator=g, device=dev)
+    dig = torch.stack([dig.min(dim=1).values, dig.max(dim=1).values], dim=1).contiguous()
+    n_tokens = torch.full((U,), cfg["ctx"], dtype=torch.int32, device=dev)
+    q = torch.randn(U * G, D, generator=g, device=dev)
+    r0 = ops.score_topk_split(q, dig, n_tokens, k, G)
+    ncpu = int(round(cfg["cpu_frac"] * k))
+    table = (torch.arange(U, device=dev, dtype=torch.int32)[:, None] * nb + torch.arange(nb, device=dev, dtype=torch.int32)[None]).contiguous()
+    drop = torch.rand(U, k, generator=g, device=dev).argsort(dim=1)[:, :ncpu]
+    table.scatter_(1, torch.gather(r0["sel_ids"].long(), 1, drop), -1)
+    cpu_o = torch.randn(U * G, D, generator=g, device=dev)
+    cpu_ml = torch.stack([torch.randn(U * G, generator=g, device=dev), torch.rand(U * G, generator=g, device=dev) + 1],
+                         -1).contiguous()
+    bufs, ws_ = {}, ops.DecodeWorkspace(U, G, dev)
+    o = torch.empty(U * G, D, device=dev)
+    ml = torch.empty(U * G, 2, device=dev)
+
+    def step(qq, co, cm):
+        r = ops.score_topk_split(qq, dig, n_tokens, k, G, block_table=table, out=bufs)
+        ops.sparse_decode(qq, pool, torch.float32, r["res_slots"], r["res_ids"], r["n_res"], n_tokens, G, cpu_o=co,
+                          cpu_ml=cm, o=o, ml=ml, workspace=ws_)
+
+    for _ in range(args.warmup):
+        step(q, cpu_o, cpu_ml)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = timed(lambda i: step(q, cpu_o, cpu_ml), args.steps, dev, ws)
+    clk = clocks.stop()
+    res_tok = int(bufs["res_tokens"].sum())
+    nbytes = res_tok * 2 * D * 4 + U * 2 * D * nb * 4 + U * G * (D * 4 * 2 + 8 + (D + 2) * 4)
+    # e2e: pinned host query + CPU partial in, output out, every step
+    hq_, hco, hcm = q.cpu().pin_memory(), cpu_o.cpu().pin_memory(), cpu_ml.cpu().pin_memory()
+    ho, hml = torch.empty(o.shape).pin_memory(), torch.empty(ml.shape).pin_memory()
+    dq, dco, dcm = torch.empty_like(q), torch.empty_like(cpu_o), torch.empty_like(cpu_ml)
+
+    def e2e_step(i):
+        dq.copy_(hq_, non_blocking=True)
+        dco.copy_(hco, non_blocking=True)
+        dcm.copy_(hcm, non_blocking=True)
+        step(dq, dco, dcm)
+        ho.copy_(o, non_blocking=True)
+        hml.copy_(ml, non_blocking=True)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    ms_e2e = timed(e2e_step, args.steps, dev, ws)
+    peaks = {}
+    try:
+        peaks = json.load(open(ROOT / "MEASURED_PEAKS.json"))
+    except OSError:
+        pass
+    peak = peaks.get("hbm_gbs", 6650.0)
+    if rank == 0:
+        line = {"metric": METRIC, "value": gb / (ms / 1000.0), "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init f32 KV, digests, query)",
+                "config": {"workload": args.config, "batch_per_gpu": cfg["batch"], "context": cfg["ctx"], "layers": 1,
+                           "heads": f"{hq}q/{hkv}kv", "head_dim": D, "block": BS, "top_k": k,
+                           "cpu_blocks_per_unit": ncpu, "kv_dtype": "f32",
+                           "path": "C ABI scout_score_topk_split + scout_sparse_decode (f32 CUDA-core K2) per step",
+                           "l2": "working set %.1f MiB: fits L2 (a latency-bound config)" % (nbytes / 2**20)},
+                "roofline": {"bound": "latency (one request, one layer: 8 units)", "achieved": nbytes / ms / 1e6,
+                             "peak": peak, "unit": "GB/s", "frac": nbytes / ms / 1e6 / peak,
+                             "traffic": None, "kernel": "K1 + K2 (f32), step bytes / step time"},
+                "clocks": clk, "gpu_launches": 3 * args.steps,
+                "e2e": {"value": gb / (ms_e2e / 1000.0), "unit": "tokens/s", "ms_per_step": ms_e2e,
+                        "h2d_bytes_per_step": int(hq_.numel() * 4 + hco.numel() * 4 + hcm.numel() * 4),
+                        "d2h_bytes_per_step": int(ho.numel() * 4 + hml.numel() * 4)}}
+        print(json.dumps(line), flush=True)
 
 
 def run_layerwise(wl, steps, dev, ws, step0):
