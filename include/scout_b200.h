@@ -418,7 +418,21 @@ typedef struct scout_engine_config {
      * the partials. */
     int cpu_worker;
     int cpu_threads;
+    /* GpuSidePolicy (engine.hpp:25-29): SCOUT_GPU_SIDE_PREDICTED (0, the
+     * default) attends to K1's predicted-and-resident share of each layer;
+     * SCOUT_GPU_SIDE_ALL_RESIDENT (1) to the layer's whole fast tier at
+     * attention time (residency_set after begin_layer, engine.hpp:253-256;
+     * the CPU share is unchanged and check_split is not applied, as in the
+     * reference). */
+    int gpu_side_policy;
+    /* layer-by-layer mode (scout_engine_decode_layer): K2 CTAs of a
+     * single-layer launch; the SMs it leaves free run K1 of the next layer
+     * beside it. 0: automatic (the grid less 28), < 0: the whole grid. */
+    int layer_ctas;
 } scout_engine_config;
+
+#define SCOUT_GPU_SIDE_PREDICTED 0
+#define SCOUT_GPU_SIDE_ALL_RESIDENT 1
 
 typedef struct scout_engine scout_engine;
 

@@ -39,7 +39,7 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
     OBJ.mkdir(exist_ok=True)
     srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
     hdrs = _headers()
-    objs = []
+    objs, cmds = [], []
     for src in srcs:
         obj = OBJ / (src.name + ".o")
         objs.append(obj)
@@ -50,7 +50,13 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
                        "-c", str(src), "-o", str(obj)]
             if verbose:
                 print(" ".join(cmd))
-            subprocess.run(cmd, check=True)
+            cmds.append(cmd)
+    # one compiler process per stale source, all at once (the kernels are
+    # independent translation units)
+    procs = [subprocess.Popen(cmd) for cmd in cmds]
+    failed = [" ".join(c) for c, p in zip(cmds, procs) if p.wait() != 0]
+    if failed:
+        raise subprocess.CalledProcessError(1, failed[0])
     if force or _stale(LIB, objs):
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB), *map(str, objs), "-cudart", "static", "-Xcompiler", "-pthread"]
         if verbose:

@@ -19,6 +19,7 @@ SCOUT_ERR_CUDA = 3
 SCOUT_ERR_UNSUPPORTED = 4
 
 SCOUT_F32, SCOUT_BF16, SCOUT_F64 = 0, 1, 2
+SCOUT_GPU_SIDE_PREDICTED, SCOUT_GPU_SIDE_ALL_RESIDENT = 0, 1
 SCOUT_DIGEST_MINMAX, SCOUT_DIGEST_MEAN = 0, 1
 HEAD_DIM = 128
 BLOCK_SIZE = 64
@@ -86,6 +87,7 @@ class EngineConfig(C.Structure):
         ("q_dtype", C.c_int),
         ("tier", _vp), ("host_blocks", C.c_longlong), ("cpu_dtype", C.c_int),
         ("recall_intervals", _vp), ("recall_stagger", C.c_int), ("cpu_worker", C.c_int), ("cpu_threads", C.c_int),
+        ("gpu_side_policy", C.c_int), ("layer_ctas", C.c_int),
     ]
 
 

@@ -109,6 +109,25 @@ struct scout_engine {
     int U = 0, G = 0, UG = 0, grid = 0, nch = 0;
     // per-layer K1 outputs, two sets (step parity)
     Buf sel_ids[2], n_sel[2], res_slots[2], res_ids[2], n_res[2], cpu_ids[2], n_cpu[2], res_tok[2], cpu_tok[2];
+    // GpuSidePolicy::all_resident: every layer's whole fast tier at attention
+    // time, [L][U][nb_stride] (K2 reads these instead of K1's resident share)
+    bool all_res = false;
+    Buf ar_ids[2], ar_slots[2], ar_n[2];
+    int resident_lists(int par, int l0, int n, cudaStream_t s) {
+        ResidentListArgs a{};
+        a.layers = tier_mode ? static_cast<const scout_tier_layer*>(tier_dev.p) : nullptr;
+        if (!tier_mode)
+            for (int i = 0; i < n; ++i) a.tables[l0 + i] = layers[l0 + i].block_table;
+        a.nbs = cfg.nb_stride;
+        a.layer0 = l0;
+        a.stride = cfg.nb_stride;
+        a.n_tokens = cfg.n_tokens;
+        a.ids = I(ar_ids[par]);
+        a.slots = I(ar_slots[par]);
+        a.n = I(ar_n[par]);
+        ++launches;
+        return scout_tier_resident_lists(a, U, n, s);
+    }
     Buf ws;  // per-layer K2 workspaces
     size_t ws_layer = 0;
     Buf flags;  // k1_flag[L] | k1_ctr[L] | recall_flag[L] | layer_done[L] | in_flag[nch]
@@ -212,6 +231,23 @@ struct scout_engine {
     // layer-by-layer mode (scout_engine_decode_layer): the layer expected next
     // and the step in progress
     int lw_next = 0, lw_step = -1;
+    // SCOUT_LW_HOSTPROF=1: host time of decode_layer by section, printed at destroy
+    double lw_host[6] = {0, 0, 0, 0, 0, 0};
+    long long lw_calls = 0;
+    // K2 CTAs of a single-layer launch (cfg.layer_ctas; SCOUT_LW_K2_CTAS
+    // overrides): 0 = automatic, the grid less LW_FREE_SMS for K1 of the next
+    // layer (measured: 148 CTAs 13.9 ms per 64-layer step, 120 12.3 ms)
+    static constexpr int LW_FREE_SMS = 28;
+    int layer_ctas() const {
+        static const int env = [] {
+            const char* s = getenv("SCOUT_LW_K2_CTAS");
+            return s ? atoi(s) : 0;
+        }();
+        const int v = env != 0 ? env : cfg.layer_ctas;
+        if (v < 0) return 0;
+        if (v > 0) return v;
+        return grid > 2 * LW_FREE_SMS ? grid - LW_FREE_SMS : 0;
+    }
 
     // instrumentation
     bool timing = false;
@@ -244,6 +280,12 @@ struct scout_engine {
     }
 
     ~scout_engine() {
+        if (lw_calls > 0 && getenv("SCOUT_LW_HOSTPROF"))
+            fprintf(stderr,
+                    "[lw host] %lld calls, us per call: step start %.1f, apply %.1f, K2 launch %.1f, K1 launch %.1f, "
+                    "post %.1f, total %.1f\n",
+                    lw_calls, lw_host[0] / lw_calls, lw_host[1] / lw_calls, lw_host[2] / lw_calls,
+                    lw_host[3] / lw_calls, lw_host[4] / lw_calls, lw_host[5] / lw_calls);
         stop_worker();
         stop_recalls();
         if (cw_pinned) cudaFreeHost(cw_pinned);
@@ -327,12 +369,12 @@ struct scout_engine {
     // layer in the layer-by-layer mode
     int launch_k2(int par, const void* const* q, const void* const* co, const float* const* cml, float* const* o,
                   float* const* ml, const unsigned* const* inflag, bool poll_k1, cudaStream_t st, int l0 = 0,
-                  int n = -1) {
+                  int n = -1, int ctas = 0) {
         if (n < 0) n = cfg.layers;
         K2StepArgs a{};
         a.n_units = U;
         a.group = G;
-        a.k_stride = cfg.k;
+        a.k_stride = all_res ? cfg.nb_stride : cfg.k;
         a.n_layers = n;
         a.scale = cfg.scale;
         a.kv_pool = cfg.kv_pool;
@@ -344,6 +386,10 @@ struct scout_engine {
         a.layer_done = layer_done + l0;
         a.token = token;
         a.max_ctas = cfg.max_ctas;
+        if (ctas > 0 && ctas < grid) {  // a narrower launch (layer-by-layer mode) still counts `grid` per layer
+            a.max_ctas = ctas;
+            a.done_extra = static_cast<unsigned>(grid - ctas);
+        }
         a.q_bf16 = cfg.q_dtype == SCOUT_BF16;
         a.cpu_bf16 = cfg.cpu_dtype == SCOUT_BF16;
         a.prof = k2_prof;
@@ -354,8 +400,11 @@ struct scout_engine {
         a.l2_prefetch = l2pf;
         for (int j = 0; j < n; ++j) {
             const int i = l0 + j;
-            a.layers[j] = K2Layer{q[j], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
-                                  co[j], cml[j], o[j], ml[j], inflag ? inflag[j] : nullptr, rc_token[i], 0u};
+            const size_t lr = static_cast<size_t>(i) * U * cfg.nb_stride;
+            a.layers[j] = all_res ? K2Layer{q[j], I(ar_slots[par]) + lr, I(ar_ids[par]) + lr, I(ar_n[par]) + lu(i),
+                                            co[j], cml[j], o[j], ml[j], inflag ? inflag[j] : nullptr, rc_token[i], 0u}
+                                  : K2Layer{q[j], I(res_slots[par]) + lk(i), I(res_ids[par]) + lk(i), I(n_res[par]) + lu(i),
+                                            co[j], cml[j], o[j], ml[j], inflag ? inflag[j] : nullptr, rc_token[i], 0u};
         }
         if (cfg.recall_mode == 1 && (cfg.recall_interval > 0 || cfg.recall_intervals)) {
             // SM-gather recalls need SMs: a persistent K2 that polls their flags
@@ -684,6 +733,8 @@ struct scout_engine {
             ++launches;
             if ((rc = scout_tier_apply_layers(ap, U, s)) != SCOUT_OK) return rc;
         }
+        // all_resident: the fast tier after begin_layer's tickets
+        if (all_res && (rc = resident_lists(par, 0, L, s)) != SCOUT_OK) return rc;
         return SCOUT_OK;
     }
     // 5. as K2 finishes each chunk of layers (layer_done flags), one launch per
@@ -731,7 +782,7 @@ struct scout_engine {
         pa.rc_ids = I(tier_rc_ids);
         pa.rc_n = I(tier_rc_n);
         pa.dst = I(tier_dst);
-        pa.res_ids = I(res_ids[par]);
+        pa.res_ids = all_res ? nullptr : I(res_ids[par]);  // check_split only for the predicted policy
         pa.n_res = I(n_res[par]);
         pa.cpu_ids = I(cpu_ids[par]);
         pa.n_cpu = I(n_cpu[par]);
@@ -879,6 +930,10 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: GQA group %d not in {1,2,4,8}", G);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
+    if (c.gpu_side_policy != SCOUT_GPU_SIDE_PREDICTED && c.gpu_side_policy != SCOUT_GPU_SIDE_ALL_RESIDENT) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: gpu_side_policy %d unknown", c.gpu_side_policy);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
     if (c.recall_intervals)
         for (int l = 0; l < c.layers; ++l)
             if (c.recall_intervals[l] < 1) {  // engine.hpp:177-178
@@ -917,6 +972,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     e->G = c.hq / c.hkv;
     e->UG = e->U * e->G;
     e->grid = scout_k2_grid(e->U, c.k, c.max_ctas);
+    e->all_res = c.gpu_side_policy == SCOUT_GPU_SIDE_ALL_RESIDENT;
     if (const char* pe = getenv("SCOUT_K2_PROF"); pe && atoi(pe) != 0) {
         // diagnostics: K2 cycle accounting, summed over every launch, printed at destroy
         CU(cudaMalloc(&e->k2_prof, static_cast<size_t>(e->grid) * 16 * sizeof(unsigned long long)));
@@ -929,6 +985,10 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         bad |= e->sel_ids[p].alloc(lk) | e->res_slots[p].alloc(lk) | e->res_ids[p].alloc(lk) |
                e->cpu_ids[p].alloc(lk) | e->n_sel[p].alloc(lu) | e->n_res[p].alloc(lu) | e->n_cpu[p].alloc(lu) |
                e->res_tok[p].alloc(lu) | e->cpu_tok[p].alloc(lu);
+    if (e->all_res) {
+        const size_t lr = static_cast<size_t>(c.layers) * e->U * c.nb_stride * 4;
+        for (int p = 0; p < 2; ++p) bad |= e->ar_ids[p].alloc(lr) | e->ar_slots[p].alloc(lr) | e->ar_n[p].alloc(lu);
+    }
     e->ws_layer = scout_k2_ws_layer_bytes(e->U, e->grid);
     bad |= e->ws.alloc(e->ws_layer * c.layers);
     const size_t nflags = 4 * static_cast<size_t>(c.layers) + e->nch;
@@ -1105,6 +1165,7 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q
     // K1 for every layer in one wide launch (bandwidth-bound, the whole GPU),
     // then the persistent K2 over all layers; stream order is the dependency
     int rc = e->select_batch(0, L, q_true, q_pred, step, par, st);
+    if (rc == SCOUT_OK && e->all_res) rc = e->resident_lists(par, 0, L, st);
     if (rc != SCOUT_OK) return rc;
     std::vector<const void*> q(L);
     std::vector<const void*> co(L);
@@ -1231,6 +1292,7 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
         if (rc == SCOUT_OK && cudaEventRecord(e->ev_pre, e->k1s) != cudaSuccess) rc = SCOUT_ERR_CUDA;
     } else {
         rc = e->select_batch(0, L, g.qt, g.qp, step, par, e->k1s);
+        if (rc == SCOUT_OK && e->all_res) rc = e->resident_lists(par, 0, L, e->k1s);
     }
     if (rc != SCOUT_OK) return rc;
     const size_t id_bytes = static_cast<size_t>(L) * e->U * e->cfg.k * 4, n_bytes = static_cast<size_t>(L) * e->U * 4;
@@ -1390,6 +1452,15 @@ extern "C" int scout_engine_decode_layer(scout_engine* e, int step, int layer, c
     auto st = static_cast<cudaStream_t>(stream);
     const int L = e->cfg.layers;
     int rc;
+    static const bool hprof = getenv("SCOUT_LW_HOSTPROF") != nullptr;
+    using hclock = std::chrono::steady_clock;
+    hclock::time_point ht[6];
+    if (hprof) ht[0] = hclock::now();
+    auto hmark = [&](int i) {
+        if (!hprof) return;
+        ht[i] = hclock::now();
+        e->lw_host[i - 1] += std::chrono::duration<double, std::micro>(ht[i] - ht[i - 1]).count();
+    };
     if (layer == 0) {
         e->token += 1;
         e->lw_step = step;
@@ -1411,6 +1482,7 @@ extern "C" int scout_engine_decode_layer(scout_engine* e, int step, int layer, c
     // this call's inputs exist on the caller's stream from here on
     CU(cudaEventRecord(e->ev_tmp, st));
     CU(cudaStreamWaitEvent(e->k1s, e->ev_tmp, 0));
+    hmark(1);
     // begin_layer(step, layer): the layer's due tickets, after K1's marks of it (one call back)
     if (e->pending[layer] >= 0 && e->pending[layer] <= e->tick(step, layer)) {
         TierApplyArgs ap{};
@@ -1429,27 +1501,41 @@ extern "C" int scout_engine_decode_layer(scout_engine* e, int step, int layer, c
         if ((rc = e->select_batch(0, 1, q_true, nullptr, step, par, e->k1s)) != SCOUT_OK) return rc;
         CU(cudaEventRecord(e->ev_k1[0], e->k1s));
     }
+    if (e->all_res && (rc = e->resident_lists(par, layer, 1, e->k1s)) != SCOUT_OK) return rc;
     CU(cudaEventRecord(e->ev_pre, e->k1s));  // this layer's tier state is final until its post
+    hmark(2);
+    // K2 + K3 for this layer, once its lists exist. Queued before K1 of the
+    // next layer: K2's persistent CTAs (one per SM, most of its shared memory)
+    // take their SMs first, and K1(i+1) runs beside them on the SMs K2 leaves
+    // free (cfg.layer_ctas) instead of holding SMs K2 then waits for
+    CU(cudaStreamWaitEvent(st, e->ev_k1[layer], 0));
+    if (e->all_res) CU(cudaStreamWaitEvent(st, e->ev_pre, 0));  // the layer's fast tier after its tickets
+    const void* q[1] = {q_true};
+    const void* co[1] = {cpu_o};
+    const float* cml[1] = {cpu_ml};
+    float* o[1] = {out_o};
+    float* ml[1] = {out_ml};
+    if ((rc = e->launch_k2(par, q, co, cml, o, ml, nullptr, false, st, layer, 1, e->layer_ctas())) != SCOUT_OK)
+        return rc;
+    hmark(3);
     if (layer + 1 < L) {
         std::vector<scout_topk_args> v{e->k1_args(layer + 1, q_pred_next, step, par)};
         ++e->launches;
         if ((rc = scout_k1_launch_batch(v.data(), 1, e->k1s)) != SCOUT_OK) return rc;
         CU(cudaEventRecord(e->ev_k1[layer + 1], e->k1s));
     }
-    // K2 + K3 for this layer, once its lists exist
-    CU(cudaStreamWaitEvent(st, e->ev_k1[layer], 0));
-    const void* q[1] = {q_true};
-    const void* co[1] = {cpu_o};
-    const float* cml[1] = {cpu_ml};
-    float* o[1] = {out_o};
-    float* ml[1] = {out_ml};
-    if ((rc = e->launch_k2(par, q, co, cml, o, ml, nullptr, false, st, layer, 1)) != SCOUT_OK) return rc;
+    hmark(4);
     // post-attention bookkeeping of this layer (append with this call's K/V row)
     const size_t row = static_cast<size_t>(layer) * e->U * SCOUT_HEAD_DIM;
     e->pa_step.k_new = k_new - row;  // the post kernel indexes [layer][unit][128]
     e->pa_step.v_new = v_new - row;
     CU(cudaStreamWaitEvent(e->post_s, e->ev_pre, 0));
     if ((rc = e->post_chunk(step, token, layer, layer, 1)) != SCOUT_OK) return rc;
+    hmark(5);
+    if (hprof) {
+        e->lw_host[5] += std::chrono::duration<double, std::micro>(ht[5] - ht[0]).count();
+        ++e->lw_calls;
+    }
     e->lw_next = layer + 1 == L ? 0 : layer + 1;
     if (layer + 1 == L) return e->post_end(step, st);
     return SCOUT_OK;

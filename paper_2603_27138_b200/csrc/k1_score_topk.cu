@@ -350,18 +350,23 @@ __device__ __forceinline__ void fast_quad(const DigT* blo, const DigT* bhi, int 
 #define SCOUT_K1_DMINB1 8  // ... and the QPT=1 variant (64 registers)
 #endif
 constexpr int DCB = SCOUT_K1_DCB;
+// single-layer launches (few CTAs beside a running K2, each unit's digests
+// latency-bound): batches of 8 channels, twice the loads in flight
+constexpr int DCB_SINGLE = 8;
+template <int B>
 __device__ __forceinline__ void ld_quad4(const __nv_bfloat16* lo, const __nv_bfloat16* hi, size_t ns, int b0, int c0,
-                                         uint2 (&L)[DCB], uint2 (&H)[DCB]) {
+                                         uint2 (&L)[B], uint2 (&H)[B]) {
 #pragma unroll
-    for (int i = 0; i < DCB; ++i) {
+    for (int i = 0; i < B; ++i) {
         L[i] = __ldcs(reinterpret_cast<const uint2*>(lo + static_cast<size_t>(c0 + i) * ns + b0));
         H[i] = __ldcs(reinterpret_cast<const uint2*>(hi + static_cast<size_t>(c0 + i) * ns + b0));
     }
 }
-__device__ __forceinline__ void sum_quad4(const uint2 (&L)[DCB], const uint2 (&H)[DCB], const float2* pn, int c0,
+template <int B>
+__device__ __forceinline__ void sum_quad4(const uint2 (&L)[B], const uint2 (&H)[B], const float2* pn, int c0,
                                           float (&t)[4], float (&a)[4]) {
 #pragma unroll
-    for (int i = 0; i < DCB; ++i) {
+    for (int i = 0; i < B; ++i) {
         float l[4], h[4];
         l[0] = __uint_as_float(L[i].x << 16); l[1] = __uint_as_float(L[i].x & 0xFFFF0000u);
         l[2] = __uint_as_float(L[i].y << 16); l[3] = __uint_as_float(L[i].y & 0xFFFF0000u);
@@ -375,24 +380,25 @@ __device__ __forceinline__ void sum_quad4(const uint2 (&L)[DCB], const uint2 (&H
         }
     }
 }
-// channels [cb, ce) (multiples of 2 * DCB)
+// channels [cb, ce) (multiples of 2 * B)
+template <int B>
 __device__ __forceinline__ void fast_quad_direct(const __nv_bfloat16* lo, const __nv_bfloat16* hi, size_t ns, int b0,
                                                  const float2* pn, double (&s)[4], float (&a)[4], int cb = 0,
                                                  int ce = D) {
-    static_assert(DCB == 4 || DCB == 8, "8-channel fp32 chains: batches of 4 (two per chain) or 8");
-    uint2 L0[DCB], H0[DCB], L1[DCB], H1[DCB];
-    ld_quad4(lo, hi, ns, b0, cb, L0, H0);
+    static_assert(B == 4 || B == 8, "8-channel fp32 chains: batches of 4 (two per chain) or 8");
+    uint2 L0[B], H0[B], L1[B], H1[B];
+    ld_quad4<B>(lo, hi, ns, b0, cb, L0, H0);
 #pragma unroll 1
-    for (int c0 = cb; c0 < ce; c0 += 2 * DCB) {
+    for (int c0 = cb; c0 < ce; c0 += 2 * B) {
         float t[4] = {0.f, 0.f, 0.f, 0.f};
-        ld_quad4(lo, hi, ns, b0, c0 + DCB, L1, H1);
-        sum_quad4(L0, H0, pn, c0, t, a);
-        if (DCB == 8) {  // one chain per batch
+        ld_quad4<B>(lo, hi, ns, b0, c0 + B, L1, H1);
+        sum_quad4<B>(L0, H0, pn, c0, t, a);
+        if (B == 8) {  // one chain per batch
 #pragma unroll
             for (int e = 0; e < 4; ++e) { s[e] += static_cast<double>(t[e]); t[e] = 0.f; }
         }
-        if (c0 + 2 * DCB < ce) ld_quad4(lo, hi, ns, b0, c0 + 2 * DCB, L0, H0);
-        sum_quad4(L1, H1, pn, c0 + DCB, t, a);
+        if (c0 + 2 * B < ce) ld_quad4<B>(lo, hi, ns, b0, c0 + 2 * B, L0, H0);
+        sum_quad4<B>(L1, H1, pn, c0 + B, t, a);
 #pragma unroll
         for (int e = 0; e < 4; ++e) s[e] += static_cast<double>(t[e]);
     }
@@ -400,10 +406,11 @@ __device__ __forceinline__ void fast_quad_direct(const __nv_bfloat16* lo, const 
 
 // QPT: block quads per thread whose running scores live in registers (1: up
 // to 512 blocks, 2: up to 1024, 4: up to 2048); 0: shared-memory accumulators.
-template <typename DigT, int G, int MODE, int QPT, bool DIRECT = false>
-__global__ void __launch_bounds__(K1_THREADS, DIRECT ? (QPT == 1 ? SCOUT_K1_DMINB1 : (QPT == 2 ? SCOUT_K1_DMINB : 4))
+template <typename DigT, int G, int MODE, int QPT, bool DIRECT = false, int NA = K1_MAX_LAYERS>
+__global__ void __launch_bounds__(K1_THREADS, DIRECT ? (NA == 1 ? 4 : (QPT == 1 ? SCOUT_K1_DMINB1 : (QPT == 2 ? SCOUT_K1_DMINB : 4)))
                                                       : ((QPT == 1 || QPT == 2) ? 7 : SCOUT_K1_MINB))
-    score_topk_kernel(const K1Batch batch) {
+    score_topk_kernel(const K1BatchT<NA> batch) {
+    constexpr int KB = NA == 1 ? DCB_SINGLE : DCB;  // channels per direct-load batch
     // Work items are (layer, unit) pairs, flattened layer-major. Classic grid
     // (units x layers): one item per CTA. Persistent grid (batch.persist): CTA
     // c takes items c, c + grid, ... and the digest ring keeps streaming across
@@ -551,7 +558,7 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (QPT == 1 ? SCOUT_K1_DMIN
                 // warp takes a quarter of the channels of every tail quad, and
                 // warp 0 adds the four partials (f64 sums of the same <= 8-channel
                 // fp32 chains: the error bound is unchanged).
-                if (tid < nq) fast_quad_direct(dlo, dhi, ns, 4 * tid, pn, rs[0], ra[0]);
+                if (tid < nq) fast_quad_direct<KB>(dlo, dhi, ns, 4 * tid, pn, rs[0], ra[0]);
                 double* ps = reinterpret_cast<double*>(stagebuf);        // [K1_WARPS][32][4]
                 float* pa = reinterpret_cast<float*>(ps + K1_WARPS * 128);  // [K1_WARPS][32][4]
                 const int w = tid >> 5, l = tid & 31;
@@ -559,7 +566,7 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (QPT == 1 ? SCOUT_K1_DMIN
                     double s4[4] = {0.0, 0.0, 0.0, 0.0};
                     float a4[4] = {0.f, 0.f, 0.f, 0.f};
                     const int cq = D / K1_WARPS;
-                    fast_quad_direct(dlo, dhi, ns, 4 * (K1_THREADS + l), pn, s4, a4, w * cq, (w + 1) * cq);
+                    fast_quad_direct<KB>(dlo, dhi, ns, 4 * (K1_THREADS + l), pn, s4, a4, w * cq, (w + 1) * cq);
 #pragma unroll
                     for (int e = 0; e < 4; ++e) { ps[(w * 32 + l) * 4 + e] = s4[e]; pa[(w * 32 + l) * 4 + e] = a4[e]; }
                 }
@@ -575,7 +582,7 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (QPT == 1 ? SCOUT_K1_DMIN
 #pragma unroll
                 for (int q = 0; q < RQ; ++q) {
                     const int j = tid + q * K1_THREADS;
-                    if (j < nq) fast_quad_direct(dlo, dhi, ns, 4 * j, pn, rs[q], ra[q]);
+                    if (j < nq) fast_quad_direct<KB>(dlo, dhi, ns, 4 * j, pn, rs[q], ra[q]);
                 }
             }
         }
@@ -768,8 +775,8 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (QPT == 1 ? SCOUT_K1_DMIN
     }
 }
 
-template <typename DigT, int MODE>
-int launch_g(K1Batch& b, cudaStream_t st) {
+template <typename DigT, int MODE, int NA>
+int launch_g(K1BatchT<NA>& b, cudaStream_t st) {
     const scout_topk_args& a = b.a[0];
     // digest ring depth (tuning knob SCOUT_K1_NBUF, 1..K1_MAXBUF)
     // and chunk bytes (SCOUT_K1_CHUNK, 4096..65536)
@@ -813,12 +820,15 @@ int launch_g(K1Batch& b, cudaStream_t st) {
         if (smem > 48 * 1024) scout_host::ensure_smem(reinterpret_cast<const void*>(kern), smem);
         // persistent grid: resident CTAs x SMs, when the items outnumber them
         const long long items = static_cast<long long>(a.n_units) * b.n;
-        int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K1_THREADS, smem);
-        int dev = 0, sms = 148;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const long long slots = static_cast<long long>(per_sm > 0 ? per_sm : 1) * sms;
+        long long slots = 0;
+        if (MODE == 0 && persist_env) {  // (occupancy queried only for the opt-in persistent grid)
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K1_THREADS, smem);
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            slots = static_cast<long long>(per_sm > 0 ? per_sm : 1) * sms;
+        }
         b.persist = MODE == 0 && persist_env && items > slots;
         const dim3 grid = b.persist ? dim3(static_cast<unsigned>(slots)) : dim3(a.n_units, b.n);
         scout_host::launch(kern, grid, dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
@@ -829,17 +839,17 @@ int launch_g(K1Batch& b, cudaStream_t st) {
         constexpr int Gv = decltype(g)::value;
         if constexpr (MODE == 0 && sizeof(DigT) == 2) {
             if (b.direct) {
-                if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1, true>);
-                else if (qpt == 2) go(score_topk_kernel<DigT, Gv, MODE, 2, true>);
-                else go(score_topk_kernel<DigT, Gv, MODE, 4, true>);
+                if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1, true, NA>);
+                else if (qpt == 2) go(score_topk_kernel<DigT, Gv, MODE, 2, true, NA>);
+                else go(score_topk_kernel<DigT, Gv, MODE, 4, true, NA>);
                 return;
             }
         }
-        if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1>);
+        if (qpt == 1) go(score_topk_kernel<DigT, Gv, MODE, 1, false, NA>);
         else if constexpr (MODE == 0) {
-            if (qpt == 2) go(score_topk_kernel<DigT, Gv, MODE, 2>);
-            else if (qpt == 4) go(score_topk_kernel<DigT, Gv, MODE, 4>);
-            else go(score_topk_kernel<DigT, Gv, MODE, 0>);
+            if (qpt == 2) go(score_topk_kernel<DigT, Gv, MODE, 2, false, NA>);
+            else if (qpt == 4) go(score_topk_kernel<DigT, Gv, MODE, 4, false, NA>);
+            else go(score_topk_kernel<DigT, Gv, MODE, 0, false, NA>);
         }
     };
     switch (a.group) {
@@ -888,7 +898,14 @@ int launch_batch(K1Batch& b, cudaStream_t st) {
     using namespace scout_host;
     const scout_topk_args& a = b.a[0];
     int rc = -1;
-    if (a.method == SCOUT_DIGEST_MINMAX) {
+    if (a.method == SCOUT_DIGEST_MINMAX && a.digest_dtype != SCOUT_F64 && b.n == 1) {
+        // single layer: the 1-slot parameter block
+        static thread_local K1Batch1 b1;
+        b1.n = 1;
+        b1.a[0] = a;
+        if (a.digest_dtype == SCOUT_BF16) rc = launch_g<__nv_bfloat16, 0>(b1, st);
+        else if (a.digest_dtype == SCOUT_F32) rc = launch_g<float, 0>(b1, st);
+    } else if (a.method == SCOUT_DIGEST_MINMAX) {
         if (a.digest_dtype == SCOUT_BF16) rc = launch_g<__nv_bfloat16, 0>(b, st);
         else if (a.digest_dtype == SCOUT_F32) rc = launch_g<float, 0>(b, st);
         else if (a.digest_dtype == SCOUT_F64) rc = launch_g<double, 1>(b, st);

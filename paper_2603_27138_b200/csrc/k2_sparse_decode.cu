@@ -30,6 +30,9 @@
 // a small combine kernel (same merge rule).
 #include "scout_common.cuh"
 
+#include <cstddef>
+#include <cstring>
+
 #include <math_constants.h>
 
 using namespace scout_dev;
@@ -87,7 +90,8 @@ struct Seg {
 // segment pieces and MAXB blocks; a layer's share is one or more chunks, so a
 // range of any length or unit count is planned whole). Built by the planner
 // warp ahead of the consumers (double-buffered).
-constexpr int ZMAX = 16;  // units without a resident block this CTA finalizes, listed in the plan
+constexpr int ZMAX = 16;
+constexpr int NR_REG = 16;  // resident counts the planner holds in registers per lane (512 units)  // units without a resident block this CTA finalizes, listed in the plan
 constexpr int CH_FIRST = 1, CH_LAST = 2;  // first / last chunk of its layer
 // A plan entry packs the pool slot (< 2^26: 2 TiB of 32 KiB slots, more than
 // any device holds) with the block's valid rows - 1 (0..63).
@@ -283,7 +287,8 @@ __device__ __forceinline__ Plan& plan_acquire(Smem& sm, int c, long long& waited
 // Finish chunk c (its segment pieces are written): pull the query rows of the
 // segments starting here into L2, fill the block list (pool slot, valid rows)
 // and publish it to the producer, consumers and combiners.
-__device__ void plan_publish(const K2StepArgs& a, const K2Layer& io, Smem& sm, int c, int nseg, int nblk, int jbase,
+template <typename Args>
+__device__ void plan_publish(const Args& a, const K2Layer& io, Smem& sm, int c, int nseg, int nblk, int jbase,
                              int layer, int flags, int lane) {
     Plan& P = sm.plan[c & 1];
     __syncwarp();  // lane 0's segment records
@@ -298,19 +303,36 @@ __device__ void plan_publish(const K2StepArgs& a, const K2Layer& io, Smem& sm, i
             asm volatile("prefetch.global.L2 [%0];" ::"l"(qp));
         }
     }
-    for (int f = lane; f < nblk; f += 32) {
-        int lo = 0, hi = nseg - 1;  // the last piece with f0 <= f (f0 ascending)
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (P.segs[mid].f0 <= f) lo = mid;
-            else hi = mid - 1;
+    // four blocks per lane per round, their loads in flight together (the
+    // producer waits for this list)
+    constexpr int PB = 4;
+    for (int f0 = 0; f0 < nblk; f0 += 32 * PB) {
+        int unit[PB], slot[PB], rid[PB], nt[PB];
+#pragma unroll
+        for (int r = 0; r < PB; ++r) {
+            const int f = f0 + 32 * r + lane;
+            unit[r] = -1;
+            if (f >= nblk) continue;
+            int lo = 0, hi = nseg - 1;  // the last piece with f0 <= f (f0 ascending)
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (P.segs[mid].f0 <= f) lo = mid;
+                else hi = mid - 1;
+            }
+            const Seg sg = P.segs[lo];
+            const size_t idx = static_cast<size_t>(sg.unit) * a.k_stride + sg.j0 + (f - sg.f0);
+            unit[r] = sg.unit;
+            slot[r] = __ldcg(io.res_slots + idx);
+            rid[r] = __ldcg(io.res_ids + idx);
+            nt[r] = __ldcg(a.n_tokens + sg.unit);
         }
-        const Seg sg = P.segs[lo];
-        const size_t idx = static_cast<size_t>(sg.unit) * a.k_stride + sg.j0 + (f - sg.f0);
-        const int nt = a.n_tokens[sg.unit];
-        const int nb = (nt + BS - 1) / BS;
-        const int rows = (io.res_ids[idx] == nb - 1) ? nt - (nb - 1) * BS : BS;  // the open block's fill
-        P.blk[f] = static_cast<uint32_t>(io.res_slots[idx]) | (static_cast<uint32_t>(rows - 1) << BLK_ROWS_SHIFT);
+#pragma unroll
+        for (int r = 0; r < PB; ++r) {
+            if (unit[r] < 0) continue;
+            const int nb = (nt[r] + BS - 1) / BS;
+            const int rows = (rid[r] == nb - 1) ? nt[r] - (nb - 1) * BS : BS;  // the open block's fill
+            P.blk[f0 + 32 * r + lane] = static_cast<uint32_t>(slot[r]) | (static_cast<uint32_t>(rows - 1) << BLK_ROWS_SHIFT);
+        }
     }
     if (lane == 0) {
         P.nsegs = nseg;
@@ -331,16 +353,40 @@ __device__ void plan_publish(const K2StepArgs& a, const K2Layer& io, Smem& sm, i
 // block); segment (cta c, unit u) owns partial slot c+u. A range may touch any
 // number of units and hold any number of blocks: pieces go into chunks of at
 // most MAXSEG pieces / MAXB blocks, a segment split at a chunk boundary.
-__device__ void plan_layer(const K2StepArgs& a, const K2Layer& io, Smem& sm, int layer, int& c, int& j, int lane,
+template <typename Args>
+__device__ void plan_layer(const Args& a, const K2Layer& io, Smem& sm, int layer, int& c, int& j, int lane,
                            long long& waited) {
     const int nunits = a.n_units;
+    // the units' resident counts: up to 32 * NR_REG units are loaded once, all
+    // loads in flight together (one dependent round trip per pass instead of
+    // one per 32 units: a single-layer launch waits for its plan)
+    int nr[NR_REG];
+    const bool cached = nunits <= 32 * NR_REG;
+    if (cached) {
+#pragma unroll
+        for (int i = 0; i < NR_REG; ++i) {
+            const int u = 32 * i + lane;
+            nr[i] = u < nunits ? __ldcg(io.n_res + u) : 0;
+        }
+    }
+    auto n_res_of = [&](int base) -> int {
+        if (cached) {
+            int v = 0;
+#pragma unroll
+            for (int i = 0; i < NR_REG; ++i)
+                if (32 * i == base) v = nr[i];
+            return v;
+        }
+        const int u = base + lane;
+        return u < nunits ? io.n_res[u] : 0;
+    };
     Plan* P = &plan_acquire(sm, c, waited, a.prof != nullptr);
     long long T = 0;
     {
         int loc = 0, nz = 0;
         for (int base = 0; base < nunits; base += 32) {
             const int u = base + lane;
-            const int n = u < nunits ? io.n_res[u] : 0;
+            const int n = n_res_of(base);
             loc += n;
             // units with no resident block that this CTA finalizes (CPU partial or zeros)
             const bool z = u < nunits && n == 0 && u % static_cast<int>(gridDim.x) == static_cast<int>(blockIdx.x);
@@ -360,8 +406,7 @@ __device__ void plan_layer(const K2StepArgs& a, const K2Layer& io, Smem& sm, int
     long long run = 0;
     int nseg = 0, nblk = 0, jb = j, first = CH_FIRST;
     for (int base = 0; base < nunits && run < hi; base += 32) {
-        const int u = base + lane;
-        const int n = u < nunits ? io.n_res[u] : 0;
+        const int n = n_res_of(base);
         int incl = n;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -422,8 +467,8 @@ __device__ void plan_layer(const K2StepArgs& a, const K2Layer& io, Smem& sm, int
 // stream) could launch next to K2 until it exited: the recalls then landed a
 // step late and K2 waited for them (tier mode 6.05 -> 7.1 ms per step). 144
 // leaves room for two 32-register warps on SMSP 0 and does not spill.
-template <int G>
-__global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
+template <int G, int NL>
+__global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgsT<NL> a) {
     extern __shared__ __align__(1024) uint8_t dsmem[];
     __shared__ Smem sm;
     uint8_t* stages = dsmem;
@@ -680,7 +725,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgs a) {
                     __threadfence();
                     if (atomicAdd(&sm.layer_fin[L], 1) == NCOMB - 1) {
                         __threadfence();
-                        atomicAdd(a.layer_done + L, 1u);
+                        atomicAdd(a.layer_done + L, 1u + (blockIdx.x == 0 ? a.done_extra : 0u));
                     }
                 }
             }
@@ -1035,18 +1080,31 @@ int scout_k2_launch(const K2StepArgs& a, cudaStream_t st, bool pdl) {
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     const int grid = scout_k2_grid(a.n_units, a.k_stride, a.max_ctas);
-    auto go = [&](auto kern) {
+    if (a.group != 1 && a.group != 2 && a.group != 4 && a.group != 8) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "K2: group %d not in {1,2,4,8}", a.group);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    auto go = [&](auto kern, const auto& args) {
         ensure_smem(reinterpret_cast<const void*>(kern), tc::SMEM_BYTES);
-        launch(kern, dim3(grid), dim3(tc::NTHREADS), tc::SMEM_BYTES, st, pdl, a);
+        launch(kern, dim3(grid), dim3(tc::NTHREADS), tc::SMEM_BYTES, st, pdl, args);
     };
-    switch (a.group) {
-        case 1: go(tc::sparse_decode_tc_kernel<1>); break;
-        case 2: go(tc::sparse_decode_tc_kernel<2>); break;
-        case 4: go(tc::sparse_decode_tc_kernel<4>); break;
-        case 8: go(tc::sparse_decode_tc_kernel<8>); break;
-        default:
-            set_error(SCOUT_ERR_INVALID_ARGUMENT, "K2: group %d not in {1,2,4,8}", a.group);
-            return SCOUT_ERR_INVALID_ARGUMENT;
+    if (a.n_layers == 1) {  // the 1-slot parameter block
+        static thread_local K2StepArgsT<1> a1;
+        std::memcpy(&a1, &a, offsetof(K2StepArgs, layers));
+        a1.layers[0] = a.layers[0];
+        switch (a.group) {
+            case 1: go(tc::sparse_decode_tc_kernel<1, 1>, a1); break;
+            case 2: go(tc::sparse_decode_tc_kernel<2, 1>, a1); break;
+            case 4: go(tc::sparse_decode_tc_kernel<4, 1>, a1); break;
+            default: go(tc::sparse_decode_tc_kernel<8, 1>, a1); break;
+        }
+    } else {
+        switch (a.group) {
+            case 1: go(tc::sparse_decode_tc_kernel<1, K2_MAX_LAYERS>, a); break;
+            case 2: go(tc::sparse_decode_tc_kernel<2, K2_MAX_LAYERS>, a); break;
+            case 4: go(tc::sparse_decode_tc_kernel<4, K2_MAX_LAYERS>, a); break;
+            default: go(tc::sparse_decode_tc_kernel<8, K2_MAX_LAYERS>, a); break;
+        }
     }
     return check_launch("scout_sparse_decode");
 }

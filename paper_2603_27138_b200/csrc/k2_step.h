@@ -21,7 +21,10 @@ struct K2Layer {
     unsigned pad;
 };
 
-struct K2StepArgs {
+// NL: layer slots. The struct is the kernel's parameter block: a single-layer
+// launch uses the 1-slot form (~170 B of parameters instead of ~8 KB)
+template <int NL>
+struct K2StepArgsT {
     int n_units, group, k_stride, n_layers;
     float scale;
     const void* kv_pool;
@@ -37,8 +40,11 @@ struct K2StepArgs {
     int cpu_bf16;             // CPU partial o is bf16 (else f32); its (m, l) stay f32
     unsigned long long* prof; // optional [grid][16] cycle counters (SCOUT_K2_PROF diagnostics)
     int l2_prefetch;          // blocks the producer prefetches into L2 ahead of the ring (0: none)
-    K2Layer layers[K2_MAX_LAYERS];
+    unsigned done_extra;      // CTA 0 adds this to layer_done too (a launch narrower than the
+                              // engine's grid still counts `grid` per layer)
+    K2Layer layers[NL];
 };
+using K2StepArgs = K2StepArgsT<K2_MAX_LAYERS>;
 
 // per-layer workspace bytes for n_units units and a grid of `grid` CTAs
 size_t scout_k2_ws_layer_bytes(int n_units, int grid);

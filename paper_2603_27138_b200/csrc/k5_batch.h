@@ -41,6 +41,19 @@ struct TierApplyArgs {
     int due_tick[K5_MAX_LAYERS];
 };
 
+// GpuSidePolicy::all_resident: every fast block of layers [layer0, layer0 +
+// n) in ascending id order (ids / slots [L][U][stride], counts n [L][U],
+// indexed by absolute layer). layers (tier mode, device array) or tables
+// (static mode: per-layer block tables [U][nbs], slot or -1).
+struct ResidentListArgs {
+    const scout_tier_layer* layers;
+    const int32_t* tables[K5_MAX_LAYERS];
+    int nbs, layer0, stride;
+    const int32_t* n_tokens;
+    int32_t *ids, *slots, *n;
+};
+int scout_tier_resident_lists(const ResidentListArgs& a, int n_units, int n_layers_launch, cudaStream_t st);
+
 int scout_tier_plan_layers(const scout_tier_layer* layers_dev, int n_layers, int n_units, int nb_stride,
                            const int32_t* n_tokens, int step, int32_t* tables, cudaStream_t st);
 // post-attention bookkeeping of layers [a.layer0, a.layer0 + n_layers_launch)

@@ -669,6 +669,46 @@ __global__ void __launch_bounds__(TT) tier_apply_layers_kernel(const TierApplyAr
     apply_unit(a.layers[l], blockIdx.x, a.nbs, a.n_tokens, a.due_tick[blockIdx.y], nullptr, S);
 }
 
+// GpuSidePolicy::all_resident (engine.hpp:28-29, 253-256): the on-device
+// side of layer l is its whole fast tier at attention time (after
+// begin_layer's tickets), residency_set(l) in ascending id order, with each
+// block's pool slot. Tier mode reads the K5 state (fast = tier flag; an
+// in-flight block already holds its destination slot in `table` but is not
+// fast yet); the static mode reads the layer's block table (slot >= 0).
+__global__ void __launch_bounds__(TT) tier_resident_lists_kernel(const ResidentListArgs a) {
+    __shared__ TierSm S;
+    const int u = blockIdx.x, l = a.layer0 + blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const size_t o = static_cast<size_t>(u) * a.nbs;
+    const int32_t* table = a.layers ? a.layers[l].table + o : a.tables[l] + o;
+    const uint8_t* tier = a.layers ? a.layers[l].tier + o : nullptr;
+    const int nb = min(n_blocks_of(a.n_tokens[u]), a.nbs);
+    const size_t row = (static_cast<size_t>(l) * gridDim.x + u) * a.stride;
+    int total = 0;
+    for (int base = 0; base < nb; base += TT) {
+        const int b = base + static_cast<int>(threadIdx.x);
+        const int slot = b < nb ? table[b] : -1;
+        const bool f = b < nb && (tier ? tier[b] != 0 : slot >= 0);
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (lane == 0) S.cnt[w] = __popc(bal);
+        __syncthreads();
+        int off = total, tot = 0;
+#pragma unroll
+        for (int i = 0; i < TW; ++i) {
+            off += i < w ? S.cnt[i] : 0;
+            tot += S.cnt[i];
+        }
+        if (f) {
+            const int pos = off + __popc(bal & ((1u << lane) - 1u));
+            a.ids[row + pos] = b;
+            a.slots[row + pos] = slot;
+        }
+        total += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.n[static_cast<size_t>(l) * gridDim.x + u] = total;
+}
+
 __global__ void advance_tokens_kernel(int32_t* n_tokens, int n) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) n_tokens[i] += 1;
@@ -692,6 +732,12 @@ int scout_tier_apply_layers(const TierApplyArgs& a, int n_units, cudaStream_t st
     if (a.n <= 0) return SCOUT_OK;
     tier_apply_layers_kernel<<<dim3(n_units, a.n), TT, 0, st>>>(a);
     return scout_host::check_launch("tier apply (due layers)");
+}
+
+int scout_tier_resident_lists(const ResidentListArgs& a, int n_units, int n_layers_launch, cudaStream_t st) {
+    if (n_layers_launch <= 0 || n_units <= 0) return SCOUT_OK;
+    tier_resident_lists_kernel<<<dim3(n_units, n_layers_launch), TT, 0, st>>>(a);
+    return scout_host::check_launch("resident lists (all_resident)");
 }
 
 int scout_tier_advance(int32_t* n_tokens, int n_units, cudaStream_t st) {

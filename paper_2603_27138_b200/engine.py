@@ -33,7 +33,8 @@ class DecodeEngine:
     def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
                  recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
                  recall_mode=0, q_dtype=torch.float32, tier=None, host_blocks=0, cpu_dtype=torch.float32,
-                 recall_intervals=None, recall_stagger=False, cpu_worker=False, cpu_threads=0):
+                 recall_intervals=None, recall_stagger=False, cpu_worker=False, cpu_threads=0,
+                 gpu_side_policy="predicted_topk_intersect_resident", layer_ctas=0):
         """tier: a tier.DeviceTieredCache whose state the engine drives on the
         device (device tier mode: decode_step_kv); host_tier then holds block
         images at ((layer*U + unit)*nb_stride + id) % host_blocks.
@@ -43,7 +44,11 @@ class DecodeEngine:
         round 1's (step + layer) % interval cadence instead.
         cpu_worker: the engine computes each step's CPU partials itself
         (device tier mode, host path; the decode calls then take no cpu_o /
-        cpu_ml) on cpu_threads host threads (0 = all)."""
+        cpu_ml) on cpu_threads host threads (0 = all).
+        gpu_side_policy: the reference's GpuSidePolicy (engine.hpp:25-29):
+        "predicted_topk_intersect_resident" or "all_resident" (the GPU side
+        attends to the layer's whole fast tier at attention time).
+        layer_ctas: K2 CTAs of a layer-by-layer launch (0 automatic, < 0 all)."""
         self.L, self.batch, self.hq, self.hkv, self.G, self.k = layers, batch, hq, hkv, hq // hkv, k
         self.U = batch * hkv
         self.layer_states = layer_states  # keep tensors alive
@@ -65,6 +70,13 @@ class DecodeEngine:
             cfg.recall_intervals = C.cast(self._rc_int, C.c_void_p)
         cfg.recall_stagger = int(bool(recall_stagger))
         cfg.cpu_worker, cfg.cpu_threads = int(bool(cpu_worker)), int(cpu_threads)
+        policies = {"predicted_topk_intersect_resident": A.SCOUT_GPU_SIDE_PREDICTED,
+                    "all_resident": A.SCOUT_GPU_SIDE_ALL_RESIDENT}
+        if gpu_side_policy not in policies:
+            raise ValueError(f"gpu_side_policy {gpu_side_policy!r}: one of {sorted(policies)}")
+        cfg.gpu_side_policy = policies[gpu_side_policy]
+        cfg.layer_ctas = int(layer_ctas)
+        self.gpu_side_policy = gpu_side_policy
         self.cpu_worker = bool(cpu_worker)
         self.tier = tier
         if tier is not None:

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 
 def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True, q_dtype=torch.float32,
-          cpu_dtype=torch.float32):
+          cpu_dtype=torch.float32, gpu_side="predicted_topk_intersect_resident"):
     dev = torch.device("cuda")
     U = batch * hkv
     nbs = ((nb + 7) // 8) * 8
@@ -43,7 +43,7 @@ def build(rng, L=4, batch=3, hkv=2, G=4, nb=40, k=8, cap=12, recall=True, q_dtyp
     eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=n_tokens, pool=pool,
                        kv_dtype=torch.bfloat16, layer_states=layers, scale=1 / math.sqrt(D),
                        recall_interval=2 if recall else 0, host_tier=host if recall else None, host_staging=True,
-                       chunk_layers=2, q_dtype=q_dtype, cpu_dtype=cpu_dtype)
+                       chunk_layers=2, q_dtype=q_dtype, cpu_dtype=cpu_dtype, gpu_side_policy=gpu_side)
     q_true = torch.randn(L, U * G, D, device=dev).to(q_dtype)
     q_pred = torch.randn(L, U * G, D, device=dev).to(q_dtype)
     cpu_o = torch.randn(L, U * G, D, device=dev).to(cpu_dtype)
@@ -124,3 +124,40 @@ def test_engine_recall_moves_blocks_after_attention(cuda):
     for li, st in enumerate(c["layers"]):
         for s_, d_ in zip(st.recall_src.tolist(), st.recall_dst.tolist()):
             assert torch.equal(pool[d_ * sb:(d_ + 1) * sb], c["host"][s_ * sb:(s_ + 1) * sb]), (li, d_)
+
+
+def test_engine_static_all_resident_matches_per_layer_ops(cuda):
+    """GpuSidePolicy::all_resident (engine.hpp:28-29, 253-256) in the static
+    view: each layer's GPU side is its whole block table (every resident
+    block, ascending ids), merged with the CPU partial, on the device path and
+    the host-buffer path."""
+    c = build(np.random.default_rng(12), recall=False, gpu_side="all_resident")
+    want = []
+    for li in range(c["L"]):
+        table = c["layers"][li].table.cpu().numpy()
+        nt = c["n_tokens"].cpu().numpy()
+        U, nbs = table.shape
+        ids = np.zeros((U, nbs), np.int32)
+        slots = np.zeros((U, nbs), np.int32)
+        n = np.zeros(U, np.int32)
+        for u in range(U):
+            f = np.nonzero(table[u, :(int(nt[u]) + 63) // 64] >= 0)[0]
+            ids[u, :len(f)], slots[u, :len(f)], n[u] = f, table[u, f], len(f)
+        to = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+        want.append(ops.sparse_decode(c["q_true"][li], c["pool"], torch.bfloat16, to(slots), to(ids), to(n),
+                                      c["n_tokens"], c["G"], cpu_o=c["cpu_o"][li], cpu_ml=c["cpu_ml"][li]))
+    out_o = torch.empty(c["q_true"].shape, device="cuda")
+    out_ml = torch.empty(c["L"], c["U"] * c["G"], 2, device="cuda")
+    for step in (1, 2):
+        c["eng"].decode_step(step, c["q_true"], c["q_pred"], c["cpu_o"], c["cpu_ml"], out_o, out_ml)
+        torch.cuda.synchronize()
+        for li in range(c["L"]):
+            assert torch.equal(out_o[li], want[li][0]) and torch.equal(out_ml[li], want[li][1]), (step, li)
+    h = lambda t: t.cpu().pin_memory()  # noqa: E731
+    h_o = torch.empty(out_o.shape).pin_memory()
+    h_ml = torch.empty(out_ml.shape).pin_memory()
+    c["eng"].decode_step_host(3, h(c["q_true"]), h(c["q_pred"]), h(c["cpu_o"]), h(c["cpu_ml"]), h_o, h_ml)
+    c["eng"].sync()
+    torch.cuda.synchronize()
+    for li in range(c["L"]):
+        assert torch.equal(h_o[li], want[li][0].cpu()), li

@@ -52,7 +52,30 @@ POLICIES = {
     "no_recall": (None, 8, False, False),
     "no_recall_external_place": (None, 8, False, True),
     "stagger_opt_in": ([3, 3, 3], 8, True, False),
+    # GpuSidePolicy::all_resident (engine.hpp:28-29, 253-256): the GPU side
+    # attends to the layer's whole fast tier after begin_layer's tickets
+    "all_resident_every_3": ([3, 3, 3], 8, False, False),
+    "all_resident_no_recall": (None, 8, False, False),
 }
+ALL_RESIDENT = {"all_resident_every_3", "all_resident_no_recall"}
+
+
+def fast_tier_lists(rt, i, n_tokens, nbs):
+    """residency_set(i) at attention time (the fast tier, ascending ids) with each
+    block's pool slot, as [U][nbs] lists for ops.sparse_decode."""
+    tier, table = rt.tier[i].cpu().numpy(), rt.table[i].cpu().numpy()
+    U = tier.shape[0]
+    ids = np.zeros((U, nbs), np.int32)
+    slots = np.zeros((U, nbs), np.int32)
+    n = np.zeros(U, np.int32)
+    for u in range(U):
+        nb = (int(n_tokens[u]) + BS - 1) // BS
+        f = np.nonzero(tier[u, :nb])[0]
+        ids[u, :len(f)] = f
+        slots[u, :len(f)] = table[u, f]
+        n[u] = len(f)
+    to = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    return to(slots), to(ids), to(n)
 
 
 @pytest.mark.parametrize("policy", sorted(POLICIES))
@@ -83,7 +106,9 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
     eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=eng_side.n_tokens,
                        pool=eng_side.pool, kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D),
                        recall_interval=0, recall_intervals=intervals, recall_stagger=stagger,
-                       host_tier=eng_side.host, tier=eng_side.tier, host_blocks=0, q_dtype=torch.bfloat16)
+                       host_tier=eng_side.host, tier=eng_side.tier, host_blocks=0, q_dtype=torch.bfloat16,
+                       gpu_side_policy="all_resident" if policy in ALL_RESIDENT else
+                       "predicted_topk_intersect_resident")
     policy_ref = P.RefRecall(U, intervals) if (intervals and not stagger) else None
     out_o = torch.empty(L, U * G, D, device="cuda")
     out_ml = torch.empty(L, U * G, 2, device="cuda")
@@ -110,8 +135,14 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
                 sel[t] = ops.score_topk_split(q, rep.dig[t], rep.n_tokens, k, G, block_table=rt.residency_table(t),
                                               step=step, last_selected=rt.last_sel[t], k_stride=k)
             r = sel[i]
-            o, ml = ops.sparse_decode(q_true[i], rep.pool, kv, r["res_slots"], r["res_ids"], r["n_res"], rep.n_tokens,
-                                      G, cpu_o=cpu_o[i], cpu_ml=cpu_ml[i])
+            if policy in ALL_RESIDENT:  # engine.hpp:253-256: gpu_ids = residency_set(i)
+                torch.cuda.synchronize()
+                a_slots, a_ids, a_n = fast_tier_lists(rt, i, rep.n_tokens.cpu().numpy(), nbs)
+                o, ml = ops.sparse_decode(q_true[i], rep.pool, kv, a_slots, a_ids, a_n, rep.n_tokens, G,
+                                          cpu_o=cpu_o[i], cpu_ml=cpu_ml[i])
+            else:
+                o, ml = ops.sparse_decode(q_true[i], rep.pool, kv, r["res_slots"], r["res_ids"], r["n_res"],
+                                          rep.n_tokens, G, cpu_o=cpu_o[i], cpu_ml=cpu_ml[i])
             want.append((o, ml))
             rt.append_token(i, k_new[i], v_new[i], rep.pool, kv, rep.dig[i], host_tier=rep.host)
             if not intervals:
@@ -242,8 +273,10 @@ def test_engine_tier_back_to_back_steps_with_recalls(cuda):
     assert int(sd.n_tokens[0]) == T0 + 60
 
 
-@pytest.mark.parametrize("stagger", [False, True])
-def test_engine_layerwise_matches_fused_step(cuda, stagger):
+@pytest.mark.parametrize("stagger,gpu_side", [(False, "predicted_topk_intersect_resident"),
+                                               (True, "predicted_topk_intersect_resident"),
+                                               (False, "all_resident")])
+def test_engine_layerwise_matches_fused_step(cuda, stagger, gpu_side):
     """scout_engine_decode_layer (one call per layer, inputs given layer by
     layer) against scout_engine_decode_step_kv (all layers at once) on an
     identical second cache: the same outputs bit for bit and the same tier
@@ -261,7 +294,7 @@ def test_engine_layerwise_matches_fused_step(cuda, stagger):
         engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
                                  kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=0,
                                  recall_intervals=[2, 3, 2, 1], recall_stagger=stagger, host_tier=sd.host,
-                                 tier=sd.tier, q_dtype=torch.bfloat16))
+                                 tier=sd.tier, q_dtype=torch.bfloat16, gpu_side_policy=gpu_side))
     out = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
     lw = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
     for step in range(1, steps + 1):
