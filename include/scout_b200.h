@@ -505,6 +505,9 @@ int scout_engine_tier_changed(scout_engine* eng);
  * call, then resets. */
 int scout_engine_set_timing(scout_engine* eng, int enable);
 int scout_engine_stats(scout_engine* eng, double* k2_ms_total, int* k2_count, long long* launches);
+/* The same window's K2 launch durations one by one (ms[0..min(n, max_n))),
+ * without resetting it (call before scout_engine_stats); synchronises. */
+int scout_engine_k2_times(scout_engine* eng, float* ms, int max_n, int* n);
 /* In-engine CPU worker (cfg.cpu_worker): the wall time its partials took
  * on the host pool, summed over the steps since the last call, then reset. */
 int scout_engine_worker_stats(scout_engine* eng, double* cpu_ms_total, int* steps);

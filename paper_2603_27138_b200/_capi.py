@@ -32,7 +32,7 @@ EXPORTED = (
     "scout_sparse_decode_grid",
     "scout_sparse_decode", "scout_merge_partials", "scout_recall_gather", "scout_recall_copy",
     "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
-    "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k1_outputs",
+    "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k2_times", "scout_engine_k1_outputs",
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv",
@@ -154,6 +154,7 @@ def lib() -> C.CDLL:
         L.scout_engine_tier_changed.argtypes = [_vp]
         L.scout_engine_set_timing.argtypes = [_vp, C.c_int]
         L.scout_engine_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]
+        L.scout_engine_k2_times.argtypes = [_vp, _vp, C.c_int, C.POINTER(C.c_int)]
         L.scout_engine_k1_outputs.argtypes = [_vp] + [C.POINTER(_vp)] * 7
         L.scout_engine_worker_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.scout_engine_check_state.argtypes = [_vp]

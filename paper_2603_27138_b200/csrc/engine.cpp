@@ -1572,6 +1572,18 @@ extern "C" int scout_engine_set_timing(scout_engine* e, int enable) {
     return SCOUT_OK;
 }
 
+extern "C" int scout_engine_k2_times(scout_engine* e, float* ms, int max_n, int* n) {
+    if (!e || (max_n > 0 && !ms)) return SCOUT_ERR_INVALID_ARGUMENT;
+    int k = 0;
+    for (size_t i = 0; i + 1 < e->tev_used; i += 2, ++k) {
+        if (k >= max_n) continue;
+        CU(cudaEventSynchronize(e->tev[i + 1]));
+        CU(cudaEventElapsedTime(ms + k, e->tev[i], e->tev[i + 1]));
+    }
+    if (n) *n = k;
+    return SCOUT_OK;
+}
+
 extern "C" int scout_engine_stats(scout_engine* e, double* k2_ms_total, int* k2_count, long long* launches) {
     if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
     double tot = 0.0;

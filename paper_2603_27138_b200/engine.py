@@ -171,6 +171,13 @@ class DecodeEngine:
     def set_timing(self, on: bool):
         A.check(A.lib().scout_engine_set_timing(self._h, int(on)))
 
+    def k2_times(self, max_n=4096):
+        """Per-launch K2 durations (ms) of the current timing window (before stats())."""
+        buf = (C.c_float * max_n)()
+        n = C.c_int()
+        A.check(A.lib().scout_engine_k2_times(self._h, C.cast(buf, C.c_void_p), max_n, C.byref(n)))
+        return list(buf[:min(n.value, max_n)])
+
     def stats(self):
         ms, n, launches = C.c_double(), C.c_int(), C.c_longlong()
         A.check(A.lib().scout_engine_stats(self._h, C.byref(ms), C.byref(n), C.byref(launches)))
