@@ -136,12 +136,21 @@ class TierWorkload:
     the tokens' new K/V. The initial placement keeps each unit's selected
     blocks minus the CPU share (the paper's 8.2%) resident, filled to capacity."""
 
-    def __init__(self, cfg, dev, seed, max_steps, requests):
+    def __init__(self, cfg, dev, seed, max_steps, requests, warm_slots=0, victim_cache=True, host_units=0):
+        """requests: a contiguous range of global request ids (this rank's
+        shard). warm_slots: pool slots per (layer, unit) beyond capacity + the
+        open block + one in-flight ticket; they start with the warm images of
+        the next-best blocks by the placement query (the victim cache, see
+        scout_tier_layer) and keep evicted blocks' images later. host_units:
+        units of the global workload (the host tier's index space, shared by
+        every rank's shard; 0 = this shard's)."""
         from paper_2603_27138_b200 import ops
         from paper_2603_27138_b200.engine import LayerState
         from paper_2603_27138_b200.tier import DeviceTieredCache
 
         self.cfg, self.dev, self.requests = cfg, dev, list(requests)
+        assert self.requests == list(range(self.requests[0], self.requests[0] + len(self.requests))), \
+            "a shard is a contiguous request range"
         L, hq, hkv = cfg["layers"], cfg["hq"], cfg["hkv"]
         B = len(self.requests)
         G = hq // hkv
@@ -150,21 +159,29 @@ class TierWorkload:
         nbs = ((nb + (max_steps + BS - 1) // BS + 1 + 7) // 8) * 8  # room for the appended tokens
         k, cap = cfg["k"], cfg["capacity"]
         self.L, self.U, self.G, self.nb, self.k, self.B, self.hkv = L, U, G, nb, k, B, hkv
+        self.host_units, self.host_unit0 = int(host_units) or U, self.requests[0] * hkv
         kv_dt = torch.bfloat16
+        W = max(0, min(int(warm_slots), nb - cap)) if victim_cache else 0
+        self.warm_slots, self.victim_cache = W, bool(victim_cache)
         # pool slots per (layer, unit): every block for the pinned layer 0; else the
         # capacity's sealed fast blocks + the open block + one recall ticket in
         # flight (at most k blocks: predicted \ residency), so a unit can never
-        # run out of slots, however far its selection drifted since the last recall
-        spu = [nbs] + [cap + 1 + k] * (L - 1)
-        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=spu, device=dev)
+        # run out of slots, however far its selection drifted since the last recall,
+        # + W slots of warm images (device victim cache)
+        spu = [nbs] + [cap + 1 + k + W] * (L - 1)
+        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=spu, device=dev,
+                                      victim_cache=victim_cache)
         self.tier.pin_layer(0)
         self.pool = ops.alloc_pool(self.tier.n_slots, kv_dt, dev)
-        pv = self.pool.view(torch.bfloat16).view(-1)
-        half = ops.slot_bytes(kv_dt) // 2  # bf16 elements per slot
-        for li in range(L):  # each (layer, request)'s slot range from its own generator
-            for i, r in enumerate(self.requests):
-                s0 = (self.tier.layer_base[li] + i * hkv * spu[li]) * half
-                pv[s0:s0 + hkv * spu[li] * half].normal_(generator=_gen(dev, seed, r, 1000 + li))
+        sb = ops.slot_bytes(kv_dt)
+        # host tier: the slow copy of every block. Synthetic and bounded: block
+        # (layer, global unit, id) is image ((layer*host_units + unit)*nbs + id) % host_blocks,
+        # the same on every rank; the device holds the same bytes for its fast
+        # and warm blocks (one content per block whichever side reads it)
+        self.host_blocks = 8192
+        self.host_tier = torch.empty(self.host_blocks * sb, dtype=torch.uint8).pin_memory()
+        self.host_tier.view(torch.bfloat16).normal_(generator=torch.Generator().manual_seed(seed))
+        host_dev = self.host_tier.to(dev)
         # requests differ in length (by < one block), so seals (and their
         # write-through) spread over steps instead of all units at once
         lens = cfg["ctx"] - 2 * (torch.tensor(self.requests, dtype=torch.int32, device=dev) % 32)
@@ -202,12 +219,11 @@ class TierWorkload:
         self.cpu_ml = torch.stack([m, l_], dim=-1).contiguous()
         self.out_o = torch.empty(L, U * G, D, device=dev)
         self.out_ml = torch.empty(L, U * G, 2, device=dev)
-        self.host_blocks = 8192
-        sb = ops.slot_bytes(kv_dt)
-        self.host_tier = torch.empty(self.host_blocks * sb, dtype=torch.uint8).pin_memory()
-        self.host_tier.view(torch.bfloat16).normal_(generator=torch.Generator().manual_seed(seed))
         cpu_per_unit = int(round(cfg["cpu_frac"] * k))
+        uid = torch.arange(U, device=dev, dtype=torch.int64)[:, None]
+        ids = torch.arange(nbs, device=dev, dtype=torch.int32)[None]
         layers = []
+        self.warm_blocks = 0
         for li in range(L):
             dig = torch.empty(U, 2, D, nbs, dtype=kv_dt, device=dev)
             for i, r in enumerate(self.requests):
@@ -218,7 +234,7 @@ class TierWorkload:
                 dig[i * hkv:(i + 1) * hkv, 1] = torch.maximum(a, b)
             dig[..., nb:] = 0  # blocks still to be appended
             base = self.tier.layer_base[li] + torch.arange(U, device=dev, dtype=torch.int32)[:, None] * spu[li]
-            ids = torch.arange(nbs, device=dev, dtype=torch.int32)[None]
+            warm = warm_rank = None
             if li == 0:  # pinned: every block resident
                 table = torch.where(ids < nb, base + ids, -1)
             else:
@@ -237,12 +253,59 @@ class TierWorkload:
                 keep = score.argsort(dim=1, descending=True)[:, :cap]
                 table = torch.full((U, nbs), -1, dtype=torch.int32, device=dev)
                 table.scatter_(1, keep, (base + torch.arange(cap, device=dev, dtype=torch.int32)[None]).to(torch.int32))
-            self.tier.adopt(li, table.contiguous(), self.n_tokens)
+                if W > 0:
+                    # warm images: the W best slow sealed blocks by the placement query's
+                    # stacked digest score (what a prefill that ends with the whole KV in
+                    # HBM can leave behind), in the slots after the fast ones; the worst
+                    # of them is reused first
+                    qs = self.q_pred[li].float().view(U, G, D)
+                    lo, hi = dig[:, 0].float(), dig[:, 1].float()  # [U][D][nbs]
+                    real = torch.zeros(U, nbs, device=dev)
+                    for g_ in range(G):
+                        qg = qs[:, g_, :, None]
+                        real += torch.maximum(qg * lo, qg * hi).sum(1)
+                    real[table >= 0] = -math.inf
+                    real[:, nb:] = -math.inf
+                    real[(self.n_tokens % BS != 0), nb - 1] = -math.inf  # the open block is fast
+                    wid = real.argsort(dim=1, descending=True)[:, :W]  # best first
+                    warm = torch.full((U, nbs), -1, dtype=torch.int32, device=dev)
+                    warm.scatter_(1, wid, (base + cap + torch.arange(W, device=dev, dtype=torch.int32)[None]))
+                    warm_rank = torch.zeros(U, nbs, dtype=torch.int64, device=dev)
+                    warm_rank.scatter_(1, wid, W - 1 - torch.arange(W, device=dev, dtype=torch.int64)[None].expand(U, W))
+                    del lo, hi, real
+            # device content of the fast (and warm) blocks = their host-tier images
+            for t in (table, warm):
+                if t is None:
+                    continue
+                uu, bb = (t >= 0).nonzero(as_tuple=True)
+                src = ((li * self.host_units + self.host_unit0 + uu.long()) * nbs + bb.long()) % self.host_blocks
+                ops.recall_gather(self.pool, kv_dt, host_dev, src, t[uu, bb])
+            if warm is not None:
+                self.warm_blocks += int((warm >= 0).sum())
+            self.tier.adopt(li, table.contiguous(), self.n_tokens, warm=warm, warm_rank=warm_rank)
             layers.append(LayerState(dig, torch.full((U, nbs), -1, dtype=torch.int32, device=dev)))
+        del host_dev
         self.layer_states = layers
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
         self.engine = None
+
+    @staticmethod
+    def auto_warm_slots(cfg, batch, max_steps, dev, reserve_gib=12.0):
+        """Warm slots per (layer, unit) that fill the HBM left after the pinned
+        layer, the digests, the query paths and a reserve for the engine and
+        the verification (the pool is sized for 180 GB of HBM3e)."""
+        free, _ = torch.cuda.mem_get_info(dev)
+        L, hkv, G = cfg["layers"], cfg["hkv"], cfg["hq"] // cfg["hkv"]
+        U = batch * hkv
+        nb = cfg["ctx"] // BS
+        nbs = ((nb + (max_steps + BS - 1) // BS + 1 + 7) // 8) * 8
+        qb = 2 if cfg["q_dtype"] == torch.bfloat16 else 4
+        fixed = (L * U * 2 * D * nbs * 2 + U * nbs * 32768
+                 + 2 * cfg.get("drift_points", 32) * L * U * G * D * qb + reserve_gib * 2**30)
+        per_slot = (L - 1) * U * 32768
+        spu = int((free - fixed) // per_slot)
+        return max(0, min(spu - (cfg["capacity"] + 1 + cfg["k"]), nb - cfg["capacity"]))
 
     def make_engine(self, **kw):
         """(Re)create the engine over this workload's state (the tier state and
@@ -253,7 +316,8 @@ class TierWorkload:
             self.engine.close()
         cfg = self.cfg
         opts = dict(recall_interval=cfg["recall"], recall_stagger=cfg.get("recall_policy") == "stagger",
-                    cpu_dtype=cfg.get("cpu_dtype", torch.float32), recall_mode=cfg.get("recall_mode", 0))
+                    cpu_dtype=cfg.get("cpu_dtype", torch.float32), recall_mode=cfg.get("recall_mode", 1),
+                    host_units=self.host_units, host_unit0=self.host_unit0)
         opts.update(kw)
         self.engine = DecodeEngine(layers=self.L, batch=self.B, hq=cfg["hq"], hkv=cfg["hkv"], k=self.k,
                                    n_tokens=self.n_tokens, pool=self.pool, kv_dtype=torch.bfloat16,
@@ -543,32 +607,39 @@ def verify_step(wl, step, n_units=8, layers=None):
                          "reference sum order is pinned in tests/"}
 
 
-def cross_rank_check(wl, cfg, args, ws, rank, dev, steps_done, seed, gb):
-    """N > 1, outside the timed region: the per-request output sums of the last
-    step gathered from every rank (the shards of one global workload), and
-    rank 0 rebuilding the first and last request of every rank's shard as a
-    workload of its own, replaying the same steps alone, and comparing."""
-    from paper_2603_27138_b200.sharding import gather_per_request, request_shard
+def output_sums(wl, gb, ws, rank):
+    """Per-request sums of the last step's outputs, gathered from every rank
+    (indexed by global request id)."""
+    from paper_2603_27138_b200.sharding import gather_per_request
 
-    G, hkv, L = wl.G, wl.hkv, wl.L
-    per = hkv * G
-    mine = wl.out_o.view(L, wl.B, per, D).double().sum(dim=(0, 2, 3))  # [B]
-    allsum = gather_per_request(mine, gb, ws, rank)
+    per = wl.hkv * wl.G
+    mine = wl.out_o.view(wl.L, wl.B, per, D).double().sum(dim=(0, 2, 3))  # [B]
+    return gather_per_request(mine, gb, ws, rank).cpu() if ws > 1 else mine.cpu()
+
+
+def cross_rank_replay(cfg, args, ws, rank, dev, steps_done, seed, gb, allsum, warm, vc):
+    """N > 1, after everything else (rank 0 has freed its own workload): rank 0
+    rebuilds the LAST rank's shard of the global workload (same requests, same
+    host-tier index space, same warm slots), replays steps 1..steps_done
+    alone and compares that step's per-request output sums with what that
+    rank produced."""
+    from paper_2603_27138_b200.sharding import request_shard
+
     res = None
     if rank == 0:
-        sample = sorted({s + off for r in range(ws) for s, n in [request_shard(gb, ws, r)] for off in (0, n - 1) if n})
-        sub = TierWorkload(cfg, dev, seed, max_steps=args.max_steps, requests=sample)
+        first, n = request_shard(gb, ws, ws - 1)
+        sub = TierWorkload(cfg, dev, seed, max_steps=args.max_steps, requests=range(first, first + n),
+                           warm_slots=warm, victim_cache=vc, host_units=gb * cfg["hkv"])
         sub.make_engine()
-        for s in range(1, steps_done + 1):
-            sub.step(s)
+        for s_ in range(1, steps_done + 1):
+            sub.step(s_)
         sub.engine.sync()
         torch.cuda.synchronize(dev)
-        got = sub.out_o.view(L, sub.B, per, D).double().sum(dim=(0, 2, 3)).cpu()
-        want = allsum.cpu()[sample]
+        got = output_sums(sub, gb, 1, 0)
+        want = allsum[first:first + n]
         rel = float(((got - want).abs() / want.abs().clamp_min(1e-30)).max())
-        res = {"requests_recomputed_alone": sample, "max_rel_diff_of_output_sums": rel, "pass": rel <= 1e-3,
-               "note": "stream-K splits differ with the batch (fp32 merge order); selections and tier state do "
-                       "not depend on it"}
+        res = {"shard_recomputed": [first, first + n], "rank": ws - 1, "steps_replayed": steps_done,
+               "max_rel_diff_of_output_sums": rel, "pass": rel <= 1e-3}
         sub.engine.close()
         del sub
     barrier(ws)
@@ -741,8 +812,14 @@ def main():
                     help="reference (default): layer i is due when step - last_recall >= 16 "
                          "(recall.hpp:114-126), so every layer recalls at steps 16, 32, ...; stagger: layer i "
                          "recalls when (step + i) %% 16 == 0 (the same volume spread over the steps)")
-    ap.add_argument("--recall-mode", default="ce", choices=["ce", "sm"],
-                    help="recall copies on the copy engines (ce, default) or an SM gather kernel (sm)")
+    ap.add_argument("--recall-mode", default="sm", choices=["ce", "sm"],
+                    help="recall copies: an SM gather kernel over the mapped host tier (sm, default) or the copy "
+                         "engines, one cudaMemcpyAsync per contiguous run (ce)")
+    ap.add_argument("--warm-slots", type=int, default=-1,
+                    help="device tier mode: pool slots per (layer, unit) for warm images of slow blocks (the device "
+                         "victim cache); -1 (default): fill the HBM left after the rest of the workload")
+    ap.add_argument("--victim-cache", default="on", choices=["on", "off"],
+                    help="off: every recall copies its blocks from the host tier (no warm images)")
     ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
                     help="query dtype (q_true / q_pred); bf16 = the model's projection output")
     ap.add_argument("--cpu-dtype", default="bf16", choices=["bf16", "f32"],
@@ -780,8 +857,16 @@ def main():
     tier_mode = args.tier == "device" and not cfg.get("static_only")
     args.max_steps = args.warmup + 3 * args.steps + 2 * args.e2e_steps + 48
     if tier_mode:
+        vc = args.victim_cache == "on"
+        warm = args.warm_slots if args.warm_slots >= 0 else (
+            TierWorkload.auto_warm_slots(cfg, cfg["batch"], args.max_steps, dev) if vc else 0)
+        if ws > 1:  # every rank the same (the smallest shard's budget decides)
+            t = torch.tensor([warm], dtype=torch.int64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+            warm = int(t)
         wl = TierWorkload(cfg, dev, seed=args.seed, max_steps=args.max_steps,
-                          requests=range(first, first + cfg["batch"]))
+                          requests=range(first, first + cfg["batch"]), warm_slots=warm, victim_cache=vc,
+                          host_units=gb * cfg["hkv"])
         wl.make_engine()
     else:
         wl = StaticWorkload(cfg, dev, seed=args.seed + rank)
@@ -808,6 +893,8 @@ def main():
     torch.cuda.synchronize(dev)
     eng = wl.engine
     eng.stats()  # reset counters
+    if tier_mode:
+        eng.recall_stats(reset=True)
     eng.set_timing(True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -832,8 +919,21 @@ def main():
         res_tok_layers = [int(x) for x in k1o["res_tokens"].sum(1).tolist()]
         cpu_tok = int(k1o["cpu_tokens"].sum())
         eng.check_state()  # no rejected ticket, no slot shortage, check_split held on every (layer, unit)
+        rc_warm, rc_copy = eng.recall_stats()
         tier_info = {"mode": "device (scout_engine_decode_step_kv)", "resident_token_frac_last_step":
                      sum(res_tok_layers) / max(sum(res_tok_layers) + cpu_tok, 1),
+                     "recall": {"blocks_per_step": (rc_warm + rc_copy) / args.steps,
+                                "warm_blocks_per_step": rc_warm / args.steps,
+                                "copied_blocks_per_step": rc_copy / args.steps,
+                                "h2d_bytes_per_step": rc_copy * 32768 / args.steps,
+                                "warm_frac": rc_warm / max(rc_warm + rc_copy, 1),
+                                "victim_cache": wl.victim_cache, "warm_slots_per_unit": wl.warm_slots,
+                                "warm_images_at_placement": wl.warm_blocks,
+                                "pool_gib": wl.pool.numel() / 2**30,
+                                "note": "a recalled block whose image still sits in a free pool slot (evicted "
+                                        "earlier, or left by the placement) takes that slot back: a tier flip "
+                                        "with no bytes moved, as in the reference (kv_store.hpp:201-218); the "
+                                        "others are copied from the pinned host tier by the SM gather (K4)"},
                      "tokens_at_end": int(wl.n_tokens[0]), "host_tier_blocks": wl.host_blocks,
                      "query_drift": cfg["drift"], "check_state": "ok (check_split on device, every layer and unit)",
                      "note": "queries follow a closed path (drift radius); the CPU share settles where the "
@@ -872,8 +972,9 @@ def main():
         verify = verify_step(wl, step_no)
         log(f"verify: {verify['pass']} (top-k {verify['topk_sets_exact']} exact, {verify['topk_sets_wrong']} wrong; "
             f"attention max rel err {verify['attention_max_rel_err']:.2e})")
-        if ws > 1:
-            verify["cross_rank"] = cross_rank_check(wl, cfg, args, ws, rank, dev, step_no, args.seed, gb)
+    allsum, verify_step_no = None, step_no
+    if tier_mode and ws > 1 and not args.profile:
+        allsum = output_sums(wl, gb, ws, rank)
     extras = {}
     if tier_mode and not args.profile and not args.no_extras:
         # ---- the other recall cadence on the same workload (state carries over)
@@ -919,6 +1020,31 @@ def main():
         e2e_worker = run_e2e_worker(wl, args.e2e_steps, dev, ws, gb, step0=step_no)
         step_no += 5 + args.e2e_steps
         log(f"e2e with CPU worker {e2e_worker['ms_per_step']:.3f} ms/step")
+    # ---- the same cadence with every recalled block copied over PCIe (no warm images)
+    if tier_mode and not args.profile and not args.no_extras and wl.victim_cache:
+        wl.tier.victim_cache = False
+        wl.make_engine()
+        run_steps(5)
+        wl.engine.sync()
+        wl.engine.recall_stats(reset=True)
+
+        def vstep(i):
+            nonlocal step_no
+            step_no += 1
+            wl.step(step_no)
+            if i == args.steps - 1:
+                wl.engine.sync()
+
+        ms_v = timed(vstep, args.steps, dev, ws)
+        w_, c_ = wl.engine.recall_stats()
+        extras["victim_cache_off"] = {
+            "value": gb / (ms_v / 1000.0), "ms_per_step": ms_v, "recall_policy": args.recall_policy,
+            "copied_blocks_per_step": c_ / args.steps, "h2d_bytes_per_step": c_ * 32768 / args.steps,
+            "note": "same workload and cadence, every recalled block copied from the host tier (PCIe)"}
+        log(f"victim cache off: {ms_v:.3f} ms/step, {c_ / args.steps:.0f} copied blocks per step")
+        wl.tier.forget_warm()
+        wl.tier.victim_cache = True
+        wl.make_engine()
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
@@ -930,6 +1056,17 @@ def main():
     cpu_worker = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.profile:
         cpu_worker = measure_cpu_worker(wl, cfg)
+    cpu_per_unit = wl.cpu_per_unit
+    if allsum is not None:  # N > 1: rank 0 replays the last rank's shard alone (its own workload freed first)
+        vc_, warm_ = wl.victim_cache, wl.warm_slots
+        wl.engine.close()
+        wl = eng = None
+        import gc
+
+        gc.collect()
+        torch.cuda.empty_cache()
+        verify["cross_rank"] = cross_rank_replay(cfg, args, ws, rank, dev, verify_step_no, args.seed, gb, allsum,
+                                                 warm_, vc_)
     if rank == 0:
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,
@@ -942,7 +1079,7 @@ def main():
                        "layers": cfg["layers"], "heads": f"{cfg['hq']}q/{cfg['hkv']}kv", "head_dim": D,
                        "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "cpu_partial_dtype": args.cpu_dtype,
                        "gpu_cache_blocks_per_unit": cfg["capacity"],
-                       "cpu_blocks_per_unit_at_placement": wl.cpu_per_unit, "recall_every": cfg["recall"],
+                       "cpu_blocks_per_unit_at_placement": cpu_per_unit, "recall_every": cfg["recall"],
                        "recall_policy": args.recall_policy, "tier": args.tier,
                        "parallelism": f"request-sharded x{ws}, no collective",
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},

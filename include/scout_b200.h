@@ -232,9 +232,11 @@ int scout_merge_partials(const float* a_o, const float* a_ml, const float* b_o, 
  * event; the kernel streams over PCIe / C2C with 16-byte loads.            */
 int scout_recall_gather(void* kv_pool, int kv_dtype, const void* host_blocks,
                         const int64_t* src_index, const int32_t* dst_slots, int n, void* stream);
-/* Same move on the copy engines (one cudaMemcpyBatchAsync, no SM time):
- * src_index / dst_slots are HOST arrays here. Preferred next to a persistent
- * K2 that needs every SM; `stream` must not be the legacy default stream. */
+/* Same move on the copy engines (no SM time): one cudaMemcpyAsync per run of
+ * consecutive (src_index, dst_slot) pairs, so it suits contiguous runs; a
+ * scattered list is per-call bound (~6.7 GB/s, profiles/r02a_pcie_recall.txt)
+ * and belongs on scout_recall_gather. src_index / dst_slots are HOST arrays
+ * here; `stream` must not be the legacy default stream.                    */
 int scout_recall_copy(void* kv_pool, int kv_dtype, const void* host_blocks, const int64_t* src_index,
                       const int32_t* dst_slots, int n, void* stream);
 
@@ -245,21 +247,35 @@ int scout_recall_copy(void* kv_pool, int kv_dtype, const void* host_blocks, cons
  * Clock ticks encode the reference's (step, layer) pairs as
  * step * n_layers + layer (pair order == integer order).
  * All arrays are device memory, row stride nb_stride blocks ([U][nb_stride])
- * or slots_per_unit (free stack); zero-initialise tier, fill table / ready
- * with -1, and push the (layer, unit)'s pool slots onto free_slots.        */
+ * or slots_per_unit (free ring); zero-initialise tier, fill table / ready /
+ * warm / free_owner with -1, zero free_head, and put the (layer, unit)'s
+ * pool slots in free_slots[u][0 .. n_free).                                */
 typedef struct scout_tier_layer {
     int32_t* table;       /* [U][nbs] pool slot of a fast or in-flight block, -1 otherwise */
     uint8_t* tier;        /* [U][nbs] 1 = fast, 0 = slow (Tier, kv_store.hpp:19) */
     int32_t* last_sel;    /* [U][nbs] last_selected step (K1 writes it: mark_selected) */
     int32_t* ready;       /* [U][nbs] ready tick of an in-flight recall, -1 none */
     int32_t* ticket;      /* [U][nbs] issue number of that recall (apply order) */
-    int32_t* free_slots;  /* [U][slots_per_unit] stack of free pool slots */
+    int32_t* free_slots;  /* [U][slots_per_unit] ring of free pool slots */
     int32_t* n_free;      /* [U] */
     int32_t* err;         /* [U] sticky first error of the unit (0 none): 1 invalid
                              argument (reference throws std::invalid_argument), 2 out of slots,
                              3 (engine) K1's split broke check_split (engine.hpp:317-329) */
     int capacity;         /* sealed fast blocks per unit; <= 0: pinned layer (pin_layer) */
-    int slots_per_unit;
+    int slots_per_unit;   /* row stride of the free ring (>= the slots a (layer, unit) owns) */
+    /* The free slots form a FIFO ring per unit: entries (head + i) % slots_per_unit,
+     * i < n_free; allocation takes the oldest entry, a freed slot goes to the back.
+     * Device victim cache (optional: free_owner and warm both set, or both NULL):
+     * a slot freed by an eviction keeps the evicted block's image, so while the
+     * slot waits in the ring the block has a WARM copy in HBM. A recall of a warm
+     * block takes that slot back and moves no bytes (the reference moves none
+     * either: the tier flip is the recall, kv_store.hpp:201-218); the tier state
+     * is exactly the reference's either way. An allocation that reuses a slot
+     * forgets its image. Sealed blocks are immutable, so a warm
+     * image stays equal to the host-tier image.                             */
+    int32_t* free_head;   /* [U] ring head */
+    int32_t* free_owner;  /* [U][slots_per_unit] block whose image the entry's slot holds, -1 */
+    int32_t* warm;        /* [U][nbs] ring position of a slow block's warm image, -1 */
 } scout_tier_layer;
 
 /* append_token's bookkeeping (kv_store.hpp:95-115), n_tokens = count BEFORE
@@ -278,8 +294,9 @@ int scout_tier_apply(const scout_tier_layer* layer, int n_units, int nb_stride, 
 /* schedule_recall (kv_store.hpp:175-197) per unit: ids[u][0..n_ids[u]) an
  * ascending set of sealed, slow, not-in-flight blocks (else the unit's ticket
  * is rejected: err = 1, dst_slots = -1); n_ids[u] == 0 skips the unit.
- * Accepted blocks get a free pool slot, written to dst_slots[u][i] (the copy
- * engines' destination), and ready_tick / ticket.                          */
+ * Accepted blocks get a pool slot and ready_tick / ticket. dst_slots[u][i]:
+ * the slot (>= 0) the block's image must be copied into, or -2 - slot when
+ * the block's warm image already sits in that slot (no copy).             */
 int scout_tier_schedule_recall(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
                                const int32_t* ids, const int32_t* n_ids, int k_stride, int ready_tick, int ticket,
                                int32_t* dst_slots, void* stream);
@@ -382,7 +399,9 @@ typedef struct scout_engine_config {
     int max_ctas;              /* K2 grid (0 = one CTA per SM) */
     int host_staging;          /* 1: allocate device staging for decode_step_host */
     int chunk_layers;          /* layers per H2D/D2H chunk of the host path (0 = 8) */
-    int recall_mode;           /* 0: copy engines (scout_recall_copy), 1: SM gather kernel (K4) */
+    int recall_mode;           /* 1: SM gather kernel over the mapped host tier (K4, the default
+                                  of the Python engine); 0: copy engines, one cudaMemcpyAsync per
+                                  contiguous run (scout_recall_copy) */
     int q_dtype;               /* q_true / q_pred element type: SCOUT_F32 (0) or SCOUT_BF16 */
     /* device tier mode (optional): per-layer K5 state (host array of `layers`
      * descs over device arrays). Residency is then planned on the device
@@ -392,7 +411,7 @@ typedef struct scout_engine_config {
      * layer's CPU-side selected blocks every recall_interval steps straight
      * from K1's lists (no host round trip). host_tier holds block images at
      * ((layer * U + unit) * nb_stride + id) % host_blocks (host_blocks <= 0:
-     * no wrap; the bench bounds it and lets images alias).                 */
+     * no wrap; the bench bounds it and lets images alias; see host_units).  */
     const scout_tier_layer* tier;
     long long host_blocks;
     int cpu_dtype;             /* CPU-partial o element type: SCOUT_F32 (0) or SCOUT_BF16 (half the
@@ -429,6 +448,12 @@ typedef struct scout_engine_config {
      * single-layer launch; the SMs it leaves free run K1 of the next layer
      * beside it. 0: automatic (the grid less 28), < 0: the whole grid. */
     int layer_ctas;
+    /* Device tier mode: the host tier's unit index space when it is shared by
+     * several engines (request-sharded ranks): block (layer, unit u, id) of
+     * this engine is image ((layer * host_units + host_unit0 + u) * nb_stride
+     * + id) % host_blocks. host_units = 0: this engine's U, host_unit0 = 0. */
+    int host_units;
+    int host_unit0;
 } scout_engine_config;
 
 #define SCOUT_GPU_SIDE_PREDICTED 0
@@ -508,6 +533,10 @@ int scout_engine_stats(scout_engine* eng, double* k2_ms_total, int* k2_count, lo
 /* The same window's K2 launch durations one by one (ms[0..min(n, max_n))),
  * without resetting it (call before scout_engine_stats); synchronises. */
 int scout_engine_k2_times(scout_engine* eng, float* ms, int max_n, int* n);
+/* Device tier mode: recalled blocks since the last reset that were served by
+ * a warm image in HBM (no bytes moved) and that were copied from the host
+ * tier; reset != 0 zeroes the counts. Synchronises the device.            */
+int scout_engine_recall_stats(scout_engine* eng, long long* warm_blocks, long long* copied_blocks, int reset);
 /* In-engine CPU worker (cfg.cpu_worker): the wall time its partials took
  * on the host pool, summed over the steps since the last call, then reset. */
 int scout_engine_worker_stats(scout_engine* eng, double* cpu_ms_total, int* steps);

@@ -35,7 +35,7 @@ EXPORTED = (
     "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k2_times", "scout_engine_k1_outputs",
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
-    "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv",
+    "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv", "scout_engine_recall_stats",
     "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
     "scout_engine_worker_stats", "scout_engine_check_state", "scout_engine_decode_layer",
 )
@@ -47,7 +47,7 @@ _i32p = C.c_void_p  # device pointers travel as void*
 class TierLayer(C.Structure):
     _fields_ = [("table", _vp), ("tier", _vp), ("last_sel", _vp), ("ready", _vp), ("ticket", _vp),
                 ("free_slots", _vp), ("n_free", _vp), ("err", _vp), ("capacity", C.c_int),
-                ("slots_per_unit", C.c_int)]
+                ("slots_per_unit", C.c_int), ("free_head", _vp), ("free_owner", _vp), ("warm", _vp)]
 
 
 class TopkArgs(C.Structure):
@@ -87,7 +87,7 @@ class EngineConfig(C.Structure):
         ("q_dtype", C.c_int),
         ("tier", _vp), ("host_blocks", C.c_longlong), ("cpu_dtype", C.c_int),
         ("recall_intervals", _vp), ("recall_stagger", C.c_int), ("cpu_worker", C.c_int), ("cpu_threads", C.c_int),
-        ("gpu_side_policy", C.c_int), ("layer_ctas", C.c_int),
+        ("gpu_side_policy", C.c_int), ("layer_ctas", C.c_int), ("host_units", C.c_int), ("host_unit0", C.c_int),
     ]
 
 
@@ -155,6 +155,7 @@ def lib() -> C.CDLL:
         L.scout_engine_set_timing.argtypes = [_vp, C.c_int]
         L.scout_engine_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_longlong)]
         L.scout_engine_k2_times.argtypes = [_vp, _vp, C.c_int, C.POINTER(C.c_int)]
+        L.scout_engine_recall_stats.argtypes = [_vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.c_int]
         L.scout_engine_k1_outputs.argtypes = [_vp] + [C.POINTER(_vp)] * 7
         L.scout_engine_worker_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.scout_engine_check_state.argtypes = [_vp]

@@ -193,12 +193,18 @@ struct scout_engine {
     Buf tier_dst;                  // [L][U][k] recall destination slots
     Buf tier_rc_ids, tier_rc_n;    // [L][U][k] / [L][U] the recalled ids (predicted \ residency)
     Buf tier_dev;                  // [L] scout_tier_layer (device copy for the multi-layer launches)
+    Buf rc_stats;                  // [2] u64: recalled blocks served by a warm image / copied (K5 counts)
     uint8_t* host_dev = nullptr;   // device view of the pinned host tier
     std::vector<int> pending;      // per layer: ready tick of its in-flight recall ticket, -1 none
     int n_tickets = 0;
     cudaEvent_t ev_side_end = nullptr, ev_kvin = nullptr;
     bool side_recorded = false;
     int tick(int step, int layer) const { return step * cfg.layers + layer; }
+    // first host-tier image index of (layer, unit) (cfg.host_units / host_unit0)
+    long long host_row(int l, int u) const {
+        const long long hu = cfg.host_units > 0 ? cfg.host_units : U;
+        return (static_cast<long long>(l) * hu + cfg.host_unit0 + u) * cfg.nb_stride;
+    }
     // ---- in-engine CPU co-attention worker (cfg.cpu_worker; the reference's
     // PrecomputeWorker, engine.hpp:88-150): per step, once K1 has selected
     // and its CPU-side ids are on the host, a worker thread computes layer
@@ -517,7 +523,7 @@ struct scout_engine {
             scout_host::set_error(SCOUT_ERR_CUDA, "recall lists: %s", cudaGetErrorString(cudaGetLastError()));
             return SCOUT_ERR_CUDA;
         }
-        const int L = cfg.layers, k = cfg.k, nbs = cfg.nb_stride, i = job.layer;
+        const int L = cfg.layers, k = cfg.k, i = job.layer;
         const int32_t* ids = reinterpret_cast<const int32_t*>(rc_pinned + job.slot * rc_slot_bytes);
         const int32_t* nn = ids + static_cast<size_t>(L) * U * k;
         const int32_t* dst = nn + static_cast<size_t>(L) * U;
@@ -530,7 +536,7 @@ struct scout_engine {
             for (int j = 0; j < n; ++j) {
                 const size_t o = (static_cast<size_t>(i) * U + u) * k + j;
                 if (dst[o] < 0) continue;
-                long long hi = (static_cast<long long>(i) * U + u) * nbs + ids[o];
+                long long hi = host_row(i, u) + ids[o];
                 if (cfg.host_blocks > 0) hi %= cfg.host_blocks;
                 src_v.push_back(hi);
                 dst_v.push_back(dst[o]);
@@ -622,7 +628,7 @@ struct scout_engine {
     // publishes the flags (with whatever the partials hold) so no K2 waits
     // forever; the error is reported by the next call.
     int cw_run(const CwJob& job) {
-        const int par = job.par, L = cfg.layers, CH = cfg.chunk_layers, k = cfg.k, nbs = cfg.nb_stride;
+        const int par = job.par, L = cfg.layers, CH = cfg.chunk_layers, k = cfg.k;
         int rc = SCOUT_OK;
         if (cudaEventSynchronize(cw_ids_ev[par]) != cudaSuccess ||
             (cw_copy_rec[par] && cudaEventSynchronize(cw_copy_ev[par]) != cudaSuccess)) {
@@ -641,7 +647,7 @@ struct scout_engine {
                 for (int l = lo; l < lo + n; ++l)
                     for (int u = 0; u < U; ++u) {
                         const size_t row = (static_cast<size_t>(l) * U + u) * k;
-                        const long long base = (static_cast<long long>(l) * U + u) * nbs;
+                        const long long base = host_row(l, u);
                         for (int i = 0; i < nn[static_cast<size_t>(l) * U + u]; ++i) {
                             long long hi = base + ids[row + i];
                             if (cfg.host_blocks > 0) hi %= cfg.host_blocks;
@@ -777,11 +783,14 @@ struct scout_engine {
         for (int i = 0; i < L; ++i) pa.digests[i] = const_cast<void*>(layers[i].digests);
         pa.host_tier = host_dev;
         pa.host_blocks = cfg.host_blocks;
+        pa.host_units = cfg.host_units > 0 ? cfg.host_units : U;
+        pa.host_unit0 = cfg.host_unit0;
         pa.sel_ids = I(sel_ids[par]);
         pa.n_sel = I(n_sel[par]);
         pa.rc_ids = I(tier_rc_ids);
         pa.rc_n = I(tier_rc_n);
         pa.dst = I(tier_dst);
+        pa.rc_stats = static_cast<unsigned long long*>(rc_stats.p);
         pa.res_ids = all_res ? nullptr : I(res_ids[par]);  // check_split only for the predicted policy
         pa.n_res = I(n_res[par]);
         pa.cpu_ids = I(cpu_ids[par]);
@@ -846,7 +855,7 @@ struct scout_engine {
                 if (!pa.recall_due[i]) continue;
                 ++launches;
                 if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier,
-                                                  static_cast<long long>(i) * U * nbs, nbs, cfg.host_blocks, U,
+                                                  host_row(i, 0), nbs, cfg.host_blocks, U,
                                                   pa.rc_ids + lk(i), pa.rc_n + lu(i), pa.dst + lk(i), cfg.k, 0,
                                                   side)) != SCOUT_OK)
                     return rc;
@@ -952,6 +961,10 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
                   "scout_engine_create: cpu_worker needs device tier mode, host_staging and a host tier");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
+    if (c.host_unit0 < 0 || c.host_units < 0 || (c.host_units > 0 && c.host_unit0 + c.batch * c.hkv > c.host_units)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: host_unit0 + U must fit host_units");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
     if ((any_recall || c.tier) && !c.host_tier) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: recall needs a host tier");
         return SCOUT_ERR_INVALID_ARGUMENT;
@@ -1049,6 +1062,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         const size_t lu = static_cast<size_t>(c.layers) * e->U;
         if (e->plan_tab.alloc(lu * c.nb_stride * 4) || e->open_slot.alloc(lu * 4) || e->sealed_id.alloc(lu * 4) ||
             e->tier_dst.alloc(lu * c.k * 4) || e->tier_rc_ids.alloc(lu * c.k * 4) || e->tier_rc_n.alloc(lu * 4) ||
+            e->rc_stats.alloc(16) || cudaMemset(e->rc_stats.p, 0, 16) != cudaSuccess ||
             cudaEventCreateWithFlags(&e->ev_side_end, cudaEventDisableTiming) ||
             cudaEventCreateWithFlags(&e->ev_kvin, cudaEventDisableTiming)) {
             delete e;
@@ -1581,6 +1595,19 @@ extern "C" int scout_engine_k2_times(scout_engine* e, float* ms, int max_n, int*
         CU(cudaEventElapsedTime(ms + k, e->tev[i], e->tev[i + 1]));
     }
     if (n) *n = k;
+    return SCOUT_OK;
+}
+
+extern "C" int scout_engine_recall_stats(scout_engine* e, long long* warm_blocks, long long* copied_blocks, int reset) {
+    if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
+    unsigned long long h[2] = {0, 0};
+    if (e->rc_stats.p) {
+        CU(cudaDeviceSynchronize());
+        CU(cudaMemcpy(h, e->rc_stats.p, 16, cudaMemcpyDeviceToHost));
+        if (reset) CU(cudaMemset(e->rc_stats.p, 0, 16));
+    }
+    if (warm_blocks) *warm_blocks = static_cast<long long>(h[0]);
+    if (copied_blocks) *copied_blocks = static_cast<long long>(h[1]);
     return SCOUT_OK;
 }
 

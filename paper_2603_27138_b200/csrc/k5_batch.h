@@ -19,11 +19,13 @@ struct TierPostArgs {
     void* digests[K5_MAX_LAYERS];    // per layer [U][2][128][nbs] bf16
     uint8_t* host_tier;              // device view of the pinned host tier (nullptr: no write-through)
     long long host_blocks;
+    int host_units, host_unit0;      // image index ((l * host_units + host_unit0 + u) * nbs + id) % host_blocks
     const int32_t* sel_ids;          // [L][U][k] K1's selection of this step (the layer's predicted set)
     const int32_t* n_sel;            // [L][U]
     int32_t* rc_ids;                 // [L][U][k] out: the recalled ids (predicted \ residency after the
     int32_t* rc_n;                   //   append, maybe_schedule_recall recall.hpp:114-126), count [L][U]
-    int32_t* dst;                    // [L][U][k] recall destination slots
+    int32_t* dst;                    // [L][U][k] recall destination slots (-2 - slot: warm, no copy; -1 rejected)
+    unsigned long long* rc_stats;    // optional [2]: recalled blocks served warm / to copy (summed)
     // K1's split of this step, checked against the selection (check_split,
     // engine.hpp:317-329): [L][U][k] ascending lists and [L][U] counts
     const int32_t *res_ids, *n_res, *cpu_ids, *n_cpu, *res_tok, *cpu_tok;

@@ -75,12 +75,106 @@ struct Unit {
     int32_t* free_slots;
     int32_t* n_free;
     int32_t* err;
+    int32_t* head;   // free ring head
+    int32_t* owner;  // [S] block whose image the ring entry's slot holds (nullptr: no victim cache)
+    int32_t* warm;   // [nbs] ring position of a slow block's image, -1
+    int S;           // ring size
 };
 
 __device__ Unit unit_of(const scout_tier_layer& L, int u, int nbs) {
-    const size_t o = static_cast<size_t>(u) * nbs;
-    return Unit{L.table + o, L.tier + o, L.last_sel + o, L.ready + o, L.ticket + o,
-                L.free_slots + static_cast<size_t>(u) * L.slots_per_unit, L.n_free + u, L.err + u};
+    const size_t o = static_cast<size_t>(u) * nbs, r = static_cast<size_t>(u) * L.slots_per_unit;
+    const bool vc = L.free_owner && L.warm;
+    return Unit{L.table + o, L.tier + o, L.last_sel + o, L.ready + o, L.ticket + o, L.free_slots + r, L.n_free + u,
+                L.err + u, L.free_head + u, vc ? L.free_owner + r : nullptr, vc ? L.warm + o : nullptr,
+                L.slots_per_unit};
+}
+
+// ---- the free ring (one thread of the unit's CTA at a time). FIFO: a slot
+// freed by an eviction waits as long as possible before it is reused, so its
+// image (the evicted block's) serves as long as possible as a warm copy.
+// The oldest entry is taken; its slot's image, if any, is forgotten.
+__device__ int ring_pop(const Unit& U) {
+    const int n = *U.n_free;
+    if (n <= 0) return -1;
+    const int h = *U.head;
+    const int slot = U.free_slots[h];
+    if (U.owner) {
+        const int o = U.owner[h];
+        if (o >= 0 && U.warm[o] == h) U.warm[o] = -1;
+    }
+    *U.head = h + 1 == U.S ? 0 : h + 1;
+    *U.n_free = n - 1;
+    return slot;
+}
+// a freed slot goes to the back; owner >= 0: it holds that (now slow) block's image
+__device__ bool ring_push(const Unit& U, int slot, int owner) {
+    const int n = *U.n_free;
+    if (n >= U.S) return false;
+    int p = *U.head + n;
+    if (p >= U.S) p -= U.S;
+    U.free_slots[p] = slot;
+    if (U.owner) {
+        U.owner[p] = owner;
+        if (owner >= 0) U.warm[owner] = p;
+    }
+    *U.n_free = n + 1;
+    return true;
+}
+// block b's warm image leaves the ring with its slot (-1: b has none); the
+// oldest entry fills the hole
+__device__ int ring_take(const Unit& U, int b) {
+    if (!U.owner) return -1;
+    const int p = U.warm[b];
+    if (p < 0) return -1;
+    const int slot = U.free_slots[p];
+    U.warm[b] = -1;
+    const int h = *U.head;
+    if (p != h) {
+        const int s2 = U.free_slots[h], o2 = U.owner[h];
+        U.free_slots[p] = s2;
+        U.owner[p] = o2;
+        if (o2 >= 0) U.warm[o2] = p;
+    }
+    *U.head = h + 1 == U.S ? 0 : h + 1;
+    *U.n_free -= 1;
+    return slot;
+}
+
+// schedule_recall's slot assignment for a validated ticket (thread 0): warm
+// blocks take their own slot back first (dst = -2 - slot: no bytes to move),
+// then the others take the oldest free slots (dst = slot: the H2D copy's
+// destination). n <= n_free was checked, and every recalled block consumes
+// exactly one ring entry, so no pop can fail. Returns the warm count.
+__device__ int assign_recall_slots(const Unit& U, const int32_t* ids, int n, int32_t* dst) {
+    int hits = 0;
+    for (int i = 0; i < n; ++i) {
+        const int b = ids[i];
+        const int s = ring_take(U, b);
+        dst[i] = s >= 0 ? -2 - s : -1;
+        if (s >= 0) {
+            U.table[b] = s;
+            ++hits;
+        }
+    }
+    if (hits < n)
+        for (int i = 0; i < n; ++i) {
+            if (dst[i] != -1) continue;
+            const int b = ids[i];
+            const int s = ring_pop(U);
+            U.table[b] = s;
+            dst[i] = s;
+        }
+    return hits;
+}
+
+__device__ bool find_sorted_dev(const int32_t* v, int n, int x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (v[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < n && v[lo] == x;
 }
 
 __device__ void set_err(Unit& U, int code) {
@@ -107,11 +201,7 @@ __device__ void enforce_capacity(const scout_tier_layer& L, Unit& U, int nb, int
         if (threadIdx.x == 0) {
             const int v = static_cast<int>(key & 0xFFFFFFFFu);
             U.tier[v] = 0;
-            const int n = *U.n_free;
-            if (n < L.slots_per_unit) {
-                U.free_slots[n] = U.table[v];
-                *U.n_free = n + 1;
-            }
+            ring_push(U, U.table[v], v);  // the slot keeps v's image: a warm copy
             U.table[v] = -1;
         }
         __syncthreads();
@@ -137,13 +227,12 @@ __global__ void __launch_bounds__(TT) tier_append_kernel(const scout_tier_layer 
         } else {
             S.err = 0;
             if (pos % BS == 0) {
-                const int n = *U.n_free;
-                if (n <= 0) {
+                const int slot = ring_pop(U);
+                if (slot < 0) {
                     set_err(U, SCOUT_ERR_LOGIC);  // no pool slot for the new open block
                     S.err = 1;
                 } else {
-                    U.table[id] = U.free_slots[n - 1];
-                    *U.n_free = n - 1;
+                    U.table[id] = slot;
                     U.tier[id] = 1;
                     U.ready[id] = -1;
                     U.last_sel[id] = clock_step;
@@ -229,8 +318,7 @@ __global__ void __launch_bounds__(TT) tier_recall_kernel(const scout_tier_layer 
             set_err(U, SCOUT_ERR_LOGIC);  // not enough free pool slots for the ticket
             S.err = 1;
         } else {
-            S.n_free = *U.n_free;
-            *U.n_free = S.n_free - n;
+            assign_recall_slots(U, my, n, dst_slots + static_cast<size_t>(u) * k_stride);
         }
     }
     __syncthreads();
@@ -240,11 +328,8 @@ __global__ void __launch_bounds__(TT) tier_recall_kernel(const scout_tier_layer 
     }
     for (int i = threadIdx.x; i < n; i += TT) {
         const int id = my[i];
-        const int slot = U.free_slots[S.n_free - 1 - i];
-        U.table[id] = slot;
         U.ready[id] = ready_tick;
         U.ticket[id] = ticket;
-        dst_slots[static_cast<size_t>(u) * k_stride + i] = slot;
     }
 }
 
@@ -267,66 +352,84 @@ __global__ void __launch_bounds__(TT) tier_plan_kernel(const scout_tier_layer L,
 
 // place_after_prefill (kv_store.hpp:271-283): sealed blocks in keep (K1's
 // top-capacity selection over the sealed blocks, ascending ids) are fast, the
-// other sealed blocks go slow and free their slots; a kept block that was slow
-// takes a free slot, reported in fill_slots[u][i] (else -1) for the H2D fill
-// of its image. Pinned layers keep all.
+// other sealed blocks go slow and free their slots (which keep their images:
+// warm copies); a kept block that was slow takes its warm slot back
+// (fill_slots[u][i] = -2 - slot, nothing to copy) or the oldest free slot
+// (fill_slots[u][i] = slot, for the H2D fill of its image), else -1. Pinned
+// layers keep all.
 __global__ void __launch_bounds__(TT) tier_place_kernel(const scout_tier_layer L, int nbs, const int32_t* n_tokens,
                                                         const int32_t* keep, const int32_t* n_keep, int k_stride,
                                                         int32_t* fill_slots) {
     __shared__ TierSm S;
     if (L.capacity <= 0) return;
-    const int u = blockIdx.x;
+    const int u = blockIdx.x, lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     Unit U = unit_of(L, u, nbs);
     const int ntok = n_tokens[u];
     const int nb = min(n_blocks_of(ntok), nbs);
     const int32_t* kp = keep + static_cast<size_t>(u) * k_stride;
     const int nk = n_keep[u];
-    if (threadIdx.x == 0) S.n_free = *U.n_free;
-    __syncthreads();
-    // demote the sealed blocks outside keep
-    for (int b = threadIdx.x; b < nb; b += TT) {
-        if (!sealed(b, ntok)) continue;
-        int lo = 0, hi = nk;  // binary search in the ascending keep list
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (kp[mid] < b) lo = mid + 1;
-            else hi = mid;
+    const int head = *U.head, n0 = *U.n_free;
+    // demote the sealed blocks outside keep; the fast ones' slots join the
+    // ring in id order (an order-preserving compaction per round)
+    int pushed = 0;
+    for (int base = 0; base < nb; base += TT) {
+        const int b = base + static_cast<int>(threadIdx.x);
+        bool freed = false;
+        if (b < nb && sealed(b, ntok) && !find_sorted_dev(kp, nk, b)) {
+            freed = U.tier[b] && U.table[b] >= 0;
+            if (!freed) U.table[b] = -1;
+            U.tier[b] = 0;
         }
-        if (lo < nk && kp[lo] == b) continue;
-        if (U.tier[b] && U.table[b] >= 0) {
-            const int i = atomicAdd(&S.n_free, 1);
-            if (i < L.slots_per_unit) U.free_slots[i] = U.table[b];
+        const unsigned bal = __ballot_sync(0xffffffffu, freed);
+        if (lane == 0) S.cnt[w] = __popc(bal);
+        __syncthreads();
+        int off = pushed, tot = 0;
+#pragma unroll
+        for (int i = 0; i < TW; ++i) {
+            off += i < w ? S.cnt[i] : 0;
+            tot += S.cnt[i];
         }
-        U.table[b] = -1;
-        U.tier[b] = 0;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        S.n_free = min(S.n_free, L.slots_per_unit);
-        S.err = 0;
-    }
-    __syncthreads();
-    // promote the kept blocks that were slow
-    for (int i = threadIdx.x; i < nk; i += TT) {
-        const int b = kp[i];
-        int fill = -1;
-        if (b >= 0 && b < nb && !U.tier[b]) {
-            const int top = atomicSub(&S.n_free, 1);
-            if (top > 0) {
-                fill = U.free_slots[top - 1];
-                U.table[b] = fill;
-                U.tier[b] = 1;
-                U.ready[b] = -1;
-            } else {
-                S.err = 1;
+        if (freed) {
+            const int q = n0 + off + __popc(bal & ((1u << lane) - 1u));
+            if (q < U.S) {
+                const int p = (head + q) % U.S;
+                U.free_slots[p] = U.table[b];
+                if (U.owner) {
+                    U.owner[p] = b;
+                    U.warm[b] = p;
+                }
             }
+            U.table[b] = -1;
         }
-        if (fill_slots) fill_slots[static_cast<size_t>(u) * k_stride + i] = fill;
+        pushed += tot;
+        __syncthreads();
     }
-    __syncthreads();
+    // promote the kept blocks that were slow (one thread: the ring's order)
     if (threadIdx.x == 0) {
-        *U.n_free = max(S.n_free, 0);
-        if (S.err) set_err(U, SCOUT_ERR_LOGIC);
+        *U.n_free = min(n0 + pushed, U.S);
+        int err = 0;
+        for (int i = 0; i < nk; ++i) {
+            const int b = kp[i];
+            int fill = -1;
+            if (b >= 0 && b < nb && !U.tier[b]) {
+                int s = ring_take(U, b);
+                if (s >= 0) {
+                    fill = -2 - s;
+                } else {
+                    s = ring_pop(U);
+                    fill = s;
+                }
+                if (s >= 0) {
+                    U.table[b] = s;
+                    U.tier[b] = 1;
+                    U.ready[b] = -1;
+                } else {
+                    err = 1;
+                }
+            }
+            if (fill_slots) fill_slots[static_cast<size_t>(u) * k_stride + i] = fill;
+        }
+        if (err) set_err(U, SCOUT_ERR_LOGIC);
     }
 }
 
@@ -346,7 +449,8 @@ int check_layer(const scout_tier_layer* L, int n_units, int nbs, const char* wha
     using namespace scout_host;
     if (!L || n_units < 0 || nbs <= 0 ||
         (n_units > 0 && (!L->table || !L->tier || !L->last_sel || !L->ready || !L->ticket || !L->free_slots ||
-                         !L->n_free || !L->err || L->slots_per_unit <= 0))) {
+                         !L->n_free || !L->err || !L->free_head || L->slots_per_unit <= 0 ||
+                         (L->free_owner == nullptr) != (L->warm == nullptr)))) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "%s: bad tier layer", what);
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
@@ -507,13 +611,12 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
             set_err(U, SCOUT_ERR_INVALID_ARGUMENT);
             S.err = 1;
         } else if (r == 0) {
-            const int n = *U.n_free;
-            if (n <= 0) {
+            const int slot = ring_pop(U);
+            if (slot < 0) {
                 set_err(U, SCOUT_ERR_LOGIC);
                 S.err = 1;
             } else {
-                U.table[id] = U.free_slots[n - 1];
-                *U.n_free = n - 1;
+                U.table[id] = slot;
                 U.tier[id] = 1;
                 U.ready[id] = -1;
                 U.last_sel[id] = a.step;
@@ -550,7 +653,7 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
         __syncthreads();  // the row just written belongs to the image
         if (c == 0) U.last_sel[sealed_blk] = a.step;
         if (a.host_tier) {
-            long long hi = (static_cast<long long>(l) * gridDim.x + u) * a.nbs + sealed_blk;
+            long long hi = (static_cast<long long>(l) * a.host_units + a.host_unit0 + u) * a.nbs + sealed_blk;
             if (a.host_blocks > 0) hi %= a.host_blocks;
             const int4* src = reinterpret_cast<const int4*>(a.pool + static_cast<size_t>(slot) * BF16_SLOT_BYTES);
             int4* dst = reinterpret_cast<int4*>(a.host_tier + static_cast<size_t>(hi) * BF16_SLOT_BYTES);
@@ -644,8 +747,11 @@ __device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Un
             set_err(U, SCOUT_ERR_LOGIC);
             S.err = 1;
         } else {
-            S.n_free = *U.n_free;
-            *U.n_free = S.n_free - n;
+            const int hits = assign_recall_slots(U, my, n, dst);
+            if (a.rc_stats) {  // warm hits (no bytes) / blocks to copy
+                atomicAdd(a.rc_stats, static_cast<unsigned long long>(hits));
+                atomicAdd(a.rc_stats + 1, static_cast<unsigned long long>(n - hits));
+            }
         }
     }
     __syncthreads();
@@ -655,11 +761,8 @@ __device__ void post_recall(const TierPostArgs& a, const scout_tier_layer& L, Un
             continue;
         }
         const int b = my[i];
-        const int s2 = U.free_slots[S.n_free - 1 - i];
-        U.table[b] = s2;
         U.ready[b] = (a.step + 1) * a.n_layers + l;
         U.ticket[b] = a.ticket_base + l;
-        dst[i] = s2;
     }
 }
 

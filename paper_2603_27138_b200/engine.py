@@ -32,9 +32,9 @@ def _p(t):
 class DecodeEngine:
     def __init__(self, *, layers, batch, hq, hkv, k, n_tokens, pool, kv_dtype, layer_states, scale,
                  recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
-                 recall_mode=0, q_dtype=torch.float32, tier=None, host_blocks=0, cpu_dtype=torch.float32,
+                 recall_mode=1, q_dtype=torch.float32, tier=None, host_blocks=0, cpu_dtype=torch.float32,
                  recall_intervals=None, recall_stagger=False, cpu_worker=False, cpu_threads=0,
-                 gpu_side_policy="predicted_topk_intersect_resident", layer_ctas=0):
+                 gpu_side_policy="predicted_topk_intersect_resident", layer_ctas=0, host_units=0, host_unit0=0):
         """tier: a tier.DeviceTieredCache whose state the engine drives on the
         device (device tier mode: decode_step_kv); host_tier then holds block
         images at ((layer*U + unit)*nb_stride + id) % host_blocks.
@@ -48,7 +48,10 @@ class DecodeEngine:
         gpu_side_policy: the reference's GpuSidePolicy (engine.hpp:25-29):
         "predicted_topk_intersect_resident" or "all_resident" (the GPU side
         attends to the layer's whole fast tier at attention time).
-        layer_ctas: K2 CTAs of a layer-by-layer launch (0 automatic, < 0 all)."""
+        layer_ctas: K2 CTAs of a layer-by-layer launch (0 automatic, < 0 all).
+        host_units / host_unit0: the host tier's unit index space when ranks
+        share one (image ((layer*host_units + host_unit0 + u)*nb_stride + id)
+        % host_blocks); 0 / 0: this engine's units."""
         self.L, self.batch, self.hq, self.hkv, self.G, self.k = layers, batch, hq, hkv, hq // hkv, k
         self.U = batch * hkv
         self.layer_states = layer_states  # keep tensors alive
@@ -76,6 +79,7 @@ class DecodeEngine:
             raise ValueError(f"gpu_side_policy {gpu_side_policy!r}: one of {sorted(policies)}")
         cfg.gpu_side_policy = policies[gpu_side_policy]
         cfg.layer_ctas = int(layer_ctas)
+        cfg.host_units, cfg.host_unit0 = int(host_units), int(host_unit0)
         self.gpu_side_policy = gpu_side_policy
         self.cpu_worker = bool(cpu_worker)
         self.tier = tier
@@ -170,6 +174,13 @@ class DecodeEngine:
 
     def set_timing(self, on: bool):
         A.check(A.lib().scout_engine_set_timing(self._h, int(on)))
+
+    def recall_stats(self, reset=False):
+        """Device tier mode: (recalled blocks served by a warm image in HBM,
+        recalled blocks copied from the host tier) since the last reset."""
+        w, c = C.c_longlong(0), C.c_longlong(0)
+        A.check(A.lib().scout_engine_recall_stats(self._h, C.byref(w), C.byref(c), int(bool(reset))))
+        return int(w.value), int(c.value)
 
     def k2_times(self, max_n=4096):
         """Per-launch K2 durations (ms) of the current timing window (before stats())."""

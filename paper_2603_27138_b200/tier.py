@@ -24,10 +24,14 @@ BS = A.BLOCK_SIZE
 
 class DeviceTieredCache:
     def __init__(self, layers: int, n_units: int, nb_stride: int, capacity: int, slots_per_unit,
-                 device="cuda", slot_base: int = 0):
+                 device="cuda", slot_base: int = 0, victim_cache: bool = True):
         """slots_per_unit: pool slots each (layer, unit) owns, an int or one per
         layer (a pinned layer needs every block, the others capacity plus
-        room for in-flight recalls and the open block)."""
+        room for in-flight recalls and the open block; slots beyond that hold
+        warm images of slow blocks). victim_cache: a recall of a block whose
+        image still sits in a free slot takes that slot back and moves no
+        bytes (scout_tier_layer.free_owner / warm); the tier state is the
+        reference's either way."""
         self.L, self.U, self.nbs = layers, n_units, nb_stride
         spu = [int(slots_per_unit)] * layers if isinstance(slots_per_unit, int) else [int(x) for x in slots_per_unit]
         self.spu_l = spu
@@ -40,13 +44,20 @@ class DeviceTieredCache:
         self.last_sel = torch.zeros((layers, U, nbs), **i32)
         self.ready = torch.full((layers, U, nbs), -1, **i32)
         self.ticket = torch.zeros((layers, U, nbs), **i32)
-        # layer l, unit u owns pool slots layer_base[l] + u*spu[l] + [0, spu[l]); stack top = lowest slot
+        # layer l, unit u owns pool slots layer_base[l] + u*spu[l] + [0, spu[l]); the free
+        # slots form a FIFO ring per unit (head, n_free), lowest slot first
         self.layer_base = [slot_base + U * sum(spu[:l]) for l in range(layers)]
         self.free_slots = torch.zeros((layers, U, self.spu), **i32)
         for l in range(layers):
             base = self.layer_base[l] + torch.arange(U, **i32).view(U, 1) * spu[l]
-            self.free_slots[l, :, :spu[l]] = base + torch.arange(spu[l] - 1, -1, -1, **i32).view(1, -1)
+            self.free_slots[l, :, :spu[l]] = base + torch.arange(spu[l], **i32).view(1, -1)
         self.n_free = torch.tensor(spu, **i32).view(layers, 1).repeat(1, U).contiguous()
+        self.free_head = torch.zeros((layers, U), **i32)
+        # device victim cache: a free slot that still holds an evicted block's image
+        # (free_owner), and each slow block's ring position of such an image (warm)
+        self.victim_cache = bool(victim_cache)
+        self.free_owner = torch.full((layers, U, self.spu), -1, **i32)
+        self.warm = torch.full((layers, U, nbs), -1, **i32)
         self.n_slots = U * sum(spu)
         self.err = torch.zeros((layers, U), **i32)
         self.n_tokens = torch.zeros((layers, U), **i32)
@@ -61,8 +72,11 @@ class DeviceTieredCache:
 
     def layer_desc(self, layer: int) -> A.TierLayer:
         d = A.TierLayer()
-        for name in ("table", "tier", "last_sel", "ready", "ticket", "free_slots", "n_free", "err"):
+        for name in ("table", "tier", "last_sel", "ready", "ticket", "free_slots", "n_free", "err", "free_head"):
             setattr(d, name, getattr(self, name)[layer].data_ptr())
+        if self.victim_cache:
+            d.free_owner = self.free_owner[layer].data_ptr()
+            d.warm = self.warm[layer].data_ptr()
         d.capacity = self.capacity[layer]
         # the free stacks' row stride: the tensor is [L][U][max spu] whatever this
         # layer's own slot count (a layer owning fewer slots just never fills it)
@@ -86,29 +100,66 @@ class DeviceTieredCache:
                 raise ValueError(f"tier layer {layer}: invalid argument in units {bad}")
             raise RuntimeError(f"tier layer {layer}: out of pool slots in units {bad}")
 
-    def adopt(self, layer: int, table: torch.Tensor, n_tokens: torch.Tensor):
+    def adopt(self, layer: int, table: torch.Tensor, n_tokens: torch.Tensor, warm: torch.Tensor | None = None,
+              warm_rank: torch.Tensor | None = None):
         """Start a layer from a placed state (a prefill done elsewhere): the
         blocks with a slot in table [U][nbs] are fast, the rest of the first
-        n_tokens' blocks slow; every slot of the (layer, unit) range not in
-        table goes on the free stack. Marks start at 0."""
+        n_tokens' blocks slow; every other slot of the (layer, unit) range goes
+        on the free ring. warm [U][nbs] (optional, victim cache): slot of the
+        range in which the caller left a slow block's image; those slots join
+        the ring after the empty ones, ordered by warm_rank [U][nbs] (lower
+        is reused first; default: block id). Marks start at 0."""
         U, spu = self.U, self.spu_l[layer]
-        table = table.to(device=self.dev, dtype=torch.int32)
+        dev = self.dev
+        table = table.to(device=dev, dtype=torch.int32)
         self.table[layer].copy_(table)
         self.tier[layer].copy_((table >= 0).to(torch.uint8))
         self.last_sel[layer].zero_()
         self.ready[layer].fill_(-1)
         self.n_tokens[layer].copy_(n_tokens)
-        base = self.layer_base[layer] + torch.arange(U, device=self.dev, dtype=torch.int32).view(U, 1) * spu
-        cand = base + torch.arange(spu - 1, -1, -1, device=self.dev, dtype=torch.int32).view(1, -1)  # [U][spu]
-        used = torch.zeros((U, spu), dtype=torch.bool, device=self.dev)
-        rel = table - base
+        self.warm[layer].fill_(-1)
+        self.free_owner[layer].fill_(-1)
+        self.free_head[layer].zero_()
+        base = self.layer_base[layer] + torch.arange(U, device=dev, dtype=torch.int32).view(U, 1) * spu
+        cand = base + torch.arange(spu, device=dev, dtype=torch.int32).view(1, -1)  # [U][spu]
+        # sort key per slot of the range: 0 empty, 1 + rank a warm image, USED a fast block's
+        USED = 1 << 40
+        key = torch.zeros((U, spu), dtype=torch.int64, device=dev)
+        owner = torch.full((U, spu), -1, dtype=torch.int32, device=dev)
+        rel = (table - base).long()
         ok = (table >= 0) & (rel >= 0) & (rel < spu)
         uu, bb = ok.nonzero(as_tuple=True)
-        used[uu, (spu - 1 - rel[uu, bb]).long()] = True
-        # free slots first, in the stack's (descending) order
-        order = torch.sort(used.to(torch.int32), dim=1, stable=True).indices
+        key[uu, rel[uu, bb]] = USED
+        if warm is not None and self.victim_cache:
+            warm = warm.to(device=dev, dtype=torch.int32)
+            wrel = (warm - base).long()
+            wok = (warm >= 0) & (table < 0) & (wrel >= 0) & (wrel < spu)
+            uu, bb = wok.nonzero(as_tuple=True)
+            rk = warm_rank[uu, bb].to(dev).long() if warm_rank is not None else bb.long()
+            key[uu, wrel[uu, bb]] = 1 + rk
+            owner[uu, wrel[uu, bb]] = bb.to(torch.int32)
+        order = torch.sort(key, dim=1, stable=True).indices  # empty, warm by rank, then used
+        nfree = (key < USED).sum(1)
         self.free_slots[layer, :, :spu] = cand.gather(1, order)
-        self.n_free[layer] = (~used).sum(1).to(torch.int32)
+        ring_owner = owner.gather(1, order)
+        pos = torch.arange(spu, device=dev).view(1, -1).expand(U, spu)
+        ring_owner = torch.where(pos < nfree.view(U, 1), ring_owner, torch.full_like(ring_owner, -1))
+        self.free_owner[layer, :, :spu] = ring_owner
+        uu, pp = (ring_owner >= 0).nonzero(as_tuple=True)
+        self.warm[layer][uu, ring_owner[uu, pp].long()] = pp.to(torch.int32)
+        self.n_free[layer] = nfree.to(torch.int32)
+
+    def forget_warm(self):
+        """Drop every warm image (after engines ran with victim_cache off: the
+        ring reused slots without updating the warm positions)."""
+        self.warm.fill_(-1)
+        self.free_owner.fill_(-1)
+
+    def free_ring(self, layer: int, unit: int) -> list:
+        """The unit's free slots, oldest (next to be reused) first."""
+        n, h = int(self.n_free[layer, unit]), int(self.free_head[layer, unit])
+        fs = self.free_slots[layer, unit].tolist()
+        return [fs[(h + i) % self.spu] for i in range(n)]
 
     # ------------------------------------------------------------- reference API
     def pin_layer(self, layer: int):

@@ -18,20 +18,22 @@ import py_oracle as P
 pytestmark = pytest.mark.gpu
 
 
-def _workload(batch, policy, steps):
+def _workload(batch, policy, steps, warm=0):
     import bench
 
     cfg = dict(bench.CONFIGS["qwen3-32b-32k"])
     cfg.update(q_dtype=torch.bfloat16, cpu_dtype=torch.bfloat16, drift=0.15, recall_policy=policy, batch=batch)
-    wl = bench.TierWorkload(cfg, torch.device("cuda"), 1234, steps + 16, range(batch))
+    wl = bench.TierWorkload(cfg, torch.device("cuda"), 1234, steps + 16, range(batch), warm_slots=warm)
     wl.make_engine()
     return bench, wl
 
 
-@pytest.mark.parametrize("policy", ["reference", "stagger"])
-def test_bench_workload_slots_and_verify(cuda, policy):
+@pytest.mark.parametrize("policy,warm", [("reference", 0), ("reference", 48), ("stagger", 48)])
+def test_bench_workload_slots_and_verify(cuda, policy, warm):
+    """warm > 0: the bench's victim cache (warm images placed with the fast
+    set, then every evicted block's): recalls served warm, same checks."""
     steps = 40
-    bench, wl = _workload(2, policy, steps)
+    bench, wl = _workload(2, policy, steps, warm)
     for s in range(1, steps + 1):
         wl.step(s)
     wl.engine.sync()
@@ -43,11 +45,14 @@ def test_bench_workload_slots_and_verify(cuda, policy):
         for u in range(wl.U):
             base = tr.layer_base[l] + u * spu
             used = tr.table[l, u][tr.table[l, u] >= 0].cpu().numpy()
-            free = tr.free_slots[l, u, :int(tr.n_free[l, u])].cpu().numpy()
+            free = np.array(tr.free_ring(l, u), dtype=np.int64)
             assert len(set(used.tolist())) == len(used), (l, u)
             allslots = np.concatenate([used, free])
             assert len(set(allslots.tolist())) == len(allslots) == spu, (l, u)
             assert allslots.min() >= base and allslots.max() < base + spu, (l, u)
+    if warm:
+        w, c = wl.engine.recall_stats()
+        assert w > 0
     v = bench.verify_step(wl, steps + 1)
     assert v["pass"], v
 

@@ -25,9 +25,9 @@ D, BS = 128, 64
 class Side:
     """One side of the comparison: its own pool, digests, host tier and tier state."""
 
-    def __init__(self, L, U, nbs, cap, kv, seed_rows):
+    def __init__(self, L, U, nbs, cap, kv, seed_rows, victim_cache=True):
         dev = torch.device("cuda")
-        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=nbs)
+        self.tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=nbs, victim_cache=victim_cache)
         self.tier.pin_layer(0)
         self.pool = ops.alloc_pool(L * U * nbs, kv)
         self.dig = [torch.zeros(U, 2, D, nbs, dtype=kv, device=dev) for _ in range(L)]
@@ -244,10 +244,56 @@ def test_engine_tier_host_path_matches_device_path(cuda, cpu_dtype):
             assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
 
 
-def test_engine_tier_back_to_back_steps_with_recalls(cuda):
+@pytest.mark.parametrize("policy", ["reference", "stagger"])
+def test_engine_victim_cache_matches_copies(cuda, policy):
+    """The device victim cache (warm images in free pool slots) against the
+    same engine with every recall copied from the host tier: identical
+    outputs and tier state step after step (an image in HBM is the block's
+    host-tier image: sealed blocks are immutable and written through), with
+    most recalled blocks served warm on the victim side."""
+    L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 48
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 11 + 50
+    torch.manual_seed(11)
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    sides = [Side(L, U, nbs, cap, kv, seed_rows, victim_cache=vc) for vc in (True, False)]
+    engs = []
+    for sd in sides:
+        layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+        engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
+                                 kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=3,
+                                 recall_stagger=policy == "stagger", host_tier=sd.host, tier=sd.tier,
+                                 q_dtype=torch.bfloat16))
+    outs = [[torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")] for _ in range(2)]
+    qs = [torch.randn(L, U * G, D, device="cuda").bfloat16() for _ in range(6)]
+    for step in range(1, steps + 1):
+        co = torch.randn(L, U * G, D, device="cuda")
+        cm = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
+        kn, vn = torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")
+        for e, o in zip(engs, outs):  # queries cycle: blocks leave the fast tier and come back
+            e.decode_step_kv(step, qs[step % 6], qs[(step + 1) % 6], co, cm, kn, vn, *o)
+        for e in engs:
+            e.sync()
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]), step
+        for name in ("tier", "last_sel"):
+            assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
+        assert torch.equal(sides[0].tier.ready >= 0, sides[1].tier.ready >= 0), step
+    warm, copied = engs[0].recall_stats()
+    warm_off, copied_off = engs[1].recall_stats()
+    assert warm_off == 0 and copied_off == warm + copied > 0
+    assert warm > copied  # the victim side moved only a minority of the recalled blocks
+    for e in engs:
+        e.check_state()
+
+
+@pytest.mark.parametrize("recall_mode", [1, 0])
+def test_engine_tier_back_to_back_steps_with_recalls(cuda, recall_mode):
     """Steps queued back to back (no host sync), a recall every step: the
-    copy-engine recalls (issuer thread) must never sit behind the next step's
-    work that waits for them (a K2 flag wait would trap after 10 s)."""
+    recall copies (SM gather, or the copy engines from the issuer thread) must
+    never sit behind the next step's work that waits for them (a K2 flag wait
+    would trap after 10 s)."""
     L, batch, hkv, G, k, cap, nbs = 4, 2, 2, 4, 6, 8, 32
     U = batch * hkv
     kv = torch.bfloat16
@@ -257,7 +303,7 @@ def test_engine_tier_back_to_back_steps_with_recalls(cuda):
     layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
     eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
                        kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=1,
-                       host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16)
+                       host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, recall_mode=recall_mode)
     qs = [torch.randn(L, U * G, D, device="cuda").bfloat16() for _ in range(4)]
     cpu_o = torch.randn(L, U * G, D, device="cuda")
     cpu_ml = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()

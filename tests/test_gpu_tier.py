@@ -146,15 +146,64 @@ def test_tier_random_ops_vs_reference(cuda, seed):
             dev.err[layer].zero_()
             _compare(dev, refs, L)
     # slot bookkeeping: fast / in-flight blocks hold distinct slots of their own
-    # range, and with the free stack they account for every slot exactly once
-    tab, nf, fs = dev.table.cpu().numpy(), dev.n_free.cpu().numpy(), dev.free_slots.cpu().numpy()
+    # range, and with the free ring they account for every slot exactly once
+    _check_slots(dev, L, U, nbs)
+
+
+def _check_slots(dev, L, U, nbs):
+    tab = dev.table.cpu().numpy()
+    tier, warm, owner = dev.tier.cpu().numpy(), dev.warm.cpu().numpy(), dev.free_owner.cpu().numpy()
+    head, nf = dev.free_head.cpu().numpy(), dev.n_free.cpu().numpy()
     for layer in range(L):
         for u in range(U):
             nb = (int(dev.n_tokens[layer, u]) + BS - 1) // BS
             used = tab[layer, u, :nb][tab[layer, u, :nb] >= 0].tolist()
-            free = fs[layer, u, :nf[layer, u]].tolist()
-            base = (layer * U + u) * nbs
-            assert sorted(used + free) == list(range(base, base + nbs))
+            free = dev.free_ring(layer, u)
+            base = dev.layer_base[layer] + u * dev.spu_l[layer]
+            assert sorted(used + free) == list(range(base, base + dev.spu_l[layer]))
+            # victim cache: a warm block is slow, and its ring entry names it
+            pos = {(int(head[layer, u]) + i) % dev.spu for i in range(int(nf[layer, u]))}
+            for b in np.nonzero(warm[layer, u] >= 0)[0].tolist():
+                p = int(warm[layer, u, b])
+                assert p in pos and owner[layer, u, p] == b and tier[layer, u, b] == 0 and tab[layer, u, b] < 0
+
+
+def test_tier_victim_cache_warm_recall(cuda):
+    """Device victim cache: an evicted block's slot keeps its image at the
+    back of the FIFO free ring; recalling the block takes the same slot back
+    with nothing to copy (dst = -2 - slot). The tier state stays the
+    reference's after every operation."""
+    dev = DeviceTieredCache(1, 1, 16, capacity=2, slots_per_unit=4)
+    ref = P.RefCache(1, 1, 2)
+    for _ in range(3 * BS):  # blocks 0, 1, 2 take slots 0, 1, 2; sealing 2 evicts 0 (LRU tie -> lower id)
+        _append_all(dev, [ref], 0)
+    _compare(dev, [ref], 1)
+    assert dev.tier[0, 0, :3].tolist() == [0, 1, 1]
+    assert int(dev.warm[0, 0, 0]) >= 0 and dev.free_ring(0, 0) == [3, 0]
+    dst = dev.schedule_recall(0, *_ids([[0]], 1), 0, 0)
+    ref.schedule_recall(0, [0], 0, 0)
+    assert int(dst[0, 0]) == -2 - 0  # warm: its own slot, no bytes to move
+    assert int(dev.table[0, 0, 0]) == 0 and int(dev.warm[0, 0, 0]) == -1 and dev.free_ring(0, 0) == [3]
+    _compare(dev, [ref], 1)
+    _check_slots(dev, 1, 1, 16)
+
+
+def test_tier_victim_cache_reused_slot_is_a_miss(cuda):
+    """A warm image is forgotten when the ring hands its slot out again: the
+    recall then gets the oldest free slot (dst >= 0, an H2D copy)."""
+    dev = DeviceTieredCache(1, 1, 16, capacity=2, slots_per_unit=4)
+    ref = P.RefCache(1, 1, 2)
+    for _ in range(4 * BS + 1):  # ring after: block 3 took slot 3, its seal evicted 1; block 4 took slot 0
+        _append_all(dev, [ref], 0)
+    _compare(dev, [ref], 1)
+    assert dev.tier[0, 0, :5].tolist() == [0, 0, 1, 1, 1]
+    assert int(dev.warm[0, 0, 0]) == -1 and int(dev.warm[0, 0, 1]) >= 0 and dev.free_ring(0, 0) == [1]
+    dst = dev.schedule_recall(0, *_ids([[0]], 1), 0, 0)
+    ref.schedule_recall(0, [0], 0, 0)
+    assert int(dst[0, 0]) == 1  # block 1's slot, whose image is now forgotten
+    assert int(dev.warm[0, 0, 1]) == -1 and dev.free_ring(0, 0) == []
+    _compare(dev, [ref], 1)
+    _check_slots(dev, 1, 1, 16)
 
 
 def test_tier_place_after_prefill_vs_reference(cuda):

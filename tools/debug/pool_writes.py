@@ -19,7 +19,7 @@ L, U = wl.L, wl.U
 # duplicate slots across the fast/in-flight tables and free stacks?
 for l in range(L):
     used = tr.table[l][tr.table[l] >= 0]
-    free = torch.cat([tr.free_slots[l, u, :int(tr.n_free[l, u])] for u in range(U)])
+    free = torch.tensor([x for u in range(U) for x in tr.free_ring(l, u)], dtype=torch.int32, device=used.device)
     both = torch.cat([used, free])
     if both.unique().numel() != both.numel():
         print("layer", l, "duplicate slots: table", used.numel(), "free", free.numel(), "unique", both.unique().numel())

@@ -2,8 +2,9 @@
 // block images (bf16 K+V of one 64-token block) move from pinned host memory
 // into scattered pool slots?
 //   (a) one contiguous cudaMemcpyAsync (the link's ceiling)
-//   (b) cudaMemcpyBatchAsync of n scattered 32 KiB copies (one call, and in
-//       per-layer calls)
+//   (b') one cudaMemcpyAsync per scattered 32 KiB copy
+//   (the batched-copy driver API measured in round 2a is closed on this GPU
+//   pool and was removed from this file)
 //   (c) an SM gather kernel over the mapped host pointer (zero-copy loads),
 //       various grid sizes and load depths
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o pcie_recall pcie_recall.cu
@@ -97,28 +98,6 @@ int main(int argc, char** argv) {
     for (int i = 0; i < n; ++i) {
         ds[i] = pool + static_cast<size_t>(dst[i]) * SB;
         ss[i] = host + src[i] * SB;
-    }
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t ai = 0, fail = 0;
-    for (int r = 0; r < 2; ++r) {
-        cudaEventRecord(a, st);
-        CK(cudaMemcpyBatchAsync(ds.data(), ss.data(), sz.data(), n, &attr, &ai, 1, &fail, st));
-        cudaEventRecord(b, st);
-    }
-    report("(b) cudaMemcpyBatchAsync, one call");
-    for (int per : {750, 3000}) {
-        for (int r = 0; r < 2; ++r) {
-            cudaEventRecord(a, st);
-            for (int o = 0; o < n; o += per) {
-                const int m = std::min(per, n - o);
-                CK(cudaMemcpyBatchAsync(ds.data() + o, ss.data() + o, sz.data() + o, m, &attr, &ai, 1, &fail, st));
-            }
-            cudaEventRecord(b, st);
-        }
-        char nm[96];
-        snprintf(nm, sizeof nm, "(b) cudaMemcpyBatchAsync, %d per call", per);
-        report(nm);
     }
     for (int r = 0; r < 2; ++r) {
         cudaEventRecord(a, st);
