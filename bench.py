@@ -1290,14 +1290,14 @@ def run_e2e(wl, steps, dev, ws, global_batch, tier_mode, step0):
                     "pre-staged" % ("kv_host" if tier_mode else "host")}
 
 
-def run_e2e_worker(wl, steps, dev, ws, global_batch, step0):
+def run_e2e_worker(wl, steps, dev, ws, global_batch, step0, threads=0, chunk_layers=4):
     """The composed step (device tier mode, host buffers): the engine's own CPU
     worker computes each layer's CPU partial during the step from the ids K1
     selected in that step and the step's predicted queries, publishing layer
     chunks that the running K2 merges (engine.hpp:236-273). Nothing is
     pre-staged: the step waits for the host's CPU share."""
     L = wl.L
-    eng = wl.make_engine(cpu_worker=True, chunk_layers=4)
+    eng = wl.make_engine(cpu_worker=True, chunk_layers=chunk_layers, cpu_threads=threads)
     n, h_qt, h_qp, h_kv = _pinned_inputs(wl, True)
     h_out = torch.empty(wl.out_o.shape, dtype=torch.float32).pin_memory()
     h_oml = torch.empty(wl.out_ml.shape, dtype=torch.float32).pin_memory()
@@ -1326,7 +1326,7 @@ def run_e2e_worker(wl, steps, dev, ws, global_batch, step0):
     d2h_bytes = sum(x.numel() * x.element_size() for x in (h_out, h_oml)) + L * wl.U * (wl.k + 1) * 4
     out = {"value": global_batch / (ms / 1000.0), "unit": "tokens/s", "ms_per_step": ms, "steps": steps,
            "cpu_worker_ms_per_step": cpu_ms / max(nsteps, 1), "cpu_blocks_last_step": cpu_blocks,
-           "threads": os.cpu_count(), "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
+           "threads": threads or os.cpu_count(), "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": d2h_bytes,
            "verified_by": "tests/test_gpu_engine_worker.py (every (step, layer, unit) against the reference's "
                           "recompute_layer_attention, harness.hpp:318-329)",
            "path": "C ABI scout_engine_decode_step_kv_host with cfg.cpu_worker (csrc/engine.cpp + cpu_coattn.cpp): "

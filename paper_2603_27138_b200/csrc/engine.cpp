@@ -669,8 +669,18 @@ struct scout_engine {
                 a.o_dtype = cfg.cpu_dtype;
                 a.ml = cw_ml(par) + lo * md;
                 a.threads = cfg.cpu_threads;
+                const auto t1 = std::chrono::steady_clock::now();
                 rc = scout_cpu_coattn_run(a);
-                ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+                const auto t2 = std::chrono::steady_clock::now();
+                ms += std::chrono::duration<double, std::milli>(t2 - t0).count();
+                static const bool cwprof = getenv("SCOUT_CW_PROF") != nullptr;
+                if (cwprof) {
+                    long long nbk = 0;
+                    for (int i = 0; i < n * U; ++i) nbk += nn[lu(lo) + i];
+                    fprintf(stderr, "[cw] step token %u chunk %d: %d units, %lld blocks, index %.3f ms, run %.3f ms\n",
+                            job.token, c, n * U, nbk, std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                            std::chrono::duration<double, std::milli>(t2 - t1).count());
+                }
             }
             if (cudaMemcpyAsync(g.co + lo * qd * cbytes(), cw_o(par) + lo * qd * cbytes(), n * qd * cbytes(),
                                 cudaMemcpyHostToDevice, cw_s) != cudaSuccess ||
