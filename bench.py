@@ -1204,12 +1204,12 @@ def run_c_abi_f32(args, cfg, ws, rank, gb):
         print(json.dumps(line), flush=True)
 
 
-def run_layerwise(wl, steps, dev, ws, step0):
+def run_layerwise(wl, steps, dev, ws, step0, **engine_kw):
     """The step as a decoder drives it: one scout_engine_decode_layer call per
     layer, layer i's queries written into the live query buffers by a copy
     queued after layer i-1's call (in a model they come from layer i-1's
     output, so nothing of layer i can start earlier)."""
-    eng = wl.make_engine()
+    eng = wl.make_engine(**engine_kw)
     L = wl.L
     qt_live = torch.empty_like(wl.q_path_t[0])
     qp_live = torch.empty_like(wl.q_path_p[0])
