@@ -342,9 +342,10 @@ class TierWorkload:
 class StaticWorkload:
     """--tier static: the kernel view. Residency fixed at the paper's 8.2% CPU
     share (all but round(8.2% k) of each unit's selected blocks resident,
-    filled to capacity), no appends; the recall plans move their bytes on the
-    copy engines but flip no tiers. Same synthetic data kinds as TierWorkload
-    (one generator per rank)."""
+    filled to capacity), no appends; the recall plans (one contiguous run of
+    host images per unit) move their bytes on the copy engines, layer by layer
+    in the staggered cadence, as synthetic PCIe load, but flip no tiers. Same
+    synthetic data kinds as TierWorkload (one generator per rank)."""
 
     def __init__(self, cfg, dev, seed):
         from paper_2603_27138_b200 import ops
@@ -414,7 +415,9 @@ class StaticWorkload:
             table.scatter_(1, keep, slots.to(torch.int32))
             nrc = min(cpu_per_unit, head)
             dst = base + torch.arange(U, device=dev)[:, None] * (cap + head) + cap + torch.arange(nrc, device=dev)[None]
-            src = (cpu_ids[:, :nrc] * 2654435761 + li * 97 + torch.arange(U, device=dev)[:, None] * 31) % host_blocks
+            # each unit's plan is one contiguous run of host images (one copy-engine call)
+            run0 = ((li * U + torch.arange(U, device=dev)[:, None]) * 2654435761) % (host_blocks - nrc)
+            src = run0 + torch.arange(nrc, device=dev)[None]
             layers.append(LayerState(dig, table, src.reshape(-1).to(torch.int64).cpu().contiguous(),
                                      dst.reshape(-1).to(torch.int32).cpu().contiguous()))
         self.layer_states = layers
@@ -422,7 +425,8 @@ class StaticWorkload:
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
                                    recall_interval=cfg["recall"], host_tier=self.host_tier, host_staging=True,
                                    q_dtype=cfg["q_dtype"], cpu_dtype=cfg.get("cpu_dtype", torch.float32),
-                                   recall_stagger=cfg.get("recall_policy") == "stagger")
+                                   recall_stagger=cfg.get("static_recall_policy", "stagger") == "stagger",
+                                   recall_mode=0)
         self.cpu_per_unit = cpu_per_unit
         self.digest_bytes_layer = U * 2 * D * nb * 2
         self.k_new = self.v_new = None
@@ -1080,7 +1084,9 @@ def main():
                        "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "cpu_partial_dtype": args.cpu_dtype,
                        "gpu_cache_blocks_per_unit": cfg["capacity"],
                        "cpu_blocks_per_unit_at_placement": cpu_per_unit, "recall_every": cfg["recall"],
-                       "recall_policy": args.recall_policy, "tier": args.tier,
+                       "recall_policy": args.recall_policy if tier_mode else "stagger (the static view's synthetic "
+                                                                            "recall load, copy engines)",
+                       "tier": args.tier,
                        "parallelism": f"request-sharded x{ws}, no collective",
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},
             "step_gbs": step_gbs,
