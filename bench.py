@@ -342,10 +342,9 @@ class TierWorkload:
 class StaticWorkload:
     """--tier static: the kernel view. Residency fixed at the paper's 8.2% CPU
     share (all but round(8.2% k) of each unit's selected blocks resident,
-    filled to capacity), no appends; the recall plans (one contiguous run of
-    host images per unit) move their bytes on the copy engines, layer by layer
-    in the staggered cadence, as synthetic PCIe load, but flip no tiers. Same
-    synthetic data kinds as TierWorkload (one generator per rank)."""
+    filled to capacity), no appends, no recalls: K1 + K2 over a fixed split,
+    the kernel view of the metric (the device tier mode carries the recall).
+    Same synthetic data kinds as TierWorkload (one generator per rank)."""
 
     def __init__(self, cfg, dev, seed):
         from paper_2603_27138_b200 import ops
@@ -423,7 +422,7 @@ class StaticWorkload:
         self.layer_states = layers
         self.engine = DecodeEngine(layers=L, batch=B, hq=hq, hkv=hkv, k=k, n_tokens=self.n_tokens, pool=pool,
                                    kv_dtype=kv_dt, layer_states=layers, scale=1.0 / math.sqrt(D),
-                                   recall_interval=cfg["recall"], host_tier=self.host_tier, host_staging=True,
+                                   recall_interval=0, host_tier=self.host_tier, host_staging=True,
                                    q_dtype=cfg["q_dtype"], cpu_dtype=cfg.get("cpu_dtype", torch.float32),
                                    recall_stagger=cfg.get("static_recall_policy", "stagger") == "stagger",
                                    recall_mode=0)
@@ -1084,8 +1083,7 @@ def main():
                        "block": BS, "top_k": cfg["k"], "q_dtype": args.q_dtype, "cpu_partial_dtype": args.cpu_dtype,
                        "gpu_cache_blocks_per_unit": cfg["capacity"],
                        "cpu_blocks_per_unit_at_placement": cpu_per_unit, "recall_every": cfg["recall"],
-                       "recall_policy": args.recall_policy if tier_mode else "stagger (the static view's synthetic "
-                                                                            "recall load, copy engines)",
+                       "recall_policy": args.recall_policy if tier_mode else "none (static view: fixed residency)",
                        "tier": args.tier,
                        "parallelism": f"request-sharded x{ws}, no collective",
                        "l2": "inputs larger than L2 (step working set %.1f GiB)" % (step_bytes / 2**30)},

@@ -34,21 +34,3 @@ e1.record(); torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / N * 1000
 byts = U * per * 64 * 2 * 128 * 2
 print(f"K2 {us:.1f} us/launch, {byts / us / 1e3:.0f} GB/s")
-if os.environ.get("SCOUT_B200_LIB"):
-    import ctypes
-    from paper_2603_27138_b200 import _capi
-    L_ = _capi.lib()
-    buf = (ctypes.c_ulonglong * (1024 * 6))()
-    # one more single launch, then read the per-CTA phase stamps
-    s, d = args[0]
-    e0.record()
-    ops.sparse_decode(q, pool, torch.bfloat16, s, d, n_res, n_tok, G, o=o, ml=ml, workspace=ws)
-    e1.record(); torch.cuda.synchronize()
-    print("single launch event time (us):", e0.elapsed_time(e1) * 1000)
-    L_.scout_debug_k2_times(buf)
-    ts = np.array(buf, dtype=np.float64).reshape(1024, 6)[:148]
-    t0 = ts[:, 0].min()
-    rel = (ts - t0) / 1000.0
-    names = ["start", "prologue done", "first data", "last seg computed", "segments done", "end"]
-    for i, n in enumerate(names):
-        print(f"{n:20s} min {rel[:, i].min():7.2f} med {np.median(rel[:, i]):7.2f} max {rel[:, i].max():7.2f} us")
