@@ -57,6 +57,13 @@ struct Mat {
     Mat() = default;
     Mat(std::size_t r, std::size_t c) : rows(r), cols(c), data(r * c, 0.0) {}
     const double* row(std::size_t r) const { return data.data() + r * cols; }
+    Vec row_vec(std::size_t r) const { return Vec(row(r), row(r) + cols); }
+    void append_row(const Vec& v) {
+        if (rows == 0 && cols == 0) cols = v.size();
+        if (v.size() != cols) throw std::invalid_argument("Mat::append_row: width mismatch");
+        data.insert(data.end(), v.begin(), v.end());
+        ++rows;
+    }
 };
 struct BlockDigest {
     DigestMethod method = DigestMethod::minmax;

@@ -67,9 +67,11 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
 
 def build_oracle(verbose: bool = False) -> None:
     """Build the CPU checkers under oracle/ (test infrastructure, not the product)
-    and, where the reference headers exist, the drop-in proof binary
+    and, where the reference headers exist, the drop-in proof binaries
     tests/cpp/_bin/test_dropin_engine (the reference engine with the
-    INTEGRATION.md §1 call swaps, linked to libscout_b200.so)."""
+    INTEGRATION.md §1 call swaps, linked to libscout_b200.so) and
+    tests/cpp/_bin/test_tier_cache (the C++ TieredKvCache drop-in beside the
+    reference's)."""
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True,
                    stdout=None if verbose else subprocess.DEVNULL)
     subprocess.run(["make", "-s", "-C", str(ROOT / "tests" / "cpp")], check=True,
