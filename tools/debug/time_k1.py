@@ -3,14 +3,16 @@ import ctypes as C, sys, os
 sys.path[:0] = ["."]
 import torch
 from paper_2603_27138_b200 import _capi as A, ops
-L, U, G, nb, k = 64, 256, 8, 512, 64
+L, U, G, k = 64, 256, 8, 64
+nb = int(os.environ.get("NBS", "512"))  # digest stride (tier mode: 520, room for appended blocks)
+ntok = int(os.environ.get("NTOK", str(512 * 64)))  # tokens per unit (tier mode: 513 blocks, the last one open)
 dev = torch.device("cuda")
 digs = [torch.randn(U, 2, 128, nb, device=dev).to(torch.bfloat16) for _ in range(L)]
 for d in digs:
     lo, hi = torch.minimum(d[:, 0], d[:, 1]), torch.maximum(d[:, 0], d[:, 1])
     d[:, 0], d[:, 1] = lo, hi
 q = torch.randn(L, U * G, 128, device=dev)
-nt = torch.full((U,), nb * 64, dtype=torch.int32, device=dev)
+nt = torch.full((U,), ntok, dtype=torch.int32, device=dev)
 tab = torch.randint(-1, 10**6, (L, U, nb), dtype=torch.int32, device=dev)
 outs = {n: torch.empty(L, U, k, dtype=torch.int32, device=dev) for n in ("sel", "rs", "ri", "ci")}
 cnts = {n: torch.empty(L, U, dtype=torch.int32, device=dev) for n in ("ns", "nr", "nc", "rt", "ct")}
@@ -36,4 +38,5 @@ for f, name in ((batch, "batch"), (single, "64 singles")):
     for _ in range(10): f()
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    print(f"K1 {name}: {ms:.3f} ms per 64 layers, {L * U * 2 * 128 * nb * 2 / ms / 1e6:.0f} GB/s digests")
+    live = (ntok + 63) // 64
+    print(f"K1 {name}: {ms:.3f} ms per 64 layers, {L * U * 2 * 128 * live * 2 / ms / 1e6:.0f} GB/s of live digests")
