@@ -439,21 +439,37 @@ class StaticWorkload:
         return res_tokens_total * 2 * D * 2 + UG * (D * qb + (D * cb + 8) + (D + 2) * 4)
 
 
+# Test hooks for the N > 1 plumbing on a 1-GPU box: SCOUT_DIST_BACKEND=gloo
+# (collectives on host tensors) and SCOUT_BENCH_ONE_GPU=1 (every rank on cuda:0).
+# The product runs NCCL, one rank per GPU.
+BACKEND = os.environ.get("SCOUT_DIST_BACKEND", "nccl")
+
+
 def dist_setup():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("SCOUT_BENCH_ONE_GPU") == "1":
+        local = 0
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(BACKEND)
     return ws, rank, local
+
+
+def coll_dev(dev):
+    """Where collective tensors live: the GPU under NCCL, the host under gloo."""
+    return dev if BACKEND == "nccl" else torch.device("cpu")
 
 
 def max_over_ranks(x, ws, dev):
     from paper_2603_27138_b200.sharding import max_over_ranks as m
 
-    return m(x, dev) if ws > 1 else x
+    return m(x, coll_dev(dev)) if ws > 1 else x
 
 
 def barrier(ws):
@@ -617,7 +633,7 @@ def output_sums(wl, gb, ws, rank):
 
     per = wl.hkv * wl.G
     mine = wl.out_o.view(wl.L, wl.B, per, D).double().sum(dim=(0, 2, 3))  # [B]
-    return gather_per_request(mine, gb, ws, rank).cpu() if ws > 1 else mine.cpu()
+    return gather_per_request(mine.to(coll_dev(mine.device)), gb, ws, rank).cpu() if ws > 1 else mine.cpu()
 
 
 def cross_rank_replay(cfg, args, ws, rank, dev, steps_done, seed, gb, allsum, warm, vc):
@@ -864,7 +880,7 @@ def main():
         warm = args.warm_slots if args.warm_slots >= 0 else (
             TierWorkload.auto_warm_slots(cfg, cfg["batch"], args.max_steps, dev) if vc else 0)
         if ws > 1:  # every rank the same (the smallest shard's budget decides)
-            t = torch.tensor([warm], dtype=torch.int64, device=dev)
+            t = torch.tensor([warm], dtype=torch.int64, device=coll_dev(dev))
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
             warm = int(t)
         wl = TierWorkload(cfg, dev, seed=args.seed, max_steps=args.max_steps,

@@ -446,7 +446,7 @@ typedef struct scout_engine_config {
     int gpu_side_policy;
     /* layer-by-layer mode (scout_engine_decode_layer): K2 CTAs of a
      * single-layer launch; the SMs it leaves free run K1 of the next layer
-     * beside it. 0: automatic (the grid less 28), < 0: the whole grid. */
+     * beside it. 0: automatic (the grid less 68), < 0: the whole grid. */
     int layer_ctas;
     /* Device tier mode: the host tier's unit index space when it is shared by
      * several engines (request-sharded ranks): block (layer, unit u, id) of

@@ -242,8 +242,10 @@ struct scout_engine {
     long long lw_calls = 0;
     // K2 CTAs of a single-layer launch (cfg.layer_ctas; SCOUT_LW_K2_CTAS
     // overrides): 0 = automatic, the grid less LW_FREE_SMS for K1 of the next
-    // layer (measured: 148 CTAs 13.9 ms per 64-layer step, 120 12.3 ms)
-    static constexpr int LW_FREE_SMS = 28;
+    // layer (measured per 64-layer step: 148 CTAs 13.9 ms, 120 12.3 ms before
+    // the victim cache; after it 148 10.9, 120 10.0, 96 9.1-9.4, 80 8.94-8.99,
+    // 72 8.97-8.99, 64 9.2: profiles/r02m_lw_ctas.txt)
+    static constexpr int LW_FREE_SMS = 68;
     int layer_ctas() const {
         static const int env = [] {
             const char* s = getenv("SCOUT_LW_K2_CTAS");
