@@ -121,13 +121,28 @@ __device__ int block_exclusive_scan(int v, int* warp_tot, int* total) {
 template <typename DigT, int G>
 __device__ __forceinline__ double exact_score_minmax(const DigT* lo, const DigT* hi, size_t ns, int b,
                                                      const double* qs) {
+    // the chain is sequential, its operands are not: each chunk's 2 x XC
+    // digest words are loaded together, so the chain waits on memory once
+    // per chunk instead of once per channel (the rare exact path of a near
+    // tie was ~30 us per block, the straggler of a single-layer launch)
+    constexpr int XC = 8;
     double acc = 0.0;
-    for (int c = 0; c < D; ++c) {
-        const double l = widen(lo[c * ns + b]), h = widen(hi[c * ns + b]);
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += XC) {
+        DigT L[XC], H[XC];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            const double qv = qs[c * G + g];
-            acc = fma(qv, qv >= 0.0 ? h : l, acc);
+        for (int i = 0; i < XC; ++i) {
+            L[i] = lo[(c0 + i) * ns + b];
+            H[i] = hi[(c0 + i) * ns + b];
+        }
+#pragma unroll
+        for (int i = 0; i < XC; ++i) {
+            const double l = widen(L[i]), h = widen(H[i]);
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const double qv = qs[(c0 + i) * G + g];
+                acc = fma(qv, qv >= 0.0 ? h : l, acc);
+            }
         }
     }
     return acc;
@@ -436,6 +451,7 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (NA == 1 ? 4 : (QPT == 1 
     __shared__ int warp_tot[K1_WARPS];
     __shared__ int s_tok[2];
     __shared__ int s_cnt[2];
+    __shared__ int s_cnt2[2];
     __shared__ float s_amax;
 
     const int tid = threadIdx.x;
@@ -677,15 +693,71 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (NA == 1 ? 4 : (QPT == 1 
         if (nin) atomicAdd(&s_cnt[0], nin);
         if (nz) atomicAdd(&s_cnt[1], nz);
         __syncthreads();
-        const int need = k - s_cnt[0];
+        int need = k - s_cnt[0];
         if (s_cnt[1] > need) {
-            // genuinely ambiguous boundary: exact reference-order scores for Z
-            for (int b = tid; b < nb; b += K1_THREADS)
-                if (cls[b] == CLS_Z) keys[b] = score_key(exact_score_minmax<DigT, G>(lo, hi, ns, b, qs));
+            // stage 2: f64 scores of the Z blocks, one warp per block (lane
+            // partial sums of 32 exact products + a 5-level butterfly): within
+            // 37 u A < 2^-47 A of the exact sum, so within 2^-42 A of the
+            // reference's sequential sum (1023 u A). The fp32 band's near-ties
+            // mostly resolve here; only blocks inside the 2^-40 A band go on
+            // to the sequential exact chain.
+            {
+                const int lane = tid & 31, warp = tid >> 5;
+                int zi = 0;  // Z blocks in id order, dealt round-robin to the warps
+                for (int base = 0; base < nb; base += 32) {
+                    const int b = base + lane;
+                    unsigned m = __ballot_sync(0xffffffffu, b < nb && cls[b] == CLS_Z);
+                    while (m) {
+                        const int j = base + __ffs(m) - 1;
+                        m &= m - 1;
+                        if (zi++ % K1_WARPS != warp) continue;
+                        double acc = 0.0;
+#pragma unroll
+                        for (int i = 0; i < D / 32; ++i) {
+                            const int c = lane + 32 * i;
+                            const double l = widen(lo[c * ns + j]), h = widen(hi[c * ns + j]);
+#pragma unroll
+                            for (int g = 0; g < G; ++g) {
+                                const double qv = qs[c * G + g];
+                                acc = fma(qv, qv >= 0.0 ? h : l, acc);
+                            }
+                        }
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                        if (lane == 0) keys[j] = score_key(acc);
+                    }
+                }
+            }
+            if (tid < 2) s_cnt2[tid] = 0;
             __syncthreads();
-            radix_kth(nb, need, [&](int b) { return keys[b]; }, [&](int b) { return cls[b] == CLS_Z; }, S, thr,
-                      need_eq);
-            z_exact = true;
+            uint64_t tkey2;
+            int dummy2;
+            radix_kth(nb, need, [&](int b) { return keys[b]; }, [&](int b) { return cls[b] == CLS_Z; }, S, tkey2,
+                      dummy2);
+            const double T2 = key_to_double(tkey2);
+            const double band2 = static_cast<double>(s_amax) * 0x1p-40;
+            int nin2 = 0, nz2 = 0;
+            for (int b = tid; b < nb; b += K1_THREADS) {
+                if (cls[b] != CLS_Z) continue;
+                const double v = key_to_double(keys[b]);
+                const uint8_t c = v > T2 + band2 ? CLS_IN : (v < T2 - band2 ? CLS_OUT : CLS_Z);
+                cls[b] = c;
+                nin2 += c == CLS_IN;
+                nz2 += c == CLS_Z;
+            }
+            if (nin2) atomicAdd(&s_cnt2[0], nin2);
+            if (nz2) atomicAdd(&s_cnt2[1], nz2);
+            __syncthreads();
+            need -= s_cnt2[0];
+            if (s_cnt2[1] > need) {
+                // genuinely ambiguous boundary: exact reference-order scores for Z
+                for (int b = tid; b < nb; b += K1_THREADS)
+                    if (cls[b] == CLS_Z) keys[b] = score_key(exact_score_minmax<DigT, G>(lo, hi, ns, b, qs));
+                __syncthreads();
+                radix_kth(nb, need, [&](int b) { return keys[b]; }, [&](int b) { return cls[b] == CLS_Z; }, S, thr,
+                          need_eq);
+                z_exact = true;
+            }
         }
     }
     __syncthreads();
