@@ -136,12 +136,14 @@ class TierWorkload:
     the tokens' new K/V. The initial placement keeps each unit's selected
     blocks minus the CPU share (the paper's 8.2%) resident, filled to capacity."""
 
-    def __init__(self, cfg, dev, seed, max_steps, requests, warm_slots=0, victim_cache=True, host_units=0):
+    def __init__(self, cfg, dev, seed, max_steps, requests, warm_slots=0, victim_cache=True, host_units=0,
+                 warm_seed=True):
         """requests: a contiguous range of global request ids (this rank's
         shard). warm_slots: pool slots per (layer, unit) beyond capacity + the
         open block + one in-flight ticket; they start with the warm images of
         the next-best blocks by the placement query (the victim cache, see
-        scout_tier_layer) and keep evicted blocks' images later. host_units:
+        scout_tier_layer) and keep evicted blocks' images later (warm_seed=False:
+        they start empty and fill only with evictions). host_units:
         units of the global workload (the host tier's index space, shared by
         every rank's shard; 0 = this shard's)."""
         from paper_2603_27138_b200 import ops
@@ -162,7 +164,7 @@ class TierWorkload:
         self.host_units, self.host_unit0 = int(host_units) or U, self.requests[0] * hkv
         kv_dt = torch.bfloat16
         W = max(0, min(int(warm_slots), nb - cap)) if victim_cache else 0
-        self.warm_slots, self.victim_cache = W, bool(victim_cache)
+        self.warm_slots, self.victim_cache, self.warm_seed = W, bool(victim_cache), bool(warm_seed)
         # pool slots per (layer, unit): every block for the pinned layer 0; else the
         # capacity's sealed fast blocks + the open block + one recall ticket in
         # flight (at most k blocks: predicted \ residency), so a unit can never
@@ -253,7 +255,7 @@ class TierWorkload:
                 keep = score.argsort(dim=1, descending=True)[:, :cap]
                 table = torch.full((U, nbs), -1, dtype=torch.int32, device=dev)
                 table.scatter_(1, keep, (base + torch.arange(cap, device=dev, dtype=torch.int32)[None]).to(torch.int32))
-                if W > 0:
+                if W > 0 and warm_seed:
                     # warm images: the W best slow sealed blocks by the placement query's
                     # stacked digest score (what a prefill that ends with the whole KV in
                     # HBM can leave behind), in the slots after the fast ones; the worst
@@ -636,7 +638,7 @@ def output_sums(wl, gb, ws, rank):
     return gather_per_request(mine.to(coll_dev(mine.device)), gb, ws, rank).cpu() if ws > 1 else mine.cpu()
 
 
-def cross_rank_replay(cfg, args, ws, rank, dev, steps_done, seed, gb, allsum, warm, vc):
+def cross_rank_replay(cfg, args, ws, rank, dev, steps_done, seed, gb, allsum, warm, vc, warm_seed=True):
     """N > 1, after everything else (rank 0 has freed its own workload): rank 0
     rebuilds the LAST rank's shard of the global workload (same requests, same
     host-tier index space, same warm slots), replays steps 1..steps_done
@@ -648,7 +650,7 @@ def cross_rank_replay(cfg, args, ws, rank, dev, steps_done, seed, gb, allsum, wa
     if rank == 0:
         first, n = request_shard(gb, ws, ws - 1)
         sub = TierWorkload(cfg, dev, seed, max_steps=args.max_steps, requests=range(first, first + n),
-                           warm_slots=warm, victim_cache=vc, host_units=gb * cfg["hkv"])
+                           warm_slots=warm, victim_cache=vc, host_units=gb * cfg["hkv"], warm_seed=warm_seed)
         sub.make_engine()
         for s_ in range(1, steps_done + 1):
             sub.step(s_)
@@ -839,6 +841,9 @@ def main():
                          "victim cache); -1 (default): fill the HBM left after the rest of the workload")
     ap.add_argument("--victim-cache", default="on", choices=["on", "off"],
                     help="off: every recall copies its blocks from the host tier (no warm images)")
+    ap.add_argument("--warm-seed", default="on", choices=["on", "off"],
+                    help="off: the warm slots start empty (no images left by the placement); only evicted "
+                         "blocks' images fill them")
     ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
                     help="query dtype (q_true / q_pred); bf16 = the model's projection output")
     ap.add_argument("--cpu-dtype", default="bf16", choices=["bf16", "f32"],
@@ -885,7 +890,7 @@ def main():
             warm = int(t)
         wl = TierWorkload(cfg, dev, seed=args.seed, max_steps=args.max_steps,
                           requests=range(first, first + cfg["batch"]), warm_slots=warm, victim_cache=vc,
-                          host_units=gb * cfg["hkv"])
+                          host_units=gb * cfg["hkv"], warm_seed=args.warm_seed == "on")
         wl.make_engine()
     else:
         wl = StaticWorkload(cfg, dev, seed=args.seed + rank)
@@ -947,6 +952,7 @@ def main():
                                 "h2d_bytes_per_step": rc_copy * 32768 / args.steps,
                                 "warm_frac": rc_warm / max(rc_warm + rc_copy, 1),
                                 "victim_cache": wl.victim_cache, "warm_slots_per_unit": wl.warm_slots,
+                                "warm_seeded_at_placement": wl.warm_seed,
                                 "warm_images_at_placement": wl.warm_blocks,
                                 "pool_gib": wl.pool.numel() / 2**30,
                                 "note": "a recalled block whose image still sits in a free pool slot (evicted "
@@ -1077,7 +1083,7 @@ def main():
         cpu_worker = measure_cpu_worker(wl, cfg)
     cpu_per_unit = wl.cpu_per_unit
     if allsum is not None:  # N > 1: rank 0 replays the last rank's shard alone (its own workload freed first)
-        vc_, warm_ = wl.victim_cache, wl.warm_slots
+        vc_, warm_, seed_ = wl.victim_cache, wl.warm_slots, wl.warm_seed
         wl.engine.close()
         wl = eng = None
         import gc
@@ -1085,7 +1091,7 @@ def main():
         gc.collect()
         torch.cuda.empty_cache()
         verify["cross_rank"] = cross_rank_replay(cfg, args, ws, rank, dev, verify_step_no, args.seed, gb, allsum,
-                                                 warm_, vc_)
+                                                 warm_, vc_, seed_)
     if rank == 0:
         line = {
             "metric": METRIC, "value": tok_s, "unit": "tokens/s", "n_gpus": ws, "steps": args.steps,

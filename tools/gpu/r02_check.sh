@@ -16,6 +16,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 2 > $OUT/bench_r
 # sweep (BASELINE configs; the f32 query / partial line; the stagger cadence; the kernel view)
 timeout 600 python bench.py --recall-policy stagger --no-cpu-baseline > $OUT/sweep_stagger_$TAG.json 2> $OUT/sweep_stagger_$TAG.err
 timeout 600 python bench.py --victim-cache off --no-extras --no-cpu-baseline > $OUT/sweep_novictim_$TAG.json 2> $OUT/sweep_novictim_$TAG.err
+timeout 600 python bench.py --warm-seed off --no-extras --no-cpu-baseline > $OUT/sweep_noseed_$TAG.json 2> $OUT/sweep_noseed_$TAG.err
 timeout 600 python bench.py --q-dtype f32 --cpu-dtype f32 --no-extras --no-cpu-baseline > $OUT/sweep_f32_$TAG.json 2> $OUT/sweep_f32_$TAG.err
 timeout 600 python bench.py --config qwen3-8b-16k --no-cpu-baseline > $OUT/sweep_cfg2_$TAG.json 2> $OUT/sweep_cfg2_$TAG.err
 timeout 600 python bench.py --config qwen3-32b-128k --no-cpu-baseline > $OUT/sweep_cfg5_$TAG.json 2> $OUT/sweep_cfg5_$TAG.err
