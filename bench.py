@@ -59,7 +59,7 @@ D, BS = 128, 64
 CONFIGS = {
     # BASELINE.json configs[2] (the metric's config) and configs[3] (sharded: --global-batch 128)
     "qwen3-32b-32k": dict(layers=64, hq=64, hkv=8, batch=32, ctx=32768, k=64, capacity=64, headroom=8,
-                          recall=16, cpu_frac=0.082),
+                          recall=16, cpu_frac=0.082, hidden=5120),
     # configs[1]: Qwen3-8B, batch 16, 16K, GPU cache = 25% of the 256 blocks
     "qwen3-8b-16k": dict(layers=36, hq=32, hkv=8, batch=16, ctx=16384, k=32, capacity=64, headroom=8,
                          recall=16, cpu_frac=0.082),
@@ -1034,6 +1034,16 @@ def main():
                     "queued after layer i-1's attention (a decoder's data dependency), then begin_layer tickets, K1 "
                     "of layer i+1 on the engine stream beside K2 of layer i, one K2 launch per layer, post per layer"}
         log(f"layerwise {ms_lw:.3f} ms/step")
+        if cfg.get("hidden"):
+            ms_lq, rfrac = run_layerwise_qpred(wl, args.steps, dev, ws, step0=step_no)
+            step_no += 5 + args.steps
+            extras["value_layerwise_qpred"] = {
+                "value": gb / (ms_lq / 1000.0), "ms_per_step": ms_lq, "resident_token_frac_last_step": rfrac,
+                "path": "scout_engine_decode_layer_x per layer: K6 (tcgen05 GEMM, predict_next_query of the "
+                        "model's hidden state, engine.hpp:237) makes q_pred of layer i+1 inside the engine, then K1 "
+                        "of layer i+1 beside K2 of layer i; hidden %d, W_Q random-init (4 distinct, cycled)"
+                        % cfg["hidden"]}
+            log(f"layerwise with q prediction {ms_lq:.3f} ms/step")
     # ---- e2e through host buffers (pre-staged CPU partials)
     e2e = None
     if not args.profile:
@@ -1262,6 +1272,55 @@ def run_layerwise(wl, steps, dev, ws, step0, **engine_kw):
     eng.check_state()
     wl.make_engine()
     return ms
+
+
+def run_layerwise_qpred(wl, steps, dev, ws, step0, n_weights=4):
+    """Layer by layer with the layer-ahead prediction inside the engine
+    (scout_engine_decode_layer_x: K6, the tcgen05 GEMM, makes q_pred of layer
+    i+1 from the model's hidden state, engine.hpp:237): x_i [batch][hidden]
+    follows a closed path like the queries, W_Q^{i+1} [hidden][Hq*128] bf16
+    random-init, n_weights distinct matrices cycled over the layers (each
+    84 MB at Qwen3-32B: every call streams its W from HBM)."""
+    from paper_2603_27138_b200 import ops
+
+    cfg = wl.cfg
+    L, B, hidden = wl.L, wl.B, cfg["hidden"]
+    n_out = cfg["hq"] * D
+    g = torch.Generator(device=dev)
+    g.manual_seed(99)
+    wqs = [ops.QueryPredictor(torch.randn(hidden, n_out, generator=g, device=dev) / math.sqrt(hidden), B)
+           for _ in range(n_weights)]
+    x0, du, dv = (torch.randn(L, B, hidden, generator=g, device=dev) for _ in range(3))
+    eng = wl.make_engine(hidden=hidden)
+    qt_live = torch.empty_like(wl.q_path_t[0])
+    radius, n_path = cfg.get("drift", 0.0), cfg.get("drift_points", 32)
+
+    def one(s):
+        j = s % len(wl.q_path_t)
+        th = 2 * math.pi * (s % n_path) / n_path
+        x = x0 + radius * (math.cos(th) * du + math.sin(th) * dv)
+        for i in range(L):
+            qt_live[i].copy_(wl.q_path_t[j][i])
+            nxt = i + 1 < L
+            eng.decode_layer_x(s, i, qt_live[i], x[i] if nxt else None, wqs[(i + 1) % n_weights] if nxt else None,
+                               wl.cpu_o[i], wl.cpu_ml[i], wl.k_new[i], wl.v_new[i], wl.out_o[i], wl.out_ml[i])
+
+    for s in range(5):
+        one(step0 + 1 + s)
+    eng.sync()
+
+    def tstep(i):
+        one(step0 + 6 + i)
+        if i == steps - 1:
+            eng.sync()
+
+    ms = timed(tstep, steps, dev, ws)
+    k1o = eng.k1_outputs()
+    res, cpu = int(k1o["res_tokens"].sum()), int(k1o["cpu_tokens"].sum())
+    eng.check_state()
+    wl.make_engine()
+    del wqs
+    return ms, res / max(res + cpu, 1)
 
 
 def _pinned_inputs(wl, tier_mode):

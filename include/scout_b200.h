@@ -454,6 +454,10 @@ typedef struct scout_engine_config {
      * + id) % host_blocks. host_units = 0: this engine's U, host_unit0 = 0. */
     int host_units;
     int host_unit0;
+    /* K6 inside the layer-by-layer mode (scout_engine_decode_layer_x): the
+     * model's hidden size (0: off). The engine then keeps the predictor's
+     * workspace and a q_pred buffer of one layer. */
+    int hidden;
 } scout_engine_config;
 
 #define SCOUT_GPU_SIDE_PREDICTED 0
@@ -517,6 +521,16 @@ int scout_engine_check_state(scout_engine* eng);
 int scout_engine_decode_layer(scout_engine* eng, int step, int layer, const void* q_true, const void* q_pred_next,
                               const void* cpu_o, const float* cpu_ml, const float* k_new, const float* v_new,
                               float* out_o, float* out_ml, void* stream);
+/* The same call with the layer-ahead prediction inside (engine.hpp:237,
+ * cfg.hidden > 0): q_pred of layer + 1 = predict_next_query(rms_normalize(
+ * x_next), W_Q^{layer+1}) on K6 (the tcgen05 GEMM, scout_predict_query) into
+ * an engine buffer, then K1 of layer + 1 on it. x_next [batch][hidden] f32 is
+ * the hidden state the model feeds layer + 1's prediction; wq_next_packed is
+ * W_Q^{layer+1} packed by scout_qpred_pack_weights (hidden x hq*128). Both
+ * NULL for the last layer.                                                 */
+int scout_engine_decode_layer_x(scout_engine* eng, int step, int layer, const void* q_true, const float* x_next,
+                                const void* wq_next_packed, const void* cpu_o, const float* cpu_ml, const float* k_new,
+                                const float* v_new, float* out_o, float* out_ml, void* stream);
 /* Order all outstanding side-stream work (recalls) before `stream`. */
 int scout_engine_sync(scout_engine* eng, void* stream);
 /* Device tier mode: the caller changed the K5 state outside the engine

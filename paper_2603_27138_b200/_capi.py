@@ -37,7 +37,7 @@ EXPORTED = (
     "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv", "scout_engine_recall_stats",
     "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
-    "scout_engine_worker_stats", "scout_engine_check_state", "scout_engine_decode_layer",
+    "scout_engine_worker_stats", "scout_engine_check_state", "scout_engine_decode_layer", "scout_engine_decode_layer_x",
 )
 
 _vp = C.c_void_p
@@ -88,6 +88,7 @@ class EngineConfig(C.Structure):
         ("tier", _vp), ("host_blocks", C.c_longlong), ("cpu_dtype", C.c_int),
         ("recall_intervals", _vp), ("recall_stagger", C.c_int), ("cpu_worker", C.c_int), ("cpu_threads", C.c_int),
         ("gpu_side_policy", C.c_int), ("layer_ctas", C.c_int), ("host_units", C.c_int), ("host_unit0", C.c_int),
+        ("hidden", C.c_int),
     ]
 
 
@@ -160,6 +161,7 @@ def lib() -> C.CDLL:
         L.scout_engine_worker_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]
         L.scout_engine_check_state.argtypes = [_vp]
         L.scout_engine_decode_layer.argtypes = [_vp, C.c_int, C.c_int] + [_vp] * 8 + [_vp]
+        L.scout_engine_decode_layer_x.argtypes = [_vp, C.c_int, C.c_int] + [_vp] * 9 + [_vp]
         _lib = L
     return _lib
 

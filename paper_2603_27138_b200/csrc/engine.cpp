@@ -234,6 +234,10 @@ struct scout_engine {
     double cw_ms = 0.0;                    // CPU time of the worker's partials (summed, reset by stats)
     int cw_steps = 0;
 
+    // K6 in the layer-by-layer mode (cfg.hidden > 0): the predictor's
+    // workspace and one layer's q_pred (q dtype)
+    Buf qp_ws, qp_buf;
+    size_t qp_ws_bytes = 0;
     // layer-by-layer mode (scout_engine_decode_layer): the layer expected next
     // and the step in progress
     int lw_next = 0, lw_step = -1;
@@ -1142,6 +1146,23 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         e->cw_on = true;
         e->cw_thread = std::thread([e] { e->cw_loop(); });
     }
+    if (c.hidden > 0) {  // K6 inside the layer-by-layer mode
+        const int n_out = c.hq * SCOUT_HEAD_DIM;
+        if (c.hidden % 128 != 0 || c.batch > 256 || !c.tier) {
+            delete e;
+            set_error(SCOUT_ERR_INVALID_ARGUMENT,
+                      "scout_engine_create: hidden %% 128, batch <= 256 and device tier mode for the q prediction");
+            return SCOUT_ERR_INVALID_ARGUMENT;
+        }
+        e->qp_ws_bytes = scout_qpred_workspace_bytes(c.hidden, n_out, c.batch, 0);
+        const size_t qb = c.q_dtype == SCOUT_BF16 ? 2 : 4;
+        if (e->qp_ws.alloc(e->qp_ws_bytes) || cudaMemset(e->qp_ws.p, 0, e->qp_ws_bytes) != cudaSuccess ||
+            e->qp_buf.alloc(static_cast<size_t>(c.batch) * n_out * qb)) {
+            delete e;
+            set_error(SCOUT_ERR_CUDA, "scout_engine_create: q prediction buffers");
+            return SCOUT_ERR_CUDA;
+        }
+    }
     e->ev_k1.resize(c.layers);
     for (auto& ev : e->ev_k1) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     e->chunk_ev.resize(e->nch);
@@ -1457,14 +1478,44 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
 // Layer i's inputs need only exist when the call is made -- q_true[i] and
 // q_pred[i+1] come from layer i-1's output in a real decoder -- and K1(i+1)
 // may run beside K2(i), on the engine's K1 stream.
+static int decode_layer_impl(scout_engine* e, int step, int layer, const void* q_true, const void* q_pred_next,
+                             const float* x_next, const void* wq_next, const void* cpu_o, const float* cpu_ml,
+                             const float* k_new, const float* v_new, float* out_o, float* out_ml, void* stream);
+
 extern "C" int scout_engine_decode_layer(scout_engine* e, int step, int layer, const void* q_true,
                                          const void* q_pred_next, const void* cpu_o, const float* cpu_ml,
                                          const float* k_new, const float* v_new, float* out_o, float* out_ml,
                                          void* stream) {
+    if (!e || (e->tier_mode && layer >= 0 && layer + 1 < e->cfg.layers && !q_pred_next)) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_decode_layer: bad arguments (device tier "
+                                                          "engine, q_pred of the next layer unless this is the last)");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    return decode_layer_impl(e, step, layer, q_true, q_pred_next, nullptr, nullptr, cpu_o, cpu_ml, k_new, v_new, out_o,
+                             out_ml, stream);
+}
+
+extern "C" int scout_engine_decode_layer_x(scout_engine* e, int step, int layer, const void* q_true,
+                                           const float* x_next, const void* wq_next_packed, const void* cpu_o,
+                                           const float* cpu_ml, const float* k_new, const float* v_new, float* out_o,
+                                           float* out_ml, void* stream) {
+    if (!e || e->cfg.hidden <= 0 ||
+        (layer >= 0 && layer + 1 < e->cfg.layers && (!x_next || !wq_next_packed))) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT,
+                              "scout_engine_decode_layer_x: needs cfg.hidden > 0, and x_next / wq_next_packed unless "
+                              "this is the last layer");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    return decode_layer_impl(e, step, layer, q_true, nullptr, x_next, wq_next_packed, cpu_o, cpu_ml, k_new, v_new,
+                             out_o, out_ml, stream);
+}
+
+static int decode_layer_impl(scout_engine* e, int step, int layer, const void* q_true, const void* q_pred_next,
+                             const float* x_next, const void* wq_next, const void* cpu_o, const float* cpu_ml,
+                             const float* k_new, const float* v_new, float* out_o, float* out_ml, void* stream) {
     using scout_host::set_error;
     if (!e || !e->tier_mode || e->cw_on || !q_true || !k_new || !v_new || !out_o || !out_ml ||
-        ((cpu_o == nullptr) != (cpu_ml == nullptr)) || layer < 0 || layer >= e->cfg.layers ||
-        (layer + 1 < e->cfg.layers && !q_pred_next)) {
+        ((cpu_o == nullptr) != (cpu_ml == nullptr)) || layer < 0 || layer >= e->cfg.layers) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_decode_layer: bad arguments (device tier engine, "
                                               "q_pred of the next layer unless this is the last)");
         return SCOUT_ERR_INVALID_ARGUMENT;
@@ -1545,6 +1596,15 @@ extern "C" int scout_engine_decode_layer(scout_engine* e, int step, int layer, c
         return rc;
     hmark(3);
     if (layer + 1 < L) {
+        if (x_next) {  // engine.hpp:237: q_pred of layer + 1 from the model's hidden state (K6, tcgen05)
+            const bool bf = e->cfg.q_dtype == SCOUT_BF16;
+            ++e->launches;
+            if ((rc = scout_predict_query(x_next, e->cfg.batch, e->cfg.hidden, wq_next, e->cfg.hq * SCOUT_HEAD_DIM,
+                                          bf ? nullptr : static_cast<float*>(e->qp_buf.p), bf ? e->qp_buf.p : nullptr,
+                                          e->qp_ws.p, e->qp_ws_bytes, 0, e->k1s)) != SCOUT_OK)
+                return rc;
+            q_pred_next = e->qp_buf.p;
+        }
         std::vector<scout_topk_args> v{e->k1_args(layer + 1, q_pred_next, step, par)};
         ++e->launches;
         if ((rc = scout_k1_launch_batch(v.data(), 1, e->k1s)) != SCOUT_OK) return rc;

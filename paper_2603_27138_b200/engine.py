@@ -34,7 +34,8 @@ class DecodeEngine:
                  recall_interval=0, host_tier=None, max_ctas=0, host_staging=False, chunk_layers=8,
                  recall_mode=1, q_dtype=torch.float32, tier=None, host_blocks=0, cpu_dtype=torch.float32,
                  recall_intervals=None, recall_stagger=False, cpu_worker=False, cpu_threads=0,
-                 gpu_side_policy="predicted_topk_intersect_resident", layer_ctas=0, host_units=0, host_unit0=0):
+                 gpu_side_policy="predicted_topk_intersect_resident", layer_ctas=0, host_units=0, host_unit0=0,
+                 hidden=0):
         """tier: a tier.DeviceTieredCache whose state the engine drives on the
         device (device tier mode: decode_step_kv); host_tier then holds block
         images at ((layer*U + unit)*nb_stride + id) % host_blocks.
@@ -49,6 +50,8 @@ class DecodeEngine:
         "predicted_topk_intersect_resident" or "all_resident" (the GPU side
         attends to the layer's whole fast tier at attention time).
         layer_ctas: K2 CTAs of a layer-by-layer launch (0 automatic, < 0 all).
+        hidden: the model's hidden size for decode_layer_x (the layer-ahead
+        q prediction, K6, inside the layer-by-layer mode); 0 = off.
         host_units / host_unit0: the host tier's unit index space when ranks
         share one (image ((layer*host_units + host_unit0 + u)*nb_stride + id)
         % host_blocks); 0 / 0: this engine's units."""
@@ -80,6 +83,7 @@ class DecodeEngine:
         cfg.gpu_side_policy = policies[gpu_side_policy]
         cfg.layer_ctas = int(layer_ctas)
         cfg.host_units, cfg.host_unit0 = int(host_units), int(host_unit0)
+        cfg.hidden = int(hidden)
         self.gpu_side_policy = gpu_side_policy
         self.cpu_worker = bool(cpu_worker)
         self.tier = tier
@@ -164,6 +168,17 @@ class DecodeEngine:
         A.check(A.lib().scout_engine_decode_layer(self._h, int(step), int(layer), _p(q_true), _p(q_pred_next),
                                                   _p(cpu_o), _p(cpu_ml), _p(k_new), _p(v_new), _p(out_o), _p(out_ml),
                                                   self._stream()))
+
+    def decode_layer_x(self, step, layer, q_true, x_next, wq_next, cpu_o, cpu_ml, k_new, v_new, out_o, out_ml):
+        """decode_layer with the next layer's q_pred predicted inside the engine
+        (engine.hpp:237): x_next [batch][hidden] f32 and wq_next, an
+        ops.QueryPredictor's packed W_Q of layer + 1 (its w_packed), or None
+        for the last layer."""
+        self._check(q_true, None, cpu_o, cpu_ml)
+        wp = None if wq_next is None else (wq_next.w_packed if hasattr(wq_next, "w_packed") else wq_next)
+        A.check(A.lib().scout_engine_decode_layer_x(self._h, int(step), int(layer), _p(q_true), _p(x_next), _p(wp),
+                                                    _p(cpu_o), _p(cpu_ml), _p(k_new), _p(v_new), _p(out_o),
+                                                    _p(out_ml), self._stream()))
 
     def tier_changed(self):
         """The tier state was changed outside the engine: plan the next step afresh."""

@@ -364,3 +364,48 @@ def test_engine_layerwise_matches_fused_step(cuda, stagger, gpu_side):
         e.check_state()
     with pytest.raises(RuntimeError):  # layers out of order
         engs[1].decode_layer(steps + 1, 2, qt[2], qp[3], None, None, kn[2], vn[2], lw[0][2], lw[1][2])
+
+
+def test_engine_layerwise_with_query_prediction(cuda):
+    """scout_engine_decode_layer_x (K6 inside: q_pred of layer i+1 =
+    predict_next_query(rms_normalize(x_i), W_Q^{i+1}), engine.hpp:237) against
+    scout_engine_decode_layer fed with the same prediction made outside
+    (ops.QueryPredictor, the same tcgen05 kernel): bit-identical outputs and
+    tier state, step after step."""
+    L, batch, hkv, G, k, cap, nbs, steps, hidden = 4, 2, 2, 4, 6, 8, 24, 24, 256
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 11 + 50
+    torch.manual_seed(13)
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    sides = [Side(L, U, nbs, cap, kv, seed_rows) for _ in range(2)]
+    engs = []
+    for sd in sides:
+        layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+        engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
+                                 kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=3,
+                                 host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, hidden=hidden))
+    wqs = [ops.QueryPredictor((torch.randn(hidden, hkv * G * D, device="cuda") / hidden ** 0.5), batch)
+           for _ in range(L)]
+    outs = [[torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")] for _ in range(2)]
+    x_base = torch.randn(L, batch, hidden, device="cuda")
+    for step in range(1, steps + 1):
+        qt = torch.randn(L, U * G, D, device="cuda").bfloat16()
+        xs = x_base + 0.1 * torch.randn(L, batch, hidden, device="cuda")
+        co = torch.randn(L, U * G, D, device="cuda")
+        cm = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
+        kn, vn = torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")
+        for i in range(L):
+            nxt = i + 1 < L
+            engs[0].decode_layer_x(step, i, qt[i], xs[i] if nxt else None, wqs[i + 1] if nxt else None, co[i], cm[i],
+                                   kn[i], vn[i], outs[0][0][i], outs[0][1][i])
+            qp = wqs[i + 1](xs[i], want=("bf16",)).view(U * G, D) if nxt else None
+            engs[1].decode_layer(step, i, qt[i], qp, co[i], cm[i], kn[i], vn[i], outs[1][0][i], outs[1][1][i])
+        for e in engs:
+            e.sync()
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]), step
+        for name in ("tier", "last_sel", "ready"):
+            assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
+    for e in engs:
+        e.check_state()
