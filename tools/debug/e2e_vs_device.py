@@ -31,7 +31,14 @@ def host_step():
     j = step[0] % n
     eng.decode_step_kv_host(step[0], h_qt[j], h_qp[j], h_co, h_cm, *h_kv, h_out, h_oml, h_ids, h_n)
 
-for name, fn in (("device", dev_step), ("host", host_step), ("device", dev_step), ("host", host_step)):
+
+def host_step_noids():
+    step[0] += 1
+    j = step[0] % n
+    eng.decode_step_kv_host(step[0], h_qt[j], h_qp[j], h_co, h_cm, *h_kv, h_out, h_oml, None, None)
+
+for name, fn in (("device", dev_step), ("host", host_step), ("host no ids", host_step_noids), ("device", dev_step),
+                 ("host", host_step), ("host no ids", host_step_noids)):
     for _ in range(5):
         fn()
     eng.sync(); torch.cuda.synchronize()
