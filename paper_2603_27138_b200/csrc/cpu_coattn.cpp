@@ -341,7 +341,8 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
     constexpr float LOG2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
     // ---- Q^T -> VNNI B tiles: column n < 8 = hi of head n, 8 + n = lo of head n;
     // a VNNI word is the (2i, 2i+1) channel pair of one column
-    std::memset(w.bq, 0, sizeof(w.bq));
+    // (w.bq's columns of heads >= G and w.pa's rows >= G stay zero: cleared
+    // when the scratch is (re)dedicated to a group size, amx_work)
     alignas(64) float qscratch[GMAX * D];
     const float* qu = unit_query(j, u, qscratch);
     const __m512 qs = _mm512_set1_ps(j.scale * LOG2E);
@@ -360,8 +361,7 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
             _mm512_i32scatter_epi32(base + g, col, hi, 4);
             _mm512_i32scatter_epi32(base + 8 + g, col, lo, 4);
         }
-    std::memset(w.o, 0, sizeof(w.o));
-    std::memset(w.pa, 0, sizeof(w.pa));  // rows >= G stay zero
+    bool first = true;  // the first chunk's P.V is the running O (no memset, no rescale of garbage)
     const __m512 ninf = _mm512_set1_ps(-std::numeric_limits<float>::infinity());
     __m512 m = ninf, l = _mm512_setzero_ps();  // lanes g and 8 + g: head g
     const __m512i pick_hi = _mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 16, 17, 18, 19, 20, 21, 22, 23);
@@ -499,13 +499,17 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
         for (int g = 0; g < G; ++g) {
             const __m512 a = _mm512_set1_ps(al[g]);
             for (int c = 0; c < D; c += 16)
-                _mm512_store_ps(&w.o[g][c], _mm512_fmadd_ps(a, _mm512_load_ps(&w.o[g][c]), _mm512_load_ps(&w.ob[g][c])));
+                _mm512_store_ps(&w.o[g][c], first ? _mm512_load_ps(&w.ob[g][c])
+                                                  : _mm512_fmadd_ps(a, _mm512_load_ps(&w.o[g][c]),
+                                                                    _mm512_load_ps(&w.ob[g][c])));
         }
+        first = false;
         PROF_MARK(4);
     }
     alignas(64) float mm[16], ll[16];
     _mm512_store_ps(mm, m);
     _mm512_store_ps(ll, l);
+    if (first) std::memset(w.o, 0, sizeof(w.o));  // no block: the empty partial, o = 0
     for (int g = 0; g < G; ++g) {
         const size_t h = static_cast<size_t>(u) * G + g;
         const float inv = ll[g] > 0.f ? 1.f / ll[g] : 0.f;
@@ -529,6 +533,12 @@ SCOUT_AMX_TARGET void amx_work(const Job& j, std::atomic<int>& next, int n_units
         }
     }
     AmxScratch* scratch = owned.get();
+    static thread_local int scratch_g = -1;  // the group size the zero padding was laid for
+    if (scratch_g != j.G) {
+        std::memset(scratch->bq, 0, sizeof(scratch->bq));
+        std::memset(scratch->pa, 0, sizeof(scratch->pa));
+        scratch_g = j.G;
+    }
     amx_config(j.G);
     for (int u; (u = next.fetch_add(1)) < n_units;) run_unit_amx(j, u, *scratch);
     _tile_release();
