@@ -1152,12 +1152,13 @@ def main():
 
 
 def run_c_abi_f32(args, cfg, ws, rank, gb):
-    """BASELINE configs[0] (fp32 KV, one layer, 1 request): the C ABI directly,
-    as a reference caller would bind it -- per step one scout_score_topk_split
+    """BASELINE configs[0] (fp32 KV, one layer, 1 request): the engine's step
+    (static residency, f32 KV) and, beside it, the C ABI called directly as a
+    reference caller would bind it -- per step one scout_score_topk_split
     (stacked select_topk + split against the residency table) and one
     scout_sparse_decode (f32 CUDA-core path, merged with a CPU partial). The
     tier holds all but round(8.2% k) selected blocks. e2e: the query and CPU
-    partial H2D and the output D2H around the two calls."""
+    partial H2D and the output D2H around the step."""
     from paper_2603_27138_b200 import ops
 
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -1214,7 +1215,44 @@ def run_c_abi_f32(args, cfg, ws, rank, gb):
 
     for i in range(args.warmup):
         e2e_step(i)
-    ms_e2e = timed(e2e_step, args.steps, dev, ws)
+    ms_e2e_direct = timed(e2e_step, args.steps, dev, ws)
+    ms_direct = ms
+    # ---- the same step through the engine (static residency, f32 KV: K1 + the
+    # per-layer f32 K2), device-resident and from pinned host buffers
+    from paper_2603_27138_b200.engine import DecodeEngine, LayerState
+
+    eng = DecodeEngine(layers=1, batch=cfg["batch"], hq=hq, hkv=hkv, k=k, n_tokens=n_tokens, pool=pool,
+                       kv_dtype=torch.float32, layer_states=[LayerState(dig, table)], scale=1.0 / math.sqrt(D),
+                       host_staging=True, q_dtype=torch.float32, cpu_dtype=torch.float32)
+    q3, co3, cm3 = q[None].contiguous(), cpu_o[None].contiguous(), cpu_ml[None].contiguous()
+    o3, ml3 = torch.empty(1, U * G, D, device=dev), torch.empty(1, U * G, 2, device=dev)
+    hq3, hco3, hcm3 = q3.cpu().pin_memory(), co3.cpu().pin_memory(), cm3.cpu().pin_memory()
+    ho3, hml3 = torch.empty(o3.shape).pin_memory(), torch.empty(ml3.shape).pin_memory()
+    st_no = [0]
+
+    def eng_step(i):
+        st_no[0] += 1
+        eng.decode_step(st_no[0], q3, q3, co3, cm3, o3, ml3)
+
+    def eng_e2e(i):
+        st_no[0] += 1
+        eng.decode_step_host(st_no[0], hq3, hq3, hco3, hcm3, ho3, hml3)
+
+    for i in range(args.warmup):
+        eng_step(i)
+    eng.sync()
+    eng.stats()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms = timed(eng_step, args.steps, dev, ws)
+    clk = clocks.stop()
+    launches = eng.stats()[2]
+    for i in range(args.warmup):
+        eng_e2e(i)
+    eng.sync()
+    ms_e2e = timed(eng_e2e, args.steps, dev, ws)
+    ok = torch.equal(o3[0], o)  # the same kernels on the same inputs as the direct calls
+    eng.close()
     peaks = {}
     try:
         peaks = json.load(open(ROOT / "MEASURED_PEAKS.json"))
@@ -1228,15 +1266,22 @@ def run_c_abi_f32(args, cfg, ws, rank, gb):
                 "config": {"workload": args.config, "batch_per_gpu": cfg["batch"], "context": cfg["ctx"], "layers": 1,
                            "heads": f"{hq}q/{hkv}kv", "head_dim": D, "block": BS, "top_k": k,
                            "cpu_blocks_per_unit": ncpu, "kv_dtype": "f32",
-                           "path": "C ABI scout_score_topk_split + scout_sparse_decode (f32 CUDA-core K2) per step",
+                           "path": "the engine (scout_engine_decode_step, static residency, f32 KV: K1 + the "
+                                   "per-layer f32 CUDA-core K2 merged with the CPU partial); e2e through "
+                                   "scout_engine_decode_step_host",
                            "l2": "working set %.1f MiB: fits L2 (a latency-bound config)" % (nbytes / 2**20)},
                 "roofline": {"bound": "latency (one request, one layer: 8 units)", "achieved": nbytes / ms / 1e6,
                              "peak": peak, "unit": "GB/s", "frac": nbytes / ms / 1e6 / peak,
                              "traffic": None, "kernel": "K1 + K2 (f32), step bytes / step time"},
-                "clocks": clk, "gpu_launches": 3 * args.steps,
+                "clocks": clk, "gpu_launches": launches,
                 "e2e": {"value": gb / (ms_e2e / 1000.0), "unit": "tokens/s", "ms_per_step": ms_e2e,
-                        "h2d_bytes_per_step": int(hq_.numel() * 4 + hco.numel() * 4 + hcm.numel() * 4),
-                        "d2h_bytes_per_step": int(ho.numel() * 4 + hml.numel() * 4)}}
+                        "h2d_bytes_per_step": int(2 * hq3.numel() * 4 + hco3.numel() * 4 + hcm3.numel() * 4),
+                        "d2h_bytes_per_step": int(ho3.numel() * 4 + hml3.numel() * 4)},
+                "engine_matches_direct_calls": bool(ok),
+                "c_abi_direct": {"ms_per_step": ms_direct, "value": gb / (ms_direct / 1000.0),
+                                 "e2e_ms_per_step": ms_e2e_direct,
+                                 "path": "scout_score_topk_split + scout_sparse_decode called directly (torch "
+                                         "copies for the e2e H2D / D2H)"}}
         print(json.dumps(line), flush=True)
 
 

@@ -67,6 +67,12 @@ struct Buf {
         }                                                                                  \
     } while (0)
 
+#define CU_RC(x)                        \
+    do {                                \
+        const int rc_ = (x);            \
+        if (rc_ != SCOUT_OK) return rc_; \
+    } while (0)
+
 // stream memory operations (driver API, resolved at run time)
 using WaitValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 using WriteValueFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
@@ -438,6 +444,45 @@ struct scout_engine {
             e1 = tev[tev_used++];
             CU(cudaEventRecord(e0, st));
         }
+        if (cfg.kv_dtype == SCOUT_F32) {
+            // f32 KV: one CUDA-core split-K launch per layer (scout_sparse_decode),
+            // with the persistent kernel's device-side gates done as stream
+            // operations: the layer's recall flag and input chunk before it,
+            // the layer_done count the post-attention launches wait for after it
+            for (int j = 0; j < n; ++j) {
+                const K2Layer& ly = a.layers[j];
+                if (ly.recall_token) CU_RC(wait_value(st, recall_flag + l0 + j, ly.recall_token));
+                if (ly.in_flag) CU_RC(wait_value(st, ly.in_flag, token));
+                scout_decode_args d{};
+                d.n_units = U;
+                d.group = G;
+                d.kv_dtype = SCOUT_F32;
+                d.k_stride = a.k_stride;
+                d.scale = cfg.scale;
+                d.q = ly.q;
+                d.kv_pool = cfg.kv_pool;
+                d.res_slots = ly.res_slots;
+                d.res_ids = ly.res_ids;
+                d.n_res = ly.n_res;
+                d.n_tokens = cfg.n_tokens;
+                d.cpu_o = static_cast<const float*>(ly.cpu_o);
+                d.cpu_ml = ly.cpu_ml;
+                d.o = ly.o;
+                d.ml = ly.ml;
+                d.workspace = static_cast<uint8_t*>(a.workspace) + static_cast<size_t>(j) * ws_layer;
+                d.workspace_bytes = ws_layer;
+                d.max_ctas = cfg.max_ctas;
+                d.q_dtype = SCOUT_F32;
+                ++launches;
+                const int rc = scout_sparse_decode(&d, st);
+                if (rc != SCOUT_OK) return rc;
+                CU_RC(write_value(st, layer_done + l0 + j, token * static_cast<unsigned>(grid)));
+            }
+            if (timing) CU(cudaEventRecord(e1, st));
+            CU(cudaEventRecord(ev_k2[par], st));
+            k2_recorded[par] = true;
+            return SCOUT_OK;
+        }
         ++launches;
         const int rc = scout_k2_launch(a, st, false);
         if (rc != SCOUT_OK) return rc;
@@ -794,6 +839,7 @@ struct scout_engine {
         n_tickets += L;
         pa.n_tokens = cfg.n_tokens;
         pa.pool = static_cast<uint8_t*>(cfg.kv_pool);
+        pa.kv_f32 = cfg.kv_dtype == SCOUT_F32;
         pa.k_new = k_new;
         pa.v_new = v_new;
         for (int i = 0; i < L; ++i) pa.digests[i] = const_cast<void*>(layers[i].digests);
@@ -945,10 +991,15 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     const scout_engine_config& c = *cfg;
     if (c.layers <= 0 || c.layers > K2_MAX_LAYERS || c.batch <= 0 || c.hkv <= 0 || c.hq % c.hkv != 0 || c.k <= 0 ||
         c.k > SCOUT_MAX_K || c.nb_stride <= 0 || !c.kv_pool || !c.n_tokens || !(c.scale > 0.f) ||
-        c.kv_dtype != SCOUT_BF16 || (c.q_dtype != SCOUT_F32 && c.q_dtype != SCOUT_BF16) ||
+        (c.kv_dtype != SCOUT_BF16 && c.kv_dtype != SCOUT_F32) || (c.q_dtype != SCOUT_F32 && c.q_dtype != SCOUT_BF16) ||
         (c.cpu_dtype != SCOUT_F32 && c.cpu_dtype != SCOUT_BF16) || c.recall_interval < 0) {
-        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 KV, k 1..%d)",
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: bad config (layers 1..%d, bf16 / f32 KV, k 1..%d)",
                   K2_MAX_LAYERS, SCOUT_MAX_K);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (c.kv_dtype == SCOUT_F32 && (c.q_dtype != SCOUT_F32 || c.cpu_dtype != SCOUT_F32 || c.hidden > 0)) {
+        // the f32 attention path (per-layer CUDA-core split-K) takes f32 queries and partials
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_create: f32 KV needs f32 queries and CPU partials");
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     if (const int G = c.hq / c.hkv; G != 1 && G != 2 && G != 4 && G != 8) {
@@ -1019,6 +1070,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
         for (int p = 0; p < 2; ++p) bad |= e->ar_ids[p].alloc(lr) | e->ar_slots[p].alloc(lr) | e->ar_n[p].alloc(lu);
     }
     e->ws_layer = scout_k2_ws_layer_bytes(e->U, e->grid);
+    if (c.kv_dtype == SCOUT_F32)  // per-layer launches of the f32 path (scout_sparse_decode)
+        e->ws_layer = std::max(e->ws_layer, (scout_sparse_decode_workspace_bytes(e->U, e->G, c.max_ctas) + 255) / 256 * 256);
     bad |= e->ws.alloc(e->ws_layer * c.layers);
     const size_t nflags = 4 * static_cast<size_t>(c.layers) + e->nch;
     bad |= e->flags.alloc(nflags * 4);

@@ -13,10 +13,11 @@ struct TierPostArgs {
     int n_layers, nbs, k, step, ticket_base;
     int layer0;                      // first layer of this launch (grid.y layers from it)
     const int32_t* n_tokens;         // count before the append (advanced after the launch)
-    uint8_t* pool;                   // bf16 KV pool
+    uint8_t* pool;                   // KV pool: bf16 tile slots, or f32 row-major slots (kv_f32)
+    int kv_f32;
     const float* k_new;              // [L][U][128]
     const float* v_new;
-    void* digests[K5_MAX_LAYERS];    // per layer [U][2][128][nbs] bf16
+    void* digests[K5_MAX_LAYERS];    // per layer [U][2][128][nbs] in the KV dtype
     uint8_t* host_tier;              // device view of the pinned host tier (nullptr: no write-through)
     long long host_blocks;
     int host_units, host_unit0;      // image index ((l * host_units + host_unit0 + u) * nbs + id) % host_blocks

@@ -627,7 +627,25 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
     }
     __syncthreads();
     const int slot = s_slot, sealed_blk = s_sealed;
-    if (slot >= 0) {
+    const size_t sbytes = a.kv_f32 ? F32_SLOT_BYTES : BF16_SLOT_BYTES;
+    if (slot >= 0 && a.kv_f32) {
+        // ---- row write + digest fold (scout_kv_append, f32 KV: row-major slot, minmax)
+        float* base = reinterpret_cast<float*>(a.pool + static_cast<size_t>(slot) * F32_SLOT_BYTES);
+        const size_t row = (static_cast<size_t>(l) * gridDim.x + u) * D + c;
+        const float v = a.k_new[row];
+        base[r * D + c] = v;
+        base[BS * D + r * D + c] = a.v_new[row];
+        float* dig = static_cast<float*>(a.digests[l]) + static_cast<size_t>(u) * 2 * D * a.nbs;
+        float& lo = dig[static_cast<size_t>(c) * a.nbs + id];
+        float& hi = dig[static_cast<size_t>(D + c) * a.nbs + id];
+        if (r == 0) {
+            lo = v;
+            hi = v;
+        } else {  // std::min / std::max fold (digest.hpp:45-46)
+            if (v < lo) lo = v;
+            if (hi < v) hi = v;
+        }
+    } else if (slot >= 0) {
         // ---- row write + digest fold (scout_kv_append, bf16 KV, minmax)
         __nv_bfloat16* base = reinterpret_cast<__nv_bfloat16*>(a.pool + static_cast<size_t>(slot) * BF16_SLOT_BYTES);
         const int off = bf16_tile_offset(r, c);
@@ -655,9 +673,9 @@ __global__ void __launch_bounds__(TT) tier_post_layers_kernel(const TierPostArgs
         if (a.host_tier) {
             long long hi = (static_cast<long long>(l) * a.host_units + a.host_unit0 + u) * a.nbs + sealed_blk;
             if (a.host_blocks > 0) hi %= a.host_blocks;
-            const int4* src = reinterpret_cast<const int4*>(a.pool + static_cast<size_t>(slot) * BF16_SLOT_BYTES);
-            int4* dst = reinterpret_cast<int4*>(a.host_tier + static_cast<size_t>(hi) * BF16_SLOT_BYTES);
-            for (int i = c; i < static_cast<int>(BF16_SLOT_BYTES / 16); i += TT) dst[i] = __ldcg(src + i);
+            const int4* src = reinterpret_cast<const int4*>(a.pool + static_cast<size_t>(slot) * sbytes);
+            int4* dst = reinterpret_cast<int4*>(a.host_tier + static_cast<size_t>(hi) * sbytes);
+            for (int i = c; i < static_cast<int>(sbytes / 16); i += TT) dst[i] = __ldcg(src + i);
         }
         __syncthreads();
         enforce_capacity(L, U, id + 1, pos + 1, S);

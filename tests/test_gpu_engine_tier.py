@@ -78,8 +78,10 @@ def fast_tier_lists(rt, i, n_tokens, nbs):
     return to(slots), to(ids), to(n)
 
 
-@pytest.mark.parametrize("policy", sorted(POLICIES))
-def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
+@pytest.mark.parametrize("policy,kv", [(p, torch.bfloat16) for p in sorted(POLICIES)] +
+                         [(p, torch.float32) for p in ("reference_every_3", "all_resident_every_3",
+                                                       "reference_per_layer_full_capacity")])
+def test_engine_tier_mode_matches_reference_order_replay(cuda, policy, kv):
     """The engine's decode steps against a replay in the reference's per-layer
     order (engine.hpp:219-307) through the validated single ops and the
     DeviceTieredCache mirror, with the recall decision and the recalled set
@@ -88,7 +90,9 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
     external: between two steps the caller re-places layer 1's fast set
     (place_after_prefill) on both sides and tells the engine
     (scout_engine_tier_changed), whose next planning view must then come from
-    the new state, not from the view the previous step's post launch wrote."""
+    the new state, not from the view the previous step's post launch wrote.
+    kv f32: the engine's f32 KV path (per-layer CUDA-core attention launches
+    gated by stream operations, f32 queries and partials)."""
     import py_oracle as P
 
     intervals, cap, stagger, external = POLICIES[policy]
@@ -96,7 +100,7 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
     torch.manual_seed(len(policy))
     L, batch, hkv, G, k, nbs, steps = 3, 2, 2, 4, 6, 24, 70
     U = batch * hkv
-    kv = torch.bfloat16
+    qdt = torch.bfloat16 if kv == torch.bfloat16 else torch.float32
     stationary = policy == "reference_per_layer_full_capacity"
     T0 = 64 * 13 if stationary else 64 * 12 + 40
     seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
@@ -106,7 +110,7 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
     eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=eng_side.n_tokens,
                        pool=eng_side.pool, kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D),
                        recall_interval=0, recall_intervals=intervals, recall_stagger=stagger,
-                       host_tier=eng_side.host, tier=eng_side.tier, host_blocks=0, q_dtype=torch.bfloat16,
+                       host_tier=eng_side.host, tier=eng_side.tier, host_blocks=0, q_dtype=qdt,
                        gpu_side_policy="all_resident" if policy in ALL_RESIDENT else
                        "predicted_topk_intersect_resident")
     policy_ref = P.RefRecall(U, intervals) if (intervals and not stagger) else None
@@ -117,8 +121,8 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
     n_recalled = evicted_predicted = 0
     q_fixed = torch.randn(L, U * G, D, device="cuda")
     for step in range(1, steps + 1):
-        q_true = (q_fixed if stationary else torch.randn(L, U * G, D, device="cuda")).bfloat16()
-        q_pred = q_true if stationary else (q_true.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).bfloat16()
+        q_true = (q_fixed if stationary else torch.randn(L, U * G, D, device="cuda")).to(qdt)
+        q_pred = q_true if stationary else (q_true.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).to(qdt)
         cpu_o = torch.randn(L, U * G, D, device="cuda")
         cpu_ml = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
         k_new = torch.randn(L, U, D, device="cuda") * (0.05 if stationary else 1.0)
@@ -206,8 +210,9 @@ def test_engine_tier_mode_matches_reference_order_replay(cuda, policy):
         assert torch.equal(eng_side.dig[i], rep.dig[i])
 
 
-@pytest.mark.parametrize("cpu_dtype", [torch.float32, torch.bfloat16])
-def test_engine_tier_host_path_matches_device_path(cuda, cpu_dtype):
+@pytest.mark.parametrize("cpu_dtype,kv", [(torch.float32, torch.bfloat16), (torch.bfloat16, torch.bfloat16),
+                                          (torch.float32, torch.float32)])
+def test_engine_tier_host_path_matches_device_path(cuda, cpu_dtype, kv):
     """scout_engine_decode_step_kv_host (pinned host inputs and outputs,
     pipelined copies) against scout_engine_decode_step_kv on an identical
     second cache: same outputs, same tier state, step after step (CPU
@@ -215,7 +220,7 @@ def test_engine_tier_host_path_matches_device_path(cuda, cpu_dtype):
     rng = np.random.default_rng(5)
     L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 40
     U = batch * hkv
-    kv = torch.bfloat16
+    qdt = torch.bfloat16 if kv == torch.bfloat16 else torch.float32
     T0 = 64 * 11 + 50
     seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
     sides = [Side(L, U, nbs, cap, kv, seed_rows) for _ in range(2)]
@@ -224,12 +229,12 @@ def test_engine_tier_host_path_matches_device_path(cuda, cpu_dtype):
         layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
         engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
                                  kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=4,
-                                 host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, host_staging=True,
+                                 host_tier=sd.host, tier=sd.tier, q_dtype=qdt, host_staging=True,
                                  chunk_layers=2, cpu_dtype=cpu_dtype))
     out = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
     h_out = [torch.empty(L, U * G, D).pin_memory(), torch.empty(L, U * G, 2).pin_memory()]
     for step in range(1, steps + 1):
-        ins = [torch.randn(L, U * G, D, device="cuda").bfloat16(), torch.randn(L, U * G, D, device="cuda").bfloat16(),
+        ins = [torch.randn(L, U * G, D, device="cuda").to(qdt), torch.randn(L, U * G, D, device="cuda").to(qdt),
                torch.randn(L, U * G, D, device="cuda").to(cpu_dtype),
                torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous(),
                torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")]
@@ -319,17 +324,18 @@ def test_engine_tier_back_to_back_steps_with_recalls(cuda, recall_mode):
     assert int(sd.n_tokens[0]) == T0 + 60
 
 
-@pytest.mark.parametrize("stagger,gpu_side", [(False, "predicted_topk_intersect_resident"),
-                                               (True, "predicted_topk_intersect_resident"),
-                                               (False, "all_resident")])
-def test_engine_layerwise_matches_fused_step(cuda, stagger, gpu_side):
+@pytest.mark.parametrize("stagger,gpu_side,kv", [(False, "predicted_topk_intersect_resident", torch.bfloat16),
+                                                  (True, "predicted_topk_intersect_resident", torch.bfloat16),
+                                                  (False, "all_resident", torch.bfloat16),
+                                                  (False, "predicted_topk_intersect_resident", torch.float32)])
+def test_engine_layerwise_matches_fused_step(cuda, stagger, gpu_side, kv):
     """scout_engine_decode_layer (one call per layer, inputs given layer by
     layer) against scout_engine_decode_step_kv (all layers at once) on an
     identical second cache: the same outputs bit for bit and the same tier
     state after every step, with recalls in both cadences."""
     L, batch, hkv, G, k, cap, nbs, steps = 4, 2, 2, 4, 6, 8, 24, 40
     U = batch * hkv
-    kv = torch.bfloat16
+    qdt = torch.bfloat16 if kv == torch.bfloat16 else torch.float32
     T0 = 64 * 11 + 50
     torch.manual_seed(7)
     seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
@@ -340,12 +346,12 @@ def test_engine_layerwise_matches_fused_step(cuda, stagger, gpu_side):
         engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
                                  kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=0,
                                  recall_intervals=[2, 3, 2, 1], recall_stagger=stagger, host_tier=sd.host,
-                                 tier=sd.tier, q_dtype=torch.bfloat16, gpu_side_policy=gpu_side))
+                                 tier=sd.tier, q_dtype=qdt, gpu_side_policy=gpu_side))
     out = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
     lw = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
     for step in range(1, steps + 1):
-        qt = torch.randn(L, U * G, D, device="cuda").bfloat16()
-        qp = (qt.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).bfloat16()
+        qt = torch.randn(L, U * G, D, device="cuda").to(qdt)
+        qp = (qt.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).to(qdt)
         co = torch.randn(L, U * G, D, device="cuda")
         cm = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
         kn, vn = torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")
