@@ -305,6 +305,21 @@ int scout_tier_schedule_recall(const scout_tier_layer* layer, int n_units, int n
  * next_tick (= next_run_of(layer), kv_store.hpp:328-331), -1 elsewhere.    */
 int scout_tier_plan(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
                     int next_tick, int32_t* block_table, void* stream);
+/* Bulk prefill of a FRESH layer (the caller side of the decode path): the
+ * state n_tokens[u] append_token calls at clock_step leave
+ * (kv_store.hpp:90-117; the last `capacity` sealed blocks and the open block
+ * fast, the others slow, every mark clock_step), in one pass: the rows
+ * k_rows / v_rows [U][max_tokens][128] f32 go into the pool slots of the
+ * fast blocks (and of warm images of the highest-id slow blocks while free
+ * slots remain), min/max digests [U][2][128][nb_stride] of every block in
+ * the KV dtype, and every sealed block's image to the host tier at
+ * (host_base + u * nb_stride + id) % host_blocks (write-through; host_tier
+ * NULL: none). blk_slot: device scratch [U][nb_stride] int32. Follow with
+ * scout_tier_place for place_after_prefill (kv_store.hpp:271-283).         */
+int scout_tier_prefill(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* n_tokens,
+                       int clock_step, const float* k_rows, const float* v_rows, int max_tokens, void* kv_pool,
+                       int kv_dtype, void* digests, void* host_tier, long long host_base, long long host_blocks,
+                       int32_t* blk_slot, void* stream);
 /* mark_selected (kv_store.hpp:222-228) for explicit ascending id lists
  * (K1 marks its own selections through scout_topk_args.last_selected).     */
 int scout_tier_mark(const scout_tier_layer* layer, int n_units, int nb_stride, const int32_t* ids,

@@ -34,7 +34,7 @@ EXPORTED = (
     "scout_engine_create", "scout_engine_destroy", "scout_engine_decode_step", "scout_engine_decode_step_host",
     "scout_engine_sync", "scout_engine_set_timing", "scout_engine_stats", "scout_engine_k2_times", "scout_engine_k1_outputs",
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
-    "scout_tier_place", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
+    "scout_tier_place", "scout_tier_prefill", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv", "scout_engine_recall_stats",
     "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
     "scout_engine_worker_stats", "scout_engine_check_state", "scout_engine_decode_layer", "scout_engine_decode_layer_x",
@@ -123,6 +123,8 @@ def lib() -> C.CDLL:
         L.scout_tier_plan.argtypes = [_tl, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp]
         L.scout_tier_mark.argtypes = [_tl, C.c_int, C.c_int, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_tier_place.argtypes = [_tl, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int, _vp, _vp]
+        L.scout_tier_prefill.argtypes = [_tl, C.c_int, C.c_int, _vp, C.c_int, _vp, _vp, C.c_int, _vp, C.c_int, _vp,
+                                         _vp, C.c_longlong, C.c_longlong, _vp, _vp]
         L.scout_qpred_workspace_bytes.argtypes = [C.c_int] * 4
         L.scout_qpred_workspace_bytes.restype = C.c_size_t
         L.scout_qpred_pack_weights.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]

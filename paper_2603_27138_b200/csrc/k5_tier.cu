@@ -445,6 +445,137 @@ __global__ void __launch_bounds__(TT) tier_mark_kernel(const scout_tier_layer L,
     }
 }
 
+// ---- bulk prefill (the caller side of the decode path): the state T_u
+// append_token calls at clock_step leave (kv_store.hpp:90-117) on a fresh
+// layer, in one pass. Sealed blocks beyond capacity went slow in id order (all
+// carry the same mark, so the LRU tie-break evicts the lowest id first); the
+// last `capacity` sealed blocks and the open block are fast. The fast blocks
+// take the ring's first entries; the highest-id slow blocks keep warm images
+// in its last entries (eviction order: lowest id reused first). blk_slot[u][b]
+// is the slot that receives block b's rows (fast or warm), else -1.
+__global__ void __launch_bounds__(TT) tier_prefill_state_kernel(const scout_tier_layer L, int nbs,
+                                                                 const int32_t* n_tokens, int clock_step,
+                                                                 int32_t* blk_slot) {
+    const int u = blockIdx.x;
+    Unit U = unit_of(L, u, nbs);
+    const int T = n_tokens[u];
+    const int nb = n_blocks_of(T), ns = T / BS;
+    const int first_fast = L.capacity <= 0 ? 0 : max(0, ns - L.capacity);
+    int32_t* bs = blk_slot + static_cast<size_t>(u) * nbs;
+    for (int b = threadIdx.x; b < nbs; b += TT) {
+        U.tier[b] = b < nb && b >= first_fast;
+        U.last_sel[b] = b < nb ? clock_step : 0;
+        U.ready[b] = -1;
+        U.ticket[b] = 0;
+        U.table[b] = -1;
+        if (U.owner) U.warm[b] = -1;
+        bs[b] = -1;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (T < 0 || nb > nbs || nb - first_fast > *U.n_free) {
+        set_err(U, nb > nbs || T < 0 ? SCOUT_ERR_INVALID_ARGUMENT : SCOUT_ERR_LOGIC);
+        return;
+    }
+    int h = *U.head, n = *U.n_free;
+    for (int b = first_fast; b < nb; ++b) {
+        const int slot = U.free_slots[h];
+        if (U.owner) U.owner[h] = -1;
+        U.table[b] = slot;
+        bs[b] = slot;
+        h = h + 1 == U.S ? 0 : h + 1;
+        --n;
+    }
+    *U.head = h;
+    *U.n_free = n;
+    if (!U.owner) return;
+    const int w = min(n, first_fast);  // warm images: slow blocks first_fast - w .. first_fast - 1
+    for (int i = 0; i < n; ++i) {
+        int p = h + i;
+        if (p >= U.S) p -= U.S;
+        const int o = i - (n - w);  // the last w entries
+        if (o >= 0) {
+            const int b = first_fast - w + o;
+            U.owner[p] = b;
+            U.warm[b] = p;
+            bs[b] = U.free_slots[p];
+        } else {
+            U.owner[p] = -1;
+        }
+    }
+}
+
+// the prefill's rows: one CTA per (block, unit), thread = channel. The block's
+// image is assembled in shared memory in the pool's slot layout, copied into
+// its slot (fast or warm) and, once sealed, to its host-tier image
+// (write-through); the min / max digest folds its rows in order as
+// build_digest does (digest.hpp:34-60).
+template <typename T>
+__global__ void __launch_bounds__(TT) tier_prefill_data_kernel(const int32_t* n_tokens, const float* k_rows,
+                                                                const float* v_rows, int max_tokens,
+                                                                const int32_t* blk_slot, int nbs, uint8_t* pool,
+                                                                void* digests, uint8_t* host_tier,
+                                                                long long host_base, long long host_blocks) {
+    extern __shared__ __align__(16) uint8_t img[];
+    const int b = blockIdx.x, u = blockIdx.y, c = threadIdx.x;
+    const int Tu = n_tokens[u];
+    if (b * BS >= Tu) return;
+    const int rows = min(BS, Tu - b * BS);
+    constexpr size_t tile = static_cast<size_t>(BS) * D;
+    constexpr size_t sbytes = 2 * tile * sizeof(T);
+    T* im = reinterpret_cast<T*>(img);
+    for (int i = c; i < static_cast<int>(sbytes / 16); i += TT) reinterpret_cast<int4*>(img)[i] = make_int4(0, 0, 0, 0);
+    __syncthreads();
+    float lo = 0.f, hi = 0.f;
+    const size_t r0 = (static_cast<size_t>(u) * max_tokens + static_cast<size_t>(b) * BS) * D + c;
+    for (int r = 0; r < rows; ++r) {
+        T kq, vq;
+        float kv;
+        if constexpr (sizeof(T) == 2) {
+            kq = __float2bfloat16_rn(k_rows[r0 + static_cast<size_t>(r) * D]);
+            vq = __float2bfloat16_rn(v_rows[r0 + static_cast<size_t>(r) * D]);
+            kv = __bfloat162float(kq);
+            const int off = bf16_tile_offset(r, c);
+            im[off] = kq;
+            im[tile + off] = vq;
+        } else {
+            kq = k_rows[r0 + static_cast<size_t>(r) * D];
+            vq = v_rows[r0 + static_cast<size_t>(r) * D];
+            kv = kq;
+            im[r * D + c] = kq;
+            im[tile + r * D + c] = vq;
+        }
+        if (r == 0) {
+            lo = kv;
+            hi = kv;
+        } else {  // std::min / std::max fold (digest.hpp:45-46)
+            if (kv < lo) lo = kv;
+            if (hi < kv) hi = kv;
+        }
+    }
+    T* dig = static_cast<T*>(digests) + static_cast<size_t>(u) * 2 * D * nbs;
+    if constexpr (sizeof(T) == 2) {
+        dig[static_cast<size_t>(c) * nbs + b] = __float2bfloat16_rn(lo);
+        dig[static_cast<size_t>(D + c) * nbs + b] = __float2bfloat16_rn(hi);
+    } else {
+        dig[static_cast<size_t>(c) * nbs + b] = lo;
+        dig[static_cast<size_t>(D + c) * nbs + b] = hi;
+    }
+    __syncthreads();
+    const int slot = blk_slot[static_cast<size_t>(u) * nbs + b];
+    const int4* src = reinterpret_cast<const int4*>(img);
+    if (slot >= 0) {
+        int4* dst = reinterpret_cast<int4*>(pool + static_cast<size_t>(slot) * sbytes);
+        for (int i = c; i < static_cast<int>(sbytes / 16); i += TT) dst[i] = src[i];
+    }
+    if (rows == BS && host_tier) {
+        long long hidx = host_base + static_cast<long long>(u) * nbs + b;
+        if (host_blocks > 0) hidx %= host_blocks;
+        int4* dst = reinterpret_cast<int4*>(host_tier + static_cast<size_t>(hidx) * sbytes);
+        for (int i = c; i < static_cast<int>(sbytes / 16); i += TT) dst[i] = src[i];
+    }
+}
+
 int check_layer(const scout_tier_layer* L, int n_units, int nbs, const char* what) {
     using namespace scout_host;
     if (!L || n_units < 0 || nbs <= 0 ||
@@ -516,6 +647,44 @@ extern "C" int scout_tier_place(const scout_tier_layer* L, int n_units, int nb_s
     tier_place_kernel<<<n_units, TT, 0, static_cast<cudaStream_t>(stream)>>>(*L, nb_stride, n_tokens, keep, n_keep,
                                                                              k_stride, fill_slots);
     return scout_host::check_launch("scout_tier_place");
+}
+
+extern "C" int scout_tier_prefill(const scout_tier_layer* L, int n_units, int nb_stride, const int32_t* n_tokens,
+                                  int clock_step, const float* k_rows, const float* v_rows, int max_tokens,
+                                  void* kv_pool, int kv_dtype, void* digests, void* host_tier, long long host_base,
+                                  long long host_blocks, int32_t* blk_slot, void* stream) {
+    int rc = check_layer(L, n_units, nb_stride, "prefill");
+    if (rc != SCOUT_OK || n_units == 0) return rc;
+    if (!n_tokens || !k_rows || !v_rows || !kv_pool || !digests || !blk_slot || max_tokens <= 0 ||
+        (kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32)) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "prefill: bad arguments (bf16 / f32 KV, min/max digests)");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    tier_prefill_state_kernel<<<n_units, TT, 0, st>>>(*L, nb_stride, n_tokens, clock_step, blk_slot);
+    if ((rc = scout_host::check_launch("scout_tier_prefill (state)")) != SCOUT_OK) return rc;
+    uint8_t* hv = nullptr;
+    if (host_tier) {
+        void* d = nullptr;
+        if (cudaHostGetDevicePointer(&d, host_tier, 0) == cudaSuccess && d) hv = static_cast<uint8_t*>(d);
+        else {
+            cudaGetLastError();
+            hv = static_cast<uint8_t*>(host_tier);  // device memory
+        }
+    }
+    const int max_blocks = (max_tokens + BS - 1) / BS;
+    const dim3 grid(max_blocks < nb_stride ? max_blocks : nb_stride, n_units);
+    if (kv_dtype == SCOUT_BF16) {
+        tier_prefill_data_kernel<__nv_bfloat16><<<grid, TT, BF16_SLOT_BYTES, st>>>(
+            n_tokens, k_rows, v_rows, max_tokens, blk_slot, nb_stride, static_cast<uint8_t*>(kv_pool), digests, hv,
+            host_base, host_blocks);
+    } else {
+        scout_host::ensure_smem(reinterpret_cast<const void*>(tier_prefill_data_kernel<float>), F32_SLOT_BYTES);
+        tier_prefill_data_kernel<float><<<grid, TT, F32_SLOT_BYTES, st>>>(
+            n_tokens, k_rows, v_rows, max_tokens, blk_slot, nb_stride, static_cast<uint8_t*>(kv_pool), digests, hv,
+            host_base, host_blocks);
+    }
+    return scout_host::check_launch("scout_tier_prefill (data)");
 }
 
 extern "C" int scout_tier_mark(const scout_tier_layer* L, int n_units, int nb_stride, const int32_t* ids,

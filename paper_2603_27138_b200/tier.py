@@ -187,6 +187,28 @@ class DeviceTieredCache:
             nt.add_(1)
         return open_slot, sealed
 
+    def prefill(self, layer: int, k_rows: torch.Tensor, v_rows: torch.Tensor, n_tokens: torch.Tensor, pool,
+                kv_dtype, digests, host_tier=None, host_blocks=0) -> torch.Tensor:
+        """The state n_tokens[u] append_token calls leave on a fresh layer
+        (kv_store.hpp:90-117), in one pass (scout_tier_prefill): k_rows /
+        v_rows [U][T][128] f32, the pool slots of the fast (and warm) blocks,
+        min/max digests, sealed blocks written through to host_tier at the
+        append path's image indices. Returns blk_slot [U][nb_stride]."""
+        U, nbs = self.U, self.nbs
+        k = k_rows.to(device=self.dev, dtype=torch.float32).contiguous()
+        v = v_rows.to(device=self.dev, dtype=torch.float32).contiguous()
+        self.n_tokens[layer].copy_(n_tokens.to(device=self.dev, dtype=torch.int32))
+        blk = torch.empty((U, nbs), dtype=torch.int32, device=self.dev)
+        desc = self.layer_desc(layer)
+        A.check(A.lib().scout_tier_prefill(C.byref(desc), U, nbs, self.n_tokens[layer].data_ptr(), self.clock_step,
+                                           k.data_ptr(), v.data_ptr(), int(k.shape[1]), pool.data_ptr(),
+                                           ops.dtype_code(kv_dtype), digests.data_ptr(),
+                                           None if host_tier is None else host_tier.data_ptr(),
+                                           layer * U * nbs, int(host_blocks), blk.data_ptr(),
+                                           torch.cuda.current_stream(self.dev).cuda_stream))
+        self.check(layer)
+        return blk
+
     def begin_layer(self, step: int, layer: int) -> int:
         """Advance the clock and apply every due ticket (kv_store.hpp:201-218)."""
         self.clock_step, self.clock_layer = step, layer

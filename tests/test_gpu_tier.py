@@ -234,3 +234,62 @@ def test_tier_place_after_prefill_vs_reference(cuda):
     _compare(dev, refs, 2)
     assert (fill[:, :cap] == -1).all()  # every kept block was already in HBM
     assert (dev.n_free[1].cpu().numpy() == nbs - (cap + 1)).all()  # kept + open block hold slots
+
+
+@pytest.mark.parametrize("kv", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("T,cap", [(1, 3), (63, 3), (64, 3), (65, 2), (9 * BS + 17, 3), (12 * BS, 4), (9 * BS + 17, 0),
+                                   (14 * BS + 5, 3)])
+def test_tier_prefill_matches_token_appends(cuda, kv, T, cap):
+    """scout_tier_prefill (one pass) against T append_token calls (the K0 / K5
+    append path, itself bit-exact against the reference TieredKvCache): the
+    same tier state (and the reference's, compared block by block), the same
+    digests bit for bit, the fast blocks' rows in their slots, every sealed
+    block's host image; warm images hold their block's rows. cap 0: a pinned
+    layer."""
+    U, nbs, spu = 3, 24, 10
+    dev = torch.device("cuda")
+    sb = ops.slot_bytes(kv)
+    k_rows = torch.randn(U, T, 128, device=dev)
+    v_rows = torch.randn(U, T, 128, device=dev)
+    sides = []
+    for _ in range(2):
+        tc = DeviceTieredCache(1, U, nbs, capacity=max(cap, 1), slots_per_unit=nbs if cap == 0 else spu)
+        if cap == 0:
+            tc.pin_layer(0)
+        pool = ops.alloc_pool(tc.n_slots, kv)
+        pool.zero_()
+        dig = torch.zeros(U, 2, 128, nbs, dtype=kv, device=dev)
+        host = torch.zeros(U * nbs * sb, dtype=torch.uint8).pin_memory()
+        sides.append((tc, pool, dig, host))
+    tc, pool, dig, host = sides[0]
+    for t in range(T):
+        tc.append_token(0, k_rows[:, t], v_rows[:, t], pool, kv, dig, host_tier=host)
+    tc2, pool2, dig2, host2 = sides[1]
+    tc2.prefill(0, k_rows, v_rows, torch.full((U,), T, dtype=torch.int32), pool2, kv, dig2, host_tier=host2)
+    torch.cuda.synchronize()
+    ref = P.RefCache(1, 1, max(cap, 1))
+    if cap == 0:
+        ref.pin_layer(0)
+    for _ in range(T):
+        ref.append_token(0, np.zeros(1), np.zeros(1))
+    for side in (tc, tc2):
+        _compare(side, [ref] * U, 1)
+    assert torch.equal(tc.tier, tc2.tier) and torch.equal(tc.last_sel, tc2.last_sel) and torch.equal(tc.ready, tc2.ready)
+    nb = (T + BS - 1) // BS
+    assert torch.equal(dig[..., :nb], dig2[..., :nb])
+    assert torch.equal(host, host2)  # the sealed blocks' images (the open one is not written through)
+    _check_slots(tc2, 1, U, nbs)
+    pv, pv2 = pool.view(-1, sb), pool2.view(-1, sb)
+    for u in range(U):
+        for b in range(nb):
+            rows = min(BS, T - b * BS)
+            s1, s2 = int(tc.table[0, u, b]), int(tc2.table[0, u, b])
+            assert (s1 >= 0) == (s2 >= 0)
+            if s2 >= 0:  # a fast block: its rows in its slot
+                k1, v1 = ops.kv_read_tokens(pool, kv, [s1] * rows, list(range(rows)))
+                k2, v2 = ops.kv_read_tokens(pool2, kv, [s2] * rows, list(range(rows)))
+                assert torch.equal(k1, k2) and torch.equal(v1, v2), (u, b)
+            p = int(tc2.warm[0, u, b])
+            if p >= 0:  # a warm image: the block's host image, byte for byte
+                slot = int(tc2.free_slots[0, u, p])
+                assert torch.equal(pv2[slot].cpu(), host2.view(-1, sb)[u * nbs + b]), (u, b)
