@@ -317,7 +317,8 @@ class TierWorkload:
         if self.engine is not None:
             self.engine.close()
         cfg = self.cfg
-        opts = dict(recall_interval=cfg["recall"], recall_stagger=cfg.get("recall_policy") == "stagger",
+        opts = dict(recall_interval=cfg["recall"], recall_intervals=cfg.get("recall_intervals"),
+                    recall_stagger=cfg.get("recall_policy") == "stagger",
                     cpu_dtype=cfg.get("cpu_dtype", torch.float32), recall_mode=cfg.get("recall_mode", 1),
                     host_units=self.host_units, host_unit0=self.host_unit0)
         opts.update(kw)
@@ -844,6 +845,11 @@ def main():
     ap.add_argument("--warm-seed", default="on", choices=["on", "off"],
                     help="off: the warm slots start empty (no images left by the placement); only evicted "
                          "blocks' images fill them")
+    ap.add_argument("--recall-calibrate", type=int, default=0,
+                    help="device tier mode: profile this many recall-free steps first and calibrate per-layer "
+                         "recall intervals from their CPU ratios (calibrate_intervals, recall.hpp:66-95, the "
+                         "harness's calibrate command); 0 (default): every 16 steps, BASELINE's config")
+    ap.add_argument("--beta", type=float, default=0.12, help="calibration threshold (EngineConfig::beta)")
     ap.add_argument("--q-dtype", default="bf16", choices=["bf16", "f32"],
                     help="query dtype (q_true / q_pred); bf16 = the model's projection output")
     ap.add_argument("--cpu-dtype", default="bf16", choices=["bf16", "f32"],
@@ -904,6 +910,32 @@ def main():
             step_no += 1
             wl.step(step_no)
 
+    calibration = None
+    if tier_mode and args.recall_calibrate > 0:
+        # harness.hpp:464-476: a recall-free profiling run, one RatioTrace sample
+        # per (layer, step) -- here the batch's CPU tokens over its budget -- then
+        # calibrate_intervals(trace, beta) for the measured run
+        from paper_2603_27138_b200.engine import calibrate_intervals
+
+        wl.make_engine(recall_interval=0)
+        cpu_tr, bud_tr = [], []
+        for _ in range(args.recall_calibrate):
+            step_no += 1
+            wl.step(step_no)
+            c_, b_ = wl.engine.cpu_tokens()
+            cpu_tr.append(c_)
+            bud_tr.append(b_)
+        ivals = calibrate_intervals(np.array(cpu_tr).T, np.array(bud_tr).T, args.beta)
+        if ws > 1:  # one schedule for every rank: the shortest interval of each layer
+            t = torch.tensor(ivals, dtype=torch.int64, device=coll_dev(dev))
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+            ivals = [int(x) for x in t.tolist()]
+        cfg["recall_intervals"] = ivals
+        calibration = {"profiling_steps": args.recall_calibrate, "beta": args.beta, "intervals": ivals,
+                       "mean_ratio": [float(np.mean(np.array(cpu_tr)[:, l] / np.array(bud_tr)[:, l]))
+                                      for l in range(wl.L)]}
+        wl.make_engine()
+        log(f"calibrated recall intervals: {ivals}")
     run_steps(args.warmup)
     wl.engine.sync()
     torch.cuda.synchronize(dev)
@@ -1141,6 +1173,7 @@ def main():
             "gpu_launches": launches,
             "verify": verify,
             "tier": tier_info,
+            "recall_calibration": calibration,
             "e2e": e2e,
             "e2e_with_cpu_worker": e2e_worker,
             **extras,

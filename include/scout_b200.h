@@ -384,6 +384,17 @@ int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, const int64
  * 2 = AMX-BF16 tiles, 1 = AVX-512 fp32, 0 = scalar.                        */
 int scout_cpu_coattn_kernel(int kv_dtype);
 
+/* ------------------------------------------------------ recall policy --
+ * calibrate_intervals (recall.hpp:66-95), host only: per layer, the longest
+ * run of leading steps of a recall-free profiling trace whose CPU ratio
+ * cpu_tokens / budget_tokens stays <= beta (a ratio equal to beta counts),
+ * floor 1. cpu_tokens / budget_tokens: [layers][steps] in step order (the
+ * reference records cpu_partial.token_count / k * block_size per (layer,
+ * step), engine.hpp:283; a batched engine's aggregate is
+ * scout_engine_cpu_tokens). beta in (0, 1), every budget > 0.            */
+int scout_calibrate_intervals(const int64_t* cpu_tokens, const int64_t* budget_tokens, int layers, int steps,
+                              double beta, int32_t* intervals);
+
 /* ------------------------------------------------------------- engine --
  * Host-side layer-ahead decode orchestration (ScoutEngine::decode_step,
  * engine.hpp:205-314, GPU side): per layer i, K1 for layer i+1 with the
@@ -566,6 +577,11 @@ int scout_engine_k2_times(scout_engine* eng, float* ms, int max_n, int* n);
  * a warm image in HBM (no bytes moved) and that were copied from the host
  * tier; reset != 0 zeroes the counts. Synchronises the device.            */
 int scout_engine_recall_stats(scout_engine* eng, long long* warm_blocks, long long* copied_blocks, int reset);
+/* The last step's CPU-side tokens per layer summed over the units (K1's
+ * split: the tokens the host co-attention attends) and the matching budget,
+ * U * k * 64 (engine.hpp:189, 283): one RatioTrace sample per layer for
+ * scout_calibrate_intervals. Synchronises.                                 */
+int scout_engine_cpu_tokens(scout_engine* eng, int64_t* cpu_tokens, int64_t* budget_tokens);
 /* In-engine CPU worker (cfg.cpu_worker): the wall time its partials took
  * on the host pool, summed over the steps since the last call, then reset. */
 int scout_engine_worker_stats(scout_engine* eng, double* cpu_ms_total, int* steps);

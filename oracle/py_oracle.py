@@ -98,6 +98,8 @@ def ref():
             L.ref_recall_new.restype = vp
             L.ref_recall_free.argtypes = [vp]
             L.ref_maybe_schedule_recall.argtypes = [vp, C.c_int, C.c_int, ll, _ip, C.c_int, _ip, C.c_int, _ip]
+            if hasattr(L, "ref_calibrate_intervals"):
+                L.ref_calibrate_intervals.argtypes = [_lp, _lp, C.c_int, C.c_int, dbl, _ip]
         _c["r"] = L
     return _c["r"]
 
@@ -335,3 +337,14 @@ def predict_query(x, w):
     if ref().ref_predict_query(x, x.shape[0], w, w.shape[1], out) != 0:
         raise ValueError("predict_next_query")
     return out
+
+
+def ref_calibrate_intervals(cpu, budget, beta):
+    """The reference's calibrate_intervals (recall.hpp:79-95) over a RatioTrace
+    of [layers][steps] samples; None if it threw."""
+    L_ = ref()
+    cpu = np.ascontiguousarray(cpu, dtype=np.int64)
+    bud = np.ascontiguousarray(budget, dtype=np.int64)
+    out = np.zeros(cpu.shape[0], dtype=np.int32)
+    rc = L_.ref_calibrate_intervals(cpu, bud, cpu.shape[0], cpu.shape[1], float(beta), out)
+    return None if rc != 0 else out.tolist()

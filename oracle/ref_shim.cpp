@@ -411,6 +411,24 @@ void* ref_recall_new(int n_units, int layers, const int32_t* intervals, double b
     return r;
 }
 void ref_recall_free(void* h) { delete static_cast<RefRecall*>(h); }
+// calibrate_intervals (recall.hpp:79-95) on a RatioTrace built from
+// [layers][steps] samples (steps 1..steps): 0, or -1 if the reference threw
+int ref_calibrate_intervals(const int64_t* cpu, const int64_t* budget, int layers, int steps, double beta,
+                            int32_t* out) {
+    try {
+        scout::RatioTrace trace(static_cast<size_t>(layers));
+        for (int l = 0; l < layers; ++l)
+            for (int t = 0; t < steps; ++t)
+                trace.record(static_cast<size_t>(l), static_cast<size_t>(t + 1),
+                             static_cast<size_t>(cpu[static_cast<size_t>(l) * steps + t]),
+                             static_cast<size_t>(budget[static_cast<size_t>(l) * steps + t]));
+        const scout::RecallSchedule s = scout::calibrate_intervals(trace, beta);
+        for (int l = 0; l < layers; ++l) out[l] = static_cast<int32_t>(s.intervals[static_cast<size_t>(l)]);
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
 // maybe_schedule_recall for one unit: -1 when the layer is not due (nullopt),
 // else the number of ids of set_difference(predicted, residency) written to out
 int ref_maybe_schedule_recall(void* h, int unit, int layer, long long step, const int32_t* pred, int n_pred,

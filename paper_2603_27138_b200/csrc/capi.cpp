@@ -49,3 +49,37 @@ extern "C" size_t scout_slot_bytes(int kv_dtype) {
     if (kv_dtype == SCOUT_F32) return 2u * 64u * 128u * 4u;
     return 0;
 }
+
+// calibrate_intervals (recall.hpp:66-95) over a recall-free profiling trace:
+// per layer, the longest run of leading steps whose CPU ratio cpu / budget
+// stays at or below beta (equal counts), floor 1. cpu_tokens / budget_tokens
+// [layers][steps] in step order (RatioTrace::record's samples, recall.hpp:29-45).
+extern "C" int scout_calibrate_intervals(const int64_t* cpu_tokens, const int64_t* budget_tokens, int layers,
+                                         int steps, double beta, int32_t* intervals) {
+    using scout_host::set_error;
+    if (!(beta > 0.0) || !(beta < 1.0)) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "calibrate_intervals: beta must be in (0, 1)");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (layers <= 0 || steps <= 0 || !cpu_tokens || !budget_tokens || !intervals) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "calibrate_intervals: no samples");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    for (int l = 0; l < layers; ++l)
+        for (int t = 0; t < steps; ++t)
+            if (budget_tokens[static_cast<size_t>(l) * steps + t] <= 0 || cpu_tokens[static_cast<size_t>(l) * steps + t] < 0) {
+                set_error(SCOUT_ERR_INVALID_ARGUMENT, "RatioTrace::record: zero budget (layer %d, step %d)", l, t);
+                return SCOUT_ERR_INVALID_ARGUMENT;
+            }
+    for (int l = 0; l < layers; ++l) {
+        int n = 0;
+        while (n < steps) {
+            const size_t i = static_cast<size_t>(l) * steps + n;
+            const double ratio = static_cast<double>(cpu_tokens[i]) / static_cast<double>(budget_tokens[i]);
+            if (!(ratio <= beta)) break;
+            ++n;
+        }
+        intervals[l] = n > 1 ? n : 1;
+    }
+    return SCOUT_OK;
+}

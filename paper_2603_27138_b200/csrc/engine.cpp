@@ -1736,6 +1736,24 @@ extern "C" int scout_engine_recall_stats(scout_engine* e, long long* warm_blocks
     return SCOUT_OK;
 }
 
+extern "C" int scout_engine_cpu_tokens(scout_engine* e, int64_t* cpu_tokens, int64_t* budget_tokens) {
+    if (!e || !cpu_tokens || e->token == 0) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_cpu_tokens: no step yet");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    const int L = e->cfg.layers, par = e->token & 1;
+    std::vector<int32_t> h(static_cast<size_t>(L) * e->U);
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(h.data(), e->I(e->cpu_tok[par]), h.size() * 4, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < L; ++l) {
+        int64_t t = 0;
+        for (int u = 0; u < e->U; ++u) t += h[static_cast<size_t>(l) * e->U + u];
+        cpu_tokens[l] = t;
+        if (budget_tokens) budget_tokens[l] = static_cast<int64_t>(e->U) * e->cfg.k * SCOUT_BLOCK_SIZE;
+    }
+    return SCOUT_OK;
+}
+
 extern "C" int scout_engine_stats(scout_engine* e, double* k2_ms_total, int* k2_count, long long* launches) {
     if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
     double tot = 0.0;

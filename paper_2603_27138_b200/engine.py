@@ -197,6 +197,14 @@ class DecodeEngine:
         A.check(A.lib().scout_engine_recall_stats(self._h, C.byref(w), C.byref(c), int(bool(reset))))
         return int(w.value), int(c.value)
 
+    def cpu_tokens(self):
+        """(cpu tokens per layer summed over the units, budget U * k * 64) of the
+        last step: one RatioTrace sample per layer (engine.hpp:283)."""
+        cpu = (C.c_int64 * self.L)()
+        bud = (C.c_int64 * self.L)()
+        A.check(A.lib().scout_engine_cpu_tokens(self._h, C.cast(cpu, C.c_void_p), C.cast(bud, C.c_void_p)))
+        return list(cpu), list(bud)
+
     def k2_times(self, max_n=4096):
         """Per-launch K2 durations (ms) of the current timing window (before stats())."""
         buf = (C.c_float * max_n)()
@@ -240,3 +248,16 @@ class _DeviceArray:
 
 
 __all__ = ["DecodeEngine", "LayerState"]
+
+
+def calibrate_intervals(cpu_tokens, budget_tokens, beta=0.12):
+    """calibrate_intervals (recall.hpp:66-95) on a recall-free trace:
+    cpu_tokens / budget_tokens [layers][steps] -> per-layer intervals."""
+    import numpy as np
+
+    cpu = np.ascontiguousarray(cpu_tokens, dtype=np.int64)
+    bud = np.ascontiguousarray(budget_tokens, dtype=np.int64)
+    L, S = cpu.shape
+    out = np.zeros(L, dtype=np.int32)
+    A.check(A.lib().scout_calibrate_intervals(cpu.ctypes.data, bud.ctypes.data, L, S, float(beta), out.ctypes.data))
+    return out.tolist()

@@ -415,3 +415,48 @@ def test_engine_layerwise_with_query_prediction(cuda):
             assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
     for e in engs:
         e.check_state()
+
+
+def test_engine_cpu_tokens_and_calibration(cuda):
+    """scout_engine_cpu_tokens: the last step's CPU-side tokens per layer (the
+    RatioTrace sample of engine.hpp:283, summed over the units) equal K1's own
+    per-unit counts; a recall-free trace of them calibrates per-layer
+    intervals (recall.hpp:66-95) that the engine then runs with."""
+    from paper_2603_27138_b200.engine import calibrate_intervals
+
+    L, batch, hkv, G, k, cap, nbs = 3, 2, 2, 4, 6, 8, 24
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 11 + 50
+    torch.manual_seed(17)
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    sd = Side(L, U, nbs, cap, kv, seed_rows)
+    layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+    mk = lambda **kw: DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens,  # noqa: E731
+                                   pool=sd.pool, kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D),
+                                   host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, **kw)
+    eng = mk(recall_interval=0)
+    out = [torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")]
+    cm = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
+    co = torch.randn(L, U * G, D, device="cuda")
+    cpu_tr, bud_tr = [], []
+    for step in range(1, 13):
+        qt = torch.randn(L, U * G, D, device="cuda").bfloat16()
+        qp = (qt.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).bfloat16()
+        eng.decode_step_kv(step, qt, qp, co, cm, torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda"),
+                           *out)
+        c, b = eng.cpu_tokens()
+        k1 = eng.k1_outputs()
+        assert c == k1["cpu_tokens"].sum(1).tolist() and b == [U * k * 64] * L
+        cpu_tr.append(c)
+        bud_tr.append(b)
+    ivals = calibrate_intervals(np.array(cpu_tr).T, np.array(bud_tr).T, 0.12)
+    assert len(ivals) == L and all(1 <= x <= 12 for x in ivals)
+    eng.close()
+    eng = mk(recall_interval=0, recall_intervals=ivals)
+    for step in range(13, 25):
+        qt = torch.randn(L, U * G, D, device="cuda").bfloat16()
+        eng.decode_step_kv(step, qt, qt, co, cm, torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda"),
+                           *out)
+    eng.sync()
+    eng.check_state()
