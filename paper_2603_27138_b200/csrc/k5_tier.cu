@@ -454,8 +454,8 @@ __global__ void __launch_bounds__(TT) tier_mark_kernel(const scout_tier_layer L,
 // in its last entries (eviction order: lowest id reused first). blk_slot[u][b]
 // is the slot that receives block b's rows (fast or warm), else -1.
 __global__ void __launch_bounds__(TT) tier_prefill_state_kernel(const scout_tier_layer L, int nbs,
-                                                                 const int32_t* n_tokens, int clock_step,
-                                                                 int32_t* blk_slot) {
+                                                                 const int32_t* n_tokens, int max_tokens,
+                                                                 int clock_step, int32_t* blk_slot) {
     const int u = blockIdx.x;
     Unit U = unit_of(L, u, nbs);
     const int T = n_tokens[u];
@@ -473,8 +473,9 @@ __global__ void __launch_bounds__(TT) tier_prefill_state_kernel(const scout_tier
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
-    if (T < 0 || nb > nbs || nb - first_fast > *U.n_free) {
-        set_err(U, nb > nbs || T < 0 ? SCOUT_ERR_INVALID_ARGUMENT : SCOUT_ERR_LOGIC);
+    if (T < 0 || T > max_tokens || nb > nbs || nb - first_fast > *U.n_free) {
+        set_err(U, nb - first_fast > *U.n_free && T <= max_tokens && nb <= nbs && T >= 0 ? SCOUT_ERR_LOGIC
+                                                                                       : SCOUT_ERR_INVALID_ARGUMENT);
         return;
     }
     int h = *U.head, n = *U.n_free;
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(TT) tier_prefill_data_kernel(const int32_t* n_
     extern __shared__ __align__(16) uint8_t img[];
     const int b = blockIdx.x, u = blockIdx.y, c = threadIdx.x;
     const int Tu = n_tokens[u];
-    if (b * BS >= Tu) return;
+    if (b * BS >= Tu || Tu > max_tokens || b >= nbs) return;  // (an oversized count is the state kernel's error)
     const int rows = min(BS, Tu - b * BS);
     constexpr size_t tile = static_cast<size_t>(BS) * D;
     constexpr size_t sbytes = 2 * tile * sizeof(T);
@@ -661,7 +662,7 @@ extern "C" int scout_tier_prefill(const scout_tier_layer* L, int n_units, int nb
         return SCOUT_ERR_INVALID_ARGUMENT;
     }
     auto st = static_cast<cudaStream_t>(stream);
-    tier_prefill_state_kernel<<<n_units, TT, 0, st>>>(*L, nb_stride, n_tokens, clock_step, blk_slot);
+    tier_prefill_state_kernel<<<n_units, TT, 0, st>>>(*L, nb_stride, n_tokens, max_tokens, clock_step, blk_slot);
     if ((rc = scout_host::check_launch("scout_tier_prefill (state)")) != SCOUT_OK) return rc;
     uint8_t* hv = nullptr;
     if (host_tier) {

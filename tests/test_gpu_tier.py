@@ -293,3 +293,15 @@ def test_tier_prefill_matches_token_appends(cuda, kv, T, cap):
             if p >= 0:  # a warm image: the block's host image, byte for byte
                 slot = int(tc2.free_slots[0, u, p])
                 assert torch.equal(pv2[slot].cpu(), host2.view(-1, sb)[u * nbs + b]), (u, b)
+
+
+def test_tier_prefill_rejects_counts_beyond_rows(cuda):
+    """A token count beyond the rows given (or the stride) is the unit's
+    invalid-argument error, and no row is read past the end."""
+    dev = torch.device("cuda")
+    tc = DeviceTieredCache(1, 2, 8, capacity=2, slots_per_unit=8)
+    pool = ops.alloc_pool(tc.n_slots, torch.bfloat16)
+    dig = torch.zeros(2, 2, 128, 8, dtype=torch.bfloat16, device=dev)
+    k = torch.randn(2, 100, 128, device=dev)
+    with pytest.raises(ValueError):
+        tc.prefill(0, k, k, torch.tensor([100, 101], dtype=torch.int32), pool, torch.bfloat16, dig)
