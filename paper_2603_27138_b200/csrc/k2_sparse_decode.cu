@@ -71,8 +71,18 @@ constexpr int NCOMB = 2;                    // combiner warps (segments alternat
 constexpr int NTHREADS = NCT + 32 * (2 + NCOMB);  // + producer, planner and combiner warps
 constexpr int NST = 2 * NPAIR;              // ring stages
 constexpr int STAGE_BYTES = 32768;          // one block: K tile (16 KiB) + V tile (16 KiB)
-constexpr int MAXSEG = 64;                  // segments per plan chunk
-constexpr int MAXB = 384;                   // blocks per plan chunk
+#ifndef SCOUT_K2_NPLAN
+#define SCOUT_K2_NPLAN 2
+#endif
+#ifndef SCOUT_K2_MAXSEG
+#define SCOUT_K2_MAXSEG 64
+#endif
+#ifndef SCOUT_K2_MAXB
+#define SCOUT_K2_MAXB 384
+#endif
+constexpr int NPLAN = SCOUT_K2_NPLAN;       // plan chunk buffers (the planner runs NPLAN - 1 chunks ahead)
+constexpr int MAXSEG = SCOUT_K2_MAXSEG;     // segments per plan chunk
+constexpr int MAXB = SCOUT_K2_MAXB;         // blocks per plan chunk
 constexpr int CB_ROW = D;  // combine rows (no pad: the conflicted state stores are once per segment)
 constexpr size_t SMEM_BYTES = static_cast<size_t>(NST) * STAGE_BYTES;
 
@@ -110,12 +120,12 @@ struct Plan {
 struct Smem {
     uint64_t full[NST];
     uint64_t empty[NST];
-    uint64_t plan_full[2];
-    uint64_t plan_empty[2];
+    uint64_t plan_full[NPLAN];
+    uint64_t plan_empty[NPLAN];
     uint64_t seg_full[NCOMB];  // the NC consumer warps left a segment's states (segment s: combiner s % NCOMB)
     uint64_t seg_empty;        // its combiner has read them
     int layer_fin[K2_MAX_LAYERS];  // combiners done with layer L (the last one counts the CTA in)
-    Plan plan[2];
+    Plan plan[NPLAN];
     int warp_area[NC];   // 1: the warp left a state in wstate, -1: no state
     // per-warp segment states (o^T rows, m, l), merged by the combiner warp
     // while the consumers go on with the next segment
@@ -279,9 +289,9 @@ __device__ void finalize_unit_warp(const void* cpu_o, bool co_bf16, const float*
 // The plan buffer of chunk c, once every role has released its previous use.
 __device__ __forceinline__ Plan& plan_acquire(Smem& sm, int c, long long& waited, bool prof) {
     const long long t0 = prof ? clock64() : 0;
-    if (c >= 2) mbar_wait(&sm.plan_empty[c & 1], ((c >> 1) - 1) & 1);
+    if (c >= NPLAN) mbar_wait(&sm.plan_empty[c % NPLAN], ((c / NPLAN) - 1) & 1);
     if (prof) waited += clock64() - t0;
-    return sm.plan[c & 1];
+    return sm.plan[c % NPLAN];
 }
 
 // Finish chunk c (its segment pieces are written): pull the query rows of the
@@ -290,7 +300,7 @@ __device__ __forceinline__ Plan& plan_acquire(Smem& sm, int c, long long& waited
 template <typename Args>
 __device__ void plan_publish(const Args& a, const K2Layer& io, Smem& sm, int c, int nseg, int nblk, int jbase,
                              int layer, int flags, int lane) {
-    Plan& P = sm.plan[c & 1];
+    Plan& P = sm.plan[c % NPLAN];
     __syncwarp();  // lane 0's segment records
     {
         const int qbytes = a.group * D * (a.q_bf16 ? 2 : 4);
@@ -342,7 +352,7 @@ __device__ void plan_publish(const Args& a, const K2Layer& io, Smem& sm, int c, 
         P.flags = flags;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.plan_full[c & 1]);
+    if (lane == 0) mbar_arrive(&sm.plan_full[c % NPLAN]);
 }
 
 // Planner (one warp): this CTA's share of layer `layer`'s resident blocks, as
@@ -482,7 +492,7 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgsT<NL> a
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 2);  // both warps of the owning pair release
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NPLAN; ++i) {
             mbar_init(&sm.plan_full[i], 1);
             mbar_init(&sm.plan_empty[i], NC + 1 + NCOMB);  // every consumer warp, the producer and the combiners
         }
@@ -533,9 +543,9 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgsT<NL> a
         long long t_plan = 0, t_empty = 0;  // SCOUT_K2_PROF: cycles blocked on a plan / a free stage
         const long long t_start = clock64();
         for (int c = 0;; ++c) {
-            const int b = c & 1;
+            const int b = c % NPLAN;
             long long t0 = a.prof ? clock64() : 0;
-            mbar_wait(&sm.plan_full[b], (c >> 1) & 1);
+            mbar_wait(&sm.plan_full[b], (c / NPLAN) & 1);
             const int L = sm.plan[b].layer, fl = sm.plan[b].flags;
             const K2Layer& io = a.layers[L];
             // blocks recalled for this layer one step ago must have landed
@@ -587,8 +597,8 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgsT<NL> a
         long long k_wait = 0, k_busy = 0, tq = 0;
         int segidx = 0;  // segments flushed by the consumers (pieces ending one)
         for (int c = 0;; ++c) {
-            const int b = c & 1;
-            mbar_wait(&sm.plan_full[b], (c >> 1) & 1);
+            const int b = c % NPLAN;
+            mbar_wait(&sm.plan_full[b], (c / NPLAN) & 1);
             const Plan& P = sm.plan[b];
             const int L = P.layer, fl = P.flags;
             const K2Layer& io = a.layers[L];
@@ -755,9 +765,9 @@ __global__ void __maxnreg__(144) sparse_decode_tc_kernel(const K2StepArgsT<NL> a
     int held = -1;  // stage of the pair's last block: handed back at the next block or the segment end
     bool any = false;
     for (int c = 0;; ++c) {
-        const int b = c & 1;
+        const int b = c % NPLAN;
         if (a.prof) tp = clock64();
-        mbar_wait(&sm.plan_full[b], (c >> 1) & 1);
+        mbar_wait(&sm.plan_full[b], (c / NPLAN) & 1);
         if (a.prof) c_plan += clock64() - tp;
         const Plan& P = sm.plan[b];
         const int nsegs = P.nsegs, jbase = P.jbase, L = P.layer, fl = P.flags;
