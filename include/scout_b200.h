@@ -577,6 +577,18 @@ int scout_engine_k2_times(scout_engine* eng, float* ms, int max_n, int* n);
  * a warm image in HBM (no bytes moved) and that were copied from the host
  * tier; reset != 0 zeroes the counts. Synchronises the device.            */
 int scout_engine_recall_stats(scout_engine* eng, long long* warm_blocks, long long* copied_blocks, int reset);
+/* ScoutEngine::prefill + place_after_prefill (engine.hpp:192-201), device
+ * tier mode, on FRESH tier state: every layer filled from the model's rows
+ * k_rows / v_rows [L][U][max_tokens][128] f32 with n_tokens[u] tokens per
+ * unit (device) by scout_tier_prefill (slots, digests into the layers'
+ * digest arrays, write-through to the host tier), the engine's token counts
+ * set to n_tokens; then, with q_place [L][U*G][128] (q dtype, the layers'
+ * last prefill queries; NULL: skip), every unpinned layer keeps its
+ * top-capacity sealed blocks fast, the promoted blocks' images taken from
+ * warm slots or gathered from the host tier (required then). Allocates
+ * scratch and synchronises. Once per engine (a second call: LOGIC).       */
+int scout_engine_prefill(scout_engine* eng, const float* k_rows, const float* v_rows, const int32_t* n_tokens,
+                         int max_tokens, const void* q_place, void* stream);
 /* The last step's CPU-side tokens per layer summed over the units (K1's
  * split: the tokens the host co-attention attends) and the matching budget,
  * U * k * 64 (engine.hpp:189, 283): one RatioTrace sample per layer for

@@ -773,6 +773,7 @@ struct scout_engine {
     //    bookkeeping ends (planned_step); a step number out of sequence (or the
     //    first step) plans here.
     int planned_step = -1;
+    bool prefilled = false;  // scout_engine_prefill ran (ScoutEngine::prefilled_)
     int tier_pre(int step, int par, const void* q_true, const void* q_pred, cudaStream_t s) {
         const int L = cfg.layers, nbs = cfg.nb_stride;
         int rc;
@@ -1733,6 +1734,108 @@ extern "C" int scout_engine_recall_stats(scout_engine* e, long long* warm_blocks
     }
     if (warm_blocks) *warm_blocks = static_cast<long long>(h[0]);
     if (copied_blocks) *copied_blocks = static_cast<long long>(h[1]);
+    return SCOUT_OK;
+}
+
+// ScoutEngine::prefill + place_after_prefill (engine.hpp:192-201) on the
+// engine's device tier state: every layer's fresh state filled from the
+// model's rows in one pass (scout_tier_prefill: the state of the token-by-token
+// appends, the rows, the digests, the write-through), then for every unpinned
+// layer the top-capacity sealed blocks by the layer's last prefill query kept
+// fast (K1 over the sealed blocks + scout_tier_place). Not a hot call: it
+// allocates scratch and synchronises.
+extern "C" int scout_engine_prefill(scout_engine* e, const float* k_rows, const float* v_rows, const int32_t* n_tokens,
+                                    int max_tokens, const void* q_place, void* stream) {
+    using scout_host::set_error;
+    if (!e || !e->tier_mode || !k_rows || !v_rows || !n_tokens || max_tokens <= 0) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_prefill: needs a device tier engine, rows and counts");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (e->prefilled) {  // engine.hpp:194
+        set_error(SCOUT_ERR_LOGIC, "scout_engine_prefill: prefill already done");
+        return SCOUT_ERR_LOGIC;
+    }
+    auto st = static_cast<cudaStream_t>(stream);
+    const int L = e->cfg.layers, U = e->U, nbs = e->cfg.nb_stride;
+    int kmax = 1;
+    for (int l = 0; l < L; ++l) kmax = std::max(kmax, e->tier[l].capacity);
+    if (kmax > SCOUT_MAX_K) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_prefill: capacity %d > %d", kmax, SCOUT_MAX_K);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    if (q_place && !e->cfg.host_tier) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "scout_engine_prefill: placement fills from the host tier");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    Buf blk, sealed, keep, nkeep, fill;
+    if (blk.alloc(static_cast<size_t>(U) * nbs * 4) || sealed.alloc(static_cast<size_t>(U) * 4) ||
+        keep.alloc(static_cast<size_t>(U) * kmax * 4) || nkeep.alloc(static_cast<size_t>(U) * 4) ||
+        fill.alloc(static_cast<size_t>(U) * kmax * 4)) {
+        set_error(SCOUT_ERR_CUDA, "scout_engine_prefill: scratch");
+        return SCOUT_ERR_CUDA;
+    }
+    int32_t* ntok = const_cast<int32_t*>(e->cfg.n_tokens);
+    CU(cudaMemcpyAsync(ntok, n_tokens, static_cast<size_t>(U) * 4, cudaMemcpyDeviceToDevice, st));
+    const size_t layer_rows = static_cast<size_t>(U) * max_tokens * SCOUT_HEAD_DIM;
+    int rc;
+    for (int l = 0; l < L; ++l) {
+        ++e->launches;
+        if ((rc = scout_tier_prefill(&e->tier[l], U, nbs, ntok, 0, k_rows + l * layer_rows, v_rows + l * layer_rows,
+                                     max_tokens, e->cfg.kv_pool, e->cfg.kv_dtype, const_cast<void*>(e->layers[l].digests),
+                                     const_cast<void*>(e->cfg.host_tier), e->host_row(l, 0), e->cfg.host_blocks,
+                                     e->I(blk), st)) != SCOUT_OK)
+            return rc;
+    }
+    if (q_place) {
+        std::vector<int32_t> h(U);
+        CU(cudaMemcpyAsync(h.data(), ntok, static_cast<size_t>(U) * 4, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        for (auto& t : h) t = t / SCOUT_BLOCK_SIZE * SCOUT_BLOCK_SIZE;  // the sealed blocks (kv_store.hpp:273-276)
+        CU(cudaMemcpyAsync(sealed.p, h.data(), static_cast<size_t>(U) * 4, cudaMemcpyHostToDevice, st));
+        for (int l = 0; l < L; ++l) {
+            const int cap = e->tier[l].capacity;
+            if (cap <= 0) continue;  // pinned
+            scout_topk_args a{};
+            a.n_units = U;
+            a.group = e->G;
+            a.digest_dtype = e->cfg.kv_dtype;
+            a.method = SCOUT_DIGEST_MINMAX;
+            a.k = cap;
+            a.k_stride = cap;
+            a.nb_stride = nbs;
+            a.q = e->qlayer(q_place, l);
+            a.digests = e->layers[l].digests;
+            a.n_tokens = e->I(sealed);
+            a.sel_ids = e->I(keep);
+            a.n_sel = e->I(nkeep);
+            a.q_dtype = e->cfg.q_dtype;
+            e->launches += 3;
+            if ((rc = scout_score_topk_split(&a, st)) != SCOUT_OK) return rc;
+            if ((rc = scout_tier_place(&e->tier[l], U, nbs, ntok, e->I(keep), e->I(nkeep), cap, e->I(fill), st)) !=
+                SCOUT_OK)
+                return rc;
+            // the promoted blocks' images: warm slots (fill <= -2) already hold
+            // them, the others come from their written-through host images
+            if ((rc = scout_recall_gather_ids(e->cfg.kv_pool, e->cfg.kv_dtype, e->cfg.host_tier, e->host_row(l, 0), nbs,
+                                              e->cfg.host_blocks, U, e->I(keep), e->I(nkeep), e->I(fill), cap, 0,
+                                              st)) != SCOUT_OK)
+                return rc;
+        }
+    }
+    CU(cudaStreamSynchronize(st));
+    e->prefilled = true;
+    e->planned_step = -1;  // the next step plans from the new state
+    std::vector<int32_t> err(U);
+    for (int l = 0; l < L; ++l) {
+        CU(cudaMemcpy(err.data(), e->tier[l].err, static_cast<size_t>(U) * 4, cudaMemcpyDeviceToHost));
+        for (int u = 0; u < U; ++u)
+            if (err[u]) {
+                set_error(err[u] == SCOUT_ERR_INVALID_ARGUMENT ? SCOUT_ERR_INVALID_ARGUMENT : SCOUT_ERR_LOGIC,
+                          "scout_engine_prefill: layer %d unit %d: tier error %d (a layer that was not fresh, or too "
+                          "few slots)", l, u, err[u]);
+                return err[u] == SCOUT_ERR_INVALID_ARGUMENT ? SCOUT_ERR_INVALID_ARGUMENT : SCOUT_ERR_LOGIC;
+            }
+    }
     return SCOUT_OK;
 }
 

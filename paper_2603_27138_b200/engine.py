@@ -197,6 +197,16 @@ class DecodeEngine:
         A.check(A.lib().scout_engine_recall_stats(self._h, C.byref(w), C.byref(c), int(bool(reset))))
         return int(w.value), int(c.value)
 
+    def prefill(self, k_rows, v_rows, n_tokens, q_place=None):
+        """ScoutEngine::prefill + place_after_prefill (engine.hpp:192-201) on
+        fresh tier state: k_rows / v_rows [L][U][T][128] f32 device, n_tokens
+        [U], q_place [L][U*G][128] (q dtype) or None."""
+        k = k_rows.float().contiguous()
+        v = v_rows.float().contiguous()
+        nt = n_tokens.to(device=k.device, dtype=torch.int32).contiguous()
+        qp = None if q_place is None else q_place.contiguous()
+        A.check(A.lib().scout_engine_prefill(self._h, _p(k), _p(v), _p(nt), int(k.shape[2]), _p(qp), self._stream()))
+
     def cpu_tokens(self):
         """(cpu tokens per layer summed over the units, budget U * k * 64) of the
         last step: one RatioTrace sample per layer (engine.hpp:283)."""

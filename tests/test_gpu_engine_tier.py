@@ -460,3 +460,113 @@ def test_engine_cpu_tokens_and_calibration(cuda):
                            *out)
     eng.sync()
     eng.check_state()
+
+
+@pytest.mark.parametrize("kv", [torch.bfloat16, torch.float32])
+def test_engine_prefill_matches_mirror_prefill_and_place(cuda, kv):
+    """scout_engine_prefill (ScoutEngine::prefill + place_after_prefill,
+    engine.hpp:192-201) against the same composition through the tier mirror
+    (DeviceTieredCache.prefill per layer, place_after_prefill with K1 on the
+    unpinned layers, the promoted blocks gathered from the host tier): the
+    same tier state, digests, host images and fast-block contents, with ragged
+    per-unit prefill lengths; then identical decode steps with recalls."""
+    L, batch, hkv, G, k, cap, nbs, steps = 3, 2, 2, 4, 6, 8, 24, 30
+    U = batch * hkv
+    qdt = torch.bfloat16 if kv == torch.bfloat16 else torch.float32
+    T = 64 * 13 + 17
+    torch.manual_seed(23)
+    n_tok = torch.tensor([T, 64 * 12, 64 * 9 + 63, 64 * 11 + 1], dtype=torch.int32, device="cuda")
+    k_rows = torch.randn(L, U, T, D, device="cuda")
+    v_rows = torch.randn(L, U, T, D, device="cuda")
+    q_place = torch.randn(L, U * G, D, device="cuda").to(qdt)
+    dev = torch.device("cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    sides, engs = [], []
+    for _ in range(2):
+        tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=nbs)
+        tier.pin_layer(0)
+        sd = type("S", (), {})()
+        sd.tier, sd.pool = tier, ops.alloc_pool(L * U * nbs, kv)
+        sd.dig = [torch.zeros(U, 2, D, nbs, dtype=kv, device=dev) for _ in range(L)]
+        sd.host = torch.zeros(L * U * nbs * ops.slot_bytes(kv), dtype=torch.uint8).pin_memory()
+        sd.n_tokens = torch.zeros(U, dtype=torch.int32, device=dev)
+        layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device=dev)) for i in range(L)]
+        engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
+                                 kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=3,
+                                 host_tier=sd.host, tier=tier, q_dtype=qdt))
+        sides.append(sd)
+    m = sides[0]  # the mirror composition
+    for i in range(L):
+        m.tier.prefill(i, k_rows[i], v_rows[i], n_tok, m.pool, kv, m.dig[i], host_tier=m.host)
+    for i in range(1, L):
+        _, fill = m.tier.place_after_prefill(i, q_place[i], m.dig[i], G, kv)
+        r = ops.score_topk_split(q_place[i], m.dig[i], ((m.tier.n_tokens[i] // BS) * BS).contiguous(), cap, G)
+        A.check(A.lib().scout_recall_gather_ids(m.pool.data_ptr(), ops.dtype_code(kv), m.host.data_ptr(), i * U * nbs,
+                                                nbs, 0, U, r["sel_ids"].data_ptr(), r["n_sel"].data_ptr(),
+                                                fill.data_ptr(), cap, 0, st))
+    m.n_tokens.copy_(n_tok)
+    engs[1].prefill(k_rows, v_rows, n_tok, q_place)
+    torch.cuda.synchronize()
+    e = sides[1]
+    assert torch.equal(e.n_tokens, n_tok)
+    for name in ("tier", "table", "last_sel", "free_head", "free_owner", "warm"):
+        a, b = getattr(m.tier, name), getattr(e.tier, name)
+        if a is not None:
+            assert torch.equal(a, b), name
+    for i in range(L):
+        assert torch.equal(m.dig[i], e.dig[i]), i
+    assert torch.equal(m.host, e.host)
+    # the fast blocks' contents: every block on the fast tier holds its rows
+    sb = ops.slot_bytes(kv)
+    pm, pe = m.pool.view(torch.uint8).view(-1, sb), e.pool.view(torch.uint8).view(-1, sb)
+    tab = m.tier.table.cpu()
+    fast = m.tier.tier.cpu()
+    for i in range(L):
+        for u in range(U):
+            nb = (int(n_tok[u]) + BS - 1) // BS
+            for b in range(nb):
+                if fast[i, u, b]:
+                    s = int(tab[i, u, b])
+                    assert torch.equal(pm[s], pe[s]), (i, u, b)
+    assert int(e.tier.err.abs().sum()) == 0
+    with pytest.raises(A.ScoutError):  # engine.hpp:194: prefill already done
+        engs[1].prefill(k_rows, v_rows, n_tok, q_place)
+    # identical decode steps from the two states
+    outs = [[torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")] for _ in range(2)]
+    for step in range(1, steps + 1):
+        qt = torch.randn(L, U * G, D, device="cuda").to(qdt)
+        qp = (qt.float() + 0.3 * torch.randn(L, U * G, D, device="cuda")).to(qdt)
+        co = torch.randn(L, U * G, D, device="cuda")
+        cm = torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1], -1).contiguous()
+        kn, vn = torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")
+        for eng, o in zip(engs, outs):
+            eng.decode_step_kv(step, qt, qp, co, cm, kn, vn, *o)
+        for eng in engs:
+            eng.sync()
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]), step
+        for name in ("tier", "last_sel"):
+            assert torch.equal(getattr(m.tier, name), getattr(e.tier, name)), (step, name)
+    for eng in engs:
+        eng.check_state()
+
+
+def test_engine_prefill_rejects_bad_calls(cuda):
+    """scout_engine_prefill's argument checks: a prefill longer than the rows
+    it is given fails loudly (the tier's sticky error, reported by the call)."""
+    L, batch, hkv, G, k, cap, nbs = 2, 1, 2, 4, 6, 8, 16
+    U = batch * hkv
+    kv = torch.bfloat16
+    tier = DeviceTieredCache(L, U, nbs, capacity=cap, slots_per_unit=nbs)
+    tier.pin_layer(0)
+    pool = ops.alloc_pool(L * U * nbs, kv)
+    dig = [torch.zeros(U, 2, D, nbs, dtype=kv, device="cuda") for _ in range(L)]
+    host = torch.zeros(L * U * nbs * ops.slot_bytes(kv), dtype=torch.uint8).pin_memory()
+    n_tokens = torch.zeros(U, dtype=torch.int32, device="cuda")
+    layers = [LayerState(dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+    eng = DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=n_tokens, pool=pool, kv_dtype=kv,
+                       layer_states=layers, scale=1 / math.sqrt(D), recall_interval=0, host_tier=host, tier=tier,
+                       q_dtype=torch.bfloat16)
+    rows = torch.randn(L, U, 100, D, device="cuda")
+    with pytest.raises(ValueError):
+        eng.prefill(rows, rows, torch.tensor([100, 101], dtype=torch.int32), None)
