@@ -1,3 +1,4 @@
+"""One K6 (q-prediction GEMM) launch at Qwen3-32B shape, for an ncu capture (round_check.sh)."""
 import sys
 sys.path[:0] = ["."]
 import torch
