@@ -39,6 +39,7 @@
 #include "cpu_coattn.h"
 #include "k1_batch.h"
 #include "k2_step.h"
+#include "k4_batch.h"
 #include "k5_batch.h"
 
 namespace scout_host {
@@ -136,8 +137,9 @@ struct scout_engine {
     }
     Buf ws;  // per-layer K2 workspaces
     size_t ws_layer = 0;
-    Buf flags;  // k1_flag[L] | k1_ctr[L] | recall_flag[L] | layer_done[L] | in_flag[nch]
-    unsigned *k1_flag = nullptr, *k1_ctr = nullptr, *recall_flag = nullptr, *layer_done = nullptr, *in_flag = nullptr;
+    Buf flags;  // k1_flag[L] | k1_ctr[L] | recall_flag[L] | layer_done[L] | in_flag[nch] | rc_ctr[L]
+    unsigned *k1_flag = nullptr, *k1_ctr = nullptr, *recall_flag = nullptr, *layer_done = nullptr, *in_flag = nullptr,
+             *rc_ctr = nullptr;
     unsigned token = 0;  // number of steps launched
     std::vector<unsigned> rc_token;  // per layer: token of its last recall (0: none)
     // recall cadence (engine.hpp:35, recall.hpp:97-126): per-layer interval
@@ -320,6 +322,7 @@ struct scout_engine {
                 if (ev) cudaEventDestroy(ev);
         if (ev_post) cudaEventDestroy(ev_post);
         if (ev_pre) cudaEventDestroy(ev_pre);
+        if (ev_rcg) cudaEventDestroy(ev_rcg);
         if (post_s) cudaStreamDestroy(post_s);
         if (rc_pinned) cudaFreeHost(rc_pinned);
         for (cudaStream_t s : {k1s, side, h2d, d2h, rc_list})
@@ -875,7 +878,6 @@ struct scout_engine {
     }
     int post_chunk(int step, unsigned tok, int c, int lo, int n) {
         TierPostArgs& pa = pa_step;
-        const int nbs = cfg.nb_stride;
         for (int i = lo; i < lo + n; ++i) pa.recall_due[i] = recall_due(step, i);
         int rc;
         if ((rc = wait_value(post_s, layer_done + lo + n - 1, tok * static_cast<unsigned>(grid))) != SCOUT_OK) return rc;
@@ -912,18 +914,14 @@ struct scout_engine {
             }
             rc_cv.notify_one();
         } else {
-            CU(cudaEventRecord(ev_chunk[slot][c], post_s));
-            CU(cudaStreamWaitEvent(side, ev_chunk[slot][c], 0));
-            for (int i = lo; i < lo + n; ++i) {
-                if (!pa.recall_due[i]) continue;
-                ++launches;
-                if ((rc = scout_recall_gather_ids(cfg.kv_pool, cfg.kv_dtype, cfg.host_tier,
-                                                  host_row(i, 0), nbs, cfg.host_blocks, U,
-                                                  pa.rc_ids + lk(i), pa.rc_n + lu(i), pa.dst + lk(i), cfg.k, 0,
-                                                  side)) != SCOUT_OK)
-                    return rc;
-                if ((rc = write_value(side, recall_flag + i, tok)) != SCOUT_OK) return rc;
-            }
+            // SM gather: the step's due layers go out in one launch after its
+            // last chunk (post_end). Gathers cannot run beside the persistent
+            // K2 (it holds every SM) nor ahead of the next K1's grid anyway,
+            // and one launch per layer cost ~16 us each after K1 (64 layers:
+            // ~0.7 ms on the step after a recall, most of them with nothing
+            // to copy once the victim cache serves the recall)
+            for (int i = lo; i < lo + n; ++i)
+                if (pa.recall_due[i]) rc_gather_layers.push_back(i);
         }
         for (int i = lo; i < lo + n; ++i) {
             if (!pa.recall_due[i]) continue;
@@ -932,9 +930,36 @@ struct scout_engine {
         }
         return SCOUT_OK;
     }
+    std::vector<int> rc_gather_layers;  // this step's due layers (SM gather), launched by post_end
+    cudaEvent_t ev_rcg = nullptr;
     int post_end(int step, cudaStream_t s) {
-        ++launches;
         int rc;
+        if (!rc_gather_layers.empty()) {
+            CU(cudaEventRecord(ev_rcg, post_s));  // after every chunk's post launch
+            CU(cudaStreamWaitEvent(side, ev_rcg, 0));
+            for (size_t b = 0; b < rc_gather_layers.size(); b += K4_MAX_LAYERS) {
+                RecallLayersArgs ra{};
+                ra.pool = static_cast<uint8_t*>(cfg.kv_pool);
+                ra.nb_stride = cfg.nb_stride;
+                ra.n_units = U;
+                ra.k_stride = cfg.k;
+                ra.host_blocks = cfg.host_blocks;
+                ra.host_base0 = host_row(0, 0);
+                ra.host_layer_stride = host_row(1, 0) - host_row(0, 0);
+                ra.ids = pa_step.rc_ids;
+                ra.n_ids = pa_step.rc_n;
+                ra.dst = pa_step.dst;
+                ra.flags = recall_flag;
+                ra.ctr = rc_ctr;
+                ra.token = token;
+                for (size_t j = b; j < rc_gather_layers.size() && ra.n < K4_MAX_LAYERS; ++j)
+                    ra.layer[ra.n++] = static_cast<int16_t>(rc_gather_layers[j]);
+                ++launches;
+                if ((rc = scout_recall_gather_layers(ra, cfg.host_tier, cfg.kv_dtype, 0, side)) != SCOUT_OK) return rc;
+            }
+            rc_gather_layers.clear();
+        }
+        ++launches;
         if ((rc = scout_tier_advance(const_cast<int32_t*>(cfg.n_tokens), U, post_s)) != SCOUT_OK) return rc;
         planned_step = step + 1;
         // the next step (planning, K1) follows the bookkeeping
@@ -1074,7 +1099,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     if (c.kv_dtype == SCOUT_F32)  // per-layer launches of the f32 path (scout_sparse_decode)
         e->ws_layer = std::max(e->ws_layer, (scout_sparse_decode_workspace_bytes(e->U, e->G, c.max_ctas) + 255) / 256 * 256);
     bad |= e->ws.alloc(e->ws_layer * c.layers);
-    const size_t nflags = 4 * static_cast<size_t>(c.layers) + e->nch;
+    const size_t nflags = 5 * static_cast<size_t>(c.layers) + e->nch;
     bad |= e->flags.alloc(nflags * 4);
     if (!bad && (cudaMemset(e->ws.p, 0, e->ws_layer * c.layers) != cudaSuccess ||
                  cudaMemset(e->flags.p, 0, nflags * 4) != cudaSuccess))
@@ -1097,6 +1122,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     e->recall_flag = f + 2 * c.layers;
     e->layer_done = f + 3 * c.layers;
     e->in_flag = f + 4 * c.layers;
+    e->rc_ctr = f + 4 * c.layers + e->nch;
     e->rc_token.assign(c.layers, 0u);
     e->rc_int.assign(c.layers, 0);
     for (int l = 0; l < c.layers; ++l) e->rc_int[l] = c.recall_intervals ? c.recall_intervals[l] : c.recall_interval;
@@ -1172,6 +1198,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
             for (auto& ev : row) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&e->ev_post, cudaEventDisableTiming);
         cudaEventCreateWithFlags(&e->ev_pre, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&e->ev_rcg, cudaEventDisableTiming);
         cudaStreamCreateWithFlags(&e->post_s, cudaStreamNonBlocking);
     }
     if (any_recall) e->rc_thread = std::thread([e] { e->recall_loop(); });

@@ -10,6 +10,7 @@
 // only flags: whole block images from device-mapped pinned host memory into
 // freed pool slots, on a side stream, 16-byte loads over PCIe / C2C.
 #include "scout_common.cuh"
+#include "k4_batch.h"
 
 #include <math_constants.h>
 
@@ -188,6 +189,50 @@ __global__ void __launch_bounds__(256) recall_ids_kernel(uint8_t* pool, const ui
     }
 }
 
+// every due layer of a step in one launch (k4_batch.h): blockIdx.y picks the
+// layer, the CTAs of a layer loop over its units as recall_ids_kernel does;
+// the last CTA of a layer to finish publishes the layer's flag (release
+// after a fence, so the next K2 sees the copies once it sees the flag)
+__global__ void __launch_bounds__(256) recall_layers_kernel(const RecallLayersArgs a) {
+    const int layer = a.layer[blockIdx.y];
+    const int nvec = static_cast<int>(a.slot_bytes / 16);
+    const size_t lu = static_cast<size_t>(layer) * a.n_units;
+    const long long hbase = a.host_base0 + static_cast<long long>(layer) * a.host_layer_stride;
+    for (int u = blockIdx.x; u < a.n_units; u += gridDim.x) {
+        const int n = a.n_ids[lu + u];
+        const size_t row = (lu + u) * a.k_stride;
+        for (int i = 0; i < n; ++i) {
+            const int slot = a.dst[row + i];
+            if (slot < 0) continue;  // a warm slot (its image is in place) or a rejected ticket
+            const long long hb = host_index(hbase, u, a.nb_stride, a.ids[row + i], a.host_blocks);
+            const int4* s = reinterpret_cast<const int4*>(a.host + static_cast<size_t>(hb) * a.slot_bytes);
+            int4* d = reinterpret_cast<int4*>(a.pool + static_cast<size_t>(slot) * a.slot_bytes);
+            for (int base = threadIdx.x; base < nvec; base += 4 * blockDim.x) {
+                int4 v[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int idx = base + k * blockDim.x;
+                    if (idx < nvec) v[k] = __ldcv(s + idx);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int idx = base + k * blockDim.x;
+                    if (idx < nvec) d[idx] = v[k];
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(a.ctr + layer, 1u) == gridDim.x - 1) {
+            a.ctr[layer] = 0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.flags + layer), "r"(a.token) : "memory");
+        }
+    }
+}
+
 // seal write-through: the block unit u sealed (sealed_id[u] >= 0, slot
 // open_slot[u]) is copied to its host-tier image, which becomes the slow copy
 __global__ void __launch_bounds__(256) writeback_kernel(const uint8_t* pool, uint8_t* host, long long host_base,
@@ -232,6 +277,21 @@ extern "C" int scout_recall_gather_ids(void* kv_pool, int kv_dtype, const void* 
         static_cast<uint8_t*>(kv_pool), static_cast<const uint8_t*>(device_view(host_tier)), host_base, nb_stride,
         host_blocks, ids, n_ids, dst_slots, k_stride, slot_bytes(kv_dtype), n_units);
     return check_launch("scout_recall_gather_ids");
+}
+
+int scout_recall_gather_layers(RecallLayersArgs a, const void* host_tier, int kv_dtype, int ctas, cudaStream_t st) {
+    using namespace scout_host;
+    if ((kv_dtype != SCOUT_BF16 && kv_dtype != SCOUT_F32) || a.n < 1 || a.n > K4_MAX_LAYERS || a.n_units < 1 ||
+        !host_tier || !a.pool || !a.flags || !a.ctr) {
+        set_error(SCOUT_ERR_INVALID_ARGUMENT, "recall gather (layers): bad arguments");
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    a.host = static_cast<const uint8_t*>(device_view(host_tier));
+    a.slot_bytes = slot_bytes(kv_dtype);
+    int grid = ctas > 0 ? ctas : 32;
+    if (grid > a.n_units) grid = a.n_units;
+    recall_layers_kernel<<<dim3(grid, a.n), 256, 0, st>>>(a);
+    return check_launch("recall gather (layers)");
 }
 
 extern "C" int scout_kv_writeback(const void* kv_pool, int kv_dtype, void* host_tier, long long host_base, int nb_stride,
