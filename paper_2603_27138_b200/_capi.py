@@ -36,6 +36,7 @@ EXPORTED = (
     "scout_tier_append", "scout_tier_apply", "scout_tier_schedule_recall", "scout_tier_plan", "scout_tier_mark",
     "scout_tier_place", "scout_tier_prefill", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv", "scout_engine_recall_stats", "scout_engine_cpu_tokens", "scout_calibrate_intervals", "scout_engine_prefill",
+    "scout_engine_overlap_stats", "scout_engine_set_overlap",
     "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
     "scout_engine_worker_stats", "scout_engine_check_state", "scout_engine_decode_layer", "scout_engine_decode_layer_x",
 )
@@ -161,6 +162,8 @@ def lib() -> C.CDLL:
         L.scout_engine_recall_stats.argtypes = [_vp, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong), C.c_int]
         L.scout_engine_cpu_tokens.argtypes = [_vp, _vp, _vp]
         L.scout_engine_prefill.argtypes = [_vp, _vp, _vp, _vp, C.c_int, _vp, _vp]
+        L.scout_engine_overlap_stats.argtypes = [_vp, _vp, _vp, C.c_int]
+        L.scout_engine_set_overlap.argtypes = [_vp, C.c_int]
         L.scout_calibrate_intervals.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_double, _vp]
         L.scout_engine_k1_outputs.argtypes = [_vp] + [C.POINTER(_vp)] * 7
         L.scout_engine_worker_stats.argtypes = [_vp, C.POINTER(C.c_double), C.POINTER(C.c_int)]

@@ -137,9 +137,10 @@ struct scout_engine {
     }
     Buf ws;  // per-layer K2 workspaces
     size_t ws_layer = 0;
-    Buf flags;  // k1_flag[L] | k1_ctr[L] | recall_flag[L] | layer_done[L] | in_flag[nch] | rc_ctr[L]
+    Buf flags;  // k1_flag[L] | k1_ctr[L] | recall_flag[L] | layer_done[L] | in_flag[nch] | rc_ctr[L] |
+                // k1_all_ctr | k1_all_flag
     unsigned *k1_flag = nullptr, *k1_ctr = nullptr, *recall_flag = nullptr, *layer_done = nullptr, *in_flag = nullptr,
-             *rc_ctr = nullptr;
+             *rc_ctr = nullptr, *k1_all_ctr = nullptr, *k1_all_flag = nullptr;
     unsigned token = 0;  // number of steps launched
     std::vector<unsigned> rc_token;  // per layer: token of its last recall (0: none)
     // recall cadence (engine.hpp:35, recall.hpp:97-126): per-layer interval
@@ -390,7 +391,7 @@ struct scout_engine {
     // layer in the layer-by-layer mode
     int launch_k2(int par, const void* const* q, const void* const* co, const float* const* cml, float* const* o,
                   float* const* ml, const unsigned* const* inflag, bool poll_k1, cudaStream_t st, int l0 = 0,
-                  int n = -1, int ctas = 0) {
+                  int n = -1, int ctas = 0, bool records = true) {
         if (n < 0) n = cfg.layers;
         K2StepArgs a{};
         a.n_units = U;
@@ -489,7 +490,81 @@ struct scout_engine {
         ++launches;
         const int rc = scout_k2_launch(a, st, false);
         if (rc != SCOUT_OK) return rc;
-        if (timing) CU(cudaEventRecord(e1, st));
+        k2_e1 = e1;
+        // records = false: the caller queues K1 right behind this launch as
+        // its programmatic dependent (nothing may sit between them in the
+        // stream) and records afterwards (k2_records)
+        return records ? k2_records(par, st) : SCOUT_OK;
+    }
+    cudaEvent_t k2_e1 = nullptr;
+    bool k1k2_loaded = false;  // K1 and K2 have launched once (their modules are loaded)
+    int ov_setting = -1;       // scout_engine_set_overlap: -1 environment / default, 0 off, > 0 K1's SMs
+    long long ov_steps = 0;    // overlapped steps since the last scout_engine_overlap_stats reset
+    int ov_last_sms = 0;
+    // The overlapped step (K1 beside K2, §6.1 of DESIGN.md): how many SMs K1
+    // gets this step, 0 = the ordinary order. K2 runs on the rest of the grid,
+    // polling K1's per-layer flags; K1 is K2's programmatic dependent (a
+    // persistent grid on the SMs K2 leaves, publishing without waiting for
+    // it), so K1's digest stream runs under K2's instead of before it.
+    // Conditions: bf16 KV, the predicted-top-k policy, no ticket due this
+    // step (begin_layer's application follows K1's marks and precedes the
+    // layer's post), the full grid, K1's register-resident paths (<= 1024
+    // blocks per unit: the 2048-block variant streams too slowly on a third
+    // of the SMs), and one ordinary step first (a kernel's first launch loads
+    // its module, which would wait for the running K2 that waits for it).
+    // SCOUT_K1K2_OVERLAP=<SMs> overrides the default (35% of the grid), 0 disables.
+    int overlap_sms(int step) const {
+        static const bool serialising = [] {
+            // kernel-serialising tools (a profiler / sanitizer injected into the
+            // process, or blocking launches) would run K2 to its end before K1
+            // starts: K2 would wait for K1's flags until its 10 s trap
+            const char* inj = getenv("CUDA_INJECTION64_PATH");
+            const char* blk = getenv("CUDA_LAUNCH_BLOCKING");
+            return (inj && *inj) || (blk && atoi(blk) != 0);
+        }();
+        static const int env_sms = [] {
+            const char* v = getenv("SCOUT_K1K2_OVERLAP");
+            return v ? atoi(v) : -1;
+        }();
+        const int want = ov_setting >= 0 ? ov_setting : env_sms;  // -1: the default share
+        if (serialising || !k1k2_loaded || want == 0 || !tier_mode || all_res || cfg.kv_dtype != SCOUT_BF16 || cfg.max_ctas > 0 ||
+            cfg.nb_stride > 1024 || grid < 100)
+            return 0;
+        for (int i = 0; i < cfg.layers; ++i)
+            if (pending[i] >= 0 && pending[i] <= tick(step, i)) return 0;
+        const int sms = want > 0 ? want : (grid * 35 + 50) / 100;
+        return sms < grid ? sms : 0;
+    }
+    // plan (when due) on st, then on ks: K2 over the grid less `sms`, K1 as its
+    // programmatic dependent, the K2 records. ev_pre (after the plan) gates
+    // the post launches; done = true publishes k1_all_flag once K1 is complete.
+    int overlapped_pair(int step, int par, int sms, const void* q_true, const void* q_pred, const void* const* q,
+                        const void* const* co, const float* const* cml, float* const* o, float* const* ml,
+                        const unsigned* const* inflag, cudaStream_t st, cudaStream_t ks, bool done) {
+        const int L = cfg.layers;
+        int rc;
+        if (planned_step != step) {
+            ++launches;
+            if ((rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(tier_dev.p), L, U, cfg.nb_stride,
+                                             cfg.n_tokens, step, I(plan_tab), st)) != SCOUT_OK)
+                return rc;
+        }
+        CU(cudaEventRecord(ev_pre, st));
+        if (ks != st) CU(cudaStreamWaitEvent(ks, ev_pre, 0));
+        if ((rc = launch_k2(par, q, co, cml, o, ml, inflag, true, ks, 0, L, grid - sms, false)) != SCOUT_OK) return rc;
+        std::vector<scout_topk_args> v(L);
+        for (int i = 0; i < L; ++i) v[i] = k1_args(i, i == 0 ? q_true : qlayer(q_pred, i), step, par);
+        ++launches;
+        if ((rc = scout_k1_launch_batch_beside(v.data(), L, sms, ks, done ? k1_all_ctr : nullptr,
+                                               done ? k1_all_flag : nullptr, token)) != SCOUT_OK)
+            return rc;
+        ++ov_steps;
+        ov_last_sms = sms;
+        return k2_records(par, ks);
+    }
+    int k2_records(int par, cudaStream_t st) {
+        if (timing && k2_e1) CU(cudaEventRecord(k2_e1, st));
+        k2_e1 = nullptr;
         CU(cudaEventRecord(ev_k2[par], st));
         k2_recorded[par] = true;
         return SCOUT_OK;
@@ -1099,7 +1174,7 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     if (c.kv_dtype == SCOUT_F32)  // per-layer launches of the f32 path (scout_sparse_decode)
         e->ws_layer = std::max(e->ws_layer, (scout_sparse_decode_workspace_bytes(e->U, e->G, c.max_ctas) + 255) / 256 * 256);
     bad |= e->ws.alloc(e->ws_layer * c.layers);
-    const size_t nflags = 5 * static_cast<size_t>(c.layers) + e->nch;
+    const size_t nflags = 5 * static_cast<size_t>(c.layers) + e->nch + 2;
     bad |= e->flags.alloc(nflags * 4);
     if (!bad && (cudaMemset(e->ws.p, 0, e->ws_layer * c.layers) != cudaSuccess ||
                  cudaMemset(e->flags.p, 0, nflags * 4) != cudaSuccess))
@@ -1123,6 +1198,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
     e->layer_done = f + 3 * c.layers;
     e->in_flag = f + 4 * c.layers;
     e->rc_ctr = f + 4 * c.layers + e->nch;
+    e->k1_all_ctr = e->rc_ctr + c.layers;
+    e->k1_all_flag = e->k1_all_ctr + 1;
     e->rc_token.assign(c.layers, 0u);
     e->rc_int.assign(c.layers, 0);
     for (int l = 0; l < c.layers; ++l) e->rc_int[l] = c.recall_intervals ? c.recall_intervals[l] : c.recall_interval;
@@ -1415,6 +1492,39 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     // go out to the host worker. Device tier mode: planning view + K1 + ticket
     // application (the previous step's bookkeeping is ordered by ev_start)
     CU(cudaStreamWaitEvent(e->k1s, e->chunk_ev[0], 0));
+    const bool have_cpu = h_cpu_o != nullptr || e->cw_on;
+    std::vector<const void*> q(L);
+    std::vector<const void*> co(L);
+    std::vector<const float*> cml(L);
+    std::vector<float*> o(L), ml(L);
+    std::vector<const unsigned*> inflag(L);
+    for (int i = 0; i < L; ++i) {
+        q[i] = g.qt + i * qd * qb;
+        co[i] = have_cpu ? g.co + i * qd * cb : nullptr;
+        cml[i] = have_cpu ? g.cm + i * md : nullptr;
+        o[i] = g.o + i * qd;
+        ml[i] = g.oml + i * md;
+        inflag[i] = e->in_flag + i / CH;
+    }
+    const size_t id_bytes = static_cast<size_t>(L) * e->U * e->cfg.k * 4, n_bytes = static_cast<size_t>(L) * e->U * 4;
+    // the overlapped step (scout_engine::overlap_sms; not with the in-engine
+    // worker, which takes K1's CPU-side ids while K2 runs)
+    const int ov = e->cw_on ? 0 : e->overlap_sms(step);
+    if (ov > 0) {
+        if ((rc = e->overlapped_pair(step, par, ov, g.qt, g.qp, q.data(), co.data(), cml.data(), o.data(), ml.data(),
+                                     inflag.data(), e->k1s, e->k1s, h_cpu_ids != nullptr)) != SCOUT_OK)
+            return rc;
+        if (h_cpu_ids) {  // K1's CPU-side ids once every layer published (K2 may still run)
+            if ((rc = wait_value(e->d2h, e->k1_all_flag, token)) != SCOUT_OK) return rc;
+            CU(cudaMemcpyAsync(h_cpu_ids, e->I(e->cpu_ids[par]), id_bytes, cudaMemcpyDeviceToHost, e->d2h));
+            if (h_n_cpu) CU(cudaMemcpyAsync(h_n_cpu, e->I(e->n_cpu[par]), n_bytes, cudaMemcpyDeviceToHost, e->d2h));
+        }
+        CU(cudaStreamWaitEvent(st, e->ev_k2[par], 0));
+    } else {
+    // ---- K1 for every layer in one launch once q_pred landed (in steady state
+    // it was copied while the previous step's K2 ran); the CPU-side ids then
+    // go out to the host worker. Device tier mode: planning view + K1 + ticket
+    // application (the previous step's bookkeeping is ordered by ev_start)
     if (e->tier_mode) {
         rc = e->tier_pre(step, par, g.qt, g.qp, e->k1s);
         if (rc == SCOUT_OK && cudaEventRecord(e->ev_pre, e->k1s) != cudaSuccess) rc = SCOUT_ERR_CUDA;
@@ -1423,7 +1533,6 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
         if (rc == SCOUT_OK && e->all_res) rc = e->resident_lists(par, 0, L, e->k1s);
     }
     if (rc != SCOUT_OK) return rc;
-    const size_t id_bytes = static_cast<size_t>(L) * e->U * e->cfg.k * 4, n_bytes = static_cast<size_t>(L) * e->U * 4;
     if (h_cpu_ids || e->cw_on) {
         CU(cudaEventRecord(e->ev_k1[0], e->k1s));
         CU(cudaStreamWaitEvent(e->d2h, e->ev_k1[0], 0));
@@ -1445,23 +1554,11 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     CU(cudaEventRecord(e->ev_k1_end, e->k1s));
     CU(cudaStreamWaitEvent(st, e->ev_k1_end, 0));
     // ---- K2: one launch; layer i waits for its input chunk's flag on the device
-    const bool have_cpu = h_cpu_o != nullptr || e->cw_on;
-    std::vector<const void*> q(L);
-    std::vector<const void*> co(L);
-    std::vector<const float*> cml(L);
-    std::vector<float*> o(L), ml(L);
-    std::vector<const unsigned*> inflag(L);
-    for (int i = 0; i < L; ++i) {
-        q[i] = g.qt + i * qd * qb;
-        co[i] = have_cpu ? g.co + i * qd * cb : nullptr;
-        cml[i] = have_cpu ? g.cm + i * md : nullptr;
-        o[i] = g.o + i * qd;
-        ml[i] = g.oml + i * md;
-        inflag[i] = e->in_flag + i / CH;
-    }
     if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), false, st)) !=
         SCOUT_OK)
         return rc;
+    if (e->tier_mode) e->k1k2_loaded = true;
+    }
     if (e->tier_mode) {
         CU(cudaStreamWaitEvent(e->post_s, e->ev_kvin, 0));  // the token's K/V landed
         if ((rc = e->tier_post(step, par, token, g.kn, g.vn, e->ev_pre, st)) != SCOUT_OK) return rc;
@@ -1515,11 +1612,6 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
             if (!ev) cudaEventCreate(&ev);
     }
     if (phases) cudaEventRecord(pe[0], st);
-    // 1-3. planning view, select + split + mark, begin_layer's ticket application
-    if ((rc = e->tier_pre(step, par, q_true, q_pred, st)) != SCOUT_OK) return rc;
-    CU(cudaEventRecord(e->ev_pre, st));
-    if (phases) cudaEventRecord(pe[1], st);
-    // 4. attention + merge over all layers (one persistent launch)
     std::vector<const void*> q(L);
     std::vector<const void*> co(L);
     std::vector<const float*> cml(L);
@@ -1531,8 +1623,26 @@ extern "C" int scout_engine_decode_step_kv(scout_engine* e, int step, const void
         o[i] = out_o + i * qd;
         ml[i] = out_ml + i * md;
     }
-    if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, false, st)) != SCOUT_OK)
-        return rc;
+    // the overlapped step (scout_engine::overlap_sms) on the engine's own
+    // stream: a programmatic launch needs its primary in the same stream, and
+    // the caller's stream may carry other work between them
+    const int ov = phases ? 0 : e->overlap_sms(step);
+    if (ov > 0) {
+        if ((rc = e->overlapped_pair(step, par, ov, q_true, q_pred, q.data(), co.data(), cml.data(), o.data(),
+                                     ml.data(), nullptr, st, e->k1s, false)) != SCOUT_OK)
+            return rc;
+        CU(cudaStreamWaitEvent(st, e->ev_k2[par], 0));
+    } else {
+        // 1-3. planning view, select + split + mark, begin_layer's ticket application
+        if ((rc = e->tier_pre(step, par, q_true, q_pred, st)) != SCOUT_OK) return rc;
+        CU(cudaEventRecord(e->ev_pre, st));
+        if (phases) cudaEventRecord(pe[1], st);
+        // 4. attention + merge over all layers (one persistent launch)
+        if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, false, st)) !=
+            SCOUT_OK)
+            return rc;
+        e->k1k2_loaded = true;
+    }
     if (phases) cudaEventRecord(pe[2], st);
     // 5-6. append + write-through + recall scheduling, then the recall copies
     if ((rc = e->tier_post(step, par, token, k_new, v_new, e->ev_pre, st)) != SCOUT_OK) return rc;
@@ -1898,6 +2008,20 @@ extern "C" int scout_engine_stats(scout_engine* e, double* k2_ms_total, int* k2_
     if (launches) *launches = e->launches;
     e->tev_used = 0;
     e->launches = 0;
+    return SCOUT_OK;
+}
+
+extern "C" int scout_engine_set_overlap(scout_engine* e, int k1_sms) {
+    if (!e || k1_sms < -1) return SCOUT_ERR_INVALID_ARGUMENT;
+    e->ov_setting = k1_sms;
+    return SCOUT_OK;
+}
+
+extern "C" int scout_engine_overlap_stats(scout_engine* e, long long* steps, int* k1_sms, int reset) {
+    if (!e) return SCOUT_ERR_INVALID_ARGUMENT;
+    if (steps) *steps = e->ov_steps;
+    if (k1_sms) *k1_sms = e->ov_last_sms;
+    if (reset) e->ov_steps = 0;
     return SCOUT_OK;
 }
 

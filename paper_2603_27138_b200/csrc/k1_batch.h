@@ -18,9 +18,19 @@ struct K1BatchT {
     int chunk;  // digest chunk bytes (set at launch)
     int persist;  // persistent grid over (layer, unit) items (set at launch)
     int direct;   // bf16 digests read straight from global memory, no ring (set at launch)
+    int nowait;   // publish without griddepcontrol.wait (launched as a programmatic dependent of a
+                  // grid that itself waits for this one's flags: the overlapped step)
+    int slots;    // > 0: persistent grid of exactly this many CTAs; < 0: resident CTAs on -slots SMs
+    unsigned* all_ctr;   // optional: layers published so far (reset by the last)
+    unsigned* all_flag;  // optional: = all_token once every layer of the launch has published
+    unsigned all_token;
     scout_topk_args a[NA];
 };
 using K1Batch = K1BatchT<K1_MAX_LAYERS>;
 using K1Batch1 = K1BatchT<1>;
 
 int scout_k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st);
+// the overlapped step's K1: a persistent grid on `sms` SMs, launched as a
+// programmatic dependent of the running K2, publishing without waiting for it
+int scout_k1_launch_batch_beside(const scout_topk_args* layers, int n, int sms, cudaStream_t st,
+                                 unsigned* all_ctr = nullptr, unsigned* all_flag = nullptr, unsigned all_token = 0);

@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (NA == 1 ? 4 : (QPT == 1 
     }
     __syncthreads();
 
-    griddep_wait();  // everything before this launch is complete: safe to publish
+    if (!batch.nowait) griddep_wait();  // everything before this launch is complete: safe to publish
     // ---- selection flags in id order: contiguous chunks per thread
     const int chunk = (nb + K1_THREADS - 1) / K1_THREADS;
     const int b_begin = min(nb, tid * chunk), b_end = min(nb, b_begin + chunk);
@@ -840,6 +840,12 @@ __global__ void __launch_bounds__(K1_THREADS, DIRECT ? (NA == 1 ? 4 : (QPT == 1 
                 *a.done_ctr = 0u;
                 __threadfence();
                 asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.done_flag), "r"(a.done_token) : "memory");
+                if (batch.all_flag && atomicAdd(batch.all_ctr, 1u) == static_cast<unsigned>(batch.n) - 1u) {
+                    *batch.all_ctr = 0u;  // every layer published: the launch's lists are complete
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(batch.all_flag), "r"(batch.all_token)
+                                 : "memory");
+                }
             }
         }
     }
@@ -893,7 +899,13 @@ int launch_g(K1BatchT<NA>& b, cudaStream_t st) {
         // persistent grid: resident CTAs x SMs, when the items outnumber them
         const long long items = static_cast<long long>(a.n_units) * b.n;
         long long slots = 0;
-        if (MODE == 0 && persist_env) {  // (occupancy queried only for the opt-in persistent grid)
+        if (b.slots > 0) {
+            slots = b.slots;
+        } else if (b.slots < 0) {  // resident CTAs on -slots SMs
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K1_THREADS, smem);
+            slots = static_cast<long long>(per_sm > 0 ? per_sm : 1) * -b.slots;
+        } else if (MODE == 0 && persist_env) {  // (occupancy queried only for the opt-in persistent grid)
             int per_sm = 0;
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, K1_THREADS, smem);
             int dev = 0, sms = 148;
@@ -901,7 +913,7 @@ int launch_g(K1BatchT<NA>& b, cudaStream_t st) {
             cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
             slots = static_cast<long long>(per_sm > 0 ? per_sm : 1) * sms;
         }
-        b.persist = MODE == 0 && persist_env && items > slots;
+        b.persist = b.slots != 0 || (MODE == 0 && persist_env && items > slots);
         const dim3 grid = b.persist ? dim3(static_cast<unsigned>(slots)) : dim3(a.n_units, b.n);
         scout_host::launch(kern, grid, dim3(K1_THREADS), smem, st, (a.flags & SCOUT_LAUNCH_PDL) != 0, b);
     };
@@ -974,6 +986,11 @@ int launch_batch(K1Batch& b, cudaStream_t st) {
         // single layer: the 1-slot parameter block
         static thread_local K1Batch1 b1;
         b1.n = 1;
+        b1.nowait = b.nowait;
+        b1.slots = b.slots;
+        b1.all_ctr = b.all_ctr;
+        b1.all_flag = b.all_flag;
+        b1.all_token = b.all_token;
         b1.a[0] = a;
         if (a.digest_dtype == SCOUT_BF16) rc = launch_g<__nv_bfloat16, 0>(b1, st);
         else if (a.digest_dtype == SCOUT_F32) rc = launch_g<float, 0>(b1, st);
@@ -1005,11 +1022,36 @@ extern "C" int scout_score_topk_split(const scout_topk_args* args, void* stream)
     if (args->n_units == 0) return SCOUT_OK;
     static thread_local K1Batch b;  // kernel parameters (copied at launch)
     b.n = 1;
+    b.nowait = 0;
+    b.slots = 0;
+    b.all_ctr = b.all_flag = nullptr;
     b.a[0] = *args;
     return launch_batch(b, static_cast<cudaStream_t>(stream));
 }
 
+static int k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st, int slots, int nowait,
+                           unsigned* all_ctr, unsigned* all_flag, unsigned all_token);
+
 int scout_k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st) {
+    return k1_launch_batch(layers, n, st, 0, 0, nullptr, nullptr, 0);
+}
+
+int scout_k1_launch_batch_beside(const scout_topk_args* layers, int n, int sms, cudaStream_t st, unsigned* all_ctr,
+                                 unsigned* all_flag, unsigned all_token) {
+    if (sms <= 0 || (all_flag && !all_ctr)) {
+        scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "K1 beside K2: %d SMs", sms);
+        return SCOUT_ERR_INVALID_ARGUMENT;
+    }
+    for (int i = 0; i < n; ++i)
+        if (!layers[i].done_flag || !layers[i].done_ctr) {
+            scout_host::set_error(SCOUT_ERR_INVALID_ARGUMENT, "K1 beside K2: every layer publishes a flag");
+            return SCOUT_ERR_INVALID_ARGUMENT;
+        }
+    return k1_launch_batch(layers, n, st, -sms, 1, all_ctr, all_flag, all_token);
+}
+
+static int k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st, int slots, int nowait,
+                           unsigned* all_ctr, unsigned* all_flag, unsigned all_token) {
     using namespace scout_host;
     if (n < 1 || n > K1_MAX_LAYERS) {
         set_error(SCOUT_ERR_INVALID_ARGUMENT, "K1 batch: %d layers (max %d)", n, K1_MAX_LAYERS);
@@ -1028,7 +1070,13 @@ int scout_k1_launch_batch(const scout_topk_args* layers, int n, cudaStream_t st)
     if (layers[0].n_units == 0) return SCOUT_OK;
     static thread_local K1Batch b;
     b.n = n;
+    b.nowait = nowait;
+    b.slots = slots;
+    b.all_ctr = all_ctr;
+    b.all_flag = all_flag;
+    b.all_token = all_token;
     for (int i = 0; i < n; ++i) b.a[i] = layers[i];
+    if (nowait) b.a[0].flags |= SCOUT_LAUNCH_PDL;
     return launch_batch(b, st);
 }
 

@@ -207,6 +207,17 @@ class DecodeEngine:
         qp = None if q_place is None else q_place.contiguous()
         A.check(A.lib().scout_engine_prefill(self._h, _p(k), _p(v), _p(nt), int(k.shape[2]), _p(qp), self._stream()))
 
+    def set_overlap(self, k1_sms: int):
+        """The overlapped step's K1 share: -1 environment / default, 0 off, > 0 SMs."""
+        A.check(A.lib().scout_engine_set_overlap(self._h, int(k1_sms)))
+
+    def overlap_stats(self, reset=False):
+        """(steps run with K1 beside K2 since the last reset, K1's SM share of
+        the last one): scout_engine_overlap_stats."""
+        n, sms = C.c_longlong(0), C.c_int(0)
+        A.check(A.lib().scout_engine_overlap_stats(self._h, C.byref(n), C.byref(sms), int(bool(reset))))
+        return int(n.value), int(sms.value)
+
     def cpu_tokens(self):
         """(cpu tokens per layer summed over the units, budget U * k * 64) of the
         last step: one RatioTrace sample per layer (engine.hpp:283)."""

@@ -570,3 +570,60 @@ def test_engine_prefill_rejects_bad_calls(cuda):
     rows = torch.randn(L, U, 100, D, device="cuda")
     with pytest.raises(ValueError):
         eng.prefill(rows, rows, torch.tensor([100, 101], dtype=torch.int32), None)
+
+
+@pytest.mark.parametrize("host", [False, True])
+def test_engine_overlapped_step_matches_ordinary(cuda, host):
+    """The overlapped step (K1 beside K2 on a share of the SMs, K2 polling
+    K1's per-layer flags) against the ordinary order (K1, then K2) on an
+    identical second cache: the same outputs, CPU-side ids and tier state bit
+    for bit, step after step, through recalls (steps with a due ticket run in
+    the ordinary order on both); the overlapped side really overlapped."""
+    L, batch, hkv, G, k, cap, nbs, steps = 4, 2, 2, 4, 6, 8, 24, 40
+    U = batch * hkv
+    kv = torch.bfloat16
+    T0 = 64 * 11 + 50
+    torch.manual_seed(29)
+    seed_rows = [[(torch.randn(U, D), torch.randn(U, D)) for _ in range(T0)] for _ in range(L)]
+    sides = [Side(L, U, nbs, cap, kv, seed_rows) for _ in range(2)]
+    engs = []
+    for sd in sides:
+        layers = [LayerState(sd.dig[i], torch.full((U, nbs), -1, dtype=torch.int32, device="cuda")) for i in range(L)]
+        engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
+                                 kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=5,
+                                 host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, host_staging=host,
+                                 chunk_layers=2))
+    engs[0].set_overlap(40)
+    engs[1].set_overlap(0)
+    outs = [[torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")] for _ in range(2)]
+    h_outs = [[torch.empty(L, U * G, D).pin_memory(), torch.empty(L, U * G, 2).pin_memory(),
+               torch.empty(L, U, k, dtype=torch.int32).pin_memory(), torch.empty(L, U, dtype=torch.int32).pin_memory()]
+              for _ in range(2)]
+    for step in range(1, steps + 1):
+        ins = [torch.randn(L, U * G, D, device="cuda").bfloat16(), torch.randn(L, U * G, D, device="cuda").bfloat16(),
+               torch.randn(L, U * G, D, device="cuda"),
+               torch.stack([torch.randn(L, U * G, device="cuda"), torch.rand(L, U * G, device="cuda") + 0.1],
+                           -1).contiguous(),
+               torch.randn(L, U, D, device="cuda"), torch.randn(L, U, D, device="cuda")]
+        if host:
+            h_ins = [t.cpu().pin_memory() for t in ins]
+            for e, ho in zip(engs, h_outs):
+                e.decode_step_kv_host(step, *h_ins, ho[0], ho[1], ho[2], ho[3])
+        else:
+            for e, o in zip(engs, outs):
+                e.decode_step_kv(step, *ins, *o)
+        for e in engs:
+            e.sync()
+        torch.cuda.synchronize()
+        if host:
+            for a, b in zip(h_outs[0], h_outs[1]):
+                assert torch.equal(a, b), step
+        else:
+            assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]), step
+        for name in ("tier", "last_sel", "table"):
+            assert torch.equal(getattr(sides[0].tier, name), getattr(sides[1].tier, name)), (step, name)
+    n_ov, sms = engs[0].overlap_stats()
+    assert sms == 40 and n_ov >= steps // 2  # every step but the first and those with a due ticket
+    assert engs[1].overlap_stats()[0] == 0
+    for e in engs:
+        e.check_state()

@@ -1,4 +1,5 @@
 #!/bin/bash
+export SCOUT_K1K2_OVERLAP=0  # the sanitizer serialises kernels: no K1 beside a K2 that waits for it
 # compute-sanitizer over small GPU tests: memcheck (out-of-bounds / misaligned
 # accesses) and racecheck (shared-memory hazards) of the K1 / K2 / K5 kernels
 # and the engine's device tier mode. Small shapes: the tools slow kernels ~100x.

@@ -1,4 +1,5 @@
 #!/bin/bash
+export SCOUT_K1K2_OVERLAP=0  # the sanitizer serialises kernels: no K1 beside a K2 that waits for it
 OUT=gpurun_out; mkdir -p $OUT; TAG=${1:-san3}
 CS=/usr/local/cuda/bin/compute-sanitizer
 T="tests/test_gpu_decode_scale.py tests/test_gpu_engine_tier.py tests/test_gpu_engine_worker.py tests/test_gpu_topk.py tests/test_gpu_tier.py"

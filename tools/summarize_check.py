@@ -86,18 +86,22 @@ def main():
               "| kernel | launches | mean us | share |", "|---|---|---|---|"]
     for k, n, mean, share in launch_table(OUT / f"launches_{tag}.csv"):
         lines.append(f"| `{k[:80]}` | {n} | {mean:.1f} | {100 * share:.1f}% |")
-    for name, rep in (("K2", "k2"), ("K1", "k1"), ("K6", "k6")):
+    k1_traffic = None
+    for name, rep in (("K1", "k1"), ("K2", "k2"), ("K6", "k6")):
         m = ncu_raw(OUT / f"prof_{rep}_{tag}.ncu-rep")
         lines += ["", f"## {name} `ncu --set full` (one launch)", "", "| metric | value |", "|---|---|"]
         for key in METRICS:
             if key in m:
                 lines.append(f"| {key} | {m[key][0]} {m[key][1]} |")
-        if name == "K2" and "dram__bytes_read.sum" in m:
+        if name in ("K1", "K2") and "dram__bytes_read.sum" in m:
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
             rd = float(m["dram__bytes_read.sum"][0]) * scale.get(m["dram__bytes_read.sum"][1], 1)
             wr = float(m["dram__bytes_write.sum"][0]) * scale.get(m["dram__bytes_write.sum"][1], 1)
+            if name == "K1":
+                k1_traffic = rd + wr
+                continue
             (PROF / "k2_traffic.json").write_text(json.dumps({
-                "bytes_per_launch": rd + wr, "read": rd, "write": wr,
+                "bytes_per_launch": rd + wr, "read": rd, "write": wr, "k1_bytes_per_launch": k1_traffic,
                 "source": f"profiles/{tag}_summary.md (ncu --set full)"}) + "\n")
     (PROF / f"{tag}_summary.md").write_text("\n".join(lines) + "\n")
     for src, dst in ((f"bench_{tag}.json", f"{tag}_bench.json"), (f"bench_ref_{tag}.json", f"{tag}_bench_ref.json"),
