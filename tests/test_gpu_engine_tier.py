@@ -616,8 +616,12 @@ def test_engine_overlapped_step_matches_ordinary(cuda, host):
             e.sync()
         torch.cuda.synchronize()
         if host:
-            for a, b in zip(h_outs[0], h_outs[1]):
-                assert torch.equal(a, b), step
+            a, b = h_outs
+            assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]) and torch.equal(a[3], b[3]), step
+            for li in range(L):  # the CPU-side ids: the first n_cpu of each row are defined
+                for u in range(U):
+                    n = int(a[3][li, u])
+                    assert torch.equal(a[2][li, u, :n], b[2][li, u, :n]), (step, li, u)
         else:
             assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1]), step
         for name in ("tier", "last_sel", "table"):
