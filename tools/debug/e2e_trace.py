@@ -11,7 +11,7 @@ cfg = dict(bench.CONFIGS["qwen3-32b-32k"])
 cfg.update(q_dtype=torch.bfloat16, cpu_dtype=torch.bfloat16, drift=0.15, recall_policy="reference")
 dev = torch.device("cuda")
 W = bench.TierWorkload.auto_warm_slots(cfg, 32, 400, dev)
-wl = bench.TierWorkload(cfg, dev, 1234, 400, range(32), warm_slots=W)
+wl = bench.TierWorkload(cfg, dev, 1234, 400, range(32), warm_slots=W, host_units=32 * cfg["hkv"])
 eng = wl.make_engine()
 n, h_qt, h_qp, h_kv = bench._pinned_inputs(wl, True)
 h_co = wl.cpu_o.cpu().pin_memory(); h_cm = wl.cpu_ml.cpu().pin_memory()
