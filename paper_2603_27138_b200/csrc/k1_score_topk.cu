@@ -367,7 +367,13 @@ __device__ __forceinline__ void fast_quad(const DigT* blo, const DigT* bhi, int 
 constexpr int DCB = SCOUT_K1_DCB;
 // single-layer launches (few CTAs beside a running K2, each unit's digests
 // latency-bound): batches of 8 channels, twice the loads in flight
-constexpr int DCB_SINGLE = 8;
+#ifndef SCOUT_K1_DCB_SINGLE
+#define SCOUT_K1_DCB_SINGLE 8
+#endif
+#ifndef SCOUT_K1_SMINB
+#define SCOUT_K1_SMINB 4  // CTAs per SM the single-layer variants are compiled for
+#endif
+constexpr int DCB_SINGLE = SCOUT_K1_DCB_SINGLE;
 template <int B>
 __device__ __forceinline__ void ld_quad4(const __nv_bfloat16* lo, const __nv_bfloat16* hi, size_t ns, int b0, int c0,
                                          uint2 (&L)[B], uint2 (&H)[B]) {
@@ -422,7 +428,7 @@ __device__ __forceinline__ void fast_quad_direct(const __nv_bfloat16* lo, const 
 // QPT: block quads per thread whose running scores live in registers (1: up
 // to 512 blocks, 2: up to 1024, 4: up to 2048); 0: shared-memory accumulators.
 template <typename DigT, int G, int MODE, int QPT, bool DIRECT = false, int NA = K1_MAX_LAYERS>
-__global__ void __launch_bounds__(K1_THREADS, DIRECT ? (NA == 1 ? 4 : (QPT == 1 ? SCOUT_K1_DMINB1 : (QPT == 2 ? SCOUT_K1_DMINB : 4)))
+__global__ void __launch_bounds__(K1_THREADS, DIRECT ? (NA == 1 ? SCOUT_K1_SMINB : (QPT == 1 ? SCOUT_K1_DMINB1 : (QPT == 2 ? SCOUT_K1_DMINB : 4)))
                                                       : ((QPT == 1 || QPT == 2) ? 7 : SCOUT_K1_MINB))
     score_topk_kernel(const K1BatchT<NA> batch) {
     constexpr int KB = NA == 1 ? DCB_SINGLE : DCB;  // channels per direct-load batch
