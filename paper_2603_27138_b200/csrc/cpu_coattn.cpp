@@ -154,6 +154,16 @@ inline void store_o(const Job& j, size_t h, const float* acc, float inv) {
     }
 }
 
+// a unit with no CPU-side block: the empty partial (o = 0, (-inf, 0))
+inline void store_empty(const Job& j, int u) {
+    const size_t h0 = static_cast<size_t>(u) * j.G;
+    const size_t esz = j.o_bf16 ? 2 : 4;
+    std::memset(static_cast<uint8_t*>(j.o) + h0 * D * esz, 0, j.G * D * esz);
+    for (int g = 0; g < j.G; ++g) {
+        j.ml[(h0 + g) * 2] = -std::numeric_limits<float>::infinity();
+        j.ml[(h0 + g) * 2 + 1] = 0.f;
+    }
+}
 // Per block: the block's rows are decoded once (K and V into fp32), then for
 // each head: 64 scores, one block maximum, 64 exponentials and the weighted V
 // sum; the running state is rescaled once per block (same result as the
@@ -171,9 +181,13 @@ void run_unit(const Job& j, int u) {
         l[g] = 0.f;
         std::memset(acc[g], 0, sizeof(acc[g]));
     }
+    const int nb = j.n_blocks[u];
+    if (nb <= 0) {
+        store_empty(j, u);
+        return;
+    }
     alignas(64) float qscratch[GMAX * D];
     const float* qu = unit_query(j, u, qscratch);
-    const int nb = j.n_blocks[u];
     for (int i = 0; i < nb; ++i) {
         const size_t idx = static_cast<size_t>(u) * j.k_stride + i;
         const uint8_t* kt = j.host + static_cast<size_t>(j.index[idx]) * j.slot_bytes;
@@ -304,6 +318,60 @@ SCOUT_AMX_TARGET inline __m512 score_pair(const float* s0, const float* s1, int 
     return _mm512_mask_blend_ps(ok, ninf, v);
 }
 
+// unit u's G query rows as f32: bf16 queries widened exactly, 16 lanes at a time
+SCOUT_AMX_TARGET inline const float* unit_query_v(const Job& j, int u, float* scratch) {
+    const size_t off = static_cast<size_t>(u) * j.G * D;
+    if (!j.q_bf16) return static_cast<const float*>(j.q) + off;
+    const uint16_t* qb = static_cast<const uint16_t*>(j.q) + off;
+    for (int i = 0; i < j.G * D; i += 16)
+        _mm512_store_ps(scratch + i, _mm512_castsi512_ps(_mm512_slli_epi32(
+                                         _mm512_cvtepu16_epi32(_mm256_loadu_si256(reinterpret_cast<const __m256i*>(qb + i))), 16)));
+    return scratch;
+}
+// store_o, 16 lanes at a time; the bf16 rounding is f_to_bf16's (nearest even,
+// inf / nan truncated), bit for bit
+SCOUT_AMX_TARGET inline void store_o_v(const Job& j, size_t h, const float* acc, float inv) {
+    const __m512 vi = _mm512_set1_ps(inv);
+    if (j.o_bf16) {
+        uint16_t* o = static_cast<uint16_t*>(j.o) + h * D;
+        const __m512i one = _mm512_set1_epi32(1), bias = _mm512_set1_epi32(0x7FFF), ex = _mm512_set1_epi32(0x7F800000);
+        for (int d = 0; d < D; d += 16) {
+            const __m512i u = _mm512_castps_si512(_mm512_mul_ps(_mm512_load_ps(acc + d), vi));
+            const __m512i r = _mm512_add_epi32(_mm512_add_epi32(u, bias), _mm512_and_si512(_mm512_srli_epi32(u, 16), one));
+            const __mmask16 special = _mm512_cmpeq_epi32_mask(_mm512_and_si512(u, ex), ex);
+            const __m512i v = _mm512_mask_mov_epi32(r, special, u);
+            _mm256_storeu_si256(reinterpret_cast<__m256i*>(o + d), _mm512_cvtepi32_epi16(_mm512_srli_epi32(v, 16)));
+        }
+    } else {
+        float* o = static_cast<float*>(j.o) + h * D;
+        for (int d = 0; d < D; d += 16) _mm512_storeu_ps(o + d, _mm512_mul_ps(_mm512_load_ps(acc + d), vi));
+    }
+}
+// 16 x 16 transpose of 32-bit words: r[n] word i -> r[i] word n
+SCOUT_AMX_TARGET inline void transpose16(__m512i r[16]) {
+    __m512i t[16], v[16];
+    for (int k = 0; k < 8; ++k) {
+        t[2 * k] = _mm512_unpacklo_epi32(r[2 * k], r[2 * k + 1]);
+        t[2 * k + 1] = _mm512_unpackhi_epi32(r[2 * k], r[2 * k + 1]);
+    }
+    for (int k = 0; k < 4; ++k) {
+        v[4 * k] = _mm512_unpacklo_epi64(t[4 * k], t[4 * k + 2]);
+        v[4 * k + 1] = _mm512_unpackhi_epi64(t[4 * k], t[4 * k + 2]);
+        v[4 * k + 2] = _mm512_unpacklo_epi64(t[4 * k + 1], t[4 * k + 3]);
+        v[4 * k + 3] = _mm512_unpackhi_epi64(t[4 * k + 1], t[4 * k + 3]);
+    }
+    // v[4k + c] 128-bit lane L holds word 4L + c of rows 4k..4k+3
+    for (int c = 0; c < 4; ++c) {
+        const __m512i a0 = _mm512_shuffle_i32x4(v[c], v[4 + c], 0x44), a1 = _mm512_shuffle_i32x4(v[c], v[4 + c], 0xEE);
+        const __m512i b0 = _mm512_shuffle_i32x4(v[8 + c], v[12 + c], 0x44),
+                      b1 = _mm512_shuffle_i32x4(v[8 + c], v[12 + c], 0xEE);
+        r[c] = _mm512_shuffle_i32x4(a0, b0, 0x88);
+        r[4 + c] = _mm512_shuffle_i32x4(a0, b0, 0xDD);
+        r[8 + c] = _mm512_shuffle_i32x4(a1, b1, 0x88);
+        r[12 + c] = _mm512_shuffle_i32x4(a1, b1, 0xDD);
+    }
+}
+
 SCOUT_AMX_TARGET inline __m512 exp2_ps(__m512 x) {
     x = _mm512_max_ps(x, _mm512_set1_ps(-200.f));  // -inf -> 0 after scalef
     const __m512 xi = _mm512_roundscale_ps(x, _MM_FROUND_TO_NEAREST_INT | _MM_FROUND_NO_EXC);
@@ -336,31 +404,60 @@ SCOUT_AMX_TARGET void amx_config(int G) {
 // two bursts per chunk instead of two per block matter (measured: an S burst
 // of 16 tile products costs ~220 TSC back to back, ~900 after 1200 cycles of
 // other work).
-SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
+#ifndef SCOUT_CPU_PREFETCH
+#define SCOUT_CPU_PREFETCH 1
+#endif
+#ifndef SCOUT_CPU_PF_HINT
+#define SCOUT_CPU_PF_HINT _MM_HINT_T1  // into L2: the staging of the current image owns L1
+#endif
+// the image of block i of unit u (NULL past the unit's blocks)
+inline const char* block_image(const Job& j, int u, int i) {
+    if (u < 0 || i >= j.n_blocks[u]) return nullptr;
+    return reinterpret_cast<const char*>(j.host + static_cast<size_t>(j.index[static_cast<size_t>(u) * j.k_stride + i]) *
+                                                      j.slot_bytes);
+}
+
+// One unit on the tile unit (`next_u`: the unit this thread runs next, whose
+// first block image is prefetched while the last one here is staged; each
+// block's image is prefetched while the one before it is staged: a single
+// thread's demand misses alone reach ~12 GB/s of host DRAM, one 32 KiB image
+// per ~2.6 us)
+SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w, int next_u) {
     const int G = j.G;
     constexpr float LOG2E = 1.4426950408889634f, LN2 = 0.6931471805599453f;
     // ---- Q^T -> VNNI B tiles: column n < 8 = hi of head n, 8 + n = lo of head n;
     // a VNNI word is the (2i, 2i+1) channel pair of one column
     // (w.bq's columns of heads >= G and w.pa's rows >= G stay zero: cleared
     // when the scratch is (re)dedicated to a group size, amx_work)
+    const int nb = j.n_blocks[u];
+    if (nb <= 0) {
+        store_empty(j, u);
+        return;
+    }
     alignas(64) float qscratch[GMAX * D];
-    const float* qu = unit_query(j, u, qscratch);
+    const float* qu = unit_query_v(j, u, qscratch);
     const __m512 qs = _mm512_set1_ps(j.scale * LOG2E);
-    const __m512i col = _mm512_mullo_epi32(_mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15),
-                                           _mm512_set1_epi32(16));
-    for (int g = 0; g < G; ++g)
-        for (int ks = 0; ks < 4; ++ks) {
+    for (int ks = 0; ks < 4; ++ks) {
+        // columns: hi words of heads 0..7, then lo words (heads >= G zero);
+        // one 16 x 16 word transpose makes the VNNI rows
+        __m512i cols[16];
+        for (int g = 0; g < GMAX; ++g) {
+            if (g >= G) {
+                cols[g] = cols[8 + g] = _mm512_setzero_si512();
+                continue;
+            }
             const __m512 v0 = _mm512_mul_ps(_mm512_loadu_ps(qu + g * D + 32 * ks), qs);
             const __m512 v1 = _mm512_mul_ps(_mm512_loadu_ps(qu + g * D + 32 * ks + 16), qs);
             const __m512i hi = (__m512i)_mm512_cvtne2ps_pbh(v1, v0);
             const __m512 h0 = _mm512_castsi512_ps(_mm512_slli_epi32(_mm512_cvtepu16_epi32(_mm512_castsi512_si256(hi)), 16));
             const __m512 h1 = _mm512_castsi512_ps(
                 _mm512_slli_epi32(_mm512_cvtepu16_epi32(_mm512_extracti64x4_epi64(hi, 1)), 16));
-            const __m512i lo = (__m512i)_mm512_cvtne2ps_pbh(_mm512_sub_ps(v1, h1), _mm512_sub_ps(v0, h0));
-            int* base = reinterpret_cast<int*>(w.bq[ks]);
-            _mm512_i32scatter_epi32(base + g, col, hi, 4);
-            _mm512_i32scatter_epi32(base + 8 + g, col, lo, 4);
+            cols[g] = hi;
+            cols[8 + g] = (__m512i)_mm512_cvtne2ps_pbh(_mm512_sub_ps(v1, h1), _mm512_sub_ps(v0, h0));
         }
+        transpose16(cols);
+        for (int i = 0; i < 16; ++i) _mm512_store_si512(w.bq[ks][i], cols[i]);
+    }
     bool first = true;  // the first chunk's P.V is the running O (no memset, no rescale of garbage)
     const __m512 ninf = _mm512_set1_ps(-std::numeric_limits<float>::infinity());
     __m512 m = ninf, l = _mm512_setzero_ps();  // lanes g and 8 + g: head g
@@ -370,7 +467,6 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
     const __m512i vp1 = _mm512_setr_epi64(4, 5, 12, 13, 6, 7, 14, 15);
     const __m512i gidx = _mm512_mullo_epi32(_mm512_setr_epi32(0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15),
                                             _mm512_set1_epi32(GMAX));
-    const int nb = j.n_blocks[u];
     for (int c0 = 0; c0 < nb; c0 += CH) {
         const int nc = std::min(CH, nb - c0);
         int rows[CH];
@@ -383,7 +479,13 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
                 reinterpret_cast<const uint16_t*>(j.host + static_cast<size_t>(j.index[idx]) * j.slot_bytes);
             const uint16_t* vt = kt + j.slot_bytes / 4;
             rows[b] = std::max(0, std::min(BS, j.rows ? static_cast<int>(j.rows[idx]) : BS));
+            const char* pf = !SCOUT_CPU_PREFETCH        ? nullptr
+                             : c0 + b + 1 < nb ? block_image(j, u, c0 + b + 1)
+                                               : block_image(j, next_u, 0);
+            const int pf_lines = static_cast<int>(j.slot_bytes / 64);  // 512: 8 per K row
             for (int r = 0; r < BS; ++r) {
+                if (pf)
+                    for (int x = 0; x < pf_lines / BS; ++x) _mm_prefetch(pf + 64 * (r * (pf_lines / BS) + x), SCOUT_CPU_PF_HINT);
                 __m512i z[4];
                 if (r < rows[b]) unswizzle_row(kt, r, z);
                 else z[0] = z[1] = z[2] = z[3] = _mm512_setzero_si512();
@@ -509,17 +611,16 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w) {
     alignas(64) float mm[16], ll[16];
     _mm512_store_ps(mm, m);
     _mm512_store_ps(ll, l);
-    if (first) std::memset(w.o, 0, sizeof(w.o));  // no block: the empty partial, o = 0
     for (int g = 0; g < G; ++g) {
         const size_t h = static_cast<size_t>(u) * G + g;
         const float inv = ll[g] > 0.f ? 1.f / ll[g] : 0.f;
-        store_o(j, h, w.o[g], inv);
+        store_o_v(j, h, w.o[g], inv);
         j.ml[h * 2] = ll[g] > 0.f ? mm[g] * LN2 : -std::numeric_limits<float>::infinity();
         j.ml[h * 2 + 1] = ll[g];
     }
 }
 
-SCOUT_AMX_TARGET void amx_work(const Job& j, std::atomic<int>& next, int n_units) {
+SCOUT_AMX_TARGET void amx_work(const Job& j, std::atomic<int>& next, int n_units, int batch) {
     // per-thread scratch, freed when the thread exits (callers' own threads run units too)
     struct Free {
         void operator()(AmxScratch* p) const { std::free(p); }
@@ -528,7 +629,8 @@ SCOUT_AMX_TARGET void amx_work(const Job& j, std::atomic<int>& next, int n_units
     if (!owned) {
         owned.reset(static_cast<AmxScratch*>(std::aligned_alloc(64, sizeof(AmxScratch))));
         if (!owned) {  // no memory for the tile staging: this thread takes the AVX-512 kernel
-            for (int u; (u = next.fetch_add(1)) < n_units;) run_unit<true>(j, u);
+            for (int u0; (u0 = next.fetch_add(batch)) < n_units;)
+                for (int u = u0; u < std::min(u0 + batch, n_units); ++u) run_unit<true>(j, u);
             return;
         }
     }
@@ -540,7 +642,16 @@ SCOUT_AMX_TARGET void amx_work(const Job& j, std::atomic<int>& next, int n_units
         scratch_g = j.G;
     }
     amx_config(j.G);
-    for (int u; (u = next.fetch_add(1)) < n_units;) run_unit_amx(j, u, *scratch);
+    // units are claimed `batch` at a time (one contended atomic per batch),
+    // one batch ahead, so the next unit's first image is in flight while the
+    // last unit of a batch finishes
+    int u0 = next.fetch_add(batch);
+    while (u0 < n_units) {
+        const int u1 = std::min(u0 + batch, n_units);
+        const int n0 = next.fetch_add(batch);
+        for (int u = u0; u < u1; ++u) run_unit_amx(j, u, *scratch, u + 1 < u1 ? u + 1 : (n0 < n_units ? n0 : -1));
+        u0 = n0;
+    }
     _tile_release();
 }
 
@@ -649,15 +760,24 @@ int scout_cpu_coattn_run(const CpuCoattnArgs& a) {
     const bool amx = a.kv_dtype == SCOUT_BF16 && !(env && env[0] == '0') && amx_ready();
     const bool avx = has_avx512();
     std::atomic<int> next{0};
+    // claim batch: units with no CPU-side block cost ~0.1 us, so a per-unit
+    // atomic shared by 16 threads would dominate them; a batch holds about
+    // two blocks' work (load balance at the tail), at most 16 units and at
+    // least ~16 claims per thread
+    long long total_blocks = 0;
+    for (int u = 0; u < n_units; ++u) total_blocks += std::max(0, a.n_blocks[u]);
+    const double per_unit = 0.05 + static_cast<double>(total_blocks) / n_units;  // in blocks
+    const int batch = std::max(1, std::min({16, n_units / (16 * T), static_cast<int>(2.0 / per_unit)}));
     const std::function<void()> work = [&] {
         if (amx) {
-            amx_work(j, next, n_units);
+            amx_work(j, next, n_units, batch);
             return;
         }
-        for (int u; (u = next.fetch_add(1)) < n_units;) {
-            if (avx) run_unit<true>(j, u);
-            else run_unit<false>(j, u);
-        }
+        for (int u0; (u0 = next.fetch_add(batch)) < n_units;)
+            for (int u = u0; u < std::min(u0 + batch, n_units); ++u) {
+                if (avx) run_unit<true>(j, u);
+                else run_unit<false>(j, u);
+            }
     };
     if (T == 1) work();
     else pool().run(T, work);

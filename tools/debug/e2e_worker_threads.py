@@ -1,5 +1,6 @@
 """The composed step (engine's own CPU worker, host buffers) at several worker
-thread counts and chunk sizes on one config-3 workload (victim cache on)."""
+thread counts and chunk sizes on one config-3 workload (victim cache on).
+Arguments: threads:chunk pairs (default 0:4 15:4 14:4 12:4 16:8 16:2; 0 = all)."""
 import sys
 sys.path[:0] = ["."]
 import torch
@@ -15,8 +16,9 @@ step = 0
 for s in range(20):
     step += 1
     wl.step(step)
-for th, ch in [(0, 4), (15, 4), (14, 4), (12, 4), (16, 8), (16, 2)]:
-    r = bench.run_e2e_worker(wl, 32, dev, 1, 32, step, threads=th, chunk_layers=ch)
-    step += 5 + 32
+pairs = [tuple(int(x) for x in a.split(":")) for a in sys.argv[1:]] or [(0, 4), (15, 4), (14, 4), (12, 4), (16, 8), (16, 2)]
+for th, ch in pairs:
+    r = bench.run_e2e_worker(wl, 64, dev, 1, 32, step, threads=th, chunk_layers=ch)
+    step += 5 + 64
     print(f"threads {th or 16:2d} chunk {ch}: {r['ms_per_step']:.2f} ms/step, worker {r['cpu_worker_ms_per_step']:.2f} ms, "
           f"{r['cpu_blocks_last_step']} CPU blocks", flush=True)
