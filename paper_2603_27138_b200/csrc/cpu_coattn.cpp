@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
 #include <cstdint>
@@ -479,9 +480,12 @@ SCOUT_AMX_TARGET void run_unit_amx(const Job& j, int u, AmxScratch& w, int next_
                 reinterpret_cast<const uint16_t*>(j.host + static_cast<size_t>(j.index[idx]) * j.slot_bytes);
             const uint16_t* vt = kt + j.slot_bytes / 4;
             rows[b] = std::max(0, std::min(BS, j.rows ? static_cast<int>(j.rows[idx]) : BS));
-            const char* pf = !SCOUT_CPU_PREFETCH        ? nullptr
-                             : c0 + b + 1 < nb ? block_image(j, u, c0 + b + 1)
-                                               : block_image(j, next_u, 0);
+            // mode 1: the block after this one (the next unit's first after the
+            // last); mode 2: block c0 + b of the next unit (a unit's compute ahead)
+            const char* pf = SCOUT_CPU_PREFETCH == 0 ? nullptr
+                             : SCOUT_CPU_PREFETCH == 2
+                                 ? block_image(j, next_u, c0 + b)
+                                 : (c0 + b + 1 < nb ? block_image(j, u, c0 + b + 1) : block_image(j, next_u, 0));
             const int pf_lines = static_cast<int>(j.slot_bytes / 64);  // 512: 8 per K row
             for (int r = 0; r < BS; ++r) {
                 if (pf)
@@ -671,6 +675,9 @@ bool amx_ready() {
 // ----------------------------------------------------------- thread pool --
 // Persistent workers (a decode step calls the worker once per layer: thread
 // creation per call would cost more than a layer's CPU share).
+#ifndef SCOUT_POOL_SPIN_US
+#define SCOUT_POOL_SPIN_US 0  // idle workers' spin before sleeping (0: sleep at once)
+#endif
 class Pool {
 public:
     void run(int T, const std::function<void()>& fn) {
@@ -684,10 +691,14 @@ public:
             fn_ = &fn;
             want_ = T - 1;
             pending_ = T - 1;
+            pending_a_.store(T - 1, std::memory_order_relaxed);
             ++gen_;
+            gen_a_.store(gen_, std::memory_order_release);
         }
         cv_.notify_all();
         fn();
+        // the workers finish within a unit or two of this thread: spin first
+        spin_until([&] { return pending_a_.load(std::memory_order_acquire) == 0; });
         std::unique_lock<std::mutex> lk(mu_);
         done_.wait(lk, [&] { return pending_ == 0; });
         fn_ = nullptr;
@@ -706,6 +717,9 @@ private:
         uint64_t seen = 0;
         for (;;) {
             const std::function<void()>* fn;
+            // a decode step calls the pool once per layer chunk, back to back:
+            // idle workers spin a short while before sleeping on the condvar
+            spin_until([&] { return gen_a_.load(std::memory_order_acquire) != seen; });
             {
                 std::unique_lock<std::mutex> lk(mu_);
                 cv_.wait(lk, [&] { return stop_ || (gen_ != seen && id < want_); });
@@ -715,9 +729,23 @@ private:
             }
             (*fn)();
             std::lock_guard<std::mutex> lk(mu_);
+            pending_a_.fetch_sub(1, std::memory_order_release);
             if (--pending_ == 0) done_.notify_one();
         }
     }
+    template <typename F>
+    static void spin_until(F done) {
+        if (SCOUT_POOL_SPIN_US <= 0) return;
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int i = 0; !done(); ++i) {
+            _mm_pause();
+            if ((i & 255) == 255 &&
+                std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(SCOUT_POOL_SPIN_US))
+                return;
+        }
+    }
+    std::atomic<uint64_t> gen_a_{0};
+    std::atomic<int> pending_a_{0};
     std::mutex call_mu_, mu_;
     std::condition_variable cv_, done_;
     std::vector<std::thread> workers_;
