@@ -380,6 +380,15 @@ int scout_kv_writeback(const void* kv_pool, int kv_dtype, void* host_tier, long 
 int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, const int64_t* host_index,
                                 const int32_t* block_rows, const int32_t* n_blocks, int k_stride, const float* q,
                                 int group, float scale, int n_units, float* o, float* ml, int threads);
+/* The same with the model's dtypes: q in q_dtype and o in o_dtype (SCOUT_F32
+ * or SCOUT_BF16; ml stays f32). A bf16 query is widened exactly; a bf16 o is
+ * the f32 result rounded to nearest even, bit for bit what the f32 entry point
+ * followed by that rounding gives. This is what the decode calls' CPU-partial
+ * input takes with cfg.cpu_dtype = SCOUT_BF16 (no host-side conversion).   */
+int scout_cpu_partial_attention_ex(const void* host_tier, int kv_dtype, const int64_t* host_index,
+                                   const int32_t* block_rows, const int32_t* n_blocks, int k_stride, const void* q,
+                                   int q_dtype, int group, float scale, int n_units, void* o, int o_dtype, float* ml,
+                                   int threads);
 /* Which kernel scout_cpu_partial_attention runs for kv_dtype on this CPU now:
  * 2 = AMX-BF16 tiles, 1 = AVX-512 fp32, 0 = scalar.                        */
 int scout_cpu_coattn_kernel(int kv_dtype);

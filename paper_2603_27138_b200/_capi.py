@@ -37,7 +37,7 @@ EXPORTED = (
     "scout_tier_place", "scout_tier_prefill", "scout_qpred_workspace_bytes", "scout_qpred_pack_weights", "scout_predict_query",
     "scout_recall_gather_ids", "scout_kv_writeback", "scout_engine_decode_step_kv", "scout_engine_recall_stats", "scout_engine_cpu_tokens", "scout_calibrate_intervals", "scout_engine_prefill",
     "scout_engine_overlap_stats", "scout_engine_set_overlap",
-    "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
+    "scout_engine_decode_step_kv_host", "scout_cpu_partial_attention", "scout_cpu_partial_attention_ex", "scout_cpu_coattn_kernel", "scout_engine_tier_changed",
     "scout_engine_worker_stats", "scout_engine_check_state", "scout_engine_decode_layer", "scout_engine_decode_layer_x",
 )
 
@@ -137,6 +137,8 @@ def lib() -> C.CDLL:
                                          _vp]
         L.scout_cpu_partial_attention.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, C.c_float,
                                                   C.c_int, _vp, _vp, C.c_int]
+        L.scout_cpu_partial_attention_ex.argtypes = [_vp, C.c_int, _vp, _vp, _vp, C.c_int, _vp, C.c_int, C.c_int,
+                                                     C.c_float, C.c_int, _vp, C.c_int, _vp, C.c_int]
         L.scout_cpu_coattn_kernel.argtypes = [C.c_int]
         L.scout_kv_append.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, _vp, _vp, C.c_int, C.c_int, _vp]
         L.scout_score_topk_split.argtypes = [C.POINTER(TopkArgs), _vp]

@@ -835,6 +835,29 @@ extern "C" int scout_cpu_partial_attention(const void* host_tier, int kv_dtype, 
     return scout_cpu_coattn_run(a);
 }
 
+extern "C" int scout_cpu_partial_attention_ex(const void* host_tier, int kv_dtype, const int64_t* host_index,
+                                              const int32_t* block_rows, const int32_t* n_blocks, int k_stride,
+                                              const void* q, int q_dtype, int group, float scale, int n_units, void* o,
+                                              int o_dtype, float* ml, int threads) {
+    CpuCoattnArgs a{};
+    a.host_tier = host_tier;
+    a.kv_dtype = kv_dtype;
+    a.host_index = host_index;
+    a.block_rows = block_rows;
+    a.n_blocks = n_blocks;
+    a.k_stride = k_stride;
+    a.q = q;
+    a.q_dtype = q_dtype;
+    a.group = group;
+    a.scale = scale;
+    a.n_units = n_units;
+    a.o = o;
+    a.o_dtype = o_dtype;
+    a.ml = ml;
+    a.threads = threads;
+    return scout_cpu_coattn_run(a);
+}
+
 extern "C" int scout_cpu_coattn_kernel(int kv_dtype) {
     const char* env = std::getenv("SCOUT_CPU_AMX");
     if (kv_dtype == SCOUT_BF16 && !(env && env[0] == '0') && amx_ready()) return 2;

@@ -237,3 +237,25 @@ def cpu_partial_attention(host_tier, kv_dtype, host_index, n_blocks, q, group, s
                                                 int(host_index.shape[1]), q.data_ptr(), int(group), float(scale),
                                                 n_units, o.data_ptr(), ml.data_ptr(), int(threads)))
     return o, ml
+
+
+def cpu_partial_attention_ex(host_tier, kv_dtype, host_index, n_blocks, q, group, o_dtype=torch.bfloat16, scale=None,
+                             block_rows=None, threads=0):
+    """scout_cpu_partial_attention_ex: as cpu_partial_attention with the query
+    in its own dtype (f32 / bf16 host tensor) and o in o_dtype. Returns
+    (o, ml) host tensors, o in o_dtype, ml f32."""
+    host_index = torch.as_tensor(host_index, dtype=torch.int64).contiguous()
+    n_blocks = torch.as_tensor(n_blocks, dtype=torch.int32).contiguous()
+    q = q.contiguous()
+    n_units = int(n_blocks.numel())
+    if scale is None:
+        scale = 1.0 / math.sqrt(A.HEAD_DIM)
+    rows = None if block_rows is None else torch.as_tensor(block_rows, dtype=torch.int32).contiguous()
+    o = torch.empty(n_units * group, A.HEAD_DIM, dtype=o_dtype)
+    ml = torch.empty(n_units * group, 2, dtype=torch.float32)
+    A.check(A.lib().scout_cpu_partial_attention_ex(host_tier.data_ptr(), dtype_code(kv_dtype), host_index.data_ptr(),
+                                                   None if rows is None else rows.data_ptr(), n_blocks.data_ptr(),
+                                                   int(host_index.shape[1]), q.data_ptr(), dtype_code(q.dtype),
+                                                   int(group), float(scale), n_units, o.data_ptr(), dtype_code(o_dtype),
+                                                   ml.data_ptr(), int(threads)))
+    return o, ml

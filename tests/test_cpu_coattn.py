@@ -113,3 +113,38 @@ def test_cpu_worker_stale_rows_and_pool():
         o, ml = ops.cpu_partial_attention(host, torch.bfloat16, idx, n, q, 8, block_rows=rows, threads=t)
         assert torch.isfinite(o).all() and torch.isfinite(ml).all()
         assert torch.equal(o, want[0]) and torch.equal(ml, want[1])
+
+
+@pytest.mark.parametrize("kv", ["bf16", "f32"])
+def test_cpu_partial_attention_ex_dtypes_and_claims(kv):
+    """scout_cpu_partial_attention_ex (the model's dtypes): a bf16 query gives
+    the bits its exact f32 widening gives, a bf16 o is the f32 result rounded
+    to nearest even (torch's rounding, bit for bit), the f32/f32 call equals
+    scout_cpu_partial_attention. Many units, most with no or one CPU-side
+    block, so units are claimed several at a time; any thread count gives the
+    same bits."""
+    rng = np.random.default_rng(21 + (kv == "f32"))
+    dt = torch.bfloat16 if kv == "bf16" else torch.float32
+    sb = ops.slot_bytes(dt)
+    nblk, U, k, G = 16, 600, 8, 8
+    host = torch.zeros(nblk * sb, dtype=torch.uint8)
+    for b in range(nblk):
+        kb, vb = rng.standard_normal((2, B, D)).astype(np.float32)
+        img = (np.concatenate([bf16_tile(kb), bf16_tile(vb)]) if kv == "bf16"
+               else np.concatenate([kb.ravel(), vb.ravel()])).view(np.uint8)
+        host[b * sb:(b + 1) * sb] = torch.from_numpy(img)
+    n = torch.from_numpy(np.minimum(rng.poisson(0.7, U), k).astype(np.int32))
+    idx = torch.from_numpy(rng.integers(0, nblk, (U, k)).astype(np.int64))
+    q_bf = torch.from_numpy(rng.standard_normal((U * G, D)).astype(np.float32)).bfloat16()
+    q32 = q_bf.float()
+    o_ref, ml_ref = ops.cpu_partial_attention(host, dt, idx, n, q32, G, threads=1)
+    for t in (1, 5):
+        o, ml = ops.cpu_partial_attention_ex(host, dt, idx, n, q32, G, o_dtype=torch.float32, threads=t)
+        assert torch.equal(o, o_ref) and torch.equal(ml, ml_ref)
+        o, ml = ops.cpu_partial_attention_ex(host, dt, idx, n, q_bf, G, o_dtype=torch.float32, threads=t)
+        assert torch.equal(o, o_ref) and torch.equal(ml, ml_ref)
+        o, ml = ops.cpu_partial_attention_ex(host, dt, idx, n, q_bf, G, o_dtype=torch.bfloat16, threads=t)
+        assert o.dtype == torch.bfloat16
+        assert torch.equal(o.view(torch.int16), o_ref.bfloat16().view(torch.int16)) and torch.equal(ml, ml_ref)
+    empty = (n == 0).repeat_interleave(G)
+    assert empty.any() and torch.all(o_ref[empty] == 0) and torch.all(ml_ref[empty, 0] == -math.inf)
