@@ -1,8 +1,15 @@
 """The composed step (engine's own CPU worker, host buffers, bench defaults:
 16-step reference cadence, 4-layer chunks, all host threads) over 64 timed
 steps, twice: for A/B runs of a CPU-worker change (SCOUT_B200_LIB)."""
+import ctypes
+import os
 import sys
 sys.path[:0] = ["."]
+if os.environ.get("SCOUT_BLOCKING_SYNC") == "1":
+    # host threads that wait on the device sleep instead of spinning
+    # (CU_CTX_SCHED_BLOCKING_SYNC on the primary context, before torch makes it)
+    cu = ctypes.CDLL("libcuda.so.1")
+    assert cu.cuInit(0) == 0 and cu.cuDevicePrimaryCtxSetFlags(0, 4) == 0
 import torch
 import bench
 
