@@ -527,11 +527,14 @@ struct scout_engine {
             return v ? atoi(v) : -1;
         }();
         const int want = ov_setting >= 0 ? ov_setting : env_sms;  // -1: the default share
-        if (serialising || !k1k2_loaded || want == 0 || !tier_mode || all_res || cfg.kv_dtype != SCOUT_BF16 || cfg.max_ctas > 0 ||
-            cfg.nb_stride > 1024 || grid < 100)
+        // static view: only without recall plans (their copies follow K2's layers)
+        const bool static_recalls = !tier_mode && (cfg.recall_interval > 0 || cfg.recall_intervals);
+        if (serialising || !k1k2_loaded || want == 0 || static_recalls || all_res || cfg.kv_dtype != SCOUT_BF16 ||
+            cfg.max_ctas > 0 || cfg.nb_stride > 1024 || grid < 100)
             return 0;
-        for (int i = 0; i < cfg.layers; ++i)
-            if (pending[i] >= 0 && pending[i] <= tick(step, i)) return 0;
+        if (tier_mode)
+            for (int i = 0; i < cfg.layers; ++i)
+                if (pending[i] >= 0 && pending[i] <= tick(step, i)) return 0;
         const int sms = want > 0 ? want : (grid * 35 + 50) / 100;
         return sms < grid ? sms : 0;
     }
@@ -543,14 +546,17 @@ struct scout_engine {
                         const unsigned* const* inflag, cudaStream_t st, cudaStream_t ks, bool done) {
         const int L = cfg.layers;
         int rc;
-        if (planned_step != step) {
+        if (tier_mode && planned_step != step) {
             ++launches;
             if ((rc = scout_tier_plan_layers(static_cast<const scout_tier_layer*>(tier_dev.p), L, U, cfg.nb_stride,
                                              cfg.n_tokens, step, I(plan_tab), st)) != SCOUT_OK)
                 return rc;
         }
-        CU(cudaEventRecord(ev_pre, st));
-        if (ks != st) CU(cudaStreamWaitEvent(ks, ev_pre, 0));
+        // ev_pre (device tier mode) gates the post launches; the static view
+        // has no post, only the order of ks after st
+        cudaEvent_t pre = tier_mode ? ev_pre : ev_tmp;
+        CU(cudaEventRecord(pre, st));
+        if (ks != st) CU(cudaStreamWaitEvent(ks, pre, 0));
         if ((rc = launch_k2(par, q, co, cml, o, ml, inflag, true, ks, 0, L, grid - sms, false)) != SCOUT_OK) return rc;
         std::vector<scout_topk_args> v(L);
         for (int i = 0; i < L; ++i) v[i] = k1_args(i, i == 0 ? q_true : qlayer(q_pred, i), step, par);
@@ -1367,11 +1373,7 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q
     if (const int rc = e->issuer_status(); rc != SCOUT_OK) return rc;
     const unsigned token = ++e->token;
     const int par = token & 1;
-    // K1 for every layer in one wide launch (bandwidth-bound, the whole GPU),
-    // then the persistent K2 over all layers; stream order is the dependency
-    int rc = e->select_batch(0, L, q_true, q_pred, step, par, st);
-    if (rc == SCOUT_OK && e->all_res) rc = e->resident_lists(par, 0, L, st);
-    if (rc != SCOUT_OK) return rc;
+    int rc;
     std::vector<const void*> q(L);
     std::vector<const void*> co(L);
     std::vector<const float*> cml(L);
@@ -1383,8 +1385,22 @@ extern "C" int scout_engine_decode_step(scout_engine* e, int step, const void* q
         o[i] = out_o + i * qd;
         ml[i] = out_ml + i * md;
     }
+    // the overlapped step (scout_engine::overlap_sms: no recall plans here) on
+    // the engine's own stream, as in the device tier mode
+    if (const int ov = e->overlap_sms(step); ov > 0) {
+        if ((rc = e->overlapped_pair(step, par, ov, q_true, q_pred, q.data(), co.data(), cml.data(), o.data(),
+                                     ml.data(), nullptr, st, e->k1s, false)) != SCOUT_OK)
+            return rc;
+        CU(cudaStreamWaitEvent(st, e->ev_k2[par], 0));
+        return e->issue_recalls(step);
+    }
+    // K1 for every layer in one wide launch (bandwidth-bound, the whole GPU),
+    // then the persistent K2 over all layers; stream order is the dependency
+    if ((rc = e->select_batch(0, L, q_true, q_pred, step, par, st)) != SCOUT_OK) return rc;
+    if (e->all_res && (rc = e->resident_lists(par, 0, L, st)) != SCOUT_OK) return rc;
     if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), nullptr, false, st)) != SCOUT_OK)
         return rc;
+    e->k1k2_loaded = true;
     return e->issue_recalls(step);
 }
 
@@ -1557,7 +1573,7 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
     if ((rc = e->launch_k2(par, q.data(), co.data(), cml.data(), o.data(), ml.data(), inflag.data(), false, st)) !=
         SCOUT_OK)
         return rc;
-    if (e->tier_mode) e->k1k2_loaded = true;
+    e->k1k2_loaded = true;
     }
     if (e->tier_mode) {
         CU(cudaStreamWaitEvent(e->post_s, e->ev_kvin, 0));  // the token's K/V landed

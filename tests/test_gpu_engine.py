@@ -161,3 +161,54 @@ def test_engine_static_all_resident_matches_per_layer_ops(cuda):
     torch.cuda.synchronize()
     for li in range(c["L"]):
         assert torch.equal(h_o[li], want[li][0].cpu()), li
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("host", [False, True])
+def test_engine_static_overlapped_step_matches_ordinary(cuda, host):
+    """The static view's overlapped step (K1 beside K2, K2 polling K1's
+    per-layer flags; only without recall plans) against the ordinary order on
+    an identical engine: outputs and CPU-side ids bit for bit, on the device
+    path and the host-buffer path; the overlapped side really overlapped."""
+    cs = []
+    for _ in range(2):  # identical inputs: the same numpy and torch streams
+        torch.manual_seed(33)
+        cs.append(build(np.random.default_rng(33), L=6, batch=4, recall=False, q_dtype=torch.bfloat16,
+                        cpu_dtype=torch.bfloat16))
+    cs[0]["eng"].set_overlap(40)
+    cs[1]["eng"].set_overlap(0)
+    outs = []
+    for c in cs:
+        if host:
+            h = lambda t: t.cpu().pin_memory()  # noqa: E731
+            o = [torch.empty(c["q_true"].shape).pin_memory(), torch.empty(c["L"], c["U"] * c["G"], 2).pin_memory(),
+                 torch.empty(c["L"], c["U"], c["k"], dtype=torch.int32).pin_memory(),
+                 torch.empty(c["L"], c["U"], dtype=torch.int32).pin_memory()]
+            res = []
+            for step in range(1, 6):
+                c["eng"].decode_step_host(step, h(c["q_true"]), h(c["q_pred"]), h(c["cpu_o"]), h(c["cpu_ml"]), *o)
+                c["eng"].sync()
+                torch.cuda.synchronize()
+                res.append([t.clone() for t in o])
+        else:
+            o = [torch.empty(c["q_true"].shape, device="cuda"), torch.empty(c["L"], c["U"] * c["G"], 2, device="cuda")]
+            res = []
+            for step in range(1, 6):
+                c["eng"].decode_step(step, c["q_true"], c["q_pred"], c["cpu_o"], c["cpu_ml"], *o)
+                torch.cuda.synchronize()
+                res.append([t.clone() for t in o])
+        outs.append(res)
+    for step, (a, b) in enumerate(zip(*outs)):
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), step
+        if host:
+            assert torch.equal(a[3], b[3]), step
+            for li in range(cs[0]["L"]):
+                for u in range(cs[0]["U"]):
+                    n = int(a[3][li, u])
+                    assert torch.equal(a[2][li, u, :n], b[2][li, u, :n]), (step, li, u)
+    n_ov, sms = cs[0]["eng"].overlap_stats()
+    assert sms == 40 and n_ov == 4  # every step after the first
+    assert cs[1]["eng"].overlap_stats()[0] == 0
+    want = reference_step(cs[1])
+    for li in range(cs[0]["L"]):  # and the ordinary side is the per-layer ops' result
+        assert torch.equal(outs[1][-1][0][li].to(want[li][0].device), want[li][0]), li
