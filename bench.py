@@ -953,7 +953,7 @@ def main():
     eng.stats()  # reset counters
     if tier_mode:
         eng.recall_stats(reset=True)
-        eng.overlap_stats(reset=True)
+    eng.overlap_stats(reset=True)
     eng.set_timing(True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -974,7 +974,7 @@ def main():
     eng.set_timing(False)
     # steps whose K1 ran beside K2 (the overlapped step): their timed launch
     # is the pair, and its bytes are K2's plus K1's digest stream
-    ov_steps, ov_sms = eng.overlap_stats(reset=True) if tier_mode else (0, 0)
+    ov_steps, ov_sms = eng.overlap_stats(reset=True)
     tier_info = None
     if tier_mode:  # the residency evolves: bytes from the last timed step's K1 lists
         k1o = eng.k1_outputs()
