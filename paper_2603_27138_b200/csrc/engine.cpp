@@ -1582,10 +1582,11 @@ static int host_step(scout_engine* e, int step, const void* h_q_true, const void
         return rc;
     }
     // ---- outputs: OUT_CH layers at a time, each group leaving once every CTA
-    // finished its last layer (a short tail after K2 ends)
+    // finished its last layer; the last OUT_CH layers one at a time, so the
+    // tail after K2 ends is one layer's copy
     constexpr int OUT_CH = 4;
-    for (int lo = 0; lo < L; lo += OUT_CH) {
-        const int n = lo + OUT_CH > L ? L - lo : OUT_CH;
+    for (int lo = 0, n = 0; lo < L; lo += n) {
+        n = lo + 2 * OUT_CH <= L ? OUT_CH : 1;
         if ((rc = wait_value(e->d2h, e->layer_done + lo + n - 1, token * static_cast<unsigned>(e->grid))) != SCOUT_OK)
             return rc;
         CU(cudaMemcpyAsync(h_out_o + lo * qd, g.o + lo * qd, n * qd * 4, cudaMemcpyDeviceToHost, e->d2h));
