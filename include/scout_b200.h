@@ -586,9 +586,10 @@ int scout_engine_k2_times(scout_engine* eng, float* ms, int max_n, int* n);
  * a warm image in HBM (no bytes moved) and that were copied from the host
  * tier; reset != 0 zeroes the counts. Synchronises the device.            */
 int scout_engine_recall_stats(scout_engine* eng, long long* warm_blocks, long long* copied_blocks, int reset);
-/* The overlapped step (device tier mode, whole-step calls): K1 of the step
- * runs beside K2 on a share of the SMs (K2 polls K1's per-layer flags)
- * instead of before it, when no begin_layer ticket is due, the policy is the
+/* The overlapped step (whole-step calls: device tier mode, and the static
+ * view when it has no recall plans): K1 of the step runs beside K2 on a share
+ * of the SMs (K2 polls K1's per-layer flags) instead of before it, from the
+ * second step on, when no begin_layer ticket is due, the policy is the
  * predicted top-k, the KV is bf16 and a unit has <= 1024 blocks; the
  * environment variable SCOUT_K1K2_OVERLAP=<SMs> sets the share (0: off),
  * scout_engine_set_overlap per engine (-1: the environment / default 35% of
