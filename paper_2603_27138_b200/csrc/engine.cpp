@@ -247,6 +247,20 @@ struct scout_engine {
     // workspace and one layer's q_pred (q dtype)
     Buf qp_ws, qp_buf;
     size_t qp_ws_bytes = 0;
+    // K6 CTAs inside decode_layer_x: one per 128-feature tile (each CTA the
+    // whole K), at most the SMs K2 of the layer leaves free, so the GEMM runs
+    // in one wave beside K2 (its default grid, two CTAs per tile, took two
+    // waves there: 9.19-9.40 ms per step against 9.08-9.25, r02g8 sweep).
+    // SCOUT_LW_QP_CTAS overrides (0: K6's default grid).
+    int qp_ctas() const {
+        static const int env = [] {
+            const char* s = getenv("SCOUT_LW_QP_CTAS");
+            return s ? atoi(s) : -1;
+        }();
+        if (env >= 0) return env;
+        const int tiles = cfg.hq * SCOUT_HEAD_DIM / 128;
+        return tiles < LW_FREE_SMS ? tiles : LW_FREE_SMS;
+    }
     // layer-by-layer mode (scout_engine_decode_layer): the layer expected next
     // and the step in progress
     int lw_next = 0, lw_step = -1;
@@ -1318,7 +1332,8 @@ extern "C" int scout_engine_create(const scout_engine_config* cfg, const scout_l
                       "scout_engine_create: hidden %% 128, batch <= 256 and device tier mode for the q prediction");
             return SCOUT_ERR_INVALID_ARGUMENT;
         }
-        e->qp_ws_bytes = scout_qpred_workspace_bytes(c.hidden, n_out, c.batch, 0);
+        e->qp_ws_bytes = std::max(scout_qpred_workspace_bytes(c.hidden, n_out, c.batch, 0),
+                                  scout_qpred_workspace_bytes(c.hidden, n_out, c.batch, e->qp_ctas()));
         const size_t qb = c.q_dtype == SCOUT_BF16 ? 2 : 4;
         if (e->qp_ws.alloc(e->qp_ws_bytes) || cudaMemset(e->qp_ws.p, 0, e->qp_ws_bytes) != cudaSuccess ||
             e->qp_buf.alloc(static_cast<size_t>(c.batch) * n_out * qb)) {
@@ -1809,7 +1824,7 @@ static int decode_layer_impl(scout_engine* e, int step, int layer, const void* q
             ++e->launches;
             if ((rc = scout_predict_query(x_next, e->cfg.batch, e->cfg.hidden, wq_next, e->cfg.hq * SCOUT_HEAD_DIM,
                                           bf ? nullptr : static_cast<float*>(e->qp_buf.p), bf ? e->qp_buf.p : nullptr,
-                                          e->qp_ws.p, e->qp_ws_bytes, 0, e->k1s)) != SCOUT_OK)
+                                          e->qp_ws.p, e->qp_ws_bytes, e->qp_ctas(), e->k1s)) != SCOUT_OK)
                 return rc;
             q_pred_next = e->qp_buf.p;
         }

@@ -391,8 +391,10 @@ def test_engine_layerwise_with_query_prediction(cuda):
         engs.append(DecodeEngine(layers=L, batch=batch, hq=hkv * G, hkv=hkv, k=k, n_tokens=sd.n_tokens, pool=sd.pool,
                                  kv_dtype=kv, layer_states=layers, scale=1 / math.sqrt(D), recall_interval=3,
                                  host_tier=sd.host, tier=sd.tier, q_dtype=torch.bfloat16, hidden=hidden))
-    wqs = [ops.QueryPredictor((torch.randn(hidden, hkv * G * D, device="cuda") / hidden ** 0.5), batch)
-           for _ in range(L)]
+    # the engine's K6 grid inside decode_layer_x: one CTA per 128-feature tile (at most 68)
+    qp_ctas = min(hkv * G * D // 128, 68)
+    wqs = [ops.QueryPredictor((torch.randn(hidden, hkv * G * D, device="cuda") / hidden ** 0.5), batch,
+                              max_ctas=qp_ctas) for _ in range(L)]
     outs = [[torch.empty(L, U * G, D, device="cuda"), torch.empty(L, U * G, 2, device="cuda")] for _ in range(2)]
     x_base = torch.randn(L, batch, hidden, device="cuda")
     for step in range(1, steps + 1):
